@@ -1,0 +1,174 @@
+/*
+ * potr_b200.h -- C ABI of the B200-native POTR hot path (libpotr_b200.so).
+ *
+ * The reference (arXiv 2601.14821, /root/reference/pkg/src/potr) is a pure
+ * Python package with no FFI; its "plugin interface" for this path is the set
+ * of module-level functions in rasterizer.py and compaction.py.  Each entry
+ * point below replaces one of them (cited file:line); the Python host mirror
+ * paper_2601_14821_b200.{rasterizer,compaction} binds these with ctypes and
+ * keeps the reference's signatures, dataclasses and exceptions.
+ *
+ * Conventions
+ *  - Plain C types only.  Arrays are float64, C-contiguous, in the reference's
+ *    layouts: positions (n,3), sh (n,3,16) channel-major with coefficient 0 =
+ *    DC, opacities (n), scales (n,3), rotations (n,4) wxyz, images (H,W,3).
+ *  - Functions without the _host suffix take DEVICE pointers and are ordered
+ *    on the context's stream (potr_set_stream; default: the legacy stream).
+ *    They do not synchronize unless stated.
+ *  - Every function returns 0 on success or a negative POTR_E* code; the
+ *    message is available from potr_last_error(ctx).  Nothing throws across
+ *    the boundary.
+ *  - A context is bound to one device and is not re-entrant: use one context
+ *    per host thread (one process per GPU).
+ */
+#ifndef POTR_B200_H
+#define POTR_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define POTR_B200_ABI_VERSION 1
+
+#define POTR_OK 0
+#define POTR_E_ARG (-1)      /* invalid argument (maps to ValueError)     */
+#define POTR_E_CUDA (-2)     /* CUDA runtime error                         */
+#define POTR_E_NOMEM (-3)    /* device allocation failed                   */
+#define POTR_E_CAPACITY (-4) /* caller buffer too small (records mode)     */
+
+typedef struct potr_ctx potr_ctx;
+
+/* scene.py:64-77 Camera.  rot = world-to-camera rows (row-major 3x3). */
+typedef struct {
+    double eye[3];
+    double rot[9];
+    double fx, fy, cx, cy;
+    int32_t width, height;
+} potr_camera;
+
+/* scene.py:42-61 Splats (activated attributes), device pointers. */
+typedef struct {
+    int64_t n;
+    const double *positions; /* (n,3)    */
+    const double *sh;        /* (n,3,16) */
+    const double *opacities; /* (n)      */
+    const double *scales;    /* (n,3)    */
+    const double *rotations; /* (n,4)    */
+} potr_splats;
+
+int potr_abi_version(void);
+int potr_create(int device, potr_ctx **out);
+void potr_destroy(potr_ctx *ctx);
+int potr_set_stream(potr_ctx *ctx, void *cuda_stream);
+int potr_synchronize(potr_ctx *ctx);
+const char *potr_last_error(potr_ctx *ctx);
+/* Number of kernels this context has launched so far (bench evidence). */
+int64_t potr_kernel_launches(potr_ctx *ctx);
+
+/* ---- prune-score pass ------------------------------------------------- */
+
+/* forward_stats (rasterizer.py:311-352) / compute_delta_mse (:361-368) /
+ * compute_importance (:355-358).
+ *   targets: host array of ncam DEVICE pointers to (H,W,3) images, or NULL.
+ *   importance (n): mean over cameras of per-camera importance.
+ *   camera_importance (ncam,n): nullable.
+ *   delta_mse (n) and mse (1): required iff targets != NULL.
+ * Deterministic: bit-identical across runs (no floating-point atomics). */
+int potr_forward_stats(potr_ctx *ctx, const potr_splats *splats, int ncam,
+                       const potr_camera *cams, const double *const *targets,
+                       double *importance, double *camera_importance, double *delta_mse,
+                       double *mse);
+
+/* The view-sharded building block of forward_stats (rasterizer.py:322-347):
+ * scores cameras [0, ncam) and ADDS, in camera order, the un-normalised sums
+ *   imp_sum[k] += I_k(s), dmse_sum[k] += dMSE_k(s), mse_sum[0] += mse(s)
+ * and writes camera_importance rows (nullable).  A multi-GPU caller
+ * all-reduces the sums, then calls potr_finalize_stats with the global
+ * camera count. */
+int potr_score_views(potr_ctx *ctx, const potr_splats *splats, int ncam,
+                     const potr_camera *cams, const double *const *targets, double *imp_sum,
+                     double *camera_importance, double *dmse_sum, double *mse_sum);
+
+/* rasterizer.py:348-352: divide the sums by the total camera count in place
+ * (dmse_sum / mse_sum nullable). */
+int potr_finalize_stats(potr_ctx *ctx, int64_t n, int total_cams, double *imp_sum,
+                        double *dmse_sum, double *mse_sum);
+
+/* render_image (rasterizer.py:270-271): image (H,W,3), trans (H,W) nullable. */
+int potr_render(potr_ctx *ctx, const potr_splats *splats, const potr_camera *cam,
+                double *image, double *trans);
+
+/* render_with_records (rasterizer.py:246-267).  Two-call protocol: call with
+ * capacity 0 to get *n_records (synchronizes), then with buffers of that
+ * capacity.  Records are in the reference's order (depth order of the splat,
+ * then row-major pixel).  colors (n,3): compositing colours of valid splats,
+ * zero elsewhere.  All arrays device pointers. */
+int potr_render_records(potr_ctx *ctx, const potr_splats *splats, const potr_camera *cam,
+                        double *image, double *trans, double *colors, int64_t capacity,
+                        int64_t *n_records, int64_t *splat_ids, int64_t *pixels,
+                        double *alphas, double *trans_at, double *partials);
+
+/* project_splats (rasterizer.py:56-97) + splat_colors (:100-110) for every
+ * splat (colors of invalid splats are computed too).  Device outputs:
+ * mean2d (n,2), cov2d (n,3), depth (n), radius (n), valid (n) uint8,
+ * colors (n,3) nullable. */
+int potr_project(potr_ctx *ctx, const potr_splats *splats, const potr_camera *cam,
+                 double *mean2d, double *cov2d, double *depth, double *radius, uint8_t *valid,
+                 double *colors);
+
+/* Tile binning evidence: the global stable depth order of valid splats
+ * (rasterizer.py:248-250) and the per-tile splat lists in (tile, depth, id)
+ * order for 16x16 tiles.  order (n) and tile_offsets (ntiles+1) are device
+ * int64 outputs; tile_splats (capacity) device int32.  *n_valid and *n_pairs
+ * are host outputs (synchronizes).  tile_splats may be NULL to size. */
+int potr_bin(potr_ctx *ctx, const potr_splats *splats, const potr_camera *cam,
+             int64_t *order, int64_t *n_valid, int64_t *tile_offsets, int32_t *tile_splats,
+             int64_t capacity, int64_t *n_pairs);
+
+/* ---- SH recompute ------------------------------------------------------ */
+
+/* compact_scene (compaction.py:195-243).  camera_importance (ncam,n) device.
+ * Outputs rgb (n,3,16), ycocg (n,3,16) and status (n) int8:
+ *   0 solved, 1 solved after the 1e-10 jitter retry (:140-145),
+ *   2 RidgeError -> original coefficients kept, 3 unseen -> DC fallback. */
+int potr_compact(potr_ctx *ctx, const potr_splats *splats, int ncam, const potr_camera *cams,
+                 const double *camera_importance, double lambda_y, double parallel_threshold,
+                 double zero_threshold, double *rgb, double *ycocg, int8_t *status);
+
+/* The two halves of potr_compact, for view-sharded multi-GPU use.
+ * normal_eqs: (POTR_NEQ_STRIDE, n) entry-major, ADDED to (zero it first):
+ *   rows 0..135 = upper triangle of G = sum_s (w_s y_s)(w_s y_s)^T,
+ *   rows 136..183 = B[i][c] = sum_s (w_s y_s)_i (w_s YCoCg(color_s))_c,
+ *   row 184 = number of cameras with w_s > 0.
+ * A caller all-reduces normal_eqs across view shards, then solves. */
+#define POTR_NEQ_STRIDE 185
+int potr_sh_accumulate(potr_ctx *ctx, const potr_splats *splats, int ncam,
+                       const potr_camera *cams, const double *camera_importance,
+                       double *normal_eqs);
+int potr_sh_solve(potr_ctx *ctx, const potr_splats *splats, const double *normal_eqs,
+                  double lambda_y, double parallel_threshold, double zero_threshold,
+                  double *rgb, double *ycocg, int8_t *status);
+
+/* ---- host-buffer convenience (reference-facing drop-in) ---------------- */
+
+/* forward_stats with HOST arrays in the reference layouts; copies in, runs,
+ * copies out and synchronizes.  targets: host array of ncam host pointers or
+ * NULL.  camera_importance nullable. */
+int potr_forward_stats_host(potr_ctx *ctx, int64_t n, const double *positions, const double *sh,
+                            const double *opacities, const double *scales,
+                            const double *rotations, int ncam, const potr_camera *cams,
+                            const double *const *targets, double *importance,
+                            double *camera_importance, double *delta_mse, double *mse);
+
+/* compact_scene with HOST arrays. */
+int potr_compact_host(potr_ctx *ctx, int64_t n, const double *positions, const double *sh,
+                      int ncam, const potr_camera *cams, const double *camera_importance,
+                      double lambda_y, double parallel_threshold, double zero_threshold,
+                      double *rgb, double *ycocg, int8_t *status);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* POTR_B200_H */

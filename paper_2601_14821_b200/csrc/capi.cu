@@ -1,0 +1,654 @@
+// capi.cu -- the extern "C" boundary (include/potr_b200.h): context, grow-only
+// device workspace, and the per-view orchestration of kernels (a)-(e).
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+#include "raster.cuh"
+
+using namespace potr;
+
+namespace {
+
+struct DevBuf {
+    void *p = nullptr;
+    size_t cap = 0;
+};
+
+}  // namespace
+
+struct potr_ctx {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    std::string err;
+    int64_t launches = 0;
+    // per-view workspace
+    DevBuf rec, key, skey, sids, cnt, cnt_sorted, offs, iota, tkey, tskey, perm, dup_id, dup_rank,
+        partial, ranges, tile_se, temp, nvalid;
+    int64_t iota_len = 0;
+    // records mode
+    DevBuf rkey, rskey, rsidx, ralpha, rt, rp, rcounter;
+    // SH
+    DevBuf eyes, neq;
+    // host-buffer API staging
+    DevBuf h_pos, h_sh, h_op, h_sc, h_rot, h_tg, h_imp, h_ci, h_dm, h_mse, h_rgb, h_yc, h_st;
+    int64_t *pinned = nullptr;  // small pinned scratch for scalars
+};
+
+namespace {
+
+int fail(potr_ctx *ctx, int code, const std::string &msg) {
+    if (ctx) ctx->err = msg;
+    return code;
+}
+
+#define CK(expr)                                                                          \
+    do {                                                                                  \
+        cudaError_t _e = (expr);                                                          \
+        if (_e != cudaSuccess)                                                            \
+            return fail(ctx, POTR_E_CUDA,                                                 \
+                        std::string(#expr) + ": " + cudaGetErrorString(_e));              \
+    } while (0)
+
+// Launch-count bookkeeping for the bench's gpu_launches evidence.
+#define LAUNCH(n_kernels, expr)    \
+    do {                           \
+        CK(expr);                  \
+        ctx->launches += (n_kernels); \
+    } while (0)
+
+int ensure(potr_ctx *ctx, DevBuf &b, size_t bytes) {
+    if (bytes == 0) bytes = 16;
+    if (b.cap >= bytes) return 0;
+    if (b.p) {
+        cudaError_t e = cudaStreamSynchronize(ctx->stream);
+        if (e != cudaSuccess) return fail(ctx, POTR_E_CUDA, cudaGetErrorString(e));
+        cudaFree(b.p);
+        b.p = nullptr;
+        b.cap = 0;
+    }
+    size_t want = bytes + bytes / 8;  // headroom for the next, slightly larger view
+    cudaError_t e = cudaMalloc(&b.p, want);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        return fail(ctx, POTR_E_NOMEM,
+                    "cudaMalloc(" + std::to_string(want) + "): " + cudaGetErrorString(e));
+    }
+    b.cap = want;
+    return 0;
+}
+
+#define ENSURE(buf, bytes)                            \
+    do {                                              \
+        int _rc = ensure(ctx, buf, (size_t)(bytes));  \
+        if (_rc) return _rc;                          \
+    } while (0)
+
+template <typename T>
+T *P(DevBuf &b) {
+    return reinterpret_cast<T *>(b.p);
+}
+
+Cam to_cam(const potr_camera &c) {
+    Cam o;
+    std::memcpy(&o, &c, sizeof(Cam));
+    return o;
+}
+
+int check_splats(potr_ctx *ctx, const potr_splats *sp) {
+    if (!sp) return fail(ctx, POTR_E_ARG, "splats is NULL");
+    if (sp->n < 0 || sp->n > 0x7ffffff0LL) return fail(ctx, POTR_E_ARG, "splat count out of range");
+    if (sp->n > 0 && (!sp->positions || !sp->sh || !sp->opacities || !sp->scales || !sp->rotations))
+        return fail(ctx, POTR_E_ARG, "splat array pointer is NULL");
+    return 0;
+}
+
+// the SH path reads only positions and sh
+int check_splats_ps(potr_ctx *ctx, const potr_splats *sp) {
+    if (!sp) return fail(ctx, POTR_E_ARG, "splats is NULL");
+    if (sp->n < 0 || sp->n > 0x7ffffff0LL) return fail(ctx, POTR_E_ARG, "splat count out of range");
+    if (sp->n > 0 && (!sp->positions || !sp->sh))
+        return fail(ctx, POTR_E_ARG, "splat array pointer is NULL");
+    return 0;
+}
+
+int check_cam(potr_ctx *ctx, const potr_camera *c) {
+    if (!c) return fail(ctx, POTR_E_ARG, "camera is NULL");
+    if (c->width <= 0 || c->height <= 0 || (int64_t)c->width * c->height > 0x7fffffffLL)
+        return fail(ctx, POTR_E_ARG, "camera size out of range");
+    return 0;
+}
+
+int ensure_iota(potr_ctx *ctx, int64_t len) {
+    if (ctx->iota_len >= len) return 0;
+    int64_t want = len + len / 8 + 16;
+    ENSURE(ctx->iota, sizeof(int32_t) * want);
+    LAUNCH(1, launch_iota(want, P<int32_t>(ctx->iota), ctx->stream));
+    ctx->iota_len = want;
+    return 0;
+}
+
+struct ViewGeom {
+    int W, H, tiles_x, tiles_y, ntiles;
+    double P;
+};
+
+ViewGeom geom(const potr_camera &c) {
+    ViewGeom g;
+    g.W = c.width;
+    g.H = c.height;
+    g.tiles_x = (g.W + kTile - 1) / kTile;
+    g.tiles_y = (g.H + kTile - 1) / kTile;
+    g.ntiles = g.tiles_x * g.tiles_y;
+    g.P = (double)g.W * (double)g.H;
+    return g;
+}
+
+// (a)+(b): preprocess, depth sort, duplicate, tile sort, tile ranges.
+// On return *K_out holds the number of (tile, splat) pairs.
+int bin_view(potr_ctx *ctx, const potr_splats &sp, const potr_camera &cam, bool all_colors,
+             bool with_rank, int64_t *K_out) {
+    const int64_t n = sp.n;
+    ViewGeom g = geom(cam);
+    Cam dc = to_cam(cam);
+    ENSURE(ctx->rec, sizeof(SplatRec) * n);
+    ENSURE(ctx->key, sizeof(uint64_t) * n);
+    ENSURE(ctx->skey, sizeof(uint64_t) * n);
+    ENSURE(ctx->sids, sizeof(int32_t) * n);
+    ENSURE(ctx->cnt, sizeof(int32_t) * n);
+    ENSURE(ctx->cnt_sorted, sizeof(int64_t) * n);
+    ENSURE(ctx->offs, sizeof(int64_t) * (n + 1));
+    ENSURE(ctx->ranges, sizeof(int2) * g.ntiles);
+    ENSURE(ctx->tile_se, sizeof(double) * g.ntiles);
+    int rc = ensure_iota(ctx, n);
+    if (rc) return rc;
+    size_t t1 = 0, t2 = 0;
+    CK(depth_sort_temp(n, &t1));
+    CK(scan_temp(n, &t2));
+    ENSURE(ctx->temp, t1 > t2 ? t1 : t2);
+
+    LAUNCH(1, launch_preprocess(sp, dc, g.tiles_x, all_colors ? 1 : 0, P<SplatRec>(ctx->rec),
+                                P<uint64_t>(ctx->key), P<int32_t>(ctx->cnt), ctx->stream));
+    CK(depth_sort(ctx->temp.p, ctx->temp.cap, P<uint64_t>(ctx->key), P<uint64_t>(ctx->skey),
+                  P<int32_t>(ctx->iota), P<int32_t>(ctx->sids), n, ctx->stream));
+    LAUNCH(1, scan_counts(ctx->temp.p, ctx->temp.cap, P<int32_t>(ctx->sids), P<int32_t>(ctx->cnt),
+                          P<int64_t>(ctx->cnt_sorted), P<int64_t>(ctx->offs), n, ctx->stream));
+    CK(cudaMemcpyAsync(ctx->pinned, P<int64_t>(ctx->offs) + n, sizeof(int64_t),
+                       cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    const int64_t K = ctx->pinned[0];
+    if (K > 0x7fffff00LL) return fail(ctx, POTR_E_ARG, "more than 2^31 tile pairs in one view");
+
+    ENSURE(ctx->tkey, sizeof(uint32_t) * K);
+    ENSURE(ctx->tskey, sizeof(uint32_t) * K);
+    ENSURE(ctx->perm, sizeof(int32_t) * K);
+    ENSURE(ctx->dup_id, sizeof(int32_t) * K);
+    ENSURE(ctx->partial, sizeof(double2) * K);
+    if (with_rank) ENSURE(ctx->dup_rank, sizeof(int32_t) * K);
+    rc = ensure_iota(ctx, K);
+    if (rc) return rc;
+    size_t t3 = 0;
+    CK(tile_sort_temp(K, g.ntiles, &t3));
+    ENSURE(ctx->temp, t3);
+
+    LAUNCH(1, launch_duplicate(n, P<int32_t>(ctx->sids), P<int64_t>(ctx->offs),
+                               P<SplatRec>(ctx->rec), g.tiles_x, P<uint32_t>(ctx->tkey),
+                               P<int32_t>(ctx->dup_id),
+                               with_rank ? P<int32_t>(ctx->dup_rank) : nullptr, ctx->stream));
+    CK(tile_sort(ctx->temp.p, ctx->temp.cap, P<uint32_t>(ctx->tkey), P<uint32_t>(ctx->tskey),
+                 P<int32_t>(ctx->iota), P<int32_t>(ctx->perm), K, g.ntiles, ctx->stream));
+    LAUNCH(1, launch_tile_ranges(K, P<uint32_t>(ctx->tskey), P<int2>(ctx->ranges), g.ntiles,
+                                 ctx->stream));
+    *K_out = K;
+    return 0;
+}
+
+RasterArgs raster_args(potr_ctx *ctx, const potr_camera &cam) {
+    ViewGeom g = geom(cam);
+    RasterArgs a;
+    std::memset(&a, 0, sizeof(a));
+    a.rec = P<SplatRec>(ctx->rec);
+    a.perm = P<int32_t>(ctx->perm);
+    a.dup_id = P<int32_t>(ctx->dup_id);
+    a.dup_rank = P<int32_t>(ctx->dup_rank);
+    a.ranges = P<int2>(ctx->ranges);
+    a.tiles_x = g.tiles_x;
+    a.width = g.W;
+    a.height = g.H;
+    a.partial = P<double2>(ctx->partial);
+    a.tile_se = P<double>(ctx->tile_se);
+    return a;
+}
+
+int score_views_impl(potr_ctx *ctx, const potr_splats *sp, int ncam, const potr_camera *cams,
+                     const double *const *targets, double *imp_sum, double *cam_imp,
+                     double *dmse_sum, double *mse_sum) {
+    for (int s = 0; s < ncam; s++) {
+        const potr_camera &cam = cams[s];
+        int rc = check_cam(ctx, &cam);
+        if (rc) return rc;
+        if (targets && !targets[s]) return fail(ctx, POTR_E_ARG, "target pointer is NULL");
+        int64_t K = 0;
+        rc = bin_view(ctx, *sp, cam, false, false, &K);
+        if (rc) return rc;
+        ViewGeom g = geom(cam);
+        RasterArgs a = raster_args(ctx, cam);
+        a.target = targets ? targets[s] : nullptr;
+        LAUNCH(1, launch_raster(targets ? kScore : kImportance, a, g.ntiles, ctx->stream));
+        LAUNCH(1, launch_splat_reduce(sp->n, P<int32_t>(ctx->sids), P<int64_t>(ctx->offs),
+                                      P<double2>(ctx->partial), g.P, s, cam_imp, imp_sum,
+                                      targets ? dmse_sum : nullptr, ctx->stream));
+        if (targets)
+            LAUNCH(1, launch_mse_reduce(g.ntiles, P<double>(ctx->tile_se), g.P, mse_sum,
+                                        ctx->stream));
+    }
+    return 0;
+}
+
+}  // namespace
+
+extern "C" {
+
+int potr_abi_version(void) { return POTR_B200_ABI_VERSION; }
+
+int potr_create(int device, potr_ctx **out) {
+    if (!out) return POTR_E_ARG;
+    *out = nullptr;
+    int count = 0;
+    if (cudaGetDeviceCount(&count) != cudaSuccess || device < 0 || device >= count) {
+        cudaGetLastError();
+        return POTR_E_CUDA;
+    }
+    if (cudaSetDevice(device) != cudaSuccess) return POTR_E_CUDA;
+    potr_ctx *ctx = new potr_ctx();
+    ctx->device = device;
+    if (cudaMallocHost(&ctx->pinned, 64) != cudaSuccess) {
+        delete ctx;
+        return POTR_E_NOMEM;
+    }
+    *out = ctx;
+    return POTR_OK;
+}
+
+void potr_destroy(potr_ctx *ctx) {
+    if (!ctx) return;
+    cudaSetDevice(ctx->device);
+    cudaStreamSynchronize(ctx->stream);
+    DevBuf *bufs[] = {&ctx->rec,     &ctx->key,     &ctx->skey,    &ctx->sids,   &ctx->cnt,
+                      &ctx->cnt_sorted, &ctx->offs, &ctx->iota,    &ctx->tkey,   &ctx->tskey,
+                      &ctx->perm,    &ctx->dup_id,  &ctx->dup_rank, &ctx->partial, &ctx->ranges,
+                      &ctx->tile_se, &ctx->temp,    &ctx->nvalid,  &ctx->rkey,   &ctx->rskey,
+                      &ctx->rsidx,   &ctx->ralpha,  &ctx->rt,      &ctx->rp,     &ctx->rcounter,
+                      &ctx->eyes,    &ctx->neq,     &ctx->h_pos,   &ctx->h_sh,   &ctx->h_op,
+                      &ctx->h_sc,    &ctx->h_rot,   &ctx->h_tg,    &ctx->h_imp,  &ctx->h_ci,
+                      &ctx->h_dm,    &ctx->h_mse,   &ctx->h_rgb,   &ctx->h_yc,   &ctx->h_st};
+    for (DevBuf *b : bufs)
+        if (b->p) cudaFree(b->p);
+    if (ctx->pinned) cudaFreeHost(ctx->pinned);
+    delete ctx;
+}
+
+int potr_set_stream(potr_ctx *ctx, void *stream) {
+    if (!ctx) return POTR_E_ARG;
+    ctx->stream = reinterpret_cast<cudaStream_t>(stream);
+    return POTR_OK;
+}
+
+int potr_synchronize(potr_ctx *ctx) {
+    if (!ctx) return POTR_E_ARG;
+    CK(cudaStreamSynchronize(ctx->stream));
+    return POTR_OK;
+}
+
+const char *potr_last_error(potr_ctx *ctx) { return ctx ? ctx->err.c_str() : "null context"; }
+
+int64_t potr_kernel_launches(potr_ctx *ctx) { return ctx ? ctx->launches : 0; }
+
+int potr_score_views(potr_ctx *ctx, const potr_splats *splats, int ncam, const potr_camera *cams,
+                     const double *const *targets, double *imp_sum, double *camera_importance,
+                     double *dmse_sum, double *mse_sum) {
+    if (!ctx) return POTR_E_ARG;
+    CK(cudaSetDevice(ctx->device));
+    int rc = check_splats(ctx, splats);
+    if (rc) return rc;
+    if (ncam < 0 || (ncam > 0 && !cams)) return fail(ctx, POTR_E_ARG, "bad camera list");
+    if (!imp_sum) return fail(ctx, POTR_E_ARG, "imp_sum is NULL");
+    if (targets && (!dmse_sum || !mse_sum))
+        return fail(ctx, POTR_E_ARG, "targets given without delta_mse/mse outputs");
+    return score_views_impl(ctx, splats, ncam, cams, targets, imp_sum, camera_importance,
+                            dmse_sum, mse_sum);
+}
+
+int potr_finalize_stats(potr_ctx *ctx, int64_t n, int total_cams, double *imp_sum,
+                        double *dmse_sum, double *mse_sum) {
+    if (!ctx || n < 0) return POTR_E_ARG;
+    CK(cudaSetDevice(ctx->device));
+    LAUNCH(1, launch_finalize(n, total_cams, imp_sum, dmse_sum, mse_sum, ctx->stream));
+    return POTR_OK;
+}
+
+int potr_forward_stats(potr_ctx *ctx, const potr_splats *splats, int ncam,
+                       const potr_camera *cams, const double *const *targets, double *importance,
+                       double *camera_importance, double *delta_mse, double *mse) {
+    if (!ctx) return POTR_E_ARG;
+    CK(cudaSetDevice(ctx->device));
+    int rc = check_splats(ctx, splats);
+    if (rc) return rc;
+    if (!importance) return fail(ctx, POTR_E_ARG, "importance is NULL");
+    if (targets && (!delta_mse || !mse))
+        return fail(ctx, POTR_E_ARG, "targets given without delta_mse/mse outputs");
+    const int64_t n = splats->n;
+    CK(cudaMemsetAsync(importance, 0, sizeof(double) * (n > 0 ? n : 0), ctx->stream));
+    if (targets) {
+        CK(cudaMemsetAsync(delta_mse, 0, sizeof(double) * (n > 0 ? n : 0), ctx->stream));
+        CK(cudaMemsetAsync(mse, 0, sizeof(double), ctx->stream));
+    }
+    rc = potr_score_views(ctx, splats, ncam, cams, targets, importance, camera_importance,
+                          delta_mse, mse);
+    if (rc) return rc;
+    return potr_finalize_stats(ctx, n, ncam, importance, targets ? delta_mse : nullptr,
+                               targets ? mse : nullptr);
+}
+
+int potr_render(potr_ctx *ctx, const potr_splats *splats, const potr_camera *cam, double *image,
+                double *trans) {
+    if (!ctx) return POTR_E_ARG;
+    CK(cudaSetDevice(ctx->device));
+    int rc = check_splats(ctx, splats);
+    if (rc) return rc;
+    if ((rc = check_cam(ctx, cam))) return rc;
+    if (!image) return fail(ctx, POTR_E_ARG, "image is NULL");
+    int64_t K = 0;
+    rc = bin_view(ctx, *splats, *cam, false, false, &K);
+    if (rc) return rc;
+    RasterArgs a = raster_args(ctx, *cam);
+    a.image = image;
+    a.trans = trans;
+    LAUNCH(1, launch_raster(kRender, a, geom(*cam).ntiles, ctx->stream));
+    return POTR_OK;
+}
+
+int potr_render_records(potr_ctx *ctx, const potr_splats *splats, const potr_camera *cam,
+                        double *image, double *trans, double *colors, int64_t capacity,
+                        int64_t *n_records, int64_t *splat_ids, int64_t *pixels, double *alphas,
+                        double *trans_at, double *partials) {
+    if (!ctx || !n_records) return POTR_E_ARG;
+    CK(cudaSetDevice(ctx->device));
+    int rc = check_splats(ctx, splats);
+    if (rc) return rc;
+    if ((rc = check_cam(ctx, cam))) return rc;
+    if (!image) return fail(ctx, POTR_E_ARG, "image is NULL");
+    if (capacity > 0 && (!splat_ids || !pixels || !alphas || !trans_at || !partials))
+        return fail(ctx, POTR_E_ARG, "record output pointer is NULL");
+    const int64_t n = splats->n;
+    int64_t K = 0;
+    rc = bin_view(ctx, *splats, *cam, true, true, &K);
+    if (rc) return rc;
+    int64_t cap = capacity > 0 ? capacity : 0;
+    ENSURE(ctx->rcounter, sizeof(unsigned long long));
+    ENSURE(ctx->rkey, sizeof(uint64_t) * cap);
+    ENSURE(ctx->ralpha, sizeof(double) * cap);
+    ENSURE(ctx->rt, sizeof(double) * cap);
+    ENSURE(ctx->rp, sizeof(double) * 3 * cap);
+    CK(cudaMemsetAsync(ctx->rcounter.p, 0, sizeof(unsigned long long), ctx->stream));
+    RasterArgs a = raster_args(ctx, *cam);
+    a.image = image;
+    a.trans = trans;
+    a.rec_counter = P<unsigned long long>(ctx->rcounter);
+    a.rec_capacity = cap;
+    a.rec_key = P<uint64_t>(ctx->rkey);
+    a.rec_alpha = P<double>(ctx->ralpha);
+    a.rec_t = P<double>(ctx->rt);
+    a.rec_p = P<double>(ctx->rp);
+    LAUNCH(1, launch_raster(kRecords, a, geom(*cam).ntiles, ctx->stream));
+    if (colors)
+        LAUNCH(1, launch_colors_from_rec(n, P<uint64_t>(ctx->key), P<SplatRec>(ctx->rec), colors,
+                                         ctx->stream));
+    CK(cudaMemcpyAsync(ctx->pinned, ctx->rcounter.p, sizeof(int64_t), cudaMemcpyDeviceToHost,
+                       ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    const int64_t m = ctx->pinned[0];
+    *n_records = m;
+    if (capacity <= 0) return POTR_OK;
+    if (m > capacity) return fail(ctx, POTR_E_CAPACITY, "record capacity too small");
+    ENSURE(ctx->rskey, sizeof(uint64_t) * m);
+    ENSURE(ctx->rsidx, sizeof(int32_t) * m);
+    rc = ensure_iota(ctx, m);
+    if (rc) return rc;
+    size_t tb = 0;
+    CK(records_sort_temp(m, &tb));
+    ENSURE(ctx->temp, tb);
+    CK(records_sort(ctx->temp.p, ctx->temp.cap, P<uint64_t>(ctx->rkey), P<uint64_t>(ctx->rskey),
+                    P<int32_t>(ctx->iota), P<int32_t>(ctx->rsidx), m, ctx->stream));
+    LAUNCH(1, launch_records_gather(m, P<uint64_t>(ctx->rskey), P<int32_t>(ctx->rsidx),
+                                    P<int32_t>(ctx->sids), P<double>(ctx->ralpha),
+                                    P<double>(ctx->rt), P<double>(ctx->rp), splat_ids, pixels,
+                                    alphas, trans_at, partials, ctx->stream));
+    return POTR_OK;
+}
+
+int potr_project(potr_ctx *ctx, const potr_splats *splats, const potr_camera *cam, double *mean2d,
+                 double *cov2d, double *depth, double *radius, uint8_t *valid, double *colors) {
+    if (!ctx) return POTR_E_ARG;
+    CK(cudaSetDevice(ctx->device));
+    int rc = check_splats(ctx, splats);
+    if (rc) return rc;
+    if ((rc = check_cam(ctx, cam))) return rc;
+    if (!mean2d || !cov2d || !depth || !radius || !valid)
+        return fail(ctx, POTR_E_ARG, "projection output is NULL");
+    LAUNCH(1, launch_project_dump(*splats, to_cam(*cam), mean2d, cov2d, depth, radius, valid,
+                                  colors, ctx->stream));
+    return POTR_OK;
+}
+
+int potr_bin(potr_ctx *ctx, const potr_splats *splats, const potr_camera *cam, int64_t *order,
+             int64_t *n_valid, int64_t *tile_offsets, int32_t *tile_splats, int64_t capacity,
+             int64_t *n_pairs) {
+    if (!ctx || !n_valid || !n_pairs || !order) return POTR_E_ARG;
+    CK(cudaSetDevice(ctx->device));
+    int rc = check_splats(ctx, splats);
+    if (rc) return rc;
+    if ((rc = check_cam(ctx, cam))) return rc;
+    int64_t K = 0;
+    rc = bin_view(ctx, *splats, *cam, false, false, &K);
+    if (rc) return rc;
+    *n_pairs = K;
+    if (tile_splats && capacity < K) return fail(ctx, POTR_E_CAPACITY, "tile list capacity");
+    ENSURE(ctx->nvalid, sizeof(unsigned long long));
+    LAUNCH(3, launch_bin_outputs(splats->n, P<uint64_t>(ctx->skey), P<int32_t>(ctx->sids),
+                                 P<unsigned long long>(ctx->nvalid), order, geom(*cam).ntiles,
+                                 P<int2>(ctx->ranges), K, tile_offsets, P<int32_t>(ctx->perm),
+                                 P<int32_t>(ctx->dup_id), tile_splats, ctx->stream));
+    CK(cudaMemcpyAsync(ctx->pinned, ctx->nvalid.p, sizeof(int64_t), cudaMemcpyDeviceToHost,
+                       ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    *n_valid = ctx->pinned[0];
+    return POTR_OK;
+}
+
+int potr_sh_accumulate(potr_ctx *ctx, const potr_splats *splats, int ncam,
+                       const potr_camera *cams, const double *camera_importance,
+                       double *normal_eqs) {
+    if (!ctx) return POTR_E_ARG;
+    CK(cudaSetDevice(ctx->device));
+    int rc = check_splats_ps(ctx, splats);
+    if (rc) return rc;
+    if (ncam < 0 || (ncam > 0 && (!cams || !camera_importance)) || !normal_eqs)
+        return fail(ctx, POTR_E_ARG, "bad arguments to sh_accumulate");
+    if (ncam == 0 || splats->n == 0) return POTR_OK;
+    std::vector<double> eyes(3 * (size_t)ncam);
+    for (int s = 0; s < ncam; s++)
+        for (int i = 0; i < 3; i++) eyes[3 * s + i] = cams[s].eye[i];
+    ENSURE(ctx->eyes, sizeof(double) * eyes.size());
+    CK(cudaMemcpyAsync(ctx->eyes.p, eyes.data(), sizeof(double) * eyes.size(),
+                       cudaMemcpyHostToDevice, ctx->stream));
+    // the pageable source must stay alive until the copy is done
+    CK(cudaStreamSynchronize(ctx->stream));
+    LAUNCH(1, launch_sh_accumulate(*splats, ncam, P<double>(ctx->eyes), camera_importance,
+                                   normal_eqs, ctx->stream));
+    return POTR_OK;
+}
+
+int potr_sh_solve(potr_ctx *ctx, const potr_splats *splats, const double *normal_eqs,
+                  double lambda_y, double parallel_threshold, double zero_threshold, double *rgb,
+                  double *ycocg, int8_t *status) {
+    if (!ctx) return POTR_E_ARG;
+    CK(cudaSetDevice(ctx->device));
+    int rc = check_splats_ps(ctx, splats);
+    if (rc) return rc;
+    if (!normal_eqs || !rgb || !ycocg || !status)
+        return fail(ctx, POTR_E_ARG, "bad arguments to sh_solve");
+    if (!(lambda_y >= 0)) return fail(ctx, POTR_E_ARG, "lambda_y must be >= 0");
+    if (!(parallel_threshold > 0 && parallel_threshold <= 1))
+        return fail(ctx, POTR_E_ARG, "parallel_threshold must be in (0, 1]");
+    LAUNCH(1, launch_sh_solve(*splats, normal_eqs, lambda_y, parallel_threshold, zero_threshold,
+                              rgb, ycocg, status, ctx->stream));
+    return POTR_OK;
+}
+
+int potr_compact(potr_ctx *ctx, const potr_splats *splats, int ncam, const potr_camera *cams,
+                 const double *camera_importance, double lambda_y, double parallel_threshold,
+                 double zero_threshold, double *rgb, double *ycocg, int8_t *status) {
+    if (!ctx) return POTR_E_ARG;
+    CK(cudaSetDevice(ctx->device));
+    int rc = check_splats_ps(ctx, splats);
+    if (rc) return rc;
+    const int64_t n = splats->n;
+    ENSURE(ctx->neq, sizeof(double) * POTR_NEQ_STRIDE * n);
+    CK(cudaMemsetAsync(ctx->neq.p, 0, sizeof(double) * POTR_NEQ_STRIDE * n, ctx->stream));
+    rc = potr_sh_accumulate(ctx, splats, ncam, cams, camera_importance, P<double>(ctx->neq));
+    if (rc) return rc;
+    return potr_sh_solve(ctx, splats, P<double>(ctx->neq), lambda_y, parallel_threshold,
+                         zero_threshold, rgb, ycocg, status);
+}
+
+// ---- host-buffer convenience entry points --------------------------------
+
+namespace {
+
+int upload_splats(potr_ctx *ctx, int64_t n, const double *pos, const double *sh,
+                  const double *op, const double *sc, const double *rot, potr_splats *out) {
+    ENSURE(ctx->h_pos, sizeof(double) * 3 * n);
+    ENSURE(ctx->h_sh, sizeof(double) * 48 * n);
+    ENSURE(ctx->h_op, sizeof(double) * n);
+    ENSURE(ctx->h_sc, sizeof(double) * 3 * n);
+    ENSURE(ctx->h_rot, sizeof(double) * 4 * n);
+    if (n > 0) {
+        CK(cudaMemcpyAsync(ctx->h_pos.p, pos, sizeof(double) * 3 * n, cudaMemcpyHostToDevice,
+                           ctx->stream));
+        CK(cudaMemcpyAsync(ctx->h_sh.p, sh, sizeof(double) * 48 * n, cudaMemcpyHostToDevice,
+                           ctx->stream));
+        if (op)
+            CK(cudaMemcpyAsync(ctx->h_op.p, op, sizeof(double) * n, cudaMemcpyHostToDevice,
+                               ctx->stream));
+        if (sc)
+            CK(cudaMemcpyAsync(ctx->h_sc.p, sc, sizeof(double) * 3 * n, cudaMemcpyHostToDevice,
+                               ctx->stream));
+        if (rot)
+            CK(cudaMemcpyAsync(ctx->h_rot.p, rot, sizeof(double) * 4 * n, cudaMemcpyHostToDevice,
+                               ctx->stream));
+    }
+    out->n = n;
+    out->positions = P<double>(ctx->h_pos);
+    out->sh = P<double>(ctx->h_sh);
+    out->opacities = P<double>(ctx->h_op);
+    out->scales = P<double>(ctx->h_sc);
+    out->rotations = P<double>(ctx->h_rot);
+    return 0;
+}
+
+}  // namespace
+
+int potr_forward_stats_host(potr_ctx *ctx, int64_t n, const double *positions, const double *sh,
+                            const double *opacities, const double *scales,
+                            const double *rotations, int ncam, const potr_camera *cams,
+                            const double *const *targets, double *importance,
+                            double *camera_importance, double *delta_mse, double *mse) {
+    if (!ctx) return POTR_E_ARG;
+    CK(cudaSetDevice(ctx->device));
+    if (n < 0 || ncam < 0 || (ncam > 0 && !cams) || !importance)
+        return fail(ctx, POTR_E_ARG, "bad arguments");
+    if (n > 0 && (!positions || !sh || !opacities || !scales || !rotations))
+        return fail(ctx, POTR_E_ARG, "splat array pointer is NULL");
+    if (targets && (!delta_mse || !mse))
+        return fail(ctx, POTR_E_ARG, "targets given without delta_mse/mse outputs");
+    potr_splats sp;
+    int rc = upload_splats(ctx, n, positions, sh, opacities, scales, rotations, &sp);
+    if (rc) return rc;
+    std::vector<const double *> dtg;
+    if (targets) {
+        size_t total = 0;
+        for (int s = 0; s < ncam; s++) {
+            if (check_cam(ctx, &cams[s])) return POTR_E_ARG;
+            total += 3 * (size_t)cams[s].width * cams[s].height;
+        }
+        ENSURE(ctx->h_tg, sizeof(double) * total);
+        size_t off = 0;
+        for (int s = 0; s < ncam; s++) {
+            size_t cnt = 3 * (size_t)cams[s].width * cams[s].height;
+            if (!targets[s]) return fail(ctx, POTR_E_ARG, "target pointer is NULL");
+            CK(cudaMemcpyAsync(P<double>(ctx->h_tg) + off, targets[s], sizeof(double) * cnt,
+                               cudaMemcpyHostToDevice, ctx->stream));
+            dtg.push_back(P<double>(ctx->h_tg) + off);
+            off += cnt;
+        }
+    }
+    ENSURE(ctx->h_imp, sizeof(double) * n);
+    ENSURE(ctx->h_dm, sizeof(double) * n);
+    ENSURE(ctx->h_mse, sizeof(double));
+    if (camera_importance) ENSURE(ctx->h_ci, sizeof(double) * (size_t)ncam * n);
+    rc = potr_forward_stats(ctx, &sp, ncam, cams, targets ? dtg.data() : nullptr,
+                            P<double>(ctx->h_imp), camera_importance ? P<double>(ctx->h_ci) : nullptr,
+                            targets ? P<double>(ctx->h_dm) : nullptr,
+                            targets ? P<double>(ctx->h_mse) : nullptr);
+    if (rc) return rc;
+    CK(cudaMemcpyAsync(importance, ctx->h_imp.p, sizeof(double) * n, cudaMemcpyDeviceToHost,
+                       ctx->stream));
+    if (camera_importance)
+        CK(cudaMemcpyAsync(camera_importance, ctx->h_ci.p, sizeof(double) * (size_t)ncam * n,
+                           cudaMemcpyDeviceToHost, ctx->stream));
+    if (targets) {
+        CK(cudaMemcpyAsync(delta_mse, ctx->h_dm.p, sizeof(double) * n, cudaMemcpyDeviceToHost,
+                           ctx->stream));
+        CK(cudaMemcpyAsync(mse, ctx->h_mse.p, sizeof(double), cudaMemcpyDeviceToHost,
+                           ctx->stream));
+    }
+    CK(cudaStreamSynchronize(ctx->stream));
+    return POTR_OK;
+}
+
+int potr_compact_host(potr_ctx *ctx, int64_t n, const double *positions, const double *sh,
+                      int ncam, const potr_camera *cams, const double *camera_importance,
+                      double lambda_y, double parallel_threshold, double zero_threshold,
+                      double *rgb, double *ycocg, int8_t *status) {
+    if (!ctx) return POTR_E_ARG;
+    CK(cudaSetDevice(ctx->device));
+    if (n < 0 || ncam < 0 || !rgb || !ycocg || !status) return fail(ctx, POTR_E_ARG, "bad arguments");
+    if (n > 0 && (!positions || !sh || (ncam > 0 && !camera_importance)))
+        return fail(ctx, POTR_E_ARG, "input pointer is NULL");
+    potr_splats sp;
+    int rc = upload_splats(ctx, n, positions, sh, nullptr, nullptr, nullptr, &sp);
+    if (rc) return rc;
+    ENSURE(ctx->h_ci, sizeof(double) * (size_t)ncam * n);
+    if (ncam > 0 && n > 0)
+        CK(cudaMemcpyAsync(ctx->h_ci.p, camera_importance, sizeof(double) * (size_t)ncam * n,
+                           cudaMemcpyHostToDevice, ctx->stream));
+    ENSURE(ctx->h_rgb, sizeof(double) * 48 * n);
+    ENSURE(ctx->h_yc, sizeof(double) * 48 * n);
+    ENSURE(ctx->h_st, n);
+    rc = potr_compact(ctx, &sp, ncam, cams, P<double>(ctx->h_ci), lambda_y, parallel_threshold,
+                      zero_threshold, P<double>(ctx->h_rgb), P<double>(ctx->h_yc),
+                      P<int8_t>(ctx->h_st));
+    if (rc) return rc;
+    CK(cudaMemcpyAsync(rgb, ctx->h_rgb.p, sizeof(double) * 48 * n, cudaMemcpyDeviceToHost,
+                       ctx->stream));
+    CK(cudaMemcpyAsync(ycocg, ctx->h_yc.p, sizeof(double) * 48 * n, cudaMemcpyDeviceToHost,
+                       ctx->stream));
+    CK(cudaMemcpyAsync(status, ctx->h_st.p, (size_t)n, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    return POTR_OK;
+}
+
+}  // extern "C"

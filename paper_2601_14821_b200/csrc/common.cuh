@@ -1,0 +1,202 @@
+// common.cuh -- shared constants, device math and the per-view splat record.
+//
+// Arithmetic is float64 and the library is compiled with --fmad=false so the
+// order of every multiply/add matches the reference's numpy/numba code
+// (which never contracts to FMA); the few places where the reference itself
+// runs through an FMA kernel (OpenBLAS dgemm, rasterizer.py:65) use explicit
+// fma() to reproduce it.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "../../include/potr_b200.h"
+
+namespace potr {
+
+// rasterizer.py:22-26
+constexpr double kAlphaFloor = 1.0 / 255.0;
+constexpr double kAlphaCap = 0.999;
+constexpr double kTTerminate = 1e-4;
+constexpr double kNearClip = 0.01;
+constexpr double kCovDilation = 0.3;
+
+// sh.py:11-18
+constexpr double kShDC = 0.28209479177387814;
+constexpr double kShC1 = 0.4886025119029199;
+constexpr double kShC2_0 = 1.0925484305920792;
+constexpr double kShC2_1 = -1.0925484305920792;
+constexpr double kShC2_2 = 0.31539156525252005;
+constexpr double kShC2_3 = -1.0925484305920792;
+constexpr double kShC2_4 = 0.5462742152960396;
+constexpr double kShC3_0 = -0.5900435899266435;
+constexpr double kShC3_1 = 2.890611442640554;
+constexpr double kShC3_2 = -0.4570457994644658;
+constexpr double kShC3_3 = 0.3731763325901154;
+constexpr double kShC3_4 = -0.4570457994644658;
+constexpr double kShC3_5 = 1.445305721320277;
+constexpr double kShC3_6 = -0.5900435899266435;
+
+// Tile geometry of the rasterizer: 16x16 pixel tiles, one CTA per tile,
+// eight warps each owning an 8x4 sub-rectangle.
+constexpr int kTile = 16;
+constexpr int kTileLog2 = 4;
+constexpr int kBlock = 256;
+
+// Prefilter margin on the Gaussian exponent: power < log(floor/o) - margin
+// guarantees o*exp(power) < floor for any exp with < 1e-12 relative error,
+// so the full-precision exp is evaluated only where the floor test could pass.
+constexpr double kPowerMargin = 1e-9;
+
+// Per-view splat record, 96 bytes, written by the preprocess kernel and read
+// per (tile, splat) pair by the rasterizer.
+struct __align__(16) SplatRec {
+    double mx, my;      // mean2d
+    double ia, ib, ic;  // conic = (c, -b, a) / det   (rasterizer.py:149-154)
+    double opac;
+    double cr, cg, cb;  // compositing colour, clamped at 0 (:100-110)
+    double pthr;        // log(ALPHA_FLOOR / opac) - margin
+    int32_t x0, x1, y0, y1;  // clipped pixel bbox (:135-148), inclusive
+};
+static_assert(sizeof(SplatRec) == 96, "SplatRec must stay 96 bytes");
+
+// sh.py:23-51 -- the 16 real SH bases, 3DGS signs.
+__device__ __forceinline__ void sh_basis16(double x, double y, double z, double *o) {
+    double xx = x * x, yy = y * y, zz = z * z;
+    double xy = x * y, yz = y * z, xz = x * z;
+    o[0] = kShDC;
+    o[1] = -kShC1 * y;
+    o[2] = kShC1 * z;
+    o[3] = -kShC1 * x;
+    o[4] = kShC2_0 * xy;
+    o[5] = kShC2_1 * yz;
+    o[6] = kShC2_2 * (2.0 * zz - xx - yy);
+    o[7] = kShC2_3 * xz;
+    o[8] = kShC2_4 * (xx - yy);
+    o[9] = kShC3_0 * y * (3.0 * xx - yy);
+    o[10] = kShC3_1 * xy * z;
+    o[11] = kShC3_2 * y * (4.0 * zz - xx - yy);
+    o[12] = kShC3_3 * z * (2.0 * zz - 3.0 * xx - 3.0 * yy);
+    o[13] = kShC3_4 * x * (4.0 * zz - xx - yy);
+    o[14] = kShC3_5 * z * (xx - yy);
+    o[15] = kShC3_6 * x * (xx - 3.0 * yy);
+}
+
+// Device-side camera (same layout as potr_camera).
+struct Cam {
+    double eye[3];
+    double rot[9];
+    double fx, fy, cx, cy;
+    int32_t width, height;
+};
+static_assert(sizeof(Cam) == sizeof(potr_camera), "camera layout");
+
+struct Proj {
+    double mx, my, a, b, c, depth, radius;
+    bool valid;
+};
+
+// project_splats for one splat (rasterizer.py:56-97, quat_to_rotmat :40-53).
+__device__ __forceinline__ Proj project_one(const double *__restrict__ p,
+                                            const double *__restrict__ s,
+                                            const double *__restrict__ q, const Cam &cam) {
+    const double *W = cam.rot;
+    double d0 = p[0] - cam.eye[0], d1 = p[1] - cam.eye[1], d2 = p[2] - cam.eye[2];
+    // (positions - eye) @ W.T: OpenBLAS accumulates with FMA in index order.
+    double t0 = fma(d2, W[2], fma(d1, W[1], d0 * W[0]));
+    double t1 = fma(d2, W[5], fma(d1, W[4], d0 * W[3]));
+    double t2 = fma(d2, W[8], fma(d1, W[7], d0 * W[6]));
+    Proj o;
+    o.valid = t2 > kNearClip;
+    double safe_z = o.valid ? t2 : 1.0;
+    double inv_z = 1.0 / safe_z;
+    o.mx = cam.fx * t0 * inv_z + cam.cx;
+    o.my = cam.fy * t1 * inv_z + cam.cy;
+
+    double w = q[0], x = q[1], y = q[2], z = q[3];
+    double R[9];
+    R[0] = 1 - 2 * (y * y + z * z);
+    R[1] = 2 * (x * y - w * z);
+    R[2] = 2 * (x * z + w * y);
+    R[3] = 2 * (x * y + w * z);
+    R[4] = 1 - 2 * (x * x + z * z);
+    R[5] = 2 * (y * z - w * x);
+    R[6] = 2 * (x * z - w * y);
+    R[7] = 2 * (y * z + w * x);
+    R[8] = 1 - 2 * (x * x + y * y);
+    double s2[3] = {s[0] * s[0], s[1] * s[1], s[2] * s[2]};
+    double S[9];
+#pragma unroll
+    for (int i = 0; i < 3; i++)
+#pragma unroll
+        for (int k = 0; k < 3; k++) {
+            double acc = 0.0;
+#pragma unroll
+            for (int j = 0; j < 3; j++) acc += R[i * 3 + j] * s2[j] * R[k * 3 + j];
+            S[i * 3 + k] = acc;
+        }
+    double V[9];
+#pragma unroll
+    for (int i = 0; i < 3; i++)
+#pragma unroll
+        for (int l = 0; l < 3; l++) {
+            double acc = 0.0;
+#pragma unroll
+            for (int j = 0; j < 3; j++)
+#pragma unroll
+                for (int k = 0; k < 3; k++) acc += W[i * 3 + j] * S[j * 3 + k] * W[l * 3 + k];
+            V[i * 3 + l] = acc;
+        }
+    double J[6] = {cam.fx * inv_z, 0.0, -cam.fx * t0 * inv_z * inv_z,
+                   0.0, cam.fy * inv_z, -cam.fy * t1 * inv_z * inv_z};
+    double C[4];
+#pragma unroll
+    for (int i = 0; i < 2; i++)
+#pragma unroll
+        for (int l = 0; l < 2; l++) {
+            double acc = 0.0;
+#pragma unroll
+            for (int j = 0; j < 3; j++)
+#pragma unroll
+                for (int k = 0; k < 3; k++) acc += J[i * 3 + j] * V[j * 3 + k] * J[l * 3 + k];
+            C[i * 2 + l] = acc;
+        }
+    o.a = C[0] + kCovDilation;
+    o.b = C[1];
+    o.c = C[3] + kCovDilation;
+    double mid = 0.5 * (o.a + o.c);
+    double det = o.a * o.c - o.b * o.b;
+    double disc = mid * mid - det;
+    double lam_max = mid + sqrt(disc > 0.0 ? disc : 0.0);
+    o.radius = 3.0 * sqrt(lam_max);
+    o.depth = t2;
+    o.valid = o.valid && (o.mx >= -o.radius) && (o.mx <= cam.width + o.radius);
+    o.valid = o.valid && (o.my >= -o.radius) && (o.my <= cam.height + o.radius);
+    return o;
+}
+
+// splat_colors for one splat (rasterizer.py:100-110): SH at the unit
+// direction eye -> centre, clamped at zero, no +0.5 offset.
+__device__ __forceinline__ void splat_color(const double *__restrict__ p,
+                                            const double *__restrict__ sh, const Cam &cam,
+                                            double *rgb) {
+    double d0 = p[0] - cam.eye[0], d1 = p[1] - cam.eye[1], d2 = p[2] - cam.eye[2];
+    double norm = sqrt(d0 * d0 + d1 * d1 + d2 * d2);
+    if (norm == 0.0) norm = 1.0;
+    double basis[16];
+    sh_basis16(d0 / norm, d1 / norm, d2 / norm, basis);
+    const double2 *sh2 = reinterpret_cast<const double2 *>(sh);
+#pragma unroll
+    for (int ch = 0; ch < 3; ch++) {
+        double acc = 0.0;
+#pragma unroll
+        for (int i = 0; i < 8; i++) {
+            double2 v = __ldg(sh2 + ch * 8 + i);
+            acc += v.x * basis[2 * i];
+            acc += v.y * basis[2 * i + 1];
+        }
+        rgb[ch] = acc > 0.0 ? acc : 0.0;
+    }
+}
+
+}  // namespace potr

@@ -1,0 +1,693 @@
+// raster.cu -- the prune-score pass on sm_100a: kernels (a)-(d).
+//
+//  (a) k_preprocess    project + cov2d + radius + clipped bbox + conic + SH
+//                      colour + fp64 depth key, one thread per splat
+//                      (rasterizer.py:56-110, :135-154)
+//  (b) k_gather_counts / k_duplicate / k_tile_ranges around two CUB onesweep
+//      radix sorts: a stable sort of the fp64 depth bits (ties keep ascending
+//      splat id == np.argsort(kind="stable"), :248-250), then a stable sort of
+//      the per-(tile, splat) duplicates on the tile id, giving every tile its
+//      splats in (tile, depth, id) order.
+//  (c)+(d) k_raster    one CTA per 16x16 tile; splat batches staged in shared
+//      memory; front-to-back compositing with the reference's exact per-pixel
+//      rules (:159-201); a second walk over the same batches evaluates the
+//      closed-form removal delta PD = a/(1-a) (P_K - P_i - T c) (:232-243),
+//      dSE = sum_ch PD^2 + 2 PD (c - c_t) (:333) and T*alpha (:228); warps
+//      reduce per splat with shuffles and the 8 warps combine in a fixed
+//      order into one slot per (tile, splat) pair -- no floating-point
+//      atomics, so scores are bit-reproducible.
+//  k_splat_reduce      per splat, sums its pair slots in tile order, divides
+//                      by P / 3P and adds into the camera-ordered accumulators
+//                      (:226-230, :334, :340-347).
+#include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_scan.cuh>
+
+#include "common.cuh"
+#include "raster.cuh"
+
+namespace potr {
+
+// ---------------------------------------------------------------------------
+// (a) preprocess
+
+__global__ void __launch_bounds__(256) k_preprocess(potr_splats sp, Cam cam, int tiles_x,
+                                                     int all_colors, SplatRec *__restrict__ rec,
+                                                     uint64_t *__restrict__ key,
+                                                     int32_t *__restrict__ cnt) {
+    int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= sp.n) return;
+    Proj pr = project_one(sp.positions + 3 * k, sp.scales + 3 * k, sp.rotations + 4 * k, cam);
+    int32_t c = 0;
+    uint64_t kk = ~0ull;
+    if (pr.valid) {
+        kk = (uint64_t)__double_as_longlong(pr.depth);  // depth > 0.01: bits are monotone
+        const int W = cam.width, H = cam.height;
+        double x0 = floor(pr.mx - pr.radius), x1 = ceil(pr.mx + pr.radius);
+        double y0 = floor(pr.my - pr.radius), y1 = ceil(pr.my + pr.radius);
+        if (x0 < 0) x0 = 0;
+        if (y0 < 0) y0 = 0;
+        if (x1 > W - 1) x1 = W - 1;
+        if (y1 > H - 1) y1 = H - 1;
+        double det = pr.a * pr.c - pr.b * pr.b;
+        bool draw = !(x0 > x1 || y0 > y1) && det > 0.0;
+        if (draw || all_colors) {
+            SplatRec r;
+            r.mx = pr.mx;
+            r.my = pr.my;
+            r.ia = pr.c / det;
+            r.ib = -pr.b / det;
+            r.ic = pr.a / det;
+            double o = sp.opacities[k];
+            r.opac = o;
+            double rgb[3];
+            splat_color(sp.positions + 3 * k, sp.sh + 48 * k, cam, rgb);
+            r.cr = rgb[0];
+            r.cg = rgb[1];
+            r.cb = rgb[2];
+            r.pthr = log(kAlphaFloor / o) - kPowerMargin;
+            r.x0 = (int32_t)x0;
+            r.x1 = (int32_t)x1;
+            r.y0 = (int32_t)y0;
+            r.y1 = (int32_t)y1;
+            if (!draw) r.x0 = 1, r.x1 = 0;  // empty: never drawn
+            rec[k] = r;
+        }
+        if (draw) {
+            int tx0 = (int)x0 >> kTileLog2, tx1 = (int)x1 >> kTileLog2;
+            int ty0 = (int)y0 >> kTileLog2, ty1 = (int)y1 >> kTileLog2;
+            c = (tx1 - tx0 + 1) * (ty1 - ty0 + 1);
+        }
+    }
+    key[k] = kk;
+    cnt[k] = c;
+}
+
+// project_splats / splat_colors dump for parity tests (potr_project).
+__global__ void k_project_dump(potr_splats sp, Cam cam, double *mean2d, double *cov2d,
+                               double *depth, double *radius, uint8_t *valid, double *colors) {
+    int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= sp.n) return;
+    Proj pr = project_one(sp.positions + 3 * k, sp.scales + 3 * k, sp.rotations + 4 * k, cam);
+    mean2d[2 * k] = pr.mx;
+    mean2d[2 * k + 1] = pr.my;
+    cov2d[3 * k] = pr.a;
+    cov2d[3 * k + 1] = pr.b;
+    cov2d[3 * k + 2] = pr.c;
+    depth[k] = pr.depth;
+    radius[k] = pr.radius;
+    valid[k] = pr.valid ? 1 : 0;
+    if (colors) splat_color(sp.positions + 3 * k, sp.sh + 48 * k, cam, colors + 3 * k);
+}
+
+// ---------------------------------------------------------------------------
+// (b) binning
+
+__global__ void k_gather_counts(int64_t n, const int32_t *__restrict__ ids,
+                                const int32_t *__restrict__ cnt, int64_t *__restrict__ out) {
+    int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (r < n) out[r] = cnt[ids[r]];
+}
+
+__global__ void k_duplicate(int64_t n, const int32_t *__restrict__ ids,
+                            const int64_t *__restrict__ offs, const SplatRec *__restrict__ rec,
+                            int tiles_x, uint32_t *__restrict__ tkey, int32_t *__restrict__ dup_id,
+                            int32_t *__restrict__ dup_rank) {
+    int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= n) return;
+    int64_t o = offs[r], e = offs[r + 1];
+    if (o == e) return;
+    int32_t id = ids[r];
+    const SplatRec &R = rec[id];
+    int tx0 = R.x0 >> kTileLog2, tx1 = R.x1 >> kTileLog2;
+    int ty0 = R.y0 >> kTileLog2, ty1 = R.y1 >> kTileLog2;
+    for (int ty = ty0; ty <= ty1; ty++)
+        for (int tx = tx0; tx <= tx1; tx++) {
+            tkey[o] = (uint32_t)(ty * tiles_x + tx);
+            dup_id[o] = id;
+            if (dup_rank) dup_rank[o] = (int32_t)r;
+            o++;
+        }
+}
+
+__global__ void k_tile_ranges(int64_t K, const uint32_t *__restrict__ skey, int2 *__restrict__ rng) {
+    int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= K) return;
+    uint32_t t = skey[j];
+    if (j == 0 || skey[j - 1] != t) rng[t].x = (int)j;
+    if (j == K - 1 || skey[j + 1] != t) rng[t].y = (int)(j + 1);
+}
+
+__global__ void k_iota(int64_t n, int32_t *out) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) out[i] = (int32_t)i;
+}
+
+// ---------------------------------------------------------------------------
+// (c)+(d) tile rasterizer and removal-effect pass
+
+struct RasterSmem {
+    SplatRec rec[kBlock];
+    int32_t dup[kBlock];
+    int32_t rank[kBlock];
+    double2 red[kBlock / 32][kBlock];  // per-warp (dSE, T*alpha) per batch slot
+    double wsum[kBlock / 32];
+};
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+    return v;
+}
+
+// MODE: kRender    forward only, writes image/trans
+//       kImportance forward with per-pair T*alpha slots (no targets)
+//       kScore     forward, then the removal-effect walk with targets
+//       kRecords   forward, appending every contribution record
+template <int MODE>
+__global__ void __launch_bounds__(kBlock, 2) k_raster(RasterArgs a) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    RasterSmem &S = *reinterpret_cast<RasterSmem *>(smem_raw);
+
+    const int tile = blockIdx.x;
+    const int tx = tile % a.tiles_x, ty = tile / a.tiles_x;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int wx0 = tx * kTile + (warp & 1) * 8, wy0 = ty * kTile + (warp >> 1) * 4;
+    const int wx1 = wx0 + 7, wy1 = wy0 + 3;
+    const int px = wx0 + (lane & 7), py = wy0 + (lane >> 3);
+    const bool inside = px < a.width && py < a.height;
+    const int64_t pix = (int64_t)py * a.width + px;
+    const int2 range = a.ranges[tile];
+    const int start = range.x, end = range.y > range.x ? range.y : range.x;
+    const int nbatch = (end - start + kBlock - 1) / kBlock;
+    const double pxc = (double)px + 0.5, pyc = (double)py + 0.5;
+
+    // ---- pass 1: front-to-back compositing (rasterizer.py:159-201) -------
+    double T = 1.0, P0 = 0.0, P1 = 0.0, P2 = 0.0;
+    bool done = !inside;
+    int batches_done = 0;
+    for (int b = 0; b < nbatch; b++) {
+        const int base = start + b * kBlock;
+        const int cnt = min(kBlock, end - base);
+        __syncthreads();
+        if (threadIdx.x < cnt) {
+            int32_t d = a.perm[base + threadIdx.x];
+            int32_t id = a.dup_id[d];
+            S.rec[threadIdx.x] = a.rec[id];
+            S.dup[threadIdx.x] = d;
+            if (MODE == kRecords) S.rank[threadIdx.x] = a.dup_rank[d];
+        }
+        if (MODE == kImportance) {
+#pragma unroll
+            for (int w = 0; w < kBlock / 32; w++) S.red[w][threadIdx.x] = make_double2(0.0, 0.0);
+        }
+        __syncthreads();
+        if (!__all_sync(0xffffffffu, done)) {
+            for (int e = 0; e < cnt; e++) {
+                const SplatRec &R = S.rec[e];
+                if (R.x1 < wx0 || R.x0 > wx1 || R.y1 < wy0 || R.y0 > wy1) continue;
+                bool contrib = false;
+                double alpha = 0.0;
+                if (!done && px >= R.x0 && px <= R.x1 && py >= R.y0 && py <= R.y1) {
+                    double dx = pxc - R.mx, dy = pyc - R.my;
+                    double power = -0.5 * (R.ia * dx * dx + R.ic * dy * dy) - R.ib * dx * dy;
+                    if (power >= R.pthr) {
+                        alpha = R.opac * exp(power);
+                        if (alpha > kAlphaCap) alpha = kAlphaCap;
+                        contrib = !(alpha < kAlphaFloor);
+                    }
+                }
+                double timp = 0.0;
+                if (contrib) {
+                    if (MODE == kRecords) {
+                        unsigned long long slot = atomicAdd(a.rec_counter, 1ull);
+                        if ((int64_t)slot < a.rec_capacity) {
+                            a.rec_key[slot] =
+                                ((uint64_t)(uint32_t)S.rank[e] << 32) | (uint64_t)(uint32_t)pix;
+                            a.rec_alpha[slot] = alpha;
+                            a.rec_t[slot] = T;
+                            a.rec_p[3 * slot] = P0;
+                            a.rec_p[3 * slot + 1] = P1;
+                            a.rec_p[3 * slot + 2] = P2;
+                        }
+                    }
+                    double w = T * alpha;
+                    timp = w;
+                    P0 += w * R.cr;
+                    P1 += w * R.cg;
+                    P2 += w * R.cb;
+                    T = T * (1.0 - alpha);
+                    done = T < kTTerminate;
+                }
+                if (MODE == kImportance) {
+                    if (__any_sync(0xffffffffu, contrib)) {
+                        double s = warp_sum(timp);
+                        if (lane == 0) S.red[warp][e] = make_double2(0.0, s);
+                    }
+                }
+                if (__all_sync(0xffffffffu, done)) break;
+            }
+        }
+        if (MODE == kImportance) {
+            __syncthreads();
+            if (threadIdx.x < cnt) {
+                double2 acc = S.red[0][threadIdx.x];
+#pragma unroll
+                for (int w = 1; w < kBlock / 32; w++) {
+                    acc.x += S.red[w][threadIdx.x].x;
+                    acc.y += S.red[w][threadIdx.x].y;
+                }
+                a.partial[S.dup[threadIdx.x]] = acc;
+            }
+        }
+        batches_done = b + 1;
+        if (__syncthreads_count(done) == kBlock) break;
+    }
+
+    if (MODE != kScore) {
+        if (inside && a.image) {
+            a.image[3 * pix] = P0;
+            a.image[3 * pix + 1] = P1;
+            a.image[3 * pix + 2] = P2;
+        }
+        if (inside && a.trans) a.trans[pix] = T;
+        if (MODE == kImportance) {
+            // pairs after the early-out contribute nothing
+            for (int j = start + batches_done * kBlock + threadIdx.x; j < end; j += kBlock)
+                a.partial[a.perm[j]] = make_double2(0.0, 0.0);
+        }
+        return;
+    }
+
+    // ---- pass 2: removal effect (rasterizer.py:232-243, :322-336) --------
+    const double PK0 = P0, PK1 = P1, PK2 = P2;
+    double ct0 = 0.0, ct1 = 0.0, ct2 = 0.0;
+    double se = 0.0;
+    if (inside) {
+        ct0 = a.target[3 * pix];
+        ct1 = a.target[3 * pix + 1];
+        ct2 = a.target[3 * pix + 2];
+        double d0 = PK0 - ct0, d1 = PK1 - ct1, d2 = PK2 - ct2;
+        se = d0 * d0 + d1 * d1 + d2 * d2;
+        if (a.image) {
+            a.image[3 * pix] = PK0;
+            a.image[3 * pix + 1] = PK1;
+            a.image[3 * pix + 2] = PK2;
+        }
+        if (a.trans) a.trans[pix] = T;
+    }
+    // per-tile squared error, fixed-order block reduction
+    {
+        double ws = warp_sum(se);
+        if (lane == 0) S.wsum[warp] = ws;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            double t = S.wsum[0];
+#pragma unroll
+            for (int w = 1; w < kBlock / 32; w++) t += S.wsum[w];
+            a.tile_se[tile] = t;
+        }
+    }
+    const double dr0 = PK0 - ct0, dr1 = PK1 - ct1, dr2 = PK2 - ct2;
+    T = 1.0;
+    P0 = P1 = P2 = 0.0;
+    done = !inside;
+    for (int b = 0; b < batches_done; b++) {
+        const int base = start + b * kBlock;
+        const int cnt = min(kBlock, end - base);
+        __syncthreads();
+        if (threadIdx.x < cnt) {
+            int32_t d = a.perm[base + threadIdx.x];
+            int32_t id = a.dup_id[d];
+            S.rec[threadIdx.x] = a.rec[id];
+            S.dup[threadIdx.x] = d;
+        }
+#pragma unroll
+        for (int w = 0; w < kBlock / 32; w++) S.red[w][threadIdx.x] = make_double2(0.0, 0.0);
+        __syncthreads();
+        if (!__all_sync(0xffffffffu, done)) {
+            for (int e = 0; e < cnt; e++) {
+                const SplatRec &R = S.rec[e];
+                if (R.x1 < wx0 || R.x0 > wx1 || R.y1 < wy0 || R.y0 > wy1) continue;
+                bool contrib = false;
+                double alpha = 0.0;
+                if (!done && px >= R.x0 && px <= R.x1 && py >= R.y0 && py <= R.y1) {
+                    double dx = pxc - R.mx, dy = pyc - R.my;
+                    double power = -0.5 * (R.ia * dx * dx + R.ic * dy * dy) - R.ib * dx * dy;
+                    if (power >= R.pthr) {
+                        alpha = R.opac * exp(power);
+                        if (alpha > kAlphaCap) alpha = kAlphaCap;
+                        contrib = !(alpha < kAlphaFloor);
+                    }
+                }
+                double dse = 0.0, timp = 0.0;
+                if (contrib) {
+                    // prune_deltas, forward form: a/(1-a) * (P_K - P_i - T c)
+                    double f = alpha / (1.0 - alpha);
+                    double pd0 = f * (PK0 - P0 - T * R.cr);
+                    double pd1 = f * (PK1 - P1 - T * R.cg);
+                    double pd2 = f * (PK2 - P2 - T * R.cb);
+                    dse = pd0 * pd0 + 2.0 * pd0 * dr0;
+                    dse = dse + (pd1 * pd1 + 2.0 * pd1 * dr1);
+                    dse = dse + (pd2 * pd2 + 2.0 * pd2 * dr2);
+                    double w = T * alpha;
+                    timp = w;
+                    P0 += w * R.cr;
+                    P1 += w * R.cg;
+                    P2 += w * R.cb;
+                    T = T * (1.0 - alpha);
+                    done = T < kTTerminate;
+                }
+                if (__any_sync(0xffffffffu, contrib)) {
+                    double s0 = warp_sum(dse);
+                    double s1 = warp_sum(timp);
+                    if (lane == 0) S.red[warp][e] = make_double2(s0, s1);
+                }
+                if (__all_sync(0xffffffffu, done)) break;
+            }
+        }
+        __syncthreads();
+        if (threadIdx.x < cnt) {
+            double2 acc = S.red[0][threadIdx.x];
+#pragma unroll
+            for (int w = 1; w < kBlock / 32; w++) {
+                acc.x += S.red[w][threadIdx.x].x;
+                acc.y += S.red[w][threadIdx.x].y;
+            }
+            a.partial[S.dup[threadIdx.x]] = acc;
+        }
+    }
+    for (int j = start + batches_done * kBlock + threadIdx.x; j < end; j += kBlock)
+        a.partial[a.perm[j]] = make_double2(0.0, 0.0);
+}
+
+// Per-splat sum of its (tile, splat) slots, in tile order (deterministic),
+// then the per-camera normalisation and the camera-ordered accumulation.
+__global__ void k_splat_reduce(int64_t n, const int32_t *__restrict__ ids,
+                               const int64_t *__restrict__ offs,
+                               const double2 *__restrict__ partial, double P, int64_t cam_row,
+                               double *__restrict__ cam_imp, double *__restrict__ imp_acc,
+                               double *__restrict__ dmse_acc) {
+    int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= n) return;
+    int32_t id = ids[r];
+    int64_t o = offs[r], e = offs[r + 1];
+    double dse = 0.0, imp = 0.0;
+    for (int64_t j = o; j < e; j++) {
+        double2 v = partial[j];
+        dse += v.x;
+        imp += v.y;
+    }
+    double ci = imp / P;  // rasterizer.py:230
+    if (cam_imp) cam_imp[cam_row * n + id] = ci;
+    imp_acc[id] += ci;                                  // :344, :348
+    if (dmse_acc) dmse_acc[id] += dse / (P * 3.0);      // :334, :346
+}
+
+// Sum of the per-tile squared errors; mse(s) = sum / 3P (:335), added to the
+// camera-ordered accumulator (:347).
+__global__ void k_mse_reduce(int ntiles, const double *__restrict__ tile_se, double P,
+                             double *__restrict__ mse_acc) {
+    __shared__ double red[32];
+    double s = 0.0;
+    for (int t = threadIdx.x; t < ntiles; t += blockDim.x) s += tile_se[t];
+    s = warp_sum(s);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t = 0.0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); w++) t += red[w];
+        mse_acc[0] += t / (P * 3.0);
+    }
+}
+
+__global__ void k_finalize(int64_t n, double S, double *imp, double *dmse, double *mse) {
+    int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (k < n) {
+        imp[k] = imp[k] / S;
+        if (dmse) dmse[k] = dmse[k] / S;
+    }
+    if (k == 0 && mse) mse[0] = mse[0] / S;
+}
+
+// records mode: gather the sorted records into the caller's arrays
+__global__ void k_records_gather(int64_t m, const uint64_t *__restrict__ skey,
+                                 const int32_t *__restrict__ sidx, const int32_t *__restrict__ ids,
+                                 const double *__restrict__ ra, const double *__restrict__ rt,
+                                 const double *__restrict__ rp, int64_t *splat_ids,
+                                 int64_t *pixels, double *alphas, double *trans_at,
+                                 double *partials) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= m) return;
+    uint64_t k = skey[i];
+    int32_t s = sidx[i];
+    splat_ids[i] = ids[(int64_t)(k >> 32)];
+    pixels[i] = (int64_t)(k & 0xffffffffu);
+    alphas[i] = ra[s];
+    trans_at[i] = rt[s];
+    partials[3 * i] = rp[3 * (int64_t)s];
+    partials[3 * i + 1] = rp[3 * (int64_t)s + 1];
+    partials[3 * i + 2] = rp[3 * (int64_t)s + 2];
+}
+
+__global__ void k_colors_from_rec(int64_t n, const uint64_t *__restrict__ key,
+                                  const SplatRec *__restrict__ rec, double *colors) {
+    int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= n) return;
+    bool valid = key[k] != ~0ull;
+    colors[3 * k] = valid ? rec[k].cr : 0.0;
+    colors[3 * k + 1] = valid ? rec[k].cg : 0.0;
+    colors[3 * k + 2] = valid ? rec[k].cb : 0.0;
+}
+
+__global__ void k_tile_offsets(int ntiles, const int2 *__restrict__ rng, int64_t K,
+                               int64_t *__restrict__ out) {
+    // tiles are sorted ascending, so offset(t) = first pair index of a tile >= t
+    int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t > ntiles) return;
+    if (t == ntiles) {
+        out[t] = K;
+        return;
+    }
+    int64_t o = K;
+    for (int u = t; u < ntiles; u++) {
+        if (rng[u].y > rng[u].x) {
+            o = rng[u].x;
+            break;
+        }
+    }
+    out[t] = o;
+}
+
+__global__ void k_tile_splats(int64_t K, const int32_t *__restrict__ perm,
+                              const int32_t *__restrict__ dup_id, int32_t *__restrict__ out) {
+    int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (j < K) out[j] = dup_id[perm[j]];
+}
+
+__global__ void k_order_out(int64_t nv, const int32_t *__restrict__ ids, int64_t *__restrict__ out) {
+    int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (r < nv) out[r] = ids[r];
+}
+
+__global__ void k_count_valid(int64_t n, const uint64_t *__restrict__ skey,
+                              unsigned long long *__restrict__ out) {
+    // sorted keys: valid ones first; find the boundary
+    int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= n) return;
+    bool v = skey[r] != ~0ull;
+    bool next_v = (r + 1 < n) ? (skey[r + 1] != ~0ull) : false;
+    if (v && !next_v) *out = (unsigned long long)(r + 1);
+}
+
+// ---------------------------------------------------------------------------
+// host-side launchers (called from capi.cu)
+
+static inline unsigned grid_for(int64_t n, int block) {
+    return (unsigned)((n + block - 1) / block);
+}
+
+size_t raster_smem_bytes() { return sizeof(RasterSmem); }
+
+cudaError_t launch_preprocess(const potr_splats &sp, const Cam &cam, int tiles_x, int all_colors,
+                              SplatRec *rec, uint64_t *key, int32_t *cnt, cudaStream_t st) {
+    if (sp.n == 0) return cudaSuccess;
+    k_preprocess<<<grid_for(sp.n, 256), 256, 0, st>>>(sp, cam, tiles_x, all_colors, rec, key, cnt);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_project_dump(const potr_splats &sp, const Cam &cam, double *mean2d,
+                                double *cov2d, double *depth, double *radius, uint8_t *valid,
+                                double *colors, cudaStream_t st) {
+    if (sp.n == 0) return cudaSuccess;
+    k_project_dump<<<grid_for(sp.n, 128), 128, 0, st>>>(sp, cam, mean2d, cov2d, depth, radius,
+                                                         valid, colors);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_iota(int64_t n, int32_t *out, cudaStream_t st) {
+    if (n == 0) return cudaSuccess;
+    k_iota<<<grid_for(n, 256), 256, 0, st>>>(n, out);
+    return cudaGetLastError();
+}
+
+cudaError_t depth_sort(void *temp, size_t temp_bytes, const uint64_t *key, uint64_t *skey,
+                       const int32_t *iota, int32_t *sids, int64_t n, cudaStream_t st) {
+    if (n == 0) return cudaSuccess;
+    return cub::DeviceRadixSort::SortPairs(temp, temp_bytes, key, skey, iota, sids, (int)n, 0, 64,
+                                           st);
+}
+
+cudaError_t depth_sort_temp(int64_t n, size_t *bytes) {
+    return cub::DeviceRadixSort::SortPairs((void *)nullptr, *bytes, (const uint64_t *)nullptr,
+                                           (uint64_t *)nullptr, (const int32_t *)nullptr,
+                                           (int32_t *)nullptr, (int)n, 0, 64);
+}
+
+cudaError_t scan_counts(void *temp, size_t temp_bytes, const int32_t *ids, const int32_t *cnt,
+                        int64_t *cnt_sorted, int64_t *offs, int64_t n, cudaStream_t st) {
+    cudaError_t e = cudaMemsetAsync(offs, 0, sizeof(int64_t), st);
+    if (e != cudaSuccess || n == 0) return e;
+    k_gather_counts<<<grid_for(n, 256), 256, 0, st>>>(n, ids, cnt, cnt_sorted);
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    return cub::DeviceScan::InclusiveSum(temp, temp_bytes, cnt_sorted, offs + 1, (int)n, st);
+}
+
+cudaError_t scan_temp(int64_t n, size_t *bytes) {
+    return cub::DeviceScan::InclusiveSum((void *)nullptr, *bytes, (const int64_t *)nullptr,
+                                         (int64_t *)nullptr, (int)n);
+}
+
+cudaError_t launch_duplicate(int64_t n, const int32_t *ids, const int64_t *offs,
+                             const SplatRec *rec, int tiles_x, uint32_t *tkey, int32_t *dup_id,
+                             int32_t *dup_rank, cudaStream_t st) {
+    if (n == 0) return cudaSuccess;
+    k_duplicate<<<grid_for(n, 256), 256, 0, st>>>(n, ids, offs, rec, tiles_x, tkey, dup_id,
+                                                   dup_rank);
+    return cudaGetLastError();
+}
+
+static int bits_for(int ntiles) {
+    int b = 1;
+    while ((1 << b) < ntiles) b++;
+    return b;
+}
+
+cudaError_t tile_sort(void *temp, size_t temp_bytes, const uint32_t *tkey, uint32_t *skey,
+                      const int32_t *iota, int32_t *perm, int64_t K, int ntiles, cudaStream_t st) {
+    if (K == 0) return cudaSuccess;
+    return cub::DeviceRadixSort::SortPairs(temp, temp_bytes, tkey, skey, iota, perm, (int)K, 0,
+                                           bits_for(ntiles), st);
+}
+
+cudaError_t tile_sort_temp(int64_t K, int ntiles, size_t *bytes) {
+    return cub::DeviceRadixSort::SortPairs((void *)nullptr, *bytes, (const uint32_t *)nullptr,
+                                           (uint32_t *)nullptr, (const int32_t *)nullptr,
+                                           (int32_t *)nullptr, (int)K, 0, bits_for(ntiles));
+}
+
+cudaError_t records_sort_temp(int64_t m, size_t *bytes) {
+    return cub::DeviceRadixSort::SortPairs((void *)nullptr, *bytes, (const uint64_t *)nullptr,
+                                           (uint64_t *)nullptr, (const int32_t *)nullptr,
+                                           (int32_t *)nullptr, (int)m, 0, 64);
+}
+
+cudaError_t records_sort(void *temp, size_t temp_bytes, const uint64_t *key, uint64_t *skey,
+                         const int32_t *iota, int32_t *sidx, int64_t m, cudaStream_t st) {
+    if (m == 0) return cudaSuccess;
+    return cub::DeviceRadixSort::SortPairs(temp, temp_bytes, key, skey, iota, sidx, (int)m, 0, 64,
+                                           st);
+}
+
+cudaError_t launch_tile_ranges(int64_t K, const uint32_t *skey, int2 *rng, int ntiles,
+                               cudaStream_t st) {
+    cudaError_t e = cudaMemsetAsync(rng, 0, sizeof(int2) * (size_t)ntiles, st);
+    if (e != cudaSuccess || K == 0) return e;
+    k_tile_ranges<<<grid_for(K, 256), 256, 0, st>>>(K, skey, rng);
+    return cudaGetLastError();
+}
+
+template <int MODE>
+static cudaError_t launch_raster_t(const RasterArgs &a, int ntiles, cudaStream_t st) {
+    size_t smem = sizeof(RasterSmem);
+    static bool configured = false;
+    if (!configured) {
+        cudaError_t e = cudaFuncSetAttribute(k_raster<MODE>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)smem);
+        if (e != cudaSuccess) return e;
+        configured = true;
+    }
+    k_raster<MODE><<<ntiles, kBlock, smem, st>>>(a);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_raster(int mode, const RasterArgs &a, int ntiles, cudaStream_t st) {
+    if (ntiles == 0) return cudaSuccess;
+    switch (mode) {
+        case kRender: return launch_raster_t<kRender>(a, ntiles, st);
+        case kImportance: return launch_raster_t<kImportance>(a, ntiles, st);
+        case kScore: return launch_raster_t<kScore>(a, ntiles, st);
+        case kRecords: return launch_raster_t<kRecords>(a, ntiles, st);
+    }
+    return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_splat_reduce(int64_t n, const int32_t *ids, const int64_t *offs,
+                                const double2 *partial, double P, int64_t cam_row, double *cam_imp,
+                                double *imp_acc, double *dmse_acc, cudaStream_t st) {
+    if (n == 0) return cudaSuccess;
+    k_splat_reduce<<<grid_for(n, 256), 256, 0, st>>>(n, ids, offs, partial, P, cam_row, cam_imp,
+                                                      imp_acc, dmse_acc);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_mse_reduce(int ntiles, const double *tile_se, double P, double *mse_acc,
+                              cudaStream_t st) {
+    k_mse_reduce<<<1, 1024, 0, st>>>(ntiles, tile_se, P, mse_acc);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_finalize(int64_t n, int S, double *imp, double *dmse, double *mse,
+                            cudaStream_t st) {
+    int64_t m = n > 0 ? n : 1;
+    k_finalize<<<grid_for(m, 256), 256, 0, st>>>(n, (double)S, imp, dmse, mse);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_records_gather(int64_t m, const uint64_t *skey, const int32_t *sidx,
+                                  const int32_t *ids, const double *ra, const double *rt,
+                                  const double *rp, int64_t *splat_ids, int64_t *pixels,
+                                  double *alphas, double *trans_at, double *partials,
+                                  cudaStream_t st) {
+    if (m == 0) return cudaSuccess;
+    k_records_gather<<<grid_for(m, 256), 256, 0, st>>>(m, skey, sidx, ids, ra, rt, rp, splat_ids,
+                                                        pixels, alphas, trans_at, partials);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_colors_from_rec(int64_t n, const uint64_t *key, const SplatRec *rec,
+                                   double *colors, cudaStream_t st) {
+    if (n == 0) return cudaSuccess;
+    k_colors_from_rec<<<grid_for(n, 256), 256, 0, st>>>(n, key, rec, colors);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_bin_outputs(int64_t n, const uint64_t *skey, const int32_t *sids,
+                               unsigned long long *nvalid_dev, int64_t *order, int ntiles,
+                               const int2 *rng, int64_t K, int64_t *tile_offsets,
+                               const int32_t *perm, const int32_t *dup_id, int32_t *tile_splats,
+                               cudaStream_t st) {
+    cudaError_t e = cudaMemsetAsync(nvalid_dev, 0, sizeof(unsigned long long), st);
+    if (e != cudaSuccess) return e;
+    if (n > 0) {
+        k_count_valid<<<grid_for(n, 256), 256, 0, st>>>(n, skey, nvalid_dev);
+        k_order_out<<<grid_for(n, 256), 256, 0, st>>>(n, sids, order);
+    }
+    if (tile_offsets) k_tile_offsets<<<grid_for(ntiles + 1, 128), 128, 0, st>>>(ntiles, rng, K,
+                                                                               tile_offsets);
+    if (tile_splats && K > 0)
+        k_tile_splats<<<grid_for(K, 256), 256, 0, st>>>(K, perm, dup_id, tile_splats);
+    return cudaGetLastError();
+}
+
+}  // namespace potr

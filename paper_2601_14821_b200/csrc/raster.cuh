@@ -1,0 +1,83 @@
+// raster.cuh -- launch interface of the prune-score kernels (raster.cu).
+#pragma once
+
+#include "common.cuh"
+
+namespace potr {
+
+enum RasterMode { kRender = 0, kImportance = 1, kScore = 2, kRecords = 3 };
+
+struct RasterArgs {
+    const SplatRec *rec;
+    const int32_t *perm;      // sorted pair -> duplicate index
+    const int32_t *dup_id;    // duplicate index -> splat id
+    const int32_t *dup_rank;  // duplicate index -> depth rank (records mode)
+    const int2 *ranges;       // per tile [start, end) into perm
+    int tiles_x;
+    int width, height;
+    const double *target;     // (H,W,3), score mode
+    double *image;            // (H,W,3) nullable
+    double *trans;            // (H,W) nullable
+    double2 *partial;         // per duplicate (dSE, T*alpha)
+    double *tile_se;          // per tile squared error (score mode)
+    // records mode
+    unsigned long long *rec_counter;
+    int64_t rec_capacity;
+    uint64_t *rec_key;
+    double *rec_alpha, *rec_t, *rec_p;
+};
+
+size_t raster_smem_bytes();
+
+cudaError_t launch_preprocess(const potr_splats &sp, const Cam &cam, int tiles_x, int all_colors,
+                              SplatRec *rec, uint64_t *key, int32_t *cnt, cudaStream_t st);
+cudaError_t launch_project_dump(const potr_splats &sp, const Cam &cam, double *mean2d,
+                                double *cov2d, double *depth, double *radius, uint8_t *valid,
+                                double *colors, cudaStream_t st);
+cudaError_t launch_iota(int64_t n, int32_t *out, cudaStream_t st);
+cudaError_t depth_sort_temp(int64_t n, size_t *bytes);
+cudaError_t depth_sort(void *temp, size_t temp_bytes, const uint64_t *key, uint64_t *skey,
+                       const int32_t *iota, int32_t *sids, int64_t n, cudaStream_t st);
+cudaError_t scan_temp(int64_t n, size_t *bytes);
+cudaError_t scan_counts(void *temp, size_t temp_bytes, const int32_t *ids, const int32_t *cnt,
+                        int64_t *cnt_sorted, int64_t *offs, int64_t n, cudaStream_t st);
+cudaError_t launch_duplicate(int64_t n, const int32_t *ids, const int64_t *offs,
+                             const SplatRec *rec, int tiles_x, uint32_t *tkey, int32_t *dup_id,
+                             int32_t *dup_rank, cudaStream_t st);
+cudaError_t tile_sort_temp(int64_t K, int ntiles, size_t *bytes);
+cudaError_t tile_sort(void *temp, size_t temp_bytes, const uint32_t *tkey, uint32_t *skey,
+                      const int32_t *iota, int32_t *perm, int64_t K, int ntiles, cudaStream_t st);
+cudaError_t records_sort_temp(int64_t m, size_t *bytes);
+cudaError_t records_sort(void *temp, size_t temp_bytes, const uint64_t *key, uint64_t *skey,
+                         const int32_t *iota, int32_t *sidx, int64_t m, cudaStream_t st);
+cudaError_t launch_tile_ranges(int64_t K, const uint32_t *skey, int2 *rng, int ntiles,
+                               cudaStream_t st);
+cudaError_t launch_raster(int mode, const RasterArgs &a, int ntiles, cudaStream_t st);
+cudaError_t launch_splat_reduce(int64_t n, const int32_t *ids, const int64_t *offs,
+                                const double2 *partial, double P, int64_t cam_row, double *cam_imp,
+                                double *imp_acc, double *dmse_acc, cudaStream_t st);
+cudaError_t launch_mse_reduce(int ntiles, const double *tile_se, double P, double *mse_acc,
+                              cudaStream_t st);
+cudaError_t launch_finalize(int64_t n, int S, double *imp, double *dmse, double *mse,
+                            cudaStream_t st);
+cudaError_t launch_records_gather(int64_t m, const uint64_t *skey, const int32_t *sidx,
+                                  const int32_t *ids, const double *ra, const double *rt,
+                                  const double *rp, int64_t *splat_ids, int64_t *pixels,
+                                  double *alphas, double *trans_at, double *partials,
+                                  cudaStream_t st);
+cudaError_t launch_colors_from_rec(int64_t n, const uint64_t *key, const SplatRec *rec,
+                                   double *colors, cudaStream_t st);
+cudaError_t launch_bin_outputs(int64_t n, const uint64_t *skey, const int32_t *sids,
+                               unsigned long long *nvalid_dev, int64_t *order, int ntiles,
+                               const int2 *rng, int64_t K, int64_t *tile_offsets,
+                               const int32_t *perm, const int32_t *dup_id, int32_t *tile_splats,
+                               cudaStream_t st);
+
+// SH recompute (sh.cu)
+cudaError_t launch_sh_accumulate(const potr_splats &sp, int ncam, const double *eyes_dev,
+                                 const double *cam_imp, double *neq, cudaStream_t st);
+cudaError_t launch_sh_solve(const potr_splats &sp, const double *neq, double lambda_y,
+                            double par_thr, double zero_thr, double *rgb, double *ycocg,
+                            int8_t *status, cudaStream_t st);
+
+}  // namespace potr

@@ -1,0 +1,63 @@
+"""Rebind the reference package (potr) to the B200 implementations.
+
+The reference binds names at import time, so patching
+potr.rasterizer alone would miss potr.pruning's `compute_delta_mse`,
+potr.pipeline's `compute_importance` / `render_targets` / `compact_scene`,
+and so on.  install() rebinds every import site listed below and returns an
+uninstall callable.
+"""
+
+import importlib
+
+from . import compaction as _comp
+from . import rasterizer as _rast
+
+PATCH_SET = {
+    "potr.rasterizer": {
+        "forward_stats": _rast.forward_stats,
+        "compute_delta_mse": _rast.compute_delta_mse,
+        "compute_importance": _rast.compute_importance,
+        "render_targets": _rast.render_targets,
+        "render_image": _rast.render_image,
+        "render_with_records": _rast.render_with_records,
+        "project_splats": _rast.project_splats,
+        "splat_colors": _rast.splat_colors,
+    },
+    "potr.pruning": {"compute_delta_mse": _rast.compute_delta_mse},
+    "potr.pipeline": {
+        "compute_importance": _rast.compute_importance,
+        "render_targets": _rast.render_targets,
+        "compact_scene": _comp.compact_scene,
+    },
+    "potr.cli": {
+        "compute_importance": _rast.compute_importance,
+        "render_targets": _rast.render_targets,
+    },
+    "potr.compaction": {
+        "render_image": _rast.render_image,
+        "compact_scene": _comp.compact_scene,
+    },
+    "potr.metrics": {"render_image": _rast.render_image},
+}
+
+
+def install(modules=None):
+    """Patch the reference modules in place; returns uninstall()."""
+    saved = []
+    for modname, names in PATCH_SET.items():
+        if modules is not None and modname not in modules:
+            continue
+        try:
+            mod = importlib.import_module(modname)
+        except ImportError:
+            continue
+        for name, fn in names.items():
+            if hasattr(mod, name):
+                saved.append((mod, name, getattr(mod, name)))
+                setattr(mod, name, fn)
+
+    def uninstall():
+        for mod, name, old in reversed(saved):
+            setattr(mod, name, old)
+
+    return uninstall

@@ -1,0 +1,307 @@
+"""CUDA path vs golden vectors (reference outputs) and the CPU oracle.
+
+Tolerances (SURVEY.md 8a / BASELINE north_star): splat order, tile keys,
+projection and prune mask bit-exact; per-splat scores within 1e-4 relative
+(we hold them to 1e-9: the path is fp64); SH coefficients and AC sparsity
+within 1e-4 absolute; PSNR after pruning within 0.01 dB.
+"""
+
+import numpy as np
+import pytest
+
+from tests.conftest import (golden, oracle_scene, perturbed, score_close, sh_scene, small_scene)
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def R(cuda):
+    from paper_2601_14821_b200 import rasterizer
+    return rasterizer
+
+
+@pytest.fixture(scope="module")
+def C(cuda):
+    from paper_2601_14821_b200 import compaction
+    return compaction
+
+
+def test_native_library_is_loaded(R):
+    import paper_2601_14821_b200._native as N
+    from paper_2601_14821_b200 import device
+    ctx = device.context()
+    assert N._lib is not None
+    before = ctx.launches()
+    splats, cams = small_scene()
+    R.render_image(splats, cams[0])
+    assert ctx.launches() > before
+
+
+def test_projection_bit_exact(R):
+    splats, cams = small_scene()
+    g = golden("small_scene")
+    p = R.project_splats(splats, cams[0])
+    assert np.array_equal(p.valid, g["proj_valid"])
+    assert np.array_equal(p.mean2d, g["proj_mean2d"])
+    assert np.array_equal(p.cov2d, g["proj_cov2d"])
+    assert np.array_equal(p.view_depth, g["proj_depth"])
+    assert np.array_equal(p.radius, g["proj_radius"])
+    ids = g["colors0_ids"]
+    col = R.splat_colors(splats.subset(ids), cams[0])
+    np.testing.assert_allclose(col, g["colors0"], rtol=0, atol=1e-15)
+
+
+def test_binning_bit_exact(R, oracle):
+    """(tile, depth, id) lists of the GPU binning == the reference-derived lists."""
+    from paper_2601_14821_b200 import binning
+    splats, cams = small_scene()
+    g = golden("small_scene")
+    for c in (0, 1):
+        order, offsets, lists = binning.tile_lists(splats, cams[c])
+        assert np.array_equal(order, g[f"order{c}"])
+        assert np.array_equal(offsets, g[f"tile_offsets{c}"])
+        assert np.array_equal(lists, g[f"tile_splats{c}"])
+    # a larger scene against the oracle restatement
+    from paper_2601_14821_b200.fixture import make_fixture
+    big, bc = make_fixture(60000, 2, 1, width=320, height=200)
+    for cam in bc:
+        order, offsets, lists = binning.tile_lists(big, cam)
+        assert np.array_equal(order, oracle.depth_order(big, cam))
+        off, lst = oracle.tile_lists(big, cam, 16)
+        assert np.array_equal(offsets, off)
+        assert np.array_equal(lists, lst)
+
+
+def test_render_targets(R):
+    splats, cams = small_scene()
+    g = golden("small_scene")
+    imgs = R.render_targets(splats, cams)
+    for s, img in enumerate(imgs):
+        assert not img.flags.writeable
+        np.testing.assert_allclose(img, g["targets"][s], rtol=0, atol=1e-14)
+
+
+def test_forward_stats_small_scene(R):
+    splats, cams = small_scene()
+    g = golden("small_scene")
+    targets = [t for t in g["targets"]]
+    st = R.compute_delta_mse(perturbed(splats), cams, targets)
+    np.testing.assert_allclose(st.importance, g["pert_importance"], rtol=1e-12, atol=1e-20)
+    np.testing.assert_allclose(np.asarray(st.camera_importance), g["pert_camera_importance"],
+                               rtol=1e-12, atol=1e-20)
+    np.testing.assert_allclose(st.delta_mse, g["pert_delta_mse"], rtol=1e-9, atol=1e-22)
+    assert score_close(st.delta_mse, g["pert_delta_mse"], rel=1e-4)
+    assert st.mse == pytest.approx(float(g["pert_mse"]), rel=1e-12)
+    st0 = R.compute_delta_mse(splats, cams, targets)
+    np.testing.assert_allclose(st0.delta_mse, g["it1_delta_mse"], rtol=1e-9, atol=1e-22)
+    imp, ci = R.compute_importance(splats, cams)
+    np.testing.assert_allclose(imp, g["importance"], rtol=1e-12, atol=1e-20)
+    np.testing.assert_allclose(np.asarray(ci), g["camera_importance"], rtol=1e-12, atol=1e-20)
+
+
+def test_forward_stats_bit_reproducible(R):
+    splats, cams = small_scene()
+    g = golden("small_scene")
+    targets = [t for t in g["targets"]]
+    runs = [R.compute_delta_mse(perturbed(splats), cams, targets, threads=t) for t in (1, 4, 1)]
+    for other in runs[1:]:
+        assert np.array_equal(runs[0].delta_mse, other.delta_mse)
+        assert np.array_equal(runs[0].importance, other.importance)
+        assert runs[0].mse == other.mse
+
+
+def test_oracle_scenes(R):
+    o = golden("oracle_scenes")
+    for seed in range(20):
+        splats, cams = oracle_scene(seed)
+        targets = R.render_targets(splats, cams)
+        np.testing.assert_allclose(targets[0], o[f"s{seed}_image0"], rtol=0, atol=1e-14)
+        st = R.compute_delta_mse(perturbed(splats), cams, targets)
+        np.testing.assert_allclose(st.importance, o[f"s{seed}_importance"], rtol=1e-12,
+                                   atol=1e-20)
+        np.testing.assert_allclose(st.delta_mse, o[f"s{seed}_delta_mse"], rtol=1e-9,
+                                   atol=1e-22)
+
+
+def test_records_mode(R):
+    from paper_2601_14821_b200.fixture import random_scene
+    g = golden("records")
+    splats, cams = random_scene(4, num_splats=20)
+    rec = R.render_with_records(splats, cams[0])
+    assert np.array_equal(rec.splat_ids, g["splat_ids"])
+    assert np.array_equal(rec.pixels, g["pixels"])
+    np.testing.assert_allclose(rec.alphas, g["alphas"], rtol=1e-14, atol=0)
+    np.testing.assert_allclose(rec.trans_at, g["trans_at"], rtol=1e-13, atol=0)
+    np.testing.assert_allclose(rec.partials, g["partials"], rtol=0, atol=1e-14)
+    np.testing.assert_allclose(rec.colors, g["colors"], rtol=0, atol=1e-15)
+    np.testing.assert_allclose(rec.prune_deltas(), g["prune_deltas"], rtol=0, atol=1e-13)
+
+
+def test_c1_config(R):
+    from paper_2601_14821_b200.fixture import make_fixture
+    g = golden("c1")
+    splats, cams = make_fixture(10000, 8, 0, 128)
+    targets = R.render_targets(splats, cams)
+    st = R.compute_delta_mse(perturbed(splats), cams, targets)
+    np.testing.assert_allclose(st.importance, g["pert_importance"], rtol=1e-11, atol=1e-20)
+    np.testing.assert_allclose(st.delta_mse, g["pert_delta_mse"], rtol=1e-8, atol=1e-20)
+    st0 = R.compute_delta_mse(splats, cams, targets)
+    np.testing.assert_allclose(st0.delta_mse, g["it1_delta_mse"], rtol=1e-8, atol=1e-20)
+
+
+def test_prune_mask_bit_exact_and_psnr(R):
+    """The reference controller's 48 iterations driven by GPU scores reproduce
+    the reference's kept set exactly; PSNR of the pruned renders within 0.01 dB."""
+    from paper_2601_14821_b200 import pruning
+    from paper_2601_14821_b200.metrics import psnr
+    splats, cams = small_scene()
+    g = golden("small_scene")
+    targets = R.render_targets(splats, cams)
+    cfg = pruning.PruneConfig(delta_mse_max=10.0 ** (-8.8 - 2.0 * 0.5))
+    pruned, kept, reports = pruning.run_pruning(splats, cams, targets, cfg)
+    assert np.array_equal(kept, g["prune_kept"])
+    assert np.array_equal([r.removed for r in reports], g["prune_removed"])
+    for s, cam in enumerate(cams):
+        ours = R.render_image(pruned, cam)
+        ref = g["pruned_images"][s]
+        assert abs(psnr(ours, targets[s]) - psnr(ref, g["targets"][s])) <= 0.01
+
+
+def test_sh_recompute(C):
+    splats, cams = sh_scene()
+    g = golden("sh_scene")
+    ci = g["camera_importance"]
+    for i, lam in enumerate(g["lambdas"]):
+        cfg = C.CompactionConfig(float(lam), 0.8175744761936437, 0.5 / 51.0)
+        out, yc, rep = C.compact_scene(splats, cams, ci, cfg)
+        ref = g[f"ycocg_{i}"]
+        assert np.array_equal(yc == 0.0, ref == 0.0)
+        np.testing.assert_allclose(yc, ref, rtol=0, atol=1e-9)
+        np.testing.assert_allclose(out.sh, g[f"rgb_{i}"], rtol=0, atol=1e-9)
+        assert rep["fallback_dc_only"] == int(g[f"fallback_{i}"])
+        assert rep["failed"] == list(g[f"failed_{i}"])
+        assert abs(C.ac_sparsity(yc) - float(g[f"sparsity_{i}"])) <= 1e-4
+
+
+def test_sh_recompute_vs_oracle_with_device_importance(R, C, oracle):
+    """compute_importance keeps (S, N) in HBM; compact_scene reads it there."""
+    from paper_2601_14821_b200.fixture import make_fixture
+    splats, cams = make_fixture(20000, 10, 2, width=96, height=64)
+    imp, ci = R.compute_importance(splats, cams)
+    cfg = C.CompactionConfig(1e-8, 0.8175744761936437, 0.5 / 51.0)
+    _, yc, rep = C.compact_scene(splats, cams, ci, cfg)
+    rgb_o, yc_o, st_o = oracle.compact(splats, cams, np.asarray(ci), 1e-8, 0.8175744761936437,
+                                       0.5 / 51.0, threads=8)
+    assert np.array_equal(yc, yc_o)
+    assert rep["fallback_dc_only"] == int(np.count_nonzero(st_o == 3))
+
+
+def test_known_answers(R):
+    """Known-answer cases of the reference's tests/test_rasterizer.py."""
+    from paper_2601_14821_b200.scene import Camera, Splats
+    SH_DC = 0.28209479177387814
+
+    def flat(position, opacity, color, scale):
+        sh = np.zeros((1, 3, 16))
+        sh[0, :, 0] = np.asarray(color) / SH_DC
+        return Splats(np.array([position], dtype=np.float64), sh,
+                      np.array([opacity], dtype=np.float64), np.full((1, 3), scale),
+                      np.array([[1.0, 0, 0, 0]]))
+
+    def stack(*ss):
+        return Splats(*(np.concatenate([getattr(s, f) for s in ss]) for f in
+                        ("positions", "sh", "opacities", "scales", "rotations")))
+
+    cam = Camera(eye=np.zeros(3), rotation=np.eye(3), fx=100.0, fy=100.0, cx=8, cy=8,
+                 width=16, height=16)
+    p = R.project_splats(flat([0, 0, 1.0], 0.5, [1, 1, 1], 0.01), cam)
+    assert p.valid[0] and np.allclose(p.mean2d[0], [8.0, 8.0], atol=1e-9)
+    assert p.cov2d[0, 0] == pytest.approx(1.3, abs=1e-9)
+    assert not R.project_splats(flat([0, 0, 0.009], 0.5, [1, 1, 1], 0.01), cam).valid[0]
+    rec = R.render_with_records(flat([0, 0, 1.0], 0.5, [1, 1, 1], 50.0), cam)
+    assert rec.image[8, 8, 0] == pytest.approx(0.5, abs=1e-6)
+    (sid, alpha, t), = rec.pixel_record(8, 8)
+    assert sid == 0 and t == 1.0
+    front = flat([0, 0, 1.0], 0.5, [1, 1, 1], 50.0)
+    back = flat([0, 0, 2.0], 0.5, [1, 1, 1], 100.0)
+    img = R.render_image(stack(back, front), cam)
+    assert img[8, 8, 0] == pytest.approx(0.75, abs=1e-6)
+    both = stack(front, back)
+    targets = R.render_targets(both, [cam])
+    st = R.compute_delta_mse(both, [cam], targets)
+    rec = R.render_with_records(both, cam)
+    covered = np.unique(rec.pixels[rec.splat_ids == 0])
+    assert st.delta_mse[0] == pytest.approx(0.0625 * len(covered) / 256, rel=1e-3)
+    assert st.mse == 0.0
+    neg = flat([0, 0, 1.0], 0.5, [1, 1, 1], 50.0)
+    neg.sh[0, 2, 0] = -2.0 / SH_DC
+    assert R.render_image(neg, cam)[8, 8, 2] == 0.0
+    with pytest.raises(ValueError, match="shape"):
+        R.compute_delta_mse(both, [cam], [np.zeros((4, 4, 3))])
+    full = R.forward_stats(flat([0, 0, 1.0], 0.5, [1, 1, 1], 500.0), [cam])
+    assert full.importance[0] == pytest.approx(0.5, abs=1e-4)
+
+
+def test_delta_mse_brute_force(R):
+    """ΔMSE equals re-render-without-splat (tests/test_rasterizer.py:242-257)."""
+    from paper_2601_14821_b200.fixture import random_scene
+    splats, cams = random_scene(11, num_splats=20, num_cameras=2)
+    targets = R.render_targets(splats, cams)
+    pert = perturbed(splats)
+    st = R.compute_delta_mse(pert, cams, targets)
+    n = len(pert)
+    base = [R.render_image(pert, c) for c in cams]
+    brute = np.zeros(n)
+    for k in range(n):
+        mask = np.ones(n, dtype=bool)
+        mask[k] = False
+        for s, cam in enumerate(cams):
+            wo = R.render_image(pert.subset(mask), cam)
+            brute[k] += np.mean((wo - targets[s]) ** 2) - np.mean((base[s] - targets[s]) ** 2)
+    brute /= len(cams)
+    assert np.abs(brute - st.delta_mse).max() <= 1e-9
+
+
+def test_empty_and_degenerate(R, C):
+    from paper_2601_14821_b200.fixture import make_fixture
+    splats, cams = make_fixture(100, 2, 0, 32)
+    empty = splats.subset(np.zeros(100, dtype=bool))
+    img = R.render_image(empty, cams[0])
+    assert img.shape == (32, 32, 3) and not img.any()
+    targets = R.render_targets(splats, cams)
+    st = R.compute_delta_mse(empty, cams, targets)
+    assert st.delta_mse.shape == (0,)
+    assert st.mse == pytest.approx(np.mean([np.mean(t ** 2) for t in targets]), rel=1e-12)
+    # ragged: non-square, non-multiple-of-16 images
+    sp, cs = make_fixture(3000, 3, 4, width=37, height=21)
+    from oracle import oracle as O
+    tg = [O.render(sp, c)[0] for c in cs]
+    st = R.compute_delta_mse(perturbed(sp), cs, tg)
+    imp, _, dm, mse = O.forward_stats(perturbed(sp), cs, tg)
+    np.testing.assert_allclose(st.delta_mse, dm, rtol=1e-9, atol=1e-22)
+    np.testing.assert_allclose(st.importance, imp, rtol=1e-12, atol=1e-20)
+
+
+def test_host_c_abi(R, oracle):
+    """potr_forward_stats_host: the reference-facing C entry with host buffers."""
+    import ctypes
+    from paper_2601_14821_b200 import _native, device
+    splats, cams = small_scene()
+    g = golden("small_scene")
+    sp = perturbed(splats)
+    ctx = device.context()
+    n, S = len(sp), len(cams)
+    arrs = [np.ascontiguousarray(a, dtype=np.float64) for a in
+            (sp.positions, sp.sh, sp.opacities, sp.scales, sp.rotations)]
+    tg = [np.ascontiguousarray(t) for t in g["targets"]]
+    tptr = (ctypes.c_void_p * S)(*[t.ctypes.data for t in tg])
+    imp, ci, dm = np.empty(n), np.empty((S, n)), np.empty(n)
+    mse = np.empty(1)
+    ctx.call("potr_forward_stats_host", ctypes.c_int64(n),
+             *[a.ctypes.data_as(ctypes.c_void_p) for a in arrs], S,
+             _native.camera_array(cams), tptr, imp.ctypes.data_as(ctypes.c_void_p),
+             ci.ctypes.data_as(ctypes.c_void_p), dm.ctypes.data_as(ctypes.c_void_p),
+             mse.ctypes.data_as(ctypes.c_void_p))
+    np.testing.assert_allclose(dm, g["pert_delta_mse"], rtol=1e-9, atol=1e-22)
+    np.testing.assert_allclose(ci, g["pert_camera_importance"], rtol=1e-12, atol=1e-20)
+    assert mse[0] == pytest.approx(float(g["pert_mse"]), rel=1e-12)
