@@ -151,6 +151,33 @@ int potr_sh_solve(potr_ctx *ctx, const potr_splats *splats, const double *normal
                   double lambda_y, double parallel_threshold, double zero_threshold,
                   double *rgb, double *ycocg, int8_t *status);
 
+/* ---- evidence: live stage timing and work counters --------------------- */
+
+/* Stages timed with CUDA events on the context stream while profiling. */
+#define POTR_STAGE_PREPROCESS 0     /* kernel (a)                          */
+#define POTR_STAGE_DEPTH_SORT 1     /* CUB radix sort of fp64 depth keys   */
+#define POTR_STAGE_SCAN 2           /* pair-count gather + scan            */
+#define POTR_STAGE_DUPLICATE 3      /* (tile, splat) pair emission         */
+#define POTR_STAGE_TILE_SORT 4      /* CUB radix sort on tile id + ranges  */
+#define POTR_STAGE_RASTER 5         /* kernels (c)+(d), fused              */
+#define POTR_STAGE_REDUCE 6         /* per-splat slot sums, mse            */
+#define POTR_STAGE_SH_ACCUMULATE 7  /* kernel (e) normal equations         */
+#define POTR_STAGE_SH_SOLVE 8       /* kernel (e) batched Cholesky         */
+#define POTR_STAGE_COUNT 9
+
+/* Enabling resets the totals; read synchronizes and returns cumulative
+ * milliseconds and launch counts per stage (arrays of POTR_STAGE_COUNT). */
+int potr_profile_enable(potr_ctx *ctx, int enable);
+int potr_profile_read(potr_ctx *ctx, double *stage_ms, int64_t *stage_launches);
+
+/* Work counters for the roofline's algorithmic units (off by default):
+ * out[0] = bbox pixel evaluations E of the reference loop (rasterizer.py:159-166),
+ * out[1] = evaluations with T >= T_TERMINATE (exp evaluated),
+ * out[2] = composited contributions M, out[3] = (tile, splat) pairs.
+ * Enabling resets; read synchronizes. */
+int potr_counters_enable(potr_ctx *ctx, int enable);
+int potr_counters_read(potr_ctx *ctx, uint64_t *out);
+
 /* ---- host-buffer convenience (reference-facing drop-in) ---------------- */
 
 /* forward_stats with HOST arrays in the reference layouts; copies in, runs,

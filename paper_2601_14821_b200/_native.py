@@ -19,6 +19,8 @@ POTR_E_CUDA = -2
 POTR_E_NOMEM = -3
 POTR_E_CAPACITY = -4
 NEQ_STRIDE = 185
+STAGES = ["preprocess", "depth_sort", "scan", "duplicate", "tile_sort", "raster", "reduce",
+          "sh_accumulate", "sh_solve"]
 
 c_double_p = ctypes.POINTER(ctypes.c_double)
 
@@ -90,6 +92,10 @@ _SIGNATURES = {
     "potr_sh_solve": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(PotrSplats), ctypes.c_void_p,
                                      ctypes.c_double, ctypes.c_double, ctypes.c_double,
                                      ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]),
+    "potr_profile_enable": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int]),
+    "potr_profile_read": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]),
+    "potr_counters_enable": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int]),
+    "potr_counters_read": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p]),
     "potr_forward_stats_host": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p,
                                                ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
                                                ctypes.c_void_p, ctypes.c_int,
@@ -193,3 +199,24 @@ class Context:
 
     def launches(self):
         return int(self.lib.potr_kernel_launches(self.handle))
+
+    def profile(self, enable=True):
+        """Start (reset) or stop live per-stage CUDA-event timing."""
+        self.call("potr_profile_enable", int(bool(enable)))
+
+    def profile_read(self):
+        """{stage: (total ms, launches)} since profile() (synchronizes)."""
+        ms = (ctypes.c_double * len(STAGES))()
+        cnt = (ctypes.c_int64 * len(STAGES))()
+        self.call("potr_profile_read", ctypes.cast(ms, ctypes.c_void_p),
+                  ctypes.cast(cnt, ctypes.c_void_p))
+        return {name: (float(ms[i]), int(cnt[i])) for i, name in enumerate(STAGES)}
+
+    def counters(self, enable=True):
+        self.call("potr_counters_enable", int(bool(enable)))
+
+    def counters_read(self):
+        """(E bbox evaluations, live evaluations, contributions M, pairs K)."""
+        out = (ctypes.c_uint64 * 4)()
+        self.call("potr_counters_read", ctypes.cast(out, ctypes.c_void_p))
+        return tuple(int(v) for v in out)

@@ -35,6 +35,15 @@ struct potr_ctx {
     // host-buffer API staging
     DevBuf h_pos, h_sh, h_op, h_sc, h_rot, h_tg, h_imp, h_ci, h_dm, h_mse, h_rgb, h_yc, h_st;
     int64_t *pinned = nullptr;  // small pinned scratch for scalars
+    // live per-stage timing (CUDA events on ctx->stream) and work counters
+    bool profile = false;
+    std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> events;
+    std::vector<cudaEvent_t> event_pool;
+    double stage_ms[POTR_STAGE_COUNT] = {0};
+    int64_t stage_launches[POTR_STAGE_COUNT] = {0};
+    bool counting = false;
+    DevBuf counters;
+    int64_t pairs_total = 0;
 };
 
 namespace {
@@ -86,6 +95,38 @@ int ensure(potr_ctx *ctx, DevBuf &b, size_t bytes) {
         if (_rc) return _rc;                          \
     } while (0)
 
+cudaEvent_t take_event(potr_ctx *ctx) {
+    if (!ctx->event_pool.empty()) {
+        cudaEvent_t e = ctx->event_pool.back();
+        ctx->event_pool.pop_back();
+        return e;
+    }
+    cudaEvent_t e = nullptr;
+    cudaEventCreate(&e);
+    return e;
+}
+
+// RAII-free stage bracket: begin/end record events when profiling is on.
+struct Stage {
+    potr_ctx *ctx;
+    int id;
+    cudaEvent_t a = nullptr;
+    Stage(potr_ctx *c, int i) : ctx(c), id(i) {
+        if (ctx->profile) {
+            a = take_event(ctx);
+            cudaEventRecord(a, ctx->stream);
+        }
+    }
+    void end() {
+        if (ctx->profile && a) {
+            cudaEvent_t b = take_event(ctx);
+            cudaEventRecord(b, ctx->stream);
+            ctx->events.push_back({id, {a, b}});
+            a = nullptr;
+        }
+    }
+};
+
 template <typename T>
 T *P(DevBuf &b) {
     return reinterpret_cast<T *>(b.p);
@@ -130,6 +171,10 @@ int ensure_iota(potr_ctx *ctx, int64_t len) {
     return 0;
 }
 
+unsigned long long *counters(potr_ctx *ctx) {
+    return ctx->counting ? P<unsigned long long>(ctx->counters) : nullptr;
+}
+
 struct ViewGeom {
     int W, H, tiles_x, tiles_y, ntiles;
     double P;
@@ -169,16 +214,30 @@ int bin_view(potr_ctx *ctx, const potr_splats &sp, const potr_camera &cam, bool 
     CK(scan_temp(n, &t2));
     ENSURE(ctx->temp, t1 > t2 ? t1 : t2);
 
-    LAUNCH(1, launch_preprocess(sp, dc, g.tiles_x, all_colors ? 1 : 0, P<SplatRec>(ctx->rec),
-                                P<uint64_t>(ctx->key), P<int32_t>(ctx->cnt), ctx->stream));
-    CK(depth_sort(ctx->temp.p, ctx->temp.cap, P<uint64_t>(ctx->key), P<uint64_t>(ctx->skey),
-                  P<int32_t>(ctx->iota), P<int32_t>(ctx->sids), n, ctx->stream));
-    LAUNCH(1, scan_counts(ctx->temp.p, ctx->temp.cap, P<int32_t>(ctx->sids), P<int32_t>(ctx->cnt),
-                          P<int64_t>(ctx->cnt_sorted), P<int64_t>(ctx->offs), n, ctx->stream));
+    {
+        Stage _st(ctx, POTR_STAGE_PREPROCESS);
+        LAUNCH(1, launch_preprocess(sp, dc, g.tiles_x, all_colors ? 1 : 0, P<SplatRec>(ctx->rec),
+                                    P<uint64_t>(ctx->key), P<int32_t>(ctx->cnt),
+                                    counters(ctx), ctx->stream));
+        _st.end();
+    }
+    {
+        Stage _st(ctx, POTR_STAGE_DEPTH_SORT);
+        CK(depth_sort(ctx->temp.p, ctx->temp.cap, P<uint64_t>(ctx->key), P<uint64_t>(ctx->skey),
+                      P<int32_t>(ctx->iota), P<int32_t>(ctx->sids), n, ctx->stream));
+        _st.end();
+    }
+    {
+        Stage _st(ctx, POTR_STAGE_SCAN);
+        LAUNCH(1, scan_counts(ctx->temp.p, ctx->temp.cap, P<int32_t>(ctx->sids), P<int32_t>(ctx->cnt),
+                              P<int64_t>(ctx->cnt_sorted), P<int64_t>(ctx->offs), n, ctx->stream));
+        _st.end();
+    }
     CK(cudaMemcpyAsync(ctx->pinned, P<int64_t>(ctx->offs) + n, sizeof(int64_t),
                        cudaMemcpyDeviceToHost, ctx->stream));
     CK(cudaStreamSynchronize(ctx->stream));
     const int64_t K = ctx->pinned[0];
+    ctx->pairs_total += K;
     if (K > 0x7fffff00LL) return fail(ctx, POTR_E_ARG, "more than 2^31 tile pairs in one view");
 
     ENSURE(ctx->tkey, sizeof(uint32_t) * K);
@@ -193,14 +252,26 @@ int bin_view(potr_ctx *ctx, const potr_splats &sp, const potr_camera &cam, bool 
     CK(tile_sort_temp(K, g.ntiles, &t3));
     ENSURE(ctx->temp, t3);
 
-    LAUNCH(1, launch_duplicate(n, P<int32_t>(ctx->sids), P<int64_t>(ctx->offs),
-                               P<SplatRec>(ctx->rec), g.tiles_x, P<uint32_t>(ctx->tkey),
-                               P<int32_t>(ctx->dup_id),
-                               with_rank ? P<int32_t>(ctx->dup_rank) : nullptr, ctx->stream));
-    CK(tile_sort(ctx->temp.p, ctx->temp.cap, P<uint32_t>(ctx->tkey), P<uint32_t>(ctx->tskey),
-                 P<int32_t>(ctx->iota), P<int32_t>(ctx->perm), K, g.ntiles, ctx->stream));
-    LAUNCH(1, launch_tile_ranges(K, P<uint32_t>(ctx->tskey), P<int2>(ctx->ranges), g.ntiles,
-                                 ctx->stream));
+    {
+        Stage _st(ctx, POTR_STAGE_DUPLICATE);
+        LAUNCH(1, launch_duplicate(n, P<int32_t>(ctx->sids), P<int64_t>(ctx->offs),
+                                   P<SplatRec>(ctx->rec), g.tiles_x, P<uint32_t>(ctx->tkey),
+                                   P<int32_t>(ctx->dup_id),
+                                   with_rank ? P<int32_t>(ctx->dup_rank) : nullptr, ctx->stream));
+        _st.end();
+    }
+    {
+        Stage _st(ctx, POTR_STAGE_TILE_SORT);
+        CK(tile_sort(ctx->temp.p, ctx->temp.cap, P<uint32_t>(ctx->tkey), P<uint32_t>(ctx->tskey),
+                     P<int32_t>(ctx->iota), P<int32_t>(ctx->perm), K, g.ntiles, ctx->stream));
+        _st.end();
+    }
+    {
+        Stage _st(ctx, POTR_STAGE_TILE_SORT);
+        LAUNCH(1, launch_tile_ranges(K, P<uint32_t>(ctx->tskey), P<int2>(ctx->ranges), g.ntiles,
+                                     ctx->stream));
+        _st.end();
+    }
     *K_out = K;
     return 0;
 }
@@ -219,6 +290,7 @@ RasterArgs raster_args(potr_ctx *ctx, const potr_camera &cam) {
     a.height = g.H;
     a.partial = P<double2>(ctx->partial);
     a.tile_se = P<double>(ctx->tile_se);
+    a.counters = counters(ctx);
     return a;
 }
 
@@ -236,13 +308,24 @@ int score_views_impl(potr_ctx *ctx, const potr_splats *sp, int ncam, const potr_
         ViewGeom g = geom(cam);
         RasterArgs a = raster_args(ctx, cam);
         a.target = targets ? targets[s] : nullptr;
-        LAUNCH(1, launch_raster(targets ? kScore : kImportance, a, g.ntiles, ctx->stream));
-        LAUNCH(1, launch_splat_reduce(sp->n, P<int32_t>(ctx->sids), P<int64_t>(ctx->offs),
-                                      P<double2>(ctx->partial), g.P, s, cam_imp, imp_sum,
-                                      targets ? dmse_sum : nullptr, ctx->stream));
-        if (targets)
+        {
+            Stage _st(ctx, POTR_STAGE_RASTER);
+            LAUNCH(1, launch_raster(targets ? kScore : kImportance, a, g.ntiles, ctx->stream));
+            _st.end();
+        }
+        {
+            Stage _st(ctx, POTR_STAGE_REDUCE);
+            LAUNCH(1, launch_splat_reduce(sp->n, P<int32_t>(ctx->sids), P<int64_t>(ctx->offs),
+                                          P<double2>(ctx->partial), g.P, s, cam_imp, imp_sum,
+                                          targets ? dmse_sum : nullptr, ctx->stream));
+            _st.end();
+        }
+        if (targets) {
+            Stage _st(ctx, POTR_STAGE_REDUCE);
             LAUNCH(1, launch_mse_reduce(g.ntiles, P<double>(ctx->tile_se), g.P, mse_sum,
                                         ctx->stream));
+            _st.end();
+        }
     }
     return 0;
 }
@@ -287,6 +370,12 @@ void potr_destroy(potr_ctx *ctx) {
     for (DevBuf *b : bufs)
         if (b->p) cudaFree(b->p);
     if (ctx->pinned) cudaFreeHost(ctx->pinned);
+    if (ctx->counters.p) cudaFree(ctx->counters.p);
+    for (auto &ev : ctx->events) {
+        cudaEventDestroy(ev.second.first);
+        cudaEventDestroy(ev.second.second);
+    }
+    for (cudaEvent_t e : ctx->event_pool) cudaEventDestroy(e);
     delete ctx;
 }
 
@@ -486,8 +575,12 @@ int potr_sh_accumulate(potr_ctx *ctx, const potr_splats *splats, int ncam,
                        cudaMemcpyHostToDevice, ctx->stream));
     // the pageable source must stay alive until the copy is done
     CK(cudaStreamSynchronize(ctx->stream));
-    LAUNCH(1, launch_sh_accumulate(*splats, ncam, P<double>(ctx->eyes), camera_importance,
-                                   normal_eqs, ctx->stream));
+    {
+        Stage _st(ctx, POTR_STAGE_SH_ACCUMULATE);
+        LAUNCH(1, launch_sh_accumulate(*splats, ncam, P<double>(ctx->eyes), camera_importance,
+                                       normal_eqs, ctx->stream));
+        _st.end();
+    }
     return POTR_OK;
 }
 
@@ -503,8 +596,12 @@ int potr_sh_solve(potr_ctx *ctx, const potr_splats *splats, const double *normal
     if (!(lambda_y >= 0)) return fail(ctx, POTR_E_ARG, "lambda_y must be >= 0");
     if (!(parallel_threshold > 0 && parallel_threshold <= 1))
         return fail(ctx, POTR_E_ARG, "parallel_threshold must be in (0, 1]");
-    LAUNCH(1, launch_sh_solve(*splats, normal_eqs, lambda_y, parallel_threshold, zero_threshold,
-                              rgb, ycocg, status, ctx->stream));
+    {
+        Stage _st(ctx, POTR_STAGE_SH_SOLVE);
+        LAUNCH(1, launch_sh_solve(*splats, normal_eqs, lambda_y, parallel_threshold, zero_threshold,
+                                  rgb, ycocg, status, ctx->stream));
+        _st.end();
+    }
     return POTR_OK;
 }
 
@@ -522,6 +619,58 @@ int potr_compact(potr_ctx *ctx, const potr_splats *splats, int ncam, const potr_
     if (rc) return rc;
     return potr_sh_solve(ctx, splats, P<double>(ctx->neq), lambda_y, parallel_threshold,
                          zero_threshold, rgb, ycocg, status);
+}
+
+int potr_profile_enable(potr_ctx *ctx, int enable) {
+    if (!ctx) return POTR_E_ARG;
+    ctx->profile = enable != 0;
+    for (int i = 0; i < POTR_STAGE_COUNT; i++) {
+        ctx->stage_ms[i] = 0.0;
+        ctx->stage_launches[i] = 0;
+    }
+    return POTR_OK;
+}
+
+int potr_profile_read(potr_ctx *ctx, double *stage_ms, int64_t *stage_launches) {
+    if (!ctx) return POTR_E_ARG;
+    CK(cudaSetDevice(ctx->device));
+    CK(cudaStreamSynchronize(ctx->stream));
+    for (auto &ev : ctx->events) {
+        float ms = 0.f;
+        CK(cudaEventElapsedTime(&ms, ev.second.first, ev.second.second));
+        ctx->stage_ms[ev.first] += ms;
+        ctx->stage_launches[ev.first] += 1;
+        ctx->event_pool.push_back(ev.second.first);
+        ctx->event_pool.push_back(ev.second.second);
+    }
+    ctx->events.clear();
+    for (int i = 0; i < POTR_STAGE_COUNT; i++) {
+        if (stage_ms) stage_ms[i] = ctx->stage_ms[i];
+        if (stage_launches) stage_launches[i] = ctx->stage_launches[i];
+    }
+    return POTR_OK;
+}
+
+int potr_counters_enable(potr_ctx *ctx, int enable) {
+    if (!ctx) return POTR_E_ARG;
+    CK(cudaSetDevice(ctx->device));
+    ENSURE(ctx->counters, 4 * sizeof(unsigned long long));
+    CK(cudaMemsetAsync(ctx->counters.p, 0, 4 * sizeof(unsigned long long), ctx->stream));
+    ctx->counting = enable != 0;
+    ctx->pairs_total = 0;
+    return POTR_OK;
+}
+
+int potr_counters_read(potr_ctx *ctx, uint64_t *out) {
+    if (!ctx || !out) return POTR_E_ARG;
+    CK(cudaSetDevice(ctx->device));
+    ENSURE(ctx->counters, 4 * sizeof(unsigned long long));
+    CK(cudaMemcpyAsync(ctx->pinned, ctx->counters.p, 4 * sizeof(uint64_t), cudaMemcpyDeviceToHost,
+                       ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    for (int i = 0; i < 3; i++) out[i] = (uint64_t)ctx->pinned[i];
+    out[3] = (uint64_t)ctx->pairs_total;
+    return POTR_OK;
 }
 
 // ---- host-buffer convenience entry points --------------------------------

@@ -33,7 +33,8 @@ namespace potr {
 __global__ void __launch_bounds__(256) k_preprocess(potr_splats sp, Cam cam, int tiles_x,
                                                      int all_colors, SplatRec *__restrict__ rec,
                                                      uint64_t *__restrict__ key,
-                                                     int32_t *__restrict__ cnt) {
+                                                     int32_t *__restrict__ cnt,
+                                                     unsigned long long *counters) {
     int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (k >= sp.n) return;
     Proj pr = project_one(sp.positions + 3 * k, sp.scales + 3 * k, sp.rotations + 4 * k, cam);
@@ -76,6 +77,9 @@ __global__ void __launch_bounds__(256) k_preprocess(potr_splats sp, Cam cam, int
             int tx0 = (int)x0 >> kTileLog2, tx1 = (int)x1 >> kTileLog2;
             int ty0 = (int)y0 >> kTileLog2, ty1 = (int)y1 >> kTileLog2;
             c = (tx1 - tx0 + 1) * (ty1 - ty0 + 1);
+            if (counters)  // E: pixels the reference loop visits (rasterizer.py:159-161)
+                atomicAdd(&counters[0],
+                          (unsigned long long)((x1 - x0 + 1.0) * (y1 - y0 + 1.0)));
         }
     }
     key[k] = kk;
@@ -207,13 +211,22 @@ __global__ void __launch_bounds__(kBlock, 2) k_raster(RasterArgs a) {
                 if (R.x1 < wx0 || R.x0 > wx1 || R.y1 < wy0 || R.y0 > wy1) continue;
                 bool contrib = false;
                 double alpha = 0.0;
-                if (!done && px >= R.x0 && px <= R.x1 && py >= R.y0 && py <= R.y1) {
+                const bool live = !done && px >= R.x0 && px <= R.x1 && py >= R.y0 && py <= R.y1;
+                if (live) {
                     double dx = pxc - R.mx, dy = pyc - R.my;
                     double power = -0.5 * (R.ia * dx * dx + R.ic * dy * dy) - R.ib * dx * dy;
                     if (power >= R.pthr) {
                         alpha = R.opac * exp(power);
                         if (alpha > kAlphaCap) alpha = kAlphaCap;
                         contrib = !(alpha < kAlphaFloor);
+                    }
+                }
+                if (a.counters) {
+                    unsigned lv = __ballot_sync(0xffffffffu, live);
+                    unsigned ct = __ballot_sync(0xffffffffu, contrib);
+                    if (lane == 0) {
+                        atomicAdd(&a.counters[1], (unsigned long long)__popc(lv));
+                        atomicAdd(&a.counters[2], (unsigned long long)__popc(ct));
                     }
                 }
                 double timp = 0.0;
@@ -509,9 +522,11 @@ static inline unsigned grid_for(int64_t n, int block) {
 size_t raster_smem_bytes() { return sizeof(RasterSmem); }
 
 cudaError_t launch_preprocess(const potr_splats &sp, const Cam &cam, int tiles_x, int all_colors,
-                              SplatRec *rec, uint64_t *key, int32_t *cnt, cudaStream_t st) {
+                              SplatRec *rec, uint64_t *key, int32_t *cnt,
+                              unsigned long long *counters, cudaStream_t st) {
     if (sp.n == 0) return cudaSuccess;
-    k_preprocess<<<grid_for(sp.n, 256), 256, 0, st>>>(sp, cam, tiles_x, all_colors, rec, key, cnt);
+    k_preprocess<<<grid_for(sp.n, 256), 256, 0, st>>>(sp, cam, tiles_x, all_colors, rec, key, cnt,
+                                                       counters);
     return cudaGetLastError();
 }
 

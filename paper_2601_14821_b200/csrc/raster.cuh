@@ -25,12 +25,15 @@ struct RasterArgs {
     int64_t rec_capacity;
     uint64_t *rec_key;
     double *rec_alpha, *rec_t, *rec_p;
+    // evidence counters (nullable): [1] live evaluations, [2] contributions
+    unsigned long long *counters;
 };
 
 size_t raster_smem_bytes();
 
 cudaError_t launch_preprocess(const potr_splats &sp, const Cam &cam, int tiles_x, int all_colors,
-                              SplatRec *rec, uint64_t *key, int32_t *cnt, cudaStream_t st);
+                              SplatRec *rec, uint64_t *key, int32_t *cnt,
+                              unsigned long long *counters, cudaStream_t st);
 cudaError_t launch_project_dump(const potr_splats &sp, const Cam &cam, double *mean2d,
                                 double *cov2d, double *depth, double *radius, uint8_t *valid,
                                 double *colors, cudaStream_t st);

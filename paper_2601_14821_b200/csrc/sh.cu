@@ -217,12 +217,11 @@ __global__ void __launch_bounds__(128) k_sh_solve(potr_splats sp, const double *
         double norms[16];
         for (int i = 0; i < 16; i++) norms[i] = sqrt(G[tri(i, i)]);
         bool mask[16];
-        mask[0] = true;
+        for (int i = 0; i < 16; i++) mask[i] = (i == 0);
         for (int i = 1; i < 16; i++) {
-            mask[i] = false;
             if (norms[i] == 0.0) continue;
             bool par = false;
-            for (int j = 0; j < 16; j++) {
+            for (int j = 0; j < i; j++) {
                 if (!mask[j]) continue;
                 double gij = j < i ? G[tri(j, i)] : G[tri(i, j)];
                 double cs = fabs(gij) / (norms[i] * norms[j]);
