@@ -120,7 +120,7 @@ int potr_project(potr_ctx *ctx, const potr_splats *splats, const potr_camera *ca
 
 /* Tile binning evidence: the global stable depth order of valid splats
  * (rasterizer.py:248-250) and the per-tile splat lists in (tile, depth, id)
- * order for 16x16 tiles.  order (n) and tile_offsets (ntiles+1) are device
+ * order for the rasterizer's 8x4-pixel tiles (row-major tile ids).  order (n) and tile_offsets (ntiles+1) are device
  * int64 outputs; tile_splats (capacity) device int32.  *n_valid and *n_pairs
  * are host outputs (synchronizes).  tile_splats may be NULL to size. */
 int potr_bin(potr_ctx *ctx, const potr_splats *splats, const potr_camera *cam,

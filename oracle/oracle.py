@@ -154,23 +154,23 @@ def forward_stats(splats, cams, targets=None, threads=1):
     return imp, cam_imp, dm, (mse.value if targets is not None else None)
 
 
-def tile_lists(splats, cam, tile=16):
+def tile_lists(splats, cam, tile_w=8, tile_h=4):
     """Per-tile splat lists in (tile, depth, id) order, restated from the
     reference's clipped bbox (rasterizer.py:135-151) and stable depth order
     (:248-250).  Returns (offsets (ntiles+1,), splat ids)."""
     n, pos, sh, op, sc, rot = _splat_arrays(splats)
-    tw = (int(cam.width) + tile - 1) // tile
-    th = (int(cam.height) + tile - 1) // tile
+    tw = (int(cam.width) + tile_w - 1) // tile_w
+    th = (int(cam.height) + tile_h - 1) // tile_h
     offsets = np.empty(tw * th + 1, dtype=np.int64)
     total = ctypes.c_int64(0)
     c = _cam(cam)
     L = lib()
     _check(L.oracle_tile_lists(ctypes.c_int64(n), _p(pos), _p(sc), _p(rot), ctypes.byref(c),
-                               ctypes.c_int(tile), _p(offsets), None, ctypes.c_int64(0),
+                               ctypes.c_int(tile_w), ctypes.c_int(tile_h), _p(offsets), None, ctypes.c_int64(0),
                                ctypes.byref(total)), "tile_lists")
     ids = np.empty(max(total.value, 1), dtype=np.int32)
     _check(L.oracle_tile_lists(ctypes.c_int64(n), _p(pos), _p(sc), _p(rot), ctypes.byref(c),
-                               ctypes.c_int(tile), _p(offsets), _p(ids), ctypes.c_int64(total.value),
+                               ctypes.c_int(tile_w), ctypes.c_int(tile_h), _p(offsets), _p(ids), ctypes.c_int64(total.value),
                                ctypes.byref(total)), "tile_lists")
     return offsets, ids[:total.value].copy()
 

@@ -576,8 +576,8 @@ int oracle_forward_stats(int64_t n, const double *pos, const double *sh, const d
 /* in *total (even when cap is too small).                                    */
 
 int oracle_tile_lists(int64_t n, const double *pos, const double *scales, const double *rot,
-                      const ocam *cam, int tile, int64_t *tile_offsets, int32_t *tile_splats,
-                      int64_t cap, int64_t *total) {
+                      const ocam *cam, int tile_w, int tile_h, int64_t *tile_offsets,
+                      int32_t *tile_splats, int64_t cap, int64_t *total) {
     oview v;
     double *zsh = (double *)calloc((size_t)(48 * (n > 0 ? n : 1)), sizeof(double));
     if (!zsh) return -1;
@@ -585,7 +585,7 @@ int oracle_tile_lists(int64_t n, const double *pos, const double *scales, const 
     free(zsh);
     if (rc) return rc;
     int W = cam->width, H = cam->height;
-    int tw = (W + tile - 1) / tile, th = (H + tile - 1) / tile;
+    int tw = (W + tile_w - 1) / tile_w, th = (H + tile_h - 1) / tile_h;
     int64_t ntiles = (int64_t)tw * th;
     int64_t *cnt = (int64_t *)calloc((size_t)(ntiles + 1), sizeof(int64_t));
     int32_t *bb = (int32_t *)malloc(sizeof(int32_t) * 4 * (size_t)(v.n_valid > 0 ? v.n_valid : 1));
@@ -619,10 +619,10 @@ int oracle_tile_lists(int64_t n, const double *pos, const double *scales, const 
                     b[0] = -1;
                     continue;
                 }
-                b[0] = (int32_t)x0 / tile;
-                b[1] = (int32_t)x1 / tile;
-                b[2] = (int32_t)y0 / tile;
-                b[3] = (int32_t)y1 / tile;
+                b[0] = (int32_t)x0 / tile_w;
+                b[1] = (int32_t)x1 / tile_w;
+                b[2] = (int32_t)y0 / tile_h;
+                b[3] = (int32_t)y1 / tile_h;
             }
             if (b[0] < 0) continue;
             for (int ty = b[2]; ty <= b[3]; ty++)

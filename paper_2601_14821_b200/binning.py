@@ -2,7 +2,7 @@
 per-tile splat lists, for parity against the reference-derived lists.
 
 depth_order == ids[np.argsort(view_depth[ids], kind="stable")] of
-rasterizer.py:248-250; tile lists are the 16x16 tiles each splat's clipped
+rasterizer.py:248-250; tile lists are the 8x4-pixel tiles each splat's clipped
 bbox (rasterizer.py:135-151) touches, in (tile, depth, id) order.
 """
 
@@ -14,7 +14,7 @@ import torch
 from . import _native
 from . import device as D
 
-TILE = 16
+TILE_W, TILE_H = 8, 4  # csrc/common.cuh kTileW x kTileH
 
 
 def tile_lists(splats, camera):
@@ -25,8 +25,8 @@ def tile_lists(splats, camera):
     ds = D.DeviceSplats.from_host(splats, dev)
     n = ds.n
     cam = _native.camera_struct(camera)
-    tw = (int(camera.width) + TILE - 1) // TILE
-    th = (int(camera.height) + TILE - 1) // TILE
+    tw = (int(camera.width) + TILE_W - 1) // TILE_W
+    th = (int(camera.height) + TILE_H - 1) // TILE_H
     order = D.empty(max(n, 1), dev, torch.int64)
     offsets = D.empty(tw * th + 1, dev, torch.int64)
     nv = ctypes.c_int64(0)

@@ -44,6 +44,7 @@ struct potr_ctx {
     bool counting = false;
     DevBuf counters;
     int64_t pairs_total = 0;
+    DevBuf tile_counter;
 };
 
 namespace {
@@ -184,8 +185,8 @@ ViewGeom geom(const potr_camera &c) {
     ViewGeom g;
     g.W = c.width;
     g.H = c.height;
-    g.tiles_x = (g.W + kTile - 1) / kTile;
-    g.tiles_y = (g.H + kTile - 1) / kTile;
+    g.tiles_x = (g.W + kTileW - 1) / kTileW;
+    g.tiles_y = (g.H + kTileH - 1) / kTileH;
     g.ntiles = g.tiles_x * g.tiles_y;
     g.P = (double)g.W * (double)g.H;
     return g;
@@ -207,6 +208,7 @@ int bin_view(potr_ctx *ctx, const potr_splats &sp, const potr_camera &cam, bool 
     ENSURE(ctx->offs, sizeof(int64_t) * (n + 1));
     ENSURE(ctx->ranges, sizeof(int2) * g.ntiles);
     ENSURE(ctx->tile_se, sizeof(double) * g.ntiles);
+    ENSURE(ctx->tile_counter, sizeof(int));
     int rc = ensure_iota(ctx, n);
     if (rc) return rc;
     size_t t1 = 0, t2 = 0;
@@ -286,6 +288,8 @@ RasterArgs raster_args(potr_ctx *ctx, const potr_camera &cam) {
     a.dup_rank = P<int32_t>(ctx->dup_rank);
     a.ranges = P<int2>(ctx->ranges);
     a.tiles_x = g.tiles_x;
+    a.ntiles = g.ntiles;
+    a.tile_counter = P<int>(ctx->tile_counter);
     a.width = g.W;
     a.height = g.H;
     a.partial = P<double2>(ctx->partial);
@@ -371,6 +375,7 @@ void potr_destroy(potr_ctx *ctx) {
         if (b->p) cudaFree(b->p);
     if (ctx->pinned) cudaFreeHost(ctx->pinned);
     if (ctx->counters.p) cudaFree(ctx->counters.p);
+    if (ctx->tile_counter.p) cudaFree(ctx->tile_counter.p);
     for (auto &ev : ctx->events) {
         cudaEventDestroy(ev.second.first);
         cudaEventDestroy(ev.second.second);

@@ -37,11 +37,14 @@ constexpr double kShC3_4 = -0.4570457994644658;
 constexpr double kShC3_5 = 1.445305721320277;
 constexpr double kShC3_6 = -0.5900435899266435;
 
-// Tile geometry of the rasterizer: 16x16 pixel tiles, one CTA per tile,
-// eight warps each owning an 8x4 sub-rectangle.
-constexpr int kTile = 16;
-constexpr int kTileLog2 = 4;
-constexpr int kBlock = 256;
+// Tile geometry of the rasterizer: 8x4-pixel tiles, one warp per tile (lane =
+// pixel), so a tile's front-to-back walk needs no block barrier and every
+// listed splat overlaps the warp's pixels.
+constexpr int kTileW = 8;
+constexpr int kTileH = 4;
+constexpr int kTileWLog2 = 3;
+constexpr int kTileHLog2 = 2;
+constexpr int kRasterWarps = 4;  // warps (= independent tile workers) per CTA
 
 // Prefilter margin on the Gaussian exponent: power < log(floor/o) - margin
 // guarantees o*exp(power) < floor for any exp with < 1e-12 relative error,

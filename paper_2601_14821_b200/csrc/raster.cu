@@ -74,8 +74,8 @@ __global__ void __launch_bounds__(256) k_preprocess(potr_splats sp, Cam cam, int
             rec[k] = r;
         }
         if (draw) {
-            int tx0 = (int)x0 >> kTileLog2, tx1 = (int)x1 >> kTileLog2;
-            int ty0 = (int)y0 >> kTileLog2, ty1 = (int)y1 >> kTileLog2;
+            int tx0 = (int)x0 >> kTileWLog2, tx1 = (int)x1 >> kTileWLog2;
+            int ty0 = (int)y0 >> kTileHLog2, ty1 = (int)y1 >> kTileHLog2;
             c = (tx1 - tx0 + 1) * (ty1 - ty0 + 1);
             if (counters)  // E: pixels the reference loop visits (rasterizer.py:159-161)
                 atomicAdd(&counters[0],
@@ -122,8 +122,8 @@ __global__ void k_duplicate(int64_t n, const int32_t *__restrict__ ids,
     if (o == e) return;
     int32_t id = ids[r];
     const SplatRec &R = rec[id];
-    int tx0 = R.x0 >> kTileLog2, tx1 = R.x1 >> kTileLog2;
-    int ty0 = R.y0 >> kTileLog2, ty1 = R.y1 >> kTileLog2;
+    int tx0 = R.x0 >> kTileWLog2, tx1 = R.x1 >> kTileWLog2;
+    int ty0 = R.y0 >> kTileHLog2, ty1 = R.y1 >> kTileHLog2;
     for (int ty = ty0; ty <= ty1; ty++)
         for (int tx = tx0; tx <= tx1; tx++) {
             tkey[o] = (uint32_t)(ty * tiles_x + tx);
@@ -149,12 +149,10 @@ __global__ void k_iota(int64_t n, int32_t *out) {
 // ---------------------------------------------------------------------------
 // (c)+(d) tile rasterizer and removal-effect pass
 
-struct RasterSmem {
-    SplatRec rec[kBlock];
-    int32_t dup[kBlock];
-    int32_t rank[kBlock];
-    double2 red[kBlock / 32][kBlock];  // per-warp (dSE, T*alpha) per batch slot
-    double wsum[kBlock / 32];
+struct WarpSmem {
+    SplatRec rec[32];
+    int32_t dup[32];
+    int32_t rank[32];
 };
 
 __device__ __forceinline__ double warp_sum(double v) {
@@ -163,67 +161,80 @@ __device__ __forceinline__ double warp_sum(double v) {
     return v;
 }
 
-// MODE: kRender    forward only, writes image/trans
-//       kImportance forward with per-pair T*alpha slots (no targets)
-//       kScore     forward, then the removal-effect walk with targets
-//       kRecords   forward, appending every contribution record
+// One sample of rasterizer.py:162-171 for this lane's pixel: returns true when
+// the splat composites here (alpha >= ALPHA_FLOOR), with the capped alpha.
+__device__ __forceinline__ bool sample_alpha(const SplatRec &R, int px, int py, double pxc,
+                                             double pyc, bool live, double &alpha) {
+    if (!live) return false;
+    double dx = pxc - R.mx, dy = pyc - R.my;
+    double power = -0.5 * (R.ia * dx * dx + R.ic * dy * dy) - R.ib * dx * dy;
+    if (power < R.pthr) return false;  // o*exp(power) < ALPHA_FLOOR for certain
+    alpha = R.opac * exp(power);
+    if (alpha > kAlphaCap) alpha = kAlphaCap;
+    return !(alpha < kAlphaFloor);
+}
+
+// Stage one chunk (<= 32 pairs) of the tile's list into this warp's smem.
 template <int MODE>
-__global__ void __launch_bounds__(kBlock, 2) k_raster(RasterArgs a) {
+__device__ __forceinline__ void load_chunk(const RasterArgs &a, WarpSmem &S, int base, int cnt,
+                                           int lane) {
+    __syncwarp();
+    if (lane < cnt) {
+        int32_t d = a.perm[base + lane];
+        S.rec[lane] = a.rec[a.dup_id[d]];
+        S.dup[lane] = d;
+        if (MODE == kRecords) S.rank[lane] = a.dup_rank[d];
+    }
+    __syncwarp();
+}
+
+// MODE: kRender     forward only, writes image/trans
+//       kImportance forward with per-pair T*alpha slots (no targets)
+//       kScore      forward, then the removal-effect walk with targets
+//       kRecords    forward, appending every contribution record
+//
+// Persistent: each warp pulls 8x4 tiles from an atomic counter until none are
+// left; a tile's result depends only on its own list, so the schedule does not
+// affect the output bits.
+template <int MODE>
+__global__ void __launch_bounds__(32 * kRasterWarps, 4) k_raster(RasterArgs a) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    RasterSmem &S = *reinterpret_cast<RasterSmem *>(smem_raw);
+    WarpSmem &S = reinterpret_cast<WarpSmem *>(smem_raw)[threadIdx.x >> 5];
+    const int lane = threadIdx.x & 31;
+    const unsigned FULL = 0xffffffffu;
 
-    const int tile = blockIdx.x;
-    const int tx = tile % a.tiles_x, ty = tile / a.tiles_x;
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int wx0 = tx * kTile + (warp & 1) * 8, wy0 = ty * kTile + (warp >> 1) * 4;
-    const int wx1 = wx0 + 7, wy1 = wy0 + 3;
-    const int px = wx0 + (lane & 7), py = wy0 + (lane >> 3);
-    const bool inside = px < a.width && py < a.height;
-    const int64_t pix = (int64_t)py * a.width + px;
-    const int2 range = a.ranges[tile];
-    const int start = range.x, end = range.y > range.x ? range.y : range.x;
-    const int nbatch = (end - start + kBlock - 1) / kBlock;
-    const double pxc = (double)px + 0.5, pyc = (double)py + 0.5;
+    for (;;) {
+        int tile = 0;
+        if (lane == 0) tile = atomicAdd(a.tile_counter, 1);
+        tile = __shfl_sync(FULL, tile, 0);
+        if (tile >= a.ntiles) return;
 
-    // ---- pass 1: front-to-back compositing (rasterizer.py:159-201) -------
-    double T = 1.0, P0 = 0.0, P1 = 0.0, P2 = 0.0;
-    bool done = !inside;
-    int batches_done = 0;
-    for (int b = 0; b < nbatch; b++) {
-        const int base = start + b * kBlock;
-        const int cnt = min(kBlock, end - base);
-        __syncthreads();
-        if (threadIdx.x < cnt) {
-            int32_t d = a.perm[base + threadIdx.x];
-            int32_t id = a.dup_id[d];
-            S.rec[threadIdx.x] = a.rec[id];
-            S.dup[threadIdx.x] = d;
-            if (MODE == kRecords) S.rank[threadIdx.x] = a.dup_rank[d];
-        }
-        if (MODE == kImportance) {
-#pragma unroll
-            for (int w = 0; w < kBlock / 32; w++) S.red[w][threadIdx.x] = make_double2(0.0, 0.0);
-        }
-        __syncthreads();
-        if (!__all_sync(0xffffffffu, done)) {
-            for (int e = 0; e < cnt; e++) {
+        const int tx = tile % a.tiles_x, ty = tile / a.tiles_x;
+        const int px = tx * kTileW + (lane & 7), py = ty * kTileH + (lane >> 3);
+        const bool inside = px < a.width && py < a.height;
+        const int64_t pix = (int64_t)py * a.width + px;
+        const int2 range = a.ranges[tile];
+        const int start = range.x, end = range.y > range.x ? range.y : range.x;
+        const double pxc = (double)px + 0.5, pyc = (double)py + 0.5;
+
+        // ---- pass 1: front-to-back compositing (rasterizer.py:159-201) ----
+        double T = 1.0, P0 = 0.0, P1 = 0.0, P2 = 0.0;
+        bool done = !inside;
+        int stop = start;      // entries [start, stop) were walked
+        int written = start;   // importance slots written up to here
+        for (int base = start; base < end && !__all_sync(FULL, done); base += 32) {
+            const int cnt = min(32, end - base);
+            load_chunk<MODE>(a, S, base, cnt, lane);
+            double my_imp = 0.0;
+            int e = 0;
+            while (e < cnt) {
                 const SplatRec &R = S.rec[e];
-                if (R.x1 < wx0 || R.x0 > wx1 || R.y1 < wy0 || R.y0 > wy1) continue;
-                bool contrib = false;
-                double alpha = 0.0;
                 const bool live = !done && px >= R.x0 && px <= R.x1 && py >= R.y0 && py <= R.y1;
-                if (live) {
-                    double dx = pxc - R.mx, dy = pyc - R.my;
-                    double power = -0.5 * (R.ia * dx * dx + R.ic * dy * dy) - R.ib * dx * dy;
-                    if (power >= R.pthr) {
-                        alpha = R.opac * exp(power);
-                        if (alpha > kAlphaCap) alpha = kAlphaCap;
-                        contrib = !(alpha < kAlphaFloor);
-                    }
-                }
+                double alpha = 0.0;
+                const bool contrib = sample_alpha(R, px, py, pxc, pyc, live, alpha);
                 if (a.counters) {
-                    unsigned lv = __ballot_sync(0xffffffffu, live);
-                    unsigned ct = __ballot_sync(0xffffffffu, contrib);
+                    unsigned lv = __ballot_sync(FULL, live);
+                    unsigned ct = __ballot_sync(FULL, contrib);
                     if (lane == 0) {
                         atomicAdd(&a.counters[1], (unsigned long long)__popc(lv));
                         atomicAdd(&a.counters[2], (unsigned long long)__popc(ct));
@@ -243,7 +254,7 @@ __global__ void __launch_bounds__(kBlock, 2) k_raster(RasterArgs a) {
                             a.rec_p[3 * slot + 2] = P2;
                         }
                     }
-                    double w = T * alpha;
+                    const double w = T * alpha;
                     timp = w;
                     P0 += w * R.cr;
                     P1 += w * R.cg;
@@ -251,118 +262,74 @@ __global__ void __launch_bounds__(kBlock, 2) k_raster(RasterArgs a) {
                     T = T * (1.0 - alpha);
                     done = T < kTTerminate;
                 }
-                if (MODE == kImportance) {
-                    if (__any_sync(0xffffffffu, contrib)) {
-                        double s = warp_sum(timp);
-                        if (lane == 0) S.red[warp][e] = make_double2(0.0, s);
-                    }
+                if (MODE == kImportance && __any_sync(FULL, contrib)) {
+                    const double s = warp_sum(timp);
+                    if (lane == e) my_imp = s;
                 }
-                if (__all_sync(0xffffffffu, done)) break;
+                e++;
+                if (__all_sync(FULL, done)) break;
+            }
+            stop = base + e;
+            if (MODE == kImportance) {
+                if (lane < cnt) a.partial[S.dup[lane]] = make_double2(0.0, my_imp);
+                written = base + cnt;
             }
         }
-        if (MODE == kImportance) {
-            __syncthreads();
-            if (threadIdx.x < cnt) {
-                double2 acc = S.red[0][threadIdx.x];
-#pragma unroll
-                for (int w = 1; w < kBlock / 32; w++) {
-                    acc.x += S.red[w][threadIdx.x].x;
-                    acc.y += S.red[w][threadIdx.x].y;
-                }
-                a.partial[S.dup[threadIdx.x]] = acc;
+
+        if (MODE != kScore) {
+            if (inside && a.image) {
+                a.image[3 * pix] = P0;
+                a.image[3 * pix + 1] = P1;
+                a.image[3 * pix + 2] = P2;
             }
+            if (inside && a.trans) a.trans[pix] = T;
+            if (MODE == kImportance)  // pairs after the early-out contribute nothing
+                for (int j = written + lane; j < end; j += 32)
+                    a.partial[a.perm[j]] = make_double2(0.0, 0.0);
+            continue;
         }
-        batches_done = b + 1;
-        if (__syncthreads_count(done) == kBlock) break;
-    }
 
-    if (MODE != kScore) {
-        if (inside && a.image) {
-            a.image[3 * pix] = P0;
-            a.image[3 * pix + 1] = P1;
-            a.image[3 * pix + 2] = P2;
+        // ---- pass 2: removal effect (rasterizer.py:232-243, :322-336) -----
+        const double PK0 = P0, PK1 = P1, PK2 = P2;
+        double dr0 = 0.0, dr1 = 0.0, dr2 = 0.0, se = 0.0;
+        if (inside) {
+            dr0 = PK0 - a.target[3 * pix];
+            dr1 = PK1 - a.target[3 * pix + 1];
+            dr2 = PK2 - a.target[3 * pix + 2];
+            se = dr0 * dr0 + dr1 * dr1 + dr2 * dr2;
+            if (a.image) {
+                a.image[3 * pix] = PK0;
+                a.image[3 * pix + 1] = PK1;
+                a.image[3 * pix + 2] = PK2;
+            }
+            if (a.trans) a.trans[pix] = T;
         }
-        if (inside && a.trans) a.trans[pix] = T;
-        if (MODE == kImportance) {
-            // pairs after the early-out contribute nothing
-            for (int j = start + batches_done * kBlock + threadIdx.x; j < end; j += kBlock)
-                a.partial[a.perm[j]] = make_double2(0.0, 0.0);
-        }
-        return;
-    }
-
-    // ---- pass 2: removal effect (rasterizer.py:232-243, :322-336) --------
-    const double PK0 = P0, PK1 = P1, PK2 = P2;
-    double ct0 = 0.0, ct1 = 0.0, ct2 = 0.0;
-    double se = 0.0;
-    if (inside) {
-        ct0 = a.target[3 * pix];
-        ct1 = a.target[3 * pix + 1];
-        ct2 = a.target[3 * pix + 2];
-        double d0 = PK0 - ct0, d1 = PK1 - ct1, d2 = PK2 - ct2;
-        se = d0 * d0 + d1 * d1 + d2 * d2;
-        if (a.image) {
-            a.image[3 * pix] = PK0;
-            a.image[3 * pix + 1] = PK1;
-            a.image[3 * pix + 2] = PK2;
-        }
-        if (a.trans) a.trans[pix] = T;
-    }
-    // per-tile squared error, fixed-order block reduction
-    {
-        double ws = warp_sum(se);
-        if (lane == 0) S.wsum[warp] = ws;
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            double t = S.wsum[0];
-#pragma unroll
-            for (int w = 1; w < kBlock / 32; w++) t += S.wsum[w];
-            a.tile_se[tile] = t;
-        }
-    }
-    const double dr0 = PK0 - ct0, dr1 = PK1 - ct1, dr2 = PK2 - ct2;
-    T = 1.0;
-    P0 = P1 = P2 = 0.0;
-    done = !inside;
-    for (int b = 0; b < batches_done; b++) {
-        const int base = start + b * kBlock;
-        const int cnt = min(kBlock, end - base);
-        __syncthreads();
-        if (threadIdx.x < cnt) {
-            int32_t d = a.perm[base + threadIdx.x];
-            int32_t id = a.dup_id[d];
-            S.rec[threadIdx.x] = a.rec[id];
-            S.dup[threadIdx.x] = d;
-        }
-#pragma unroll
-        for (int w = 0; w < kBlock / 32; w++) S.red[w][threadIdx.x] = make_double2(0.0, 0.0);
-        __syncthreads();
-        if (!__all_sync(0xffffffffu, done)) {
-            for (int e = 0; e < cnt; e++) {
+        se = warp_sum(se);
+        if (lane == 0) a.tile_se[tile] = se;
+        T = 1.0;
+        P0 = P1 = P2 = 0.0;
+        done = !inside;
+        for (int base = start; base < stop; base += 32) {
+            const int cnt = min(32, end - base);
+            const int lim = min(cnt, stop - base);
+            load_chunk<MODE>(a, S, base, cnt, lane);
+            double my_dse = 0.0, my_imp = 0.0;
+            for (int e = 0; e < lim; e++) {
                 const SplatRec &R = S.rec[e];
-                if (R.x1 < wx0 || R.x0 > wx1 || R.y1 < wy0 || R.y0 > wy1) continue;
-                bool contrib = false;
+                const bool live = !done && px >= R.x0 && px <= R.x1 && py >= R.y0 && py <= R.y1;
                 double alpha = 0.0;
-                if (!done && px >= R.x0 && px <= R.x1 && py >= R.y0 && py <= R.y1) {
-                    double dx = pxc - R.mx, dy = pyc - R.my;
-                    double power = -0.5 * (R.ia * dx * dx + R.ic * dy * dy) - R.ib * dx * dy;
-                    if (power >= R.pthr) {
-                        alpha = R.opac * exp(power);
-                        if (alpha > kAlphaCap) alpha = kAlphaCap;
-                        contrib = !(alpha < kAlphaFloor);
-                    }
-                }
+                const bool contrib = sample_alpha(R, px, py, pxc, pyc, live, alpha);
                 double dse = 0.0, timp = 0.0;
                 if (contrib) {
                     // prune_deltas, forward form: a/(1-a) * (P_K - P_i - T c)
-                    double f = alpha / (1.0 - alpha);
-                    double pd0 = f * (PK0 - P0 - T * R.cr);
-                    double pd1 = f * (PK1 - P1 - T * R.cg);
-                    double pd2 = f * (PK2 - P2 - T * R.cb);
+                    const double f = alpha / (1.0 - alpha);
+                    const double pd0 = f * (PK0 - P0 - T * R.cr);
+                    const double pd1 = f * (PK1 - P1 - T * R.cg);
+                    const double pd2 = f * (PK2 - P2 - T * R.cb);
                     dse = pd0 * pd0 + 2.0 * pd0 * dr0;
                     dse = dse + (pd1 * pd1 + 2.0 * pd1 * dr1);
                     dse = dse + (pd2 * pd2 + 2.0 * pd2 * dr2);
-                    double w = T * alpha;
+                    const double w = T * alpha;
                     timp = w;
                     P0 += w * R.cr;
                     P1 += w * R.cg;
@@ -370,27 +337,21 @@ __global__ void __launch_bounds__(kBlock, 2) k_raster(RasterArgs a) {
                     T = T * (1.0 - alpha);
                     done = T < kTTerminate;
                 }
-                if (__any_sync(0xffffffffu, contrib)) {
-                    double s0 = warp_sum(dse);
-                    double s1 = warp_sum(timp);
-                    if (lane == 0) S.red[warp][e] = make_double2(s0, s1);
+                if (__any_sync(FULL, contrib)) {
+                    const double s0 = warp_sum(dse);
+                    const double s1 = warp_sum(timp);
+                    if (lane == e) {
+                        my_dse = s0;
+                        my_imp = s1;
+                    }
                 }
-                if (__all_sync(0xffffffffu, done)) break;
             }
+            if (lane < cnt) a.partial[S.dup[lane]] = make_double2(my_dse, my_imp);
+            written = base + cnt;
         }
-        __syncthreads();
-        if (threadIdx.x < cnt) {
-            double2 acc = S.red[0][threadIdx.x];
-#pragma unroll
-            for (int w = 1; w < kBlock / 32; w++) {
-                acc.x += S.red[w][threadIdx.x].x;
-                acc.y += S.red[w][threadIdx.x].y;
-            }
-            a.partial[S.dup[threadIdx.x]] = acc;
-        }
+        for (int j = written + lane; j < end; j += 32)
+            a.partial[a.perm[j]] = make_double2(0.0, 0.0);
     }
-    for (int j = start + batches_done * kBlock + threadIdx.x; j < end; j += kBlock)
-        a.partial[a.perm[j]] = make_double2(0.0, 0.0);
 }
 
 // Per-splat sum of its (tile, splat) slots, in tile order (deterministic),
@@ -519,7 +480,7 @@ static inline unsigned grid_for(int64_t n, int block) {
     return (unsigned)((n + block - 1) / block);
 }
 
-size_t raster_smem_bytes() { return sizeof(RasterSmem); }
+size_t raster_smem_bytes() { return sizeof(WarpSmem) * kRasterWarps; }
 
 cudaError_t launch_preprocess(const potr_splats &sp, const Cam &cam, int tiles_x, int all_colors,
                               SplatRec *rec, uint64_t *key, int32_t *cnt,
@@ -622,27 +583,32 @@ cudaError_t launch_tile_ranges(int64_t K, const uint32_t *skey, int2 *rng, int n
 }
 
 template <int MODE>
-static cudaError_t launch_raster_t(const RasterArgs &a, int ntiles, cudaStream_t st) {
-    size_t smem = sizeof(RasterSmem);
-    static bool configured = false;
-    if (!configured) {
-        cudaError_t e = cudaFuncSetAttribute(k_raster<MODE>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             (int)smem);
+static cudaError_t launch_raster_t(const RasterArgs &a, cudaStream_t st) {
+    const size_t smem = sizeof(WarpSmem) * kRasterWarps;
+    static int grid = 0;
+    if (grid == 0) {
+        int dev = 0, sms = 0, per_sm = 0;
+        cudaError_t e = cudaGetDevice(&dev);
+        if (e == cudaSuccess) e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        if (e == cudaSuccess)
+            e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_raster<MODE>,
+                                                              32 * kRasterWarps, smem);
         if (e != cudaSuccess) return e;
-        configured = true;
+        grid = sms * (per_sm > 0 ? per_sm : 1);  // persistent: fill every SM exactly
     }
-    k_raster<MODE><<<ntiles, kBlock, smem, st>>>(a);
+    k_raster<MODE><<<grid, 32 * kRasterWarps, smem, st>>>(a);
     return cudaGetLastError();
 }
 
 cudaError_t launch_raster(int mode, const RasterArgs &a, int ntiles, cudaStream_t st) {
     if (ntiles == 0) return cudaSuccess;
+    cudaError_t e = cudaMemsetAsync(a.tile_counter, 0, sizeof(int), st);
+    if (e != cudaSuccess) return e;
     switch (mode) {
-        case kRender: return launch_raster_t<kRender>(a, ntiles, st);
-        case kImportance: return launch_raster_t<kImportance>(a, ntiles, st);
-        case kScore: return launch_raster_t<kScore>(a, ntiles, st);
-        case kRecords: return launch_raster_t<kRecords>(a, ntiles, st);
+        case kRender: return launch_raster_t<kRender>(a, st);
+        case kImportance: return launch_raster_t<kImportance>(a, st);
+        case kScore: return launch_raster_t<kScore>(a, st);
+        case kRecords: return launch_raster_t<kRecords>(a, st);
     }
     return cudaErrorInvalidValue;
 }

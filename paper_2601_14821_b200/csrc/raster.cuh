@@ -13,7 +13,8 @@ struct RasterArgs {
     const int32_t *dup_id;    // duplicate index -> splat id
     const int32_t *dup_rank;  // duplicate index -> depth rank (records mode)
     const int2 *ranges;       // per tile [start, end) into perm
-    int tiles_x;
+    int tiles_x, ntiles;
+    int *tile_counter;        // persistent-warp work counter (zeroed per launch)
     int width, height;
     const double *target;     // (H,W,3), score mode
     double *image;            // (H,W,3) nullable

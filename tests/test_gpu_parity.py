@@ -67,7 +67,7 @@ def test_binning_bit_exact(R, oracle):
     for cam in bc:
         order, offsets, lists = binning.tile_lists(big, cam)
         assert np.array_equal(order, oracle.depth_order(big, cam))
-        off, lst = oracle.tile_lists(big, cam, 16)
+        off, lst = oracle.tile_lists(big, cam)
         assert np.array_equal(offsets, off)
         assert np.array_equal(lists, lst)
 

@@ -38,7 +38,7 @@ def test_depth_order_and_tile_lists_bit_exact(oracle):
     g = golden("small_scene")
     for c in (0, 1):
         assert np.array_equal(oracle.depth_order(splats, cams[c]), g[f"order{c}"])
-        off, lst = oracle.tile_lists(splats, cams[c], 16)
+        off, lst = oracle.tile_lists(splats, cams[c])
         assert np.array_equal(off, g[f"tile_offsets{c}"])
         assert np.array_equal(lst, g[f"tile_splats{c}"])
 
