@@ -11,6 +11,7 @@
 #include <cuda_runtime.h>
 
 #include "../../include/potr_b200.h"
+#include "exp_table.h"
 
 namespace potr {
 
@@ -50,6 +51,29 @@ constexpr int kRasterWarps = 4;  // warps (= independent tile workers) per CTA
 // guarantees o*exp(power) < floor for any exp with < 1e-12 relative error,
 // so the full-precision exp is evaluated only where the floor test could pass.
 constexpr double kPowerMargin = 1e-9;
+
+__constant__ double kExpTable[64][2] = POTR_EXP_TABLE_INIT;
+
+// exp(x) for the Gaussian exponent after the ALPHA_FLOOR prefilter
+// (x in [log(ALPHA_FLOOR), 0]).  Table-driven (2^(j/64) double-double, held
+// in shared memory) with a degree-5 Estrin polynomial: 11 FP64 operations and
+// a 6-deep dependency chain instead of the libdevice exp's ~19 / 17, at
+// < 0.82 ulp (tests/test_exp.py; the reference's glibc exp is ~0.5 ulp).
+__device__ __forceinline__ double exp_neg(double x, const double2 *__restrict__ tab) {
+    const double t = fma(x, POTR_EXP_INV_STEP, POTR_EXP_SHIFT);
+    const double k = t - POTR_EXP_SHIFT;
+    const int ki = __double2loint(t);
+    double r = fma(k, -POTR_EXP_STEP_HI, x);
+    r = fma(k, -POTR_EXP_STEP_LO, r);
+    const double r2 = r * r;
+    const double a = fma(r, POTR_EXP_C3, POTR_EXP_C2);
+    const double b = fma(r, POTR_EXP_C5, POTR_EXP_C4);
+    const double q = fma(r2, b, a);
+    const double p = fma(r2, q, r);
+    const double2 T = tab[ki & 63];
+    const double res = fma(T.x, p, T.y) + T.x;
+    return __hiloint2double(__double2hiint(res) + (ki >> 6) * (1 << 20), __double2loint(res));
+}
 
 // Per-view splat record, 96 bytes, written by the preprocess kernel and read
 // per (tile, splat) pair by the rasterizer.

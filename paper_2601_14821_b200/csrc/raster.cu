@@ -25,6 +25,10 @@
 #include "common.cuh"
 #include "raster.cuh"
 
+#ifndef POTR_RASTER_MIN_BLOCKS
+#define POTR_RASTER_MIN_BLOCKS 6
+#endif
+
 namespace potr {
 
 // ---------------------------------------------------------------------------
@@ -164,12 +168,13 @@ __device__ __forceinline__ double warp_sum(double v) {
 // One sample of rasterizer.py:162-171 for this lane's pixel: returns true when
 // the splat composites here (alpha >= ALPHA_FLOOR), with the capped alpha.
 __device__ __forceinline__ bool sample_alpha(const SplatRec &R, int px, int py, double pxc,
-                                             double pyc, bool live, double &alpha) {
+                                             double pyc, bool live, const double2 *tab,
+                                             double &alpha) {
     if (!live) return false;
     double dx = pxc - R.mx, dy = pyc - R.my;
     double power = -0.5 * (R.ia * dx * dx + R.ic * dy * dy) - R.ib * dx * dy;
     if (power < R.pthr) return false;  // o*exp(power) < ALPHA_FLOOR for certain
-    alpha = R.opac * exp(power);
+    alpha = R.opac * exp_neg(power, tab);
     if (alpha > kAlphaCap) alpha = kAlphaCap;
     return !(alpha < kAlphaFloor);
 }
@@ -197,11 +202,15 @@ __device__ __forceinline__ void load_chunk(const RasterArgs &a, WarpSmem &S, int
 // left; a tile's result depends only on its own list, so the schedule does not
 // affect the output bits.
 template <int MODE>
-__global__ void __launch_bounds__(32 * kRasterWarps, 4) k_raster(RasterArgs a) {
+__global__ void __launch_bounds__(32 * kRasterWarps, POTR_RASTER_MIN_BLOCKS) k_raster(RasterArgs a) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     WarpSmem &S = reinterpret_cast<WarpSmem *>(smem_raw)[threadIdx.x >> 5];
+    double2 *tab = reinterpret_cast<double2 *>(smem_raw + sizeof(WarpSmem) * kRasterWarps);
     const int lane = threadIdx.x & 31;
     const unsigned FULL = 0xffffffffu;
+    for (int i = threadIdx.x; i < 64; i += blockDim.x)
+        tab[i] = make_double2(kExpTable[i][0], kExpTable[i][1]);
+    __syncthreads();
 
     for (;;) {
         int tile = 0;
@@ -231,7 +240,7 @@ __global__ void __launch_bounds__(32 * kRasterWarps, 4) k_raster(RasterArgs a) {
                 const SplatRec &R = S.rec[e];
                 const bool live = !done && px >= R.x0 && px <= R.x1 && py >= R.y0 && py <= R.y1;
                 double alpha = 0.0;
-                const bool contrib = sample_alpha(R, px, py, pxc, pyc, live, alpha);
+                const bool contrib = sample_alpha(R, px, py, pxc, pyc, live, tab, alpha);
                 if (a.counters) {
                     unsigned lv = __ballot_sync(FULL, live);
                     unsigned ct = __ballot_sync(FULL, contrib);
@@ -318,7 +327,7 @@ __global__ void __launch_bounds__(32 * kRasterWarps, 4) k_raster(RasterArgs a) {
                 const SplatRec &R = S.rec[e];
                 const bool live = !done && px >= R.x0 && px <= R.x1 && py >= R.y0 && py <= R.y1;
                 double alpha = 0.0;
-                const bool contrib = sample_alpha(R, px, py, pxc, pyc, live, alpha);
+                const bool contrib = sample_alpha(R, px, py, pxc, pyc, live, tab, alpha);
                 double dse = 0.0, timp = 0.0;
                 if (contrib) {
                     // prune_deltas, forward form: a/(1-a) * (P_K - P_i - T c)
@@ -480,7 +489,7 @@ static inline unsigned grid_for(int64_t n, int block) {
     return (unsigned)((n + block - 1) / block);
 }
 
-size_t raster_smem_bytes() { return sizeof(WarpSmem) * kRasterWarps; }
+size_t raster_smem_bytes() { return sizeof(WarpSmem) * kRasterWarps + 64 * sizeof(double2); }
 
 cudaError_t launch_preprocess(const potr_splats &sp, const Cam &cam, int tiles_x, int all_colors,
                               SplatRec *rec, uint64_t *key, int32_t *cnt,
@@ -584,7 +593,7 @@ cudaError_t launch_tile_ranges(int64_t K, const uint32_t *skey, int2 *rng, int n
 
 template <int MODE>
 static cudaError_t launch_raster_t(const RasterArgs &a, cudaStream_t st) {
-    const size_t smem = sizeof(WarpSmem) * kRasterWarps;
+    const size_t smem = raster_smem_bytes();
     static int grid = 0;
     if (grid == 0) {
         int dev = 0, sms = 0, per_sm = 0;
@@ -596,7 +605,7 @@ static cudaError_t launch_raster_t(const RasterArgs &a, cudaStream_t st) {
         if (e != cudaSuccess) return e;
         grid = sms * (per_sm > 0 ? per_sm : 1);  // persistent: fill every SM exactly
     }
-    k_raster<MODE><<<grid, 32 * kRasterWarps, smem, st>>>(a);
+    k_raster<MODE><<<grid, 32 * kRasterWarps, raster_smem_bytes(), st>>>(a);
     return cudaGetLastError();
 }
 
