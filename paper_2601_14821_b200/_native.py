@@ -111,7 +111,8 @@ _SIGNATURES = {
 
 
 def library_path():
-    return _build.LIB
+    # POTR_B200_LIB: load an alternative in-tree build (A/B experiments)
+    return os.environ.get("POTR_B200_LIB", _build.LIB)
 
 
 def load(build_if_missing=True):
@@ -120,8 +121,9 @@ def load(build_if_missing=True):
     with _lock:
         if _lib is not None:
             return _lib
-        path = _build.LIB
-        if build_if_missing and (not os.path.exists(path) or _build.needs_build()):
+        path = library_path()
+        if path == _build.LIB and build_if_missing and (not os.path.exists(path) or
+                                                        _build.needs_build()):
             _build.build()
         if not os.path.exists(path):
             raise ImportError(f"libpotr_b200.so not found at {path}; run "

@@ -44,7 +44,7 @@ struct potr_ctx {
     bool counting = false;
     DevBuf counters;
     int64_t pairs_total = 0;
-    DevBuf tile_counter;
+    DevBuf tile_counter, sid;
 };
 
 namespace {
@@ -246,6 +246,7 @@ int bin_view(potr_ctx *ctx, const potr_splats &sp, const potr_camera &cam, bool 
     ENSURE(ctx->tskey, sizeof(uint32_t) * K);
     ENSURE(ctx->perm, sizeof(int32_t) * K);
     ENSURE(ctx->dup_id, sizeof(int32_t) * K);
+    ENSURE(ctx->sid, sizeof(int32_t) * K);
     ENSURE(ctx->partial, sizeof(double2) * K);
     if (with_rank) ENSURE(ctx->dup_rank, sizeof(int32_t) * K);
     rc = ensure_iota(ctx, K);
@@ -270,7 +271,9 @@ int bin_view(potr_ctx *ctx, const potr_splats &sp, const potr_camera &cam, bool 
     }
     {
         Stage _st(ctx, POTR_STAGE_TILE_SORT);
-        LAUNCH(1, launch_tile_ranges(K, P<uint32_t>(ctx->tskey), P<int2>(ctx->ranges), g.ntiles,
+        LAUNCH(1, launch_tile_ranges(K, P<uint32_t>(ctx->tskey), P<int32_t>(ctx->perm),
+                                 P<int32_t>(ctx->dup_id), P<int32_t>(ctx->sid),
+                                 P<int2>(ctx->ranges), g.ntiles,
                                      ctx->stream));
         _st.end();
     }
@@ -285,6 +288,7 @@ RasterArgs raster_args(potr_ctx *ctx, const potr_camera &cam) {
     a.rec = P<SplatRec>(ctx->rec);
     a.perm = P<int32_t>(ctx->perm);
     a.dup_id = P<int32_t>(ctx->dup_id);
+    a.sid = P<int32_t>(ctx->sid);
     a.dup_rank = P<int32_t>(ctx->dup_rank);
     a.ranges = P<int2>(ctx->ranges);
     a.tiles_x = g.tiles_x;
@@ -376,6 +380,7 @@ void potr_destroy(potr_ctx *ctx) {
     if (ctx->pinned) cudaFreeHost(ctx->pinned);
     if (ctx->counters.p) cudaFree(ctx->counters.p);
     if (ctx->tile_counter.p) cudaFree(ctx->tile_counter.p);
+    if (ctx->sid.p) cudaFree(ctx->sid.p);
     for (auto &ev : ctx->events) {
         cudaEventDestroy(ev.second.first);
         cudaEventDestroy(ev.second.second);

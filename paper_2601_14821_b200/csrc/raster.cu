@@ -137,9 +137,14 @@ __global__ void k_duplicate(int64_t n, const int32_t *__restrict__ ids,
         }
 }
 
-__global__ void k_tile_ranges(int64_t K, const uint32_t *__restrict__ skey, int2 *__restrict__ rng) {
+// Tile [start, end) ranges of the sorted pairs, plus each sorted pair's splat
+// id (so the rasterizer's chunk fetch is two loads deep, not three).
+__global__ void k_tile_ranges(int64_t K, const uint32_t *__restrict__ skey,
+                              const int32_t *__restrict__ perm, const int32_t *__restrict__ dup_id,
+                              int32_t *__restrict__ sid, int2 *__restrict__ rng) {
     int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (j >= K) return;
+    sid[j] = dup_id[perm[j]];
     uint32_t t = skey[j];
     if (j == 0 || skey[j - 1] != t) rng[t].x = (int)j;
     if (j == K - 1 || skey[j + 1] != t) rng[t].y = (int)(j + 1);
@@ -153,10 +158,16 @@ __global__ void k_iota(int64_t n, int32_t *out) {
 // ---------------------------------------------------------------------------
 // (c)+(d) tile rasterizer and removal-effect pass
 
+// Per-warp staging: two chunk buffers so the next chunk's records stream in
+// with cp.async while the current one is composited.
+constexpr int kChunkBitsCap = 128;  // chunks per tile whose contribution bits are kept
+
 struct WarpSmem {
-    SplatRec rec[32];
-    int32_t dup[32];
-    int32_t rank[32];
+    SplatRec rec[2][32];
+    int32_t dup[2][32];
+    // score mode: bit e of cbits[c] = entry e of chunk c composited somewhere
+    // in pass 1; pass 2 visits only those (others leave T and P unchanged)
+    unsigned cbits[kChunkBitsCap];
 };
 
 __device__ __forceinline__ double warp_sum(double v) {
@@ -165,11 +176,22 @@ __device__ __forceinline__ double warp_sum(double v) {
     return v;
 }
 
+__device__ __forceinline__ void cp_async16(void *smem, const void *gmem) {
+    const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() {
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
+}
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+    asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
+}
+
 // One sample of rasterizer.py:162-171 for this lane's pixel: returns true when
 // the splat composites here (alpha >= ALPHA_FLOOR), with the capped alpha.
-__device__ __forceinline__ bool sample_alpha(const SplatRec &R, int px, int py, double pxc,
-                                             double pyc, bool live, const double2 *tab,
-                                             double &alpha) {
+__device__ __forceinline__ bool sample_alpha(const SplatRec &R, double pxc, double pyc, bool live,
+                                             const double2 *tab, double &alpha) {
     if (!live) return false;
     double dx = pxc - R.mx, dy = pyc - R.my;
     double power = -0.5 * (R.ia * dx * dx + R.ic * dy * dy) - R.ib * dx * dy;
@@ -179,18 +201,35 @@ __device__ __forceinline__ bool sample_alpha(const SplatRec &R, int px, int py, 
     return !(alpha < kAlphaFloor);
 }
 
-// Stage one chunk (<= 32 pairs) of the tile's list into this warp's smem.
+// The lane's slice of a chunk: pair index, splat id (and depth rank).
+struct ChunkIds {
+    int32_t d, id;
+    bool valid;
+};
+
 template <int MODE>
-__device__ __forceinline__ void load_chunk(const RasterArgs &a, WarpSmem &S, int base, int cnt,
-                                           int lane) {
-    __syncwarp();
-    if (lane < cnt) {
-        int32_t d = a.perm[base + lane];
-        S.rec[lane] = a.rec[a.dup_id[d]];
-        S.dup[lane] = d;
-        if (MODE == kRecords) S.rank[lane] = a.dup_rank[d];
+__device__ __forceinline__ ChunkIds fetch_ids(const RasterArgs &a, int cbase, int end, int lane) {
+    ChunkIds c;
+    const int j = cbase + lane;
+    c.valid = j < end;
+    c.d = c.valid ? a.perm[j] : 0;
+    c.id = c.valid ? a.sid[j] : 0;
+    return c;
+}
+
+// Start the async copy of a chunk's records into buffer `b`; always commits a
+// group so wait_group counts stay uniform.
+template <int MODE>
+__device__ __forceinline__ void issue_chunk(const RasterArgs &a, WarpSmem &S, int b,
+                                            const ChunkIds &c, int lane) {
+    if (c.valid) {
+        const char *src = reinterpret_cast<const char *>(a.rec + c.id);
+        char *dst = reinterpret_cast<char *>(&S.rec[b][lane]);
+#pragma unroll
+        for (int q = 0; q < (int)(sizeof(SplatRec) / 16); q++) cp_async16(dst + 16 * q, src + 16 * q);
+        S.dup[b][lane] = c.d;
     }
-    __syncwarp();
+    cp_async_commit();
 }
 
 // MODE: kRender     forward only, writes image/trans
@@ -200,7 +239,8 @@ __device__ __forceinline__ void load_chunk(const RasterArgs &a, WarpSmem &S, int
 //
 // Persistent: each warp pulls 8x4 tiles from an atomic counter until none are
 // left; a tile's result depends only on its own list, so the schedule does not
-// affect the output bits.
+// affect the output bits.  Each pass walks the tile's list in 32-pair chunks
+// through a two-stage cp.async pipeline.
 template <int MODE>
 __global__ void __launch_bounds__(32 * kRasterWarps, POTR_RASTER_MIN_BLOCKS) k_raster(RasterArgs a) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -231,58 +271,75 @@ __global__ void __launch_bounds__(32 * kRasterWarps, POTR_RASTER_MIN_BLOCKS) k_r
         bool done = !inside;
         int stop = start;      // entries [start, stop) were walked
         int written = start;   // importance slots written up to here
-        for (int base = start; base < end && !__all_sync(FULL, done); base += 32) {
-            const int cnt = min(32, end - base);
-            load_chunk<MODE>(a, S, base, cnt, lane);
-            double my_imp = 0.0;
-            int e = 0;
-            while (e < cnt) {
-                const SplatRec &R = S.rec[e];
-                const bool live = !done && px >= R.x0 && px <= R.x1 && py >= R.y0 && py <= R.y1;
-                double alpha = 0.0;
-                const bool contrib = sample_alpha(R, px, py, pxc, pyc, live, tab, alpha);
-                if (a.counters) {
-                    unsigned lv = __ballot_sync(FULL, live);
-                    unsigned ct = __ballot_sync(FULL, contrib);
-                    if (lane == 0) {
-                        atomicAdd(&a.counters[1], (unsigned long long)__popc(lv));
-                        atomicAdd(&a.counters[2], (unsigned long long)__popc(ct));
-                    }
-                }
-                double timp = 0.0;
-                if (contrib) {
-                    if (MODE == kRecords) {
-                        unsigned long long slot = atomicAdd(a.rec_counter, 1ull);
-                        if ((int64_t)slot < a.rec_capacity) {
-                            a.rec_key[slot] =
-                                ((uint64_t)(uint32_t)S.rank[e] << 32) | (uint64_t)(uint32_t)pix;
-                            a.rec_alpha[slot] = alpha;
-                            a.rec_t[slot] = T;
-                            a.rec_p[3 * slot] = P0;
-                            a.rec_p[3 * slot + 1] = P1;
-                            a.rec_p[3 * slot + 2] = P2;
+        if (start < end && !__all_sync(FULL, done)) {
+            issue_chunk<MODE>(a, S, 0, fetch_ids<MODE>(a, start, end, lane), lane);
+            ChunkIds next = fetch_ids<MODE>(a, start + 32, end, lane);
+            int b = 0;
+            for (int base = start; base < end; base += 32, b ^= 1) {
+                issue_chunk<MODE>(a, S, b ^ 1, next, lane);
+                next = fetch_ids<MODE>(a, base + 64, end, lane);
+                cp_async_wait<1>();
+                __syncwarp();
+                const int cnt = min(32, end - base);
+                double my_imp = 0.0;
+                unsigned cbits = 0u;
+                int e = 0;
+                while (e < cnt) {
+                    const SplatRec &R = S.rec[b][e];
+                    const bool live =
+                        !done && px >= R.x0 && px <= R.x1 && py >= R.y0 && py <= R.y1;
+                    double alpha = 0.0;
+                    const bool contrib = sample_alpha(R, pxc, pyc, live, tab, alpha);
+                    if (a.counters) {
+                        unsigned lv = __ballot_sync(FULL, live);
+                        unsigned ct = __ballot_sync(FULL, contrib);
+                        if (lane == 0) {
+                            atomicAdd(&a.counters[1], (unsigned long long)__popc(lv));
+                            atomicAdd(&a.counters[2], (unsigned long long)__popc(ct));
                         }
                     }
-                    const double w = T * alpha;
-                    timp = w;
-                    P0 += w * R.cr;
-                    P1 += w * R.cg;
-                    P2 += w * R.cb;
-                    T = T * (1.0 - alpha);
-                    done = T < kTTerminate;
+                    double timp = 0.0;
+                    if (contrib) {
+                        if (MODE == kRecords) {
+                            unsigned long long slot = atomicAdd(a.rec_counter, 1ull);
+                            if ((int64_t)slot < a.rec_capacity) {
+                                a.rec_key[slot] = ((uint64_t)(uint32_t)a.dup_rank[S.dup[b][e]] << 32) |
+                                                  (uint64_t)(uint32_t)pix;
+                                a.rec_alpha[slot] = alpha;
+                                a.rec_t[slot] = T;
+                                a.rec_p[3 * slot] = P0;
+                                a.rec_p[3 * slot + 1] = P1;
+                                a.rec_p[3 * slot + 2] = P2;
+                            }
+                        }
+                        const double w = T * alpha;
+                        timp = w;
+                        P0 += w * R.cr;
+                        P1 += w * R.cg;
+                        P2 += w * R.cb;
+                        T = T * (1.0 - alpha);
+                        done = T < kTTerminate;
+                    }
+                    if (MODE == kImportance && __any_sync(FULL, contrib)) {
+                        const double s = warp_sum(timp);
+                        if (lane == e) my_imp = s;
+                    }
+                    if (MODE == kScore && __any_sync(FULL, contrib)) cbits |= 1u << e;
+                    e++;
+                    if (__all_sync(FULL, done)) break;
                 }
-                if (MODE == kImportance && __any_sync(FULL, contrib)) {
-                    const double s = warp_sum(timp);
-                    if (lane == e) my_imp = s;
+                stop = base + e;
+                if (MODE == kScore && lane == 0 && ((base - start) >> 5) < kChunkBitsCap)
+                    S.cbits[(base - start) >> 5] = cbits;
+                if (MODE == kImportance) {
+                    if (lane < cnt) a.partial[S.dup[b][lane]] = make_double2(0.0, my_imp);
+                    written = base + cnt;
                 }
-                e++;
+                __syncwarp();
                 if (__all_sync(FULL, done)) break;
             }
-            stop = base + e;
-            if (MODE == kImportance) {
-                if (lane < cnt) a.partial[S.dup[lane]] = make_double2(0.0, my_imp);
-                written = base + cnt;
-            }
+            cp_async_wait<0>();
+            __syncwarp();
         }
 
         if (MODE != kScore) {
@@ -318,45 +375,62 @@ __global__ void __launch_bounds__(32 * kRasterWarps, POTR_RASTER_MIN_BLOCKS) k_r
         T = 1.0;
         P0 = P1 = P2 = 0.0;
         done = !inside;
-        for (int base = start; base < stop; base += 32) {
-            const int cnt = min(32, end - base);
-            const int lim = min(cnt, stop - base);
-            load_chunk<MODE>(a, S, base, cnt, lane);
-            double my_dse = 0.0, my_imp = 0.0;
-            for (int e = 0; e < lim; e++) {
-                const SplatRec &R = S.rec[e];
-                const bool live = !done && px >= R.x0 && px <= R.x1 && py >= R.y0 && py <= R.y1;
-                double alpha = 0.0;
-                const bool contrib = sample_alpha(R, px, py, pxc, pyc, live, tab, alpha);
-                double dse = 0.0, timp = 0.0;
-                if (contrib) {
-                    // prune_deltas, forward form: a/(1-a) * (P_K - P_i - T c)
-                    const double f = alpha / (1.0 - alpha);
-                    const double pd0 = f * (PK0 - P0 - T * R.cr);
-                    const double pd1 = f * (PK1 - P1 - T * R.cg);
-                    const double pd2 = f * (PK2 - P2 - T * R.cb);
-                    dse = pd0 * pd0 + 2.0 * pd0 * dr0;
-                    dse = dse + (pd1 * pd1 + 2.0 * pd1 * dr1);
-                    dse = dse + (pd2 * pd2 + 2.0 * pd2 * dr2);
-                    const double w = T * alpha;
-                    timp = w;
-                    P0 += w * R.cr;
-                    P1 += w * R.cg;
-                    P2 += w * R.cb;
-                    T = T * (1.0 - alpha);
-                    done = T < kTTerminate;
-                }
-                if (__any_sync(FULL, contrib)) {
-                    const double s0 = warp_sum(dse);
-                    const double s1 = warp_sum(timp);
-                    if (lane == e) {
-                        my_dse = s0;
-                        my_imp = s1;
+        if (start < stop) {
+            issue_chunk<MODE>(a, S, 0, fetch_ids<MODE>(a, start, end, lane), lane);
+            ChunkIds next = fetch_ids<MODE>(a, start + 32, end, lane);
+            int b = 0;
+            for (int base = start; base < stop; base += 32, b ^= 1) {
+                issue_chunk<MODE>(a, S, b ^ 1, next, lane);
+                next = fetch_ids<MODE>(a, base + 64, end, lane);
+                cp_async_wait<1>();
+                __syncwarp();
+                const int cnt = min(32, end - base);
+                const int lim = min(cnt, stop - base);
+                const int ci = (base - start) >> 5;
+                unsigned todo = ci < kChunkBitsCap ? S.cbits[ci] : 0xffffffffu;
+                if (lim < 32) todo &= (1u << lim) - 1u;
+                double my_dse = 0.0, my_imp = 0.0;
+                while (todo) {
+                    const int e = __ffs(todo) - 1;
+                    todo &= todo - 1u;
+                    const SplatRec &R = S.rec[b][e];
+                    const bool live =
+                        !done && px >= R.x0 && px <= R.x1 && py >= R.y0 && py <= R.y1;
+                    double alpha = 0.0;
+                    const bool contrib = sample_alpha(R, pxc, pyc, live, tab, alpha);
+                    double dse = 0.0, timp = 0.0;
+                    if (contrib) {
+                        // prune_deltas, forward form: a/(1-a) * (P_K - P_i - T c)
+                        const double f = alpha / (1.0 - alpha);
+                        const double pd0 = f * (PK0 - P0 - T * R.cr);
+                        const double pd1 = f * (PK1 - P1 - T * R.cg);
+                        const double pd2 = f * (PK2 - P2 - T * R.cb);
+                        dse = pd0 * pd0 + 2.0 * pd0 * dr0;
+                        dse = dse + (pd1 * pd1 + 2.0 * pd1 * dr1);
+                        dse = dse + (pd2 * pd2 + 2.0 * pd2 * dr2);
+                        const double w = T * alpha;
+                        timp = w;
+                        P0 += w * R.cr;
+                        P1 += w * R.cg;
+                        P2 += w * R.cb;
+                        T = T * (1.0 - alpha);
+                        done = T < kTTerminate;
+                    }
+                    if (__any_sync(FULL, contrib)) {
+                        const double s0 = warp_sum(dse);
+                        const double s1 = warp_sum(timp);
+                        if (lane == e) {
+                            my_dse = s0;
+                            my_imp = s1;
+                        }
                     }
                 }
+                if (lane < cnt) a.partial[S.dup[b][lane]] = make_double2(my_dse, my_imp);
+                written = base + cnt;
+                __syncwarp();
             }
-            if (lane < cnt) a.partial[S.dup[lane]] = make_double2(my_dse, my_imp);
-            written = base + cnt;
+            cp_async_wait<0>();
+            __syncwarp();
         }
         for (int j = written + lane; j < end; j += 32)
             a.partial[a.perm[j]] = make_double2(0.0, 0.0);
@@ -583,11 +657,12 @@ cudaError_t records_sort(void *temp, size_t temp_bytes, const uint64_t *key, uin
                                            st);
 }
 
-cudaError_t launch_tile_ranges(int64_t K, const uint32_t *skey, int2 *rng, int ntiles,
+cudaError_t launch_tile_ranges(int64_t K, const uint32_t *skey, const int32_t *perm,
+                               const int32_t *dup_id, int32_t *sid, int2 *rng, int ntiles,
                                cudaStream_t st) {
     cudaError_t e = cudaMemsetAsync(rng, 0, sizeof(int2) * (size_t)ntiles, st);
     if (e != cudaSuccess || K == 0) return e;
-    k_tile_ranges<<<grid_for(K, 256), 256, 0, st>>>(K, skey, rng);
+    k_tile_ranges<<<grid_for(K, 256), 256, 0, st>>>(K, skey, perm, dup_id, sid, rng);
     return cudaGetLastError();
 }
 

@@ -11,6 +11,7 @@ struct RasterArgs {
     const SplatRec *rec;
     const int32_t *perm;      // sorted pair -> duplicate index
     const int32_t *dup_id;    // duplicate index -> splat id
+    const int32_t *sid;       // sorted pair -> splat id
     const int32_t *dup_rank;  // duplicate index -> depth rank (records mode)
     const int2 *ranges;       // per tile [start, end) into perm
     int tiles_x, ntiles;
@@ -54,7 +55,8 @@ cudaError_t tile_sort(void *temp, size_t temp_bytes, const uint32_t *tkey, uint3
 cudaError_t records_sort_temp(int64_t m, size_t *bytes);
 cudaError_t records_sort(void *temp, size_t temp_bytes, const uint64_t *key, uint64_t *skey,
                          const int32_t *iota, int32_t *sidx, int64_t m, cudaStream_t st);
-cudaError_t launch_tile_ranges(int64_t K, const uint32_t *skey, int2 *rng, int ntiles,
+cudaError_t launch_tile_ranges(int64_t K, const uint32_t *skey, const int32_t *perm,
+                               const int32_t *dup_id, int32_t *sid, int2 *rng, int ntiles,
                                cudaStream_t st);
 cudaError_t launch_raster(int mode, const RasterArgs &a, int ntiles, cudaStream_t st);
 cudaError_t launch_splat_reduce(int64_t n, const int32_t *ids, const int64_t *offs,
