@@ -158,16 +158,21 @@ __global__ void k_iota(int64_t n, int32_t *out) {
 // ---------------------------------------------------------------------------
 // (c)+(d) tile rasterizer and removal-effect pass
 
-// Per-warp staging: two chunk buffers so the next chunk's records stream in
-// with cp.async while the current one is composited.
-constexpr int kChunkBitsCap = 128;  // chunks per tile whose contribution bits are kept
+// Per-warp staging.  A chunk is 32 consecutive pairs of the tile's list; its
+// records are held field-major (six 16-byte fields x 32 entries) so lanes that
+// read different entries hit different banks.  Two buffers: the next chunk
+// streams in with cp.async while the current one is composited.
+constexpr int kMaskChunks = 16;  // chunks per tile whose per-lane contribution masks are kept
+
+struct ChunkBuf {
+    double2 f[6][32];  // (mx,my) (ia,ib) (ic,opac) (cr,cg) (cb,pthr) bbox(int4)
+    int32_t dup[32];
+};
 
 struct WarpSmem {
-    SplatRec rec[2][32];
-    int32_t dup[2][32];
-    // score mode: bit e of cbits[c] = entry e of chunk c composited somewhere
-    // in pass 1; pass 2 visits only those (others leave T and P unchanged)
-    unsigned cbits[kChunkBitsCap];
+    ChunkBuf buf[2];
+    unsigned cmask[kMaskChunks][32];  // pass-1 contribution mask of each lane, per chunk
+    double2 acc[32];                  // per-entry (dSE, T*alpha) sums of the current chunk
 };
 
 __device__ __forceinline__ double warp_sum(double v) {
@@ -188,26 +193,12 @@ __device__ __forceinline__ void cp_async_wait() {
     asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
 }
 
-// One sample of rasterizer.py:162-171 for this lane's pixel: returns true when
-// the splat composites here (alpha >= ALPHA_FLOOR), with the capped alpha.
-__device__ __forceinline__ bool sample_alpha(const SplatRec &R, double pxc, double pyc, bool live,
-                                             const double2 *tab, double &alpha) {
-    if (!live) return false;
-    double dx = pxc - R.mx, dy = pyc - R.my;
-    double power = -0.5 * (R.ia * dx * dx + R.ic * dy * dy) - R.ib * dx * dy;
-    if (power < R.pthr) return false;  // o*exp(power) < ALPHA_FLOOR for certain
-    alpha = R.opac * exp_neg(power, tab);
-    if (alpha > kAlphaCap) alpha = kAlphaCap;
-    return !(alpha < kAlphaFloor);
-}
-
-// The lane's slice of a chunk: pair index, splat id (and depth rank).
+// The lane's slice of a chunk: pair index and splat id.
 struct ChunkIds {
     int32_t d, id;
     bool valid;
 };
 
-template <int MODE>
 __device__ __forceinline__ ChunkIds fetch_ids(const RasterArgs &a, int cbase, int end, int lane) {
     ChunkIds c;
     const int j = cbase + lane;
@@ -219,28 +210,85 @@ __device__ __forceinline__ ChunkIds fetch_ids(const RasterArgs &a, int cbase, in
 
 // Start the async copy of a chunk's records into buffer `b`; always commits a
 // group so wait_group counts stay uniform.
-template <int MODE>
-__device__ __forceinline__ void issue_chunk(const RasterArgs &a, WarpSmem &S, int b,
-                                            const ChunkIds &c, int lane) {
+__device__ __forceinline__ void issue_chunk(const RasterArgs &a, ChunkBuf &B, const ChunkIds &c,
+                                            int lane) {
     if (c.valid) {
         const char *src = reinterpret_cast<const char *>(a.rec + c.id);
-        char *dst = reinterpret_cast<char *>(&S.rec[b][lane]);
 #pragma unroll
-        for (int q = 0; q < (int)(sizeof(SplatRec) / 16); q++) cp_async16(dst + 16 * q, src + 16 * q);
-        S.dup[b][lane] = c.d;
+        for (int q = 0; q < 6; q++) cp_async16(&B.f[q][lane], src + 16 * q);
+        B.dup[lane] = c.d;
     }
     cp_async_commit();
 }
 
-// MODE: kRender     forward only, writes image/trans
-//       kImportance forward with per-pair T*alpha slots (no targets)
-//       kScore      forward, then the removal-effect walk with targets
-//       kRecords    forward, appending every contribution record
+__device__ __forceinline__ int4 bbox_of(const ChunkBuf &B, int e) {
+    return *reinterpret_cast<const int4 *>(&B.f[5][e]);
+}
+
+// Entries of this chunk whose clipped bbox (rasterizer.py:135-148) contains
+// the lane's pixel.
+__device__ __forceinline__ unsigned live_mask(const ChunkBuf &B, int cnt, int px, int py) {
+    unsigned m = 0u;
+    for (int e = 0; e < cnt; e++) {
+        const int4 bb = bbox_of(B, e);  // same address in every lane: broadcast
+        const bool in = px >= bb.x && px <= bb.y && py >= bb.z && py <= bb.w;
+        m |= (unsigned)in << e;
+    }
+    return m;
+}
+
+// rasterizer.py:165-171 for entry e at this lane's pixel: the Gaussian exponent
+// with the exp prefilter, then alpha capped at ALPHA_CAP.  Returns false when
+// alpha < ALPHA_FLOOR (the sample is skipped and T is untouched).
+__device__ __forceinline__ bool eval_alpha(const ChunkBuf &B, int e, double pxc, double pyc,
+                                           const double2 *tab, double &alpha) {
+    const double2 m = B.f[0][e], ab = B.f[1][e], co = B.f[2][e];
+    const double pthr = B.f[4][e].y;
+    const double dx = pxc - m.x, dy = pyc - m.y;
+    const double power = -0.5 * (ab.x * dx * dx + co.x * dy * dy) - ab.y * dx * dy;
+    if (power < pthr) return false;  // o*exp(power) < ALPHA_FLOOR for certain
+    alpha = co.y * exp_neg(power, tab);
+    if (alpha > kAlphaCap) alpha = kAlphaCap;
+    return !(alpha < kAlphaFloor);
+}
+
+// Deterministic segmented sum over the lanes that hold the same key: pointer
+// jumping along each group's members in lane order leaves the group total in
+// its lowest lane.  The add order depends only on group membership.
+__device__ __forceinline__ bool group_sum(int key, double &v0, double &v1) {
+    const unsigned FULL = 0xffffffffu;
+    const int lane = threadIdx.x & 31;
+    const unsigned peers = __match_any_sync(FULL, key);
+    const unsigned above = peers & ~((2u << lane) - 1u);
+    int nxt = above ? __ffs(above) - 1 : -1;
+    const int gmax = __reduce_max_sync(FULL, (unsigned)__popc(peers));
+    for (int span = 1; span < gmax; span <<= 1) {
+        const int src = nxt >= 0 ? nxt : lane;
+        const double t0 = __shfl_sync(FULL, v0, src);
+        const double t1 = __shfl_sync(FULL, v1, src);
+        const int n2 = __shfl_sync(FULL, nxt, src);
+        if (nxt >= 0) {
+            v0 += t0;
+            v1 += t1;
+            nxt = n2;
+        }
+    }
+    return (peers & ((1u << lane) - 1u)) == 0u;  // this lane leads its group
+}
+
+// MODE: kRender     pass 1 only, writes image/trans
+//       kImportance pass 1, then the replay accumulating T*alpha slots
+//       kScore      pass 1, then the replay with the removal effect (targets)
+//       kRecords    pass 1, appending every contribution record
 //
-// Persistent: each warp pulls 8x4 tiles from an atomic counter until none are
-// left; a tile's result depends only on its own list, so the schedule does not
-// affect the output bits.  Each pass walks the tile's list in 32-pair chunks
-// through a two-stage cp.async pipeline.
+// Persistent warps pull 8x4-pixel tiles from an atomic counter; a tile's
+// result depends only on its own list, so the schedule does not change bits.
+// Pass 1 is a per-lane walk: each lane visits only the chunk entries whose
+// bbox holds its pixel, in list (depth) order, compositing exactly as the
+// reference (rasterizer.py:159-201), and records which entries it composited.
+// The replay visits exactly those (lane, entry) samples again, evaluates the
+// closed-form removal delta (forward form, :232-243), dSE (:333) and T*alpha
+// (:228), and sums them per (tile, splat) with group_sum.
 template <int MODE>
 __global__ void __launch_bounds__(32 * kRasterWarps, POTR_RASTER_MIN_BLOCKS) k_raster(RasterArgs a) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -266,166 +314,165 @@ __global__ void __launch_bounds__(32 * kRasterWarps, POTR_RASTER_MIN_BLOCKS) k_r
         const int start = range.x, end = range.y > range.x ? range.y : range.x;
         const double pxc = (double)px + 0.5, pyc = (double)py + 0.5;
 
-        // ---- pass 1: front-to-back compositing (rasterizer.py:159-201) ----
+        // ---- pass 1: per-lane front-to-back compositing -------------------
         double T = 1.0, P0 = 0.0, P1 = 0.0, P2 = 0.0;
         bool done = !inside;
-        int stop = start;      // entries [start, stop) were walked
-        int written = start;   // importance slots written up to here
+        int stop = start;  // chunks [start, stop) were walked
         if (start < end && !__all_sync(FULL, done)) {
-            issue_chunk<MODE>(a, S, 0, fetch_ids<MODE>(a, start, end, lane), lane);
-            ChunkIds next = fetch_ids<MODE>(a, start + 32, end, lane);
+            issue_chunk(a, S.buf[0], fetch_ids(a, start, end, lane), lane);
+            ChunkIds next = fetch_ids(a, start + 32, end, lane);
             int b = 0;
             for (int base = start; base < end; base += 32, b ^= 1) {
-                issue_chunk<MODE>(a, S, b ^ 1, next, lane);
-                next = fetch_ids<MODE>(a, base + 64, end, lane);
+                issue_chunk(a, S.buf[b ^ 1], next, lane);
+                next = fetch_ids(a, base + 64, end, lane);
                 cp_async_wait<1>();
                 __syncwarp();
+                const ChunkBuf &B = S.buf[b];
                 const int cnt = min(32, end - base);
-                double my_imp = 0.0;
-                unsigned cbits = 0u;
-                int e = 0;
-                while (e < cnt) {
-                    const SplatRec &R = S.rec[b][e];
-                    const bool live =
-                        !done && px >= R.x0 && px <= R.x1 && py >= R.y0 && py <= R.y1;
-                    double alpha = 0.0;
-                    const bool contrib = sample_alpha(R, pxc, pyc, live, tab, alpha);
-                    if (a.counters) {
-                        unsigned lv = __ballot_sync(FULL, live);
-                        unsigned ct = __ballot_sync(FULL, contrib);
-                        if (lane == 0) {
-                            atomicAdd(&a.counters[1], (unsigned long long)__popc(lv));
-                            atomicAdd(&a.counters[2], (unsigned long long)__popc(ct));
+                unsigned m = done ? 0u : live_mask(B, cnt, px, py);
+                unsigned cm = 0u;
+                unsigned n_live = 0u;
+                while (m) {
+                    const int e = __ffs(m) - 1;
+                    m &= m - 1u;
+                    n_live++;
+                    double alpha;
+                    if (!eval_alpha(B, e, pxc, pyc, tab, alpha)) continue;
+                    cm |= 1u << e;
+                    if (MODE == kRecords) {
+                        unsigned long long slot = atomicAdd(a.rec_counter, 1ull);
+                        if ((int64_t)slot < a.rec_capacity) {
+                            a.rec_key[slot] =
+                                ((uint64_t)(uint32_t)a.dup_rank[B.dup[e]] << 32) | (uint64_t)(uint32_t)pix;
+                            a.rec_alpha[slot] = alpha;
+                            a.rec_t[slot] = T;
+                            a.rec_p[3 * slot] = P0;
+                            a.rec_p[3 * slot + 1] = P1;
+                            a.rec_p[3 * slot + 2] = P2;
                         }
                     }
-                    double timp = 0.0;
-                    if (contrib) {
-                        if (MODE == kRecords) {
-                            unsigned long long slot = atomicAdd(a.rec_counter, 1ull);
-                            if ((int64_t)slot < a.rec_capacity) {
-                                a.rec_key[slot] = ((uint64_t)(uint32_t)a.dup_rank[S.dup[b][e]] << 32) |
-                                                  (uint64_t)(uint32_t)pix;
-                                a.rec_alpha[slot] = alpha;
-                                a.rec_t[slot] = T;
-                                a.rec_p[3 * slot] = P0;
-                                a.rec_p[3 * slot + 1] = P1;
-                                a.rec_p[3 * slot + 2] = P2;
-                            }
-                        }
-                        const double w = T * alpha;
-                        timp = w;
-                        P0 += w * R.cr;
-                        P1 += w * R.cg;
-                        P2 += w * R.cb;
-                        T = T * (1.0 - alpha);
-                        done = T < kTTerminate;
+                    const double2 c01 = B.f[3][e];
+                    const double c2 = B.f[4][e].x;
+                    const double w = T * alpha;
+                    P0 += w * c01.x;
+                    P1 += w * c01.y;
+                    P2 += w * c2;
+                    T = T * (1.0 - alpha);
+                    if (T < kTTerminate) {  // every later sample is skipped (:162-164)
+                        done = true;
+                        m = 0u;
                     }
-                    if (MODE == kImportance && __any_sync(FULL, contrib)) {
-                        const double s = warp_sum(timp);
-                        if (lane == e) my_imp = s;
+                }
+                if (a.counters) {
+                    const unsigned lv = __reduce_add_sync(FULL, n_live);
+                    const unsigned ct = __reduce_add_sync(FULL, (unsigned)__popc(cm));
+                    if (lane == 0) {
+                        atomicAdd(&a.counters[1], (unsigned long long)lv);
+                        atomicAdd(&a.counters[2], (unsigned long long)ct);
                     }
-                    if (MODE == kScore && __any_sync(FULL, contrib)) cbits |= 1u << e;
-                    e++;
-                    if (__all_sync(FULL, done)) break;
                 }
-                stop = base + e;
-                if (MODE == kScore && lane == 0 && ((base - start) >> 5) < kChunkBitsCap)
-                    S.cbits[(base - start) >> 5] = cbits;
-                if (MODE == kImportance) {
-                    if (lane < cnt) a.partial[S.dup[b][lane]] = make_double2(0.0, my_imp);
-                    written = base + cnt;
-                }
+                const int ci = (base - start) >> 5;
+                if (ci < kMaskChunks) S.cmask[ci][lane] = cm;
+                stop = base + 32;
                 __syncwarp();
                 if (__all_sync(FULL, done)) break;
             }
             cp_async_wait<0>();
             __syncwarp();
+            if (stop > end) stop = end;
         }
 
-        if (MODE != kScore) {
+        if (MODE == kRender || MODE == kRecords) {
             if (inside && a.image) {
                 a.image[3 * pix] = P0;
                 a.image[3 * pix + 1] = P1;
                 a.image[3 * pix + 2] = P2;
             }
             if (inside && a.trans) a.trans[pix] = T;
-            if (MODE == kImportance)  // pairs after the early-out contribute nothing
-                for (int j = written + lane; j < end; j += 32)
-                    a.partial[a.perm[j]] = make_double2(0.0, 0.0);
             continue;
         }
 
-        // ---- pass 2: removal effect (rasterizer.py:232-243, :322-336) -----
+        // ---- replay: removal effect / importance (rasterizer.py:226-243, :322-336)
         const double PK0 = P0, PK1 = P1, PK2 = P2;
-        double dr0 = 0.0, dr1 = 0.0, dr2 = 0.0, se = 0.0;
-        if (inside) {
-            dr0 = PK0 - a.target[3 * pix];
-            dr1 = PK1 - a.target[3 * pix + 1];
-            dr2 = PK2 - a.target[3 * pix + 2];
-            se = dr0 * dr0 + dr1 * dr1 + dr2 * dr2;
-            if (a.image) {
-                a.image[3 * pix] = PK0;
-                a.image[3 * pix + 1] = PK1;
-                a.image[3 * pix + 2] = PK2;
+        double dr0 = 0.0, dr1 = 0.0, dr2 = 0.0;
+        if (MODE == kScore) {
+            double se = 0.0;
+            if (inside) {
+                dr0 = PK0 - a.target[3 * pix];
+                dr1 = PK1 - a.target[3 * pix + 1];
+                dr2 = PK2 - a.target[3 * pix + 2];
+                se = dr0 * dr0 + dr1 * dr1 + dr2 * dr2;
             }
-            if (a.trans) a.trans[pix] = T;
+            se = warp_sum(se);
+            if (lane == 0) a.tile_se[tile] = se;
         }
-        se = warp_sum(se);
-        if (lane == 0) a.tile_se[tile] = se;
+        if (inside && a.image) {
+            a.image[3 * pix] = PK0;
+            a.image[3 * pix + 1] = PK1;
+            a.image[3 * pix + 2] = PK2;
+        }
+        if (inside && a.trans) a.trans[pix] = T;
         T = 1.0;
         P0 = P1 = P2 = 0.0;
         done = !inside;
+        int written = start;
         if (start < stop) {
-            issue_chunk<MODE>(a, S, 0, fetch_ids<MODE>(a, start, end, lane), lane);
-            ChunkIds next = fetch_ids<MODE>(a, start + 32, end, lane);
+            issue_chunk(a, S.buf[0], fetch_ids(a, start, end, lane), lane);
+            ChunkIds next = fetch_ids(a, start + 32, end, lane);
             int b = 0;
             for (int base = start; base < stop; base += 32, b ^= 1) {
-                issue_chunk<MODE>(a, S, b ^ 1, next, lane);
-                next = fetch_ids<MODE>(a, base + 64, end, lane);
+                issue_chunk(a, S.buf[b ^ 1], next, lane);
+                next = fetch_ids(a, base + 64, end, lane);
+                S.acc[lane] = make_double2(0.0, 0.0);
                 cp_async_wait<1>();
                 __syncwarp();
+                const ChunkBuf &B = S.buf[b];
                 const int cnt = min(32, end - base);
-                const int lim = min(cnt, stop - base);
                 const int ci = (base - start) >> 5;
-                unsigned todo = ci < kChunkBitsCap ? S.cbits[ci] : 0xffffffffu;
-                if (lim < 32) todo &= (1u << lim) - 1u;
-                double my_dse = 0.0, my_imp = 0.0;
-                while (todo) {
-                    const int e = __ffs(todo) - 1;
-                    todo &= todo - 1u;
-                    const SplatRec &R = S.rec[b][e];
-                    const bool live =
-                        !done && px >= R.x0 && px <= R.x1 && py >= R.y0 && py <= R.y1;
-                    double alpha = 0.0;
-                    const bool contrib = sample_alpha(R, pxc, pyc, live, tab, alpha);
+                // beyond the kept masks the samples are re-decided exactly as in pass 1
+                const bool known = ci < kMaskChunks;
+                unsigned m = known ? S.cmask[ci][lane] : (done ? 0u : live_mask(B, cnt, px, py));
+                while (__any_sync(FULL, m != 0u)) {
+                    int key = 32 + lane;
                     double dse = 0.0, timp = 0.0;
-                    if (contrib) {
-                        // prune_deltas, forward form: a/(1-a) * (P_K - P_i - T c)
-                        const double f = alpha / (1.0 - alpha);
-                        const double pd0 = f * (PK0 - P0 - T * R.cr);
-                        const double pd1 = f * (PK1 - P1 - T * R.cg);
-                        const double pd2 = f * (PK2 - P2 - T * R.cb);
-                        dse = pd0 * pd0 + 2.0 * pd0 * dr0;
-                        dse = dse + (pd1 * pd1 + 2.0 * pd1 * dr1);
-                        dse = dse + (pd2 * pd2 + 2.0 * pd2 * dr2);
-                        const double w = T * alpha;
-                        timp = w;
-                        P0 += w * R.cr;
-                        P1 += w * R.cg;
-                        P2 += w * R.cb;
-                        T = T * (1.0 - alpha);
-                        done = T < kTTerminate;
-                    }
-                    if (__any_sync(FULL, contrib)) {
-                        const double s0 = warp_sum(dse);
-                        const double s1 = warp_sum(timp);
-                        if (lane == e) {
-                            my_dse = s0;
-                            my_imp = s1;
+                    if (m) {
+                        const int e = __ffs(m) - 1;
+                        m &= m - 1u;
+                        double alpha = 0.0;
+                        const bool ok = eval_alpha(B, e, pxc, pyc, tab, alpha);
+                        if (ok) {
+                            key = e;
+                            const double2 c01 = B.f[3][e];
+                            const double c2 = B.f[4][e].x;
+                            if (MODE == kScore) {
+                                // prune_deltas, forward form: a/(1-a) * (P_K - P_i - T c)
+                                const double f = alpha / (1.0 - alpha);
+                                const double pd0 = f * (PK0 - P0 - T * c01.x);
+                                const double pd1 = f * (PK1 - P1 - T * c01.y);
+                                const double pd2 = f * (PK2 - P2 - T * c2);
+                                dse = pd0 * pd0 + 2.0 * pd0 * dr0;
+                                dse = dse + (pd1 * pd1 + 2.0 * pd1 * dr1);
+                                dse = dse + (pd2 * pd2 + 2.0 * pd2 * dr2);
+                            }
+                            const double w = T * alpha;
+                            timp = w;
+                            P0 += w * c01.x;
+                            P1 += w * c01.y;
+                            P2 += w * c2;
+                            T = T * (1.0 - alpha);
+                            if (T < kTTerminate) {
+                                done = true;
+                                m = 0u;
+                            }
                         }
                     }
+                    if (group_sum(key, dse, timp) && key < 32) {
+                        S.acc[key].x += dse;
+                        S.acc[key].y += timp;
+                    }
                 }
-                if (lane < cnt) a.partial[S.dup[b][lane]] = make_double2(my_dse, my_imp);
+                __syncwarp();
+                if (lane < cnt) a.partial[B.dup[lane]] = S.acc[lane];
                 written = base + cnt;
                 __syncwarp();
             }
