@@ -258,7 +258,21 @@ __device__ __forceinline__ bool eval_alpha(const ChunkBuf &B, int e, double pxc,
 __device__ __forceinline__ bool group_sum(int key, double &v0, double &v1) {
     const unsigned FULL = 0xffffffffu;
     const int lane = threadIdx.x & 31;
+#ifndef POTR_BALLOT_GROUPS
     const unsigned peers = __match_any_sync(FULL, key);
+#else
+    // keys are entry indices 0..31 (valid) or 32+lane (singletons): five
+    // ballots on the key bits give every valid lane its group
+    const bool grouped = key < 32;
+    unsigned peers = __ballot_sync(FULL, grouped);
+#pragma unroll
+    for (int bit = 0; bit < 5; bit++) {
+        const bool kb = (key >> bit) & 1;
+        const unsigned x = __ballot_sync(FULL, kb);
+        peers &= kb ? x : ~x;
+    }
+    if (!grouped) peers = 1u << lane;
+#endif
     const unsigned above = peers & ~((2u << lane) - 1u);
     int nxt = above ? __ffs(above) - 1 : -1;
     const int gmax = __reduce_max_sync(FULL, (unsigned)__popc(peers));
