@@ -1,6 +1,7 @@
 // capi.cu -- the extern "C" boundary (include/potr_b200.h): context, grow-only
 // device workspace, and the per-view orchestration of kernels (a)-(e).
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -44,7 +45,8 @@ struct potr_ctx {
     bool counting = false;
     DevBuf counters;
     int64_t pairs_total = 0;
-    DevBuf tile_counter, sid;
+    DevBuf tile_counter, sid, ci_v, dm_v;
+    int view_batch = kMaxViewBatch;
 };
 
 namespace {
@@ -192,55 +194,64 @@ ViewGeom geom(const potr_camera &c) {
     return g;
 }
 
-// (a)+(b): preprocess, depth sort, duplicate, tile sort, tile ranges.
-// On return *K_out holds the number of (tile, splat) pairs.
-int bin_view(potr_ctx *ctx, const potr_splats &sp, const potr_camera &cam, bool all_colors,
-             bool with_rank, int64_t *K_out) {
+// (a)+(b) for a batch of `nview` views of equal size: preprocess (splat
+// attributes read once per batch), per-view stable depth sorts, one scan over
+// all (view, rank) counts, one duplicate, one stable tile sort over batch-global
+// tile keys, tile ranges.  On return *K_out holds the number of pairs.
+int bin_batch(potr_ctx *ctx, const potr_splats &sp, const potr_camera *cams, int nview,
+              bool all_colors, bool with_rank, int64_t *K_out) {
     const int64_t n = sp.n;
-    ViewGeom g = geom(cam);
-    Cam dc = to_cam(cam);
-    ENSURE(ctx->rec, sizeof(SplatRec) * n);
-    ENSURE(ctx->key, sizeof(uint64_t) * n);
-    ENSURE(ctx->skey, sizeof(uint64_t) * n);
-    ENSURE(ctx->sids, sizeof(int32_t) * n);
-    ENSURE(ctx->cnt, sizeof(int32_t) * n);
-    ENSURE(ctx->cnt_sorted, sizeof(int64_t) * n);
-    ENSURE(ctx->offs, sizeof(int64_t) * (n + 1));
-    ENSURE(ctx->ranges, sizeof(int2) * g.ntiles);
-    ENSURE(ctx->tile_se, sizeof(double) * g.ntiles);
+    const int64_t total = n * nview;
+    ViewGeom g = geom(cams[0]);
+    const int ntiles_b = g.ntiles * nview;
+    CamBatch cb;
+    std::memset(&cb, 0, sizeof(cb));
+    for (int v = 0; v < nview; v++) cb.cam[v] = to_cam(cams[v]);
+    ENSURE(ctx->rec, sizeof(SplatRec) * total);
+    ENSURE(ctx->key, sizeof(uint64_t) * total);
+    ENSURE(ctx->skey, sizeof(uint64_t) * total);
+    ENSURE(ctx->sids, sizeof(int32_t) * total);
+    ENSURE(ctx->cnt, sizeof(int32_t) * total);
+    ENSURE(ctx->cnt_sorted, sizeof(int64_t) * total);
+    ENSURE(ctx->offs, sizeof(int64_t) * (total + 1));
+    ENSURE(ctx->ranges, sizeof(int2) * ntiles_b);
+    ENSURE(ctx->tile_se, sizeof(double) * ntiles_b);
     ENSURE(ctx->tile_counter, sizeof(int));
     int rc = ensure_iota(ctx, n);
     if (rc) return rc;
     size_t t1 = 0, t2 = 0;
     CK(depth_sort_temp(n, &t1));
-    CK(scan_temp(n, &t2));
+    CK(scan_temp(total, &t2));
     ENSURE(ctx->temp, t1 > t2 ? t1 : t2);
 
     {
         Stage _st(ctx, POTR_STAGE_PREPROCESS);
-        LAUNCH(1, launch_preprocess(sp, dc, g.tiles_x, all_colors ? 1 : 0, P<SplatRec>(ctx->rec),
-                                    P<uint64_t>(ctx->key), P<int32_t>(ctx->cnt),
-                                    counters(ctx), ctx->stream));
+        LAUNCH(1, launch_preprocess(sp, cb, nview, g.tiles_x, all_colors ? 1 : 0,
+                                    P<SplatRec>(ctx->rec), P<uint64_t>(ctx->key),
+                                    P<int32_t>(ctx->cnt), counters(ctx), ctx->stream));
         _st.end();
     }
     {
         Stage _st(ctx, POTR_STAGE_DEPTH_SORT);
-        CK(depth_sort(ctx->temp.p, ctx->temp.cap, P<uint64_t>(ctx->key), P<uint64_t>(ctx->skey),
-                      P<int32_t>(ctx->iota), P<int32_t>(ctx->sids), n, ctx->stream));
+        for (int v = 0; v < nview; v++)
+            CK(depth_sort(ctx->temp.p, ctx->temp.cap, P<uint64_t>(ctx->key) + v * n,
+                          P<uint64_t>(ctx->skey) + v * n, P<int32_t>(ctx->iota),
+                          P<int32_t>(ctx->sids) + v * n, n, ctx->stream));
         _st.end();
     }
     {
         Stage _st(ctx, POTR_STAGE_SCAN);
-        LAUNCH(1, scan_counts(ctx->temp.p, ctx->temp.cap, P<int32_t>(ctx->sids), P<int32_t>(ctx->cnt),
-                              P<int64_t>(ctx->cnt_sorted), P<int64_t>(ctx->offs), n, ctx->stream));
+        LAUNCH(1, scan_counts(ctx->temp.p, ctx->temp.cap, P<int32_t>(ctx->sids),
+                              P<int32_t>(ctx->cnt), P<int64_t>(ctx->cnt_sorted),
+                              P<int64_t>(ctx->offs), total, n, ctx->stream));
         _st.end();
     }
-    CK(cudaMemcpyAsync(ctx->pinned, P<int64_t>(ctx->offs) + n, sizeof(int64_t),
+    CK(cudaMemcpyAsync(ctx->pinned, P<int64_t>(ctx->offs) + total, sizeof(int64_t),
                        cudaMemcpyDeviceToHost, ctx->stream));
     CK(cudaStreamSynchronize(ctx->stream));
     const int64_t K = ctx->pinned[0];
     ctx->pairs_total += K;
-    if (K > 0x7fffff00LL) return fail(ctx, POTR_E_ARG, "more than 2^31 tile pairs in one view");
+    if (K > 0x7fffff00LL) return fail(ctx, POTR_E_ARG, "more than 2^31 tile pairs in one batch");
 
     ENSURE(ctx->tkey, sizeof(uint32_t) * K);
     ENSURE(ctx->tskey, sizeof(uint32_t) * K);
@@ -252,36 +263,31 @@ int bin_view(potr_ctx *ctx, const potr_splats &sp, const potr_camera &cam, bool 
     rc = ensure_iota(ctx, K);
     if (rc) return rc;
     size_t t3 = 0;
-    CK(tile_sort_temp(K, g.ntiles, &t3));
+    CK(tile_sort_temp(K, ntiles_b, &t3));
     ENSURE(ctx->temp, t3);
 
     {
         Stage _st(ctx, POTR_STAGE_DUPLICATE);
-        LAUNCH(1, launch_duplicate(n, P<int32_t>(ctx->sids), P<int64_t>(ctx->offs),
-                                   P<SplatRec>(ctx->rec), g.tiles_x, P<uint32_t>(ctx->tkey),
-                                   P<int32_t>(ctx->dup_id),
+        LAUNCH(1, launch_duplicate(total, n, P<int32_t>(ctx->sids), P<int64_t>(ctx->offs),
+                                   P<SplatRec>(ctx->rec), g.tiles_x, g.ntiles,
+                                   P<uint32_t>(ctx->tkey), P<int32_t>(ctx->dup_id),
                                    with_rank ? P<int32_t>(ctx->dup_rank) : nullptr, ctx->stream));
         _st.end();
     }
     {
         Stage _st(ctx, POTR_STAGE_TILE_SORT);
         CK(tile_sort(ctx->temp.p, ctx->temp.cap, P<uint32_t>(ctx->tkey), P<uint32_t>(ctx->tskey),
-                     P<int32_t>(ctx->iota), P<int32_t>(ctx->perm), K, g.ntiles, ctx->stream));
-        _st.end();
-    }
-    {
-        Stage _st(ctx, POTR_STAGE_TILE_SORT);
+                     P<int32_t>(ctx->iota), P<int32_t>(ctx->perm), K, ntiles_b, ctx->stream));
         LAUNCH(1, launch_tile_ranges(K, P<uint32_t>(ctx->tskey), P<int32_t>(ctx->perm),
-                                 P<int32_t>(ctx->dup_id), P<int32_t>(ctx->sid),
-                                 P<int2>(ctx->ranges), g.ntiles,
-                                     ctx->stream));
+                                     P<int32_t>(ctx->dup_id), P<int32_t>(ctx->sid),
+                                     P<int2>(ctx->ranges), ntiles_b, ctx->stream));
         _st.end();
     }
     *K_out = K;
     return 0;
 }
 
-RasterArgs raster_args(potr_ctx *ctx, const potr_camera &cam) {
+RasterArgs raster_args(potr_ctx *ctx, const potr_camera &cam, int nview) {
     ViewGeom g = geom(cam);
     RasterArgs a;
     std::memset(&a, 0, sizeof(a));
@@ -292,7 +298,8 @@ RasterArgs raster_args(potr_ctx *ctx, const potr_camera &cam) {
     a.dup_rank = P<int32_t>(ctx->dup_rank);
     a.ranges = P<int2>(ctx->ranges);
     a.tiles_x = g.tiles_x;
-    a.ntiles = g.ntiles;
+    a.ntiles_view = g.ntiles;
+    a.ntiles = g.ntiles * nview;
     a.tile_counter = P<int>(ctx->tile_counter);
     a.width = g.W;
     a.height = g.H;
@@ -302,38 +309,59 @@ RasterArgs raster_args(potr_ctx *ctx, const potr_camera &cam) {
     return a;
 }
 
+// Views per batch: consecutive views of the same size, at most the configured
+// batch (POTR_B200_VIEW_BATCH, default kMaxViewBatch), and bounded so the
+// batch workspace stays within about 12 GB.
+int batch_len(potr_ctx *ctx, const potr_camera *cams, int s, int ncam, int64_t n) {
+    int cap = ctx->view_batch;
+    const int64_t per_view = n * (int64_t)(sizeof(SplatRec) + 48) + 64 * 1024 * 1024;
+    while (cap > 1 && per_view * cap > (int64_t)12 << 30) cap--;
+    int b = 1;
+    while (b < cap && s + b < ncam && cams[s + b].width == cams[s].width &&
+           cams[s + b].height == cams[s].height)
+        b++;
+    return b;
+}
+
 int score_views_impl(potr_ctx *ctx, const potr_splats *sp, int ncam, const potr_camera *cams,
                      const double *const *targets, double *imp_sum, double *cam_imp,
                      double *dmse_sum, double *mse_sum) {
-    for (int s = 0; s < ncam; s++) {
-        const potr_camera &cam = cams[s];
-        int rc = check_cam(ctx, &cam);
+    const int64_t n = sp->n;
+    for (int s = 0; s < ncam;) {
+        int rc = check_cam(ctx, &cams[s]);
         if (rc) return rc;
-        if (targets && !targets[s]) return fail(ctx, POTR_E_ARG, "target pointer is NULL");
+        const int nb = batch_len(ctx, cams, s, ncam, n);
+        for (int v = 0; v < nb; v++)
+            if (targets && !targets[s + v]) return fail(ctx, POTR_E_ARG, "target pointer is NULL");
         int64_t K = 0;
-        rc = bin_view(ctx, *sp, cam, false, false, &K);
+        rc = bin_batch(ctx, *sp, cams + s, nb, false, false, &K);
         if (rc) return rc;
-        ViewGeom g = geom(cam);
-        RasterArgs a = raster_args(ctx, cam);
-        a.target = targets ? targets[s] : nullptr;
+        ViewGeom g = geom(cams[s]);
+        RasterArgs a = raster_args(ctx, cams[s], nb);
+        for (int v = 0; v < nb; v++) a.target[v] = targets ? targets[s + v] : nullptr;
+        ENSURE(ctx->ci_v, sizeof(double) * n * nb);
+        if (targets) ENSURE(ctx->dm_v, sizeof(double) * n * nb);
         {
             Stage _st(ctx, POTR_STAGE_RASTER);
-            LAUNCH(1, launch_raster(targets ? kScore : kImportance, a, g.ntiles, ctx->stream));
+            LAUNCH(1, launch_raster(targets ? kScore : kImportance, a, a.ntiles, ctx->stream));
             _st.end();
         }
         {
             Stage _st(ctx, POTR_STAGE_REDUCE);
-            LAUNCH(1, launch_splat_reduce(sp->n, P<int32_t>(ctx->sids), P<int64_t>(ctx->offs),
-                                          P<double2>(ctx->partial), g.P, s, cam_imp, imp_sum,
-                                          targets ? dmse_sum : nullptr, ctx->stream));
+            LAUNCH(1, launch_splat_reduce(n * nb, n, P<int32_t>(ctx->sids), P<int64_t>(ctx->offs),
+                                          P<double2>(ctx->partial), g.P,
+                                          cam_imp ? cam_imp + (int64_t)s * n : nullptr,
+                                          P<double>(ctx->ci_v),
+                                          targets ? P<double>(ctx->dm_v) : nullptr, ctx->stream));
+            LAUNCH(1, launch_view_accumulate(n, nb, P<double>(ctx->ci_v),
+                                             targets ? P<double>(ctx->dm_v) : nullptr, imp_sum,
+                                             targets ? dmse_sum : nullptr, ctx->stream));
+            if (targets)
+                LAUNCH(1, launch_mse_reduce(nb, g.ntiles, P<double>(ctx->tile_se), g.P, mse_sum,
+                                            ctx->stream));
             _st.end();
         }
-        if (targets) {
-            Stage _st(ctx, POTR_STAGE_REDUCE);
-            LAUNCH(1, launch_mse_reduce(g.ntiles, P<double>(ctx->tile_se), g.P, mse_sum,
-                                        ctx->stream));
-            _st.end();
-        }
+        s += nb;
     }
     return 0;
 }
@@ -355,6 +383,10 @@ int potr_create(int device, potr_ctx **out) {
     if (cudaSetDevice(device) != cudaSuccess) return POTR_E_CUDA;
     potr_ctx *ctx = new potr_ctx();
     ctx->device = device;
+    if (const char *vb = std::getenv("POTR_B200_VIEW_BATCH")) {
+        int b = std::atoi(vb);
+        ctx->view_batch = b < 1 ? 1 : (b > kMaxViewBatch ? kMaxViewBatch : b);
+    }
     if (cudaMallocHost(&ctx->pinned, 64) != cudaSuccess) {
         delete ctx;
         return POTR_E_NOMEM;
@@ -380,6 +412,8 @@ void potr_destroy(potr_ctx *ctx) {
     if (ctx->pinned) cudaFreeHost(ctx->pinned);
     if (ctx->counters.p) cudaFree(ctx->counters.p);
     if (ctx->tile_counter.p) cudaFree(ctx->tile_counter.p);
+    if (ctx->ci_v.p) cudaFree(ctx->ci_v.p);
+    if (ctx->dm_v.p) cudaFree(ctx->dm_v.p);
     if (ctx->sid.p) cudaFree(ctx->sid.p);
     for (auto &ev : ctx->events) {
         cudaEventDestroy(ev.second.first);
@@ -460,12 +494,12 @@ int potr_render(potr_ctx *ctx, const potr_splats *splats, const potr_camera *cam
     if ((rc = check_cam(ctx, cam))) return rc;
     if (!image) return fail(ctx, POTR_E_ARG, "image is NULL");
     int64_t K = 0;
-    rc = bin_view(ctx, *splats, *cam, false, false, &K);
+    rc = bin_batch(ctx, *splats, cam, 1, false, false, &K);
     if (rc) return rc;
-    RasterArgs a = raster_args(ctx, *cam);
-    a.image = image;
-    a.trans = trans;
-    LAUNCH(1, launch_raster(kRender, a, geom(*cam).ntiles, ctx->stream));
+    RasterArgs a = raster_args(ctx, *cam, 1);
+    a.image[0] = image;
+    a.trans[0] = trans;
+    LAUNCH(1, launch_raster(kRender, a, a.ntiles, ctx->stream));
     return POTR_OK;
 }
 
@@ -483,7 +517,7 @@ int potr_render_records(potr_ctx *ctx, const potr_splats *splats, const potr_cam
         return fail(ctx, POTR_E_ARG, "record output pointer is NULL");
     const int64_t n = splats->n;
     int64_t K = 0;
-    rc = bin_view(ctx, *splats, *cam, true, true, &K);
+    rc = bin_batch(ctx, *splats, cam, 1, true, true, &K);
     if (rc) return rc;
     int64_t cap = capacity > 0 ? capacity : 0;
     ENSURE(ctx->rcounter, sizeof(unsigned long long));
@@ -492,16 +526,16 @@ int potr_render_records(potr_ctx *ctx, const potr_splats *splats, const potr_cam
     ENSURE(ctx->rt, sizeof(double) * cap);
     ENSURE(ctx->rp, sizeof(double) * 3 * cap);
     CK(cudaMemsetAsync(ctx->rcounter.p, 0, sizeof(unsigned long long), ctx->stream));
-    RasterArgs a = raster_args(ctx, *cam);
-    a.image = image;
-    a.trans = trans;
+    RasterArgs a = raster_args(ctx, *cam, 1);
+    a.image[0] = image;
+    a.trans[0] = trans;
     a.rec_counter = P<unsigned long long>(ctx->rcounter);
     a.rec_capacity = cap;
     a.rec_key = P<uint64_t>(ctx->rkey);
     a.rec_alpha = P<double>(ctx->ralpha);
     a.rec_t = P<double>(ctx->rt);
     a.rec_p = P<double>(ctx->rp);
-    LAUNCH(1, launch_raster(kRecords, a, geom(*cam).ntiles, ctx->stream));
+    LAUNCH(1, launch_raster(kRecords, a, a.ntiles, ctx->stream));
     if (colors)
         LAUNCH(1, launch_colors_from_rec(n, P<uint64_t>(ctx->key), P<SplatRec>(ctx->rec), colors,
                                          ctx->stream));
@@ -551,7 +585,7 @@ int potr_bin(potr_ctx *ctx, const potr_splats *splats, const potr_camera *cam, i
     if (rc) return rc;
     if ((rc = check_cam(ctx, cam))) return rc;
     int64_t K = 0;
-    rc = bin_view(ctx, *splats, *cam, false, false, &K);
+    rc = bin_batch(ctx, *splats, cam, 1, false, false, &K);
     if (rc) return rc;
     *n_pairs = K;
     if (tile_splats && capacity < K) return fail(ctx, POTR_E_CAPACITY, "tile list capacity");

@@ -118,6 +118,14 @@ struct Cam {
 };
 static_assert(sizeof(Cam) == sizeof(potr_camera), "camera layout");
 
+// Views processed together by one pipeline round (one preprocess, one scan,
+// one duplicate, one tile sort, one persistent raster launch).
+constexpr int kMaxViewBatch = 8;
+
+struct CamBatch {
+    Cam cam[kMaxViewBatch];
+};
+
 struct Proj {
     double mx, my, a, b, c, depth, radius;
     bool valid;

@@ -34,60 +34,76 @@ namespace potr {
 // ---------------------------------------------------------------------------
 // (a) preprocess
 
-__global__ void __launch_bounds__(256) k_preprocess(potr_splats sp, Cam cam, int tiles_x,
-                                                     int all_colors, SplatRec *__restrict__ rec,
+__global__ void __launch_bounds__(256) k_preprocess(potr_splats sp, CamBatch cams, int nview,
+                                                     int tiles_x, int all_colors,
+                                                     SplatRec *__restrict__ rec,
                                                      uint64_t *__restrict__ key,
                                                      int32_t *__restrict__ cnt,
                                                      unsigned long long *counters) {
-    int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (k >= sp.n) return;
-    Proj pr = project_one(sp.positions + 3 * k, sp.scales + 3 * k, sp.rotations + 4 * k, cam);
-    int32_t c = 0;
-    uint64_t kk = ~0ull;
-    if (pr.valid) {
-        kk = (uint64_t)__double_as_longlong(pr.depth);  // depth > 0.01: bits are monotone
-        const int W = cam.width, H = cam.height;
-        double x0 = floor(pr.mx - pr.radius), x1 = ceil(pr.mx + pr.radius);
-        double y0 = floor(pr.my - pr.radius), y1 = ceil(pr.my + pr.radius);
-        if (x0 < 0) x0 = 0;
-        if (y0 < 0) y0 = 0;
-        if (x1 > W - 1) x1 = W - 1;
-        if (y1 > H - 1) y1 = H - 1;
-        double det = pr.a * pr.c - pr.b * pr.b;
-        bool draw = !(x0 > x1 || y0 > y1) && det > 0.0;
-        if (draw || all_colors) {
-            SplatRec r;
-            r.mx = pr.mx;
-            r.my = pr.my;
-            r.ia = pr.c / det;
-            r.ib = -pr.b / det;
-            r.ic = pr.a / det;
-            double o = sp.opacities[k];
-            r.opac = o;
-            double rgb[3];
-            splat_color(sp.positions + 3 * k, sp.sh + 48 * k, cam, rgb);
-            r.cr = rgb[0];
-            r.cg = rgb[1];
-            r.cb = rgb[2];
-            r.pthr = log(kAlphaFloor / o) - kPowerMargin;
-            r.x0 = (int32_t)x0;
-            r.x1 = (int32_t)x1;
-            r.y0 = (int32_t)y0;
-            r.y1 = (int32_t)y1;
-            if (!draw) r.x0 = 1, r.x1 = 0;  // empty: never drawn
-            rec[k] = r;
-        }
-        if (draw) {
-            int tx0 = (int)x0 >> kTileWLog2, tx1 = (int)x1 >> kTileWLog2;
-            int ty0 = (int)y0 >> kTileHLog2, ty1 = (int)y1 >> kTileHLog2;
-            c = (tx1 - tx0 + 1) * (ty1 - ty0 + 1);
-            if (counters)  // E: pixels the reference loop visits (rasterizer.py:159-161)
-                atomicAdd(&counters[0],
-                          (unsigned long long)((x1 - x0 + 1.0) * (y1 - y0 + 1.0)));
-        }
+    const int64_t n = sp.n;
+    const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= n) return;
+    // the splat's attributes are read once for all views of the batch
+    double pos[3], scl[3], rot[4];
+#pragma unroll
+    for (int i = 0; i < 3; i++) {
+        pos[i] = sp.positions[3 * k + i];
+        scl[i] = sp.scales[3 * k + i];
     }
-    key[k] = kk;
-    cnt[k] = c;
+#pragma unroll
+    for (int i = 0; i < 4; i++) rot[i] = sp.rotations[4 * k + i];
+    const double o = sp.opacities[k];
+    const double pthr = log(kAlphaFloor / o) - kPowerMargin;
+    for (int v = 0; v < nview; v++) {
+        const Cam &cam = cams.cam[v];
+        const int64_t g = (int64_t)v * n + k;
+        Proj pr = project_one(pos, scl, rot, cam);
+        int32_t c = 0;
+        uint64_t kk = ~0ull;
+        if (pr.valid) {
+            kk = (uint64_t)__double_as_longlong(pr.depth);  // depth > 0.01: bits are monotone
+            const int W = cam.width, H = cam.height;
+            double x0 = floor(pr.mx - pr.radius), x1 = ceil(pr.mx + pr.radius);
+            double y0 = floor(pr.my - pr.radius), y1 = ceil(pr.my + pr.radius);
+            if (x0 < 0) x0 = 0;
+            if (y0 < 0) y0 = 0;
+            if (x1 > W - 1) x1 = W - 1;
+            if (y1 > H - 1) y1 = H - 1;
+            const double det = pr.a * pr.c - pr.b * pr.b;
+            const bool draw = !(x0 > x1 || y0 > y1) && det > 0.0;
+            if (draw || all_colors) {
+                SplatRec r;
+                r.mx = pr.mx;
+                r.my = pr.my;
+                r.ia = pr.c / det;
+                r.ib = -pr.b / det;
+                r.ic = pr.a / det;
+                r.opac = o;
+                double rgb[3];
+                splat_color(pos, sp.sh + 48 * k, cam, rgb);
+                r.cr = rgb[0];
+                r.cg = rgb[1];
+                r.cb = rgb[2];
+                r.pthr = pthr;
+                r.x0 = (int32_t)x0;
+                r.x1 = (int32_t)x1;
+                r.y0 = (int32_t)y0;
+                r.y1 = (int32_t)y1;
+                if (!draw) r.x0 = 1, r.x1 = 0;  // empty: never drawn
+                rec[g] = r;
+            }
+            if (draw) {
+                const int tx0 = (int)x0 >> kTileWLog2, tx1 = (int)x1 >> kTileWLog2;
+                const int ty0 = (int)y0 >> kTileHLog2, ty1 = (int)y1 >> kTileHLog2;
+                c = (tx1 - tx0 + 1) * (ty1 - ty0 + 1);
+                if (counters)  // E: pixels the reference loop visits (rasterizer.py:159-161)
+                    atomicAdd(&counters[0],
+                              (unsigned long long)((x1 - x0 + 1.0) * (y1 - y0 + 1.0)));
+            }
+        }
+        key[g] = kk;
+        cnt[g] = c;
+    }
 }
 
 // project_splats / splat_colors dump for parity tests (potr_project).
@@ -110,29 +126,36 @@ __global__ void k_project_dump(potr_splats sp, Cam cam, double *mean2d, double *
 // ---------------------------------------------------------------------------
 // (b) binning
 
-__global__ void k_gather_counts(int64_t n, const int32_t *__restrict__ ids,
+// Batch arrays are view-major: element (v, i) at v*n + i.
+__global__ void k_gather_counts(int64_t total, int64_t n, const int32_t *__restrict__ ids,
                                 const int32_t *__restrict__ cnt, int64_t *__restrict__ out) {
-    int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (r < n) out[r] = cnt[ids[r]];
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < total) out[i] = cnt[(i / n) * n + ids[i]];
 }
 
-__global__ void k_duplicate(int64_t n, const int32_t *__restrict__ ids,
+// Emit the (tile, splat) pairs of every drawn splat, walking splats in depth
+// order so a stable sort on the tile key yields (tile, depth, id) order.
+// Tile keys are batch-global: v * ntiles + ty * tiles_x + tx.
+__global__ void k_duplicate(int64_t total, int64_t n, const int32_t *__restrict__ ids,
                             const int64_t *__restrict__ offs, const SplatRec *__restrict__ rec,
-                            int tiles_x, uint32_t *__restrict__ tkey, int32_t *__restrict__ dup_id,
-                            int32_t *__restrict__ dup_rank) {
-    int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (r >= n) return;
-    int64_t o = offs[r], e = offs[r + 1];
+                            int tiles_x, int ntiles, uint32_t *__restrict__ tkey,
+                            int32_t *__restrict__ dup_gid, int32_t *__restrict__ dup_rank) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= total) return;
+    int64_t o = offs[i];
+    const int64_t e = offs[i + 1];
     if (o == e) return;
-    int32_t id = ids[r];
-    const SplatRec &R = rec[id];
-    int tx0 = R.x0 >> kTileWLog2, tx1 = R.x1 >> kTileWLog2;
-    int ty0 = R.y0 >> kTileHLog2, ty1 = R.y1 >> kTileHLog2;
+    const int64_t v = i / n;
+    const int32_t g = (int32_t)(v * n + ids[i]);
+    const SplatRec &R = rec[g];
+    const int tx0 = R.x0 >> kTileWLog2, tx1 = R.x1 >> kTileWLog2;
+    const int ty0 = R.y0 >> kTileHLog2, ty1 = R.y1 >> kTileHLog2;
+    const uint32_t tbase = (uint32_t)(v * ntiles);
     for (int ty = ty0; ty <= ty1; ty++)
         for (int tx = tx0; tx <= tx1; tx++) {
-            tkey[o] = (uint32_t)(ty * tiles_x + tx);
-            dup_id[o] = id;
-            if (dup_rank) dup_rank[o] = (int32_t)r;
+            tkey[o] = tbase + (uint32_t)(ty * tiles_x + tx);
+            dup_gid[o] = g;
+            if (dup_rank) dup_rank[o] = (int32_t)(i - v * n);
             o++;
         }
 }
@@ -320,8 +343,13 @@ __global__ void __launch_bounds__(32 * kRasterWarps, POTR_RASTER_MIN_BLOCKS) k_r
         tile = __shfl_sync(FULL, tile, 0);
         if (tile >= a.ntiles) return;
 
-        const int tx = tile % a.tiles_x, ty = tile / a.tiles_x;
+        const int view = tile / a.ntiles_view;
+        const int vt = tile - view * a.ntiles_view;
+        const int tx = vt % a.tiles_x, ty = vt / a.tiles_x;
         const int px = tx * kTileW + (lane & 7), py = ty * kTileH + (lane >> 3);
+        const double *target = a.target[view];
+        double *image = a.image[view];
+        double *trans = a.trans[view];
         const bool inside = px < a.width && py < a.height;
         const int64_t pix = (int64_t)py * a.width + px;
         const int2 range = a.ranges[tile];
@@ -397,12 +425,12 @@ __global__ void __launch_bounds__(32 * kRasterWarps, POTR_RASTER_MIN_BLOCKS) k_r
         }
 
         if (MODE == kRender || MODE == kRecords) {
-            if (inside && a.image) {
-                a.image[3 * pix] = P0;
-                a.image[3 * pix + 1] = P1;
-                a.image[3 * pix + 2] = P2;
+            if (inside && image) {
+                image[3 * pix] = P0;
+                image[3 * pix + 1] = P1;
+                image[3 * pix + 2] = P2;
             }
-            if (inside && a.trans) a.trans[pix] = T;
+            if (inside && trans) trans[pix] = T;
             continue;
         }
 
@@ -412,20 +440,20 @@ __global__ void __launch_bounds__(32 * kRasterWarps, POTR_RASTER_MIN_BLOCKS) k_r
         if (MODE == kScore) {
             double se = 0.0;
             if (inside) {
-                dr0 = PK0 - a.target[3 * pix];
-                dr1 = PK1 - a.target[3 * pix + 1];
-                dr2 = PK2 - a.target[3 * pix + 2];
+                dr0 = PK0 - target[3 * pix];
+                dr1 = PK1 - target[3 * pix + 1];
+                dr2 = PK2 - target[3 * pix + 2];
                 se = dr0 * dr0 + dr1 * dr1 + dr2 * dr2;
             }
             se = warp_sum(se);
             if (lane == 0) a.tile_se[tile] = se;
         }
-        if (inside && a.image) {
-            a.image[3 * pix] = PK0;
-            a.image[3 * pix + 1] = PK1;
-            a.image[3 * pix + 2] = PK2;
+        if (inside && image) {
+            image[3 * pix] = PK0;
+            image[3 * pix + 1] = PK1;
+            image[3 * pix + 2] = PK2;
         }
-        if (inside && a.trans) a.trans[pix] = T;
+        if (inside && trans) trans[pix] = T;
         T = 1.0;
         P0 = P1 = P2 = 0.0;
         done = !inside;
@@ -498,43 +526,63 @@ __global__ void __launch_bounds__(32 * kRasterWarps, POTR_RASTER_MIN_BLOCKS) k_r
     }
 }
 
-// Per-splat sum of its (tile, splat) slots, in tile order (deterministic),
-// then the per-camera normalisation and the camera-ordered accumulation.
-__global__ void k_splat_reduce(int64_t n, const int32_t *__restrict__ ids,
+// Per (view, splat): sum of its (tile, splat) slots in tile order
+// (deterministic), normalised by P and 3P (rasterizer.py:230, :334).
+__global__ void k_splat_reduce(int64_t total, int64_t n, const int32_t *__restrict__ ids,
                                const int64_t *__restrict__ offs,
-                               const double2 *__restrict__ partial, double P, int64_t cam_row,
-                               double *__restrict__ cam_imp, double *__restrict__ imp_acc,
-                               double *__restrict__ dmse_acc) {
-    int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (r >= n) return;
-    int32_t id = ids[r];
-    int64_t o = offs[r], e = offs[r + 1];
+                               const double2 *__restrict__ partial, double P,
+                               double *__restrict__ cam_imp_rows, double *__restrict__ ci_out,
+                               double *__restrict__ dm_out) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= total) return;
+    const int64_t v = i / n;
+    const int64_t g = v * n + ids[i];
+    const int64_t o = offs[i], e = offs[i + 1];
     double dse = 0.0, imp = 0.0;
     for (int64_t j = o; j < e; j++) {
-        double2 v = partial[j];
-        dse += v.x;
-        imp += v.y;
+        const double2 x = partial[j];
+        dse += x.x;
+        imp += x.y;
     }
-    double ci = imp / P;  // rasterizer.py:230
-    if (cam_imp) cam_imp[cam_row * n + id] = ci;
-    imp_acc[id] += ci;                                  // :344, :348
-    if (dmse_acc) dmse_acc[id] += dse / (P * 3.0);      // :334, :346
+    const double ci = imp / P;
+    ci_out[g] = ci;
+    if (cam_imp_rows) cam_imp_rows[g] = ci;
+    if (dm_out) dm_out[g] = dse / (P * 3.0);
 }
 
-// Sum of the per-tile squared errors; mse(s) = sum / 3P (:335), added to the
-// camera-ordered accumulator (:347).
-__global__ void k_mse_reduce(int ntiles, const double *__restrict__ tile_se, double P,
+// Camera-ordered accumulation over the views of the batch (rasterizer.py:343-347).
+__global__ void k_view_accumulate(int64_t n, int nview, const double *__restrict__ ci,
+                                  const double *__restrict__ dm, double *__restrict__ imp_acc,
+                                  double *__restrict__ dmse_acc) {
+    const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= n) return;
+    double ia = imp_acc[k];
+    double da = dm ? dmse_acc[k] : 0.0;
+    for (int v = 0; v < nview; v++) {
+        ia += ci[(int64_t)v * n + k];
+        if (dm) da += dm[(int64_t)v * n + k];
+    }
+    imp_acc[k] = ia;
+    if (dm) dmse_acc[k] = da;
+}
+
+// Per view, the sum of its tiles' squared errors; mse(s) = sum / 3P (:335),
+// added to the camera-ordered accumulator (:347).
+__global__ void k_mse_reduce(int nview, int ntiles, const double *__restrict__ tile_se, double P,
                              double *__restrict__ mse_acc) {
     __shared__ double red[32];
-    double s = 0.0;
-    for (int t = threadIdx.x; t < ntiles; t += blockDim.x) s += tile_se[t];
-    s = warp_sum(s);
-    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        double t = 0.0;
-        for (int w = 0; w < (int)(blockDim.x >> 5); w++) t += red[w];
-        mse_acc[0] += t / (P * 3.0);
+    for (int v = 0; v < nview; v++) {
+        double s = 0.0;
+        for (int t = threadIdx.x; t < ntiles; t += blockDim.x) s += tile_se[(int64_t)v * ntiles + t];
+        s = warp_sum(s);
+        if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            double t = 0.0;
+            for (int w = 0; w < (int)(blockDim.x >> 5); w++) t += red[w];
+            mse_acc[0] += t / (P * 3.0);
+        }
+        __syncthreads();
     }
 }
 
@@ -626,12 +674,12 @@ static inline unsigned grid_for(int64_t n, int block) {
 
 size_t raster_smem_bytes() { return sizeof(WarpSmem) * kRasterWarps + 64 * sizeof(double2); }
 
-cudaError_t launch_preprocess(const potr_splats &sp, const Cam &cam, int tiles_x, int all_colors,
-                              SplatRec *rec, uint64_t *key, int32_t *cnt,
-                              unsigned long long *counters, cudaStream_t st) {
+cudaError_t launch_preprocess(const potr_splats &sp, const CamBatch &cams, int nview,
+                              int tiles_x, int all_colors, SplatRec *rec, uint64_t *key,
+                              int32_t *cnt, unsigned long long *counters, cudaStream_t st) {
     if (sp.n == 0) return cudaSuccess;
-    k_preprocess<<<grid_for(sp.n, 256), 256, 0, st>>>(sp, cam, tiles_x, all_colors, rec, key, cnt,
-                                                       counters);
+    k_preprocess<<<grid_for(sp.n, 128), 128, 0, st>>>(sp, cams, nview, tiles_x, all_colors, rec,
+                                                       key, cnt, counters);
     return cudaGetLastError();
 }
 
@@ -664,12 +712,13 @@ cudaError_t depth_sort_temp(int64_t n, size_t *bytes) {
 }
 
 cudaError_t scan_counts(void *temp, size_t temp_bytes, const int32_t *ids, const int32_t *cnt,
-                        int64_t *cnt_sorted, int64_t *offs, int64_t n, cudaStream_t st) {
+                        int64_t *cnt_sorted, int64_t *offs, int64_t total, int64_t n,
+                        cudaStream_t st) {
     cudaError_t e = cudaMemsetAsync(offs, 0, sizeof(int64_t), st);
-    if (e != cudaSuccess || n == 0) return e;
-    k_gather_counts<<<grid_for(n, 256), 256, 0, st>>>(n, ids, cnt, cnt_sorted);
+    if (e != cudaSuccess || total == 0) return e;
+    k_gather_counts<<<grid_for(total, 256), 256, 0, st>>>(total, n, ids, cnt, cnt_sorted);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
-    return cub::DeviceScan::InclusiveSum(temp, temp_bytes, cnt_sorted, offs + 1, (int)n, st);
+    return cub::DeviceScan::InclusiveSum(temp, temp_bytes, cnt_sorted, offs + 1, (int)total, st);
 }
 
 cudaError_t scan_temp(int64_t n, size_t *bytes) {
@@ -677,12 +726,12 @@ cudaError_t scan_temp(int64_t n, size_t *bytes) {
                                          (int64_t *)nullptr, (int)n);
 }
 
-cudaError_t launch_duplicate(int64_t n, const int32_t *ids, const int64_t *offs,
-                             const SplatRec *rec, int tiles_x, uint32_t *tkey, int32_t *dup_id,
-                             int32_t *dup_rank, cudaStream_t st) {
-    if (n == 0) return cudaSuccess;
-    k_duplicate<<<grid_for(n, 256), 256, 0, st>>>(n, ids, offs, rec, tiles_x, tkey, dup_id,
-                                                   dup_rank);
+cudaError_t launch_duplicate(int64_t total, int64_t n, const int32_t *ids, const int64_t *offs,
+                             const SplatRec *rec, int tiles_x, int ntiles, uint32_t *tkey,
+                             int32_t *dup_gid, int32_t *dup_rank, cudaStream_t st) {
+    if (total == 0) return cudaSuccess;
+    k_duplicate<<<grid_for(total, 256), 256, 0, st>>>(total, n, ids, offs, rec, tiles_x, ntiles,
+                                                       tkey, dup_gid, dup_rank);
     return cudaGetLastError();
 }
 
@@ -758,18 +807,25 @@ cudaError_t launch_raster(int mode, const RasterArgs &a, int ntiles, cudaStream_
     return cudaErrorInvalidValue;
 }
 
-cudaError_t launch_splat_reduce(int64_t n, const int32_t *ids, const int64_t *offs,
-                                const double2 *partial, double P, int64_t cam_row, double *cam_imp,
-                                double *imp_acc, double *dmse_acc, cudaStream_t st) {
-    if (n == 0) return cudaSuccess;
-    k_splat_reduce<<<grid_for(n, 256), 256, 0, st>>>(n, ids, offs, partial, P, cam_row, cam_imp,
-                                                      imp_acc, dmse_acc);
+cudaError_t launch_splat_reduce(int64_t total, int64_t n, const int32_t *ids, const int64_t *offs,
+                                const double2 *partial, double P, double *cam_imp_rows,
+                                double *ci_out, double *dm_out, cudaStream_t st) {
+    if (total == 0) return cudaSuccess;
+    k_splat_reduce<<<grid_for(total, 256), 256, 0, st>>>(total, n, ids, offs, partial, P,
+                                                          cam_imp_rows, ci_out, dm_out);
     return cudaGetLastError();
 }
 
-cudaError_t launch_mse_reduce(int ntiles, const double *tile_se, double P, double *mse_acc,
-                              cudaStream_t st) {
-    k_mse_reduce<<<1, 1024, 0, st>>>(ntiles, tile_se, P, mse_acc);
+cudaError_t launch_view_accumulate(int64_t n, int nview, const double *ci, const double *dm,
+                                   double *imp_acc, double *dmse_acc, cudaStream_t st) {
+    if (n == 0) return cudaSuccess;
+    k_view_accumulate<<<grid_for(n, 256), 256, 0, st>>>(n, nview, ci, dm, imp_acc, dmse_acc);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_mse_reduce(int nview, int ntiles, const double *tile_se, double P,
+                              double *mse_acc, cudaStream_t st) {
+    k_mse_reduce<<<1, 1024, 0, st>>>(nview, ntiles, tile_se, P, mse_acc);
     return cudaGetLastError();
 }
 

@@ -10,16 +10,17 @@ enum RasterMode { kRender = 0, kImportance = 1, kScore = 2, kRecords = 3 };
 struct RasterArgs {
     const SplatRec *rec;
     const int32_t *perm;      // sorted pair -> duplicate index
-    const int32_t *dup_id;    // duplicate index -> splat id
-    const int32_t *sid;       // sorted pair -> splat id
+    const int32_t *dup_id;    // duplicate index -> batch record index (v * n + splat id)
+    const int32_t *sid;       // sorted pair -> batch record index
     const int32_t *dup_rank;  // duplicate index -> depth rank (records mode)
     const int2 *ranges;       // per tile [start, end) into perm
-    int tiles_x, ntiles;
+    int tiles_x, ntiles;      // ntiles: all tiles of the batch (nview * ntiles_view)
+    int ntiles_view;
     int *tile_counter;        // persistent-warp work counter (zeroed per launch)
     int width, height;
-    const double *target;     // (H,W,3), score mode
-    double *image;            // (H,W,3) nullable
-    double *trans;            // (H,W) nullable
+    const double *target[kMaxViewBatch];  // per view (H,W,3), score mode
+    double *image[kMaxViewBatch];         // per view (H,W,3), nullable
+    double *trans[kMaxViewBatch];         // per view (H,W), nullable
     double2 *partial;         // per duplicate (dSE, T*alpha)
     double *tile_se;          // per tile squared error (score mode)
     // records mode
@@ -33,9 +34,9 @@ struct RasterArgs {
 
 size_t raster_smem_bytes();
 
-cudaError_t launch_preprocess(const potr_splats &sp, const Cam &cam, int tiles_x, int all_colors,
-                              SplatRec *rec, uint64_t *key, int32_t *cnt,
-                              unsigned long long *counters, cudaStream_t st);
+cudaError_t launch_preprocess(const potr_splats &sp, const CamBatch &cams, int nview,
+                              int tiles_x, int all_colors, SplatRec *rec, uint64_t *key,
+                              int32_t *cnt, unsigned long long *counters, cudaStream_t st);
 cudaError_t launch_project_dump(const potr_splats &sp, const Cam &cam, double *mean2d,
                                 double *cov2d, double *depth, double *radius, uint8_t *valid,
                                 double *colors, cudaStream_t st);
@@ -45,10 +46,11 @@ cudaError_t depth_sort(void *temp, size_t temp_bytes, const uint64_t *key, uint6
                        const int32_t *iota, int32_t *sids, int64_t n, cudaStream_t st);
 cudaError_t scan_temp(int64_t n, size_t *bytes);
 cudaError_t scan_counts(void *temp, size_t temp_bytes, const int32_t *ids, const int32_t *cnt,
-                        int64_t *cnt_sorted, int64_t *offs, int64_t n, cudaStream_t st);
-cudaError_t launch_duplicate(int64_t n, const int32_t *ids, const int64_t *offs,
-                             const SplatRec *rec, int tiles_x, uint32_t *tkey, int32_t *dup_id,
-                             int32_t *dup_rank, cudaStream_t st);
+                        int64_t *cnt_sorted, int64_t *offs, int64_t total, int64_t n,
+                        cudaStream_t st);
+cudaError_t launch_duplicate(int64_t total, int64_t n, const int32_t *ids, const int64_t *offs,
+                             const SplatRec *rec, int tiles_x, int ntiles, uint32_t *tkey,
+                             int32_t *dup_gid, int32_t *dup_rank, cudaStream_t st);
 cudaError_t tile_sort_temp(int64_t K, int ntiles, size_t *bytes);
 cudaError_t tile_sort(void *temp, size_t temp_bytes, const uint32_t *tkey, uint32_t *skey,
                       const int32_t *iota, int32_t *perm, int64_t K, int ntiles, cudaStream_t st);
@@ -59,11 +61,13 @@ cudaError_t launch_tile_ranges(int64_t K, const uint32_t *skey, const int32_t *p
                                const int32_t *dup_id, int32_t *sid, int2 *rng, int ntiles,
                                cudaStream_t st);
 cudaError_t launch_raster(int mode, const RasterArgs &a, int ntiles, cudaStream_t st);
-cudaError_t launch_splat_reduce(int64_t n, const int32_t *ids, const int64_t *offs,
-                                const double2 *partial, double P, int64_t cam_row, double *cam_imp,
-                                double *imp_acc, double *dmse_acc, cudaStream_t st);
-cudaError_t launch_mse_reduce(int ntiles, const double *tile_se, double P, double *mse_acc,
-                              cudaStream_t st);
+cudaError_t launch_splat_reduce(int64_t total, int64_t n, const int32_t *ids, const int64_t *offs,
+                                const double2 *partial, double P, double *cam_imp_rows,
+                                double *ci_out, double *dm_out, cudaStream_t st);
+cudaError_t launch_view_accumulate(int64_t n, int nview, const double *ci, const double *dm,
+                                   double *imp_acc, double *dmse_acc, cudaStream_t st);
+cudaError_t launch_mse_reduce(int nview, int ntiles, const double *tile_se, double P,
+                              double *mse_acc, cudaStream_t st);
 cudaError_t launch_finalize(int64_t n, int S, double *imp, double *dmse, double *mse,
                             cudaStream_t st);
 cudaError_t launch_records_gather(int64_t m, const uint64_t *skey, const int32_t *sidx,
