@@ -151,6 +151,14 @@ int potr_sh_solve(potr_ctx *ctx, const potr_splats *splats, const double *normal
                   double lambda_y, double parallel_threshold, double zero_threshold,
                   double *rgb, double *ycocg, int8_t *status);
 
+/* ---- tuning ------------------------------------------------------------- */
+
+/* Views processed per pipeline round (1..8, default 8; env POTR_B200_VIEW_BATCH). */
+#define POTR_OPT_VIEW_BATCH 1
+/* 1: sort raw 64-bit depth bits per view instead of the compact batch key. */
+#define POTR_OPT_RAW_DEPTH_KEYS 2
+int potr_set_option(potr_ctx *ctx, int option, int value);
+
 /* ---- evidence: live stage timing and work counters --------------------- */
 
 /* Stages timed with CUDA events on the context stream while profiling. */

@@ -19,6 +19,8 @@ POTR_E_CUDA = -2
 POTR_E_NOMEM = -3
 POTR_E_CAPACITY = -4
 NEQ_STRIDE = 185
+OPT_VIEW_BATCH = 1
+OPT_RAW_DEPTH_KEYS = 2
 STAGES = ["preprocess", "depth_sort", "scan", "duplicate", "tile_sort", "raster", "reduce",
           "sh_accumulate", "sh_solve"]
 
@@ -92,6 +94,7 @@ _SIGNATURES = {
     "potr_sh_solve": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(PotrSplats), ctypes.c_void_p,
                                      ctypes.c_double, ctypes.c_double, ctypes.c_double,
                                      ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]),
+    "potr_set_option": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.c_int]),
     "potr_profile_enable": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int]),
     "potr_profile_read": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]),
     "potr_counters_enable": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int]),

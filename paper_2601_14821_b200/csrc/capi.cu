@@ -1,6 +1,7 @@
 // capi.cu -- the extern "C" boundary (include/potr_b200.h): context, grow-only
 // device workspace, and the per-view orchestration of kernels (a)-(e).
 #include <cstdio>
+#include <cmath>
 #include <cstdlib>
 #include <cstring>
 #include <string>
@@ -45,8 +46,11 @@ struct potr_ctx {
     bool counting = false;
     DevBuf counters;
     int64_t pairs_total = 0;
-    DevBuf tile_counter, sid, ci_v, dm_v;
+    DevBuf tile_counter, sid, ci_v, dm_v, bbox, overflow;
+    double scene_lo[3] = {0, 0, 0}, scene_hi[3] = {0, 0, 0};  // splat position bbox
+    uint64_t invalid_key0 = ~0ull;  // depth key of an invalid splat in view 0 of the last batch
     int view_batch = kMaxViewBatch;
+    bool raw_depth_keys = false;
 };
 
 namespace {
@@ -194,12 +198,91 @@ ViewGeom geom(const potr_camera &c) {
     return g;
 }
 
+double ordered_to_double(unsigned long long u) {
+    const unsigned long long b = (u >> 63) ? (u & ~(1ull << 63)) : ~u;
+    double d;
+    std::memcpy(&d, &b, sizeof(d));
+    return d;
+}
+
+uint64_t dbits(double d) {
+    uint64_t b;
+    std::memcpy(&b, &d, sizeof(b));
+    return b;
+}
+
+int bitlen(uint64_t x) {
+    int b = 0;
+    while (x) {
+        b++;
+        x >>= 1;
+    }
+    return b;
+}
+
+// Axis-aligned bounds of the splat centres (one reduction + sync per call):
+// they bound every view's depth range, which makes the batch depth key compact.
+int compute_scene_bounds(potr_ctx *ctx, const potr_splats &sp) {
+    ENSURE(ctx->bbox, 6 * sizeof(unsigned long long));
+    LAUNCH(1, launch_bbox(sp.n, sp.positions, P<unsigned long long>(ctx->bbox), ctx->stream));
+    CK(cudaMemcpyAsync(ctx->pinned, ctx->bbox.p, 6 * sizeof(uint64_t), cudaMemcpyDeviceToHost,
+                       ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    for (int i = 0; i < 3; i++) {
+        ctx->scene_lo[i] = ordered_to_double((unsigned long long)ctx->pinned[i]);
+        ctx->scene_hi[i] = ordered_to_double((unsigned long long)ctx->pinned[3 + i]);
+    }
+    return 0;
+}
+
+// The compact batch depth key (raster.cuh DepthKey) from the scene bounds.
+DepthKey depth_key_for(potr_ctx *ctx, const potr_camera *cams, int nview, int64_t n) {
+    DepthKey dk;
+    std::memset(&dk, 0, sizeof(dk));
+    dk.overflow = P<int>(ctx->overflow);
+    if (n == 0) return dk;
+    double zmin = 1e300, zmax = -1e300;
+    for (int v = 0; v < nview; v++) {
+        const double *w = cams[v].rot + 6;
+        double lo = 0.0, hi = 0.0;
+        for (int i = 0; i < 3; i++) {
+            const double a = w[i] * (ctx->scene_lo[i] - cams[v].eye[i]);
+            const double b = w[i] * (ctx->scene_hi[i] - cams[v].eye[i]);
+            lo += a < b ? a : b;
+            hi += a < b ? b : a;
+        }
+        zmin = lo < zmin ? lo : zmin;
+        zmax = hi > zmax ? hi : zmax;
+    }
+    if (!(zmax == zmax) || !(zmin == zmin)) return dk;  // NaN bounds: raw keys
+    const double margin = 1e-9 * (std::fabs(zmin) + std::fabs(zmax) + 1.0);
+    double lo = zmin - margin;
+    if (lo < kNearClip) lo = kNearClip;
+    const double hi = zmax + margin;
+    if (!(hi > lo)) {
+        dk.compact = 1;  // nothing can be valid: any width works
+        dk.nbits = 1;
+        dk.lo_bits = dbits(kNearClip);
+        dk.sentinel = 1;
+        return dk;
+    }
+    const uint64_t range = dbits(hi) - dbits(lo) + 1;
+    const int nbits = bitlen(range + 1);
+    const int vbits = bitlen((uint64_t)(nview - 1));
+    if (nbits + vbits > 64) return dk;
+    dk.compact = 1;
+    dk.nbits = nbits;
+    dk.lo_bits = dbits(lo);
+    dk.sentinel = (nbits == 64) ? ~0ull : ((1ull << nbits) - 1);
+    return dk;
+}
+
 // (a)+(b) for a batch of `nview` views of equal size: preprocess (splat
 // attributes read once per batch), per-view stable depth sorts, one scan over
 // all (view, rank) counts, one duplicate, one stable tile sort over batch-global
 // tile keys, tile ranges.  On return *K_out holds the number of pairs.
 int bin_batch(potr_ctx *ctx, const potr_splats &sp, const potr_camera *cams, int nview,
-              bool all_colors, bool with_rank, int64_t *K_out) {
+              bool all_colors, bool with_rank, int64_t *K_out, bool allow_compact = true) {
     const int64_t n = sp.n;
     const int64_t total = n * nview;
     ViewGeom g = geom(cams[0]);
@@ -217,26 +300,39 @@ int bin_batch(potr_ctx *ctx, const potr_splats &sp, const potr_camera *cams, int
     ENSURE(ctx->ranges, sizeof(int2) * ntiles_b);
     ENSURE(ctx->tile_se, sizeof(double) * ntiles_b);
     ENSURE(ctx->tile_counter, sizeof(int));
-    int rc = ensure_iota(ctx, n);
+    ENSURE(ctx->overflow, sizeof(int));
+    int rc = ensure_iota(ctx, total);
     if (rc) return rc;
+    DepthKey dk;
+    std::memset(&dk, 0, sizeof(dk));
+    dk.overflow = P<int>(ctx->overflow);
+    if (allow_compact && !ctx->raw_depth_keys) dk = depth_key_for(ctx, cams, nview, n);
+    CK(cudaMemsetAsync(ctx->overflow.p, 0, sizeof(int), ctx->stream));
     size_t t1 = 0, t2 = 0;
-    CK(depth_sort_temp(n, &t1));
+    CK(depth_sort_temp(total, &t1));
     CK(scan_temp(total, &t2));
     ENSURE(ctx->temp, t1 > t2 ? t1 : t2);
 
     {
         Stage _st(ctx, POTR_STAGE_PREPROCESS);
-        LAUNCH(1, launch_preprocess(sp, cb, nview, g.tiles_x, all_colors ? 1 : 0,
+        LAUNCH(1, launch_preprocess(sp, cb, nview, g.tiles_x, all_colors ? 1 : 0, dk,
                                     P<SplatRec>(ctx->rec), P<uint64_t>(ctx->key),
                                     P<int32_t>(ctx->cnt), counters(ctx), ctx->stream));
         _st.end();
     }
     {
         Stage _st(ctx, POTR_STAGE_DEPTH_SORT);
-        for (int v = 0; v < nview; v++)
-            CK(depth_sort(ctx->temp.p, ctx->temp.cap, P<uint64_t>(ctx->key) + v * n,
-                          P<uint64_t>(ctx->skey) + v * n, P<int32_t>(ctx->iota),
-                          P<int32_t>(ctx->sids) + v * n, n, ctx->stream));
+        if (dk.compact) {  // one stable sort of the whole batch
+            const int end_bit = dk.nbits + bitlen((uint64_t)(nview - 1));
+            CK(depth_sort(ctx->temp.p, ctx->temp.cap, P<uint64_t>(ctx->key),
+                          P<uint64_t>(ctx->skey), P<int32_t>(ctx->iota), P<int32_t>(ctx->sids),
+                          total, end_bit, ctx->stream));
+        } else {  // raw 64-bit depth bits: one sort per view
+            for (int v = 0; v < nview; v++)
+                CK(depth_sort(ctx->temp.p, ctx->temp.cap, P<uint64_t>(ctx->key) + v * n,
+                              P<uint64_t>(ctx->skey) + v * n, P<int32_t>(ctx->iota) + v * n,
+                              P<int32_t>(ctx->sids) + v * n, n, 64, ctx->stream));
+        }
         _st.end();
     }
     {
@@ -248,8 +344,13 @@ int bin_batch(potr_ctx *ctx, const potr_splats &sp, const potr_camera *cams, int
     }
     CK(cudaMemcpyAsync(ctx->pinned, P<int64_t>(ctx->offs) + total, sizeof(int64_t),
                        cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaMemcpyAsync(ctx->pinned + 1, ctx->overflow.p, sizeof(int), cudaMemcpyDeviceToHost,
+                       ctx->stream));
     CK(cudaStreamSynchronize(ctx->stream));
+    if (dk.compact && (int)(ctx->pinned[1] & 0xffffffff) != 0)  // bound violated: exact fallback
+        return bin_batch(ctx, sp, cams, nview, all_colors, with_rank, K_out, false);
     const int64_t K = ctx->pinned[0];
+    ctx->invalid_key0 = dk.compact ? dk.sentinel : ~0ull;
     ctx->pairs_total += K;
     if (K > 0x7fffff00LL) return fail(ctx, POTR_E_ARG, "more than 2^31 tile pairs in one batch");
 
@@ -327,6 +428,8 @@ int score_views_impl(potr_ctx *ctx, const potr_splats *sp, int ncam, const potr_
                      const double *const *targets, double *imp_sum, double *cam_imp,
                      double *dmse_sum, double *mse_sum) {
     const int64_t n = sp->n;
+    int brc = compute_scene_bounds(ctx, *sp);
+    if (brc) return brc;
     for (int s = 0; s < ncam;) {
         int rc = check_cam(ctx, &cams[s]);
         if (rc) return rc;
@@ -412,6 +515,8 @@ void potr_destroy(potr_ctx *ctx) {
     if (ctx->pinned) cudaFreeHost(ctx->pinned);
     if (ctx->counters.p) cudaFree(ctx->counters.p);
     if (ctx->tile_counter.p) cudaFree(ctx->tile_counter.p);
+    if (ctx->bbox.p) cudaFree(ctx->bbox.p);
+    if (ctx->overflow.p) cudaFree(ctx->overflow.p);
     if (ctx->ci_v.p) cudaFree(ctx->ci_v.p);
     if (ctx->dm_v.p) cudaFree(ctx->dm_v.p);
     if (ctx->sid.p) cudaFree(ctx->sid.p);
@@ -494,6 +599,7 @@ int potr_render(potr_ctx *ctx, const potr_splats *splats, const potr_camera *cam
     if ((rc = check_cam(ctx, cam))) return rc;
     if (!image) return fail(ctx, POTR_E_ARG, "image is NULL");
     int64_t K = 0;
+    if ((rc = compute_scene_bounds(ctx, *splats))) return rc;
     rc = bin_batch(ctx, *splats, cam, 1, false, false, &K);
     if (rc) return rc;
     RasterArgs a = raster_args(ctx, *cam, 1);
@@ -517,6 +623,7 @@ int potr_render_records(potr_ctx *ctx, const potr_splats *splats, const potr_cam
         return fail(ctx, POTR_E_ARG, "record output pointer is NULL");
     const int64_t n = splats->n;
     int64_t K = 0;
+    if ((rc = compute_scene_bounds(ctx, *splats))) return rc;
     rc = bin_batch(ctx, *splats, cam, 1, true, true, &K);
     if (rc) return rc;
     int64_t cap = capacity > 0 ? capacity : 0;
@@ -537,8 +644,8 @@ int potr_render_records(potr_ctx *ctx, const potr_splats *splats, const potr_cam
     a.rec_p = P<double>(ctx->rp);
     LAUNCH(1, launch_raster(kRecords, a, a.ntiles, ctx->stream));
     if (colors)
-        LAUNCH(1, launch_colors_from_rec(n, P<uint64_t>(ctx->key), P<SplatRec>(ctx->rec), colors,
-                                         ctx->stream));
+        LAUNCH(1, launch_colors_from_rec(n, P<uint64_t>(ctx->key), ctx->invalid_key0,
+                                         P<SplatRec>(ctx->rec), colors, ctx->stream));
     CK(cudaMemcpyAsync(ctx->pinned, ctx->rcounter.p, sizeof(int64_t), cudaMemcpyDeviceToHost,
                        ctx->stream));
     CK(cudaStreamSynchronize(ctx->stream));
@@ -585,12 +692,14 @@ int potr_bin(potr_ctx *ctx, const potr_splats *splats, const potr_camera *cam, i
     if (rc) return rc;
     if ((rc = check_cam(ctx, cam))) return rc;
     int64_t K = 0;
+    if ((rc = compute_scene_bounds(ctx, *splats))) return rc;
     rc = bin_batch(ctx, *splats, cam, 1, false, false, &K);
     if (rc) return rc;
     *n_pairs = K;
     if (tile_splats && capacity < K) return fail(ctx, POTR_E_CAPACITY, "tile list capacity");
     ENSURE(ctx->nvalid, sizeof(unsigned long long));
-    LAUNCH(3, launch_bin_outputs(splats->n, P<uint64_t>(ctx->skey), P<int32_t>(ctx->sids),
+    LAUNCH(3, launch_bin_outputs(splats->n, P<uint64_t>(ctx->skey), ctx->invalid_key0,
+                                 P<int32_t>(ctx->sids),
                                  P<unsigned long long>(ctx->nvalid), order, geom(*cam).ntiles,
                                  P<int2>(ctx->ranges), K, tile_offsets, P<int32_t>(ctx->perm),
                                  P<int32_t>(ctx->dup_id), tile_splats, ctx->stream));
@@ -663,6 +772,21 @@ int potr_compact(potr_ctx *ctx, const potr_splats *splats, int ncam, const potr_
     if (rc) return rc;
     return potr_sh_solve(ctx, splats, P<double>(ctx->neq), lambda_y, parallel_threshold,
                          zero_threshold, rgb, ycocg, status);
+}
+
+int potr_set_option(potr_ctx *ctx, int option, int value) {
+    if (!ctx) return POTR_E_ARG;
+    switch (option) {
+        case POTR_OPT_VIEW_BATCH:
+            if (value < 1 || value > kMaxViewBatch)
+                return fail(ctx, POTR_E_ARG, "view batch must be in [1, 8]");
+            ctx->view_batch = value;
+            return POTR_OK;
+        case POTR_OPT_RAW_DEPTH_KEYS:
+            ctx->raw_depth_keys = value != 0;
+            return POTR_OK;
+    }
+    return fail(ctx, POTR_E_ARG, "unknown option");
 }
 
 int potr_profile_enable(potr_ctx *ctx, int enable) {

@@ -131,23 +131,10 @@ struct Proj {
     bool valid;
 };
 
-// project_splats for one splat (rasterizer.py:56-97, quat_to_rotmat :40-53).
-__device__ __forceinline__ Proj project_one(const double *__restrict__ p,
-                                            const double *__restrict__ s,
-                                            const double *__restrict__ q, const Cam &cam) {
-    const double *W = cam.rot;
-    double d0 = p[0] - cam.eye[0], d1 = p[1] - cam.eye[1], d2 = p[2] - cam.eye[2];
-    // (positions - eye) @ W.T: OpenBLAS accumulates with FMA in index order.
-    double t0 = fma(d2, W[2], fma(d1, W[1], d0 * W[0]));
-    double t1 = fma(d2, W[5], fma(d1, W[4], d0 * W[3]));
-    double t2 = fma(d2, W[8], fma(d1, W[7], d0 * W[6]));
-    Proj o;
-    o.valid = t2 > kNearClip;
-    double safe_z = o.valid ? t2 : 1.0;
-    double inv_z = 1.0 / safe_z;
-    o.mx = cam.fx * t0 * inv_z + cam.cx;
-    o.my = cam.fy * t1 * inv_z + cam.cy;
-
+// Sigma = R diag(s^2) R^T (rasterizer.py:75-76, quat_to_rotmat :40-53): view
+// independent, so a batch computes it once per splat.
+__device__ __forceinline__ void splat_sigma(const double *__restrict__ s,
+                                            const double *__restrict__ q, double *S) {
     double w = q[0], x = q[1], y = q[2], z = q[3];
     double R[9];
     R[0] = 1 - 2 * (y * y + z * z);
@@ -160,7 +147,6 @@ __device__ __forceinline__ Proj project_one(const double *__restrict__ p,
     R[7] = 2 * (y * z + w * x);
     R[8] = 1 - 2 * (x * x + y * y);
     double s2[3] = {s[0] * s[0], s[1] * s[1], s[2] * s[2]};
-    double S[9];
 #pragma unroll
     for (int i = 0; i < 3; i++)
 #pragma unroll
@@ -170,11 +156,33 @@ __device__ __forceinline__ Proj project_one(const double *__restrict__ p,
             for (int j = 0; j < 3; j++) acc += R[i * 3 + j] * s2[j] * R[k * 3 + j];
             S[i * 3 + k] = acc;
         }
+}
+
+// project_splats for one splat given its Sigma (rasterizer.py:64-97).  The
+// sums follow numpy's einsum order term by term; in J V J^T the terms with a
+// structural zero of J are dropped (adding them changes nothing but the sign
+// of an exact zero).
+__device__ __forceinline__ Proj project_sigma(const double *__restrict__ p,
+                                              const double *__restrict__ S, const Cam &cam) {
+    const double *W = cam.rot;
+    double d0 = p[0] - cam.eye[0], d1 = p[1] - cam.eye[1], d2 = p[2] - cam.eye[2];
+    // (positions - eye) @ W.T: OpenBLAS accumulates with FMA in index order.
+    double t0 = fma(d2, W[2], fma(d1, W[1], d0 * W[0]));
+    double t1 = fma(d2, W[5], fma(d1, W[4], d0 * W[3]));
+    double t2 = fma(d2, W[8], fma(d1, W[7], d0 * W[6]));
+    Proj o;
+    o.valid = t2 > kNearClip;
+    double safe_z = o.valid ? t2 : 1.0;
+    double inv_z = 1.0 / safe_z;
+    o.mx = cam.fx * t0 * inv_z + cam.cx;
+    o.my = cam.fy * t1 * inv_z + cam.cy;
+    // Sigma_view = W Sigma W^T, entry (i, l) = sum_j sum_k W_ij S_jk W_lk
     double V[9];
 #pragma unroll
     for (int i = 0; i < 3; i++)
 #pragma unroll
         for (int l = 0; l < 3; l++) {
+            if (i == 1 && l == 0) continue;  // unused by J V J^T
             double acc = 0.0;
 #pragma unroll
             for (int j = 0; j < 3; j++)
@@ -182,23 +190,25 @@ __device__ __forceinline__ Proj project_one(const double *__restrict__ p,
                 for (int k = 0; k < 3; k++) acc += W[i * 3 + j] * S[j * 3 + k] * W[l * 3 + k];
             V[i * 3 + l] = acc;
         }
-    double J[6] = {cam.fx * inv_z, 0.0, -cam.fx * t0 * inv_z * inv_z,
-                   0.0, cam.fy * inv_z, -cam.fy * t1 * inv_z * inv_z};
-    double C[4];
-#pragma unroll
-    for (int i = 0; i < 2; i++)
-#pragma unroll
-        for (int l = 0; l < 2; l++) {
-            double acc = 0.0;
-#pragma unroll
-            for (int j = 0; j < 3; j++)
-#pragma unroll
-                for (int k = 0; k < 3; k++) acc += J[i * 3 + j] * V[j * 3 + k] * J[l * 3 + k];
-            C[i * 2 + l] = acc;
-        }
-    o.a = C[0] + kCovDilation;
-    o.b = C[1];
-    o.c = C[3] + kCovDilation;
+    const double j00 = cam.fx * inv_z, j02 = -cam.fx * t0 * inv_z * inv_z;
+    const double j11 = cam.fy * inv_z, j12 = -cam.fy * t1 * inv_z * inv_z;
+    // cov = J V J^T with J = [[j00, 0, j02], [0, j11, j12]]
+    double c00 = 0.0, c01 = 0.0, c11 = 0.0;
+    c00 += j00 * V[0] * j00;
+    c00 += j00 * V[2] * j02;
+    c00 += j02 * V[6] * j00;
+    c00 += j02 * V[8] * j02;
+    c01 += j00 * V[1] * j11;
+    c01 += j00 * V[2] * j12;
+    c01 += j02 * V[7] * j11;
+    c01 += j02 * V[8] * j12;
+    c11 += j11 * V[4] * j11;
+    c11 += j11 * V[5] * j12;
+    c11 += j12 * V[7] * j11;
+    c11 += j12 * V[8] * j12;
+    o.a = c00 + kCovDilation;
+    o.b = c01;
+    o.c = c11 + kCovDilation;
     double mid = 0.5 * (o.a + o.c);
     double det = o.a * o.c - o.b * o.b;
     double disc = mid * mid - det;
@@ -208,6 +218,14 @@ __device__ __forceinline__ Proj project_one(const double *__restrict__ p,
     o.valid = o.valid && (o.mx >= -o.radius) && (o.mx <= cam.width + o.radius);
     o.valid = o.valid && (o.my >= -o.radius) && (o.my <= cam.height + o.radius);
     return o;
+}
+
+__device__ __forceinline__ Proj project_one(const double *__restrict__ p,
+                                            const double *__restrict__ s,
+                                            const double *__restrict__ q, const Cam &cam) {
+    double S[9];
+    splat_sigma(s, q, S);
+    return project_sigma(p, S, cam);
 }
 
 // splat_colors for one splat (rasterizer.py:100-110): SH at the unit

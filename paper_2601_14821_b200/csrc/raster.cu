@@ -35,7 +35,7 @@ namespace potr {
 // (a) preprocess
 
 __global__ void __launch_bounds__(256) k_preprocess(potr_splats sp, CamBatch cams, int nview,
-                                                     int tiles_x, int all_colors,
+                                                     int tiles_x, int all_colors, DepthKey dk,
                                                      SplatRec *__restrict__ rec,
                                                      uint64_t *__restrict__ key,
                                                      int32_t *__restrict__ cnt,
@@ -54,14 +54,29 @@ __global__ void __launch_bounds__(256) k_preprocess(potr_splats sp, CamBatch cam
     for (int i = 0; i < 4; i++) rot[i] = sp.rotations[4 * k + i];
     const double o = sp.opacities[k];
     const double pthr = log(kAlphaFloor / o) - kPowerMargin;
+    double Sig[9];
+    splat_sigma(scl, rot, Sig);
     for (int v = 0; v < nview; v++) {
         const Cam &cam = cams.cam[v];
         const int64_t g = (int64_t)v * n + k;
-        Proj pr = project_one(pos, scl, rot, cam);
+        Proj pr = project_sigma(pos, Sig, cam);
         int32_t c = 0;
-        uint64_t kk = ~0ull;
+        uint64_t kk = dk.compact ? ((uint64_t)v << dk.nbits) | dk.sentinel : ~0ull;
         if (pr.valid) {
-            kk = (uint64_t)__double_as_longlong(pr.depth);  // depth > 0.01: bits are monotone
+            // depth > 0.01 > 0: its IEEE bits are monotone in depth
+            const uint64_t bits = (uint64_t)__double_as_longlong(pr.depth);
+            if (dk.compact) {
+                // batch-wide key: view in the high bits, depth bits relative to a
+                // bound of the scene's depth range below (exact, order preserving)
+                uint64_t rel = bits >= dk.lo_bits ? bits - dk.lo_bits : 0ull;
+                if (bits < dk.lo_bits || rel >= dk.sentinel) {
+                    *dk.overflow = 1;
+                    rel = rel >= dk.sentinel ? dk.sentinel - 1 : rel;
+                }
+                kk = ((uint64_t)v << dk.nbits) | rel;
+            } else {
+                kk = bits;
+            }
             const int W = cam.width, H = cam.height;
             double x0 = floor(pr.mx - pr.radius), x1 = ceil(pr.mx + pr.radius);
             double y0 = floor(pr.my - pr.radius), y1 = ceil(pr.my + pr.radius);
@@ -130,7 +145,7 @@ __global__ void k_project_dump(potr_splats sp, Cam cam, double *mean2d, double *
 __global__ void k_gather_counts(int64_t total, int64_t n, const int32_t *__restrict__ ids,
                                 const int32_t *__restrict__ cnt, int64_t *__restrict__ out) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i < total) out[i] = cnt[(i / n) * n + ids[i]];
+    if (i < total) out[i] = cnt[ids[i]];  // ids hold batch record indices v*n + k
 }
 
 // Emit the (tile, splat) pairs of every drawn splat, walking splats in depth
@@ -146,7 +161,7 @@ __global__ void k_duplicate(int64_t total, int64_t n, const int32_t *__restrict_
     const int64_t e = offs[i + 1];
     if (o == e) return;
     const int64_t v = i / n;
-    const int32_t g = (int32_t)(v * n + ids[i]);
+    const int32_t g = ids[i];
     const SplatRec &R = rec[g];
     const int tx0 = R.x0 >> kTileWLog2, tx1 = R.x1 >> kTileWLog2;
     const int ty0 = R.y0 >> kTileHLog2, ty1 = R.y1 >> kTileHLog2;
@@ -536,7 +551,7 @@ __global__ void k_splat_reduce(int64_t total, int64_t n, const int32_t *__restri
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= total) return;
     const int64_t v = i / n;
-    const int64_t g = v * n + ids[i];
+    const int64_t g = ids[i];
     const int64_t o = offs[i], e = offs[i + 1];
     double dse = 0.0, imp = 0.0;
     for (int64_t j = o; j < e; j++) {
@@ -615,11 +630,11 @@ __global__ void k_records_gather(int64_t m, const uint64_t *__restrict__ skey,
     partials[3 * i + 2] = rp[3 * (int64_t)s + 2];
 }
 
-__global__ void k_colors_from_rec(int64_t n, const uint64_t *__restrict__ key,
+__global__ void k_colors_from_rec(int64_t n, const uint64_t *__restrict__ key, uint64_t invalid,
                                   const SplatRec *__restrict__ rec, double *colors) {
     int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (k >= n) return;
-    bool valid = key[k] != ~0ull;
+    bool valid = key[k] != invalid;
     colors[3 * k] = valid ? rec[k].cr : 0.0;
     colors[3 * k + 1] = valid ? rec[k].cg : 0.0;
     colors[3 * k + 2] = valid ? rec[k].cb : 0.0;
@@ -655,13 +670,13 @@ __global__ void k_order_out(int64_t nv, const int32_t *__restrict__ ids, int64_t
     if (r < nv) out[r] = ids[r];
 }
 
-__global__ void k_count_valid(int64_t n, const uint64_t *__restrict__ skey,
+__global__ void k_count_valid(int64_t n, const uint64_t *__restrict__ skey, uint64_t invalid,
                               unsigned long long *__restrict__ out) {
     // sorted keys: valid ones first; find the boundary
     int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (r >= n) return;
-    bool v = skey[r] != ~0ull;
-    bool next_v = (r + 1 < n) ? (skey[r + 1] != ~0ull) : false;
+    bool v = skey[r] != invalid;
+    bool next_v = (r + 1 < n) ? (skey[r + 1] != invalid) : false;
     if (v && !next_v) *out = (unsigned long long)(r + 1);
 }
 
@@ -675,11 +690,12 @@ static inline unsigned grid_for(int64_t n, int block) {
 size_t raster_smem_bytes() { return sizeof(WarpSmem) * kRasterWarps + 64 * sizeof(double2); }
 
 cudaError_t launch_preprocess(const potr_splats &sp, const CamBatch &cams, int nview,
-                              int tiles_x, int all_colors, SplatRec *rec, uint64_t *key,
-                              int32_t *cnt, unsigned long long *counters, cudaStream_t st) {
+                              int tiles_x, int all_colors, const DepthKey &dk, SplatRec *rec,
+                              uint64_t *key, int32_t *cnt, unsigned long long *counters,
+                              cudaStream_t st) {
     if (sp.n == 0) return cudaSuccess;
-    k_preprocess<<<grid_for(sp.n, 128), 128, 0, st>>>(sp, cams, nview, tiles_x, all_colors, rec,
-                                                       key, cnt, counters);
+    k_preprocess<<<grid_for(sp.n, 128), 128, 0, st>>>(sp, cams, nview, tiles_x, all_colors, dk,
+                                                       rec, key, cnt, counters);
     return cudaGetLastError();
 }
 
@@ -699,16 +715,48 @@ cudaError_t launch_iota(int64_t n, int32_t *out, cudaStream_t st) {
 }
 
 cudaError_t depth_sort(void *temp, size_t temp_bytes, const uint64_t *key, uint64_t *skey,
-                       const int32_t *iota, int32_t *sids, int64_t n, cudaStream_t st) {
+                       const int32_t *iota, int32_t *sids, int64_t n, int end_bit,
+                       cudaStream_t st) {
     if (n == 0) return cudaSuccess;
-    return cub::DeviceRadixSort::SortPairs(temp, temp_bytes, key, skey, iota, sids, (int)n, 0, 64,
-                                           st);
+    return cub::DeviceRadixSort::SortPairs(temp, temp_bytes, key, skey, iota, sids, (int)n, 0,
+                                           end_bit, st);
 }
 
 cudaError_t depth_sort_temp(int64_t n, size_t *bytes) {
     return cub::DeviceRadixSort::SortPairs((void *)nullptr, *bytes, (const uint64_t *)nullptr,
                                            (uint64_t *)nullptr, (const int32_t *)nullptr,
                                            (int32_t *)nullptr, (int)n, 0, 64);
+}
+
+__global__ void k_bbox(int64_t n, const double *__restrict__ pos,
+                       unsigned long long *__restrict__ out) {
+    // out[0..2] = ordered-int min of x,y,z; out[3..5] = ordered-int max
+    unsigned long long mn[3] = {~0ull, ~0ull, ~0ull}, mx[3] = {0ull, 0ull, 0ull};
+    for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n;
+         k += (int64_t)gridDim.x * blockDim.x) {
+#pragma unroll
+        for (int i = 0; i < 3; i++) {
+            const long long b = __double_as_longlong(pos[3 * k + i]);
+            // total order on doubles as unsigned integers
+            const unsigned long long u = b < 0 ? ~(unsigned long long)b
+                                               : ((unsigned long long)b | (1ull << 63));
+            mn[i] = u < mn[i] ? u : mn[i];
+            mx[i] = u > mx[i] ? u : mx[i];
+        }
+    }
+#pragma unroll
+    for (int i = 0; i < 3; i++) {
+        atomicMin(&out[i], mn[i]);
+        atomicMax(&out[3 + i], mx[i]);
+    }
+}
+
+cudaError_t launch_bbox(int64_t n, const double *pos, unsigned long long *out, cudaStream_t st) {
+    unsigned long long init[6] = {~0ull, ~0ull, ~0ull, 0ull, 0ull, 0ull};
+    cudaError_t e = cudaMemcpyAsync(out, init, sizeof(init), cudaMemcpyHostToDevice, st);
+    if (e != cudaSuccess || n == 0) return e;
+    k_bbox<<<296, 256, 0, st>>>(n, pos, out);
+    return cudaGetLastError();
 }
 
 cudaError_t scan_counts(void *temp, size_t temp_bytes, const int32_t *ids, const int32_t *cnt,
@@ -847,14 +895,15 @@ cudaError_t launch_records_gather(int64_t m, const uint64_t *skey, const int32_t
     return cudaGetLastError();
 }
 
-cudaError_t launch_colors_from_rec(int64_t n, const uint64_t *key, const SplatRec *rec,
-                                   double *colors, cudaStream_t st) {
+cudaError_t launch_colors_from_rec(int64_t n, const uint64_t *key, uint64_t invalid,
+                                   const SplatRec *rec, double *colors, cudaStream_t st) {
     if (n == 0) return cudaSuccess;
-    k_colors_from_rec<<<grid_for(n, 256), 256, 0, st>>>(n, key, rec, colors);
+    k_colors_from_rec<<<grid_for(n, 256), 256, 0, st>>>(n, key, invalid, rec, colors);
     return cudaGetLastError();
 }
 
-cudaError_t launch_bin_outputs(int64_t n, const uint64_t *skey, const int32_t *sids,
+cudaError_t launch_bin_outputs(int64_t n, const uint64_t *skey, uint64_t invalid,
+                               const int32_t *sids,
                                unsigned long long *nvalid_dev, int64_t *order, int ntiles,
                                const int2 *rng, int64_t K, int64_t *tile_offsets,
                                const int32_t *perm, const int32_t *dup_id, int32_t *tile_splats,
@@ -862,7 +911,7 @@ cudaError_t launch_bin_outputs(int64_t n, const uint64_t *skey, const int32_t *s
     cudaError_t e = cudaMemsetAsync(nvalid_dev, 0, sizeof(unsigned long long), st);
     if (e != cudaSuccess) return e;
     if (n > 0) {
-        k_count_valid<<<grid_for(n, 256), 256, 0, st>>>(n, skey, nvalid_dev);
+        k_count_valid<<<grid_for(n, 256), 256, 0, st>>>(n, skey, invalid, nvalid_dev);
         k_order_out<<<grid_for(n, 256), 256, 0, st>>>(n, sids, order);
     }
     if (tile_offsets) k_tile_offsets<<<grid_for(ntiles + 1, 128), 128, 0, st>>>(ntiles, rng, K,

@@ -34,16 +34,30 @@ struct RasterArgs {
 
 size_t raster_smem_bytes();
 
+// Batch-wide depth key: (view << nbits) | (depth bits - lo_bits), exact and
+// order preserving when every valid depth of the batch lies in the bound.
+struct DepthKey {
+    int compact;          // 0: raw 64-bit depth bits per view (per-view sorts)
+    int nbits;
+    uint64_t lo_bits;
+    uint64_t sentinel;    // (1 << nbits) - 1: invalid splats sort last in their view
+    int *overflow;        // set when a depth falls outside the bound
+};
+
+cudaError_t launch_bbox(int64_t n, const double *pos, unsigned long long *out, cudaStream_t st);
+
 cudaError_t launch_preprocess(const potr_splats &sp, const CamBatch &cams, int nview,
-                              int tiles_x, int all_colors, SplatRec *rec, uint64_t *key,
-                              int32_t *cnt, unsigned long long *counters, cudaStream_t st);
+                              int tiles_x, int all_colors, const DepthKey &dk, SplatRec *rec,
+                              uint64_t *key, int32_t *cnt, unsigned long long *counters,
+                              cudaStream_t st);
 cudaError_t launch_project_dump(const potr_splats &sp, const Cam &cam, double *mean2d,
                                 double *cov2d, double *depth, double *radius, uint8_t *valid,
                                 double *colors, cudaStream_t st);
 cudaError_t launch_iota(int64_t n, int32_t *out, cudaStream_t st);
 cudaError_t depth_sort_temp(int64_t n, size_t *bytes);
 cudaError_t depth_sort(void *temp, size_t temp_bytes, const uint64_t *key, uint64_t *skey,
-                       const int32_t *iota, int32_t *sids, int64_t n, cudaStream_t st);
+                       const int32_t *iota, int32_t *sids, int64_t n, int end_bit,
+                       cudaStream_t st);
 cudaError_t scan_temp(int64_t n, size_t *bytes);
 cudaError_t scan_counts(void *temp, size_t temp_bytes, const int32_t *ids, const int32_t *cnt,
                         int64_t *cnt_sorted, int64_t *offs, int64_t total, int64_t n,
@@ -75,9 +89,10 @@ cudaError_t launch_records_gather(int64_t m, const uint64_t *skey, const int32_t
                                   const double *rp, int64_t *splat_ids, int64_t *pixels,
                                   double *alphas, double *trans_at, double *partials,
                                   cudaStream_t st);
-cudaError_t launch_colors_from_rec(int64_t n, const uint64_t *key, const SplatRec *rec,
-                                   double *colors, cudaStream_t st);
-cudaError_t launch_bin_outputs(int64_t n, const uint64_t *skey, const int32_t *sids,
+cudaError_t launch_colors_from_rec(int64_t n, const uint64_t *key, uint64_t invalid,
+                                   const SplatRec *rec, double *colors, cudaStream_t st);
+cudaError_t launch_bin_outputs(int64_t n, const uint64_t *skey, uint64_t invalid,
+                               const int32_t *sids,
                                unsigned long long *nvalid_dev, int64_t *order, int ntiles,
                                const int2 *rng, int64_t K, int64_t *tile_offsets,
                                const int32_t *perm, const int32_t *dup_id, int32_t *tile_splats,

@@ -99,6 +99,31 @@ def test_forward_stats_small_scene(R):
     np.testing.assert_allclose(np.asarray(ci), g["camera_importance"], rtol=1e-12, atol=1e-20)
 
 
+@pytest.mark.parametrize("batch,raw", [(1, 0), (3, 0), (8, 1), (5, 1)])
+def test_view_batching_and_key_modes_bit_identical(R, batch, raw):
+    """Batch size and depth-key encoding never change a bit of the result."""
+    from paper_2601_14821_b200 import _native, device
+    splats, cams = small_scene()
+    g = golden("small_scene")
+    targets = [t for t in g["targets"]]
+    ref = R.compute_delta_mse(perturbed(splats), cams, targets)
+    ctx = device.context()
+    try:
+        ctx.call("potr_set_option", _native.OPT_VIEW_BATCH, batch)
+        ctx.call("potr_set_option", _native.OPT_RAW_DEPTH_KEYS, raw)
+        st = R.compute_delta_mse(perturbed(splats), cams, targets)
+        from paper_2601_14821_b200 import binning
+        order, off, lst = binning.tile_lists(splats, cams[0])
+    finally:
+        ctx.call("potr_set_option", _native.OPT_VIEW_BATCH, 8)
+        ctx.call("potr_set_option", _native.OPT_RAW_DEPTH_KEYS, 0)
+    assert np.array_equal(st.delta_mse, ref.delta_mse)
+    assert np.array_equal(st.importance, ref.importance)
+    assert np.array_equal(np.asarray(st.camera_importance), np.asarray(ref.camera_importance))
+    assert st.mse == ref.mse
+    assert np.array_equal(order, g["order0"]) and np.array_equal(lst, g["tile_splats0"])
+
+
 def test_forward_stats_bit_reproducible(R):
     splats, cams = small_scene()
     g = golden("small_scene")
