@@ -354,8 +354,13 @@ int bin_batch(potr_ctx *ctx, const potr_splats &sp, const potr_camera *cams, int
     ctx->pairs_total += K;
     if (K > 0x7fffff00LL) return fail(ctx, POTR_E_ARG, "more than 2^31 tile pairs in one batch");
 
-    ENSURE(ctx->tkey, sizeof(uint32_t) * K);
-    ENSURE(ctx->tskey, sizeof(uint32_t) * K);
+    // tile sort groups: sb views per stable sort, 16-bit keys when they fit
+    const int sb_max = 65536 / g.ntiles;
+    const bool key16 = sb_max >= 1;
+    const int sb = key16 ? (sb_max < nview ? sb_max : nview) : nview;
+    const size_t kbytes = key16 ? sizeof(uint16_t) : sizeof(uint32_t);
+    ENSURE(ctx->tkey, kbytes * K);
+    ENSURE(ctx->tskey, kbytes * K);
     ENSURE(ctx->perm, sizeof(int32_t) * K);
     ENSURE(ctx->dup_id, sizeof(int32_t) * K);
     ENSURE(ctx->sid, sizeof(int32_t) * K);
@@ -364,24 +369,41 @@ int bin_batch(potr_ctx *ctx, const potr_splats &sp, const potr_camera *cams, int
     rc = ensure_iota(ctx, K);
     if (rc) return rc;
     size_t t3 = 0;
-    CK(tile_sort_temp(K, ntiles_b, &t3));
+    CK(tile_sort_temp(K, sb * g.ntiles, key16, &t3));
     ENSURE(ctx->temp, t3);
+    // pair index where each sort group begins (pairs are view-major)
+    std::vector<int64_t> vstart(nview + 1, 0);
+    vstart[nview] = K;
+    if (nview > sb) {
+        for (int v = sb; v < nview; v += sb)
+            CK(cudaMemcpyAsync(&ctx->pinned[2 + v], P<int64_t>(ctx->offs) + (int64_t)v * n,
+                               sizeof(int64_t), cudaMemcpyDeviceToHost, ctx->stream));
+        CK(cudaStreamSynchronize(ctx->stream));
+        for (int v = sb; v < nview; v += sb) vstart[v] = ctx->pinned[2 + v];
+    }
 
     {
         Stage _st(ctx, POTR_STAGE_DUPLICATE);
         LAUNCH(1, launch_duplicate(total, n, P<int32_t>(ctx->sids), P<int64_t>(ctx->offs),
-                                   P<SplatRec>(ctx->rec), g.tiles_x, g.ntiles,
-                                   P<uint32_t>(ctx->tkey), P<int32_t>(ctx->dup_id),
+                                   P<SplatRec>(ctx->rec), g.tiles_x, g.ntiles, sb, key16,
+                                   ctx->tkey.p, P<int32_t>(ctx->dup_id),
                                    with_rank ? P<int32_t>(ctx->dup_rank) : nullptr, ctx->stream));
         _st.end();
     }
     {
         Stage _st(ctx, POTR_STAGE_TILE_SORT);
-        CK(tile_sort(ctx->temp.p, ctx->temp.cap, P<uint32_t>(ctx->tkey), P<uint32_t>(ctx->tskey),
-                     P<int32_t>(ctx->iota), P<int32_t>(ctx->perm), K, ntiles_b, ctx->stream));
-        LAUNCH(1, launch_tile_ranges(K, P<uint32_t>(ctx->tskey), P<int32_t>(ctx->perm),
-                                     P<int32_t>(ctx->dup_id), P<int32_t>(ctx->sid),
-                                     P<int2>(ctx->ranges), ntiles_b, ctx->stream));
+        CK(cudaMemsetAsync(ctx->ranges.p, 0, sizeof(int2) * (size_t)ntiles_b, ctx->stream));
+        for (int v0 = 0; v0 < nview; v0 += sb) {
+            const int v1 = v0 + sb < nview ? v0 + sb : nview;
+            const int64_t j0 = vstart[v0], kk = vstart[v1] - vstart[v0];
+            const size_t koff = kbytes * (size_t)j0;
+            CK(tile_sort(ctx->temp.p, ctx->temp.cap, key16, (const char *)ctx->tkey.p + koff,
+                         (char *)ctx->tskey.p + koff, P<int32_t>(ctx->iota) + j0,
+                         P<int32_t>(ctx->perm) + j0, kk, sb * g.ntiles, ctx->stream));
+            LAUNCH(1, launch_tile_ranges(j0, kk, key16, ctx->tskey.p, P<int32_t>(ctx->perm),
+                                         P<int32_t>(ctx->dup_id), P<int32_t>(ctx->sid),
+                                         P<int2>(ctx->ranges), v0 * g.ntiles, ctx->stream));
+        }
         _st.end();
     }
     *K_out = K;
@@ -490,7 +512,7 @@ int potr_create(int device, potr_ctx **out) {
         int b = std::atoi(vb);
         ctx->view_batch = b < 1 ? 1 : (b > kMaxViewBatch ? kMaxViewBatch : b);
     }
-    if (cudaMallocHost(&ctx->pinned, 64) != cudaSuccess) {
+    if (cudaMallocHost(&ctx->pinned, 64 * sizeof(int64_t)) != cudaSuccess) {
         delete ctx;
         return POTR_E_NOMEM;
     }

@@ -34,91 +34,90 @@ namespace potr {
 // ---------------------------------------------------------------------------
 // (a) preprocess
 
-__global__ void __launch_bounds__(256) k_preprocess(potr_splats sp, CamBatch cams, int nview,
+// One thread per (splat, view) of the batch; the views of a splat are adjacent
+// threads, so its attributes come from one cache line fetch.
+__global__ void __launch_bounds__(128) k_preprocess(potr_splats sp, CamBatch cams, int nview,
                                                      int tiles_x, int all_colors, DepthKey dk,
                                                      SplatRec *__restrict__ rec,
                                                      uint64_t *__restrict__ key,
                                                      int32_t *__restrict__ cnt,
                                                      unsigned long long *counters) {
     const int64_t n = sp.n;
-    const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (k >= n) return;
-    // the splat's attributes are read once for all views of the batch
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= n * nview) return;
+    const int64_t k = t / nview;
+    const int v = (int)(t - k * nview);
+    const Cam &cam = cams.cam[v];
+    const int64_t g = (int64_t)v * n + k;
     double pos[3], scl[3], rot[4];
 #pragma unroll
     for (int i = 0; i < 3; i++) {
-        pos[i] = sp.positions[3 * k + i];
-        scl[i] = sp.scales[3 * k + i];
+        pos[i] = __ldg(sp.positions + 3 * k + i);
+        scl[i] = __ldg(sp.scales + 3 * k + i);
     }
 #pragma unroll
-    for (int i = 0; i < 4; i++) rot[i] = sp.rotations[4 * k + i];
-    const double o = sp.opacities[k];
-    const double pthr = log(kAlphaFloor / o) - kPowerMargin;
+    for (int i = 0; i < 4; i++) rot[i] = __ldg(sp.rotations + 4 * k + i);
     double Sig[9];
     splat_sigma(scl, rot, Sig);
-    for (int v = 0; v < nview; v++) {
-        const Cam &cam = cams.cam[v];
-        const int64_t g = (int64_t)v * n + k;
-        Proj pr = project_sigma(pos, Sig, cam);
-        int32_t c = 0;
-        uint64_t kk = dk.compact ? ((uint64_t)v << dk.nbits) | dk.sentinel : ~0ull;
-        if (pr.valid) {
-            // depth > 0.01 > 0: its IEEE bits are monotone in depth
-            const uint64_t bits = (uint64_t)__double_as_longlong(pr.depth);
-            if (dk.compact) {
-                // batch-wide key: view in the high bits, depth bits relative to a
-                // bound of the scene's depth range below (exact, order preserving)
-                uint64_t rel = bits >= dk.lo_bits ? bits - dk.lo_bits : 0ull;
-                if (bits < dk.lo_bits || rel >= dk.sentinel) {
-                    *dk.overflow = 1;
-                    rel = rel >= dk.sentinel ? dk.sentinel - 1 : rel;
-                }
-                kk = ((uint64_t)v << dk.nbits) | rel;
-            } else {
-                kk = bits;
+    const Proj pr = project_sigma(pos, Sig, cam);
+    int32_t c = 0;
+    uint64_t kk = dk.compact ? ((uint64_t)v << dk.nbits) | dk.sentinel : ~0ull;
+    if (pr.valid) {
+        // depth > 0.01 > 0: its IEEE bits are monotone in depth
+        const uint64_t bits = (uint64_t)__double_as_longlong(pr.depth);
+        if (dk.compact) {
+            // batch-wide key: view in the high bits, depth bits relative to a
+            // bound of the scene's depth range below (exact, order preserving)
+            uint64_t rel = bits >= dk.lo_bits ? bits - dk.lo_bits : 0ull;
+            if (bits < dk.lo_bits || rel >= dk.sentinel) {
+                *dk.overflow = 1;
+                rel = rel >= dk.sentinel ? dk.sentinel - 1 : rel;
             }
-            const int W = cam.width, H = cam.height;
-            double x0 = floor(pr.mx - pr.radius), x1 = ceil(pr.mx + pr.radius);
-            double y0 = floor(pr.my - pr.radius), y1 = ceil(pr.my + pr.radius);
-            if (x0 < 0) x0 = 0;
-            if (y0 < 0) y0 = 0;
-            if (x1 > W - 1) x1 = W - 1;
-            if (y1 > H - 1) y1 = H - 1;
-            const double det = pr.a * pr.c - pr.b * pr.b;
-            const bool draw = !(x0 > x1 || y0 > y1) && det > 0.0;
-            if (draw || all_colors) {
-                SplatRec r;
-                r.mx = pr.mx;
-                r.my = pr.my;
-                r.ia = pr.c / det;
-                r.ib = -pr.b / det;
-                r.ic = pr.a / det;
-                r.opac = o;
-                double rgb[3];
-                splat_color(pos, sp.sh + 48 * k, cam, rgb);
-                r.cr = rgb[0];
-                r.cg = rgb[1];
-                r.cb = rgb[2];
-                r.pthr = pthr;
-                r.x0 = (int32_t)x0;
-                r.x1 = (int32_t)x1;
-                r.y0 = (int32_t)y0;
-                r.y1 = (int32_t)y1;
-                if (!draw) r.x0 = 1, r.x1 = 0;  // empty: never drawn
-                rec[g] = r;
-            }
-            if (draw) {
-                const int tx0 = (int)x0 >> kTileWLog2, tx1 = (int)x1 >> kTileWLog2;
-                const int ty0 = (int)y0 >> kTileHLog2, ty1 = (int)y1 >> kTileHLog2;
-                c = (tx1 - tx0 + 1) * (ty1 - ty0 + 1);
-                if (counters)  // E: pixels the reference loop visits (rasterizer.py:159-161)
-                    atomicAdd(&counters[0],
-                              (unsigned long long)((x1 - x0 + 1.0) * (y1 - y0 + 1.0)));
-            }
+            kk = ((uint64_t)v << dk.nbits) | rel;
+        } else {
+            kk = bits;
         }
-        key[g] = kk;
-        cnt[g] = c;
+        const int W = cam.width, H = cam.height;
+        double x0 = floor(pr.mx - pr.radius), x1 = ceil(pr.mx + pr.radius);
+        double y0 = floor(pr.my - pr.radius), y1 = ceil(pr.my + pr.radius);
+        if (x0 < 0) x0 = 0;
+        if (y0 < 0) y0 = 0;
+        if (x1 > W - 1) x1 = W - 1;
+        if (y1 > H - 1) y1 = H - 1;
+        const double det = pr.a * pr.c - pr.b * pr.b;
+        const bool draw = !(x0 > x1 || y0 > y1) && det > 0.0;
+        if (draw || all_colors) {
+            const double o = __ldg(sp.opacities + k);
+            SplatRec r;
+            r.mx = pr.mx;
+            r.my = pr.my;
+            r.ia = pr.c / det;
+            r.ib = -pr.b / det;
+            r.ic = pr.a / det;
+            r.opac = o;
+            double rgb[3];
+            splat_color(pos, sp.sh + 48 * k, cam, rgb);
+            r.cr = rgb[0];
+            r.cg = rgb[1];
+            r.cb = rgb[2];
+            r.pthr = log(kAlphaFloor / o) - kPowerMargin;
+            r.x0 = (int32_t)x0;
+            r.x1 = (int32_t)x1;
+            r.y0 = (int32_t)y0;
+            r.y1 = (int32_t)y1;
+            if (!draw) r.x0 = 1, r.x1 = 0;  // empty: never drawn
+            rec[g] = r;
+        }
+        if (draw) {
+            const int tx0 = (int)x0 >> kTileWLog2, tx1 = (int)x1 >> kTileWLog2;
+            const int ty0 = (int)y0 >> kTileHLog2, ty1 = (int)y1 >> kTileHLog2;
+            c = (tx1 - tx0 + 1) * (ty1 - ty0 + 1);
+            if (counters)  // E: pixels the reference loop visits (rasterizer.py:159-161)
+                atomicAdd(&counters[0], (unsigned long long)((x1 - x0 + 1.0) * (y1 - y0 + 1.0)));
+        }
     }
+    key[g] = kk;
+    cnt[g] = c;
 }
 
 // project_splats / splat_colors dump for parity tests (potr_project).
@@ -150,10 +149,13 @@ __global__ void k_gather_counts(int64_t total, int64_t n, const int32_t *__restr
 
 // Emit the (tile, splat) pairs of every drawn splat, walking splats in depth
 // order so a stable sort on the tile key yields (tile, depth, id) order.
-// Tile keys are batch-global: v * ntiles + ty * tiles_x + tx.
+// Views are sorted in groups of `sb`; a pair's key is its tile index inside
+// its group, (v % sb) * ntiles + ty * tiles_x + tx, which fits 16 bits
+// whenever sb * ntiles <= 65536 (halving the sort's key traffic).
+template <typename KeyT>
 __global__ void k_duplicate(int64_t total, int64_t n, const int32_t *__restrict__ ids,
                             const int64_t *__restrict__ offs, const SplatRec *__restrict__ rec,
-                            int tiles_x, int ntiles, uint32_t *__restrict__ tkey,
+                            int tiles_x, int ntiles, int sb, KeyT *__restrict__ tkey,
                             int32_t *__restrict__ dup_gid, int32_t *__restrict__ dup_rank) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= total) return;
@@ -165,27 +167,31 @@ __global__ void k_duplicate(int64_t total, int64_t n, const int32_t *__restrict_
     const SplatRec &R = rec[g];
     const int tx0 = R.x0 >> kTileWLog2, tx1 = R.x1 >> kTileWLog2;
     const int ty0 = R.y0 >> kTileHLog2, ty1 = R.y1 >> kTileHLog2;
-    const uint32_t tbase = (uint32_t)(v * ntiles);
+    const uint32_t tbase = (uint32_t)((v % sb) * ntiles);
     for (int ty = ty0; ty <= ty1; ty++)
         for (int tx = tx0; tx <= tx1; tx++) {
-            tkey[o] = tbase + (uint32_t)(ty * tiles_x + tx);
+            tkey[o] = (KeyT)(tbase + (uint32_t)(ty * tiles_x + tx));
             dup_gid[o] = g;
             if (dup_rank) dup_rank[o] = (int32_t)(i - v * n);
             o++;
         }
 }
 
-// Tile [start, end) ranges of the sorted pairs, plus each sorted pair's splat
-// id (so the rasterizer's chunk fetch is two loads deep, not three).
-__global__ void k_tile_ranges(int64_t K, const uint32_t *__restrict__ skey,
+// Tile [start, end) ranges of the sorted pairs of one sort group (pairs
+// [j0, j0 + K) carrying group-local keys; tile index = tbase + key), plus each
+// sorted pair's record index (so the rasterizer's chunk fetch is two loads
+// deep, not three).
+template <typename KeyT>
+__global__ void k_tile_ranges(int64_t j0, int64_t K, const KeyT *__restrict__ skey,
                               const int32_t *__restrict__ perm, const int32_t *__restrict__ dup_id,
-                              int32_t *__restrict__ sid, int2 *__restrict__ rng) {
-    int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (j >= K) return;
+                              int32_t *__restrict__ sid, int2 *__restrict__ rng, int tbase) {
+    const int64_t jj = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (jj >= K) return;
+    const int64_t j = j0 + jj;
     sid[j] = dup_id[perm[j]];
-    uint32_t t = skey[j];
-    if (j == 0 || skey[j - 1] != t) rng[t].x = (int)j;
-    if (j == K - 1 || skey[j + 1] != t) rng[t].y = (int)(j + 1);
+    const uint32_t t = skey[j];
+    if (jj == 0 || skey[j - 1] != t) rng[tbase + t].x = (int)j;
+    if (jj == K - 1 || skey[j + 1] != t) rng[tbase + t].y = (int)(j + 1);
 }
 
 __global__ void k_iota(int64_t n, int32_t *out) {
@@ -694,8 +700,9 @@ cudaError_t launch_preprocess(const potr_splats &sp, const CamBatch &cams, int n
                               uint64_t *key, int32_t *cnt, unsigned long long *counters,
                               cudaStream_t st) {
     if (sp.n == 0) return cudaSuccess;
-    k_preprocess<<<grid_for(sp.n, 128), 128, 0, st>>>(sp, cams, nview, tiles_x, all_colors, dk,
-                                                       rec, key, cnt, counters);
+    k_preprocess<<<grid_for(sp.n * nview, 128), 128, 0, st>>>(sp, cams, nview, tiles_x,
+                                                               all_colors, dk, rec, key, cnt,
+                                                               counters);
     return cudaGetLastError();
 }
 
@@ -775,11 +782,15 @@ cudaError_t scan_temp(int64_t n, size_t *bytes) {
 }
 
 cudaError_t launch_duplicate(int64_t total, int64_t n, const int32_t *ids, const int64_t *offs,
-                             const SplatRec *rec, int tiles_x, int ntiles, uint32_t *tkey,
-                             int32_t *dup_gid, int32_t *dup_rank, cudaStream_t st) {
+                             const SplatRec *rec, int tiles_x, int ntiles, int sb, bool key16,
+                             void *tkey, int32_t *dup_gid, int32_t *dup_rank, cudaStream_t st) {
     if (total == 0) return cudaSuccess;
-    k_duplicate<<<grid_for(total, 256), 256, 0, st>>>(total, n, ids, offs, rec, tiles_x, ntiles,
-                                                       tkey, dup_gid, dup_rank);
+    if (key16)
+        k_duplicate<uint16_t><<<grid_for(total, 256), 256, 0, st>>>(
+            total, n, ids, offs, rec, tiles_x, ntiles, sb, (uint16_t *)tkey, dup_gid, dup_rank);
+    else
+        k_duplicate<uint32_t><<<grid_for(total, 256), 256, 0, st>>>(
+            total, n, ids, offs, rec, tiles_x, ntiles, sb, (uint32_t *)tkey, dup_gid, dup_rank);
     return cudaGetLastError();
 }
 
@@ -789,17 +800,26 @@ static int bits_for(int ntiles) {
     return b;
 }
 
-cudaError_t tile_sort(void *temp, size_t temp_bytes, const uint32_t *tkey, uint32_t *skey,
-                      const int32_t *iota, int32_t *perm, int64_t K, int ntiles, cudaStream_t st) {
+cudaError_t tile_sort(void *temp, size_t temp_bytes, bool key16, const void *tkey, void *skey,
+                      const int32_t *iota, int32_t *perm, int64_t K, int nkeys, cudaStream_t st) {
     if (K == 0) return cudaSuccess;
-    return cub::DeviceRadixSort::SortPairs(temp, temp_bytes, tkey, skey, iota, perm, (int)K, 0,
-                                           bits_for(ntiles), st);
+    if (key16)
+        return cub::DeviceRadixSort::SortPairs(temp, temp_bytes, (const uint16_t *)tkey,
+                                               (uint16_t *)skey, iota, perm, (int)K, 0,
+                                               bits_for(nkeys), st);
+    return cub::DeviceRadixSort::SortPairs(temp, temp_bytes, (const uint32_t *)tkey,
+                                           (uint32_t *)skey, iota, perm, (int)K, 0,
+                                           bits_for(nkeys), st);
 }
 
-cudaError_t tile_sort_temp(int64_t K, int ntiles, size_t *bytes) {
+cudaError_t tile_sort_temp(int64_t K, int nkeys, bool key16, size_t *bytes) {
+    if (key16)
+        return cub::DeviceRadixSort::SortPairs((void *)nullptr, *bytes, (const uint16_t *)nullptr,
+                                               (uint16_t *)nullptr, (const int32_t *)nullptr,
+                                               (int32_t *)nullptr, (int)K, 0, bits_for(nkeys));
     return cub::DeviceRadixSort::SortPairs((void *)nullptr, *bytes, (const uint32_t *)nullptr,
                                            (uint32_t *)nullptr, (const int32_t *)nullptr,
-                                           (int32_t *)nullptr, (int)K, 0, bits_for(ntiles));
+                                           (int32_t *)nullptr, (int)K, 0, bits_for(nkeys));
 }
 
 cudaError_t records_sort_temp(int64_t m, size_t *bytes) {
@@ -815,12 +835,16 @@ cudaError_t records_sort(void *temp, size_t temp_bytes, const uint64_t *key, uin
                                            st);
 }
 
-cudaError_t launch_tile_ranges(int64_t K, const uint32_t *skey, const int32_t *perm,
-                               const int32_t *dup_id, int32_t *sid, int2 *rng, int ntiles,
-                               cudaStream_t st) {
-    cudaError_t e = cudaMemsetAsync(rng, 0, sizeof(int2) * (size_t)ntiles, st);
-    if (e != cudaSuccess || K == 0) return e;
-    k_tile_ranges<<<grid_for(K, 256), 256, 0, st>>>(K, skey, perm, dup_id, sid, rng);
+cudaError_t launch_tile_ranges(int64_t j0, int64_t K, bool key16, const void *skey,
+                               const int32_t *perm, const int32_t *dup_id, int32_t *sid,
+                               int2 *rng, int tbase, cudaStream_t st) {
+    if (K == 0) return cudaSuccess;
+    if (key16)
+        k_tile_ranges<uint16_t><<<grid_for(K, 256), 256, 0, st>>>(
+            j0, K, (const uint16_t *)skey, perm, dup_id, sid, rng, tbase);
+    else
+        k_tile_ranges<uint32_t><<<grid_for(K, 256), 256, 0, st>>>(
+            j0, K, (const uint32_t *)skey, perm, dup_id, sid, rng, tbase);
     return cudaGetLastError();
 }
 

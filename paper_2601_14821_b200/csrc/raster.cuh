@@ -63,17 +63,17 @@ cudaError_t scan_counts(void *temp, size_t temp_bytes, const int32_t *ids, const
                         int64_t *cnt_sorted, int64_t *offs, int64_t total, int64_t n,
                         cudaStream_t st);
 cudaError_t launch_duplicate(int64_t total, int64_t n, const int32_t *ids, const int64_t *offs,
-                             const SplatRec *rec, int tiles_x, int ntiles, uint32_t *tkey,
-                             int32_t *dup_gid, int32_t *dup_rank, cudaStream_t st);
-cudaError_t tile_sort_temp(int64_t K, int ntiles, size_t *bytes);
-cudaError_t tile_sort(void *temp, size_t temp_bytes, const uint32_t *tkey, uint32_t *skey,
-                      const int32_t *iota, int32_t *perm, int64_t K, int ntiles, cudaStream_t st);
+                             const SplatRec *rec, int tiles_x, int ntiles, int sb, bool key16,
+                             void *tkey, int32_t *dup_gid, int32_t *dup_rank, cudaStream_t st);
+cudaError_t tile_sort_temp(int64_t K, int nkeys, bool key16, size_t *bytes);
+cudaError_t tile_sort(void *temp, size_t temp_bytes, bool key16, const void *tkey, void *skey,
+                      const int32_t *iota, int32_t *perm, int64_t K, int nkeys, cudaStream_t st);
 cudaError_t records_sort_temp(int64_t m, size_t *bytes);
 cudaError_t records_sort(void *temp, size_t temp_bytes, const uint64_t *key, uint64_t *skey,
                          const int32_t *iota, int32_t *sidx, int64_t m, cudaStream_t st);
-cudaError_t launch_tile_ranges(int64_t K, const uint32_t *skey, const int32_t *perm,
-                               const int32_t *dup_id, int32_t *sid, int2 *rng, int ntiles,
-                               cudaStream_t st);
+cudaError_t launch_tile_ranges(int64_t j0, int64_t K, bool key16, const void *skey,
+                               const int32_t *perm, const int32_t *dup_id, int32_t *sid,
+                               int2 *rng, int tbase, cudaStream_t st);
 cudaError_t launch_raster(int mode, const RasterArgs &a, int ntiles, cudaStream_t st);
 cudaError_t launch_splat_reduce(int64_t total, int64_t n, const int32_t *ids, const int64_t *offs,
                                 const double2 *partial, double P, double *cam_imp_rows,
