@@ -464,8 +464,7 @@ int score_views_impl(potr_ctx *ctx, const potr_splats *sp, int ncam, const potr_
         ViewGeom g = geom(cams[s]);
         RasterArgs a = raster_args(ctx, cams[s], nb);
         for (int v = 0; v < nb; v++) a.target[v] = targets ? targets[s + v] : nullptr;
-        ENSURE(ctx->ci_v, sizeof(double) * n * nb);
-        if (targets) ENSURE(ctx->dm_v, sizeof(double) * n * nb);
+        ENSURE(ctx->ci_v, sizeof(double2) * n * nb);
         {
             Stage _st(ctx, POTR_STAGE_RASTER);
             LAUNCH(1, launch_raster(targets ? kScore : kImportance, a, a.ntiles, ctx->stream));
@@ -474,12 +473,10 @@ int score_views_impl(potr_ctx *ctx, const potr_splats *sp, int ncam, const potr_
         {
             Stage _st(ctx, POTR_STAGE_REDUCE);
             LAUNCH(1, launch_splat_reduce(n * nb, n, P<int32_t>(ctx->sids), P<int64_t>(ctx->offs),
-                                          P<double2>(ctx->partial), g.P,
-                                          cam_imp ? cam_imp + (int64_t)s * n : nullptr,
-                                          P<double>(ctx->ci_v),
-                                          targets ? P<double>(ctx->dm_v) : nullptr, ctx->stream));
-            LAUNCH(1, launch_view_accumulate(n, nb, P<double>(ctx->ci_v),
-                                             targets ? P<double>(ctx->dm_v) : nullptr, imp_sum,
+                                          P<double2>(ctx->partial), g.P, P<double2>(ctx->ci_v),
+                                          ctx->stream));
+            LAUNCH(1, launch_view_accumulate(n, nb, P<double2>(ctx->ci_v),
+                                             cam_imp ? cam_imp + (int64_t)s * n : nullptr, imp_sum,
                                              targets ? dmse_sum : nullptr, ctx->stream));
             if (targets)
                 LAUNCH(1, launch_mse_reduce(nb, g.ntiles, P<double>(ctx->tile_se), g.P, mse_sum,

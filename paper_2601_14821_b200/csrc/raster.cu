@@ -548,43 +548,65 @@ __global__ void __launch_bounds__(32 * kRasterWarps, POTR_RASTER_MIN_BLOCKS) k_r
 }
 
 // Per (view, splat): sum of its (tile, splat) slots in tile order
-// (deterministic), normalised by P and 3P (rasterizer.py:230, :334).
-__global__ void k_splat_reduce(int64_t total, int64_t n, const int32_t *__restrict__ ids,
-                               const int64_t *__restrict__ offs,
-                               const double2 *__restrict__ partial, double P,
-                               double *__restrict__ cam_imp_rows, double *__restrict__ ci_out,
-                               double *__restrict__ dm_out) {
-    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= total) return;
-    const int64_t v = i / n;
-    const int64_t g = ids[i];
-    const int64_t o = offs[i], e = offs[i + 1];
+// (deterministic), normalised by P and 3P (rasterizer.py:230, :334).  A warp
+// takes 32 consecutive (view, rank) entries, whose slots are one contiguous
+// range: it stages that range in shared memory with coalesced loads, then
+// each lane sums its own entry's slots in order.
+constexpr int kReduceStage = 256;  // slots staged per warp
+
+__global__ void __launch_bounds__(256) k_splat_reduce(int64_t total, int64_t n,
+                                                      const int32_t *__restrict__ ids,
+                                                      const int64_t *__restrict__ offs,
+                                                      const double2 *__restrict__ partial,
+                                                      double P, double2 *__restrict__ vals) {
+    __shared__ double2 stage[8][kReduceStage];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int64_t i0 = ((int64_t)blockIdx.x * 8 + w) * 32;
+    if (i0 >= total) return;
+    const int64_t i = i0 + lane;
+    const bool act = i < total;
+    const int64_t o = act ? offs[i] : 0, e = act ? offs[i + 1] : 0;
+    const int64_t base = __shfl_sync(0xffffffffu, o, 0);
+    const int64_t last = total - i0 < 32 ? total - i0 - 1 : 31;
+    const int64_t top = __shfl_sync(0xffffffffu, e, (int)last);
     double dse = 0.0, imp = 0.0;
-    for (int64_t j = o; j < e; j++) {
-        const double2 x = partial[j];
-        dse += x.x;
-        imp += x.y;
+    if (top - base <= kReduceStage) {
+        for (int64_t j = base + lane; j < top; j += 32) stage[w][j - base] = partial[j];
+        __syncwarp();
+        for (int64_t j = o; j < e; j++) {
+            const double2 x = stage[w][j - base];
+            dse += x.x;
+            imp += x.y;
+        }
+    } else {
+        for (int64_t j = o; j < e; j++) {
+            const double2 x = partial[j];
+            dse += x.x;
+            imp += x.y;
+        }
     }
-    const double ci = imp / P;
-    ci_out[g] = ci;
-    if (cam_imp_rows) cam_imp_rows[g] = ci;
-    if (dm_out) dm_out[g] = dse / (P * 3.0);
+    if (!act) return;
+    // one 16-byte scatter per (view, splat): (I_k(s), dMSE_k(s)) by record index
+    vals[ids[i]] = make_double2(imp / P, dse / (P * 3.0));
 }
 
-// Camera-ordered accumulation over the views of the batch (rasterizer.py:343-347).
-__global__ void k_view_accumulate(int64_t n, int nview, const double *__restrict__ ci,
-                                  const double *__restrict__ dm, double *__restrict__ imp_acc,
+// Camera-ordered accumulation over the views of the batch (rasterizer.py:343-347),
+// writing the camera_importance rows on the way (coalesced, by splat id).
+__global__ void k_view_accumulate(int64_t n, int nview, const double2 *__restrict__ vals,
+                                  double *__restrict__ cam_imp_rows, double *__restrict__ imp_acc,
                                   double *__restrict__ dmse_acc) {
     const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (k >= n) return;
     double ia = imp_acc[k];
-    double da = dm ? dmse_acc[k] : 0.0;
+    double da = dmse_acc ? dmse_acc[k] : 0.0;
     for (int v = 0; v < nview; v++) {
-        ia += ci[(int64_t)v * n + k];
-        if (dm) da += dm[(int64_t)v * n + k];
+        const double2 x = vals[(int64_t)v * n + k];
+        if (cam_imp_rows) cam_imp_rows[(int64_t)v * n + k] = x.x;
+        ia += x.x;
+        da += x.y;
     }
     imp_acc[k] = ia;
-    if (dm) dmse_acc[k] = da;
+    if (dmse_acc) dmse_acc[k] = da;
 }
 
 // Per view, the sum of its tiles' squared errors; mse(s) = sum / 3P (:335),
@@ -880,18 +902,20 @@ cudaError_t launch_raster(int mode, const RasterArgs &a, int ntiles, cudaStream_
 }
 
 cudaError_t launch_splat_reduce(int64_t total, int64_t n, const int32_t *ids, const int64_t *offs,
-                                const double2 *partial, double P, double *cam_imp_rows,
-                                double *ci_out, double *dm_out, cudaStream_t st) {
+                                const double2 *partial, double P, double2 *vals,
+                                cudaStream_t st) {
     if (total == 0) return cudaSuccess;
-    k_splat_reduce<<<grid_for(total, 256), 256, 0, st>>>(total, n, ids, offs, partial, P,
-                                                          cam_imp_rows, ci_out, dm_out);
+    k_splat_reduce<<<grid_for(total, 256), 256, 0, st>>>(total, n, ids, offs, partial, P, vals);
+    // (one warp per 32 entries, 8 warps per block: grid_for(total, 256) blocks)
     return cudaGetLastError();
 }
 
-cudaError_t launch_view_accumulate(int64_t n, int nview, const double *ci, const double *dm,
-                                   double *imp_acc, double *dmse_acc, cudaStream_t st) {
+cudaError_t launch_view_accumulate(int64_t n, int nview, const double2 *vals,
+                                   double *cam_imp_rows, double *imp_acc, double *dmse_acc,
+                                   cudaStream_t st) {
     if (n == 0) return cudaSuccess;
-    k_view_accumulate<<<grid_for(n, 256), 256, 0, st>>>(n, nview, ci, dm, imp_acc, dmse_acc);
+    k_view_accumulate<<<grid_for(n, 256), 256, 0, st>>>(n, nview, vals, cam_imp_rows, imp_acc,
+                                                         dmse_acc);
     return cudaGetLastError();
 }
 
