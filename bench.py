@@ -147,19 +147,19 @@ def load_peaks():
         return {"hbm_gbs": FALLBACK_HBM_GBS, "sm_max_mhz": 1965.0}, "fallback"
 
 
-# FLOP model of the reference's per-pixel arithmetic:
-#   live bbox evaluation (rasterizer.py:165-171): dx 1, power 9, o*exp 1 -> 11 + 1 exp
-#   contribution, forward (:197-201): 9
-#   contribution, removal effect (:226-243, :333-334): 34
-FLOP_LIVE_EVAL = 11
-FLOP_EXP = 1
-FLOP_CONTRIB = 9 + 34
+# Work model of the fused raster + removal-effect kernel: SURVEY.md section 8(d),
+# per view W = 24 E + 37 M lane-ops + 2 E exp, an fp64 exp costing ~20 DFMA
+# ("fp64 parity mode"), i.e. W = 64 E + 37 M FP64 lane-ops (FMA = 1), with
+#   E = bbox pixel evaluations of the reference loop (rasterizer.py:159-166),
+#   M = composited contributions (:170-201).
+OPS_PER_E = 24 + 2 * 20
+OPS_PER_M = 37
 
 
-def fp64_peak_tflops(peaks):
-    # B200: 148 SMs x 64 FP64 FMA/clk (2 flops) at the max SM clock -- nominal,
-    # MEASURED_PEAKS.json has no FP64 CUDA-core figure.
-    return 148 * 64 * 2 * float(peaks.get("sm_max_mhz", 1965.0)) * 1e6 / 1e12
+def fp64_peak_lane_ops(peaks):
+    # B200: 148 SMs x 64 FP64 lanes/clk at the max SM clock -- nominal; the
+    # MEASURED_PEAKS.json figures are HBM copy and bf16 tensor only.
+    return 148 * 64 * float(peaks.get("sm_max_mhz", 1965.0)) * 1e6 / 1e12
 
 
 # ---------------------------------------------------------------------------
@@ -278,12 +278,7 @@ def main():
     n = ds.n
 
     # targets of this rank's views, rendered on the GPU and kept resident
-    tg = []
-    for cam in my_cams:
-        img = torch.empty((H, W, 3), dtype=torch.float64, device=dev)
-        ctx.call("potr_render", ctypes.byref(ds_ref.struct()),
-                 ctypes.byref(_native_cam(cam)), D.ptr(img), None)
-        tg.append(img)
+    tg = rasterizer.render_targets_device(ds_ref, my_cams)
     del ds_ref
     tptr = (ctypes.c_void_p * max(1, len(tg)))(*[t.data_ptr() for t in tg])
     cam_arr = _native_cams(my_cams)
@@ -352,14 +347,18 @@ def main():
     step_ms_sum = sum(v[0] for v in prof.values())
     E, E_live, M, K = counts
     views_here = max(1, hi - lo)
-    flop_per_launch = (E_live * (FLOP_LIVE_EVAL + FLOP_EXP) + M * FLOP_CONTRIB) / views_here
+    views_per_launch = views_here / max(1, raster_n / args.steps)
+    ops_per_launch = (E * OPS_PER_E + M * OPS_PER_M) / views_here * views_per_launch
     raster_avg_ms = raster_ms / max(1, raster_n)
-    achieved = flop_per_launch / (raster_avg_ms / 1000.0) / 1e12
-    peak = fp64_peak_tflops(peaks)
+    achieved = ops_per_launch / (raster_avg_ms / 1000.0) / 1e12
+    peak = fp64_peak_lane_ops(peaks)
     roofline = {"bound": "fp64", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                 "frac": achieved / peak, "traffic": None, "kernel": "k_raster<kScore>",
-                "peak_source": "nominal FP64 CUDA-core rate at sm_max_mhz (148 SMs x 64 DFMA/clk);"
+                "unit_note": "FP64 lane-operations per second, FMA = 1 (SURVEY.md 8(d) model: "
+                             "W = 24E + 37M + 2E exp at 20 DFMA each, per view)",
+                "peak_source": "nominal FP64 CUDA-core rate at sm_max_mhz (148 SMs x 64 lanes/clk);"
                                " MEASURED_PEAKS.json has only HBM and bf16 tensor peaks",
+                "views_per_launch": views_per_launch,
                 "raster_share_of_step": raster_ms / step_ms_sum if step_ms_sum else None,
                 "per_view": {"E_bbox_evals": E / views_here, "E_live": E_live / views_here,
                              "M_contributions": M / views_here, "tile_pairs": K / views_here},
@@ -493,9 +492,9 @@ def scene_measure(args, world, ds, cams, my_cams, tptr, cam_arr, lo, hi, ctx, de
         if world > 1:
             dist.barrier()
         t0 = time.perf_counter()
-        for cam, img in zip(my_cams, imgs):
-            ctx.call("potr_render", ctypes.byref(ds0.struct()), ctypes.byref(_native_cam(cam)),
-                     D.ptr(img), None)
+        iptr = (ctypes.c_void_p * max(1, len(imgs)))(*[t.data_ptr() for t in imgs])
+        ctx.call("potr_render_batch", ctypes.byref(ds0.struct()), len(my_cams),
+                 _native_cams(my_cams), iptr, None)
         torch.cuda.synchronize()
         t1 = time.perf_counter()
         imp.zero_(), dm.zero_(), mse.zero_()

@@ -100,6 +100,11 @@ int potr_finalize_stats(potr_ctx *ctx, int64_t n, int total_cams, double *imp_su
 int potr_render(potr_ctx *ctx, const potr_splats *splats, const potr_camera *cam,
                 double *image, double *trans);
 
+/* render_targets (rasterizer.py:371-377): ncam views, batched; images and
+ * trans are host arrays of ncam device pointers (trans nullable). */
+int potr_render_batch(potr_ctx *ctx, const potr_splats *splats, int ncam,
+                      const potr_camera *cams, double *const *images, double *const *trans);
+
 /* render_with_records (rasterizer.py:246-267).  Two-call protocol: call with
  * capacity 0 to get *n_records (synchronizes), then with buffers of that
  * capacity.  Records are in the reference's order (depth order of the splat,

@@ -70,6 +70,9 @@ _SIGNATURES = {
                                            ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]),
     "potr_render": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(PotrSplats),
                                    ctypes.POINTER(PotrCamera), ctypes.c_void_p, ctypes.c_void_p]),
+    "potr_render_batch": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(PotrSplats), ctypes.c_int,
+                                         ctypes.POINTER(PotrCamera), ctypes.c_void_p,
+                                         ctypes.c_void_p]),
     "potr_render_records": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(PotrSplats),
                                            ctypes.POINTER(PotrCamera), ctypes.c_void_p,
                                            ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64,

@@ -609,23 +609,44 @@ int potr_forward_stats(potr_ctx *ctx, const potr_splats *splats, int ncam,
                                targets ? mse : nullptr);
 }
 
-int potr_render(potr_ctx *ctx, const potr_splats *splats, const potr_camera *cam, double *image,
-                double *trans) {
+int potr_render_batch(potr_ctx *ctx, const potr_splats *splats, int ncam, const potr_camera *cams,
+                      double *const *images, double *const *trans) {
     if (!ctx) return POTR_E_ARG;
     CK(cudaSetDevice(ctx->device));
     int rc = check_splats(ctx, splats);
     if (rc) return rc;
-    if ((rc = check_cam(ctx, cam))) return rc;
-    if (!image) return fail(ctx, POTR_E_ARG, "image is NULL");
-    int64_t K = 0;
+    if (ncam < 0 || (ncam > 0 && (!cams || !images)))
+        return fail(ctx, POTR_E_ARG, "bad camera / image list");
+    if (ncam == 0) return POTR_OK;
     if ((rc = compute_scene_bounds(ctx, *splats))) return rc;
-    rc = bin_batch(ctx, *splats, cam, 1, false, false, &K);
-    if (rc) return rc;
-    RasterArgs a = raster_args(ctx, *cam, 1);
-    a.image[0] = image;
-    a.trans[0] = trans;
-    LAUNCH(1, launch_raster(kRender, a, a.ntiles, ctx->stream));
+    for (int s = 0; s < ncam;) {
+        if ((rc = check_cam(ctx, &cams[s]))) return rc;
+        const int nb = batch_len(ctx, cams, s, ncam, splats->n);
+        for (int v = 0; v < nb; v++)
+            if (!images[s + v]) return fail(ctx, POTR_E_ARG, "image pointer is NULL");
+        int64_t K = 0;
+        rc = bin_batch(ctx, *splats, cams + s, nb, false, false, &K);
+        if (rc) return rc;
+        RasterArgs a = raster_args(ctx, cams[s], nb);
+        for (int v = 0; v < nb; v++) {
+            a.image[v] = images[s + v];
+            a.trans[v] = trans ? trans[s + v] : nullptr;
+        }
+        {
+            Stage _st(ctx, POTR_STAGE_RASTER);
+            LAUNCH(1, launch_raster(kRender, a, a.ntiles, ctx->stream));
+            _st.end();
+        }
+        s += nb;
+    }
     return POTR_OK;
+}
+
+int potr_render(potr_ctx *ctx, const potr_splats *splats, const potr_camera *cam, double *image,
+                double *trans) {
+    if (!ctx) return POTR_E_ARG;
+    if (!image) return fail(ctx, POTR_E_ARG, "image is NULL");
+    return potr_render_batch(ctx, splats, 1, cam, &image, trans ? &trans : nullptr);
 }
 
 int potr_render_records(potr_ctx *ctx, const potr_splats *splats, const potr_camera *cam,

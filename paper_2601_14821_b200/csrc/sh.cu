@@ -27,84 +27,130 @@ __device__ __forceinline__ int tri(int i, int j) { return i * 16 - (i * (i - 1))
 __constant__ double kRgbToYcocg[9] = {0.25, 0.5, 0.25, 0.5, 0.0, -0.5, -0.25, 0.5, -0.25};
 __constant__ double kYcocgToRgb[9] = {1.0, 1.0, -1.0, 1.0, 0.0, 1.0, 1.0, -1.0, -1.0};
 
-__global__ void __launch_bounds__(256) k_sh_accumulate(potr_splats sp, int ncam,
+// Normal equations of 16 consecutive splats per CTA (4 warps x 4 splats).  Views are taken 32 at a
+// time: the (view, splat) tile of camera_importance is staged in shared
+// memory with coalesced loads; then for each splat a warp evaluates one view
+// per lane (direction, SH basis, raw colour, YCoCg -- compaction.py:100-107),
+// publishes (w*y, w*YCoCg(colour)) to shared memory, and every lane adds the
+// 32 views, in ascending order, into the ~6 of the 184 entries it owns
+// (G_ij += (w y_i)(w y_j), B_ic += (w y_i)(w c_c)).  Views a splat is not seen
+// from have w = 0 and add exact zeros, so the sums equal the reference's sums
+// over its `seen` rows (compaction.py:97-107, :114, :133-137).
+constexpr int kShSplatsPerBlock = 16;
+constexpr int kShWarps = 4;
+constexpr int kShRow = 19;  // w*y (16) + w*YCoCg (3)
+
+__global__ void __launch_bounds__(32 * kShWarps, 4) k_sh_accumulate(potr_splats sp, int ncam,
                                                        const double *__restrict__ eyes,
                                                        const double *__restrict__ cam_imp,
                                                        double *__restrict__ neq) {
+    __shared__ double wtile[32][kShSplatsPerBlock + 1];
+    __shared__ double A[kShWarps][32][kShRow];
+    __shared__ double shs[kShSplatsPerBlock][48];
+    __shared__ double pos[kShSplatsPerBlock][3];
     const int64_t n = sp.n;
-    const int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    const int64_t k = gid >> 3;
-    const int g = threadIdx.x & 7;
-    const unsigned gmask = 0xffu << (threadIdx.x & 24);
-    const bool active = k < n;
-    const int64_t kk = active ? k : 0;
-    if (n == 0) return;
-    const double px = sp.positions[3 * kk], py = sp.positions[3 * kk + 1],
-                 pz = sp.positions[3 * kk + 2];
-    const int ch = g < 3 ? g : 0;
-    double shc[16];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int64_t k0 = (int64_t)blockIdx.x * kShSplatsPerBlock;
+    const int nk = (int)(n - k0 < kShSplatsPerBlock ? n - k0 : kShSplatsPerBlock);
+    for (int i = threadIdx.x; i < nk * 48; i += blockDim.x)
+        shs[i / 48][i % 48] = sp.sh[(k0 + i / 48) * 48 + i % 48];
+    for (int i = threadIdx.x; i < nk * 3; i += blockDim.x)
+        pos[i / 3][i % 3] = sp.positions[(k0 + i / 3) * 3 + i % 3];
+
+    // entries owned by this lane: e = lane + 32 q, read as A[v][p] * A[v][q]
+    int ep[6], eq[6];
 #pragma unroll
-    for (int i = 0; i < 16; i++) shc[i] = sp.sh[48 * kk + ch * 16 + i];
-    const int ra = g, rb = 15 - g;
-    double ga[16], gb[16], ba[3], bb[3];
-#pragma unroll
-    for (int j = 0; j < 16; j++) ga[j] = gb[j] = 0.0;
-#pragma unroll
-    for (int c = 0; c < 3; c++) ba[c] = bb[c] = 0.0;
-    int seen = 0;
-    for (int s = 0; s < ncam; s++) {
-        const double w = active ? cam_imp[(int64_t)s * n + k] : 0.0;
-        if (!(w > 0.0)) continue;  // compaction.py:97 seen = w > 0
-        double d0 = px - eyes[3 * s], d1 = py - eyes[3 * s + 1], d2 = pz - eyes[3 * s + 2];
-        double nrm = sqrt(d0 * d0 + d1 * d1 + d2 * d2);
-        double y[16];
-        sh_basis16(d0 / nrm, d1 / nrm, d2 / nrm, y);
-        double col = 0.0;
-#pragma unroll
-        for (int i = 0; i < 16; i++) col += y[i] * shc[i];
-        double c0 = __shfl_sync(gmask, col, 0, 8);
-        double c1 = __shfl_sync(gmask, col, 1, 8);
-        double c2 = __shfl_sync(gmask, col, 2, 8);
-        double cw[3];
-#pragma unroll
-        for (int c = 0; c < 3; c++) {
-            double yc = c0 * kRgbToYcocg[c * 3] + c1 * kRgbToYcocg[c * 3 + 1] +
-                        c2 * kRgbToYcocg[c * 3 + 2];
-            cw[c] = yc * w;
+    for (int qq = 0; qq < 6; qq++) {
+        const int e = lane + 32 * qq;
+        ep[qq] = 0;
+        eq[qq] = 0;
+        if (e < 136) {
+            int i = 0, rem = e;
+            while (rem >= 16 - i) {
+                rem -= 16 - i;
+                i++;
+            }
+            ep[qq] = i;
+            eq[qq] = i + rem;
+        } else if (e < 184) {
+            ep[qq] = (e - 136) / 3;
+            eq[qq] = 16 + (e - 136) % 3;
         }
-        double yw[16];
-#pragma unroll
-        for (int i = 0; i < 16; i++) yw[i] = y[i] * w;
-        double a = 0.0, b = 0.0;
-#pragma unroll
-        for (int i = 0; i < 16; i++) {
-            a = (i == ra) ? yw[i] : a;
-            b = (i == rb) ? yw[i] : b;
-        }
-#pragma unroll
-        for (int j = 0; j < 16; j++) {
-            ga[j] += a * yw[j];
-            gb[j] += b * yw[j];
-        }
-#pragma unroll
-        for (int c = 0; c < 3; c++) {
-            ba[c] += a * cw[c];
-            bb[c] += b * cw[c];
-        }
-        seen++;
     }
-    if (!active) return;
+    constexpr int kPer = kShSplatsPerBlock / kShWarps;  // splats per warp
+    double acc[kPer][6];
+    int seen[kPer];
 #pragma unroll
-    for (int j = 0; j < 16; j++) {
-        if (j >= ra) neq[(int64_t)tri(ra, j) * n + k] += ga[j];
-        if (j >= rb) neq[(int64_t)tri(rb, j) * n + k] += gb[j];
+    for (int j = 0; j < kPer; j++) {
+        seen[j] = 0;
+#pragma unroll
+        for (int qq = 0; qq < 6; qq++) acc[j][qq] = 0.0;
+    }
+
+    for (int s0 = 0; s0 < ncam; s0 += 32) {
+        const int nv = ncam - s0 < 32 ? ncam - s0 : 32;
+        __syncthreads();  // previous round done with wtile; first round: sh/pos staged
+        for (int i = threadIdx.x; i < 32 * kShSplatsPerBlock; i += blockDim.x) {
+            const int v = i / kShSplatsPerBlock, kk = i % kShSplatsPerBlock;
+            wtile[v][kk] = (v < nv && kk < nk) ? cam_imp[(int64_t)(s0 + v) * n + k0 + kk] : 0.0;
+        }
+        __syncthreads();
+        const bool lv = lane < nv;
+        const double ex = lv ? eyes[3 * (s0 + lane)] : 0.0;
+        const double ey = lv ? eyes[3 * (s0 + lane) + 1] : 0.0;
+        const double ez = lv ? eyes[3 * (s0 + lane) + 2] : 0.0;
+#pragma unroll
+        for (int j = 0; j < kPer; j++) {
+            const int kk = w * kPer + j;
+            if (kk >= nk) break;  // warp-uniform
+            const double wv = wtile[lane][kk];
+            seen[j] += __popc(__ballot_sync(0xffffffffu, lv && wv > 0.0));
+            double *row = A[w][lane];
+            if (wv > 0.0) {
+                const double d0 = pos[kk][0] - ex, d1 = pos[kk][1] - ey, d2 = pos[kk][2] - ez;
+                const double nrm = sqrt(d0 * d0 + d1 * d1 + d2 * d2);
+                double y[16];
+                sh_basis16(d0 / nrm, d1 / nrm, d2 / nrm, y);
+                double col[3];
+#pragma unroll
+                for (int c = 0; c < 3; c++) {
+                    double t = 0.0;
+#pragma unroll
+                    for (int i = 0; i < 16; i++) t += y[i] * shs[kk][c * 16 + i];
+                    col[c] = t;
+                }
+#pragma unroll
+                for (int i = 0; i < 16; i++) row[i] = y[i] * wv;
+#pragma unroll
+                for (int c = 0; c < 3; c++) {
+                    const double yc = col[0] * kRgbToYcocg[c * 3] + col[1] * kRgbToYcocg[c * 3 + 1] +
+                                      col[2] * kRgbToYcocg[c * 3 + 2];
+                    row[16 + c] = yc * wv;
+                }
+            } else {
+#pragma unroll
+                for (int i = 0; i < 19; i++) row[i] = 0.0;  // unseen: exact zeros
+            }
+            __syncwarp();
+            for (int v = 0; v < nv; v++) {
+#pragma unroll
+                for (int qq = 0; qq < 6; qq++) acc[j][qq] += A[w][v][ep[qq]] * A[w][v][eq[qq]];
+            }
+            __syncwarp();
+        }
     }
 #pragma unroll
-    for (int c = 0; c < 3; c++) {
-        neq[(int64_t)(136 + ra * 3 + c) * n + k] += ba[c];
-        neq[(int64_t)(136 + rb * 3 + c) * n + k] += bb[c];
+    for (int j = 0; j < kPer; j++) {
+        const int kk = w * kPer + j;
+        if (kk >= nk) break;
+        const int64_t k = k0 + kk;
+#pragma unroll
+        for (int qq = 0; qq < 6; qq++) {
+            const int e = lane + 32 * qq;
+            if (e < 184) neq[(int64_t)e * n + k] += acc[j][qq];
+        }
+        if (lane == 0) neq[(int64_t)184 * n + k] += (double)seen[j];
     }
-    if (g == 0) neq[(int64_t)184 * n + k] += (double)seen;
 }
 
 // Upper Cholesky of the m x m principal block, packed with tri() (LAPACK
@@ -264,9 +310,8 @@ __global__ void __launch_bounds__(128) k_sh_solve(potr_splats sp, const double *
 cudaError_t launch_sh_accumulate(const potr_splats &sp, int ncam, const double *eyes_dev,
                                  const double *cam_imp, double *neq, cudaStream_t st) {
     if (sp.n == 0) return cudaSuccess;
-    int64_t threads = sp.n * 8;
-    k_sh_accumulate<<<(unsigned)((threads + 255) / 256), 256, 0, st>>>(sp, ncam, eyes_dev, cam_imp,
-                                                                        neq);
+    const unsigned blocks = (unsigned)((sp.n + kShSplatsPerBlock - 1) / kShSplatsPerBlock);
+    k_sh_accumulate<<<blocks, 32 * kShWarps, 0, st>>>(sp, ncam, eyes_dev, cam_imp, neq);
     return cudaGetLastError();
 }
 

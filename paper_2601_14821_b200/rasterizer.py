@@ -255,14 +255,23 @@ def compute_delta_mse(splats, cameras, targets, threads=1):
     return forward_stats(splats, cameras, targets=targets, threads=threads)
 
 
-def render_targets(splats, cameras, threads=1):
-    """Reference renders of the uncompressed model, read-only (:371-377)."""
+def render_targets_device(splats, cameras):
+    """All views rendered in view batches; device (H, W, 3) tensors."""
     ctx = D.context()
     dev = D.current_device()
     ds = D.DeviceSplats.from_host(splats, dev)
+    imgs = [D.empty((int(c.height), int(c.width), 3), dev) for c in cameras]
+    if cameras:
+        ptrs = (ctypes.c_void_p * len(imgs))(*[t.data_ptr() for t in imgs])
+        ctx.call("potr_render_batch", ctypes.byref(ds.struct()), len(cameras),
+                 _native.camera_array(cameras), ptrs, None)
+    return imgs
+
+
+def render_targets(splats, cameras, threads=1):
+    """Reference renders of the uncompressed model, read-only (:371-377)."""
     imgs = []
-    for cam in cameras:
-        image, _ = _render_device(ds, cam, ctx, dev)
+    for image in render_targets_device(splats, cameras):
         img = image.cpu().numpy()
         img.flags.writeable = False
         imgs.append(img)
