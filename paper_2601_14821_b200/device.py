@@ -6,6 +6,7 @@ pointer.  There is no CPU path: without a CUDA device these raise.
 """
 
 import ctypes
+import warnings
 
 import numpy as np
 import torch
@@ -54,7 +55,10 @@ def to_device(arr, device, shape=None):
         a = a.reshape(shape)
     if a.size == 0:
         return torch.empty(a.shape, dtype=torch.float64, device=device)
-    return torch.from_numpy(a).to(device, non_blocking=False)
+    with warnings.catch_warnings():
+        # read-only inputs (the reference freezes its targets) are only read here
+        warnings.simplefilter("ignore", UserWarning)
+        return torch.from_numpy(a).to(device, non_blocking=False)
 
 
 def empty(shape, device, dtype=torch.float64):
