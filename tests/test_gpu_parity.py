@@ -330,3 +330,71 @@ def test_host_c_abi(R, oracle):
     np.testing.assert_allclose(dm, g["pert_delta_mse"], rtol=1e-9, atol=1e-22)
     np.testing.assert_allclose(ci, g["pert_camera_importance"], rtol=1e-12, atol=1e-20)
     assert mse[0] == pytest.approx(float(g["pert_mse"]), rel=1e-12)
+
+
+def _stress_scene(seed=0):
+    """Edge cases in one scene: a 1500-deep stack on a few tiles (long tile
+    lists, termination), huge footprints, splats behind / at the near plane,
+    off-screen, opacity extremes, and a plain random population."""
+    from paper_2601_14821_b200.fixture import random_scene
+    from paper_2601_14821_b200.scene import Splats
+    rng = np.random.default_rng(seed)
+    base, cams = random_scene(seed, num_splats=400, num_cameras=3, resolution=40)
+    n_stack = 1500
+    eye, fwd = cams[0].eye, cams[0].rotation[2]
+    stack_pos = eye + fwd[None, :] * rng.uniform(1.0, 3.0, n_stack)[:, None] \
+        + 0.01 * rng.standard_normal((n_stack, 3))
+    extra_pos = np.stack([eye + 0.005 * fwd, eye - 1.0 * fwd, eye + 0.0101 * fwd,
+                          eye + 2.0 * fwd, eye + 50.0 * cams[0].rotation[0]])
+    pos = np.concatenate([base.positions, stack_pos, extra_pos])
+    n = len(pos)
+    sh = np.concatenate([base.sh, 0.3 * rng.standard_normal((n - len(base.sh), 3, 16))])
+    sh[len(base.sh):, :, 0] += 1.5
+    op = np.concatenate([base.opacities, rng.uniform(0.05, 0.99, n_stack),
+                         np.array([0.9, 0.9, 0.9, 1.0 - 1e-9, 0.5])])
+    op[5] = 1e-9  # never reaches the alpha floor
+    sc = np.concatenate([base.scales, rng.uniform(0.005, 0.05, (n_stack, 3)),
+                         np.array([[0.01] * 3, [0.5] * 3, [0.01] * 3, [3.0, 3.0, 0.01],
+                                   [0.01] * 3])])
+    q = np.concatenate([base.rotations, rng.standard_normal((n - len(base.rotations), 4))])
+    q /= np.linalg.norm(q, axis=1, keepdims=True)
+    q[q[:, 0] < 0] *= -1.0
+    return Splats(pos, sh, op, sc, q), cams
+
+
+def test_stress_edge_cases_vs_oracle(R, oracle):
+    from paper_2601_14821_b200 import binning
+    splats, cams = _stress_scene()
+    targets = [oracle.render(splats, c)[0] for c in cams]
+    gt = R.render_targets(splats, cams)
+    for a, b in zip(gt, targets):
+        np.testing.assert_allclose(a, b, rtol=0, atol=1e-13)
+    pert = perturbed(splats)
+    st = R.compute_delta_mse(pert, cams, targets)
+    imp, ci, dm, mse = oracle.forward_stats(pert, cams, targets)
+    np.testing.assert_allclose(st.importance, imp, rtol=1e-11, atol=1e-20)
+    np.testing.assert_allclose(np.asarray(st.camera_importance), ci, rtol=1e-11, atol=1e-20)
+    np.testing.assert_allclose(st.delta_mse, dm, rtol=1e-8, atol=1e-22)
+    assert st.mse == pytest.approx(mse, rel=1e-12)
+    for cam in cams:
+        order, off, lst = binning.tile_lists(splats, cam)
+        assert np.array_equal(order, oracle.depth_order(splats, cam))
+        o2, l2 = oracle.tile_lists(splats, cam)
+        assert np.array_equal(off, o2) and np.array_equal(lst, l2)
+    assert np.diff(off).max() > 16 * 32  # tile lists longer than the kept pass-1 masks
+
+
+@pytest.mark.slow
+def test_large_scene_views_vs_oracle(R, oracle):
+    """300k splats at 800x800 (the C2 shape), two views, against the oracle."""
+    from paper_2601_14821_b200.fixture import make_fixture
+    splats, cams = make_fixture(300_000, 100, 0, 800)
+    cams = cams[:2]
+    targets = R.render_targets(splats, cams)
+    pert = perturbed(splats)
+    st = R.compute_delta_mse(pert, cams, targets)
+    imp, ci, dm, mse = oracle.forward_stats(pert, cams, [np.asarray(t) for t in targets],
+                                            threads=2)
+    np.testing.assert_allclose(st.importance, imp, rtol=1e-10, atol=1e-22)
+    assert score_close(st.delta_mse, dm, rel=1e-6, floor=1e-24)
+    assert st.mse == pytest.approx(mse, rel=1e-11)
