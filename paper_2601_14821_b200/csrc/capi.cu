@@ -3,6 +3,7 @@
 #include <cstdio>
 #include <cmath>
 #include <cstdlib>
+#include <utility>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -46,7 +47,7 @@ struct potr_ctx {
     bool counting = false;
     DevBuf counters;
     int64_t pairs_total = 0;
-    DevBuf tile_counter, sid, ci_v, dm_v, bbox, overflow;
+    DevBuf tile_counter, sid, ci_v, dm_v, bbox, overflow, vidx;
     double scene_lo[3] = {0, 0, 0}, scene_hi[3] = {0, 0, 0};  // splat position bbox
     uint64_t invalid_key0 = ~0ull;  // depth key of an invalid splat in view 0 of the last batch
     int view_batch = kMaxViewBatch;
@@ -294,6 +295,7 @@ int bin_batch(potr_ctx *ctx, const potr_splats &sp, const potr_camera *cams, int
     ENSURE(ctx->key, sizeof(uint64_t) * total);
     ENSURE(ctx->skey, sizeof(uint64_t) * total);
     ENSURE(ctx->sids, sizeof(int32_t) * total);
+    ENSURE(ctx->vidx, sizeof(int32_t) * total);
     ENSURE(ctx->cnt, sizeof(int32_t) * total);
     ENSURE(ctx->cnt_sorted, sizeof(int64_t) * total);
     ENSURE(ctx->offs, sizeof(int64_t) * (total + 1));
@@ -317,21 +319,35 @@ int bin_batch(potr_ctx *ctx, const potr_splats &sp, const potr_camera *cams, int
         Stage _st(ctx, POTR_STAGE_PREPROCESS);
         LAUNCH(1, launch_preprocess(sp, cb, nview, g.tiles_x, all_colors ? 1 : 0, dk,
                                     P<SplatRec>(ctx->rec), P<uint64_t>(ctx->key),
-                                    P<int32_t>(ctx->cnt), counters(ctx), ctx->stream));
+                                    P<int32_t>(ctx->cnt), P<int32_t>(ctx->vidx), counters(ctx),
+                                    ctx->stream));
         _st.end();
     }
     {
         Stage _st(ctx, POTR_STAGE_DEPTH_SORT);
+        // sorted keys / record indices end in skey / sids (buffers swapped
+        // when the double-buffered sort finished in the other half)
         if (dk.compact) {  // one stable sort of the whole batch
             const int end_bit = dk.nbits + bitlen((uint64_t)(nview - 1));
+            bool alt = false;
             CK(depth_sort(ctx->temp.p, ctx->temp.cap, P<uint64_t>(ctx->key),
-                          P<uint64_t>(ctx->skey), P<int32_t>(ctx->iota), P<int32_t>(ctx->sids),
-                          total, end_bit, ctx->stream));
-        } else {  // raw 64-bit depth bits: one sort per view
+                          P<uint64_t>(ctx->skey), P<int32_t>(ctx->vidx), P<int32_t>(ctx->sids),
+                          total, end_bit, &alt, ctx->stream));
+            if (!alt) {
+                std::swap(ctx->key, ctx->skey);
+                std::swap(ctx->vidx, ctx->sids);
+            }
+        } else {  // raw 64-bit depth bits: one sort per view, all with the same
+                  // pass count, so every view's result ends in the same half
+            bool alt = true;
             for (int v = 0; v < nview; v++)
                 CK(depth_sort(ctx->temp.p, ctx->temp.cap, P<uint64_t>(ctx->key) + v * n,
-                              P<uint64_t>(ctx->skey) + v * n, P<int32_t>(ctx->iota) + v * n,
-                              P<int32_t>(ctx->sids) + v * n, n, 64, ctx->stream));
+                              P<uint64_t>(ctx->skey) + v * n, P<int32_t>(ctx->vidx) + v * n,
+                              P<int32_t>(ctx->sids) + v * n, n, 64, &alt, ctx->stream));
+            if (!alt) {
+                std::swap(ctx->key, ctx->skey);
+                std::swap(ctx->vidx, ctx->sids);
+            }
         }
         _st.end();
     }
@@ -534,6 +550,7 @@ void potr_destroy(potr_ctx *ctx) {
     if (ctx->pinned) cudaFreeHost(ctx->pinned);
     if (ctx->counters.p) cudaFree(ctx->counters.p);
     if (ctx->tile_counter.p) cudaFree(ctx->tile_counter.p);
+    if (ctx->vidx.p) cudaFree(ctx->vidx.p);
     if (ctx->bbox.p) cudaFree(ctx->bbox.p);
     if (ctx->overflow.p) cudaFree(ctx->overflow.p);
     if (ctx->ci_v.p) cudaFree(ctx->ci_v.p);

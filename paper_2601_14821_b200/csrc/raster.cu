@@ -41,6 +41,7 @@ __global__ void __launch_bounds__(128) k_preprocess(potr_splats sp, CamBatch cam
                                                      SplatRec *__restrict__ rec,
                                                      uint64_t *__restrict__ key,
                                                      int32_t *__restrict__ cnt,
+                                                     int32_t *__restrict__ vidx,
                                                      unsigned long long *counters) {
     const int64_t n = sp.n;
     const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -118,6 +119,7 @@ __global__ void __launch_bounds__(128) k_preprocess(potr_splats sp, CamBatch cam
     }
     key[g] = kk;
     cnt[g] = c;
+    vidx[g] = (int32_t)g;
 }
 
 // project_splats / splat_colors dump for parity tests (potr_project).
@@ -719,12 +721,12 @@ size_t raster_smem_bytes() { return sizeof(WarpSmem) * kRasterWarps + 64 * sizeo
 
 cudaError_t launch_preprocess(const potr_splats &sp, const CamBatch &cams, int nview,
                               int tiles_x, int all_colors, const DepthKey &dk, SplatRec *rec,
-                              uint64_t *key, int32_t *cnt, unsigned long long *counters,
-                              cudaStream_t st) {
+                              uint64_t *key, int32_t *cnt, int32_t *vidx,
+                              unsigned long long *counters, cudaStream_t st) {
     if (sp.n == 0) return cudaSuccess;
     k_preprocess<<<grid_for(sp.n * nview, 128), 128, 0, st>>>(sp, cams, nview, tiles_x,
                                                                all_colors, dk, rec, key, cnt,
-                                                               counters);
+                                                               vidx, counters);
     return cudaGetLastError();
 }
 
@@ -743,18 +745,24 @@ cudaError_t launch_iota(int64_t n, int32_t *out, cudaStream_t st) {
     return cudaGetLastError();
 }
 
-cudaError_t depth_sort(void *temp, size_t temp_bytes, const uint64_t *key, uint64_t *skey,
-                       const int32_t *iota, int32_t *sids, int64_t n, int end_bit,
+// Double-buffered: no copy-back pass when the pass count is odd.  *in_alt is
+// set when the sorted keys/values ended in the second buffer of each pair.
+cudaError_t depth_sort(void *temp, size_t temp_bytes, uint64_t *key_a, uint64_t *key_b,
+                       int32_t *val_a, int32_t *val_b, int64_t n, int end_bit, bool *in_alt,
                        cudaStream_t st) {
+    *in_alt = false;
     if (n == 0) return cudaSuccess;
-    return cub::DeviceRadixSort::SortPairs(temp, temp_bytes, key, skey, iota, sids, (int)n, 0,
-                                           end_bit, st);
+    cub::DoubleBuffer<uint64_t> k(key_a, key_b);
+    cub::DoubleBuffer<int32_t> v(val_a, val_b);
+    cudaError_t e = cub::DeviceRadixSort::SortPairs(temp, temp_bytes, k, v, (int)n, 0, end_bit, st);
+    *in_alt = k.Current() == key_b;
+    return e;
 }
 
 cudaError_t depth_sort_temp(int64_t n, size_t *bytes) {
-    return cub::DeviceRadixSort::SortPairs((void *)nullptr, *bytes, (const uint64_t *)nullptr,
-                                           (uint64_t *)nullptr, (const int32_t *)nullptr,
-                                           (int32_t *)nullptr, (int)n, 0, 64);
+    cub::DoubleBuffer<uint64_t> k(nullptr, nullptr);
+    cub::DoubleBuffer<int32_t> v(nullptr, nullptr);
+    return cub::DeviceRadixSort::SortPairs((void *)nullptr, *bytes, k, v, (int)n, 0, 64);
 }
 
 __global__ void k_bbox(int64_t n, const double *__restrict__ pos,

@@ -48,15 +48,15 @@ cudaError_t launch_bbox(int64_t n, const double *pos, unsigned long long *out, c
 
 cudaError_t launch_preprocess(const potr_splats &sp, const CamBatch &cams, int nview,
                               int tiles_x, int all_colors, const DepthKey &dk, SplatRec *rec,
-                              uint64_t *key, int32_t *cnt, unsigned long long *counters,
-                              cudaStream_t st);
+                              uint64_t *key, int32_t *cnt, int32_t *vidx,
+                              unsigned long long *counters, cudaStream_t st);
 cudaError_t launch_project_dump(const potr_splats &sp, const Cam &cam, double *mean2d,
                                 double *cov2d, double *depth, double *radius, uint8_t *valid,
                                 double *colors, cudaStream_t st);
 cudaError_t launch_iota(int64_t n, int32_t *out, cudaStream_t st);
 cudaError_t depth_sort_temp(int64_t n, size_t *bytes);
-cudaError_t depth_sort(void *temp, size_t temp_bytes, const uint64_t *key, uint64_t *skey,
-                       const int32_t *iota, int32_t *sids, int64_t n, int end_bit,
+cudaError_t depth_sort(void *temp, size_t temp_bytes, uint64_t *key_a, uint64_t *key_b,
+                       int32_t *val_a, int32_t *val_b, int64_t n, int end_bit, bool *in_alt,
                        cudaStream_t st);
 cudaError_t scan_temp(int64_t n, size_t *bytes);
 cudaError_t scan_counts(void *temp, size_t temp_bytes, const int32_t *ids, const int32_t *cnt,
