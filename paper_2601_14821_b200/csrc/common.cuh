@@ -54,20 +54,27 @@ constexpr double kPowerMargin = 1e-9;
 
 __constant__ double kExpTable[64][2] = POTR_EXP_TABLE_INIT;
 
+// exp_neg's scalar constants in the constant bank: DFMA/DMUL/DADD take them
+// as c[][] operands, so the hot loops do not rematerialise 64-bit immediates
+// (two UMOVs each) on every iteration.
+__constant__ double kExpK[8] = {POTR_EXP_INV_STEP, POTR_EXP_SHIFT, -POTR_EXP_STEP_HI,
+                                -POTR_EXP_STEP_LO, POTR_EXP_C2, POTR_EXP_C3,
+                                POTR_EXP_C4, POTR_EXP_C5};
+
 // exp(x) for the Gaussian exponent after the ALPHA_FLOOR prefilter
 // (x in [log(ALPHA_FLOOR), 0]).  Table-driven (2^(j/64) double-double, held
 // in shared memory) with a degree-5 Estrin polynomial: 11 FP64 operations and
 // a 6-deep dependency chain instead of the libdevice exp's ~19 / 17, at
 // < 0.82 ulp (tests/test_exp.py; the reference's glibc exp is ~0.5 ulp).
 __device__ __forceinline__ double exp_neg(double x, const double2 *__restrict__ tab) {
-    const double t = fma(x, POTR_EXP_INV_STEP, POTR_EXP_SHIFT);
-    const double k = t - POTR_EXP_SHIFT;
+    const double t = fma(x, kExpK[0], kExpK[1]);
+    const double k = t - kExpK[1];
     const int ki = __double2loint(t);
-    double r = fma(k, -POTR_EXP_STEP_HI, x);
-    r = fma(k, -POTR_EXP_STEP_LO, r);
+    double r = fma(k, kExpK[2], x);
+    r = fma(k, kExpK[3], r);
     const double r2 = r * r;
-    const double a = fma(r, POTR_EXP_C3, POTR_EXP_C2);
-    const double b = fma(r, POTR_EXP_C5, POTR_EXP_C4);
+    const double a = fma(r, kExpK[5], kExpK[4]);
+    const double b = fma(r, kExpK[7], kExpK[6]);
     const double q = fma(r2, b, a);
     const double p = fma(r2, q, r);
     const double2 T = tab[ki & 63];
