@@ -1,11 +1,15 @@
 """Pruning controller over GPU scores (reference: potr/pruning.py).
 
-SURVEY.md section 8(f) row 1: the controller is O(N log N) host logic that
-consumes the per-splat scores; it is restated here (same numpy semantics:
-stable argsort on the V-shaped priority, sequential cumsum crossing the
-budget, zero-importance sweep) so the bit-exact prune mask can be checked on
-the GPU box, where the reference package is absent.  The re-scoring call of
-every iteration is this package's compute_delta_mse (the B200 kernels).
+SURVEY.md section 8(f) row 1.  The functions restate the reference's numpy
+semantics (stable argsort on the V-shaped priority, sequential cumsum
+crossing the budget, zero-importance sweep) and give the bit-exact prune mask.
+
+run_pruning is device-resident when it drives this package's own scorer: the
+splats are uploaded once and subset in HBM between iterations, the targets
+stay resident, and the O(N log N) removal order is a stable GPU sort of the
+same fp64 priorities (bitwise equal to numpy's, -0.0 canonicalised).  The O(N)
+budget sum and the cumulative-importance crossing run in numpy on the
+downloaded scores, so the mask is bit-identical to the reference's.
 """
 
 from dataclasses import dataclass, field
@@ -96,12 +100,111 @@ def select_removal_set(delta_mse, importance, budget, delta_mse_max, a=10.0):
     return np.sort(cand[take])
 
 
+def _mapping_m_torch(x, a):
+    import torch
+    neg = (torch.sqrt(1.0 - 2.0 * a * torch.clamp(x, max=0.0)) - 1.0) / a
+    return torch.where(x >= 0.0, x, neg)
+
+
+def _removal_order_device(dm_dev, idx_dev, delta_mse_max, a):
+    """idx_dev[stable argsort of m(dm / max)] on the GPU (pruning.py:80-83, :99-100)."""
+    import torch
+    scores = _mapping_m_torch(dm_dev[idx_dev] / delta_mse_max, a) + 0.0  # -0.0 -> +0.0
+    order = torch.sort(scores, stable=True).indices
+    return idx_dev[order]
+
+
+def select_removal_set_device(dm_dev, delta_mse, importance, budget, delta_mse_max, a=10.0):
+    """select_removal_set with the candidate ordering sorted on the device."""
+    import torch
+    cand_dev = torch.nonzero(dm_dev < delta_mse_max).squeeze(1)
+    if cand_dev.numel() == 0:
+        return np.empty(0, dtype=np.int64)
+    cand = _removal_order_device(dm_dev, cand_dev, delta_mse_max, a).cpu().numpy()
+    imp = np.asarray(importance, dtype=np.float64)[cand]
+    positive = imp > 0.0
+    take = ~positive
+    if budget > 0.0:
+        cum = np.cumsum(np.where(positive, imp, 0.0))
+        crossed = np.nonzero(cum >= budget)[0]
+        cut = int(crossed[0]) if len(crossed) else len(cand) - 1
+        take = take.copy()
+        take[:cut + 1] = True
+    return np.sort(cand[take])
+
+
+def _device_scorer_active():
+    from . import rasterizer, distributed
+    return compute_delta_mse is rasterizer.compute_delta_mse and not distributed.sharding_active()
+
+
+def _check_targets(cameras, targets):
+    for s, cam in enumerate(cameras):
+        if targets[s].shape != (cam.height, cam.width, 3):
+            raise ValueError(
+                f"target {s} has shape {targets[s].shape}, camera expects "
+                f"{(cam.height, cam.width, 3)}")
+
+
+def _to_host_splats(ds):
+    from .scene import Splats
+    return Splats(ds.positions.cpu().numpy(), ds.sh.cpu().numpy(), ds.opacities.cpu().numpy(),
+                  ds.scales.cpu().numpy(), ds.rotations.cpu().numpy())
+
+
+def _run_pruning_device(splats, cameras, targets, config, report_sink, first_iteration,
+                        last_iteration):
+    import torch
+    from . import device as D
+    from .rasterizer import forward_stats_device
+    _check_targets(cameras, targets)
+    if len(cameras) == 0:
+        raise ZeroDivisionError("float division by zero")
+    dev = D.current_device()
+    ds = D.DeviceSplats.from_host(splats, dev)
+    dev_targets = D.targets_cache.get(targets, cameras, dev)
+    kept = np.arange(ds.n, dtype=np.int64)
+    reports = []
+    cum_removed = 0.0
+    for it in range(first_iteration, last_iteration + 1):
+        imp_d, _, dm_d, mse_d = forward_stats_device(ds, cameras, dev_targets,
+                                                     want_cam_imp=False)
+        host = torch.cat([imp_d, dm_d, mse_d]).cpu().numpy()
+        n = ds.n
+        importance, delta_mse, mse = host[:n], host[n:2 * n], float(host[2 * n])
+        if not (delta_mse < config.delta_mse_max).any():
+            break
+        remaining = config.iterations - it + 1
+        budget = compute_budget(delta_mse, importance, config.delta_mse_max, remaining)
+        sel = select_removal_set_device(dm_d, delta_mse, importance, budget,
+                                        config.delta_mse_max, config.a)
+        removed_importance = float(importance[sel].sum())
+        cum_removed += removed_importance
+        report = PruneIterationReport(it, budget, len(sel), removed_importance, cum_removed,
+                                      n, n - len(sel), mse, kept[sel])
+        reports.append(report)
+        if report_sink is not None:
+            report_sink(report.to_dict())
+        if len(sel) == 0:
+            continue
+        mask = np.ones(n, dtype=bool)
+        mask[sel] = False
+        mask_d = torch.from_numpy(mask).to(dev)
+        ds = D.DeviceSplats(ds.positions[mask_d], ds.sh[mask_d], ds.opacities[mask_d],
+                            ds.scales[mask_d], ds.rotations[mask_d])
+        kept = kept[mask]
+    return _to_host_splats(ds), kept, reports
+
+
 def run_pruning(splats, cameras, targets, config: PruneConfig, threads=1, report_sink=None,
                 first_iteration=1, last_iteration=None):
     """The iterative controller (:114-163).  Returns (pruned splats, kept
     original indices, iteration reports)."""
     if last_iteration is None:
         last_iteration = config.iterations
+    if _device_scorer_active():
+        return _run_pruning_device(splats, cameras, targets, config, report_sink,
+                                   first_iteration, last_iteration)
     current = splats
     kept = np.arange(len(splats.positions), dtype=np.int64)
     reports = []

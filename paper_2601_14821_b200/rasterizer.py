@@ -215,13 +215,25 @@ def _score_device(ds, cameras, dev_targets, ctx, dev, want_cam_imp=True):
     return imp, cam_imp, dm, mse
 
 
+def forward_stats_device(ds, cameras, dev_targets, want_cam_imp=True):
+    """forward_stats on device-resident splats and targets.  Returns device
+    tensors (importance (N,), camera_importance (S, N) or None, delta_mse (N,)
+    or None, mse (1,) or None), normalised by the camera count."""
+    ctx = D.context()
+    dev = ds.device
+    n, S = ds.n, len(cameras)
+    imp, cam_imp, dm, mse = _score_device(ds, cameras, dev_targets, ctx, dev, want_cam_imp)
+    ctx.call("potr_finalize_stats", ctypes.c_int64(n), S, D.ptr(imp), D.ptr(dm), D.ptr(mse))
+    return (imp[:n], cam_imp[:S, :n] if cam_imp is not None else None,
+            dm[:n] if dm is not None else None, mse)
+
+
 def forward_stats(splats, cameras, targets=None, threads=1) -> ForwardStats:
     """Render every camera once; importance and, with targets, the exact
     removal effect of each splat on the MSE (:311-352)."""
     from . import distributed
     if distributed.sharding_active():
         return distributed.forward_stats_sharded(splats, cameras, targets)
-    ctx = D.context()
     dev = D.current_device()
     ds = D.DeviceSplats.from_host(splats, dev)
     n, S = ds.n, len(cameras)
@@ -230,12 +242,11 @@ def forward_stats(splats, cameras, targets=None, threads=1) -> ForwardStats:
             raise ZeroDivisionError("float division by zero")
         return ForwardStats(np.full(n, np.nan), np.zeros((0, n)), None, None)
     dev_targets = D.targets_cache.get(targets, cameras, dev) if targets is not None else None
-    imp, cam_imp, dm, mse = _score_device(ds, cameras, dev_targets, ctx, dev)
-    ctx.call("potr_finalize_stats", ctypes.c_int64(n), S, D.ptr(imp), D.ptr(dm), D.ptr(mse))
-    cam_imp = D.LazyHostArray(cam_imp[:S, :n])
+    imp, cam_imp, dm, mse = forward_stats_device(ds, cameras, dev_targets)
+    cam_imp = D.LazyHostArray(cam_imp)
     if targets is None:
-        return ForwardStats(imp[:n].cpu().numpy(), cam_imp, None, None)
-    host = torch.cat([imp[:n], dm[:n], mse]).cpu().numpy()
+        return ForwardStats(imp.cpu().numpy(), cam_imp, None, None)
+    host = torch.cat([imp, dm, mse]).cpu().numpy()
     return ForwardStats(host[:n], cam_imp, host[n:2 * n], float(host[2 * n]))
 
 

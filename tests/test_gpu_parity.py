@@ -192,6 +192,28 @@ def test_prune_mask_bit_exact_and_psnr(R):
         assert abs(psnr(ours, targets[s]) - psnr(ref, g["targets"][s])) <= 0.01
 
 
+def test_prune_device_controller_matches_host_controller(R, monkeypatch):
+    """The device-resident controller (splats subset in HBM, GPU stable sort)
+    and the host controller over the same GPU scores give identical reports,
+    kept sets and pruned splats, on a scene with many removals per iteration."""
+    from paper_2601_14821_b200 import pruning, fixture
+    splats, cams = fixture.config_scene("C1")
+    targets = R.render_targets(splats, cams)
+    cfg = pruning.PruneConfig(delta_mse_max=10.0 ** (-8.8 - 2.0 * 0.9), iterations=6)
+    assert pruning._device_scorer_active()
+    dev = pruning.run_pruning(splats, cams, targets, cfg)
+    monkeypatch.setattr(pruning, "compute_delta_mse",
+                        lambda *a, **k: R.compute_delta_mse(*a, **k))
+    assert not pruning._device_scorer_active()
+    host = pruning.run_pruning(splats, cams, targets, cfg)
+    assert np.array_equal(dev[1], host[1])
+    assert sum(r.removed for r in dev[2]) > 0
+    for a, b in zip(dev[2], host[2]):
+        assert a.to_dict() == b.to_dict()
+    for f in ("positions", "sh", "opacities", "scales", "rotations"):
+        assert np.array_equal(getattr(dev[0], f), getattr(host[0], f))
+
+
 def test_sh_recompute(C):
     splats, cams = sh_scene()
     g = golden("sh_scene")
