@@ -66,6 +66,18 @@ __constant__ double kExpK[8] = {POTR_EXP_INV_STEP, POTR_EXP_SHIFT, -POTR_EXP_STE
 // in shared memory) with a degree-5 Estrin polynomial: 11 FP64 operations and
 // a 6-deep dependency chain instead of the libdevice exp's ~19 / 17, at
 // < 0.82 ulp (tests/test_exp.py; the reference's glibc exp is ~0.5 ulp).
+// 1/d for d in [0.01, 1]: the MUFU approximation refined by two Newton steps
+// (relative error below 2^-52; not correctly rounded, which the removal
+// scores' 1e-4 tolerance does not need).
+__device__ __forceinline__ double rcp_nr(double d) {
+    double r;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(d));
+    double e = fma(-d, r, 1.0);
+    r = fma(r, e, r);
+    e = fma(-d, r, 1.0);
+    return fma(r, e, r);
+}
+
 __device__ __forceinline__ double exp_neg(double x, const double2 *__restrict__ tab) {
     const double t = fma(x, kExpK[0], kExpK[1]);
     const double k = t - kExpK[1];

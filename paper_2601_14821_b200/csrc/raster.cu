@@ -272,15 +272,33 @@ __device__ __forceinline__ int4 bbox_of(const ChunkBuf &B, int e) {
 }
 
 // Entries of this chunk whose clipped bbox (rasterizer.py:135-148) contains
-// the lane's pixel.
-__device__ __forceinline__ unsigned live_mask(const ChunkBuf &B, int cnt, int px, int py) {
-    unsigned m = 0u;
-    for (int e = 0; e < cnt; e++) {
-        const int4 bb = bbox_of(B, e);  // same address in every lane: broadcast
-        const bool in = px >= bb.x && px <= bb.y && py >= bb.z && py <= bb.w;
-        m |= (unsigned)in << e;
+// the lane's pixel.  Lane e turns entry e's bbox into the 32-bit set of tile
+// pixels it covers (bit c + 8r <-> lane c + 8r, the lane's pixel); a 32x32 bit
+// transpose over the warp then hands every lane its per-entry bits.  Must be
+// called by the whole warp.
+__device__ __forceinline__ unsigned live_mask(const ChunkBuf &B, int cnt, int ox, int oy,
+                                              int lane) {
+    unsigned w = 0u;
+    if (lane < cnt) {
+        const int4 bb = bbox_of(B, lane);
+        const int c0 = max(bb.x - ox, 0), c1 = min(bb.y - ox, kTileW - 1);
+        const int r0 = max(bb.z - oy, 0), r1 = min(bb.w - oy, kTileH - 1);
+        if (c0 <= c1 && r0 <= r1) {
+            const unsigned cols = (0xFFu >> (7 - c1)) & (0xFFu << c0);
+            const unsigned rows = (0xFFFFFFFFu >> (8 * (3 - r1))) & (0xFFFFFFFFu << (8 * r0));
+            w = (cols * 0x01010101u) & rows;
+        }
     }
-    return m;
+    // transpose: swap the off-diagonal j x j blocks, j = 16, 8, 4, 2, 1
+    const unsigned FULL = 0xffffffffu;
+#pragma unroll
+    for (int j = 16, k = 0; j > 0; j >>= 1, k++) {
+        const unsigned hm = k == 0 ? 0xFFFF0000u : k == 1 ? 0xFF00FF00u : k == 2 ? 0xF0F0F0F0u
+                          : k == 3 ? 0xCCCCCCCCu : 0xAAAAAAAAu;
+        const unsigned y = __shfl_xor_sync(FULL, w, j);
+        w = (lane & j) ? ((w & hm) | ((y & hm) >> j)) : ((w & ~hm) | ((y & ~hm) << j));
+    }
+    return w;
 }
 
 // rasterizer.py:165-171 for entry e at this lane's pixel: the Gaussian exponent
@@ -394,7 +412,8 @@ __global__ void __launch_bounds__(32 * kRasterWarps, POTR_RASTER_MIN_BLOCKS) k_r
                 __syncwarp();
                 const ChunkBuf &B = S.buf[b];
                 const int cnt = min(32, end - base);
-                unsigned m = done ? 0u : live_mask(B, cnt, px, py);
+                unsigned m = live_mask(B, cnt, px - (lane & 7), py - (lane >> 3), lane);
+                if (done) m = 0u;
                 unsigned cm = 0u;
                 unsigned n_live = 0u;
                 while (m) {
@@ -496,7 +515,9 @@ __global__ void __launch_bounds__(32 * kRasterWarps, POTR_RASTER_MIN_BLOCKS) k_r
                 const int ci = (base - start) >> 5;
                 // beyond the kept masks the samples are re-decided exactly as in pass 1
                 const bool known = ci < kMaskChunks;
-                unsigned m = known ? S.cmask[ci][lane] : (done ? 0u : live_mask(B, cnt, px, py));
+                unsigned m = known ? S.cmask[ci][lane]
+                                   : live_mask(B, cnt, px - (lane & 7), py - (lane >> 3), lane);
+                if (done) m = 0u;
                 while (__any_sync(FULL, m != 0u)) {
                     int key = 32 + lane;
                     double dse = 0.0, timp = 0.0;
@@ -511,7 +532,7 @@ __global__ void __launch_bounds__(32 * kRasterWarps, POTR_RASTER_MIN_BLOCKS) k_r
                             const double c2 = B.f[4][e].x;
                             if (MODE == kScore) {
                                 // prune_deltas, forward form: a/(1-a) * (P_K - P_i - T c)
-                                const double f = alpha / (1.0 - alpha);
+                                const double f = alpha * rcp_nr(1.0 - alpha);
                                 const double pd0 = f * (PK0 - P0 - T * c01.x);
                                 const double pd1 = f * (PK1 - P1 - T * c01.y);
                                 const double pd2 = f * (PK2 - P2 - T * c2);
