@@ -61,11 +61,9 @@ __constant__ double kExpK[8] = {POTR_EXP_INV_STEP, POTR_EXP_SHIFT, -POTR_EXP_STE
                                 -POTR_EXP_STEP_LO, POTR_EXP_C2, POTR_EXP_C3,
                                 POTR_EXP_C4, POTR_EXP_C5};
 
-// exp(x) for the Gaussian exponent after the ALPHA_FLOOR prefilter
-// (x in [log(ALPHA_FLOOR), 0]).  Table-driven (2^(j/64) double-double, held
-// in shared memory) with a degree-5 Estrin polynomial: 11 FP64 operations and
-// a 6-deep dependency chain instead of the libdevice exp's ~19 / 17, at
-// < 0.82 ulp (tests/test_exp.py; the reference's glibc exp is ~0.5 ulp).
+// The compositing thresholds, for the same reason (DSETP takes c[][] operands).
+__constant__ double kCompositeK[3] = {kAlphaCap, kAlphaFloor, kTTerminate};
+
 // 1/d for d in [0.01, 1]: the MUFU approximation refined by two Newton steps
 // (relative error below 2^-52; not correctly rounded, which the removal
 // scores' 1e-4 tolerance does not need).
@@ -78,7 +76,21 @@ __device__ __forceinline__ double rcp_nr(double d) {
     return fma(r, e, r);
 }
 
-__device__ __forceinline__ double exp_neg(double x, const double2 *__restrict__ tab) {
+// exp(x) for the Gaussian exponent after the ALPHA_FLOOR prefilter
+// (x in [log(ALPHA_FLOOR), 0]).  Table-driven (2^(j/64) double-double, held
+// in shared memory) with a degree-5 Estrin polynomial: 11 FP64 operations and
+// a 6-deep dependency chain instead of the libdevice exp's ~19 / 17, at
+// < 0.82 ulp (tests/test_exp.py; the reference's glibc exp is ~0.5 ulp).
+// 16-byte shared load from a 32-bit shared-window address held in a register.
+__device__ __forceinline__ double2 lds_double2(unsigned addr) {
+    double2 v;
+    asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(addr));
+    return v;
+}
+
+// tab_s: shared-window address of the 64-entry table (kExpTable copied to
+// shared memory by the caller).
+__device__ __forceinline__ double exp_neg(double x, unsigned tab_s) {
     const double t = fma(x, kExpK[0], kExpK[1]);
     const double k = t - kExpK[1];
     const int ki = __double2loint(t);
@@ -89,7 +101,7 @@ __device__ __forceinline__ double exp_neg(double x, const double2 *__restrict__ 
     const double b = fma(r, kExpK[7], kExpK[6]);
     const double q = fma(r2, b, a);
     const double p = fma(r2, q, r);
-    const double2 T = tab[ki & 63];
+    const double2 T = lds_double2(tab_s + ((unsigned)(ki & 63) << 4));
     const double res = fma(T.x, p, T.y) + T.x;
     return __hiloint2double(__double2hiint(res) + (ki >> 6) * (1 << 20), __double2loint(res));
 }

@@ -26,7 +26,7 @@
 #include "raster.cuh"
 
 #ifndef POTR_RASTER_MIN_BLOCKS
-#define POTR_RASTER_MIN_BLOCKS 6
+#define POTR_RASTER_MIN_BLOCKS 8
 #endif
 
 namespace potr {
@@ -215,8 +215,15 @@ struct ChunkBuf {
     int32_t dup[32];
 };
 
+#ifndef POTR_CHUNK_BUFFERS
+#define POTR_CHUNK_BUFFERS 1
+#endif
+// 1: single-buffered chunks; at 8 CTAs x 4 warps per SM the other warps hide
+// the copy (measured faster at C3 than double buffering at 6 CTAs per SM)
+constexpr int kChunkBufs = POTR_CHUNK_BUFFERS;
+
 struct WarpSmem {
-    ChunkBuf buf[2];
+    ChunkBuf buf[kChunkBufs];
     unsigned cmask[kMaskChunks][32];  // pass-1 contribution mask of each lane, per chunk
     double2 acc[32];                  // per-entry (dSE, T*alpha) sums of the current chunk
 };
@@ -305,15 +312,15 @@ __device__ __forceinline__ unsigned live_mask(const ChunkBuf &B, int cnt, int ox
 // with the exp prefilter, then alpha capped at ALPHA_CAP.  Returns false when
 // alpha < ALPHA_FLOOR (the sample is skipped and T is untouched).
 __device__ __forceinline__ bool eval_alpha(const ChunkBuf &B, int e, double pxc, double pyc,
-                                           const double2 *tab, double &alpha) {
+                                           unsigned tab, double &alpha) {
     const double2 m = B.f[0][e], ab = B.f[1][e], co = B.f[2][e];
     const double pthr = B.f[4][e].y;
     const double dx = pxc - m.x, dy = pyc - m.y;
     const double power = -0.5 * (ab.x * dx * dx + co.x * dy * dy) - ab.y * dx * dy;
     if (power < pthr) return false;  // o*exp(power) < ALPHA_FLOOR for certain
     alpha = co.y * exp_neg(power, tab);
-    if (alpha > kAlphaCap) alpha = kAlphaCap;
-    return !(alpha < kAlphaFloor);
+    if (alpha > kCompositeK[0]) alpha = kCompositeK[0];
+    return !(alpha < kCompositeK[1]);
 }
 
 // Deterministic segmented sum over the lanes that hold the same key: pointer
@@ -354,6 +361,37 @@ __device__ __forceinline__ bool group_sum(int key, double &v0, double &v1) {
     return (peers & ((1u << lane) - 1u)) == 0u;  // this lane leads its group
 }
 
+// S.acc[key] += (v0, v1) for every lane with a valid key (< 32), in a fixed
+// order: per key, the lanes of the group add in lane order.  Small groups
+// (the common case: ~5 lanes at the C3 shape) do that directly, one rank per
+// round; large ones reduce first with group_sum.  Either way the result
+// depends only on the keys and values, never on scheduling.
+constexpr int kSerialGroups = 8;
+
+__device__ __forceinline__ void accumulate(WarpSmem &S, int key, double v0, double v1) {
+    const unsigned FULL = 0xffffffffu;
+    const int lane = threadIdx.x & 31;
+    const unsigned peers = __match_any_sync(FULL, key);
+    const int gmax = __reduce_max_sync(FULL, (unsigned)__popc(peers));
+    if (gmax <= kSerialGroups) {
+        const int rank = __popc(peers & ((1u << lane) - 1u));
+        for (int r = 0; r < gmax; r++) {
+            if (rank == r && key < 32) {
+                double2 t = S.acc[key];
+                t.x += v0;
+                t.y += v1;
+                S.acc[key] = t;
+            }
+            __syncwarp();
+        }
+        return;
+    }
+    if (group_sum(key, v0, v1) && key < 32) {
+        S.acc[key].x += v0;
+        S.acc[key].y += v1;
+    }
+}
+
 // MODE: kRender     pass 1 only, writes image/trans
 //       kImportance pass 1, then the replay accumulating T*alpha slots
 //       kScore      pass 1, then the replay with the removal effect (targets)
@@ -371,12 +409,15 @@ template <int MODE>
 __global__ void __launch_bounds__(32 * kRasterWarps, POTR_RASTER_MIN_BLOCKS) k_raster(RasterArgs a) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     WarpSmem &S = reinterpret_cast<WarpSmem *>(smem_raw)[threadIdx.x >> 5];
-    double2 *tab = reinterpret_cast<double2 *>(smem_raw + sizeof(WarpSmem) * kRasterWarps);
+    __shared__ double2 tab[64];
     const int lane = threadIdx.x & 31;
     const unsigned FULL = 0xffffffffu;
     for (int i = threadIdx.x; i < 64; i += blockDim.x)
         tab[i] = make_double2(kExpTable[i][0], kExpTable[i][1]);
     __syncthreads();
+    // the table's shared address, opaque so it stays in one register
+    unsigned tab_s = (unsigned)__cvta_generic_to_shared(tab);
+    asm volatile("" : "+r"(tab_s));
 
     for (;;) {
         int tile = 0;
@@ -402,13 +443,22 @@ __global__ void __launch_bounds__(32 * kRasterWarps, POTR_RASTER_MIN_BLOCKS) k_r
         bool done = !inside;
         int stop = start;  // chunks [start, stop) were walked
         if (start < end && !__all_sync(FULL, done)) {
-            issue_chunk(a, S.buf[0], fetch_ids(a, start, end, lane), lane);
-            ChunkIds next = fetch_ids(a, start + 32, end, lane);
+            ChunkIds next = fetch_ids(a, start, end, lane);
+            if (kChunkBufs == 2) {
+                issue_chunk(a, S.buf[0], next, lane);
+                next = fetch_ids(a, start + 32, end, lane);
+            }
             int b = 0;
-            for (int base = start; base < end; base += 32, b ^= 1) {
-                issue_chunk(a, S.buf[b ^ 1], next, lane);
-                next = fetch_ids(a, base + 64, end, lane);
-                cp_async_wait<1>();
+            for (int base = start; base < end; base += 32, b ^= kChunkBufs - 1) {
+                if (kChunkBufs == 2) {
+                    issue_chunk(a, S.buf[(b ^ 1) & (kChunkBufs - 1)], next, lane);
+                    next = fetch_ids(a, base + 64, end, lane);
+                    cp_async_wait<1>();
+                } else {
+                    issue_chunk(a, S.buf[0], next, lane);
+                    next = fetch_ids(a, base + 32, end, lane);
+                    cp_async_wait<0>();
+                }
                 __syncwarp();
                 const ChunkBuf &B = S.buf[b];
                 const int cnt = min(32, end - base);
@@ -421,7 +471,7 @@ __global__ void __launch_bounds__(32 * kRasterWarps, POTR_RASTER_MIN_BLOCKS) k_r
                     m &= m - 1u;
                     n_live++;
                     double alpha;
-                    if (!eval_alpha(B, e, pxc, pyc, tab, alpha)) continue;
+                    if (!eval_alpha(B, e, pxc, pyc, tab_s, alpha)) continue;
                     cm |= 1u << e;
                     if (MODE == kRecords) {
                         unsigned long long slot = atomicAdd(a.rec_counter, 1ull);
@@ -442,7 +492,7 @@ __global__ void __launch_bounds__(32 * kRasterWarps, POTR_RASTER_MIN_BLOCKS) k_r
                     P1 += w * c01.y;
                     P2 += w * c2;
                     T = T * (1.0 - alpha);
-                    if (T < kTTerminate) {  // every later sample is skipped (:162-164)
+                    if (T < kCompositeK[2]) {  // every later sample is skipped (:162-164)
                         done = true;
                         m = 0u;
                     }
@@ -501,14 +551,23 @@ __global__ void __launch_bounds__(32 * kRasterWarps, POTR_RASTER_MIN_BLOCKS) k_r
         done = !inside;
         int written = start;
         if (start < stop) {
-            issue_chunk(a, S.buf[0], fetch_ids(a, start, end, lane), lane);
-            ChunkIds next = fetch_ids(a, start + 32, end, lane);
+            ChunkIds next = fetch_ids(a, start, end, lane);
+            if (kChunkBufs == 2) {
+                issue_chunk(a, S.buf[0], next, lane);
+                next = fetch_ids(a, start + 32, end, lane);
+            }
             int b = 0;
-            for (int base = start; base < stop; base += 32, b ^= 1) {
-                issue_chunk(a, S.buf[b ^ 1], next, lane);
-                next = fetch_ids(a, base + 64, end, lane);
+            for (int base = start; base < stop; base += 32, b ^= kChunkBufs - 1) {
+                if (kChunkBufs == 2) {
+                    issue_chunk(a, S.buf[(b ^ 1) & (kChunkBufs - 1)], next, lane);
+                    next = fetch_ids(a, base + 64, end, lane);
+                } else {
+                    issue_chunk(a, S.buf[0], next, lane);
+                    next = fetch_ids(a, base + 32, end, lane);
+                }
                 S.acc[lane] = make_double2(0.0, 0.0);
-                cp_async_wait<1>();
+                if (kChunkBufs == 2) cp_async_wait<1>();
+                else cp_async_wait<0>();
                 __syncwarp();
                 const ChunkBuf &B = S.buf[b];
                 const int cnt = min(32, end - base);
@@ -525,7 +584,7 @@ __global__ void __launch_bounds__(32 * kRasterWarps, POTR_RASTER_MIN_BLOCKS) k_r
                         const int e = __ffs(m) - 1;
                         m &= m - 1u;
                         double alpha = 0.0;
-                        const bool ok = eval_alpha(B, e, pxc, pyc, tab, alpha);
+                        const bool ok = eval_alpha(B, e, pxc, pyc, tab_s, alpha);
                         if (ok) {
                             key = e;
                             const double2 c01 = B.f[3][e];
@@ -546,16 +605,13 @@ __global__ void __launch_bounds__(32 * kRasterWarps, POTR_RASTER_MIN_BLOCKS) k_r
                             P1 += w * c01.y;
                             P2 += w * c2;
                             T = T * (1.0 - alpha);
-                            if (T < kTTerminate) {
+                            if (T < kCompositeK[2]) {
                                 done = true;
                                 m = 0u;
                             }
                         }
                     }
-                    if (group_sum(key, dse, timp) && key < 32) {
-                        S.acc[key].x += dse;
-                        S.acc[key].y += timp;
-                    }
+                    accumulate(S, key, dse, timp);
                 }
                 __syncwarp();
                 if (lane < cnt) a.partial[B.dup[lane]] = S.acc[lane];
@@ -738,7 +794,7 @@ static inline unsigned grid_for(int64_t n, int block) {
     return (unsigned)((n + block - 1) / block);
 }
 
-size_t raster_smem_bytes() { return sizeof(WarpSmem) * kRasterWarps + 64 * sizeof(double2); }
+size_t raster_smem_bytes() { return sizeof(WarpSmem) * kRasterWarps; }
 
 cudaError_t launch_preprocess(const potr_splats &sp, const CamBatch &cams, int nview,
                               int tiles_x, int all_colors, const DepthKey &dk, SplatRec *rec,
