@@ -160,7 +160,9 @@ int potr_sh_solve(potr_ctx *ctx, const potr_splats *splats, const double *normal
 
 /* Views processed per pipeline round (1..8, default 8; env POTR_B200_VIEW_BATCH). */
 #define POTR_OPT_VIEW_BATCH 1
-/* 1: sort raw 64-bit depth bits per view instead of the compact batch key. */
+/* Depth-sort key: 0 (default) compact batch key sorted as 32-bit hi parts with
+ * runs of equal hi re-ordered by the full key; 1 raw 64-bit depth bits, one
+ * sort per view; 2 the compact key sorted as 64 bits.  All give the same order. */
 #define POTR_OPT_RAW_DEPTH_KEYS 2
 int potr_set_option(potr_ctx *ctx, int option, int value);
 

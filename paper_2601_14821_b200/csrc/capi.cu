@@ -47,11 +47,12 @@ struct potr_ctx {
     bool counting = false;
     DevBuf counters;
     int64_t pairs_total = 0;
-    DevBuf tile_counter, sid, ci_v, dm_v, bbox, overflow, vidx;
+    DevBuf tile_counter, sid, ci_v, dm_v, bbox, overflow, vidx, khi, skhi;
+    bool depth_split = false;  // last bin_batch sorted split keys: skey not materialised
     double scene_lo[3] = {0, 0, 0}, scene_hi[3] = {0, 0, 0};  // splat position bbox
     uint64_t invalid_key0 = ~0ull;  // depth key of an invalid splat in view 0 of the last batch
     int view_batch = kMaxViewBatch;
-    bool raw_depth_keys = false;
+    int depth_keys = 0;  // POTR_OPT_RAW_DEPTH_KEYS: 0 split compact, 1 raw, 2 compact 64-bit
 };
 
 namespace {
@@ -282,8 +283,11 @@ DepthKey depth_key_for(potr_ctx *ctx, const potr_camera *cams, int nview, int64_
 // attributes read once per batch), per-view stable depth sorts, one scan over
 // all (view, rank) counts, one duplicate, one stable tile sort over batch-global
 // tile keys, tile ranges.  On return *K_out holds the number of pairs.
+// depth_mode: 2 split compact keys (32-bit sort + run fixup), 1 compact 64-bit
+// keys, 0 raw per-view 64-bit sorts; a violated bound falls back to 0, an
+// over-long run of equal hi keys to 1.
 int bin_batch(potr_ctx *ctx, const potr_splats &sp, const potr_camera *cams, int nview,
-              bool all_colors, bool with_rank, int64_t *K_out, bool allow_compact = true) {
+              bool all_colors, bool with_rank, int64_t *K_out, int depth_mode = 2) {
     const int64_t n = sp.n;
     const int64_t total = n * nview;
     ViewGeom g = geom(cams[0]);
@@ -302,16 +306,27 @@ int bin_batch(potr_ctx *ctx, const potr_splats &sp, const potr_camera *cams, int
     ENSURE(ctx->ranges, sizeof(int2) * ntiles_b);
     ENSURE(ctx->tile_se, sizeof(double) * ntiles_b);
     ENSURE(ctx->tile_counter, sizeof(int));
-    ENSURE(ctx->overflow, sizeof(int));
+    ENSURE(ctx->overflow, 2 * sizeof(int));
     int rc = ensure_iota(ctx, total);
     if (rc) return rc;
     DepthKey dk;
     std::memset(&dk, 0, sizeof(dk));
     dk.overflow = P<int>(ctx->overflow);
-    if (allow_compact && !ctx->raw_depth_keys) dk = depth_key_for(ctx, cams, nview, n);
-    CK(cudaMemsetAsync(ctx->overflow.p, 0, sizeof(int), ctx->stream));
+    const int forced = ctx->depth_keys == 1 ? 0 : ctx->depth_keys == 2 ? 1 : 2;
+    if (depth_mode > forced) depth_mode = forced;
+    if (depth_mode > 0) dk = depth_key_for(ctx, cams, nview, n);
+    const int key_bits = dk.compact ? dk.nbits + bitlen((uint64_t)(nview - 1)) : 64;
+    const bool split = dk.compact && depth_mode == 2;
+    if (split) {
+        ENSURE(ctx->khi, sizeof(uint32_t) * total);
+        ENSURE(ctx->skhi, sizeof(uint32_t) * total);
+        dk.shift = key_bits > 32 ? key_bits - 32 : 0;
+        dk.khi = P<uint32_t>(ctx->khi);
+    }
+    ctx->depth_split = split;
+    CK(cudaMemsetAsync(ctx->overflow.p, 0, 2 * sizeof(int), ctx->stream));
     size_t t1 = 0, t2 = 0;
-    CK(depth_sort_temp(total, &t1));
+    CK(split ? depth_sort32_temp(total, &t1) : depth_sort_temp(total, &t1));
     CK(scan_temp(total, &t2));
     ENSURE(ctx->temp, t1 > t2 ? t1 : t2);
 
@@ -327,8 +342,21 @@ int bin_batch(potr_ctx *ctx, const potr_splats &sp, const potr_camera *cams, int
         Stage _st(ctx, POTR_STAGE_DEPTH_SORT);
         // sorted keys / record indices end in skey / sids (buffers swapped
         // when the double-buffered sort finished in the other half)
-        if (dk.compact) {  // one stable sort of the whole batch
-            const int end_bit = dk.nbits + bitlen((uint64_t)(nview - 1));
+        if (split) {  // 32-bit sort of the hi keys, then runs of equal hi by full key
+            bool alt = false;
+            CK(depth_sort32(ctx->temp.p, ctx->temp.cap, P<uint32_t>(ctx->khi),
+                            P<uint32_t>(ctx->skhi), P<int32_t>(ctx->vidx), P<int32_t>(ctx->sids),
+                            total, key_bits - dk.shift, &alt, ctx->stream));
+            if (!alt) {
+                std::swap(ctx->khi, ctx->skhi);
+                std::swap(ctx->vidx, ctx->sids);
+            }
+            if (dk.shift)
+                LAUNCH(1, launch_depth_fixup(total, P<uint32_t>(ctx->skhi), P<int32_t>(ctx->sids),
+                                             P<uint64_t>(ctx->key), dk.shift, dk.sentinel, dk.nbits,
+                                             P<int>(ctx->overflow) + 1, ctx->stream));
+        } else if (dk.compact) {  // one stable sort of the whole batch
+            const int end_bit = key_bits;
             bool alt = false;
             CK(depth_sort(ctx->temp.p, ctx->temp.cap, P<uint64_t>(ctx->key),
                           P<uint64_t>(ctx->skey), P<int32_t>(ctx->vidx), P<int32_t>(ctx->sids),
@@ -360,11 +388,15 @@ int bin_batch(potr_ctx *ctx, const potr_splats &sp, const potr_camera *cams, int
     }
     CK(cudaMemcpyAsync(ctx->pinned, P<int64_t>(ctx->offs) + total, sizeof(int64_t),
                        cudaMemcpyDeviceToHost, ctx->stream));
-    CK(cudaMemcpyAsync(ctx->pinned + 1, ctx->overflow.p, sizeof(int), cudaMemcpyDeviceToHost,
+    CK(cudaMemcpyAsync(ctx->pinned + 1, ctx->overflow.p, 2 * sizeof(int), cudaMemcpyDeviceToHost,
                        ctx->stream));
     CK(cudaStreamSynchronize(ctx->stream));
-    if (dk.compact && (int)(ctx->pinned[1] & 0xffffffff) != 0)  // bound violated: exact fallback
-        return bin_batch(ctx, sp, cams, nview, all_colors, with_rank, K_out, false);
+    int flags[2];
+    std::memcpy(flags, ctx->pinned + 1, sizeof(flags));
+    if (dk.compact && flags[0] != 0)  // bound violated: exact raw-key fallback
+        return bin_batch(ctx, sp, cams, nview, all_colors, with_rank, K_out, 0);
+    if (split && flags[1] != 0)  // a long run of equal hi keys: 64-bit compact sort
+        return bin_batch(ctx, sp, cams, nview, all_colors, with_rank, K_out, 1);
     const int64_t K = ctx->pinned[0];
     ctx->invalid_key0 = dk.compact ? dk.sentinel : ~0ull;
     ctx->pairs_total += K;
@@ -556,6 +588,8 @@ void potr_destroy(potr_ctx *ctx) {
     if (ctx->ci_v.p) cudaFree(ctx->ci_v.p);
     if (ctx->dm_v.p) cudaFree(ctx->dm_v.p);
     if (ctx->sid.p) cudaFree(ctx->sid.p);
+    if (ctx->khi.p) cudaFree(ctx->khi.p);
+    if (ctx->skhi.p) cudaFree(ctx->skhi.p);
     for (auto &ev : ctx->events) {
         cudaEventDestroy(ev.second.first);
         cudaEventDestroy(ev.second.second);
@@ -701,8 +735,7 @@ int potr_render_records(potr_ctx *ctx, const potr_splats *splats, const potr_cam
     a.rec_p = P<double>(ctx->rp);
     LAUNCH(1, launch_raster(kRecords, a, a.ntiles, ctx->stream));
     if (colors)
-        LAUNCH(1, launch_colors_from_rec(n, P<uint64_t>(ctx->key), ctx->invalid_key0,
-                                         P<SplatRec>(ctx->rec), colors, ctx->stream));
+        LAUNCH(1, launch_colors_from_rec(n, P<SplatRec>(ctx->rec), colors, ctx->stream));
     CK(cudaMemcpyAsync(ctx->pinned, ctx->rcounter.p, sizeof(int64_t), cudaMemcpyDeviceToHost,
                        ctx->stream));
     CK(cudaStreamSynchronize(ctx->stream));
@@ -755,6 +788,9 @@ int potr_bin(potr_ctx *ctx, const potr_splats *splats, const potr_camera *cam, i
     *n_pairs = K;
     if (tile_splats && capacity < K) return fail(ctx, POTR_E_CAPACITY, "tile list capacity");
     ENSURE(ctx->nvalid, sizeof(unsigned long long));
+    if (ctx->depth_split)  // sorted full keys for the validity count
+        LAUNCH(1, launch_gather_keys(splats->n, P<int32_t>(ctx->sids), P<uint64_t>(ctx->key),
+                                     P<uint64_t>(ctx->skey), ctx->stream));
     LAUNCH(3, launch_bin_outputs(splats->n, P<uint64_t>(ctx->skey), ctx->invalid_key0,
                                  P<int32_t>(ctx->sids),
                                  P<unsigned long long>(ctx->nvalid), order, geom(*cam).ntiles,
@@ -840,7 +876,8 @@ int potr_set_option(potr_ctx *ctx, int option, int value) {
             ctx->view_batch = value;
             return POTR_OK;
         case POTR_OPT_RAW_DEPTH_KEYS:
-            ctx->raw_depth_keys = value != 0;
+            if (value < 0 || value > 2) return fail(ctx, POTR_E_ARG, "depth key mode must be 0..2");
+            ctx->depth_keys = value;
             return POTR_OK;
     }
     return fail(ctx, POTR_E_ARG, "unknown option");

@@ -75,6 +75,8 @@ __global__ void __launch_bounds__(128) k_preprocess(potr_splats sp, CamBatch cam
                 rel = rel >= dk.sentinel ? dk.sentinel - 1 : rel;
             }
             kk = ((uint64_t)v << dk.nbits) | rel;
+            // the invalid sentinel's hi part is reserved for invalid splats
+            if (dk.shift && (rel >> dk.shift) == (dk.sentinel >> dk.shift)) *dk.overflow = 1;
         } else {
             kk = bits;
         }
@@ -117,7 +119,14 @@ __global__ void __launch_bounds__(128) k_preprocess(potr_splats sp, CamBatch cam
                 atomicAdd(&counters[0], (unsigned long long)((x1 - x0 + 1.0) * (y1 - y0 + 1.0)));
         }
     }
+    if (!pr.valid && all_colors) {  // an invalid splat's colour output is 0 (records mode)
+        SplatRec r;
+        memset(&r, 0, sizeof(r));
+        r.x0 = 1, r.x1 = 0;
+        rec[g] = r;
+    }
     key[g] = kk;
+    if (dk.shift) dk.khi[g] = (uint32_t)(kk >> dk.shift);
     cnt[g] = c;
     vidx[g] = (int32_t)g;
 }
@@ -737,14 +746,14 @@ __global__ void k_records_gather(int64_t m, const uint64_t *__restrict__ skey,
     partials[3 * i + 2] = rp[3 * (int64_t)s + 2];
 }
 
-__global__ void k_colors_from_rec(int64_t n, const uint64_t *__restrict__ key, uint64_t invalid,
-                                  const SplatRec *__restrict__ rec, double *colors) {
+// Records mode preprocesses with all_colors: every splat has a record, with
+// zero colour when it is invalid (rasterizer.py:252-254 leaves those at 0).
+__global__ void k_colors_from_rec(int64_t n, const SplatRec *__restrict__ rec, double *colors) {
     int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (k >= n) return;
-    bool valid = key[k] != invalid;
-    colors[3 * k] = valid ? rec[k].cr : 0.0;
-    colors[3 * k + 1] = valid ? rec[k].cg : 0.0;
-    colors[3 * k + 2] = valid ? rec[k].cb : 0.0;
+    colors[3 * k] = rec[k].cr;
+    colors[3 * k + 1] = rec[k].cg;
+    colors[3 * k + 2] = rec[k].cb;
 }
 
 __global__ void k_tile_offsets(int ntiles, const int2 *__restrict__ rng, int64_t K,
@@ -834,6 +843,89 @@ cudaError_t depth_sort(void *temp, size_t temp_bytes, uint64_t *key_a, uint64_t 
     cudaError_t e = cub::DeviceRadixSort::SortPairs(temp, temp_bytes, k, v, (int)n, 0, end_bit, st);
     *in_alt = k.Current() == key_b;
     return e;
+}
+
+cudaError_t depth_sort32(void *temp, size_t temp_bytes, uint32_t *key_a, uint32_t *key_b,
+                         int32_t *val_a, int32_t *val_b, int64_t n, int end_bit, bool *in_alt,
+                         cudaStream_t st) {
+    *in_alt = false;
+    if (n == 0) return cudaSuccess;
+    cub::DoubleBuffer<uint32_t> k(key_a, key_b);
+    cub::DoubleBuffer<int32_t> v(val_a, val_b);
+    cudaError_t e = cub::DeviceRadixSort::SortPairs(temp, temp_bytes, k, v, (int)n, 0, end_bit, st);
+    *in_alt = k.Current() == key_b;
+    return e;
+}
+
+cudaError_t depth_sort32_temp(int64_t n, size_t *bytes) {
+    cub::DoubleBuffer<uint32_t> k(nullptr, nullptr);
+    cub::DoubleBuffer<int32_t> v(nullptr, nullptr);
+    return cub::DeviceRadixSort::SortPairs((void *)nullptr, *bytes, k, v, (int)n, 0, 32);
+}
+
+// One thread per sorted position; the first position of each run of equal hi
+// keys insertion-sorts the run's record ids by their full keys.  The hi sort
+// was stable, so equal full keys keep record-index order (the tiebreak).
+__global__ void k_depth_fixup(int64_t total, const uint32_t *__restrict__ hi,
+                              int32_t *__restrict__ sids, const uint64_t *__restrict__ key,
+                              uint32_t invalid_lo, uint32_t lo_mask, int *overflow) {
+    const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (j + 1 >= total) return;
+    const uint32_t h = hi[j];
+    if (h != hi[j + 1] || (j > 0 && hi[j - 1] == h)) return;  // not the start of a run
+    if ((h & lo_mask) == invalid_lo) return;  // invalid splats: already in record order
+    int len = 2;
+    while (j + len < total && hi[j + len] == h) {
+        if (++len > kFixupRun) {
+            *overflow = 1;
+            return;
+        }
+    }
+    int32_t id[kFixupRun];
+    uint64_t kv[kFixupRun];
+    for (int i = 0; i < len; i++) {
+        id[i] = sids[j + i];
+        kv[i] = key[id[i]];
+    }
+    for (int i = 1; i < len; i++) {
+        const int32_t x = id[i];
+        const uint64_t y = kv[i];
+        int q = i - 1;
+        while (q >= 0 && kv[q] > y) {
+            kv[q + 1] = kv[q];
+            id[q + 1] = id[q];
+            q--;
+        }
+        kv[q + 1] = y;
+        id[q + 1] = x;
+    }
+    for (int i = 0; i < len; i++) sids[j + i] = id[i];
+}
+
+cudaError_t launch_depth_fixup(int64_t total, const uint32_t *khi_sorted, int32_t *sids,
+                               const uint64_t *key, int shift, uint64_t sentinel, int nbits,
+                               int *overflow, cudaStream_t st) {
+    if (total < 2) return cudaSuccess;
+    // hi = (view << (nbits - shift)) | depth part; the invalid sentinel's depth part
+    const int dbits = nbits - shift;
+    const uint32_t lo_mask = dbits >= 32 ? 0xffffffffu : ((1u << dbits) - 1u);
+    const uint32_t invalid_lo = (uint32_t)(sentinel >> shift) & lo_mask;
+    k_depth_fixup<<<grid_for(total, 256), 256, 0, st>>>(total, khi_sorted, sids, key, invalid_lo,
+                                                        lo_mask, overflow);
+    return cudaGetLastError();
+}
+
+__global__ void k_gather_keys(int64_t total, const int32_t *__restrict__ sids,
+                              const uint64_t *__restrict__ key, uint64_t *__restrict__ skey) {
+    const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (j < total) skey[j] = key[sids[j]];
+}
+
+cudaError_t launch_gather_keys(int64_t total, const int32_t *sids, const uint64_t *key,
+                               uint64_t *skey, cudaStream_t st) {
+    if (total == 0) return cudaSuccess;
+    k_gather_keys<<<grid_for(total, 256), 256, 0, st>>>(total, sids, key, skey);
+    return cudaGetLastError();
 }
 
 cudaError_t depth_sort_temp(int64_t n, size_t *bytes) {
@@ -1028,10 +1120,10 @@ cudaError_t launch_records_gather(int64_t m, const uint64_t *skey, const int32_t
     return cudaGetLastError();
 }
 
-cudaError_t launch_colors_from_rec(int64_t n, const uint64_t *key, uint64_t invalid,
-                                   const SplatRec *rec, double *colors, cudaStream_t st) {
+cudaError_t launch_colors_from_rec(int64_t n, const SplatRec *rec, double *colors,
+                                  cudaStream_t st) {
     if (n == 0) return cudaSuccess;
-    k_colors_from_rec<<<grid_for(n, 256), 256, 0, st>>>(n, key, invalid, rec, colors);
+    k_colors_from_rec<<<grid_for(n, 256), 256, 0, st>>>(n, rec, colors);
     return cudaGetLastError();
 }
 

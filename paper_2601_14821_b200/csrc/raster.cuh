@@ -42,6 +42,10 @@ struct DepthKey {
     uint64_t lo_bits;
     uint64_t sentinel;    // (1 << nbits) - 1: invalid splats sort last in their view
     int *overflow;        // set when a depth falls outside the bound
+    // split keys (compact only): hi = key >> shift as 32 bits, sorted first;
+    // ties in hi are then ordered by the full key (k_depth_fixup)
+    int shift;            // 0: no split (the 64-bit key is sorted directly)
+    uint32_t *khi;        // per record: key >> shift
 };
 
 cudaError_t launch_bbox(int64_t n, const double *pos, unsigned long long *out, cudaStream_t st);
@@ -55,6 +59,20 @@ cudaError_t launch_project_dump(const potr_splats &sp, const Cam &cam, double *m
                                 double *colors, cudaStream_t st);
 cudaError_t launch_iota(int64_t n, int32_t *out, cudaStream_t st);
 cudaError_t depth_sort_temp(int64_t n, size_t *bytes);
+cudaError_t depth_sort32_temp(int64_t n, size_t *bytes);
+cudaError_t depth_sort32(void *temp, size_t temp_bytes, uint32_t *key_a, uint32_t *key_b,
+                         int32_t *val_a, int32_t *val_b, int64_t n, int end_bit, bool *in_alt,
+                         cudaStream_t st);
+// Orders every run of equal hi keys in the hi-sorted (khi_sorted, sids) by the
+// full 64-bit key of its records (stable).  Runs longer than kFixupRun (or a
+// valid key sharing the invalid sentinel's hi) set *overflow: the caller falls
+// back to the 64-bit sort.
+constexpr int kFixupRun = 64;
+cudaError_t launch_depth_fixup(int64_t total, const uint32_t *khi_sorted, int32_t *sids,
+                               const uint64_t *key, int shift, uint64_t sentinel, int nbits,
+                               int *overflow, cudaStream_t st);
+cudaError_t launch_gather_keys(int64_t total, const int32_t *sids, const uint64_t *key,
+                               uint64_t *skey, cudaStream_t st);
 cudaError_t depth_sort(void *temp, size_t temp_bytes, uint64_t *key_a, uint64_t *key_b,
                        int32_t *val_a, int32_t *val_b, int64_t n, int end_bit, bool *in_alt,
                        cudaStream_t st);
@@ -90,8 +108,8 @@ cudaError_t launch_records_gather(int64_t m, const uint64_t *skey, const int32_t
                                   const double *rp, int64_t *splat_ids, int64_t *pixels,
                                   double *alphas, double *trans_at, double *partials,
                                   cudaStream_t st);
-cudaError_t launch_colors_from_rec(int64_t n, const uint64_t *key, uint64_t invalid,
-                                   const SplatRec *rec, double *colors, cudaStream_t st);
+cudaError_t launch_colors_from_rec(int64_t n, const SplatRec *rec, double *colors,
+                                  cudaStream_t st);
 cudaError_t launch_bin_outputs(int64_t n, const uint64_t *skey, uint64_t invalid,
                                const int32_t *sids,
                                unsigned long long *nvalid_dev, int64_t *order, int ntiles,

@@ -99,7 +99,7 @@ def test_forward_stats_small_scene(R):
     np.testing.assert_allclose(np.asarray(ci), g["camera_importance"], rtol=1e-12, atol=1e-20)
 
 
-@pytest.mark.parametrize("batch,raw", [(1, 0), (3, 0), (8, 1), (5, 1)])
+@pytest.mark.parametrize("batch,raw", [(1, 0), (3, 0), (8, 1), (5, 1), (8, 2), (2, 2)])
 def test_view_batching_and_key_modes_bit_identical(R, batch, raw):
     """Batch size and depth-key encoding never change a bit of the result."""
     from paper_2601_14821_b200 import _native, device
@@ -404,6 +404,49 @@ def test_stress_edge_cases_vs_oracle(R, oracle):
         o2, l2 = oracle.tile_lists(splats, cam)
         assert np.array_equal(off, o2) and np.array_equal(lst, l2)
     assert np.diff(off).max() > 16 * 32  # tile lists longer than the kept pass-1 masks
+
+
+def _depth_tie_scene(n_long):
+    """random_scene plus splats whose depths tie in the high bits of the
+    depth key: groups a few hundred ulps apart (stored in reverse depth order,
+    so the stable hi sort alone would be wrong), exact duplicates, and
+    n_long identical splats (a run longer than the fixup bound when > 64)."""
+    from paper_2601_14821_b200.fixture import random_scene
+    from paper_2601_14821_b200.scene import Splats
+    base, cams = random_scene(3, num_splats=300, num_cameras=4, resolution=48)
+    eye, fwd = cams[0].eye, cams[0].rotation[2]
+    rows = []
+    for g in range(12):
+        p0 = base.positions[g]
+        d0 = float(np.dot(p0 - eye, fwd))
+        for k in range(6, -1, -1):  # reverse depth order in the array
+            rows.append((p0 + fwd * (d0 * 2.0 ** -44 * k), g))
+        rows.append((p0.copy(), g))  # exact duplicate of the group's first
+    rows += [(base.positions[20].copy(), 20)] * n_long
+    src = np.array([g for _, g in rows])
+    pos = np.concatenate([base.positions, np.stack([p for p, _ in rows])])
+    pick = lambda a: np.concatenate([a, a[src]])
+    return Splats(pos, pick(base.sh), pick(base.opacities), pick(base.scales),
+                  pick(base.rotations)), cams
+
+
+@pytest.mark.parametrize("n_long", [3, 90])
+def test_depth_key_ties_vs_oracle(R, oracle, n_long):
+    """Near-equal and equal depths keep the reference's (depth, id) order
+    through the split-key sort, its run fixup and its long-run fallback, in
+    the per-view binning and in the batched scoring path."""
+    from paper_2601_14821_b200 import binning
+    splats, cams = _depth_tie_scene(n_long)
+    for cam in cams:
+        order, off, lst = binning.tile_lists(splats, cam)
+        assert np.array_equal(order, oracle.depth_order(splats, cam))
+        o2, l2 = oracle.tile_lists(splats, cam)
+        assert np.array_equal(off, o2) and np.array_equal(lst, l2)
+    targets = [oracle.render(splats, c)[0] for c in cams]
+    st = R.compute_delta_mse(perturbed(splats), cams, targets)
+    imp, ci, dm, mse = oracle.forward_stats(perturbed(splats), cams, targets)
+    np.testing.assert_allclose(st.importance, imp, rtol=1e-11, atol=1e-20)
+    np.testing.assert_allclose(st.delta_mse, dm, rtol=1e-8, atol=1e-22)
 
 
 @pytest.mark.slow
