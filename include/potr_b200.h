@@ -164,6 +164,11 @@ int potr_sh_solve(potr_ctx *ctx, const potr_splats *splats, const double *normal
  * runs of equal hi re-ordered by the full key; 1 raw 64-bit depth bits, one
  * sort per view; 2 the compact key sorted as 64 bits.  All give the same order. */
 #define POTR_OPT_RAW_DEPTH_KEYS 2
+/* 1 (default): drop (tile, splat) pairs whose tile no prefilter-passing sample
+ * can reach (conservative ellipse test: renders and records bit-identical,
+ * scores equal up to summation order); 0: the full bbox tile rectangle.
+ * potr_bin always reports the bbox lists. */
+#define POTR_OPT_TILE_CULL 3
 int potr_set_option(potr_ctx *ctx, int option, int value);
 
 /* ---- evidence: live stage timing and work counters --------------------- */

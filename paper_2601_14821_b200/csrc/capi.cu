@@ -53,6 +53,7 @@ struct potr_ctx {
     uint64_t invalid_key0 = ~0ull;  // depth key of an invalid splat in view 0 of the last batch
     int view_batch = kMaxViewBatch;
     int depth_keys = 0;  // POTR_OPT_RAW_DEPTH_KEYS: 0 split compact, 1 raw, 2 compact 64-bit
+    bool tile_cull = true;  // POTR_OPT_TILE_CULL
 };
 
 namespace {
@@ -286,8 +287,10 @@ DepthKey depth_key_for(potr_ctx *ctx, const potr_camera *cams, int nview, int64_
 // depth_mode: 2 split compact keys (32-bit sort + run fixup), 1 compact 64-bit
 // keys, 0 raw per-view 64-bit sorts; a violated bound falls back to 0, an
 // over-long run of equal hi keys to 1.
+// cull: drop (tile, splat) pairs no sample of which passes the exp prefilter
+// (raster.cu row_span); off for potr_bin, whose lists are the bbox lists.
 int bin_batch(potr_ctx *ctx, const potr_splats &sp, const potr_camera *cams, int nview,
-              bool all_colors, bool with_rank, int64_t *K_out, int depth_mode = 2) {
+              bool all_colors, bool with_rank, bool cull, int64_t *K_out, int depth_mode = 2) {
     const int64_t n = sp.n;
     const int64_t total = n * nview;
     ViewGeom g = geom(cams[0]);
@@ -332,7 +335,7 @@ int bin_batch(potr_ctx *ctx, const potr_splats &sp, const potr_camera *cams, int
 
     {
         Stage _st(ctx, POTR_STAGE_PREPROCESS);
-        LAUNCH(1, launch_preprocess(sp, cb, nview, g.tiles_x, all_colors ? 1 : 0, dk,
+        LAUNCH(1, launch_preprocess(sp, cb, nview, g.tiles_x, all_colors ? 1 : 0, cull ? 1 : 0, dk,
                                     P<SplatRec>(ctx->rec), P<uint64_t>(ctx->key),
                                     P<int32_t>(ctx->cnt), P<int32_t>(ctx->vidx), counters(ctx),
                                     ctx->stream));
@@ -394,9 +397,9 @@ int bin_batch(potr_ctx *ctx, const potr_splats &sp, const potr_camera *cams, int
     int flags[2];
     std::memcpy(flags, ctx->pinned + 1, sizeof(flags));
     if (dk.compact && flags[0] != 0)  // bound violated: exact raw-key fallback
-        return bin_batch(ctx, sp, cams, nview, all_colors, with_rank, K_out, 0);
+        return bin_batch(ctx, sp, cams, nview, all_colors, with_rank, cull, K_out, 0);
     if (split && flags[1] != 0)  // a long run of equal hi keys: 64-bit compact sort
-        return bin_batch(ctx, sp, cams, nview, all_colors, with_rank, K_out, 1);
+        return bin_batch(ctx, sp, cams, nview, all_colors, with_rank, cull, K_out, 1);
     const int64_t K = ctx->pinned[0];
     ctx->invalid_key0 = dk.compact ? dk.sentinel : ~0ull;
     ctx->pairs_total += K;
@@ -434,7 +437,7 @@ int bin_batch(potr_ctx *ctx, const potr_splats &sp, const potr_camera *cams, int
         Stage _st(ctx, POTR_STAGE_DUPLICATE);
         LAUNCH(1, launch_duplicate(total, n, P<int32_t>(ctx->sids), P<int64_t>(ctx->offs),
                                    P<SplatRec>(ctx->rec), g.tiles_x, g.ntiles, sb, key16,
-                                   ctx->tkey.p, P<int32_t>(ctx->dup_id),
+                                   cull ? 1 : 0, ctx->tkey.p, P<int32_t>(ctx->dup_id),
                                    with_rank ? P<int32_t>(ctx->dup_rank) : nullptr, ctx->stream));
         _st.end();
     }
@@ -507,7 +510,7 @@ int score_views_impl(potr_ctx *ctx, const potr_splats *sp, int ncam, const potr_
         for (int v = 0; v < nb; v++)
             if (targets && !targets[s + v]) return fail(ctx, POTR_E_ARG, "target pointer is NULL");
         int64_t K = 0;
-        rc = bin_batch(ctx, *sp, cams + s, nb, false, false, &K);
+        rc = bin_batch(ctx, *sp, cams + s, nb, false, false, ctx->tile_cull, &K);
         if (rc) return rc;
         ViewGeom g = geom(cams[s]);
         RasterArgs a = raster_args(ctx, cams[s], nb);
@@ -676,7 +679,7 @@ int potr_render_batch(potr_ctx *ctx, const potr_splats *splats, int ncam, const 
         for (int v = 0; v < nb; v++)
             if (!images[s + v]) return fail(ctx, POTR_E_ARG, "image pointer is NULL");
         int64_t K = 0;
-        rc = bin_batch(ctx, *splats, cams + s, nb, false, false, &K);
+        rc = bin_batch(ctx, *splats, cams + s, nb, false, false, ctx->tile_cull, &K);
         if (rc) return rc;
         RasterArgs a = raster_args(ctx, cams[s], nb);
         for (int v = 0; v < nb; v++) {
@@ -715,7 +718,7 @@ int potr_render_records(potr_ctx *ctx, const potr_splats *splats, const potr_cam
     const int64_t n = splats->n;
     int64_t K = 0;
     if ((rc = compute_scene_bounds(ctx, *splats))) return rc;
-    rc = bin_batch(ctx, *splats, cam, 1, true, true, &K);
+    rc = bin_batch(ctx, *splats, cam, 1, true, true, ctx->tile_cull, &K);
     if (rc) return rc;
     int64_t cap = capacity > 0 ? capacity : 0;
     ENSURE(ctx->rcounter, sizeof(unsigned long long));
@@ -783,7 +786,7 @@ int potr_bin(potr_ctx *ctx, const potr_splats *splats, const potr_camera *cam, i
     if ((rc = check_cam(ctx, cam))) return rc;
     int64_t K = 0;
     if ((rc = compute_scene_bounds(ctx, *splats))) return rc;
-    rc = bin_batch(ctx, *splats, cam, 1, false, false, &K);
+    rc = bin_batch(ctx, *splats, cam, 1, false, false, false, &K);
     if (rc) return rc;
     *n_pairs = K;
     if (tile_splats && capacity < K) return fail(ctx, POTR_E_CAPACITY, "tile list capacity");
@@ -878,6 +881,9 @@ int potr_set_option(potr_ctx *ctx, int option, int value) {
         case POTR_OPT_RAW_DEPTH_KEYS:
             if (value < 0 || value > 2) return fail(ctx, POTR_E_ARG, "depth key mode must be 0..2");
             ctx->depth_keys = value;
+            return POTR_OK;
+        case POTR_OPT_TILE_CULL:
+            ctx->tile_cull = value != 0;
             return POTR_OK;
     }
     return fail(ctx, POTR_E_ARG, "unknown option");

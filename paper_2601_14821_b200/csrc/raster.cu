@@ -34,10 +34,53 @@ namespace potr {
 // ---------------------------------------------------------------------------
 // (a) preprocess
 
+// Tile culling: the tile columns [*c0, *c1] of tile row ty whose pixel centres
+// can pass the exp prefilter (power >= pthr) of record r.  The region
+// power >= pthr is the ellipse q(d) = ia dx^2 + 2 ib dx dy + ic dy^2 <= R,
+// R = -2 pthr; over the row's band of pixel-centre dy its x extent is
+// [min g, max f] with f, g = (-ib dy +- sqrt(ia R - det dy^2)) / ia, concave /
+// convex in dy with extrema at dy = -+ ib sqrt(R / (det ic)), clamped to the
+// band.  A margin on R and on the pixel bounds keeps the cut conservative
+// against rounding, so a culled (tile, splat) pair holds no sample that the
+// rasterizer would composite: renders and records are bit-identical with or
+// without it (scores up to the add order of the per-(tile, splat) sums).
+// Near-degenerate conics keep the full bbox row.
+constexpr double kCullMarginPower = 1e-6;
+constexpr double kCullMarginPixel = 1e-6;
+
+__device__ __forceinline__ bool row_span(const SplatRec &r, int ty, int *c0, int *c1) {
+    const int py0 = max(ty * kTileH, r.y0), py1 = min(ty * kTileH + kTileH - 1, r.y1);
+    if (py0 > py1 || r.x0 > r.x1) return false;
+    int px0 = r.x0, px1 = r.x1;
+    const double R = -2.0 * (r.pthr - kCullMarginPower);
+    if (!(R > 0.0)) return false;  // pthr >= margin > 0 >= power: nothing passes
+    const double a = r.ia, b = r.ib, c = r.ic;
+    const double det = a * c - b * b;
+    if (a > 0.0 && c > 0.0 && det > 1e-4 * (a * c) && isfinite(R) && isfinite(det)) {
+        const double d0 = (double)py0 + 0.5 - r.my, d1 = (double)py1 + 0.5 - r.my;
+        const double ymax = sqrt(R * a / det);
+        const double lo = fmax(d0, -ymax), hi = fmin(d1, ymax);
+        if (lo > hi + kCullMarginPixel) return false;
+        const double sdy = b * sqrt(R / (det * c));
+        const double ya = fmin(fmax(-sdy, lo), hi), yb = fmin(fmax(sdy, lo), hi);
+        const double xmax = (-b * ya + sqrt(fmax(a * R - det * ya * ya, 0.0))) / a;
+        const double xmin = (-b * yb - sqrt(fmax(a * R - det * yb * yb, 0.0))) / a;
+        const double e0 = ceil(r.mx + xmin - 0.5 - kCullMarginPixel);
+        const double e1 = floor(r.mx + xmax - 0.5 + kCullMarginPixel);
+        if (e0 > (double)px0) px0 = e0 > (double)px1 ? px1 + 1 : (int)e0;
+        if (e1 < (double)px1) px1 = e1 < (double)px0 ? px0 - 1 : (int)e1;
+        if (px0 > px1) return false;
+    }
+    *c0 = px0 >> kTileWLog2;
+    *c1 = px1 >> kTileWLog2;
+    return true;
+}
+
 // One thread per (splat, view) of the batch; the views of a splat are adjacent
 // threads, so its attributes come from one cache line fetch.
 __global__ void __launch_bounds__(128) k_preprocess(potr_splats sp, CamBatch cams, int nview,
-                                                     int tiles_x, int all_colors, DepthKey dk,
+                                                     int tiles_x, int all_colors, int cull,
+                                                     DepthKey dk,
                                                      SplatRec *__restrict__ rec,
                                                      uint64_t *__restrict__ key,
                                                      int32_t *__restrict__ cnt,
@@ -110,11 +153,17 @@ __global__ void __launch_bounds__(128) k_preprocess(potr_splats sp, CamBatch cam
             r.y1 = (int32_t)y1;
             if (!draw) r.x0 = 1, r.x1 = 0;  // empty: never drawn
             rec[g] = r;
+            if (draw && cull) {
+                for (int ty = r.y0 >> kTileHLog2; ty <= (r.y1 >> kTileHLog2); ty++) {
+                    int t0, t1;
+                    if (row_span(r, ty, &t0, &t1)) c += t1 - t0 + 1;
+                }
+            }
         }
         if (draw) {
             const int tx0 = (int)x0 >> kTileWLog2, tx1 = (int)x1 >> kTileWLog2;
             const int ty0 = (int)y0 >> kTileHLog2, ty1 = (int)y1 >> kTileHLog2;
-            c = (tx1 - tx0 + 1) * (ty1 - ty0 + 1);
+            if (!cull) c = (tx1 - tx0 + 1) * (ty1 - ty0 + 1);
             if (counters)  // E: pixels the reference loop visits (rasterizer.py:159-161)
                 atomicAdd(&counters[0], (unsigned long long)((x1 - x0 + 1.0) * (y1 - y0 + 1.0)));
         }
@@ -166,7 +215,7 @@ __global__ void k_gather_counts(int64_t total, int64_t n, const int32_t *__restr
 template <typename KeyT>
 __global__ void k_duplicate(int64_t total, int64_t n, const int32_t *__restrict__ ids,
                             const int64_t *__restrict__ offs, const SplatRec *__restrict__ rec,
-                            int tiles_x, int ntiles, int sb, KeyT *__restrict__ tkey,
+                            int tiles_x, int ntiles, int sb, int cull, KeyT *__restrict__ tkey,
                             int32_t *__restrict__ dup_gid, int32_t *__restrict__ dup_rank) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= total) return;
@@ -179,13 +228,17 @@ __global__ void k_duplicate(int64_t total, int64_t n, const int32_t *__restrict_
     const int tx0 = R.x0 >> kTileWLog2, tx1 = R.x1 >> kTileWLog2;
     const int ty0 = R.y0 >> kTileHLog2, ty1 = R.y1 >> kTileHLog2;
     const uint32_t tbase = (uint32_t)((v % sb) * ntiles);
-    for (int ty = ty0; ty <= ty1; ty++)
-        for (int tx = tx0; tx <= tx1; tx++) {
+    const SplatRec r = R;
+    for (int ty = ty0; ty <= ty1; ty++) {
+        int c0 = tx0, c1 = tx1;
+        if (cull && !row_span(r, ty, &c0, &c1)) continue;
+        for (int tx = c0; tx <= c1; tx++) {
             tkey[o] = (KeyT)(tbase + (uint32_t)(ty * tiles_x + tx));
             dup_gid[o] = g;
             if (dup_rank) dup_rank[o] = (int32_t)(i - v * n);
             o++;
         }
+    }
 }
 
 // Tile [start, end) ranges of the sorted pairs of one sort group (pairs
@@ -806,13 +859,13 @@ static inline unsigned grid_for(int64_t n, int block) {
 size_t raster_smem_bytes() { return sizeof(WarpSmem) * kRasterWarps; }
 
 cudaError_t launch_preprocess(const potr_splats &sp, const CamBatch &cams, int nview,
-                              int tiles_x, int all_colors, const DepthKey &dk, SplatRec *rec,
-                              uint64_t *key, int32_t *cnt, int32_t *vidx,
+                              int tiles_x, int all_colors, int cull, const DepthKey &dk,
+                              SplatRec *rec, uint64_t *key, int32_t *cnt, int32_t *vidx,
                               unsigned long long *counters, cudaStream_t st) {
     if (sp.n == 0) return cudaSuccess;
     k_preprocess<<<grid_for(sp.n * nview, 128), 128, 0, st>>>(sp, cams, nview, tiles_x,
-                                                               all_colors, dk, rec, key, cnt,
-                                                               vidx, counters);
+                                                               all_colors, cull, dk, rec, key,
+                                                               cnt, vidx, counters);
     return cudaGetLastError();
 }
 
@@ -982,14 +1035,17 @@ cudaError_t scan_temp(int64_t n, size_t *bytes) {
 
 cudaError_t launch_duplicate(int64_t total, int64_t n, const int32_t *ids, const int64_t *offs,
                              const SplatRec *rec, int tiles_x, int ntiles, int sb, bool key16,
-                             void *tkey, int32_t *dup_gid, int32_t *dup_rank, cudaStream_t st) {
+                             int cull, void *tkey, int32_t *dup_gid, int32_t *dup_rank,
+                             cudaStream_t st) {
     if (total == 0) return cudaSuccess;
     if (key16)
         k_duplicate<uint16_t><<<grid_for(total, 256), 256, 0, st>>>(
-            total, n, ids, offs, rec, tiles_x, ntiles, sb, (uint16_t *)tkey, dup_gid, dup_rank);
+            total, n, ids, offs, rec, tiles_x, ntiles, sb, cull, (uint16_t *)tkey, dup_gid,
+            dup_rank);
     else
         k_duplicate<uint32_t><<<grid_for(total, 256), 256, 0, st>>>(
-            total, n, ids, offs, rec, tiles_x, ntiles, sb, (uint32_t *)tkey, dup_gid, dup_rank);
+            total, n, ids, offs, rec, tiles_x, ntiles, sb, cull, (uint32_t *)tkey, dup_gid,
+            dup_rank);
     return cudaGetLastError();
 }
 

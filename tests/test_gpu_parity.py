@@ -449,6 +449,39 @@ def test_depth_key_ties_vs_oracle(R, oracle, n_long):
     np.testing.assert_allclose(st.delta_mse, dm, rtol=1e-8, atol=1e-22)
 
 
+def test_tile_cull_bit_identical(R):
+    """Culling (tile, splat) pairs by the prefilter ellipse never changes a
+    bit of the renders or contribution records (no composited sample is
+    dropped); the scores move only by the changed add order inside the
+    per-(tile, splat) sums (chunk boundaries shift)."""
+    from paper_2601_14821_b200 import _native, device
+    from paper_2601_14821_b200.fixture import make_fixture
+    ctx = device.context()
+    scenes = [small_scene(), _stress_scene(), _depth_tie_scene(3),
+              make_fixture(20000, 3, 2, width=160, height=120)]
+    for splats, cams in scenes:
+        out = []
+        for cull in (1, 0):
+            ctx.call("potr_set_option", _native.OPT_TILE_CULL, cull)
+            try:
+                tg = R.render_targets(splats, cams)
+                st = R.compute_delta_mse(perturbed(splats), cams, tg)
+                rec = R.render_with_records(splats, cams[0])
+            finally:
+                ctx.call("potr_set_option", _native.OPT_TILE_CULL, 1)
+            out.append((tg, st, rec))
+        (t1, s1, r1), (t0, s0, r0) = out
+        for a, b in zip(t1, t0):
+            assert np.array_equal(a, b)
+        np.testing.assert_allclose(s1.importance, s0.importance, rtol=1e-12, atol=1e-30)
+        np.testing.assert_allclose(s1.delta_mse, s0.delta_mse, rtol=1e-9, atol=1e-24)
+        np.testing.assert_allclose(np.asarray(s1.camera_importance),
+                                   np.asarray(s0.camera_importance), rtol=1e-12, atol=1e-30)
+        assert s1.mse == s0.mse
+        for f in ("splat_ids", "pixels", "alphas", "trans_at", "partials", "colors"):
+            assert np.array_equal(getattr(r1, f), getattr(r0, f))
+
+
 @pytest.mark.slow
 def test_large_scene_views_vs_oracle(R, oracle):
     """300k splats at 800x800 (the C2 shape), two views, against the oracle."""
