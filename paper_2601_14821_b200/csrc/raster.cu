@@ -46,27 +46,46 @@ namespace potr {
 // without it (scores up to the add order of the per-(tile, splat) sums).
 // Near-degenerate conics keep the full bbox row.
 constexpr double kCullMarginPower = 1e-6;
-constexpr double kCullMarginPixel = 1e-6;
+constexpr double kCullMarginPixel = 1e-3;  // covers the fp32 sqrt below (|x| < 1e4 px)
 
-__device__ __forceinline__ bool row_span(const SplatRec &r, int ty, int *c0, int *c1) {
-    const int py0 = max(ty * kTileH, r.y0), py1 = min(ty * kTileH + kTileH - 1, r.y1);
-    if (py0 > py1 || r.x0 > r.x1) return false;
-    int px0 = r.x0, px1 = r.x1;
+// The per-splat part of the test, computed once per (splat, view).
+struct CullEllipse {
+    double mx, my, b, inv_a, aR, det, ymax, sdy;
+    int x0, x1, y0, y1;
+    bool none, full;  // none: no sample passes; full: degenerate conic, keep the bbox rows
+};
+
+__device__ __forceinline__ CullEllipse cull_ellipse(const SplatRec &r) {
+    CullEllipse e;
+    e.mx = r.mx, e.my = r.my, e.b = r.ib;
+    e.x0 = r.x0, e.x1 = r.x1, e.y0 = r.y0, e.y1 = r.y1;
     const double R = -2.0 * (r.pthr - kCullMarginPower);
-    if (!(R > 0.0)) return false;  // pthr >= margin > 0 >= power: nothing passes
-    const double a = r.ia, b = r.ib, c = r.ic;
-    const double det = a * c - b * b;
-    if (a > 0.0 && c > 0.0 && det > 1e-4 * (a * c) && isfinite(R) && isfinite(det)) {
-        const double d0 = (double)py0 + 0.5 - r.my, d1 = (double)py1 + 0.5 - r.my;
-        const double ymax = sqrt(R * a / det);
-        const double lo = fmax(d0, -ymax), hi = fmin(d1, ymax);
+    e.none = !(R > 0.0) || r.x0 > r.x1;  // pthr >= margin > 0 >= power: nothing passes
+    const double a = r.ia, c = r.ic;
+    e.det = a * c - e.b * e.b;
+    e.full = !(a > 0.0 && c > 0.0 && e.det > 1e-4 * (a * c) && isfinite(R) && isfinite(e.det));
+    e.inv_a = 1.0 / a;
+    e.aR = a * R;
+    e.ymax = sqrt(R * a / e.det);
+    e.sdy = e.b * sqrt(R / (e.det * c));
+    return e;
+}
+
+__device__ __forceinline__ bool row_span(const CullEllipse &e, int ty, int *c0, int *c1) {
+    const int py0 = max(ty * kTileH, e.y0), py1 = min(ty * kTileH + kTileH - 1, e.y1);
+    if (py0 > py1 || e.none) return false;
+    int px0 = e.x0, px1 = e.x1;
+    if (!e.full) {
+        const double d0 = (double)py0 + 0.5 - e.my, d1 = (double)py1 + 0.5 - e.my;
+        const double lo = fmax(d0, -e.ymax), hi = fmin(d1, e.ymax);
         if (lo > hi + kCullMarginPixel) return false;
-        const double sdy = b * sqrt(R / (det * c));
-        const double ya = fmin(fmax(-sdy, lo), hi), yb = fmin(fmax(sdy, lo), hi);
-        const double xmax = (-b * ya + sqrt(fmax(a * R - det * ya * ya, 0.0))) / a;
-        const double xmin = (-b * yb - sqrt(fmax(a * R - det * yb * yb, 0.0))) / a;
-        const double e0 = ceil(r.mx + xmin - 0.5 - kCullMarginPixel);
-        const double e1 = floor(r.mx + xmax - 0.5 + kCullMarginPixel);
+        const double ya = fmin(fmax(-e.sdy, lo), hi), yb = fmin(fmax(e.sdy, lo), hi);
+        const double sa = (double)sqrtf((float)fmax(e.aR - e.det * ya * ya, 0.0));
+        const double sb = (double)sqrtf((float)fmax(e.aR - e.det * yb * yb, 0.0));
+        const double xmax = (sa - e.b * ya) * e.inv_a;
+        const double xmin = (-sb - e.b * yb) * e.inv_a;
+        const double e0 = ceil(e.mx + xmin - 0.5 - kCullMarginPixel);
+        const double e1 = floor(e.mx + xmax - 0.5 + kCullMarginPixel);
         if (e0 > (double)px0) px0 = e0 > (double)px1 ? px1 + 1 : (int)e0;
         if (e1 < (double)px1) px1 = e1 < (double)px0 ? px0 - 1 : (int)e1;
         if (px0 > px1) return false;
@@ -154,9 +173,10 @@ __global__ void __launch_bounds__(128) k_preprocess(potr_splats sp, CamBatch cam
             if (!draw) r.x0 = 1, r.x1 = 0;  // empty: never drawn
             rec[g] = r;
             if (draw && cull) {
+                const CullEllipse ce = cull_ellipse(r);
                 for (int ty = r.y0 >> kTileHLog2; ty <= (r.y1 >> kTileHLog2); ty++) {
                     int t0, t1;
-                    if (row_span(r, ty, &t0, &t1)) c += t1 - t0 + 1;
+                    if (row_span(ce, ty, &t0, &t1)) c += t1 - t0 + 1;
                 }
             }
         }
@@ -228,10 +248,11 @@ __global__ void k_duplicate(int64_t total, int64_t n, const int32_t *__restrict_
     const int tx0 = R.x0 >> kTileWLog2, tx1 = R.x1 >> kTileWLog2;
     const int ty0 = R.y0 >> kTileHLog2, ty1 = R.y1 >> kTileHLog2;
     const uint32_t tbase = (uint32_t)((v % sb) * ntiles);
-    const SplatRec r = R;
+    CullEllipse ce;
+    if (cull) ce = cull_ellipse(R);
     for (int ty = ty0; ty <= ty1; ty++) {
         int c0 = tx0, c1 = tx1;
-        if (cull && !row_span(r, ty, &c0, &c1)) continue;
+        if (cull && !row_span(ce, ty, &c0, &c1)) continue;
         for (int tx = c0; tx <= c1; tx++) {
             tkey[o] = (KeyT)(tbase + (uint32_t)(ty * tiles_x + tx));
             dup_gid[o] = g;
