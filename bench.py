@@ -156,6 +156,21 @@ OPS_PER_E = 24 + 2 * 20
 OPS_PER_M = 37
 
 
+def load_traffic(views_per_launch):
+    """DRAM bytes (read + write) per k_raster<kScore> launch from the committed
+    `ncu --set full` capture summary (profiles/raster_traffic.json), scaled to
+    this run's views per launch; (None, None) without one."""
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles",
+                        "raster_traffic.json")
+    try:
+        with open(path) as f:
+            t = json.load(f)
+        per_view = float(t["dram_bytes_per_launch"]) / float(t["views_per_launch"])
+        return per_view * views_per_launch, t.get("source")
+    except (OSError, ValueError, KeyError):
+        return None, None
+
+
 def fp64_peak_lane_ops(peaks):
     # B200: 148 SMs x 64 FP64 lanes/clk at the max SM clock -- nominal; the
     # MEASURED_PEAKS.json figures are HBM copy and bf16 tensor only.
@@ -314,6 +329,14 @@ def main():
     counts = ctx.counters_read()
     ctx.counters(False)
 
+    if os.environ.get("POTR_PROFILE_STEP"):
+        # one step bracketed for `ncu --profile-from-start off` (launch list of the step)
+        torch.cuda.synchronize()
+        torch.cuda.cudart().cudaProfilerStart()
+        step()
+        torch.cuda.synchronize()
+        torch.cuda.cudart().cudaProfilerStop()
+
     for _ in range(args.warmup):
         step()
     barrier()
@@ -352,8 +375,10 @@ def main():
     raster_avg_ms = raster_ms / max(1, raster_n)
     achieved = ops_per_launch / (raster_avg_ms / 1000.0) / 1e12
     peak = fp64_peak_lane_ops(peaks)
+    traffic, traffic_src = load_traffic(views_per_launch)
     roofline = {"bound": "fp64", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                "frac": achieved / peak, "traffic": None, "kernel": "k_raster<kScore>",
+                "frac": achieved / peak, "traffic": traffic, "traffic_source": traffic_src,
+                "kernel": "k_raster<kScore>",
                 "unit_note": "FP64 lane-operations per second, FMA = 1 (SURVEY.md 8(d) model: "
                              "W = 24E + 37M + 2E exp at 20 DFMA each, per view)",
                 "peak_source": "nominal FP64 CUDA-core rate at sm_max_mhz (148 SMs x 64 lanes/clk);"
