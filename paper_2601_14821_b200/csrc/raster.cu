@@ -61,7 +61,7 @@ __device__ __forceinline__ CullEllipse cull_ellipse(const SplatRec &r) {
     e.x0 = r.x0, e.x1 = r.x1, e.y0 = r.y0, e.y1 = r.y1;
     const double R = -2.0 * (r.pthr - kCullMarginPower);
     e.none = !(R > 0.0) || r.x0 > r.x1;  // pthr >= margin > 0 >= power: nothing passes
-    const double a = r.ia, c = r.ic;
+    const double a = -2.0 * r.ha, c = -2.0 * r.hc;
     e.det = a * c - e.b * e.b;
     e.full = !(a > 0.0 && c > 0.0 && e.det > 1e-4 * (a * c) && isfinite(R) && isfinite(e.det));
     e.inv_a = 1.0 / a;
@@ -156,9 +156,10 @@ __global__ void __launch_bounds__(128) k_preprocess(potr_splats sp, CamBatch cam
             SplatRec r;
             r.mx = pr.mx;
             r.my = pr.my;
-            r.ia = pr.c / det;
+            // -0.5 * (a dx^2 + c dy^2) == ha dx^2 + hc dy^2 exactly (power-of-two scale)
+            r.ha = -0.5 * (pr.c / det);
             r.ib = -pr.b / det;
-            r.ic = pr.a / det;
+            r.hc = -0.5 * (pr.a / det);
             r.opac = o;
             double rgb[3];
             splat_color(pos, sp.sh + 48 * k, cam, rgb);
@@ -396,12 +397,12 @@ __device__ __forceinline__ unsigned live_mask(const ChunkBuf &B, int cnt, int ox
 // alpha < ALPHA_FLOOR (the sample is skipped and T is untouched).
 __device__ __forceinline__ bool eval_alpha(const ChunkBuf &B, int e, double pxc, double pyc,
                                            unsigned tab, double &alpha) {
-    const double2 m = B.f[0][e], ab = B.f[1][e], co = B.f[2][e];
-    const double pthr = B.f[4][e].y;
+    const double2 m = B.f[0][e], ab = B.f[1][e], cp = B.f[2][e];
     const double dx = pxc - m.x, dy = pyc - m.y;
-    const double power = -0.5 * (ab.x * dx * dx + co.x * dy * dy) - ab.y * dx * dy;
-    if (power < pthr) return false;  // o*exp(power) < ALPHA_FLOOR for certain
-    alpha = co.y * exp_neg(power, tab);
+    // -0.5 * (a dx dx + c dy dy) - b dx dy, with the -0.5 folded into ha, hc
+    const double power = (ab.x * dx * dx + cp.x * dy * dy) - ab.y * dx * dy;
+    if (power < cp.y) return false;  // o*exp(power) < ALPHA_FLOOR for certain
+    alpha = B.f[3][e].x * exp_neg(power, tab);
     if (alpha > kCompositeK[0]) alpha = kCompositeK[0];
     return !(alpha < kCompositeK[1]);
 }
@@ -568,12 +569,12 @@ __global__ void __launch_bounds__(32 * kRasterWarps, POTR_RASTER_MIN_BLOCKS) k_r
                             a.rec_p[3 * slot + 2] = P2;
                         }
                     }
-                    const double2 c01 = B.f[3][e];
-                    const double c2 = B.f[4][e].x;
+                    const double c0 = B.f[3][e].y;
+                    const double2 c12 = B.f[4][e];
                     const double w = T * alpha;
-                    P0 += w * c01.x;
-                    P1 += w * c01.y;
-                    P2 += w * c2;
+                    P0 += w * c0;
+                    P1 += w * c12.x;
+                    P2 += w * c12.y;
                     T = T * (1.0 - alpha);
                     if (T < kCompositeK[2]) {  // every later sample is skipped (:162-164)
                         done = true;
@@ -670,23 +671,23 @@ __global__ void __launch_bounds__(32 * kRasterWarps, POTR_RASTER_MIN_BLOCKS) k_r
                         const bool ok = eval_alpha(B, e, pxc, pyc, tab_s, alpha);
                         if (ok) {
                             key = e;
-                            const double2 c01 = B.f[3][e];
-                            const double c2 = B.f[4][e].x;
+                            const double c0 = B.f[3][e].y;
+                            const double2 c12 = B.f[4][e];
                             if (MODE == kScore) {
                                 // prune_deltas, forward form: a/(1-a) * (P_K - P_i - T c)
                                 const double f = alpha * rcp_nr(1.0 - alpha);
-                                const double pd0 = f * (PK0 - P0 - T * c01.x);
-                                const double pd1 = f * (PK1 - P1 - T * c01.y);
-                                const double pd2 = f * (PK2 - P2 - T * c2);
+                                const double pd0 = f * (PK0 - P0 - T * c0);
+                                const double pd1 = f * (PK1 - P1 - T * c12.x);
+                                const double pd2 = f * (PK2 - P2 - T * c12.y);
                                 dse = pd0 * pd0 + 2.0 * pd0 * dr0;
                                 dse = dse + (pd1 * pd1 + 2.0 * pd1 * dr1);
                                 dse = dse + (pd2 * pd2 + 2.0 * pd2 * dr2);
                             }
                             const double w = T * alpha;
                             timp = w;
-                            P0 += w * c01.x;
-                            P1 += w * c01.y;
-                            P2 += w * c2;
+                            P0 += w * c0;
+                            P1 += w * c12.x;
+                            P2 += w * c12.y;
                             T = T * (1.0 - alpha);
                             if (T < kCompositeK[2]) {
                                 done = true;
