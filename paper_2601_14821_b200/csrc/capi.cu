@@ -47,7 +47,7 @@ struct potr_ctx {
     bool counting = false;
     DevBuf counters;
     int64_t pairs_total = 0;
-    DevBuf tile_counter, sid, ci_v, dm_v, bbox, overflow, vidx, khi, skhi;
+    DevBuf tile_counter, sid, ci_v, dm_v, bbox, overflow, vidx, khi, skhi, prep;
     bool depth_split = false;  // last bin_batch sorted split keys: skey not materialised
     double scene_lo[3] = {0, 0, 0}, scene_hi[3] = {0, 0, 0};  // splat position bbox
     uint64_t invalid_key0 = ~0ull;  // depth key of an invalid splat in view 0 of the last batch
@@ -225,7 +225,15 @@ int bitlen(uint64_t x) {
 
 // Axis-aligned bounds of the splat centres (one reduction + sync per call):
 // they bound every view's depth range, which makes the batch depth key compact.
+// Once per call of a binning entry point: the splats' position bounds (for the
+// compact depth key) and their view-independent terms (k_splat_prep).
 int compute_scene_bounds(potr_ctx *ctx, const potr_splats &sp) {
+    ENSURE(ctx->prep, sizeof(SplatPrep) * (sp.n > 0 ? sp.n : 1));
+    {
+        Stage _st(ctx, POTR_STAGE_PREPROCESS);
+        LAUNCH(1, launch_splat_prep(sp, P<SplatPrep>(ctx->prep), ctx->stream));
+        _st.end();
+    }
     ENSURE(ctx->bbox, 6 * sizeof(unsigned long long));
     LAUNCH(1, launch_bbox(sp.n, sp.positions, P<unsigned long long>(ctx->bbox), ctx->stream));
     CK(cudaMemcpyAsync(ctx->pinned, ctx->bbox.p, 6 * sizeof(uint64_t), cudaMemcpyDeviceToHost,
@@ -335,7 +343,7 @@ int bin_batch(potr_ctx *ctx, const potr_splats &sp, const potr_camera *cams, int
 
     {
         Stage _st(ctx, POTR_STAGE_PREPROCESS);
-        LAUNCH(1, launch_preprocess(sp, cb, nview, g.tiles_x, all_colors ? 1 : 0, cull ? 1 : 0, dk,
+        LAUNCH(1, launch_preprocess(sp, P<SplatPrep>(ctx->prep), cb, nview, g.tiles_x, all_colors ? 1 : 0, cull ? 1 : 0, dk,
                                     P<SplatRec>(ctx->rec), P<uint64_t>(ctx->key),
                                     P<int32_t>(ctx->cnt), P<int32_t>(ctx->vidx), counters(ctx),
                                     ctx->stream));
@@ -592,6 +600,7 @@ void potr_destroy(potr_ctx *ctx) {
     if (ctx->dm_v.p) cudaFree(ctx->dm_v.p);
     if (ctx->sid.p) cudaFree(ctx->sid.p);
     if (ctx->khi.p) cudaFree(ctx->khi.p);
+    if (ctx->prep.p) cudaFree(ctx->prep.p);
     if (ctx->skhi.p) cudaFree(ctx->skhi.p);
     for (auto &ev : ctx->events) {
         cudaEventDestroy(ev.second.first);

@@ -164,8 +164,15 @@ struct Proj {
     bool valid;
 };
 
-// Sigma = R diag(s^2) R^T (rasterizer.py:75-76, quat_to_rotmat :40-53): view
-// independent, so a batch computes it once per splat.
+// View-independent per-splat terms, computed once per call (k_splat_prep)
+// and read by the preprocess of every view batch.
+struct __align__(16) SplatPrep {
+    double S[9];  // Sigma, all nine entries (the sums are not exactly symmetric)
+    double pthr;  // log(ALPHA_FLOOR / opacity) - margin
+};
+static_assert(sizeof(SplatPrep) == 80, "SplatPrep must stay 80 bytes");
+
+// Sigma = R diag(s^2) R^T (rasterizer.py:75-76, quat_to_rotmat :40-53).
 __device__ __forceinline__ void splat_sigma(const double *__restrict__ s,
                                             const double *__restrict__ q, double *S) {
     double w = q[0], x = q[1], y = q[2], z = q[3];

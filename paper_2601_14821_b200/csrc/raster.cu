@@ -97,7 +97,31 @@ __device__ __forceinline__ bool row_span(const CullEllipse &e, int ty, int *c0, 
 
 // One thread per (splat, view) of the batch; the views of a splat are adjacent
 // threads, so its attributes come from one cache line fetch.
-__global__ void __launch_bounds__(128) k_preprocess(potr_splats sp, CamBatch cams, int nview,
+__global__ void k_splat_prep(int64_t n, const double *__restrict__ scales,
+                             const double *__restrict__ rotations,
+                             const double *__restrict__ opacities, SplatPrep *__restrict__ prep) {
+    const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= n) return;
+    double scl[3], rot[4];
+#pragma unroll
+    for (int i = 0; i < 3; i++) scl[i] = scales[3 * k + i];
+#pragma unroll
+    for (int i = 0; i < 4; i++) rot[i] = rotations[4 * k + i];
+    SplatPrep p;
+    splat_sigma(scl, rot, p.S);
+    p.pthr = log(kAlphaFloor / opacities[k]) - kPowerMargin;
+    prep[k] = p;
+}
+
+cudaError_t launch_splat_prep(const potr_splats &sp, SplatPrep *prep, cudaStream_t st) {
+    if (sp.n == 0) return cudaSuccess;
+    k_splat_prep<<<(unsigned)((sp.n + 127) / 128), 128, 0, st>>>(sp.n, sp.scales, sp.rotations,
+                                                                 sp.opacities, prep);
+    return cudaGetLastError();
+}
+
+__global__ void __launch_bounds__(128) k_preprocess(potr_splats sp, const SplatPrep *__restrict__ prep,
+                                                     CamBatch cams, int nview,
                                                      int tiles_x, int all_colors, int cull,
                                                      DepthKey dk,
                                                      SplatRec *__restrict__ rec,
@@ -112,16 +136,19 @@ __global__ void __launch_bounds__(128) k_preprocess(potr_splats sp, CamBatch cam
     const int v = (int)(t - k * nview);
     const Cam &cam = cams.cam[v];
     const int64_t g = (int64_t)v * n + k;
-    double pos[3], scl[3], rot[4];
+    double pos[3], Sig[9];
 #pragma unroll
-    for (int i = 0; i < 3; i++) {
-        pos[i] = __ldg(sp.positions + 3 * k + i);
-        scl[i] = __ldg(sp.scales + 3 * k + i);
+    for (int i = 0; i < 3; i++) pos[i] = __ldg(sp.positions + 3 * k + i);
+    const double2 *pp = reinterpret_cast<const double2 *>(prep + k);
+#pragma unroll
+    for (int i = 0; i < 4; i++) {
+        const double2 v = __ldg(pp + i);
+        Sig[2 * i] = v.x;
+        Sig[2 * i + 1] = v.y;
     }
-#pragma unroll
-    for (int i = 0; i < 4; i++) rot[i] = __ldg(sp.rotations + 4 * k + i);
-    double Sig[9];
-    splat_sigma(scl, rot, Sig);
+    const double2 v4 = __ldg(pp + 4);
+    Sig[8] = v4.x;
+    const double pthr = v4.y;
     const Proj pr = project_sigma(pos, Sig, cam);
     int32_t c = 0;
     uint64_t kk = dk.compact ? ((uint64_t)v << dk.nbits) | dk.sentinel : ~0ull;
@@ -166,7 +193,7 @@ __global__ void __launch_bounds__(128) k_preprocess(potr_splats sp, CamBatch cam
             r.cr = rgb[0];
             r.cg = rgb[1];
             r.cb = rgb[2];
-            r.pthr = log(kAlphaFloor / o) - kPowerMargin;
+            r.pthr = pthr;  // log(kAlphaFloor / o) - kPowerMargin, from k_splat_prep
             r.x0 = (int32_t)x0;
             r.x1 = (int32_t)x1;
             r.y0 = (int32_t)y0;
@@ -880,12 +907,13 @@ static inline unsigned grid_for(int64_t n, int block) {
 
 size_t raster_smem_bytes() { return sizeof(WarpSmem) * kRasterWarps; }
 
-cudaError_t launch_preprocess(const potr_splats &sp, const CamBatch &cams, int nview,
+cudaError_t launch_preprocess(const potr_splats &sp, const SplatPrep *prep, const CamBatch &cams,
+                              int nview,
                               int tiles_x, int all_colors, int cull, const DepthKey &dk,
                               SplatRec *rec, uint64_t *key, int32_t *cnt, int32_t *vidx,
                               unsigned long long *counters, cudaStream_t st) {
     if (sp.n == 0) return cudaSuccess;
-    k_preprocess<<<grid_for(sp.n * nview, 128), 128, 0, st>>>(sp, cams, nview, tiles_x,
+    k_preprocess<<<grid_for(sp.n * nview, 128), 128, 0, st>>>(sp, prep, cams, nview, tiles_x,
                                                                all_colors, cull, dk, rec, key,
                                                                cnt, vidx, counters);
     return cudaGetLastError();

@@ -50,7 +50,10 @@ struct DepthKey {
 
 cudaError_t launch_bbox(int64_t n, const double *pos, unsigned long long *out, cudaStream_t st);
 
-cudaError_t launch_preprocess(const potr_splats &sp, const CamBatch &cams, int nview,
+// Per-splat view-independent terms (Sigma, prefilter threshold), once per call.
+cudaError_t launch_splat_prep(const potr_splats &sp, SplatPrep *prep, cudaStream_t st);
+cudaError_t launch_preprocess(const potr_splats &sp, const SplatPrep *prep, const CamBatch &cams,
+                              int nview,
                               int tiles_x, int all_colors, int cull, const DepthKey &dk,
                               SplatRec *rec, uint64_t *key, int32_t *cnt, int32_t *vidx,
                               unsigned long long *counters, cudaStream_t st);
