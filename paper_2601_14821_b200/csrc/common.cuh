@@ -108,15 +108,16 @@ __device__ __forceinline__ double exp_neg(double x, unsigned tab_s) {
 
 // Per-view splat record, 96 bytes, written by the preprocess kernel and read
 // per (tile, splat) pair by the rasterizer.
-// Six 16-byte fields, ordered for the rasterizer: the exponent and its
-// prefilter need the first three, a composited sample the next two.
+// Six 16-byte fields: the exponent and its prefilter need the first three,
+// a composited sample the last two; the duplicate kernel's cull test reads
+// only the first 64 bytes (two sectors).
 struct __align__(16) SplatRec {
     double mx, my;      // mean2d
     double ha, ib;      // conic (a, b, c) = (c, -b, a) / det (rasterizer.py:149-154): ha = -a/2
     double hc, pthr;    // hc = -c/2; pthr = log(ALPHA_FLOOR / opac) - margin
+    int32_t x0, x1, y0, y1;  // clipped pixel bbox (:135-148), inclusive
     double opac, cr;    // opacity, compositing colour clamped at 0 (:100-110)
     double cg, cb;
-    int32_t x0, x1, y0, y1;  // clipped pixel bbox (:135-148), inclusive
 };
 static_assert(sizeof(SplatRec) == 96, "SplatRec must stay 96 bytes");
 

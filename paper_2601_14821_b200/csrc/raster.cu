@@ -120,7 +120,12 @@ cudaError_t launch_splat_prep(const potr_splats &sp, SplatPrep *prep, cudaStream
     return cudaGetLastError();
 }
 
-__global__ void __launch_bounds__(128) k_preprocess(potr_splats sp, const SplatPrep *__restrict__ prep,
+#ifdef POTR_PRE_MIN_BLOCKS
+#define POTR_PRE_BOUNDS __launch_bounds__(128, POTR_PRE_MIN_BLOCKS)
+#else
+#define POTR_PRE_BOUNDS __launch_bounds__(128)
+#endif
+__global__ void POTR_PRE_BOUNDS k_preprocess(potr_splats sp, const SplatPrep *__restrict__ prep,
                                                      CamBatch cams, int nview,
                                                      int tiles_x, int all_colors, int cull,
                                                      DepthKey dk,
@@ -322,7 +327,7 @@ __global__ void k_iota(int64_t n, int32_t *out) {
 constexpr int kMaskChunks = 16;  // chunks per tile whose per-lane contribution masks are kept
 
 struct ChunkBuf {
-    double2 f[6][32];  // (mx,my) (ia,ib) (ic,opac) (cr,cg) (cb,pthr) bbox(int4)
+    double2 f[6][32];  // (mx,my) (ha,ib) (hc,pthr) bbox(int4) (opac,cr) (cg,cb)
     int32_t dup[32];
 };
 
@@ -386,7 +391,7 @@ __device__ __forceinline__ void issue_chunk(const RasterArgs &a, ChunkBuf &B, co
 }
 
 __device__ __forceinline__ int4 bbox_of(const ChunkBuf &B, int e) {
-    return *reinterpret_cast<const int4 *>(&B.f[5][e]);
+    return *reinterpret_cast<const int4 *>(&B.f[3][e]);
 }
 
 // Entries of this chunk whose clipped bbox (rasterizer.py:135-148) contains
@@ -429,7 +434,7 @@ __device__ __forceinline__ bool eval_alpha(const ChunkBuf &B, int e, double pxc,
     // -0.5 * (a dx dx + c dy dy) - b dx dy, with the -0.5 folded into ha, hc
     const double power = (ab.x * dx * dx + cp.x * dy * dy) - ab.y * dx * dy;
     if (power < cp.y) return false;  // o*exp(power) < ALPHA_FLOOR for certain
-    alpha = B.f[3][e].x * exp_neg(power, tab);
+    alpha = B.f[4][e].x * exp_neg(power, tab);
     if (alpha > kCompositeK[0]) alpha = kCompositeK[0];
     return !(alpha < kCompositeK[1]);
 }
@@ -596,8 +601,8 @@ __global__ void __launch_bounds__(32 * kRasterWarps, POTR_RASTER_MIN_BLOCKS) k_r
                             a.rec_p[3 * slot + 2] = P2;
                         }
                     }
-                    const double c0 = B.f[3][e].y;
-                    const double2 c12 = B.f[4][e];
+                    const double c0 = B.f[4][e].y;
+                    const double2 c12 = B.f[5][e];
                     const double w = T * alpha;
                     P0 += w * c0;
                     P1 += w * c12.x;
@@ -698,8 +703,8 @@ __global__ void __launch_bounds__(32 * kRasterWarps, POTR_RASTER_MIN_BLOCKS) k_r
                         const bool ok = eval_alpha(B, e, pxc, pyc, tab_s, alpha);
                         if (ok) {
                             key = e;
-                            const double c0 = B.f[3][e].y;
-                            const double2 c12 = B.f[4][e];
+                            const double c0 = B.f[4][e].y;
+                            const double2 c12 = B.f[5][e];
                             if (MODE == kScore) {
                                 // prune_deltas, forward form: a/(1-a) * (P_K - P_i - T c)
                                 const double f = alpha * rcp_nr(1.0 - alpha);
