@@ -439,6 +439,17 @@ __device__ __forceinline__ bool eval_alpha(const ChunkBuf &B, int e, double pxc,
     return !(alpha < kCompositeK[1]);
 }
 
+// eval_alpha for a sample pass 1 already composited (its tests passed): the
+// same arithmetic, so the same bits, without the tests.
+__device__ __forceinline__ double known_alpha(const ChunkBuf &B, int e, double pxc, double pyc,
+                                              unsigned tab) {
+    const double2 m = B.f[0][e], ab = B.f[1][e], cp = B.f[2][e];
+    const double dx = pxc - m.x, dy = pyc - m.y;
+    const double power = (ab.x * dx * dx + cp.x * dy * dy) - ab.y * dx * dy;
+    const double alpha = B.f[4][e].x * exp_neg(power, tab);
+    return alpha > kCompositeK[0] ? kCompositeK[0] : alpha;
+}
+
 // Deterministic segmented sum over the lanes that hold the same key: pointer
 // jumping along each group's members in lane order leaves the group total in
 // its lowest lane.  The add order depends only on group membership.
@@ -662,8 +673,10 @@ __global__ void __launch_bounds__(32 * kRasterWarps, POTR_RASTER_MIN_BLOCKS) k_r
             image[3 * pix + 2] = PK2;
         }
         if (inside && trans) trans[pix] = T;
+        // the replay carries Q = P_K - P_i (the colour still to come) and 2 dr
+        P0 = PK0, P1 = PK1, P2 = PK2;
+        dr0 = 2.0 * dr0, dr1 = 2.0 * dr1, dr2 = 2.0 * dr2;
         T = 1.0;
-        P0 = P1 = P2 = 0.0;
         done = !inside;
         int written = start;
         if (start < stop) {
@@ -700,26 +713,29 @@ __global__ void __launch_bounds__(32 * kRasterWarps, POTR_RASTER_MIN_BLOCKS) k_r
                         const int e = __ffs(m) - 1;
                         m &= m - 1u;
                         double alpha = 0.0;
-                        const bool ok = eval_alpha(B, e, pxc, pyc, tab_s, alpha);
+                        bool ok = true;
+                        if (known) alpha = known_alpha(B, e, pxc, pyc, tab_s);
+                        else ok = eval_alpha(B, e, pxc, pyc, tab_s, alpha);
                         if (ok) {
                             key = e;
                             const double c0 = B.f[4][e].y;
                             const double2 c12 = B.f[5][e];
                             if (MODE == kScore) {
-                                // prune_deltas, forward form: a/(1-a) * (P_K - P_i - T c)
+                                // prune_deltas, forward form: a/(1-a) * (P_K - P_i - T c),
+                                // dSE = |pd|^2 + 2 pd . dr (rasterizer.py:232-243, :333)
                                 const double f = alpha * rcp_nr(1.0 - alpha);
-                                const double pd0 = f * (PK0 - P0 - T * c0);
-                                const double pd1 = f * (PK1 - P1 - T * c12.x);
-                                const double pd2 = f * (PK2 - P2 - T * c12.y);
-                                dse = pd0 * pd0 + 2.0 * pd0 * dr0;
-                                dse = dse + (pd1 * pd1 + 2.0 * pd1 * dr1);
-                                dse = dse + (pd2 * pd2 + 2.0 * pd2 * dr2);
+                                const double pd0 = f * (P0 - T * c0);
+                                const double pd1 = f * (P1 - T * c12.x);
+                                const double pd2 = f * (P2 - T * c12.y);
+                                dse = pd0 * (pd0 + dr0);
+                                dse = dse + pd1 * (pd1 + dr1);
+                                dse = dse + pd2 * (pd2 + dr2);
                             }
                             const double w = T * alpha;
                             timp = w;
-                            P0 += w * c0;
-                            P1 += w * c12.x;
-                            P2 += w * c12.y;
+                            P0 -= w * c0;
+                            P1 -= w * c12.x;
+                            P2 -= w * c12.y;
                             T = T * (1.0 - alpha);
                             if (T < kCompositeK[2]) {
                                 done = true;
