@@ -28,7 +28,10 @@ struct potr_ctx {
     std::string err;
     int64_t launches = 0;
     // per-view workspace
-    DevBuf rec, key, skey, sids, cnt, cnt_sorted, offs, iota, tkey, tskey, perm, dup_id, dup_rank,
+    // dup_id: record of each duplicated pair; perm: tile-sorted slot order;
+    // pair: per sorted pair (slot, record)
+    DevBuf rec, key, skey, sids, cnt, cnt_sorted, offs, iota, tkey, tskey, perm, pair, dup_id,
+        dup_rank,
         partial, ranges, tile_se, temp, nvalid;
     int64_t iota_len = 0;
     // records mode
@@ -47,7 +50,7 @@ struct potr_ctx {
     bool counting = false;
     DevBuf counters;
     int64_t pairs_total = 0;
-    DevBuf tile_counter, sid, ci_v, dm_v, bbox, overflow, vidx, khi, skhi, prep;
+    DevBuf tile_counter, ci_v, dm_v, bbox, overflow, vidx, khi, skhi, prep;
     bool depth_split = false;  // last bin_batch sorted split keys: skey not materialised
     double scene_lo[3] = {0, 0, 0}, scene_hi[3] = {0, 0, 0};  // splat position bbox
     uint64_t invalid_key0 = ~0ull;  // depth key of an invalid splat in view 0 of the last batch
@@ -318,8 +321,7 @@ int bin_batch(potr_ctx *ctx, const potr_splats &sp, const potr_camera *cams, int
     ENSURE(ctx->tile_se, sizeof(double) * ntiles_b);
     ENSURE(ctx->tile_counter, sizeof(int));
     ENSURE(ctx->overflow, 2 * sizeof(int));
-    int rc = ensure_iota(ctx, total);
-    if (rc) return rc;
+    int rc = 0;
     DepthKey dk;
     std::memset(&dk, 0, sizeof(dk));
     dk.overflow = P<int>(ctx->overflow);
@@ -421,8 +423,8 @@ int bin_batch(potr_ctx *ctx, const potr_splats &sp, const potr_camera *cams, int
     ENSURE(ctx->tkey, kbytes * K);
     ENSURE(ctx->tskey, kbytes * K);
     ENSURE(ctx->perm, sizeof(int32_t) * K);
+    ENSURE(ctx->pair, sizeof(int2) * K);
     ENSURE(ctx->dup_id, sizeof(int32_t) * K);
-    ENSURE(ctx->sid, sizeof(int32_t) * K);
     ENSURE(ctx->partial, sizeof(double2) * K);
     if (with_rank) ENSURE(ctx->dup_rank, sizeof(int32_t) * K);
     rc = ensure_iota(ctx, K);
@@ -460,7 +462,7 @@ int bin_batch(potr_ctx *ctx, const potr_splats &sp, const potr_camera *cams, int
                          (char *)ctx->tskey.p + koff, P<int32_t>(ctx->iota) + j0,
                          P<int32_t>(ctx->perm) + j0, kk, sb * g.ntiles, ctx->stream));
             LAUNCH(1, launch_tile_ranges(j0, kk, key16, ctx->tskey.p, P<int32_t>(ctx->perm),
-                                         P<int32_t>(ctx->dup_id), P<int32_t>(ctx->sid),
+                                         P<int32_t>(ctx->dup_id), P<int2>(ctx->pair),
                                          P<int2>(ctx->ranges), v0 * g.ntiles, ctx->stream));
         }
         _st.end();
@@ -474,9 +476,7 @@ RasterArgs raster_args(potr_ctx *ctx, const potr_camera &cam, int nview) {
     RasterArgs a;
     std::memset(&a, 0, sizeof(a));
     a.rec = P<SplatRec>(ctx->rec);
-    a.perm = P<int32_t>(ctx->perm);
-    a.dup_id = P<int32_t>(ctx->dup_id);
-    a.sid = P<int32_t>(ctx->sid);
+    a.pair = P<int2>(ctx->pair);
     a.dup_rank = P<int32_t>(ctx->dup_rank);
     a.ranges = P<int2>(ctx->ranges);
     a.tiles_x = g.tiles_x;
@@ -582,7 +582,8 @@ void potr_destroy(potr_ctx *ctx) {
     cudaStreamSynchronize(ctx->stream);
     DevBuf *bufs[] = {&ctx->rec,     &ctx->key,     &ctx->skey,    &ctx->sids,   &ctx->cnt,
                       &ctx->cnt_sorted, &ctx->offs, &ctx->iota,    &ctx->tkey,   &ctx->tskey,
-                      &ctx->perm,    &ctx->dup_id,  &ctx->dup_rank, &ctx->partial, &ctx->ranges,
+                      &ctx->pair,    &ctx->dup_id,  &ctx->dup_rank, &ctx->partial, &ctx->ranges,
+                      &ctx->perm,
                       &ctx->tile_se, &ctx->temp,    &ctx->nvalid,  &ctx->rkey,   &ctx->rskey,
                       &ctx->rsidx,   &ctx->ralpha,  &ctx->rt,      &ctx->rp,     &ctx->rcounter,
                       &ctx->eyes,    &ctx->neq,     &ctx->h_pos,   &ctx->h_sh,   &ctx->h_op,
@@ -598,7 +599,6 @@ void potr_destroy(potr_ctx *ctx) {
     if (ctx->overflow.p) cudaFree(ctx->overflow.p);
     if (ctx->ci_v.p) cudaFree(ctx->ci_v.p);
     if (ctx->dm_v.p) cudaFree(ctx->dm_v.p);
-    if (ctx->sid.p) cudaFree(ctx->sid.p);
     if (ctx->khi.p) cudaFree(ctx->khi.p);
     if (ctx->prep.p) cudaFree(ctx->prep.p);
     if (ctx->skhi.p) cudaFree(ctx->skhi.p);
@@ -806,8 +806,8 @@ int potr_bin(potr_ctx *ctx, const potr_splats *splats, const potr_camera *cam, i
     LAUNCH(3, launch_bin_outputs(splats->n, P<uint64_t>(ctx->skey), ctx->invalid_key0,
                                  P<int32_t>(ctx->sids),
                                  P<unsigned long long>(ctx->nvalid), order, geom(*cam).ntiles,
-                                 P<int2>(ctx->ranges), K, tile_offsets, P<int32_t>(ctx->perm),
-                                 P<int32_t>(ctx->dup_id), tile_splats, ctx->stream));
+                                 P<int2>(ctx->ranges), K, tile_offsets, P<int2>(ctx->pair),
+                                 tile_splats, ctx->stream));
     CK(cudaMemcpyAsync(ctx->pinned, ctx->nvalid.p, sizeof(int64_t), cudaMemcpyDeviceToHost,
                        ctx->stream));
     CK(cudaStreamSynchronize(ctx->stream));

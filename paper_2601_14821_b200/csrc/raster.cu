@@ -269,7 +269,7 @@ template <typename KeyT>
 __global__ void k_duplicate(int64_t total, int64_t n, const int32_t *__restrict__ ids,
                             const int64_t *__restrict__ offs, const SplatRec *__restrict__ rec,
                             int tiles_x, int ntiles, int sb, int cull, KeyT *__restrict__ tkey,
-                            int32_t *__restrict__ dup_gid, int32_t *__restrict__ dup_rank) {
+                            int32_t *__restrict__ dup_id, int32_t *__restrict__ dup_rank) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= total) return;
     int64_t o = offs[i];
@@ -288,7 +288,7 @@ __global__ void k_duplicate(int64_t total, int64_t n, const int32_t *__restrict_
         if (cull && !row_span(ce, ty, &c0, &c1)) continue;
         for (int tx = c0; tx <= c1; tx++) {
             tkey[o] = (KeyT)(tbase + (uint32_t)(ty * tiles_x + tx));
-            dup_gid[o] = g;
+            dup_id[o] = g;
             if (dup_rank) dup_rank[o] = (int32_t)(i - v * n);
             o++;
         }
@@ -296,17 +296,17 @@ __global__ void k_duplicate(int64_t total, int64_t n, const int32_t *__restrict_
 }
 
 // Tile [start, end) ranges of the sorted pairs of one sort group (pairs
-// [j0, j0 + K) carrying group-local keys; tile index = tbase + key), plus each
-// sorted pair's record index (so the rasterizer's chunk fetch is two loads
-// deep, not three).
+// [j0, j0 + K) carrying group-local keys; tile index = tbase + key), and each
+// sorted pair's (slot, record) for the rasterizer's one 8-byte fetch.
 template <typename KeyT>
 __global__ void k_tile_ranges(int64_t j0, int64_t K, const KeyT *__restrict__ skey,
                               const int32_t *__restrict__ perm, const int32_t *__restrict__ dup_id,
-                              int32_t *__restrict__ sid, int2 *__restrict__ rng, int tbase) {
+                              int2 *__restrict__ pair, int2 *__restrict__ rng, int tbase) {
     const int64_t jj = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (jj >= K) return;
     const int64_t j = j0 + jj;
-    sid[j] = dup_id[perm[j]];
+    const int32_t d = perm[j];
+    pair[j] = make_int2(d, dup_id[d]);
     const uint32_t t = skey[j];
     if (jj == 0 || skey[j - 1] != t) rng[tbase + t].x = (int)j;
     if (jj == K - 1 || skey[j + 1] != t) rng[tbase + t].y = (int)(j + 1);
@@ -372,8 +372,9 @@ __device__ __forceinline__ ChunkIds fetch_ids(const RasterArgs &a, int cbase, in
     ChunkIds c;
     const int j = cbase + lane;
     c.valid = j < end;
-    c.d = c.valid ? a.perm[j] : 0;
-    c.id = c.valid ? a.sid[j] : 0;
+    const int2 p = c.valid ? a.pair[j] : make_int2(0, 0);
+    c.d = p.x;
+    c.id = p.y;
     return c;
 }
 
@@ -754,7 +755,7 @@ __global__ void __launch_bounds__(32 * kRasterWarps, POTR_RASTER_MIN_BLOCKS) k_r
             __syncwarp();
         }
         for (int j = written + lane; j < end; j += 32)
-            a.partial[a.perm[j]] = make_double2(0.0, 0.0);
+            a.partial[a.pair[j].x] = make_double2(0.0, 0.0);
     }
 }
 
@@ -898,10 +899,9 @@ __global__ void k_tile_offsets(int ntiles, const int2 *__restrict__ rng, int64_t
     out[t] = o;
 }
 
-__global__ void k_tile_splats(int64_t K, const int32_t *__restrict__ perm,
-                              const int32_t *__restrict__ dup_id, int32_t *__restrict__ out) {
+__global__ void k_tile_splats(int64_t K, const int2 *__restrict__ pair, int32_t *__restrict__ out) {
     int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (j < K) out[j] = dup_id[perm[j]];
+    if (j < K) out[j] = pair[j].y;
 }
 
 __global__ void k_order_out(int64_t nv, const int32_t *__restrict__ ids, int64_t *__restrict__ out) {
@@ -1106,16 +1106,16 @@ cudaError_t scan_temp(int64_t n, size_t *bytes) {
 
 cudaError_t launch_duplicate(int64_t total, int64_t n, const int32_t *ids, const int64_t *offs,
                              const SplatRec *rec, int tiles_x, int ntiles, int sb, bool key16,
-                             int cull, void *tkey, int32_t *dup_gid, int32_t *dup_rank,
+                             int cull, void *tkey, int32_t *dup_id, int32_t *dup_rank,
                              cudaStream_t st) {
     if (total == 0) return cudaSuccess;
     if (key16)
         k_duplicate<uint16_t><<<grid_for(total, 256), 256, 0, st>>>(
-            total, n, ids, offs, rec, tiles_x, ntiles, sb, cull, (uint16_t *)tkey, dup_gid,
+            total, n, ids, offs, rec, tiles_x, ntiles, sb, cull, (uint16_t *)tkey, dup_id,
             dup_rank);
     else
         k_duplicate<uint32_t><<<grid_for(total, 256), 256, 0, st>>>(
-            total, n, ids, offs, rec, tiles_x, ntiles, sb, cull, (uint32_t *)tkey, dup_gid,
+            total, n, ids, offs, rec, tiles_x, ntiles, sb, cull, (uint32_t *)tkey, dup_id,
             dup_rank);
     return cudaGetLastError();
 }
@@ -1126,6 +1126,8 @@ static int bits_for(int ntiles) {
     return b;
 }
 
+// Stable sort of the pairs by tile key (4-byte values: 8-byte ones measured
+// 10 ms slower per C3 step than the gather in k_tile_ranges).
 cudaError_t tile_sort(void *temp, size_t temp_bytes, bool key16, const void *tkey, void *skey,
                       const int32_t *iota, int32_t *perm, int64_t K, int nkeys, cudaStream_t st) {
     if (K == 0) return cudaSuccess;
@@ -1162,15 +1164,15 @@ cudaError_t records_sort(void *temp, size_t temp_bytes, const uint64_t *key, uin
 }
 
 cudaError_t launch_tile_ranges(int64_t j0, int64_t K, bool key16, const void *skey,
-                               const int32_t *perm, const int32_t *dup_id, int32_t *sid,
-                               int2 *rng, int tbase, cudaStream_t st) {
+                               const int32_t *perm, const int32_t *dup_id, int2 *pair, int2 *rng,
+                               int tbase, cudaStream_t st) {
     if (K == 0) return cudaSuccess;
     if (key16)
         k_tile_ranges<uint16_t><<<grid_for(K, 256), 256, 0, st>>>(
-            j0, K, (const uint16_t *)skey, perm, dup_id, sid, rng, tbase);
+            j0, K, (const uint16_t *)skey, perm, dup_id, pair, rng, tbase);
     else
         k_tile_ranges<uint32_t><<<grid_for(K, 256), 256, 0, st>>>(
-            j0, K, (const uint32_t *)skey, perm, dup_id, sid, rng, tbase);
+            j0, K, (const uint32_t *)skey, perm, dup_id, pair, rng, tbase);
     return cudaGetLastError();
 }
 
@@ -1258,8 +1260,7 @@ cudaError_t launch_bin_outputs(int64_t n, const uint64_t *skey, uint64_t invalid
                                const int32_t *sids,
                                unsigned long long *nvalid_dev, int64_t *order, int ntiles,
                                const int2 *rng, int64_t K, int64_t *tile_offsets,
-                               const int32_t *perm, const int32_t *dup_id, int32_t *tile_splats,
-                               cudaStream_t st) {
+                               const int2 *pair, int32_t *tile_splats, cudaStream_t st) {
     cudaError_t e = cudaMemsetAsync(nvalid_dev, 0, sizeof(unsigned long long), st);
     if (e != cudaSuccess) return e;
     if (n > 0) {
@@ -1269,7 +1270,7 @@ cudaError_t launch_bin_outputs(int64_t n, const uint64_t *skey, uint64_t invalid
     if (tile_offsets) k_tile_offsets<<<grid_for(ntiles + 1, 128), 128, 0, st>>>(ntiles, rng, K,
                                                                                tile_offsets);
     if (tile_splats && K > 0)
-        k_tile_splats<<<grid_for(K, 256), 256, 0, st>>>(K, perm, dup_id, tile_splats);
+        k_tile_splats<<<grid_for(K, 256), 256, 0, st>>>(K, pair, tile_splats);
     return cudaGetLastError();
 }
 

@@ -9,9 +9,7 @@ enum RasterMode { kRender = 0, kImportance = 1, kScore = 2, kRecords = 3 };
 
 struct RasterArgs {
     const SplatRec *rec;
-    const int32_t *perm;      // sorted pair -> duplicate index
-    const int32_t *dup_id;    // duplicate index -> batch record index (v * n + splat id)
-    const int32_t *sid;       // sorted pair -> batch record index
+    const int2 *pair;         // sorted pair -> (duplicate index = slot, batch record index v*n + id)
     const int32_t *dup_rank;  // duplicate index -> depth rank (records mode)
     const int2 *ranges;       // per tile [start, end) into perm
     int tiles_x, ntiles;      // ntiles: all tiles of the batch (nview * ntiles_view)
@@ -85,7 +83,7 @@ cudaError_t scan_counts(void *temp, size_t temp_bytes, const int32_t *ids, const
                         cudaStream_t st);
 cudaError_t launch_duplicate(int64_t total, int64_t n, const int32_t *ids, const int64_t *offs,
                              const SplatRec *rec, int tiles_x, int ntiles, int sb, bool key16,
-                             int cull, void *tkey, int32_t *dup_gid, int32_t *dup_rank,
+                             int cull, void *tkey, int32_t *dup_id, int32_t *dup_rank,
                              cudaStream_t st);
 cudaError_t tile_sort_temp(int64_t K, int nkeys, bool key16, size_t *bytes);
 cudaError_t tile_sort(void *temp, size_t temp_bytes, bool key16, const void *tkey, void *skey,
@@ -94,8 +92,8 @@ cudaError_t records_sort_temp(int64_t m, size_t *bytes);
 cudaError_t records_sort(void *temp, size_t temp_bytes, const uint64_t *key, uint64_t *skey,
                          const int32_t *iota, int32_t *sidx, int64_t m, cudaStream_t st);
 cudaError_t launch_tile_ranges(int64_t j0, int64_t K, bool key16, const void *skey,
-                               const int32_t *perm, const int32_t *dup_id, int32_t *sid,
-                               int2 *rng, int tbase, cudaStream_t st);
+                               const int32_t *perm, const int32_t *dup_id, int2 *pair, int2 *rng,
+                               int tbase, cudaStream_t st);
 cudaError_t launch_raster(int mode, const RasterArgs &a, int ntiles, cudaStream_t st);
 cudaError_t launch_splat_reduce(int64_t total, int64_t n, const int32_t *ids, const int64_t *offs,
                                 const double2 *partial, double P, double2 *vals,
@@ -118,8 +116,7 @@ cudaError_t launch_bin_outputs(int64_t n, const uint64_t *skey, uint64_t invalid
                                const int32_t *sids,
                                unsigned long long *nvalid_dev, int64_t *order, int ntiles,
                                const int2 *rng, int64_t K, int64_t *tile_offsets,
-                               const int32_t *perm, const int32_t *dup_id, int32_t *tile_splats,
-                               cudaStream_t st);
+                               const int2 *pair, int32_t *tile_splats, cudaStream_t st);
 
 // SH recompute (sh.cu)
 cudaError_t launch_sh_accumulate(const potr_splats &sp, int ncam, const double *eyes_dev,
