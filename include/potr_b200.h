@@ -156,6 +156,15 @@ int potr_sh_solve(potr_ctx *ctx, const potr_splats *splats, const double *normal
                   double lambda_y, double parallel_threshold, double zero_threshold,
                   double *rgb, double *ycocg, int8_t *status);
 
+/* ---- image metrics (metrics.py:24-52) ------------------------------------ */
+
+/* MSE of the [0, 1]-clamped images (psnr's, metrics.py:24-30) and mean SSIM
+ * over the three channels (11-tap Gaussian window, sigma 1.5, reflect
+ * borders, 5-pixel crop, K1 0.01, K2 0.03; :33-52).  a, b: device (H, W, 3)
+ * float64; mse, ssim: host outputs (nullable).  Synchronizes the stream. */
+int potr_image_compare(potr_ctx *ctx, int width, int height, const double *a, const double *b,
+                       double *mse, double *ssim);
+
 /* ---- tuning ------------------------------------------------------------- */
 
 /* Views processed per pipeline round (1..8, default 8; env POTR_B200_VIEW_BATCH). */

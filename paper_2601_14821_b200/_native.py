@@ -103,6 +103,9 @@ _SIGNATURES = {
     "potr_profile_read": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]),
     "potr_counters_enable": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int]),
     "potr_counters_read": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p]),
+    "potr_image_compare": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.c_int,
+                                          ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+                                          ctypes.c_void_p]),
     "potr_forward_stats_host": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p,
                                                ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
                                                ctypes.c_void_p, ctypes.c_int,

@@ -51,6 +51,7 @@ struct potr_ctx {
     DevBuf counters;
     int64_t pairs_total = 0;
     DevBuf tile_counter, ci_v, dm_v, bbox, overflow, vidx, khi, skhi, prep;
+    DevBuf met_mom, met_part, met_w, met_out;  // image metrics scratch
     bool depth_split = false;  // last bin_batch sorted split keys: skey not materialised
     double scene_lo[3] = {0, 0, 0}, scene_hi[3] = {0, 0, 0};  // splat position bbox
     uint64_t invalid_key0 = ~0ull;  // depth key of an invalid splat in view 0 of the last batch
@@ -600,6 +601,8 @@ void potr_destroy(potr_ctx *ctx) {
     if (ctx->ci_v.p) cudaFree(ctx->ci_v.p);
     if (ctx->dm_v.p) cudaFree(ctx->dm_v.p);
     if (ctx->khi.p) cudaFree(ctx->khi.p);
+    for (DevBuf *b : {&ctx->met_mom, &ctx->met_part, &ctx->met_w, &ctx->met_out})
+        if (b->p) cudaFree(b->p);
     if (ctx->prep.p) cudaFree(ctx->prep.p);
     if (ctx->skhi.p) cudaFree(ctx->skhi.p);
     for (auto &ev : ctx->events) {
@@ -877,6 +880,50 @@ int potr_compact(potr_ctx *ctx, const potr_splats *splats, int ncam, const potr_
     if (rc) return rc;
     return potr_sh_solve(ctx, splats, P<double>(ctx->neq), lambda_y, parallel_threshold,
                          zero_threshold, rgb, ycocg, status);
+}
+
+// scipy.ndimage._gaussian_kernel1d(1.5, 0, 5): exp(-0.5 / sigma^2 * x^2) over
+// x = -5..5, divided by its numpy sum (pairwise: eight running partials, then
+// the tail added in order).
+static void ssim_weights(double *w) {
+    const double sigma2 = 1.5 * 1.5;
+    for (int i = 0; i < 11; i++) {
+        const double x = (double)(i - 5);
+        w[i] = std::exp(-0.5 / sigma2 * (x * x));
+    }
+    double s = ((w[0] + w[1]) + (w[2] + w[3])) + ((w[4] + w[5]) + (w[6] + w[7]));
+    for (int i = 8; i < 11; i++) s += w[i];
+    for (int i = 0; i < 11; i++) w[i] = w[i] / s;
+}
+
+int potr_image_compare(potr_ctx *ctx, int width, int height, const double *a, const double *b,
+                       double *mse, double *ssim) {
+    if (!ctx || width <= 0 || height <= 0 || !a || !b)
+        return fail(ctx, POTR_E_ARG, "image_compare: bad image arguments");
+    CK(cudaSetDevice(ctx->device));
+    const size_t plane = (size_t)width * height;
+    ENSURE(ctx->met_mom, 5 * plane * sizeof(double));
+    ENSURE(ctx->met_part, (size_t)image_compare_partials() * sizeof(double));
+    ENSURE(ctx->met_w, 11 * sizeof(double));
+    ENSURE(ctx->met_out, 4 * sizeof(double));
+    double w[11];
+    ssim_weights(w);
+    CK(cudaMemcpyAsync(ctx->met_w.p, w, sizeof(w), cudaMemcpyHostToDevice, ctx->stream));
+    LAUNCH(9, launch_image_compare(width, height, a, b, P<double>(ctx->met_w),
+                                   P<double>(ctx->met_mom), P<double>(ctx->met_part),
+                                   P<double>(ctx->met_out), ctx->stream));
+    double out[4];
+    CK(cudaMemcpyAsync(out, ctx->met_out.p, sizeof(out), cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    if (mse) *mse = out[0] / (double)(plane * 3);
+    if (ssim) {
+        const int64_t cw = width - 10, ch = height - 10;
+        const double cnt = cw > 0 && ch > 0 ? (double)(cw * ch) : 0.0;
+        // np.mean of an empty crop is NaN, as in the reference
+        const double s0 = out[1] / cnt, s1 = out[2] / cnt, s2 = out[3] / cnt;
+        *ssim = ((s0 + s1) + s2) / 3.0;
+    }
+    return POTR_OK;
 }
 
 int potr_set_option(potr_ctx *ctx, int option, int value) {

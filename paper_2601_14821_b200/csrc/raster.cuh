@@ -118,6 +118,13 @@ cudaError_t launch_bin_outputs(int64_t n, const uint64_t *skey, uint64_t invalid
                                const int2 *rng, int64_t K, int64_t *tile_offsets,
                                const int2 *pair, int32_t *tile_splats, cudaStream_t st);
 
+// Image metrics (metrics.cu): out[0] = sum of clamped squared differences,
+// out[1..3] = per-channel sums of the cropped SSIM map.
+cudaError_t launch_image_compare(int W, int H, const double *a, const double *b,
+                                 const double *gauss_w, double *mom, double *partial, double *out,
+                                 cudaStream_t st);
+int image_compare_partials();
+
 // SH recompute (sh.cu)
 cudaError_t launch_sh_accumulate(const potr_splats &sp, int ncam, const double *eyes_dev,
                                  const double *cam_imp, double *neq, cudaStream_t st);

@@ -10,6 +10,7 @@ uninstall callable.
 import importlib
 
 from . import compaction as _comp
+from . import metrics as _met
 from . import rasterizer as _rast
 
 PATCH_SET = {
@@ -37,7 +38,12 @@ PATCH_SET = {
         "render_image": _rast.render_image,
         "compact_scene": _comp.compact_scene,
     },
-    "potr.metrics": {"render_image": _rast.render_image},
+    "potr.metrics": {
+        "render_image": _rast.render_image,
+        "ssim": _met.ssim,
+        "compare_renders": _met.compare_renders,
+        "compute_metrics": _met.compute_metrics,
+    },
 }
 
 

@@ -406,6 +406,33 @@ def test_stress_edge_cases_vs_oracle(R, oracle):
     assert np.diff(off).max() > 16 * 32  # tile lists longer than the kept pass-1 masks
 
 
+def test_image_metrics_vs_reference(R):
+    """psnr / ssim / compute_metrics on the device against the reference's
+    own values (tests/golden/metrics.npz): clamping, the SSIM window and
+    crop, an image too small for the crop (NaN), identical images (99 dB)."""
+    from paper_2601_14821_b200 import metrics as M
+    from paper_2601_14821_b200.fixture import make_fixture
+    from tests.conftest import fingerprint
+    g = golden("metrics")
+    mse, ss = M.compare_device(g["a"], g["b"])
+    assert M.psnr(g["a"], g["b"]) == float(g["psnr_ab"])
+    assert M.psnr_from_mse(mse) == pytest.approx(float(g["psnr_ab"]), rel=1e-13)
+    assert ss == pytest.approx(float(g["ssim_ab"]), abs=1e-13)
+    assert M.ssim(g["a"], g["a"]) == pytest.approx(float(g["ssim_same"]), abs=1e-15)
+    assert M.psnr_from_mse(M.compare_device(g["a"], g["a"])[0]) == float(g["psnr_same"])
+    mse_t, ss_t = M.compare_device(g["tiny_a"], g["tiny_b"])
+    assert np.isnan(ss_t) and np.isnan(float(g["ssim_tiny"]))
+    assert M.psnr_from_mse(mse_t) == pytest.approx(float(g["psnr_tiny"]), rel=1e-13)
+    splats, cams = make_fixture(3000, 3, 1, 48)
+    assert fingerprint(splats, cams) == str(g["fingerprint"])
+    rep = M.compute_metrics(splats, perturbed(splats), cams)
+    np.testing.assert_allclose(rep.psnr_per_camera, g["model_psnr"], rtol=0, atol=1e-8)
+    np.testing.assert_allclose(rep.ssim_per_camera, g["model_ssim"], rtol=0, atol=1e-12)
+    assert rep.splat_count == int(g["model_count"])
+    with pytest.raises(ValueError):
+        M.compare_device(g["a"], g["tiny_b"])
+
+
 def _depth_tie_scene(n_long):
     """random_scene plus splats whose depths tie in the high bits of the
     depth key: groups a few hundred ulps apart (stored in reverse depth order,
