@@ -29,6 +29,7 @@ YCOCG_TO_RGB = np.array([
 ])
 
 STATUS_OK, STATUS_JITTER, STATUS_FAILED, STATUS_DC_FALLBACK = 0, 1, 2, 3
+NEQ_STRIDE = 185  # POTR_NEQ_STRIDE: G upper triangle 136 + B 48 + seen count
 
 
 class RidgeError(RuntimeError):
@@ -156,17 +157,56 @@ def mean_abs_nonzero_ac(ycocg):
 def sweep(splats, cameras, targets, camera_importance, lambdas, alphas, zero_threshold,
           threads=1):
     """Regularization sweep (:258-278): rows of (lambda, alpha, AC sparsity,
-    mean |nonzero AC|, MSE vs targets), all compaction and rendering on GPU."""
-    from .rasterizer import render_image
+    mean |nonzero AC|, MSE vs targets), one per (lambda, alpha).
+
+    Device-resident: the weighted normal equations do not depend on
+    (lambda, alpha), so they are accumulated once (potr_sh_accumulate) and
+    only the solves, the re-renders and the error reductions run per grid
+    point; nothing but the row scalars comes back to the host."""
+    from .rasterizer import render_targets_device
+    ctx = D.context()
+    dev = D.current_device()
+    ds = D.DeviceSplats.from_host(splats, dev)
+    n, S = ds.n, len(cameras)
     rows = []
+    if n == 0 or S == 0:
+        for alpha in alphas:
+            for lam in lambdas:
+                compacted, ycocg, _ = compact_scene(splats, cameras, camera_importance,
+                                                    CompactionConfig(lam, alpha, zero_threshold))
+                mse = 0.0
+                from .rasterizer import render_image
+                for s_, cam in enumerate(cameras):
+                    mse += float(np.mean((render_image(compacted, cam) - targets[s_]) ** 2))
+                rows.append((lam, alpha, ac_sparsity(ycocg), mean_abs_nonzero_ac(ycocg),
+                             mse / len(cameras)))
+        return rows
+    ci = D.as_device_matrix(camera_importance, (S, n), dev)
+    neq = torch.zeros((NEQ_STRIDE, n), dtype=torch.float64, device=dev)
+    cams = _native.camera_array(cameras)
+    ctx.call("potr_sh_accumulate", ctypes.byref(ds.struct()), S, cams, D.ptr(ci), D.ptr(neq))
+    dev_targets = D.targets_cache.get(targets, cameras, dev)
+    rgb = D.empty((n, 3, 16), dev)
+    yc = D.empty((n, 3, 16), dev)
+    status = D.empty(n, dev, torch.int8)
     for alpha in alphas:
         for lam in lambdas:
             cfg = CompactionConfig(lambda_y=lam, parallel_threshold=alpha,
                                    zero_threshold=zero_threshold)
-            compacted, ycocg, _ = compact_scene(splats, cameras, camera_importance, cfg)
+            ctx.call("potr_sh_solve", ctypes.byref(ds.struct()), D.ptr(neq),
+                     ctypes.c_double(cfg.lambda_y), ctypes.c_double(cfg.parallel_threshold),
+                     ctypes.c_double(cfg.zero_threshold), D.ptr(rgb), D.ptr(yc), D.ptr(status))
+            compacted = D.DeviceSplats(ds.positions, rgb, ds.opacities, ds.scales,
+                                       ds.rotations)
+            imgs = render_targets_device(compacted, cameras)
+            errs = torch.stack([((im - t) ** 2).mean() for im, t in zip(imgs, dev_targets)])
+            ac = yc[:, :, 1:]
+            nz = ac != 0.0
+            n_nz = int(nz.sum().item())
+            sparsity = float(ac.numel() - n_nz) / ac.numel()  # == np.mean(ac == 0)
+            mean_nz = float(ac.abs()[nz].mean().item()) if n_nz else 0.0
             mse = 0.0
-            for s, cam in enumerate(cameras):
-                mse += float(np.mean((render_image(compacted, cam) - targets[s]) ** 2))
-            rows.append((lam, alpha, ac_sparsity(ycocg), mean_abs_nonzero_ac(ycocg),
-                         mse / len(cameras)))
+            for e in errs.cpu().numpy():
+                mse += float(e)
+            rows.append((lam, alpha, sparsity, mean_nz, mse / S))
     return rows

@@ -235,9 +235,46 @@ def run_pruning(splats, cameras, targets, config: PruneConfig, threads=1, report
     return current, kept, reports
 
 
+def _run_pruning_to_counts_device(splats, cameras, targets, cumulative_counts, delta_mse_max, a):
+    import torch
+    from . import device as D
+    from .rasterizer import forward_stats_device
+    _check_targets(cameras, targets)
+    if len(cameras) == 0:
+        raise ZeroDivisionError("float division by zero")
+    dev = D.current_device()
+    ds = D.DeviceSplats.from_host(splats, dev)
+    n0 = ds.n
+    dev_targets = D.targets_cache.get(targets, cameras, dev)
+    kept = np.arange(n0, dtype=np.int64)
+    checkpoints = []
+    removed = 0
+    for target in cumulative_counts:
+        batch = min(target, n0) - removed
+        if batch > 0:
+            _, _, dm_d, _ = forward_stats_device(ds, cameras, dev_targets, want_cam_imp=False)
+            idx = torch.arange(ds.n, device=dev)
+            order = _removal_order_device(dm_d, idx, delta_mse_max, a)
+            sel = np.sort(order[:batch].cpu().numpy())
+            mask = np.ones(ds.n, dtype=bool)
+            mask[sel] = False
+            mask_d = torch.from_numpy(mask).to(dev)
+            ds = D.DeviceSplats(ds.positions[mask_d], ds.sh[mask_d], ds.opacities[mask_d],
+                                ds.scales[mask_d], ds.rotations[mask_d])
+            kept = kept[mask]
+            removed = target
+        checkpoints.append(kept.copy())
+    return checkpoints
+
+
 def run_pruning_to_counts(splats, cameras, targets, cumulative_counts, delta_mse_max, a=10.0,
                           threads=1):
-    """Rate-sweep variant with fixed batch sizes (:166-190)."""
+    """Rate-sweep variant with fixed batch sizes (:166-190); device-resident
+    (splats subset in HBM, GPU stable sort of the whole removal order) when it
+    drives this package's scorer."""
+    if _device_scorer_active():
+        return _run_pruning_to_counts_device(splats, cameras, targets, cumulative_counts,
+                                             delta_mse_max, a)
     current = splats
     kept = np.arange(len(splats.positions), dtype=np.int64)
     checkpoints = []

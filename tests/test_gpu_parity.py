@@ -214,6 +214,24 @@ def test_prune_device_controller_matches_host_controller(R, monkeypatch):
         assert np.array_equal(getattr(dev[0], f), getattr(host[0], f))
 
 
+def test_pruning_to_counts_device_matches_host(R, monkeypatch):
+    """The device-resident rate sweep (run_pruning_to_counts) equals the host
+    loop over the same GPU scores, checkpoint by checkpoint."""
+    from paper_2601_14821_b200 import pruning, fixture
+    splats, cams = fixture.config_scene("C1")
+    targets = R.render_targets(splats, cams)
+    counts = [0, 500, 500, 2000, 10**6]
+    dmax = 10.0 ** (-8.8 - 2.0 * 0.5)
+    dev = pruning.run_pruning_to_counts(splats, cams, targets, counts, dmax)
+    monkeypatch.setattr(pruning, "compute_delta_mse",
+                        lambda *a, **k: R.compute_delta_mse(*a, **k))
+    host = pruning.run_pruning_to_counts(splats, cams, targets, counts, dmax)
+    assert len(dev) == len(host) == len(counts)
+    for a_, b_ in zip(dev, host):
+        assert np.array_equal(a_, b_)
+    assert len(dev[-1]) == 0 and len(dev[1]) == len(splats.positions) - 500
+
+
 def test_sh_recompute(C):
     splats, cams = sh_scene()
     g = golden("sh_scene")
@@ -431,6 +449,32 @@ def test_image_metrics_vs_reference(R):
     assert rep.splat_count == int(g["model_count"])
     with pytest.raises(ValueError):
         M.compare_device(g["a"], g["tiny_b"])
+
+
+def test_sh_sweep_matches_per_point_compaction(R, C):
+    """compaction.sweep (normal equations accumulated once, solves / renders /
+    errors per grid point on the device) == the reference's loop of
+    compact_scene + render_image + numpy means (compaction.py:258-278)."""
+    splats, cams = sh_scene()
+    targets = R.render_targets(splats, cams)
+    _, ci = R.compute_importance(splats, cams)
+    lambdas, alphas = [10.0 ** -0.5, 1e-7], [0.8175744761936437, 0.95]
+    rows = C.sweep(splats, cams, targets, ci, lambdas, alphas, 0.5 / 51.0)
+    k = 0
+    for alpha in alphas:
+        for lam in lambdas:
+            cfg = C.CompactionConfig(lam, alpha, 0.5 / 51.0)
+            comp, yc, _ = C.compact_scene(splats, cams, ci, cfg)
+            mse = 0.0
+            for s_, cam in enumerate(cams):
+                mse += float(np.mean((R.render_image(comp, cam) - targets[s_]) ** 2))
+            ref = (lam, alpha, C.ac_sparsity(yc), C.mean_abs_nonzero_ac(yc), mse / len(cams))
+            got = rows[k]
+            assert got[:3] == ref[:3]
+            assert got[3] == pytest.approx(ref[3], rel=1e-12, abs=0)
+            assert got[4] == pytest.approx(ref[4], rel=1e-12, abs=0)
+            k += 1
+    assert k == len(rows)
 
 
 def _depth_tie_scene(n_long):
