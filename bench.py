@@ -50,6 +50,8 @@ def parse_args():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-scene", action="store_true", help="skip the s/scene measurement")
+    ap.add_argument("--no-prune48", action="store_true",
+                    help="skip the 48-iteration run_pruning timing")
     ap.add_argument("--cpu-threads", type=int, default=0)
     return ap.parse_args()
 
@@ -548,8 +550,28 @@ def scene_measure(args, world, ds, cams, my_cams, tptr, cam_arr, lo, hi, ctx, de
     run()  # warm
     parts = run()
     ac = float((yc[:, :, 1:] == 0).double().mean().item())
-    return {"total_s": sum(parts), "render_targets_s": parts[0], "prune_score_s": parts[1],
-            "sh_recompute_s": parts[2], "lambda_y": 1e-7, "ac_sparsity": ac}
+    out = {"total_s": sum(parts), "render_targets_s": parts[0], "prune_score_s": parts[1],
+           "sh_recompute_s": parts[2], "lambda_y": 1e-7, "ac_sparsity": ac}
+    if world == 1 and not args.no_prune48:
+        out.update(prune48_measure(splats, cams, imgs))
+    return out
+
+
+def prune48_measure(splats, cams, targets_dev):
+    """The encoder's pruning stage ("48-iteration run_pruning"):
+    pruning.run_pruning at q = 0.5 (delta_mse_max = 10^-9.8) through the public
+    API from host splats, with the device-resident controller; targets are the
+    fixed renders already in HBM."""
+    import torch
+    from paper_2601_14821_b200 import pruning
+    cfg = pruning.PruneConfig(delta_mse_max=10.0 ** (-8.8 - 2.0 * 0.5))
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    pruned, kept, reports = pruning.run_pruning(splats, cams, targets_dev, cfg)
+    torch.cuda.synchronize()
+    dt = time.perf_counter() - t0
+    return {"prune48_s": dt, "prune48_iterations": len(reports),
+            "prune48_kept": int(len(kept)), "prune48_input": int(len(splats.positions))}
 
 
 if __name__ == "__main__":
