@@ -1,24 +1,28 @@
-// raster.cu -- the prune-score pass on sm_100a: kernels (a)-(d).
+// raster.cu -- the prune-score pass on sm_100a: kernels (a)-(d).  All work is
+// done for a batch of up to 8 equal-size views at a time.
 //
-//  (a) k_preprocess    project + cov2d + radius + clipped bbox + conic + SH
-//                      colour + fp64 depth key, one thread per splat
+//  (a) k_splat_prep    view-independent Sigma and prefilter threshold, once per
+//                      call; k_preprocess: one thread per (splat, view): EWA
+//                      projection, cov2d, radius, clipped bbox, conic, SH
+//                      colour, compact depth key, culled tile count
 //                      (rasterizer.py:56-110, :135-154)
-//  (b) k_gather_counts / k_duplicate / k_tile_ranges around two CUB onesweep
-//      radix sorts: a stable sort of the fp64 depth bits (ties keep ascending
-//      splat id == np.argsort(kind="stable"), :248-250), then a stable sort of
-//      the per-(tile, splat) duplicates on the tile id, giving every tile its
-//      splats in (tile, depth, id) order.
-//  (c)+(d) k_raster    one CTA per 16x16 tile; splat batches staged in shared
-//      memory; front-to-back compositing with the reference's exact per-pixel
-//      rules (:159-201); a second walk over the same batches evaluates the
-//      closed-form removal delta PD = a/(1-a) (P_K - P_i - T c) (:232-243),
-//      dSE = sum_ch PD^2 + 2 PD (c - c_t) (:333) and T*alpha (:228); warps
-//      reduce per splat with shuffles and the 8 warps combine in a fixed
-//      order into one slot per (tile, splat) pair -- no floating-point
-//      atomics, so scores are bit-reproducible.
-//  k_splat_reduce      per splat, sums its pair slots in tile order, divides
-//                      by P / 3P and adds into the camera-ordered accumulators
-//                      (:226-230, :334, :340-347).
+//  (b) depth order: CUB sort of the 32-bit hi part of the depth key +
+//      k_depth_fixup (runs of equal hi ordered by the full key) -- stable, so
+//      ties keep ascending splat id == np.argsort(kind="stable") (:248-250);
+//      k_gather_counts + CUB scan, k_duplicate (pairs in depth order, tiles
+//      culled by the prefilter ellipse), CUB stable sort on 16-bit tile keys,
+//      k_tile_ranges: every tile gets its splats in (tile, depth, id) order.
+//  (c)+(d) k_raster    persistent warps, one warp per 8x4-pixel tile (lane =
+//      pixel).  Pass 1 composites front to back with the reference's exact
+//      per-pixel rules (:159-201), each lane walking only the chunk entries
+//      that cover its pixel; the replay revisits the composited samples and
+//      evaluates the closed-form removal delta PD = a/(1-a) (P_K - P_i - T c)
+//      (:232-243), dSE = sum_ch PD^2 + 2 PD (c - c_t) (:333) and T*alpha
+//      (:228), adding them per (tile, splat) slot in a fixed lane order -- no
+//      floating-point atomics, so scores are bit-reproducible.
+//  k_splat_reduce / k_view_accumulate / k_mse_reduce: per splat, its slots in
+//      tile order, divided by P / 3P, added in camera order (:226-230, :334,
+//      :340-347).
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
 
