@@ -303,22 +303,27 @@ def main():
     dm = torch.zeros(n, dtype=torch.float64, device=dev)
     mse = torch.zeros(1, dtype=torch.float64, device=dev)
     ci = torch.empty((max(1, hi - lo), n), dtype=torch.float64, device=dev)
-    red = torch.empty(2 * n + 1, dtype=torch.float64, device=dev)
+
+    if world > 1:  # per-view rows for the ordered (GPU-count-invariant) reduction
+        dm_rows = torch.empty((max(1, hi - lo), n), dtype=torch.float64, device=dev)
+        mse_rows = torch.empty(max(1, hi - lo), dtype=torch.float64, device=dev)
 
     def step():
-        imp.zero_()
-        dm.zero_()
-        mse.zero_()
-        ctx.call("potr_score_views", ctypes.byref(ds.struct()), hi - lo, cam_arr, tptr,
-                 D.ptr(imp), D.ptr(ci), D.ptr(dm), D.ptr(mse))
-        if world > 1:
-            torch.cat([imp, dm, mse], out=red)
-            dist.all_reduce(red)
-            imp.copy_(red[:n])
-            dm.copy_(red[n:2 * n])
-            mse.copy_(red[2 * n:])
-        ctx.call("potr_finalize_stats", ctypes.c_int64(n), S, D.ptr(imp), D.ptr(dm),
-                 D.ptr(mse))
+        if world == 1:
+            imp.zero_()
+            dm.zero_()
+            mse.zero_()
+            ctx.call("potr_score_views", ctypes.byref(ds.struct()), hi - lo, cam_arr, tptr,
+                     D.ptr(imp), D.ptr(ci), D.ptr(dm), D.ptr(mse))
+            ctx.call("potr_finalize_stats", ctypes.c_int64(n), S, D.ptr(imp), D.ptr(dm),
+                     D.ptr(mse))
+            return
+        # view-sharded: rows of this rank's views, then the ordered chain
+        # 0 -> 1 -> ... -> W-1 + broadcast (distributed.ordered_reduce)
+        ctx.call("potr_score_views_rows", ctypes.byref(ds.struct()), hi - lo, cam_arr, tptr,
+                 D.ptr(ci), D.ptr(dm_rows), D.ptr(mse_rows))
+        acc = distributed.ordered_reduce(ci[:hi - lo], dm_rows[:hi - lo], mse_rows[:hi - lo], n)
+        distributed.finalize_sums(acc, n, S)
 
     def barrier():
         if world > 1:

@@ -91,6 +91,15 @@ int potr_score_views(potr_ctx *ctx, const potr_splats *splats, int ncam,
                      const potr_camera *cams, const double *const *targets, double *imp_sum,
                      double *camera_importance, double *dmse_sum, double *mse_sum);
 
+/* The per-view values behind those sums, for an exactly ordered multi-GPU
+ * reduction: camera_importance rows (ncam, n), delta-MSE rows (ncam, n) and
+ * per-view MSE (ncam) -- each already divided by P / 3P (:230, :334-335).
+ * Adding the rows in camera order reproduces potr_score_views' sums bit for
+ * bit.  dmse_rows / mse_rows required with targets. */
+int potr_score_views_rows(potr_ctx *ctx, const potr_splats *splats, int ncam,
+                          const potr_camera *cams, const double *const *targets,
+                          double *camera_importance, double *dmse_rows, double *mse_rows);
+
 /* rasterizer.py:348-352: divide the sums by the total camera count in place
  * (dmse_sum / mse_sum nullable). */
 int potr_finalize_stats(potr_ctx *ctx, int64_t n, int total_cams, double *imp_sum,

@@ -508,7 +508,8 @@ int batch_len(potr_ctx *ctx, const potr_camera *cams, int s, int ncam, int64_t n
 
 int score_views_impl(potr_ctx *ctx, const potr_splats *sp, int ncam, const potr_camera *cams,
                      const double *const *targets, double *imp_sum, double *cam_imp,
-                     double *dmse_sum, double *mse_sum) {
+                     double *dmse_sum, double *mse_sum, double *dmse_rows = nullptr,
+                     double *mse_rows = nullptr) {
     const int64_t n = sp->n;
     int brc = compute_scene_bounds(ctx, *sp);
     if (brc) return brc;
@@ -537,10 +538,12 @@ int score_views_impl(potr_ctx *ctx, const potr_splats *sp, int ncam, const potr_
                                           ctx->stream));
             LAUNCH(1, launch_view_accumulate(n, nb, P<double2>(ctx->ci_v),
                                              cam_imp ? cam_imp + (int64_t)s * n : nullptr, imp_sum,
-                                             targets ? dmse_sum : nullptr, ctx->stream));
+                                             targets ? dmse_sum : nullptr,
+                                             dmse_rows ? dmse_rows + (int64_t)s * n : nullptr,
+                                             ctx->stream));
             if (targets)
                 LAUNCH(1, launch_mse_reduce(nb, g.ntiles, P<double>(ctx->tile_se), g.P, mse_sum,
-                                            ctx->stream));
+                                            mse_rows ? mse_rows + s : nullptr, ctx->stream));
             _st.end();
         }
         s += nb;
@@ -642,6 +645,27 @@ int potr_score_views(potr_ctx *ctx, const potr_splats *splats, int ncam, const p
         return fail(ctx, POTR_E_ARG, "targets given without delta_mse/mse outputs");
     return score_views_impl(ctx, splats, ncam, cams, targets, imp_sum, camera_importance,
                             dmse_sum, mse_sum);
+}
+
+int potr_score_views_rows(potr_ctx *ctx, const potr_splats *splats, int ncam,
+                          const potr_camera *cams, const double *const *targets,
+                          double *camera_importance, double *dmse_rows, double *mse_rows) {
+    if (!ctx) return POTR_E_ARG;
+    CK(cudaSetDevice(ctx->device));
+    int rc = check_splats(ctx, splats);
+    if (rc) return rc;
+    if (ncam < 0 || (ncam > 0 && !cams)) return fail(ctx, POTR_E_ARG, "bad camera list");
+    if (!camera_importance) return fail(ctx, POTR_E_ARG, "camera_importance is NULL");
+    if (targets && (!dmse_rows || !mse_rows))
+        return fail(ctx, POTR_E_ARG, "targets given without delta_mse/mse row outputs");
+    const int64_t n = splats->n;
+    // the sums are produced on the way and discarded
+    ENSURE(ctx->dm_v, sizeof(double) * (2 * (n > 0 ? n : 1) + 1));
+    double *scratch = P<double>(ctx->dm_v);
+    CK(cudaMemsetAsync(scratch, 0, sizeof(double) * (2 * (n > 0 ? n : 1) + 1), ctx->stream));
+    return score_views_impl(ctx, splats, ncam, cams, targets, scratch, camera_importance,
+                            targets ? scratch + n : nullptr, targets ? scratch + 2 * n : nullptr,
+                            dmse_rows, mse_rows);
 }
 
 int potr_finalize_stats(potr_ctx *ctx, int64_t n, int total_cams, double *imp_sum,

@@ -810,7 +810,7 @@ __global__ void __launch_bounds__(256) k_splat_reduce(int64_t total, int64_t n,
 // writing the camera_importance rows on the way (coalesced, by splat id).
 __global__ void k_view_accumulate(int64_t n, int nview, const double2 *__restrict__ vals,
                                   double *__restrict__ cam_imp_rows, double *__restrict__ imp_acc,
-                                  double *__restrict__ dmse_acc) {
+                                  double *__restrict__ dmse_acc, double *__restrict__ dmse_rows) {
     const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (k >= n) return;
     double ia = imp_acc[k];
@@ -818,6 +818,7 @@ __global__ void k_view_accumulate(int64_t n, int nview, const double2 *__restric
     for (int v = 0; v < nview; v++) {
         const double2 x = vals[(int64_t)v * n + k];
         if (cam_imp_rows) cam_imp_rows[(int64_t)v * n + k] = x.x;
+        if (dmse_rows) dmse_rows[(int64_t)v * n + k] = x.y;
         ia += x.x;
         da += x.y;
     }
@@ -828,7 +829,7 @@ __global__ void k_view_accumulate(int64_t n, int nview, const double2 *__restric
 // Per view, the sum of its tiles' squared errors; mse(s) = sum / 3P (:335),
 // added to the camera-ordered accumulator (:347).
 __global__ void k_mse_reduce(int nview, int ntiles, const double *__restrict__ tile_se, double P,
-                             double *__restrict__ mse_acc) {
+                             double *__restrict__ mse_acc, double *__restrict__ mse_rows) {
     __shared__ double red[32];
     for (int v = 0; v < nview; v++) {
         double s = 0.0;
@@ -840,6 +841,7 @@ __global__ void k_mse_reduce(int nview, int ntiles, const double *__restrict__ t
             double t = 0.0;
             for (int w = 0; w < (int)(blockDim.x >> 5); w++) t += red[w];
             mse_acc[0] += t / (P * 3.0);
+            if (mse_rows) mse_rows[v] = t / (P * 3.0);
         }
         __syncthreads();
     }
@@ -1222,16 +1224,16 @@ cudaError_t launch_splat_reduce(int64_t total, int64_t n, const int32_t *ids, co
 
 cudaError_t launch_view_accumulate(int64_t n, int nview, const double2 *vals,
                                    double *cam_imp_rows, double *imp_acc, double *dmse_acc,
-                                   cudaStream_t st) {
+                                   double *dmse_rows, cudaStream_t st) {
     if (n == 0) return cudaSuccess;
     k_view_accumulate<<<grid_for(n, 256), 256, 0, st>>>(n, nview, vals, cam_imp_rows, imp_acc,
-                                                         dmse_acc);
+                                                         dmse_acc, dmse_rows);
     return cudaGetLastError();
 }
 
 cudaError_t launch_mse_reduce(int nview, int ntiles, const double *tile_se, double P,
-                              double *mse_acc, cudaStream_t st) {
-    k_mse_reduce<<<1, 1024, 0, st>>>(nview, ntiles, tile_se, P, mse_acc);
+                              double *mse_acc, double *mse_rows, cudaStream_t st) {
+    k_mse_reduce<<<1, 1024, 0, st>>>(nview, ntiles, tile_se, P, mse_acc, mse_rows);
     return cudaGetLastError();
 }
 

@@ -31,6 +31,39 @@ def _oracle_scorer(splats, cams, targets):
             torch.tensor([mse * S], dtype=torch.float64))
 
 
+def _oracle_rows(splats, cams, targets):
+    """Per-view rows, as potr_score_views_rows produces them."""
+    from oracle import oracle as O
+    n = len(splats.positions)
+    imp, dm, mse = [], [], []
+    for c, t in zip(cams, targets):
+        i1, _, d1, m1 = O.forward_stats(splats, [c], [t])
+        imp.append(i1), dm.append(d1), mse.append(m1)
+    L = len(cams)
+    f = lambda rows: torch.from_numpy(np.array(rows, dtype=np.float64).reshape(L, n))  # noqa
+    return f(imp), f(dm), torch.tensor(mse, dtype=torch.float64).reshape(L)
+
+
+def _worker_ordered(rank, world, port, out_path):
+    import sys
+    sys.path.insert(0, ROOT)
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2601_14821_b200 import distributed
+    from paper_2601_14821_b200.fixture import make_fixture
+    from oracle import oracle as O
+    splats, cams = make_fixture(600, 7, 3, 32)
+    targets = [O.render(splats, c)[0] for c in cams]
+    pert = splats.copy()
+    pert.opacities = pert.opacities * 0.97
+    st = distributed.forward_stats_sharded(pert, cams, targets, ordered=True,
+                                           rows_fn=_oracle_rows)
+    np.savez(out_path + f".{rank}.npz", importance=st.importance, delta_mse=st.delta_mse,
+             mse=st.mse)
+    dist.destroy_process_group()
+
+
 def _worker(rank, world, port, out_path):
     import sys
     sys.path.insert(0, ROOT)
@@ -44,7 +77,8 @@ def _worker(rank, world, port, out_path):
     targets = [O.render(splats, c)[0] for c in cams]
     pert = splats.copy()
     pert.opacities = pert.opacities * 0.97
-    st = distributed.forward_stats_sharded(pert, cams, targets, score_fn=_oracle_scorer)
+    st = distributed.forward_stats_sharded(pert, cams, targets, score_fn=_oracle_scorer,
+                                           ordered=False)
     lo, hi = distributed.shard_range(len(cams), rank, world)
     assert st.camera_importance.view_range == (lo, hi)
     np.savez(out_path + f".{rank}.npz", importance=st.importance, delta_mse=st.delta_mse,
@@ -82,3 +116,35 @@ def test_two_rank_gloo_matches_single_process(tmp_path):
         np.testing.assert_allclose(r["delta_mse"], dm, rtol=1e-12, atol=1e-24)
         assert float(r["mse"]) == pytest.approx(mse, rel=1e-13)
     np.testing.assert_array_equal(np.concatenate([r0["rows"], r1["rows"]]), ci)
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_ordered_chain_bit_identical_to_camera_order(tmp_path, world):
+    """The ordered reduction (send/recv chain + broadcast) gives every rank
+    exactly the single-device camera-order sums, for any world size."""
+    from oracle import oracle as O
+    from paper_2601_14821_b200.fixture import make_fixture
+    import socket
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    out = str(tmp_path / "res")
+    mp.start_processes(_worker_ordered, args=(world, port, out), nprocs=world, join=True,
+                       start_method="spawn")
+    splats, cams = make_fixture(600, 7, 3, 32)
+    targets = [O.render(splats, c)[0] for c in cams]
+    pert = splats.copy()
+    pert.opacities = pert.opacities * 0.97
+    imp_r, dm_r, mse_r = _oracle_rows(pert, cams, targets)
+    n = len(pert.positions)
+    acc = torch.zeros(2 * n + 1, dtype=torch.float64)
+    for v in range(len(cams)):
+        acc[:n] += imp_r[v]
+        acc[n:2 * n] += dm_r[v]
+        acc[2 * n:] += mse_r[v:v + 1]
+    ref = torch.div(acc, torch.tensor(float(len(cams)), dtype=torch.float64)).numpy()
+    for r in range(world):
+        got = np.load(out + f".{r}.npz")
+        assert np.array_equal(got["importance"], ref[:n])
+        assert np.array_equal(got["delta_mse"], ref[n:2 * n])
+        assert float(got["mse"]) == float(ref[2 * n])

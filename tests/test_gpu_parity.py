@@ -124,6 +124,30 @@ def test_view_batching_and_key_modes_bit_identical(R, batch, raw):
     assert np.array_equal(order, g["order0"]) and np.array_equal(lst, g["tile_splats0"])
 
 
+def test_score_rows_sum_to_fused_sums(R):
+    """potr_score_views_rows' per-view rows, added in camera order (what the
+    ordered multi-GPU chain does), equal potr_score_views' sums bit for bit."""
+    import torch
+    from paper_2601_14821_b200 import distributed, device
+    splats, cams = small_scene()
+    g = golden("small_scene")
+    targets = [t for t in g["targets"]]
+    pert = perturbed(splats)
+    ci, dm_rows, mse_rows = distributed._gpu_score_rows(pert, cams, targets)
+    n = len(pert.positions)
+    acc = torch.zeros(2 * n + 1, dtype=torch.float64, device=ci.device)
+    for v in range(len(cams)):
+        acc[:n] += ci[v]
+        acc[n:2 * n] += dm_rows[v]
+        acc[2 * n:] += mse_rows[v:v + 1]
+    st = R.compute_delta_mse(pert, cams, targets)
+    host = distributed.finalize_sums(acc, n, len(cams)).cpu().numpy()
+    assert np.array_equal(host[:n], st.importance)
+    assert np.array_equal(host[n:2 * n], st.delta_mse)
+    assert float(host[2 * n]) == st.mse
+    assert np.array_equal(ci.cpu().numpy(), np.asarray(st.camera_importance))
+
+
 def test_forward_stats_bit_reproducible(R):
     splats, cams = small_scene()
     g = golden("small_scene")
