@@ -319,7 +319,7 @@ int bin_batch(potr_ctx *ctx, const potr_splats &sp, const potr_camera *cams, int
     ENSURE(ctx->cnt_sorted, sizeof(int64_t) * total);
     ENSURE(ctx->offs, sizeof(int64_t) * (total + 1));
     ENSURE(ctx->ranges, sizeof(int2) * ntiles_b);
-    ENSURE(ctx->tile_se, sizeof(double) * ntiles_b);
+    ENSURE(ctx->tile_se, sizeof(double) * (ntiles_b + kMaxViewBatch));  // + per-view MSE
     ENSURE(ctx->tile_counter, sizeof(int));
     ENSURE(ctx->overflow, 2 * sizeof(int));
     int rc = 0;
@@ -542,7 +542,7 @@ int score_views_impl(potr_ctx *ctx, const potr_splats *sp, int ncam, const potr_
                                              dmse_rows ? dmse_rows + (int64_t)s * n : nullptr,
                                              ctx->stream));
             if (targets)
-                LAUNCH(1, launch_mse_reduce(nb, g.ntiles, P<double>(ctx->tile_se), g.P, mse_sum,
+                LAUNCH(2, launch_mse_reduce(nb, g.ntiles, P<double>(ctx->tile_se), g.P, mse_sum,
                                             mse_rows ? mse_rows + s : nullptr, ctx->stream));
             _st.end();
         }

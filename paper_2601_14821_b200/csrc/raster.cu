@@ -826,25 +826,34 @@ __global__ void k_view_accumulate(int64_t n, int nview, const double2 *__restric
     if (dmse_acc) dmse_acc[k] = da;
 }
 
-// Per view, the sum of its tiles' squared errors; mse(s) = sum / 3P (:335),
-// added to the camera-ordered accumulator (:347).
-__global__ void k_mse_reduce(int nview, int ntiles, const double *__restrict__ tile_se, double P,
-                             double *__restrict__ mse_acc, double *__restrict__ mse_rows) {
+// Per view (one block each), the sum of its tiles' squared errors in a fixed
+// order; mse(s) = sum / 3P (:335).  k_mse_accumulate then adds the views to
+// the camera-ordered accumulator (:347).
+__global__ void k_mse_reduce(int ntiles, const double *__restrict__ tile_se, double P,
+                             double *__restrict__ mse_view) {
     __shared__ double red[32];
-    for (int v = 0; v < nview; v++) {
-        double s = 0.0;
-        for (int t = threadIdx.x; t < ntiles; t += blockDim.x) s += tile_se[(int64_t)v * ntiles + t];
-        s = warp_sum(s);
-        if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            double t = 0.0;
-            for (int w = 0; w < (int)(blockDim.x >> 5); w++) t += red[w];
-            mse_acc[0] += t / (P * 3.0);
-            if (mse_rows) mse_rows[v] = t / (P * 3.0);
-        }
-        __syncthreads();
+    const int v = blockIdx.x;
+    double s = 0.0;
+    for (int t = threadIdx.x; t < ntiles; t += blockDim.x) s += tile_se[(int64_t)v * ntiles + t];
+    s = warp_sum(s);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t = 0.0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); w++) t += red[w];
+        mse_view[v] = t / (P * 3.0);
     }
+}
+
+__global__ void k_mse_accumulate(int nview, const double *__restrict__ mse_view,
+                                 double *__restrict__ mse_acc, double *__restrict__ mse_rows) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    double a = mse_acc[0];
+    for (int v = 0; v < nview; v++) {
+        a += mse_view[v];
+        if (mse_rows) mse_rows[v] = mse_view[v];
+    }
+    mse_acc[0] = a;
 }
 
 __global__ void k_finalize(int64_t n, double S, double *imp, double *dmse, double *mse) {
@@ -1231,9 +1240,11 @@ cudaError_t launch_view_accumulate(int64_t n, int nview, const double2 *vals,
     return cudaGetLastError();
 }
 
-cudaError_t launch_mse_reduce(int nview, int ntiles, const double *tile_se, double P,
+cudaError_t launch_mse_reduce(int nview, int ntiles, double *tile_se, double P,
                               double *mse_acc, double *mse_rows, cudaStream_t st) {
-    k_mse_reduce<<<1, 1024, 0, st>>>(nview, ntiles, tile_se, P, mse_acc, mse_rows);
+    k_mse_reduce<<<nview, 1024, 0, st>>>(ntiles, tile_se, P, tile_se + (int64_t)nview * ntiles);
+    k_mse_accumulate<<<1, 32, 0, st>>>(nview, tile_se + (int64_t)nview * ntiles, mse_acc,
+                                       mse_rows);
     return cudaGetLastError();
 }
 

@@ -102,7 +102,7 @@ cudaError_t launch_splat_reduce(int64_t total, int64_t n, const int32_t *ids, co
 cudaError_t launch_view_accumulate(int64_t n, int nview, const double2 *vals,
                                    double *cam_imp_rows, double *imp_acc, double *dmse_acc,
                                    double *dmse_rows, cudaStream_t st);
-cudaError_t launch_mse_reduce(int nview, int ntiles, const double *tile_se, double P,
+cudaError_t launch_mse_reduce(int nview, int ntiles, double *tile_se, double P,
                               double *mse_acc, double *mse_rows, cudaStream_t st);
 cudaError_t launch_finalize(int64_t n, int S, double *imp, double *dmse, double *mse,
                             cudaStream_t st);
