@@ -50,7 +50,7 @@ struct potr_ctx {
     bool counting = false;
     DevBuf counters;
     int64_t pairs_total = 0;
-    DevBuf tile_counter, ci_v, dm_v, bbox, overflow, vidx, khi, skhi, prep;
+    DevBuf tile_counter, ci_v, dm_v, bbox, overflow, vidx, khi, skhi, prep, spans;
     DevBuf met_mom, met_part, met_w, met_out;  // image metrics scratch
     bool depth_split = false;  // last bin_batch sorted split keys: skey not materialised
     double scene_lo[3] = {0, 0, 0}, scene_hi[3] = {0, 0, 0};  // splat position bbox
@@ -311,6 +311,7 @@ int bin_batch(potr_ctx *ctx, const potr_splats &sp, const potr_camera *cams, int
     std::memset(&cb, 0, sizeof(cb));
     for (int v = 0; v < nview; v++) cb.cam[v] = to_cam(cams[v]);
     ENSURE(ctx->rec, sizeof(SplatRec) * total);
+    ENSURE(ctx->spans, sizeof(TileSpan) * total);
     ENSURE(ctx->key, sizeof(uint64_t) * total);
     ENSURE(ctx->skey, sizeof(uint64_t) * total);
     ENSURE(ctx->sids, sizeof(int32_t) * total);
@@ -347,7 +348,8 @@ int bin_batch(potr_ctx *ctx, const potr_splats &sp, const potr_camera *cams, int
     {
         Stage _st(ctx, POTR_STAGE_PREPROCESS);
         LAUNCH(1, launch_preprocess(sp, P<SplatPrep>(ctx->prep), cb, nview, g.tiles_x, all_colors ? 1 : 0, cull ? 1 : 0, dk,
-                                    P<SplatRec>(ctx->rec), P<uint64_t>(ctx->key),
+                                    P<SplatRec>(ctx->rec), P<TileSpan>(ctx->spans),
+                                    P<uint64_t>(ctx->key),
                                     P<int32_t>(ctx->cnt), P<int32_t>(ctx->vidx), counters(ctx),
                                     ctx->stream));
         _st.end();
@@ -447,7 +449,8 @@ int bin_batch(potr_ctx *ctx, const potr_splats &sp, const potr_camera *cams, int
     {
         Stage _st(ctx, POTR_STAGE_DUPLICATE);
         LAUNCH(1, launch_duplicate(total, n, P<int32_t>(ctx->sids), P<int64_t>(ctx->offs),
-                                   P<SplatRec>(ctx->rec), g.tiles_x, g.ntiles, sb, key16,
+                                   P<SplatRec>(ctx->rec), P<TileSpan>(ctx->spans), g.tiles_x,
+                                   g.ntiles, sb, key16,
                                    cull ? 1 : 0, ctx->tkey.p, P<int32_t>(ctx->dup_id),
                                    with_rank ? P<int32_t>(ctx->dup_rank) : nullptr, ctx->stream));
         _st.end();
@@ -604,6 +607,7 @@ void potr_destroy(potr_ctx *ctx) {
     if (ctx->ci_v.p) cudaFree(ctx->ci_v.p);
     if (ctx->dm_v.p) cudaFree(ctx->dm_v.p);
     if (ctx->khi.p) cudaFree(ctx->khi.p);
+    if (ctx->spans.p) cudaFree(ctx->spans.p);
     for (DevBuf *b : {&ctx->met_mom, &ctx->met_part, &ctx->met_w, &ctx->met_out})
         if (b->p) cudaFree(b->p);
     if (ctx->prep.p) cudaFree(ctx->prep.p);

@@ -165,6 +165,17 @@ struct Proj {
     bool valid;
 };
 
+// Tile rows of a drawn (splat, view) entry as the preprocess culled them, so
+// the duplicate kernel need not redo the ellipse test: rows [ty0, ty0 + nrows),
+// tile columns [c[2r], c[2r+1]] of the first kSpanRows rows (c0 > c1: culled
+// row).  Entries with more rows are recomputed from the record.
+constexpr int kSpanRows = 3;
+struct __align__(16) TileSpan {
+    uint16_t ty0, nrows;
+    uint16_t c[2 * kSpanRows];
+};
+static_assert(sizeof(TileSpan) == 16, "TileSpan must stay 16 bytes");
+
 // View-independent per-splat terms, computed once per call (k_splat_prep)
 // and read by the preprocess of every view batch.
 struct __align__(16) SplatPrep {

@@ -134,6 +134,7 @@ __global__ void POTR_PRE_BOUNDS k_preprocess(potr_splats sp, const SplatPrep *__
                                                      int tiles_x, int all_colors, int cull,
                                                      DepthKey dk,
                                                      SplatRec *__restrict__ rec,
+                                                     TileSpan *__restrict__ spans,
                                                      uint64_t *__restrict__ key,
                                                      int32_t *__restrict__ cnt,
                                                      int32_t *__restrict__ vidx,
@@ -209,18 +210,27 @@ __global__ void POTR_PRE_BOUNDS k_preprocess(potr_splats sp, const SplatPrep *__
             r.y1 = (int32_t)y1;
             if (!draw) r.x0 = 1, r.x1 = 0;  // empty: never drawn
             rec[g] = r;
-            if (draw && cull) {
-                const CullEllipse ce = cull_ellipse(r);
-                for (int ty = r.y0 >> kTileHLog2; ty <= (r.y1 >> kTileHLog2); ty++) {
-                    int t0, t1;
-                    if (row_span(ce, ty, &t0, &t1)) c += t1 - t0 + 1;
+            if (draw) {
+                const int ty0 = r.y0 >> kTileHLog2, ty1 = r.y1 >> kTileHLog2;
+                const int bx0 = r.x0 >> kTileWLog2, bx1 = r.x1 >> kTileWLog2;
+                TileSpan sp_;
+                sp_.ty0 = (uint16_t)ty0;
+                sp_.nrows = (uint16_t)(ty1 - ty0 + 1);
+                CullEllipse ce;
+                if (cull) ce = cull_ellipse(r);
+                for (int ty = ty0; ty <= ty1; ty++) {
+                    int t0 = bx0, t1 = bx1;
+                    if (cull && !row_span(ce, ty, &t0, &t1)) t0 = 1, t1 = 0;
+                    c += t1 - t0 + 1;
+                    if (ty - ty0 < kSpanRows) {
+                        sp_.c[2 * (ty - ty0)] = (uint16_t)t0;
+                        sp_.c[2 * (ty - ty0) + 1] = (uint16_t)t1;
+                    }
                 }
+                spans[g] = sp_;
             }
         }
         if (draw) {
-            const int tx0 = (int)x0 >> kTileWLog2, tx1 = (int)x1 >> kTileWLog2;
-            const int ty0 = (int)y0 >> kTileHLog2, ty1 = (int)y1 >> kTileHLog2;
-            if (!cull) c = (tx1 - tx0 + 1) * (ty1 - ty0 + 1);
             if (counters)  // E: pixels the reference loop visits (rasterizer.py:159-161)
                 atomicAdd(&counters[0], (unsigned long long)((x1 - x0 + 1.0) * (y1 - y0 + 1.0)));
         }
@@ -272,8 +282,9 @@ __global__ void k_gather_counts(int64_t total, int64_t n, const int32_t *__restr
 template <typename KeyT>
 __global__ void k_duplicate(int64_t total, int64_t n, const int32_t *__restrict__ ids,
                             const int64_t *__restrict__ offs, const SplatRec *__restrict__ rec,
-                            int tiles_x, int ntiles, int sb, int cull, KeyT *__restrict__ tkey,
-                            int32_t *__restrict__ dup_id, int32_t *__restrict__ dup_rank) {
+                            const TileSpan *__restrict__ spans, int tiles_x, int ntiles, int sb,
+                            int cull, KeyT *__restrict__ tkey, int32_t *__restrict__ dup_id,
+                            int32_t *__restrict__ dup_rank) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= total) return;
     int64_t o = offs[i];
@@ -281,6 +292,21 @@ __global__ void k_duplicate(int64_t total, int64_t n, const int32_t *__restrict_
     if (o == e) return;
     const int64_t v = i / n;
     const int32_t g = ids[i];
+    const uint32_t tbase0 = (uint32_t)((v % sb) * ntiles);
+    const int32_t rank = (int32_t)(i - v * n);
+    const TileSpan s = spans[g];
+    if (s.nrows <= kSpanRows) {  // the preprocess's rows: no record read, no recompute
+        for (int r = 0; r < s.nrows; r++) {
+            const int ty = s.ty0 + r;
+            for (int tx = s.c[2 * r]; tx <= (int)s.c[2 * r + 1]; tx++) {
+                tkey[o] = (KeyT)(tbase0 + (uint32_t)(ty * tiles_x + tx));
+                dup_id[o] = g;
+                if (dup_rank) dup_rank[o] = rank;
+                o++;
+            }
+        }
+        return;
+    }
     const SplatRec &R = rec[g];
     const int tx0 = R.x0 >> kTileWLog2, tx1 = R.x1 >> kTileWLog2;
     const int ty0 = R.y0 >> kTileHLog2, ty1 = R.y1 >> kTileHLog2;
@@ -946,12 +972,12 @@ size_t raster_smem_bytes() { return sizeof(WarpSmem) * kRasterWarps; }
 cudaError_t launch_preprocess(const potr_splats &sp, const SplatPrep *prep, const CamBatch &cams,
                               int nview,
                               int tiles_x, int all_colors, int cull, const DepthKey &dk,
-                              SplatRec *rec, uint64_t *key, int32_t *cnt, int32_t *vidx,
-                              unsigned long long *counters, cudaStream_t st) {
+                              SplatRec *rec, TileSpan *spans, uint64_t *key, int32_t *cnt,
+                              int32_t *vidx, unsigned long long *counters, cudaStream_t st) {
     if (sp.n == 0) return cudaSuccess;
     k_preprocess<<<grid_for(sp.n * nview, 128), 128, 0, st>>>(sp, prep, cams, nview, tiles_x,
-                                                               all_colors, cull, dk, rec, key,
-                                                               cnt, vidx, counters);
+                                                               all_colors, cull, dk, rec, spans,
+                                                               key, cnt, vidx, counters);
     return cudaGetLastError();
 }
 
@@ -1120,17 +1146,17 @@ cudaError_t scan_temp(int64_t n, size_t *bytes) {
 }
 
 cudaError_t launch_duplicate(int64_t total, int64_t n, const int32_t *ids, const int64_t *offs,
-                             const SplatRec *rec, int tiles_x, int ntiles, int sb, bool key16,
-                             int cull, void *tkey, int32_t *dup_id, int32_t *dup_rank,
-                             cudaStream_t st) {
+                             const SplatRec *rec, const TileSpan *spans, int tiles_x, int ntiles,
+                             int sb, bool key16, int cull, void *tkey, int32_t *dup_id,
+                             int32_t *dup_rank, cudaStream_t st) {
     if (total == 0) return cudaSuccess;
     if (key16)
         k_duplicate<uint16_t><<<grid_for(total, 256), 256, 0, st>>>(
-            total, n, ids, offs, rec, tiles_x, ntiles, sb, cull, (uint16_t *)tkey, dup_id,
+            total, n, ids, offs, rec, spans, tiles_x, ntiles, sb, cull, (uint16_t *)tkey, dup_id,
             dup_rank);
     else
         k_duplicate<uint32_t><<<grid_for(total, 256), 256, 0, st>>>(
-            total, n, ids, offs, rec, tiles_x, ntiles, sb, cull, (uint32_t *)tkey, dup_id,
+            total, n, ids, offs, rec, spans, tiles_x, ntiles, sb, cull, (uint32_t *)tkey, dup_id,
             dup_rank);
     return cudaGetLastError();
 }

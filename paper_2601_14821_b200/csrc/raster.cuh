@@ -51,10 +51,9 @@ cudaError_t launch_bbox(int64_t n, const double *pos, unsigned long long *out, c
 // Per-splat view-independent terms (Sigma, prefilter threshold), once per call.
 cudaError_t launch_splat_prep(const potr_splats &sp, SplatPrep *prep, cudaStream_t st);
 cudaError_t launch_preprocess(const potr_splats &sp, const SplatPrep *prep, const CamBatch &cams,
-                              int nview,
-                              int tiles_x, int all_colors, int cull, const DepthKey &dk,
-                              SplatRec *rec, uint64_t *key, int32_t *cnt, int32_t *vidx,
-                              unsigned long long *counters, cudaStream_t st);
+                              int nview, int tiles_x, int all_colors, int cull, const DepthKey &dk,
+                              SplatRec *rec, TileSpan *spans, uint64_t *key, int32_t *cnt,
+                              int32_t *vidx, unsigned long long *counters, cudaStream_t st);
 cudaError_t launch_project_dump(const potr_splats &sp, const Cam &cam, double *mean2d,
                                 double *cov2d, double *depth, double *radius, uint8_t *valid,
                                 double *colors, cudaStream_t st);
@@ -82,9 +81,9 @@ cudaError_t scan_counts(void *temp, size_t temp_bytes, const int32_t *ids, const
                         int64_t *cnt_sorted, int64_t *offs, int64_t total, int64_t n,
                         cudaStream_t st);
 cudaError_t launch_duplicate(int64_t total, int64_t n, const int32_t *ids, const int64_t *offs,
-                             const SplatRec *rec, int tiles_x, int ntiles, int sb, bool key16,
-                             int cull, void *tkey, int32_t *dup_id, int32_t *dup_rank,
-                             cudaStream_t st);
+                             const SplatRec *rec, const TileSpan *spans, int tiles_x, int ntiles,
+                             int sb, bool key16, int cull, void *tkey, int32_t *dup_id,
+                             int32_t *dup_rank, cudaStream_t st);
 cudaError_t tile_sort_temp(int64_t K, int nkeys, bool key16, size_t *bytes);
 cudaError_t tile_sort(void *temp, size_t temp_bytes, bool key16, const void *tkey, void *skey,
                       const int32_t *iota, int32_t *perm, int64_t K, int nkeys, cudaStream_t st);
