@@ -115,9 +115,9 @@ def compact_scene(splats, cameras, camera_importance, config: CompactionConfig, 
                                                          splats.rotations))),
                 np.zeros((0, 3, 16)), {"failed": [], "fallback_dc_only": 0})
     rgb, yc, status = compact_device(splats, cameras, camera_importance, config)
-    rgb = rgb.cpu().numpy()
-    yc = yc.cpu().numpy()
-    status = status.cpu().numpy()
+    rgb = D.to_host(rgb)
+    yc = D.to_host(yc)
+    status = D.to_host(status)
     failed = np.nonzero(status == STATUS_FAILED)[0]
     fallback = int(np.count_nonzero(status == STATUS_DC_FALLBACK))
     out = Splats(np.array(splats.positions, dtype=np.float64, copy=True), rgb,

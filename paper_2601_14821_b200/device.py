@@ -61,6 +61,41 @@ def to_device(arr, device, shape=None):
         return torch.from_numpy(a).to(device, non_blocking=False)
 
 
+_PINNED_MAX = 256 << 20        # results up to this size land in pinned memory directly
+_STAGE_BYTES = 64 << 20        # larger ones stream through one pinned staging buffer
+_stage = None
+
+
+def to_host(t):
+    """Device tensor -> fresh numpy array, through pinned memory.
+
+    A pageable destination makes the driver stage the copy at ~2 GB/s (22 ms
+    for forward_stats' 48 MB at C3, 2.4 s for 200 targets); pinned memory
+    takes the DMA at PCIe speed.  Results up to 256 MB are returned as views
+    of a pinned tensor (torch's caching host allocator recycles it once the
+    array is dropped); larger ones are copied through a 64 MB pinned buffer."""
+    global _stage
+    t = t.detach().contiguous()
+    nbytes = t.numel() * t.element_size()
+    if not t.is_cuda or nbytes == 0:
+        return t.cpu().numpy()
+    if nbytes <= _PINNED_MAX:
+        out = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
+        out.copy_(t)
+        return out.numpy()
+    out = np.empty(tuple(t.shape), dtype=torch.empty(0, dtype=t.dtype).numpy().dtype)
+    if _stage is None:
+        _stage = torch.empty(_STAGE_BYTES, dtype=torch.uint8, pin_memory=True)
+    src = t.reshape(-1).view(torch.uint8)
+    dst = out.reshape(-1).view(np.uint8)
+    stage_np = _stage.numpy()
+    for off in range(0, nbytes, _STAGE_BYTES):
+        m = min(_STAGE_BYTES, nbytes - off)
+        _stage[:m].copy_(src[off:off + m])
+        dst[off:off + m] = stage_np[:m]
+    return out
+
+
 def empty(shape, device, dtype=torch.float64):
     """Device buffer; never zero-sized (the C ABI wants a real pointer)."""
     t = torch.empty(shape, dtype=dtype, device=device)
@@ -170,7 +205,7 @@ class LazyHostArray:
 
     def numpy(self):
         if self._host is None:
-            self._host = self._tensor.cpu().numpy()
+            self._host = to_host(self._tensor)
         return self._host
 
     def __array__(self, dtype=None, copy=None):

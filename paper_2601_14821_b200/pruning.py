@@ -117,10 +117,11 @@ def _removal_order_device(dm_dev, idx_dev, delta_mse_max, a):
 def select_removal_set_device(dm_dev, delta_mse, importance, budget, delta_mse_max, a=10.0):
     """select_removal_set with the candidate ordering sorted on the device."""
     import torch
+    from . import device as D
     cand_dev = torch.nonzero(dm_dev < delta_mse_max).squeeze(1)
     if cand_dev.numel() == 0:
         return np.empty(0, dtype=np.int64)
-    cand = _removal_order_device(dm_dev, cand_dev, delta_mse_max, a).cpu().numpy()
+    cand = D.to_host(_removal_order_device(dm_dev, cand_dev, delta_mse_max, a))
     imp = np.asarray(importance, dtype=np.float64)[cand]
     positive = imp > 0.0
     take = ~positive
@@ -148,8 +149,9 @@ def _check_targets(cameras, targets):
 
 def _to_host_splats(ds):
     from .scene import Splats
-    return Splats(ds.positions.cpu().numpy(), ds.sh.cpu().numpy(), ds.opacities.cpu().numpy(),
-                  ds.scales.cpu().numpy(), ds.rotations.cpu().numpy())
+    from . import device as D
+    return Splats(D.to_host(ds.positions), D.to_host(ds.sh), D.to_host(ds.opacities),
+                  D.to_host(ds.scales), D.to_host(ds.rotations))
 
 
 def _run_pruning_device(splats, cameras, targets, config, report_sink, first_iteration,
@@ -169,7 +171,7 @@ def _run_pruning_device(splats, cameras, targets, config, report_sink, first_ite
     for it in range(first_iteration, last_iteration + 1):
         imp_d, _, dm_d, mse_d = forward_stats_device(ds, cameras, dev_targets,
                                                      want_cam_imp=False)
-        host = torch.cat([imp_d, dm_d, mse_d]).cpu().numpy()
+        host = D.to_host(torch.cat([imp_d, dm_d, mse_d]))
         n = ds.n
         importance, delta_mse, mse = host[:n], host[n:2 * n], float(host[2 * n])
         if not (delta_mse < config.delta_mse_max).any():
@@ -255,7 +257,7 @@ def _run_pruning_to_counts_device(splats, cameras, targets, cumulative_counts, d
             _, _, dm_d, _ = forward_stats_device(ds, cameras, dev_targets, want_cam_imp=False)
             idx = torch.arange(ds.n, device=dev)
             order = _removal_order_device(dm_d, idx, delta_mse_max, a)
-            sel = np.sort(order[:batch].cpu().numpy())
+            sel = np.sort(D.to_host(order[:batch]))
             mask = np.ones(ds.n, dtype=bool)
             mask[sel] = False
             mask_d = torch.from_numpy(mask).to(dev)

@@ -179,7 +179,7 @@ def render_image(splats, camera) -> np.ndarray:
     ctx = D.context()
     dev = D.current_device()
     image, _ = _render_device(D.DeviceSplats.from_host(splats, dev), camera, ctx, dev)
-    return image.cpu().numpy()
+    return D.to_host(image)
 
 
 def prune_difference(record: RenderRecord, x, y, splat_id):
@@ -245,8 +245,8 @@ def forward_stats(splats, cameras, targets=None, threads=1) -> ForwardStats:
     imp, cam_imp, dm, mse = forward_stats_device(ds, cameras, dev_targets)
     cam_imp = D.LazyHostArray(cam_imp)
     if targets is None:
-        return ForwardStats(imp.cpu().numpy(), cam_imp, None, None)
-    host = torch.cat([imp, dm, mse]).cpu().numpy()
+        return ForwardStats(D.to_host(imp), cam_imp, None, None)
+    host = D.to_host(torch.cat([imp, dm, mse]))
     return ForwardStats(host[:n], cam_imp, host[n:2 * n], float(host[2 * n]))
 
 
@@ -283,7 +283,7 @@ def render_targets(splats, cameras, threads=1):
     """Reference renders of the uncompressed model, read-only (:371-377)."""
     imgs = []
     for image in render_targets_device(splats, cameras):
-        img = image.cpu().numpy()
+        img = D.to_host(image)
         img.flags.writeable = False
         imgs.append(img)
     return imgs
