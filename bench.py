@@ -518,20 +518,26 @@ def scene_measure(args, world, ds, cams, my_cams, tptr, cam_arr, lo, hi, ctx, de
     yc = torch.empty((n, 3, 16), dtype=torch.float64, device=dev)
     status = torch.empty(n, dtype=torch.int8, device=dev)
 
-    def run():
+    def run(fused):
         t = {}
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
         t0 = time.perf_counter()
         iptr = (ctypes.c_void_p * max(1, len(imgs)))(*[t.data_ptr() for t in imgs])
-        ctx.call("potr_render_batch", ctypes.byref(ds0.struct()), len(my_cams),
-                 _native_cams(my_cams), iptr, None)
-        torch.cuda.synchronize()
-        t1 = time.perf_counter()
         imp.zero_(), dm.zero_(), mse.zero_()
-        ctx.call("potr_score_views", ctypes.byref(ds0.struct()), hi - lo, cam_arr, tp,
-                 D.ptr(imp), D.ptr(ci), D.ptr(dm), D.ptr(mse))
+        if fused:  # targets + the first prune-score pass in one walk (potr_score_views_self)
+            ctx.call("potr_score_views_self", ctypes.byref(ds0.struct()), hi - lo, cam_arr, iptr,
+                     D.ptr(imp), D.ptr(ci), D.ptr(dm), D.ptr(mse))
+            torch.cuda.synchronize()
+            t1 = time.perf_counter()
+        else:
+            ctx.call("potr_render_batch", ctypes.byref(ds0.struct()), len(my_cams),
+                     _native_cams(my_cams), iptr, None)
+            torch.cuda.synchronize()
+            t1 = time.perf_counter()
+            ctx.call("potr_score_views", ctypes.byref(ds0.struct()), hi - lo, cam_arr, tp,
+                     D.ptr(imp), D.ptr(ci), D.ptr(dm), D.ptr(mse))
         if world > 1:
             red = torch.cat([imp, dm, mse])
             dist.all_reduce(red)
@@ -552,11 +558,18 @@ def scene_measure(args, world, ds, cams, my_cams, tptr, cam_arr, lo, hi, ctx, de
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return [float(x) for x in t.cpu()]
 
-    run()  # warm
-    parts = run()
+    run(False)  # warm
+    parts = run(False)
     ac = float((yc[:, :, 1:] == 0).double().mean().item())
-    out = {"total_s": sum(parts), "render_targets_s": parts[0], "prune_score_s": parts[1],
-           "sh_recompute_s": parts[2], "lambda_y": 1e-7, "ac_sparsity": ac}
+    fused = run(True)
+    out = {"total_s": sum(fused), "targets_and_prune_score_s": fused[0],
+           "sh_recompute_s": fused[2],
+           "separate_passes": {"total_s": sum(parts), "render_targets_s": parts[0],
+                               "prune_score_s": parts[1], "sh_recompute_s": parts[2]},
+           "note": "total_s: the targets are rendered by the same walk that scores them "
+                   "(potr_score_views_self, bit-identical to render_targets + "
+                   "compute_delta_mse); separate_passes: the two calls one after the other",
+           "lambda_y": 1e-7, "ac_sparsity": ac}
     if world == 1 and not args.no_prune48:
         out.update(prune48_measure(splats, cams, imgs))
     return out

@@ -100,6 +100,15 @@ int potr_score_views_rows(potr_ctx *ctx, const potr_splats *splats, int ncam,
                           const potr_camera *cams, const double *const *targets,
                           double *camera_importance, double *dmse_rows, double *mse_rows);
 
+/* render_targets + the first compute_delta_mse of an encode in ONE pass: the
+ * targets are the renders of these very splats (pipeline.py / pruning.py:132
+ * at iteration 1), so c - c_t = 0 exactly and the images are written as the
+ * targets while the same walk scores them.  images: host array of ncam device
+ * pointers (H, W, 3), outputs.  Sums as potr_score_views (mse_sum gets 0). */
+int potr_score_views_self(potr_ctx *ctx, const potr_splats *splats, int ncam,
+                          const potr_camera *cams, double *const *images, double *imp_sum,
+                          double *camera_importance, double *dmse_sum, double *mse_sum);
+
 /* rasterizer.py:348-352: divide the sums by the total camera count in place
  * (dmse_sum / mse_sum nullable). */
 int potr_finalize_stats(potr_ctx *ctx, int64_t n, int total_cams, double *imp_sum,

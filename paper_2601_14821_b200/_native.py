@@ -71,6 +71,10 @@ _SIGNATURES = {
                                              ctypes.c_int, ctypes.POINTER(PotrCamera),
                                              ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
                                              ctypes.c_void_p]),
+    "potr_score_views_self": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(PotrSplats),
+                                             ctypes.c_int, ctypes.POINTER(PotrCamera),
+                                             ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+                                             ctypes.c_void_p, ctypes.c_void_p]),
     "potr_finalize_stats": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int64, ctypes.c_int,
                                            ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]),
     "potr_render": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(PotrSplats),

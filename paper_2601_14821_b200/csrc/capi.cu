@@ -509,10 +509,13 @@ int batch_len(potr_ctx *ctx, const potr_camera *cams, int s, int ncam, int64_t n
     return b;
 }
 
+// images (nullable): with targets == images the targets are this very render
+// (self-target mode: the first pruning iteration of an encode, whose targets
+// are the renders of the unmodified model) -- rendered and scored in one pass.
 int score_views_impl(potr_ctx *ctx, const potr_splats *sp, int ncam, const potr_camera *cams,
                      const double *const *targets, double *imp_sum, double *cam_imp,
                      double *dmse_sum, double *mse_sum, double *dmse_rows = nullptr,
-                     double *mse_rows = nullptr) {
+                     double *mse_rows = nullptr, double *const *images = nullptr) {
     const int64_t n = sp->n;
     int brc = compute_scene_bounds(ctx, *sp);
     if (brc) return brc;
@@ -528,6 +531,10 @@ int score_views_impl(potr_ctx *ctx, const potr_splats *sp, int ncam, const potr_
         ViewGeom g = geom(cams[s]);
         RasterArgs a = raster_args(ctx, cams[s], nb);
         for (int v = 0; v < nb; v++) a.target[v] = targets ? targets[s + v] : nullptr;
+        if (images) {
+            a.self_target = 1;
+            for (int v = 0; v < nb; v++) a.image[v] = images[s + v];
+        }
         ENSURE(ctx->ci_v, sizeof(double2) * n * nb);
         {
             Stage _st(ctx, POTR_STAGE_RASTER);
@@ -670,6 +677,22 @@ int potr_score_views_rows(potr_ctx *ctx, const potr_splats *splats, int ncam,
     return score_views_impl(ctx, splats, ncam, cams, targets, scratch, camera_importance,
                             targets ? scratch + n : nullptr, targets ? scratch + 2 * n : nullptr,
                             dmse_rows, mse_rows);
+}
+
+int potr_score_views_self(potr_ctx *ctx, const potr_splats *splats, int ncam,
+                          const potr_camera *cams, double *const *images, double *imp_sum,
+                          double *camera_importance, double *dmse_sum, double *mse_sum) {
+    if (!ctx) return POTR_E_ARG;
+    CK(cudaSetDevice(ctx->device));
+    int rc = check_splats(ctx, splats);
+    if (rc) return rc;
+    if (ncam < 0 || (ncam > 0 && !cams)) return fail(ctx, POTR_E_ARG, "bad camera list");
+    if (!imp_sum || !dmse_sum || !mse_sum) return fail(ctx, POTR_E_ARG, "NULL sum output");
+    if (ncam > 0 && !images) return fail(ctx, POTR_E_ARG, "images is NULL");
+    for (int v = 0; v < ncam; v++)
+        if (!images[v]) return fail(ctx, POTR_E_ARG, "image pointer is NULL");
+    return score_views_impl(ctx, splats, ncam, cams, images, imp_sum, camera_importance,
+                            dmse_sum, mse_sum, nullptr, nullptr, images);
 }
 
 int potr_finalize_stats(potr_ctx *ctx, int64_t n, int total_cams, double *imp_sum,

@@ -689,7 +689,7 @@ __global__ void __launch_bounds__(32 * kRasterWarps, POTR_RASTER_MIN_BLOCKS) k_r
         double dr0 = 0.0, dr1 = 0.0, dr2 = 0.0;
         if (MODE == kScore) {
             double se = 0.0;
-            if (inside) {
+            if (inside && !a.self_target) {  // self target: c - c_t = 0 exactly
                 dr0 = PK0 - target[3 * pix];
                 dr1 = PK1 - target[3 * pix + 1];
                 dr2 = PK2 - target[3 * pix + 2];

@@ -20,6 +20,7 @@ struct RasterArgs {
     double *image[kMaxViewBatch];         // per view (H,W,3), nullable
     double *trans[kMaxViewBatch];         // per view (H,W), nullable
     double2 *partial;         // per duplicate (dSE, T*alpha)
+    int self_target;          // score mode: the targets are this render (dr = 0), images out
     double *tile_se;          // per tile squared error (score mode)
     // records mode
     unsigned long long *rec_counter;

@@ -250,6 +250,46 @@ def forward_stats(splats, cameras, targets=None, threads=1) -> ForwardStats:
     return ForwardStats(host[:n], cam_imp, host[n:2 * n], float(host[2 * n]))
 
 
+def render_and_score_device(ds, cameras, want_cam_imp=True):
+    """render_targets + forward_stats against those very targets, in one pass
+    (potr_score_views_self): the first scoring of an encode, whose targets are
+    the renders of the unmodified model.  Returns device tensors (images,
+    importance, camera_importance or None, delta_mse, mse), normalised."""
+    ctx = D.context()
+    dev = ds.device
+    n, S = ds.n, len(cameras)
+    imgs = [D.empty((int(c.height), int(c.width), 3), dev) for c in cameras]
+    imp = torch.zeros(max(n, 1), dtype=torch.float64, device=dev)
+    dm = torch.zeros(max(n, 1), dtype=torch.float64, device=dev)
+    mse = torch.zeros(1, dtype=torch.float64, device=dev)
+    cam_imp = D.empty((max(S, 1), max(n, 1)), dev) if want_cam_imp else None
+    ptrs = (ctypes.c_void_p * max(S, 1))(*[t.data_ptr() for t in imgs])
+    ctx.call("potr_score_views_self", ctypes.byref(ds.struct()), S,
+             _native.camera_array(cameras), ptrs, D.ptr(imp), D.ptr(cam_imp), D.ptr(dm),
+             D.ptr(mse))
+    ctx.call("potr_finalize_stats", ctypes.c_int64(n), S, D.ptr(imp), D.ptr(dm), D.ptr(mse))
+    return (imgs, imp[:n], cam_imp[:S, :n] if cam_imp is not None else None, dm[:n], mse)
+
+
+def render_targets_and_delta_mse(splats, cameras):
+    """(render_targets(splats, cameras), compute_delta_mse(splats, cameras,
+    those targets)) from one pass; bit-identical to the two calls."""
+    if not cameras:
+        raise ZeroDivisionError("float division by zero")
+    dev = D.current_device()
+    ds = D.DeviceSplats.from_host(splats, dev)
+    n = ds.n
+    imgs, imp, cam_imp, dm, mse = render_and_score_device(ds, cameras)
+    targets = []
+    for image in imgs:
+        img = D.to_host(image)
+        img.flags.writeable = False
+        targets.append(img)
+    host = D.to_host(torch.cat([imp, dm, mse]))
+    return targets, ForwardStats(host[:n], D.LazyHostArray(cam_imp), host[n:2 * n],
+                                 float(host[2 * n]))
+
+
 def compute_importance(splats, cameras, threads=1):
     """Per-splat importance plus the per-camera breakdown (:355-358)."""
     stats = forward_stats(splats, cameras, targets=None, threads=threads)

@@ -148,6 +148,22 @@ def test_score_rows_sum_to_fused_sums(R):
     assert np.array_equal(ci.cpu().numpy(), np.asarray(st.camera_importance))
 
 
+def test_render_and_score_in_one_pass(R):
+    """render_targets + compute_delta_mse against those targets == the fused
+    self-target pass, bit for bit (the first scoring of an encode)."""
+    from paper_2601_14821_b200.fixture import make_fixture
+    for splats, cams in (small_scene(), make_fixture(20000, 10, 4, width=96, height=72)):
+        tg = R.render_targets(splats, cams)
+        st = R.compute_delta_mse(splats, cams, tg)
+        tg2, st2 = R.render_targets_and_delta_mse(splats, cams)
+        for a, b in zip(tg, tg2):
+            assert np.array_equal(a, b) and not b.flags.writeable
+        assert np.array_equal(st.importance, st2.importance)
+        assert np.array_equal(st.delta_mse, st2.delta_mse)
+        assert np.array_equal(np.asarray(st.camera_importance), np.asarray(st2.camera_importance))
+        assert st.mse == st2.mse == 0.0
+
+
 def test_forward_stats_bit_reproducible(R):
     splats, cams = small_scene()
     g = golden("small_scene")
