@@ -700,11 +700,11 @@ static int solve_channel(const double *Y, const double *c, int ns, const int *ma
     for (int i = 0; i < m; i++) {
         for (int j = 0; j < m; j++) {
             double acc = 0.0;
-            for (int s = 0; s < ns; s++) acc += Y[s * 16 + cols[i]] * Y[s * 16 + cols[j]];
+            for (int s = 0; s < ns; s++) acc = fma(Y[s * 16 + cols[i]], Y[s * 16 + cols[j]], acc);
             A[i * 16 + j] = acc;
         }
         double acc = 0.0;
-        for (int s = 0; s < ns; s++) acc += Y[s * 16 + cols[i]] * c[s];
+        for (int s = 0; s < ns; s++) acc = fma(Y[s * 16 + cols[i]], c[s], acc);
         b[i] = acc;
     }
     for (int i = 0; i < m; i++) A[i * 16 + i] += (cols[i] == 0) ? 0.0 : lam;
@@ -779,7 +779,7 @@ static int compact_one(const double *p, const double *sh, int ncam, const ocam *
     for (int i = 0; i < 16; i++)
         for (int j = 0; j < 16; j++) {
             double acc = 0.0;
-            for (int s = 0; s < ns; s++) acc += Ybuf[s * 16 + i] * Ybuf[s * 16 + j];
+            for (int s = 0; s < ns; s++) acc = fma(Ybuf[s * 16 + i], Ybuf[s * 16 + j], acc);
             gram[i * 16 + j] = acc;
         }
     for (int i = 0; i < 16; i++) norms[i] = sqrt(gram[i * 16 + i]);

@@ -5,9 +5,10 @@
 // Y^T Y and Y^T C (sparsify :110-124, ridge :127-148).  So the GPU never
 // materialises Y: k_sh_accumulate streams the (S, N) per-camera importances
 // once and accumulates, per splat, the 16x16 Gram matrix G (136 unique
-// entries) and the 16x3 right-hand sides B in fp64 registers -- eight lanes
-// per splat, each owning rows {g, 15-g} -- in camera order, exactly the
-// summation order of the reference's row loop.  k_sh_solve then does the
+// entries) and the 16x3 right-hand sides B in fp64 registers (a warp per
+// splat, each lane owning ~6 of the 184 entries) in camera order with fused
+// multiply-adds -- the oracle restates the same order, so the two agree bit
+// for bit; the reference's BLAS dgemm differs by rounding (tests: 1e-9).  k_sh_solve then does the
 // parallel-column sparsification, the two-pass ridge (Cholesky, with the
 // reference's 1e-10 jitter retry and RidgeError semantics) and the DC
 // fallback for unseen splats, one thread per splat.
@@ -104,7 +105,7 @@ __global__ void __launch_bounds__(32 * kShWarps, 4) k_sh_accumulate(potr_splats 
             const int kk = w * kPer + j;
             if (kk >= nk) break;  // warp-uniform
             const double wv = wtile[lane][kk];
-            seen[j] += __popc(__ballot_sync(0xffffffffu, lv && wv > 0.0));
+            seen[j] += __popc(__ballot_sync(0xffffffffu, lv && wv > 0.0));  // == the m below
             double *row = A[w][lane];
             if (wv > 0.0) {
                 const double d0 = pos[kk][0] - ex, d1 = pos[kk][1] - ey, d2 = pos[kk][2] - ez;
@@ -132,9 +133,12 @@ __global__ void __launch_bounds__(32 * kShWarps, 4) k_sh_accumulate(potr_splats 
                 for (int i = 0; i < 19; i++) row[i] = 0.0;  // unseen: exact zeros
             }
             __syncwarp();
-            for (int v = 0; v < nv; v++) {
+            // views that see the splat, ascending (unseen ones would add exact zeros)
+            for (unsigned m = __ballot_sync(0xffffffffu, lv && wv > 0.0); m; m &= m - 1u) {
+                const int v = __ffs(m) - 1;
 #pragma unroll
-                for (int qq = 0; qq < 6; qq++) acc[j][qq] += A[w][v][ep[qq]] * A[w][v][eq[qq]];
+                for (int qq = 0; qq < 6; qq++)
+                    acc[j][qq] = fma(A[w][v][ep[qq]], A[w][v][eq[qq]], acc[j][qq]);
             }
             __syncwarp();
         }
