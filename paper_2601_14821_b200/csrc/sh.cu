@@ -31,22 +31,49 @@ __constant__ double kYcocgToRgb[9] = {1.0, 1.0, -1.0, 1.0, 0.0, 1.0, 1.0, -1.0, 
 // Normal equations of 16 consecutive splats per CTA (4 warps x 4 splats).  Views are taken 32 at a
 // time: the (view, splat) tile of camera_importance is staged in shared
 // memory with coalesced loads; then for each splat a warp evaluates one view
-// per lane (direction, SH basis, raw colour, YCoCg -- compaction.py:100-107),
-// publishes (w*y, w*YCoCg(colour)) to shared memory, and every lane adds the
-// 32 views, in ascending order, into the ~6 of the 184 entries it owns
-// (G_ij += (w y_i)(w y_j), B_ic += (w y_i)(w c_c)).  Views a splat is not seen
-// from have w = 0 and add exact zeros, so the sums equal the reference's sums
-// over its `seen` rows (compaction.py:97-107, :114, :133-137).
+// per lane (direction, SH basis, raw colour, YCoCg -- compaction.py:100-107)
+// and publishes the row a = (w*y (16), w*YCoCg(colour) (3)) to shared memory.
+// The 184 wanted entries of a a^T -- G_ij, i <= j < 16, and B_ic = a_i a_16+c
+// -- are tiled by 2x4 register blocks (rows 2r, 2r+1; columns c0..c0+3): 28
+// lanes own one block each and add, per seen view in ascending order, 8 fused
+// products from three 16-byte shared loads.  Views a splat is not seen from
+// (w = 0) are skipped: they would add exact zeros, so the sums equal the
+// reference's sums over its `seen` rows (compaction.py:97-107, :114, :133-137).
 constexpr int kShSplatsPerBlock = 16;
 constexpr int kShWarps = 4;
-constexpr int kShRow = 19;  // w*y (16) + w*YCoCg (3)
+constexpr int kShRow = 24;  // w*y (16) + w*YCoCg (3), padded for the 2x4 blocks' 16-byte loads
+constexpr int kShBlocks = 28;
+
+// Block b of the tiling: rows 2r, 2r+1; columns c0 .. c0+3 (c0 = 2r + 4t).
+__device__ __forceinline__ void sh_block(int b, int *r, int *c0) {
+    int cum = 0;
+    for (int rr = 0; rr < 8; rr++) {
+        const int nb = (19 - 2 * rr + 3) / 4;
+        if (b < cum + nb) {
+            *r = rr;
+            *c0 = 2 * rr + 4 * (b - cum);
+            return;
+        }
+        cum += nb;
+    }
+    *r = -1;
+    *c0 = 0;
+}
+
+// Entry index of (i, j), j >= i, in the (185, N) layout: G upper triangle
+// then B (136 + 3 i + c); -1 outside the wanted region.
+__device__ __forceinline__ int sh_entry(int i, int j) {
+    if (j < i || j > 18) return -1;
+    if (j < 16) return i * 16 - (i * (i - 1)) / 2 + (j - i);
+    return 136 + 3 * i + (j - 16);
+}
 
 __global__ void __launch_bounds__(32 * kShWarps, 4) k_sh_accumulate(potr_splats sp, int ncam,
                                                        const double *__restrict__ eyes,
                                                        const double *__restrict__ cam_imp,
                                                        double *__restrict__ neq) {
     __shared__ double wtile[32][kShSplatsPerBlock + 1];
-    __shared__ double A[kShWarps][32][kShRow];
+    __shared__ __align__(16) double A[kShWarps][32][kShRow];
     __shared__ double shs[kShSplatsPerBlock][48];
     __shared__ double pos[kShSplatsPerBlock][3];
     const int64_t n = sp.n;
@@ -57,35 +84,20 @@ __global__ void __launch_bounds__(32 * kShWarps, 4) k_sh_accumulate(potr_splats 
         shs[i / 48][i % 48] = sp.sh[(k0 + i / 48) * 48 + i % 48];
     for (int i = threadIdx.x; i < nk * 3; i += blockDim.x)
         pos[i / 3][i % 3] = sp.positions[(k0 + i / 3) * 3 + i % 3];
+    for (int i = threadIdx.x; i < kShWarps * 32 * kShRow; i += blockDim.x)
+        (&A[0][0][0])[i] = 0.0;  // the pad columns stay zero
 
-    // entries owned by this lane: e = lane + 32 q, read as A[v][p] * A[v][q]
-    int ep[6], eq[6];
-#pragma unroll
-    for (int qq = 0; qq < 6; qq++) {
-        const int e = lane + 32 * qq;
-        ep[qq] = 0;
-        eq[qq] = 0;
-        if (e < 136) {
-            int i = 0, rem = e;
-            while (rem >= 16 - i) {
-                rem -= 16 - i;
-                i++;
-            }
-            ep[qq] = i;
-            eq[qq] = i + rem;
-        } else if (e < 184) {
-            ep[qq] = (e - 136) / 3;
-            eq[qq] = 16 + (e - 136) % 3;
-        }
-    }
+    int br = 0, bc = 0;
+    sh_block(lane < kShBlocks ? lane : 0, &br, &bc);
+    const bool owner = lane < kShBlocks;
     constexpr int kPer = kShSplatsPerBlock / kShWarps;  // splats per warp
-    double acc[kPer][6];
+    double acc[kPer][8];
     int seen[kPer];
 #pragma unroll
     for (int j = 0; j < kPer; j++) {
         seen[j] = 0;
 #pragma unroll
-        for (int qq = 0; qq < 6; qq++) acc[j][qq] = 0.0;
+        for (int q = 0; q < 8; q++) acc[j][q] = 0.0;
     }
 
     for (int s0 = 0; s0 < ncam; s0 += 32) {
@@ -105,7 +117,8 @@ __global__ void __launch_bounds__(32 * kShWarps, 4) k_sh_accumulate(potr_splats 
             const int kk = w * kPer + j;
             if (kk >= nk) break;  // warp-uniform
             const double wv = wtile[lane][kk];
-            seen[j] += __popc(__ballot_sync(0xffffffffu, lv && wv > 0.0));  // == the m below
+            const unsigned seen_mask = __ballot_sync(0xffffffffu, lv && wv > 0.0);
+            seen[j] += __popc(seen_mask);
             double *row = A[w][lane];
             if (wv > 0.0) {
                 const double d0 = pos[kk][0] - ex, d1 = pos[kk][1] - ey, d2 = pos[kk][2] - ez;
@@ -128,17 +141,23 @@ __global__ void __launch_bounds__(32 * kShWarps, 4) k_sh_accumulate(potr_splats 
                                       col[2] * kRgbToYcocg[c * 3 + 2];
                     row[16 + c] = yc * wv;
                 }
-            } else {
-#pragma unroll
-                for (int i = 0; i < 19; i++) row[i] = 0.0;  // unseen: exact zeros
             }
             __syncwarp();
-            // views that see the splat, ascending (unseen ones would add exact zeros)
-            for (unsigned m = __ballot_sync(0xffffffffu, lv && wv > 0.0); m; m &= m - 1u) {
-                const int v = __ffs(m) - 1;
-#pragma unroll
-                for (int qq = 0; qq < 6; qq++)
-                    acc[j][qq] = fma(A[w][v][ep[qq]], A[w][v][eq[qq]], acc[j][qq]);
+            if (owner) {
+                for (unsigned m = seen_mask; m; m &= m - 1u) {
+                    const int v = __ffs(m) - 1;
+                    const double2 a = *reinterpret_cast<const double2 *>(&A[w][v][2 * br]);
+                    const double2 b01 = *reinterpret_cast<const double2 *>(&A[w][v][bc]);
+                    const double2 b23 = *reinterpret_cast<const double2 *>(&A[w][v][bc + 2]);
+                    acc[j][0] = fma(a.x, b01.x, acc[j][0]);
+                    acc[j][1] = fma(a.x, b01.y, acc[j][1]);
+                    acc[j][2] = fma(a.x, b23.x, acc[j][2]);
+                    acc[j][3] = fma(a.x, b23.y, acc[j][3]);
+                    acc[j][4] = fma(a.y, b01.x, acc[j][4]);
+                    acc[j][5] = fma(a.y, b01.y, acc[j][5]);
+                    acc[j][6] = fma(a.y, b23.x, acc[j][6]);
+                    acc[j][7] = fma(a.y, b23.y, acc[j][7]);
+                }
             }
             __syncwarp();
         }
@@ -148,10 +167,12 @@ __global__ void __launch_bounds__(32 * kShWarps, 4) k_sh_accumulate(potr_splats 
         const int kk = w * kPer + j;
         if (kk >= nk) break;
         const int64_t k = k0 + kk;
+        if (owner) {
 #pragma unroll
-        for (int qq = 0; qq < 6; qq++) {
-            const int e = lane + 32 * qq;
-            if (e < 184) neq[(int64_t)e * n + k] += acc[j][qq];
+            for (int q = 0; q < 8; q++) {
+                const int e = sh_entry(2 * br + (q >> 2), bc + (q & 3));
+                if (e >= 0) neq[(int64_t)e * n + k] += acc[j][q];
+            }
         }
         if (lane == 0) neq[(int64_t)184 * n + k] += (double)seen[j];
     }
