@@ -39,6 +39,9 @@ __constant__ double kYcocgToRgb[9] = {1.0, 1.0, -1.0, 1.0, 0.0, 1.0, 1.0, -1.0, 
 // products from three 16-byte shared loads.  Views a splat is not seen from
 // (w = 0) are skipped: they would add exact zeros, so the sums equal the
 // reference's sums over its `seen` rows (compaction.py:97-107, :114, :133-137).
+#ifndef POTR_SH_MIN_BLOCKS
+#define POTR_SH_MIN_BLOCKS 4
+#endif
 constexpr int kShSplatsPerBlock = 16;
 constexpr int kShWarps = 4;
 constexpr int kShRow = 24;  // w*y (16) + w*YCoCg (3), padded for the 2x4 blocks' 16-byte loads
@@ -68,7 +71,7 @@ __device__ __forceinline__ int sh_entry(int i, int j) {
     return 136 + 3 * i + (j - 16);
 }
 
-__global__ void __launch_bounds__(32 * kShWarps, 4) k_sh_accumulate(potr_splats sp, int ncam,
+__global__ void __launch_bounds__(32 * kShWarps, POTR_SH_MIN_BLOCKS) k_sh_accumulate(potr_splats sp, int ncam,
                                                        const double *__restrict__ eyes,
                                                        const double *__restrict__ cam_imp,
                                                        double *__restrict__ neq) {
