@@ -387,6 +387,44 @@ def test_empty_and_degenerate(R, C):
     np.testing.assert_allclose(st.importance, imp, rtol=1e-12, atol=1e-20)
 
 
+def test_c_abi_argument_errors(R):
+    """Bad arguments come back as POTR_E_ARG (ValueError in Python), never a
+    crash: NULL outputs, NULL per-view pointers, bad image sizes, unknown
+    options."""
+    import ctypes
+    import torch
+    from paper_2601_14821_b200 import _native, device as D
+    splats, cams = small_scene()
+    ctx = D.context()
+    dev = D.current_device()
+    ds = D.DeviceSplats.from_host(splats, dev)
+    n, S = ds.n, len(cams)
+    buf = torch.zeros((S, n), dtype=torch.float64, device=dev)
+    one = torch.zeros(n, dtype=torch.float64, device=dev)
+    cam_arr = _native.camera_array(cams)
+    nulls = (ctypes.c_void_p * S)()
+    with pytest.raises(ValueError):  # targets without row outputs
+        ctx.call("potr_score_views_rows", ctypes.byref(ds.struct()), S, cam_arr,
+                 (ctypes.c_void_p * S)(*[buf.data_ptr()] * S), D.ptr(buf), None, None)
+    with pytest.raises(ValueError):  # no camera_importance output
+        ctx.call("potr_score_views_rows", ctypes.byref(ds.struct()), S, cam_arr, None, None,
+                 None, None)
+    with pytest.raises(ValueError):  # NULL image pointers
+        ctx.call("potr_score_views_self", ctypes.byref(ds.struct()), S, cam_arr, nulls,
+                 D.ptr(one), None, D.ptr(one), D.ptr(one))
+    with pytest.raises(ValueError):
+        ctx.call("potr_image_compare", 0, 5, D.ptr(one), D.ptr(one), None, None)
+    with pytest.raises(ValueError):
+        ctx.call("potr_set_option", 99, 1)
+    with pytest.raises(ValueError):
+        ctx.call("potr_set_option", _native.OPT_RAW_DEPTH_KEYS, 3)
+    with pytest.raises(ValueError):
+        ctx.call("potr_set_option", _native.OPT_VIEW_BATCH, 0)
+    # the context is still usable afterwards
+    st = R.compute_delta_mse(splats, cams, R.render_targets(splats, cams))
+    assert np.all(np.isfinite(st.delta_mse))
+
+
 def test_host_c_abi(R, oracle):
     """potr_forward_stats_host: the reference-facing C entry with host buffers."""
     import ctypes
