@@ -173,6 +173,9 @@ int check_cam(potr_ctx *ctx, const potr_camera *c) {
     if (!c) return fail(ctx, POTR_E_ARG, "camera is NULL");
     if (c->width <= 0 || c->height <= 0 || (int64_t)c->width * c->height > 0x7fffffffLL)
         return fail(ctx, POTR_E_ARG, "camera size out of range");
+    // tile rows / columns are 16-bit in the per-entry TileSpan
+    if (c->width > 65535 * kTileW || c->height > 65535 * kTileH)
+        return fail(ctx, POTR_E_ARG, "camera size out of range (tile grid over 65535)");
     return 0;
 }
 
