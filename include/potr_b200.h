@@ -183,6 +183,31 @@ int potr_sh_solve(potr_ctx *ctx, const potr_splats *splats, const double *normal
 int potr_image_compare(potr_ctx *ctx, int width, int height, const double *a, const double *b,
                        double *mse, double *ssim);
 
+/* ---- codec back end (quantize.py, bitstream.py) ---------- */
+
+/* build_octree + serialize_octree (quantize.py:98-170): positions (device,
+ * n x 3), camera eyes (host, neyes x 3), tolerance max(gamma, beta * distance
+ * to the nearest eye), root cube (host center[3], half; _root_cube or the
+ * pinned cube), depth limit <= 24.  Writes the DFS byte stream to `stream`
+ * (device, capacity bytes; n * (max_depth + 6) always suffices), its length
+ * to *stream_len and the DFS order (original indices) to `order` (device,
+ * int64 n).  Synchronizes. */
+int potr_octree(potr_ctx *ctx, int64_t n, const double *positions, int neyes, const double *eyes,
+                double beta, double gamma, const double *center, double half, int max_depth,
+                uint8_t *stream, int64_t capacity, int64_t *stream_len, int64_t *order);
+
+/* encode_attribute_streams (bitstream.py:116-155) of the splats taken in
+ * `order`: ycocg (n, 3, 16), opacities, log(scales) (n, 3), rotations (n, 4),
+ * all device float64 in original order.  The 55 streams (DC x3, AC x45,
+ * opacity, scale x3, rotation x3) are written back to back into `out`
+ * (device; 550 n bytes always suffice); their lengths to stream_lengths
+ * (host int64[55]).  Synchronizes. */
+int potr_attribute_streams(potr_ctx *ctx, int64_t n, const int64_t *order, const double *ycocg,
+                           const double *opacities, const double *log_scales,
+                           const double *rotations, double sf_sh, double sf_opacity,
+                           double sf_rotation, double sf_scale, uint8_t *out, int64_t capacity,
+                           int64_t *stream_lengths);
+
 /* ---- tuning ------------------------------------------------------------- */
 
 /* Views processed per pipeline round (1..8, default 8; env POTR_B200_VIEW_BATCH). */

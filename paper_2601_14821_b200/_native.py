@@ -111,6 +111,16 @@ _SIGNATURES = {
     "potr_profile_read": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]),
     "potr_counters_enable": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int]),
     "potr_counters_read": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p]),
+    "potr_octree": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p, ctypes.c_int,
+                                   ctypes.c_void_p, ctypes.c_double, ctypes.c_double,
+                                   ctypes.c_void_p, ctypes.c_double, ctypes.c_int,
+                                   ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p,
+                                   ctypes.c_void_p]),
+    "potr_attribute_streams": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p,
+                                              ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+                                              ctypes.c_void_p, ctypes.c_double, ctypes.c_double,
+                                              ctypes.c_double, ctypes.c_double, ctypes.c_void_p,
+                                              ctypes.c_int64, ctypes.c_void_p]),
     "potr_image_compare": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.c_int,
                                           ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
                                           ctypes.c_void_p]),

@@ -1,0 +1,156 @@
+"""Codec back end with its data-parallel parts on the device (SURVEY.md 8f
+row 4; reference: potr/quantize.py, potr/bitstream.py, potr/varint.py).
+
+encode_container keeps the reference's signature and output bytes: the
+camera-adaptive octree is built and serialised by potr_octree
+(csrc/codec.cu), the 55 quantised attribute streams by
+potr_attribute_streams, and only the header packing and the zstd frame
+(libzstd, for byte identity) run on the host.  The reference builds the
+octree by Python recursion (96 s for 300k splats on one core); here it is a
+few sorts and scans.
+
+Host-side pieces kept in numpy because their rounding is numpy's: the root
+cube (_root_cube, quantize.py:79-89), log(scales) and the RGB -> YCoCg
+coefficient transform (compaction.py:80-82).
+"""
+
+import ctypes
+import struct
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _native
+from . import device as D
+from . import _zstd
+
+DEFAULT_MAX_DEPTH = 24
+MAGIC = b"POTR"
+VERSION = 1
+NUM_STREAMS = 56
+_HEADER_FMT = "<4sBI11fBB" + f"{NUM_STREAMS}I"
+HEADER_SIZE = struct.calcsize(_HEADER_FMT)
+
+
+@dataclass
+class QuantParams:
+    """quantize.py:26-36."""
+    sf_sh: float
+    sf_opacity: float
+    sf_rotation: float
+    sf_scale: float
+
+    def __post_init__(self):
+        for name in ("sf_sh", "sf_opacity", "sf_rotation", "sf_scale"):
+            if getattr(self, name) <= 0:
+                raise ValueError(f"{name} must be > 0")
+
+
+def root_cube(positions):
+    """_root_cube (quantize.py:79-89): the AABB centre rounded to float32 and
+    the max |p - centre| rounded outward to float32."""
+    positions = np.asarray(positions, dtype=np.float64)
+    lo = positions.min(axis=0)
+    hi = positions.max(axis=0)
+    center = np.float64(np.asarray((lo + hi) * 0.5, dtype=np.float32))
+    half_needed = float(np.abs(positions - center).max()) if len(positions) else 0.0
+    half = np.float32(half_needed)
+    if np.float64(half) < half_needed:
+        half = np.nextafter(half, np.float32(np.inf), dtype=np.float32)
+    return center, float(np.float64(half))
+
+
+def octree_stream(positions, camera_eyes, beta, gamma, max_depth=DEFAULT_MAX_DEPTH,
+                  root_cube_=None):
+    """serialize_octree(build_octree(...)) (quantize.py:98-170) on the device.
+    Returns (stream bytes, DFS order (int64, original indices), centre (3,),
+    half)."""
+    positions = np.asarray(positions, dtype=np.float64)
+    if positions.ndim != 2 or positions.shape[0] < 1:
+        raise ValueError("need at least one position")
+    if gamma <= 0 or beta < 0:
+        raise ValueError("gamma must be > 0 and beta >= 0")
+    if root_cube_ is None:
+        center, half = root_cube(positions)
+    else:
+        center = np.float64(np.asarray(root_cube_[0], dtype=np.float32))
+        half = float(np.float64(np.float32(root_cube_[1])))
+    n = positions.shape[0]
+    dev = D.current_device()
+    pos = D.to_device(positions, dev, (n, 3))
+    eyes = np.ascontiguousarray(np.asarray(camera_eyes, dtype=np.float64).reshape(-1, 3))
+    cap = n * (max_depth + 6)
+    out = torch.empty(max(cap, 1), dtype=torch.uint8, device=dev)
+    order = torch.empty(n, dtype=torch.int64, device=dev)
+    ln = ctypes.c_int64(0)
+    c = (ctypes.c_double * 3)(*[float(x) for x in center])
+    D.context().call("potr_octree", ctypes.c_int64(n), D.ptr(pos), int(eyes.shape[0]),
+                     eyes.ctypes.data_as(ctypes.c_void_p) if len(eyes) else None,
+                     ctypes.c_double(beta), ctypes.c_double(gamma), c, ctypes.c_double(half),
+                     int(max_depth), D.ptr(out), ctypes.c_int64(cap), ctypes.byref(ln),
+                     D.ptr(order))
+    return (D.to_host(out[:ln.value]).tobytes(), D.to_host(order), np.asarray(center), half)
+
+
+def _attribute_streams_device(splats, params, order_dev, sh_ycocg):
+    from .compaction import coeffs_rgb_to_ycocg
+    n = len(splats.positions)
+    dev = D.current_device()
+    yc = coeffs_rgb_to_ycocg(splats.sh) if sh_ycocg is None else sh_ycocg
+    yc_d = D.to_device(yc, dev, (n, 3, 16))
+    op_d = D.to_device(splats.opacities, dev, (n,))
+    ls_d = D.to_device(np.log(np.asarray(splats.scales, dtype=np.float64)), dev, (n, 3))
+    rot_d = D.to_device(splats.rotations, dev, (n, 4))
+    cap = 550 * n
+    out = torch.empty(max(cap, 1), dtype=torch.uint8, device=dev)
+    lens = (ctypes.c_int64 * 55)()
+    D.context().call("potr_attribute_streams", ctypes.c_int64(n), D.ptr(order_dev), D.ptr(yc_d),
+                     D.ptr(op_d), D.ptr(ls_d), D.ptr(rot_d), ctypes.c_double(params.sf_sh),
+                     ctypes.c_double(params.sf_opacity), ctypes.c_double(params.sf_rotation),
+                     ctypes.c_double(params.sf_scale), D.ptr(out), ctypes.c_int64(cap), lens)
+    total = int(sum(lens))
+    blob = D.to_host(out[:total]).tobytes()
+    streams, pos = [], 0
+    for L in lens:
+        streams.append(blob[pos:pos + L])
+        pos += L
+    return streams
+
+
+def encode_attribute_streams(splats, params: QuantParams, sh_ycocg=None):
+    """bitstream.py:116-155 for splats already in octree DFS order: the 55
+    non-octree streams."""
+    n = len(splats.positions)
+    if n == 0:
+        return [b""] * (NUM_STREAMS - 1)
+    order = torch.arange(n, dtype=torch.int64, device=D.current_device())
+    return _attribute_streams_device(splats, params, order, sh_ycocg)
+
+
+def pack_header(splat_count, q, params, beta, gamma, root_center, root_half, max_depth,
+                zstd_level, stream_lengths):
+    """ContainerHeader.pack (bitstream.py:77-85)."""
+    return struct.pack(_HEADER_FMT, MAGIC, VERSION, splat_count, q, params.sf_sh,
+                       params.sf_opacity, params.sf_rotation, params.sf_scale, beta, gamma,
+                       float(root_center[0]), float(root_center[1]), float(root_center[2]),
+                       root_half, max_depth, zstd_level, *stream_lengths)
+
+
+def encode_container(splats, params: QuantParams, q, beta, gamma, zstd_level=19,
+                     max_depth=DEFAULT_MAX_DEPTH, root_cube=None, sh_ycocg=None, camera_eyes=()):
+    """bitstream.py:232-259: octree the positions, quantise and serialise every
+    attribute in DFS order, compress.  Returns (container bytes, DFS order)."""
+    n = len(splats.positions)
+    if n == 0:
+        streams = [b""] * NUM_STREAMS
+        header = pack_header(0, q, params, beta, gamma, np.zeros(3), 0.0, max_depth,
+                             zstd_level, [0] * NUM_STREAMS)
+        return header + _zstd.compress(b"", zstd_level), np.empty(0, dtype=np.int64)
+    octree, order, center, half = octree_stream(splats.positions, camera_eyes, beta, gamma,
+                                                max_depth=max_depth, root_cube_=root_cube)
+    order_dev = torch.from_numpy(np.ascontiguousarray(order)).to(D.current_device())
+    streams = [octree] + _attribute_streams_device(splats, params, order_dev, sh_ycocg)
+    header = pack_header(n, q, params, beta, gamma, center, half, max_depth, zstd_level,
+                         [len(s) for s in streams])
+    return header + _zstd.compress(b"".join(streams), zstd_level), order

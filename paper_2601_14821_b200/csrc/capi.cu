@@ -52,6 +52,9 @@ struct potr_ctx {
     int64_t pairs_total = 0;
     DevBuf tile_counter, ci_v, dm_v, bbox, overflow, vidx, khi, skhi, prep, spans;
     DevBuf met_mom, met_part, met_w, met_out;  // image metrics scratch
+    void *codec_scratch = nullptr;             // codec back end scratch
+    size_t codec_cap = 0;
+    DevBuf codec_eyes;
     bool depth_split = false;  // last bin_batch sorted split keys: skey not materialised
     double scene_lo[3] = {0, 0, 0}, scene_hi[3] = {0, 0, 0};  // splat position bbox
     uint64_t invalid_key0 = ~0ull;  // depth key of an invalid splat in view 0 of the last batch
@@ -618,8 +621,9 @@ void potr_destroy(potr_ctx *ctx) {
     if (ctx->dm_v.p) cudaFree(ctx->dm_v.p);
     if (ctx->khi.p) cudaFree(ctx->khi.p);
     if (ctx->spans.p) cudaFree(ctx->spans.p);
-    for (DevBuf *b : {&ctx->met_mom, &ctx->met_part, &ctx->met_w, &ctx->met_out})
+    for (DevBuf *b : {&ctx->met_mom, &ctx->met_part, &ctx->met_w, &ctx->met_out, &ctx->codec_eyes})
         if (b->p) cudaFree(b->p);
+    if (ctx->codec_scratch) cudaFree(ctx->codec_scratch);
     if (ctx->prep.p) cudaFree(ctx->prep.p);
     if (ctx->skhi.p) cudaFree(ctx->skhi.p);
     for (auto &ev : ctx->events) {
@@ -977,6 +981,46 @@ int potr_image_compare(potr_ctx *ctx, int width, int height, const double *a, co
         const double s0 = out[1] / cnt, s1 = out[2] / cnt, s2 = out[3] / cnt;
         *ssim = ((s0 + s1) + s2) / 3.0;
     }
+    return POTR_OK;
+}
+
+int potr_octree(potr_ctx *ctx, int64_t n, const double *positions, int neyes, const double *eyes,
+                double beta, double gamma, const double *center, double half, int max_depth,
+                uint8_t *stream, int64_t capacity, int64_t *stream_len, int64_t *order) {
+    if (!ctx || !stream_len || !order || !center) return fail(ctx, POTR_E_ARG, "octree: NULL argument");
+    if (n < 1 || n > 0x7ffffff0LL || !positions) return fail(ctx, POTR_E_ARG, "need at least one position");
+    if (!(gamma > 0.0) || beta < 0.0) return fail(ctx, POTR_E_ARG, "gamma must be > 0 and beta >= 0");
+    if (max_depth < 0 || max_depth > 24) return fail(ctx, POTR_E_ARG, "max_depth must be in [0, 24]");
+    if (neyes < 0 || (neyes > 0 && !eyes)) return fail(ctx, POTR_E_ARG, "bad camera eyes");
+    CK(cudaSetDevice(ctx->device));
+    ENSURE(ctx->codec_eyes, sizeof(double) * 3 * (neyes > 0 ? neyes : 1));
+    if (neyes > 0)
+        CK(cudaMemcpyAsync(ctx->codec_eyes.p, eyes, sizeof(double) * 3 * neyes,
+                           cudaMemcpyHostToDevice, ctx->stream));
+    LAUNCH(9 + 3 * max_depth,
+           run_octree(n, positions, neyes, P<double>(ctx->codec_eyes), beta, gamma, center, half,
+                      max_depth, stream, capacity, stream_len, order, &ctx->codec_scratch,
+                      &ctx->codec_cap, ctx->pinned, ctx->stream));
+    if (stream && capacity < *stream_len) return fail(ctx, POTR_E_CAPACITY, "octree stream capacity");
+    return POTR_OK;
+}
+
+int potr_attribute_streams(potr_ctx *ctx, int64_t n, const int64_t *order, const double *ycocg,
+                           const double *opacities, const double *log_scales,
+                           const double *rotations, double sf_sh, double sf_opacity,
+                           double sf_rotation, double sf_scale, uint8_t *out, int64_t capacity,
+                           int64_t *stream_lengths) {
+    if (!ctx || !stream_lengths) return fail(ctx, POTR_E_ARG, "attribute_streams: NULL argument");
+    if (n < 1 || (int64_t)55 * n > 0x7ffffff0LL || !order || !ycocg || !opacities || !log_scales ||
+        !rotations)
+        return fail(ctx, POTR_E_ARG, "attribute_streams: bad arrays");
+    CK(cudaSetDevice(ctx->device));
+    LAUNCH(4, run_attr_streams(n, order, ycocg, opacities, log_scales, rotations, sf_sh,
+                               sf_opacity, sf_rotation, sf_scale, out, capacity, stream_lengths,
+                               &ctx->codec_scratch, &ctx->codec_cap, ctx->pinned, ctx->stream));
+    int64_t total = 0;
+    for (int s = 0; s < 55; s++) total += stream_lengths[s];
+    if (out && capacity < total) return fail(ctx, POTR_E_CAPACITY, "attribute stream capacity");
     return POTR_OK;
 }
 

@@ -1,0 +1,469 @@
+// codec.cu -- the data-parallel parts of the codec back end (SURVEY.md 8f
+// row 4): the camera-adaptive position octree (quantize.py:92-170) built and
+// serialised on the GPU, and the quantised, zigzag/LEB128-coded attribute
+// streams (bitstream.py:116-155, varint.py).  zstd stays libzstd on the host
+// (byte identity).  Every output byte equals the reference's
+// (tests/test_gpu_parity.py::test_codec_*).
+//
+// Octree.  The reference recurses: a node with one splat whose half-diagonal
+// sqrt(3) h is below the splat's tolerance, or any node at the depth limit,
+// is a leaf; otherwise the splats are split by octant (4 (x >= cx) + 2 (y >=
+// cy) + (z >= cz)) and the children visited in ascending octant order.  Here
+// every splat descends alone to the depth limit with the same arithmetic
+// (centre +- h/2, h/2 per level), giving its 3-bit octant path; a stable sort
+// of the paths is the DFS order (equal paths keep ascending index, as
+// `idx[octant == o]` does).  With lcp(t) the common path length of sorted
+// neighbours, a splat is alone from depth D = 1 + max(lcp(t), lcp(t+1)) and
+// its leaf depth is min(max_depth, max(D, first depth whose half-diagonal
+// meets its tolerance)); identical paths share one leaf at the limit.  In DFS
+// order, the leading splat of each leaf emits the internal nodes deeper than
+// lcp(t) on its path (their occupancy bytes) and then its leaf (0x00 +
+// LEB128 count).  A node's occupancy collects its own first splat's child
+// octant and, by atomicOr, the octant of every later leaf that branches off
+// exactly at its depth.
+#include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_scan.cuh>
+#include <cub/device/device_select.cuh>
+
+#include "common.cuh"
+#include "raster.cuh"
+
+namespace potr {
+
+constexpr double kSqrt3 = 1.7320508075688772;  // np.sqrt(3.0)
+
+static inline unsigned blocks_for(int64_t n, int b) { return (unsigned)((n + b - 1) / b); }
+
+// quantize.py:92-96 + :120-123: tol = max(gamma, beta * min over eyes of |p - eye|)
+__global__ void k_oct_tol(int64_t n, const double *__restrict__ pos, int neyes,
+                          const double *__restrict__ eyes, double beta, double gamma,
+                          double *__restrict__ tol) {
+    const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= n) return;
+    double t = gamma;
+    if (beta > 0.0 && neyes > 0) {
+        double dmin = 0.0;
+        for (int e = 0; e < neyes; e++) {
+            const double d0 = pos[3 * k] - eyes[3 * e], d1 = pos[3 * k + 1] - eyes[3 * e + 1];
+            const double d2 = pos[3 * k + 2] - eyes[3 * e + 2];
+            const double d = sqrt(d0 * d0 + d1 * d1 + d2 * d2);
+            dmin = (e == 0 || d < dmin) ? d : dmin;
+        }
+        const double bt = beta * dmin;
+        t = bt > gamma ? bt : gamma;  // np.maximum(gamma, .)
+    }
+    tol[k] = t;
+}
+
+// The octant path to the depth limit (hi: levels 0-11, lo: 12-23, 3 bits
+// each, level 0 most significant) and the first depth whose half-diagonal
+// meets the tolerance.
+__global__ void k_oct_path(int64_t n, const double *__restrict__ pos,
+                           const double *__restrict__ tol, double cx, double cy, double cz,
+                           double half, int max_depth, uint64_t *__restrict__ khi,
+                           uint64_t *__restrict__ klo, int8_t *__restrict__ dtol,
+                           int32_t *__restrict__ idx) {
+    const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= n) return;
+    const double p0 = pos[3 * k], p1 = pos[3 * k + 1], p2 = pos[3 * k + 2], t = tol[k];
+    double c0 = cx, c1 = cy, c2 = cz, h = half;
+    uint64_t hi = 0, lo = 0;
+    int dt = max_depth;
+    for (int d = 0; d < max_depth; d++) {
+        if (dt == max_depth && kSqrt3 * h < t) dt = d;
+        const int o = 4 * (p0 >= c0) + 2 * (p1 >= c1) + (p2 >= c2);
+        if (d < 12) hi |= (uint64_t)o << (3 * (11 - d));
+        else lo |= (uint64_t)o << (3 * (23 - d));
+        const double off = h * 0.5;  // _child_center (quantize.py:66-73)
+        c0 = c0 + ((o & 4) ? off : -off);
+        c1 = c1 + ((o & 2) ? off : -off);
+        c2 = c2 + ((o & 1) ? off : -off);
+        h = h * 0.5;
+    }
+    khi[k] = hi;
+    klo[k] = lo;
+    dtol[k] = (int8_t)dt;
+    idx[k] = (int32_t)k;
+}
+
+__global__ void k_gather_u64(int64_t n, const int32_t *__restrict__ idx,
+                             const uint64_t *__restrict__ src, uint64_t *__restrict__ dst) {
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t < n) dst[t] = src[idx[t]];
+}
+
+__device__ __forceinline__ int digit_at(uint64_t hi, uint64_t lo, int d) {
+    return d < 12 ? (int)((hi >> (3 * (11 - d))) & 7) : (int)((lo >> (3 * (23 - d))) & 7);
+}
+
+__device__ __forceinline__ int path_lcp(uint64_t ha, uint64_t la, uint64_t hb, uint64_t lb,
+                                        int max_depth) {
+    int l;
+    if (ha != hb) l = (__clzll((long long)(ha ^ hb)) - 28) / 3;
+    else if (la != lb) l = 12 + (__clzll((long long)(la ^ lb)) - 28) / 3;
+    else l = 24;
+    return l < max_depth ? l : max_depth;
+}
+
+// Per sorted position: lcp with the previous splat (-1 at 0), group-start flag.
+__global__ void k_oct_lcp(int64_t n, const int32_t *__restrict__ order,
+                          const uint64_t *__restrict__ khi, const uint64_t *__restrict__ klo,
+                          int max_depth, int32_t *__restrict__ lcp, uint8_t *__restrict__ start) {
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= n) return;
+    int l = -1;
+    if (t > 0) {
+        const int a = order[t - 1], b = order[t];
+        l = path_lcp(khi[a], klo[a], khi[b], klo[b], max_depth);
+    }
+    lcp[t] = l;
+    start[t] = (uint8_t)(l < max_depth);
+}
+
+__device__ __forceinline__ int uleb_len(uint64_t v) {
+    int c = 1;
+    while (v > 0x7F) {
+        v >>= 7;
+        c++;
+    }
+    return c;
+}
+
+// Per leaf (group of equal paths, led by sorted position t = gstart[j]):
+// depth range [a, L) of the internal nodes it emits, leaf depth L, count,
+// byte count; and the child octant of its own new internal nodes.
+__global__ void k_oct_leaf(int64_t ng, int64_t n, const int32_t *__restrict__ gstart,
+                           const int32_t *__restrict__ lcp, const int32_t *__restrict__ order,
+                           const uint64_t *__restrict__ khi, const uint64_t *__restrict__ klo,
+                           const int8_t *__restrict__ dtol, int max_depth,
+                           int32_t *__restrict__ glcp, int8_t *__restrict__ gleaf,
+                           int32_t *__restrict__ gcount, int64_t *__restrict__ gbytes,
+                           uint32_t *__restrict__ occ) {
+    const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= ng) return;
+    const int64_t t = gstart[j];
+    const int64_t e = j + 1 < ng ? gstart[j + 1] : n;
+    const int count = (int)(e - t);
+    const int l0 = lcp[t];
+    int L = max_depth;
+    if (count == 1) {
+        const int l1 = t + 1 < n ? lcp[t + 1] : -1;
+        const int D = 1 + (l0 > l1 ? l0 : l1);
+        const int dt = dtol[order[t]];
+        const int m = D > dt ? D : dt;
+        L = m < max_depth ? m : max_depth;
+    }
+    const int a = l0 + 1;
+    glcp[j] = l0;
+    gleaf[j] = (int8_t)L;
+    gcount[j] = count;
+    gbytes[j] = (int64_t)(L - a) + 1 + uleb_len((uint64_t)count);
+    const int s = order[t];
+    const uint64_t hi = khi[s], lo = klo[s];
+    for (int d = a; d < L; d++) occ[j * max_depth + d] = 1u << digit_at(hi, lo, d);
+}
+
+// Level d of the "node start" scan: the latest group at or before j whose
+// lcp is below d starts the depth-d node containing j.
+__global__ void k_oct_mark(int64_t ng, const int32_t *__restrict__ glcp, int d,
+                           int32_t *__restrict__ mark) {
+    const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (j < ng) mark[j] = glcp[j] < d ? (int32_t)j : -1;
+}
+
+// Groups branching at depth d add their child octant to that node.
+__global__ void k_oct_branch(int64_t ng, const int32_t *__restrict__ glcp,
+                             const int32_t *__restrict__ seg, int d,
+                             const int32_t *__restrict__ gstart, const int32_t *__restrict__ order,
+                             const uint64_t *__restrict__ khi, const uint64_t *__restrict__ klo,
+                             int max_depth, uint32_t *__restrict__ occ) {
+    const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= ng || j == 0 || glcp[j] != d) return;
+    const int S = seg[j - 1];
+    const int s = order[gstart[j]];
+    atomicOr(&occ[(int64_t)S * max_depth + d], 1u << digit_at(khi[s], klo[s], d));
+}
+
+__global__ void k_oct_emit(int64_t ng, const int32_t *__restrict__ glcp,
+                           const int8_t *__restrict__ gleaf, const int32_t *__restrict__ gcount,
+                           const int64_t *__restrict__ goff, const uint32_t *__restrict__ occ,
+                           int max_depth, uint8_t *__restrict__ out) {
+    const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= ng) return;
+    int64_t o = goff[j];
+    const int a = glcp[j] + 1, L = gleaf[j];
+    for (int d = a; d < L; d++) out[o++] = (uint8_t)occ[j * max_depth + d];
+    out[o++] = 0x00;
+    uint64_t v = (uint64_t)gcount[j];
+    while (v > 0x7F) {
+        out[o++] = (uint8_t)((v & 0x7F) | 0x80);
+        v >>= 7;
+    }
+    out[o] = (uint8_t)v;
+}
+
+__global__ void k_iota32(int64_t n, int32_t *__restrict__ out) {
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t < n) out[t] = (int32_t)t;
+}
+
+__global__ void k_order_i64(int64_t n, const int32_t *__restrict__ src, int64_t *__restrict__ dst) {
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t < n) dst[t] = src[t];
+}
+
+// ---------------------------------------------------------------------------
+// attribute streams (bitstream.py:116-155): 55 streams x n values, stream s
+// of value i at s * n + i, each coded as a LEB128 varint (zigzag first for
+// the signed ones), concatenated in stream order.
+
+__device__ __forceinline__ int64_t quant(double x, double sf) {
+    return (int64_t)floor(0.5 + x * sf);  // quantize_uniform: floor(0.5 + x * sf)
+}
+__device__ __forceinline__ uint64_t zigzag(int64_t x) {
+    return ((uint64_t)x << 1) ^ (uint64_t)(x >> 63);
+}
+
+constexpr int kStreams = 55;  // streams 1..55 of the container (0 is the octree)
+
+__global__ void k_attr_values(int64_t n, const int64_t *__restrict__ order,
+                              const double *__restrict__ ycocg, const double *__restrict__ opac,
+                              const double *__restrict__ log_scales,
+                              const double *__restrict__ rot, double sf_sh, double sf_op,
+                              double sf_rot, double sf_sc, uint64_t *__restrict__ val,
+                              uint8_t *__restrict__ len) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const int64_t k = order[i];
+    const int64_t kp = i > 0 ? order[i - 1] : -1;
+    auto put = [&](int s, uint64_t v) {  // s: 0-based index among the 55
+        val[(int64_t)s * n + i] = v;
+        len[(int64_t)s * n + i] = (uint8_t)uleb_len(v);
+    };
+    // DC per channel: differences along the DFS order, first value raw
+    for (int ch = 0; ch < 3; ch++) {
+        const int64_t v = quant(ycocg[48 * k + 16 * ch], sf_sh);
+        const int64_t p = kp >= 0 ? quant(ycocg[48 * kp + 16 * ch], sf_sh) : 0;
+        put(ch, zigzag(v - p));
+    }
+    // AC: stream 3 + coef * 3 + ch holds coefficient coef + 1 of channel ch
+    for (int coef = 0; coef < 15; coef++)
+        for (int ch = 0; ch < 3; ch++)
+            put(3 + coef * 3 + ch, zigzag(quant(ycocg[48 * k + 16 * ch + coef + 1], sf_sh)));
+    put(48, (uint64_t)quant(opac[k], sf_op));  // astype(uint64), no zigzag
+    for (int ax = 0; ax < 3; ax++) put(49 + ax, zigzag(quant(log_scales[3 * k + ax], sf_sc)));
+    const double sgn = rot[4 * k] < 0.0 ? -1.0 : 1.0;  // _ensure_w_nonneg
+    for (int ax = 0; ax < 3; ax++) put(52 + ax, zigzag(quant(rot[4 * k + 1 + ax] * sgn, sf_rot)));
+}
+
+__global__ void k_attr_len64(int64_t m, const uint8_t *__restrict__ len, int64_t *__restrict__ l64) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < m) l64[i] = len[i];
+}
+
+__global__ void k_attr_emit(int64_t m, const uint64_t *__restrict__ val,
+                            const int64_t *__restrict__ off, uint8_t *__restrict__ out) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= m) return;
+    int64_t o = off[i];
+    uint64_t v = val[i];
+    while (v > 0x7F) {
+        out[o++] = (uint8_t)((v & 0x7F) | 0x80);
+        v >>= 7;
+    }
+    out[o] = (uint8_t)v;
+}
+
+// ---------------------------------------------------------------------------
+
+struct CodecScratch {
+    void *p = nullptr;
+    size_t cap = 0;
+};
+
+static cudaError_t grow(CodecScratch &b, size_t bytes) {
+    if (b.cap >= bytes) return cudaSuccess;
+    if (b.p) cudaFree(b.p);
+    b.p = nullptr;
+    b.cap = 0;
+    cudaError_t e = cudaMalloc(&b.p, bytes);
+    if (e == cudaSuccess) b.cap = bytes;
+    return e;
+}
+
+#define CODEC_CK(x)                          \
+    do {                                     \
+        cudaError_t _e = (x);                \
+        if (_e != cudaSuccess) return _e;    \
+    } while (0)
+
+// Carves typed arrays out of one allocation.
+struct Carver {
+    char *base;
+    size_t off = 0;
+    template <typename T>
+    T *take(int64_t count) {
+        off = (off + 255) & ~(size_t)255;
+        T *p = reinterpret_cast<T *>(base + off);
+        off += sizeof(T) * (size_t)(count > 0 ? count : 1);
+        return p;
+    }
+};
+
+static size_t octree_scratch_bytes(int64_t n, int max_depth, size_t temp) {
+    // khi klo (x2 for the sorts) idx x3 dtol tol lcp start gstart glcp gleaf gcount gbytes
+    // goff mark seg occ, temp
+    size_t b = 0;
+    auto add = [&](size_t s) { b += ((s + 255) & ~(size_t)255) + 256; };
+    add(8 * n), add(8 * n), add(8 * n), add(8 * n), add(8 * n);
+    add(4 * n), add(4 * n), add(4 * n);
+    add(n), add(8 * n), add(4 * n), add(n), add(4 * n), add(4 * n), add(n), add(4 * n);
+    add(8 * n), add(8 * (n + 1)), add(4 * n), add(4 * n), add(4 * n * (size_t)max_depth), add(8);
+    add(temp);
+    return b;
+}
+
+cudaError_t run_octree(int64_t n, const double *pos, int neyes, const double *eyes_dev,
+                       double beta, double gamma, const double *center, double half,
+                       int max_depth, uint8_t *out, int64_t capacity, int64_t *out_len,
+                       int64_t *order_out, void **scratch, size_t *scratch_cap,
+                       int64_t *pinned, cudaStream_t st) {
+    // temp storage for CUB (the largest of the three kinds of call)
+    size_t t1 = 0, t2 = 0, t3 = 0;
+    {
+        cub::DoubleBuffer<uint64_t> k(nullptr, nullptr);
+        cub::DoubleBuffer<int32_t> v(nullptr, nullptr);
+        CODEC_CK(cub::DeviceRadixSort::SortPairs((void *)nullptr, t1, k, v, (int)n, 0, 36));
+        CODEC_CK(cub::DeviceSelect::Flagged((void *)nullptr, t2, (int32_t *)nullptr,
+                                            (uint8_t *)nullptr, (int32_t *)nullptr,
+                                            (int32_t *)nullptr, (int)n));
+        CODEC_CK(cub::DeviceScan::ExclusiveSum((void *)nullptr, t3, (int64_t *)nullptr,
+                                               (int64_t *)nullptr, (int)n + 1));
+        size_t t4 = 0;
+        CODEC_CK(cub::DeviceScan::InclusiveScan((void *)nullptr, t4, (int32_t *)nullptr,
+                                                (int32_t *)nullptr, cub::Max(), (int)n));
+        t1 = t1 > t2 ? t1 : t2;
+        t1 = t1 > t3 ? t1 : t3;
+        t1 = t1 > t4 ? t1 : t4;
+    }
+    const size_t need = octree_scratch_bytes(n, max_depth, t1);
+    if (*scratch_cap < need) {
+        if (*scratch) cudaFree(*scratch);
+        *scratch = nullptr;
+        *scratch_cap = 0;
+        CODEC_CK(cudaMalloc(scratch, need));
+        *scratch_cap = need;
+    }
+    Carver cv{reinterpret_cast<char *>(*scratch)};
+    uint64_t *khi = cv.take<uint64_t>(n), *klo = cv.take<uint64_t>(n);
+    uint64_t *ka = cv.take<uint64_t>(n), *kb = cv.take<uint64_t>(n), *kc = cv.take<uint64_t>(n);
+    int32_t *ia = cv.take<int32_t>(n), *ib = cv.take<int32_t>(n), *ic = cv.take<int32_t>(n);
+    int8_t *dtol = cv.take<int8_t>(n);
+    double *tol = cv.take<double>(n);
+    int32_t *lcp = cv.take<int32_t>(n);
+    uint8_t *start = cv.take<uint8_t>(n);
+    int32_t *gstart = cv.take<int32_t>(n), *glcp = cv.take<int32_t>(n);
+    int8_t *gleaf = cv.take<int8_t>(n);
+    int32_t *gcount = cv.take<int32_t>(n);
+    int64_t *gbytes = cv.take<int64_t>(n + 1), *goff = cv.take<int64_t>(n + 1);
+    int32_t *mark = cv.take<int32_t>(n), *seg = cv.take<int32_t>(n);
+    uint32_t *occ = cv.take<uint32_t>(n * (int64_t)max_depth);
+    int32_t *ng_dev = cv.take<int32_t>(2);
+    void *temp = cv.take<char>((int64_t)t1);
+
+    k_oct_tol<<<blocks_for(n, 256), 256, 0, st>>>(n, pos, neyes, eyes_dev, beta, gamma, tol);
+    k_oct_path<<<blocks_for(n, 256), 256, 0, st>>>(n, pos, tol, center[0], center[1], center[2],
+                                                   half, max_depth, khi, klo, dtol, ia);
+    CODEC_CK(cudaGetLastError());
+    // stable sort by (hi, lo): by lo first, then stably by hi
+    {
+        CODEC_CK(cudaMemcpyAsync(ka, klo, 8 * n, cudaMemcpyDeviceToDevice, st));
+        cub::DoubleBuffer<uint64_t> k(ka, kb);
+        cub::DoubleBuffer<int32_t> v(ia, ib);
+        size_t tb = t1;
+        CODEC_CK(cub::DeviceRadixSort::SortPairs(temp, tb, k, v, (int)n, 0, 36, st));
+        int32_t *idx1 = v.Current();
+        k_gather_u64<<<blocks_for(n, 256), 256, 0, st>>>(n, idx1, khi, kc);
+        cub::DoubleBuffer<uint64_t> k2(kc, k.Alternate());
+        cub::DoubleBuffer<int32_t> v2(idx1, v.Alternate());
+        CODEC_CK(cub::DeviceRadixSort::SortPairs(temp, tb, k2, v2, (int)n, 0, 36, st));
+        int32_t *ord = v2.Current();
+        if (ord != ic) CODEC_CK(cudaMemcpyAsync(ic, ord, 4 * n, cudaMemcpyDeviceToDevice, st));
+    }
+    int32_t *order = ic;
+    k_oct_lcp<<<blocks_for(n, 256), 256, 0, st>>>(n, order, khi, klo, max_depth, lcp, start);
+    {
+        size_t tb = t1;
+        k_iota32<<<blocks_for(n, 256), 256, 0, st>>>(n, mark);
+        CODEC_CK(cub::DeviceSelect::Flagged(temp, tb, mark, start, gstart, ng_dev, (int)n, st));
+    }
+    int32_t ngh = 0;
+    CODEC_CK(cudaMemcpyAsync(pinned, ng_dev, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+    CODEC_CK(cudaStreamSynchronize(st));
+    std::memcpy(&ngh, pinned, sizeof(int32_t));
+    const int64_t ng = ngh;
+    k_oct_leaf<<<blocks_for(ng, 256), 256, 0, st>>>(ng, n, gstart, lcp, order, khi, klo, dtol,
+                                                    max_depth, glcp, gleaf, gcount, gbytes, occ);
+    CODEC_CK(cudaGetLastError());
+    for (int d = 0; d < max_depth; d++) {
+        k_oct_mark<<<blocks_for(ng, 256), 256, 0, st>>>(ng, glcp, d, mark);
+        size_t tb = t1;
+        CODEC_CK(cub::DeviceScan::InclusiveScan(temp, tb, mark, seg, cub::Max(), (int)ng, st));
+        k_oct_branch<<<blocks_for(ng, 256), 256, 0, st>>>(ng, glcp, seg, d, gstart, order, khi,
+                                                          klo, max_depth, occ);
+    }
+    {
+        size_t tb = t1;
+        CODEC_CK(cudaMemsetAsync(gbytes + ng, 0, sizeof(int64_t), st));
+        CODEC_CK(cub::DeviceScan::ExclusiveSum(temp, tb, gbytes, goff, (int)ng + 1, st));
+    }
+    CODEC_CK(cudaMemcpyAsync(pinned, goff + ng, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    CODEC_CK(cudaStreamSynchronize(st));
+    *out_len = pinned[0];
+    k_order_i64<<<blocks_for(n, 256), 256, 0, st>>>(n, order, order_out);
+    if (out && capacity >= *out_len)
+        k_oct_emit<<<blocks_for(ng, 256), 256, 0, st>>>(ng, glcp, gleaf, gcount, goff, occ,
+                                                        max_depth, out);
+    return cudaGetLastError();
+}
+
+cudaError_t run_attr_streams(int64_t n, const int64_t *order, const double *ycocg,
+                             const double *opac, const double *log_scales, const double *rot,
+                             double sf_sh, double sf_op, double sf_rot, double sf_sc, uint8_t *out,
+                             int64_t capacity, int64_t *stream_lengths, void **scratch,
+                             size_t *scratch_cap, int64_t *pinned, cudaStream_t st) {
+    const int64_t m = (int64_t)kStreams * n;
+    size_t tb = 0;
+    CODEC_CK(cub::DeviceScan::ExclusiveSum((void *)nullptr, tb, (int64_t *)nullptr,
+                                           (int64_t *)nullptr, (int)(m + 1)));
+    const size_t need = 8 * (size_t)m + (size_t)m + 8 * (size_t)(m + 1) * 2 + tb + 4096;
+    if (*scratch_cap < need) {
+        if (*scratch) cudaFree(*scratch);
+        *scratch = nullptr;
+        *scratch_cap = 0;
+        CODEC_CK(cudaMalloc(scratch, need));
+        *scratch_cap = need;
+    }
+    Carver cv{reinterpret_cast<char *>(*scratch)};
+    uint64_t *val = cv.take<uint64_t>(m);
+    uint8_t *len = cv.take<uint8_t>(m);
+    int64_t *l64 = cv.take<int64_t>(m + 1);
+    int64_t *off = cv.take<int64_t>(m + 1);
+    void *temp = cv.take<char>((int64_t)tb);
+    k_attr_values<<<blocks_for(n, 128), 128, 0, st>>>(n, order, ycocg, opac, log_scales, rot,
+                                                      sf_sh, sf_op, sf_rot, sf_sc, val, len);
+    k_attr_len64<<<blocks_for(m, 256), 256, 0, st>>>(m, len, l64);
+    CODEC_CK(cudaMemsetAsync(l64 + m, 0, sizeof(int64_t), st));
+    CODEC_CK(cub::DeviceScan::ExclusiveSum(temp, tb, l64, off, (int)(m + 1), st));
+    // stream boundaries: off[s * n] for s = 0..55
+    for (int s = 0; s <= kStreams; s++)
+        CODEC_CK(cudaMemcpyAsync(pinned + s, off + (int64_t)s * n, sizeof(int64_t),
+                                 cudaMemcpyDeviceToHost, st));
+    CODEC_CK(cudaStreamSynchronize(st));
+    for (int s = 0; s < kStreams; s++) stream_lengths[s] = pinned[s + 1] - pinned[s];
+    if (out && capacity >= pinned[kStreams])
+        k_attr_emit<<<blocks_for(m, 256), 256, 0, st>>>(m, val, off, out);
+    return cudaGetLastError();
+}
+
+}  // namespace potr

@@ -126,6 +126,19 @@ cudaError_t launch_image_compare(int W, int H, const double *a, const double *b,
                                  cudaStream_t st);
 int image_compare_partials();
 
+// Codec back end (codec.cu).  Scratch is owned by the caller (grown on demand);
+// pinned: >= 64 int64 of pinned host memory.
+cudaError_t run_octree(int64_t n, const double *pos, int neyes, const double *eyes_dev,
+                       double beta, double gamma, const double *center, double half,
+                       int max_depth, uint8_t *out, int64_t capacity, int64_t *out_len,
+                       int64_t *order_out, void **scratch, size_t *scratch_cap,
+                       int64_t *pinned, cudaStream_t st);
+cudaError_t run_attr_streams(int64_t n, const int64_t *order, const double *ycocg,
+                             const double *opac, const double *log_scales, const double *rot,
+                             double sf_sh, double sf_op, double sf_rot, double sf_sc, uint8_t *out,
+                             int64_t capacity, int64_t *stream_lengths, void **scratch,
+                             size_t *scratch_cap, int64_t *pinned, cudaStream_t st);
+
 // SH recompute (sh.cu)
 cudaError_t launch_sh_accumulate(const potr_splats &sp, int ncam, const double *eyes_dev,
                                  const double *cam_imp, double *neq, cudaStream_t st);

@@ -645,3 +645,60 @@ def test_large_scene_views_vs_oracle(R, oracle):
     np.testing.assert_allclose(st.importance, imp, rtol=1e-10, atol=1e-22)
     assert score_close(st.delta_mse, dm, rel=1e-6, floor=1e-24)
     assert st.mse == pytest.approx(mse, rel=1e-11)
+
+
+def _codec_cases():
+    """Inputs of oracle/gen_golden.py's codec fixture, regenerated here."""
+    from paper_2601_14821_b200.fixture import make_fixture
+    from paper_2601_14821_b200.scene import Splats
+    rng = np.random.default_rng(11)
+    cases = []
+    s, c = make_fixture(3000, 6, 5, 32)
+    cases.append((s, c, 24, None, False))
+    s2, c2 = make_fixture(800, 4, 6, 32)
+    pos = s2.positions.copy()
+    pos[100:140] = pos[99]
+    pos[200:203] = pos[500]
+    s2 = Splats(pos, s2.sh, s2.opacities, s2.scales, s2.rotations)
+    cases.append((s2, c2, 24, None, True))
+    cases.append((s2, c2, 5, None, False))
+    cases.append((s, c, 24, (np.array([0.01, -0.02, 0.03]), 1.3), True))
+    cases.append((s.subset(np.arange(1)), c, 24, None, False))
+    s3, c3 = make_fixture(500, 3, 7, 32)
+    rot = s3.rotations.copy()
+    rot[::3] *= -1.0
+    s3 = Splats(s3.positions, s3.sh * 3.0, s3.opacities,
+                s3.scales * rng.uniform(0.5, 2.0, (500, 1)), rot)
+    cases.append((s3, c3, 24, None, False))
+    return cases
+
+
+def test_codec_bytes_match_reference(C):
+    """The device codec back end reproduces the reference's bytes exactly:
+    octree stream and DFS order (multi-splat leaves at the depth limit, a
+    shallow depth limit, a pinned root cube, a single splat), the 55
+    attribute streams (negative rotation real parts, values past the
+    quantiser's usual range) and the whole zstd container."""
+    from paper_2601_14821_b200 import codec
+    from tests.conftest import fingerprint
+    g = golden("codec")
+    params = codec.QuantParams(51.0, 101.0, 201.0, 2001.0)
+    q, beta, gamma = 0.5, 7e-05, 1.5811388300841894e-05
+    for i, (s, c, md, rc, with_yc) in enumerate(_codec_cases()):
+        assert fingerprint(s, c) == str(g[f"fingerprint_{i}"])
+        eyes = [cam.eye for cam in c]
+        yc = C.coeffs_rgb_to_ycocg(s.sh) * 0.5 if with_yc else None
+        octree, order, center, half = codec.octree_stream(s.positions, eyes, beta, gamma,
+                                                          max_depth=md, root_cube_=rc)
+        assert octree == g[f"octree_{i}"].tobytes(), f"case {i}: octree stream"
+        assert np.array_equal(order, g[f"order_{i}"])
+        assert np.array_equal(center, g[f"center_{i}"]) and half == float(g[f"half_{i}"])
+        streams = codec.encode_attribute_streams(s.subset(order), params,
+                                                 sh_ycocg=None if yc is None else yc[order])
+        assert [len(x) for x in streams] == list(g[f"stream_lengths_{i}"]), f"case {i}"
+        assert b"".join(streams) == g[f"streams_{i}"].tobytes(), f"case {i}: streams"
+        data, order2 = codec.encode_container(s, params, q, beta, gamma, zstd_level=3,
+                                              max_depth=md, root_cube=rc, sh_ycocg=yc,
+                                              camera_eyes=eyes)
+        assert np.array_equal(order2, order)
+        assert data == g[f"container_{i}"].tobytes(), f"case {i}: container"
