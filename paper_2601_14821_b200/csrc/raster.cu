@@ -425,9 +425,51 @@ __device__ __forceinline__ int4 bbox_of(const ChunkBuf &B, int e) {
     return *reinterpret_cast<const int4 *>(&B.f[3][e]);
 }
 
+#ifndef POTR_PIXEL_CULL
+#define POTR_PIXEL_CULL 1
+#endif
+
+// Pixel culling of one entry over the tile: the columns [c0, c1] (tile-local,
+// already clipped to the bbox) of each bbox row whose pixel centre can pass
+// the exp prefilter (power >= pthr), as a 32-bit tile mask.  The same
+// ellipse and margins as the tile culling (cull_ellipse / row_span), at a
+// single pixel-centre dy per row, so it is conservative: every sample the
+// rasterizer would composite keeps its bit and renders stay bit-identical.
+__device__ __forceinline__ unsigned ellipse_rows(const ChunkBuf &B, int e, int ox, int oy,
+                                                 int c0, int c1, int r0, int r1) {
+    const double2 m = B.f[0][e], ab = B.f[1][e], cp = B.f[2][e];
+    const double R = -2.0 * (cp.y - kCullMarginPower);
+    const double a = -2.0 * ab.x, c = -2.0 * cp.x, b = ab.y;
+    const double det = a * c - b * b;
+    const bool full = !(a > 0.0 && c > 0.0 && det > 1e-4 * (a * c) && isfinite(R) && isfinite(det));
+    const unsigned cols = (0xFFu >> (7 - c1)) & (0xFFu << c0);
+    if (full) {
+        const unsigned rows = (0xFFFFFFFFu >> (8 * (3 - r1))) & (0xFFFFFFFFu << (8 * r0));
+        return (cols * 0x01010101u) & rows;
+    }
+    if (!(R > 0.0)) return 0u;
+    const double inv_a = 1.0 / a, aR = a * R;
+    unsigned w = 0u;
+    for (int r = r0; r <= r1; r++) {
+        const double dy = (double)(oy + r) + 0.5 - m.y;
+        const double D = aR - det * dy * dy;
+        if (D < 0.0) continue;
+        const double s = (double)sqrtf((float)D);
+        const double xmax = (s - b * dy) * inv_a, xmin = (-s - b * dy) * inv_a;
+        // pixel px is in when px + 0.5 - mx lies in [xmin, xmax] (+- margin)
+        const double e0 = ceil(m.x + xmin - 0.5 - kCullMarginPixel) - (double)ox;
+        const double e1 = floor(m.x + xmax - 0.5 + kCullMarginPixel) - (double)ox;
+        const int k0 = e0 > (double)c0 ? (e0 > (double)c1 ? 8 : (int)e0) : c0;
+        const int k1 = e1 < (double)c1 ? (e1 < (double)c0 ? -1 : (int)e1) : c1;
+        if (k0 <= k1) w |= ((0xFFu >> (7 - k1)) & (0xFFu << k0)) << (8 * r);
+    }
+    return w;
+}
+
 // Entries of this chunk whose clipped bbox (rasterizer.py:135-148) contains
-// the lane's pixel.  Lane e turns entry e's bbox into the 32-bit set of tile
-// pixels it covers (bit c + 8r <-> lane c + 8r, the lane's pixel); a 32x32 bit
+// the lane's pixel (and, with POTR_PIXEL_CULL, whose prefilter ellipse can
+// reach it).  Lane e turns entry e into the 32-bit set of tile pixels it
+// covers (bit c + 8r <-> lane c + 8r, the lane's pixel); a 32x32 bit
 // transpose over the warp then hands every lane its per-entry bits.  Must be
 // called by the whole warp.
 __device__ __forceinline__ unsigned live_mask(const ChunkBuf &B, int cnt, int ox, int oy,
@@ -438,9 +480,13 @@ __device__ __forceinline__ unsigned live_mask(const ChunkBuf &B, int cnt, int ox
         const int c0 = max(bb.x - ox, 0), c1 = min(bb.y - ox, kTileW - 1);
         const int r0 = max(bb.z - oy, 0), r1 = min(bb.w - oy, kTileH - 1);
         if (c0 <= c1 && r0 <= r1) {
-            const unsigned cols = (0xFFu >> (7 - c1)) & (0xFFu << c0);
-            const unsigned rows = (0xFFFFFFFFu >> (8 * (3 - r1))) & (0xFFFFFFFFu << (8 * r0));
-            w = (cols * 0x01010101u) & rows;
+            if (POTR_PIXEL_CULL) {
+                w = ellipse_rows(B, lane, ox, oy, c0, c1, r0, r1);
+            } else {
+                const unsigned cols = (0xFFu >> (7 - c1)) & (0xFFu << c0);
+                const unsigned rows = (0xFFFFFFFFu >> (8 * (3 - r1))) & (0xFFFFFFFFu << (8 * r0));
+                w = (cols * 0x01010101u) & rows;
+            }
         }
     }
     // transpose: swap the off-diagonal j x j blocks, j = 16, 8, 4, 2, 1
