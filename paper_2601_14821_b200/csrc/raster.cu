@@ -570,7 +570,10 @@ __device__ __forceinline__ bool group_sum(int key, double &v0, double &v1) {
 // (the common case: ~5 lanes at the C3 shape) do that directly, one rank per
 // round; large ones reduce first with group_sum.  Either way the result
 // depends only on the keys and values, never on scheduling.
-constexpr int kSerialGroups = 8;
+#ifndef POTR_SERIAL_GROUPS
+#define POTR_SERIAL_GROUPS 8
+#endif
+constexpr int kSerialGroups = POTR_SERIAL_GROUPS;
 
 __device__ __forceinline__ void accumulate(WarpSmem &S, int key, double v0, double v1) {
     const unsigned FULL = 0xffffffffu;
@@ -754,7 +757,6 @@ __global__ void __launch_bounds__(32 * kRasterWarps, POTR_RASTER_MIN_BLOCKS) k_r
         P0 = PK0, P1 = PK1, P2 = PK2;
         dr0 = 2.0 * dr0, dr1 = 2.0 * dr1, dr2 = 2.0 * dr2;
         T = 1.0;
-        done = !inside;
         int written = start;
         if (start < stop) {
             ChunkIds next = fetch_ids(a, start, end, lane);
@@ -778,49 +780,65 @@ __global__ void __launch_bounds__(32 * kRasterWarps, POTR_RASTER_MIN_BLOCKS) k_r
                 const ChunkBuf &B = S.buf[b];
                 const int cnt = min(32, end - base);
                 const int ci = (base - start) >> 5;
-                // beyond the kept masks the samples are re-decided exactly as in pass 1
-                const bool known = ci < kMaskChunks;
-                unsigned m = known ? S.cmask[ci][lane]
-                                   : live_mask(B, cnt, px - (lane & 7), py - (lane >> 3), lane);
-                if (done) m = 0u;
-                while (__any_sync(FULL, m != 0u)) {
-                    int key = 32 + lane;
-                    double dse = 0.0, timp = 0.0;
-                    if (m) {
-                        const int e = __ffs(m) - 1;
-                        m &= m - 1u;
-                        double alpha = 0.0;
-                        bool ok = true;
-                        if (known) alpha = known_alpha(B, e, pxc, pyc, tab_s);
-                        else ok = eval_alpha(B, e, pxc, pyc, tab_s, alpha);
-                        if (ok) {
+                // One composited sample of entry e: the removal delta, dSE and
+                // T*alpha; P carries the colour still to come.
+                auto removal = [&](int e, double alpha, double &dse, double &timp) {
+                    const double c0 = B.f[4][e].y;
+                    const double2 c12 = B.f[5][e];
+                    if (MODE == kScore) {
+                        // prune_deltas, forward form: a/(1-a) * (P_K - P_i - T c),
+                        // dSE = |pd|^2 + 2 pd . dr (rasterizer.py:232-243, :333)
+                        const double f = alpha * rcp_nr(1.0 - alpha);
+                        const double pd0 = f * (P0 - T * c0);
+                        const double pd1 = f * (P1 - T * c12.x);
+                        const double pd2 = f * (P2 - T * c12.y);
+                        dse = pd0 * (pd0 + dr0);
+                        dse = dse + pd1 * (pd1 + dr1);
+                        dse = dse + pd2 * (pd2 + dr2);
+                    }
+                    const double w = T * alpha;
+                    timp = w;
+                    P0 -= w * c0;
+                    P1 -= w * c12.x;
+                    P2 -= w * c12.y;
+                    T = T * (1.0 - alpha);
+                };
+                if (ci < kMaskChunks) {
+                    // pass 1's masks: exactly the composited samples, none after
+                    // termination (T evolves bit for bit as in pass 1), so
+                    // neither the alpha tests nor the T test are repeated
+                    unsigned m = S.cmask[ci][lane];
+                    while (__any_sync(FULL, m != 0u)) {
+                        int key = 32 + lane;
+                        double dse = 0.0, timp = 0.0;
+                        if (m) {
+                            const int e = __ffs(m) - 1;
+                            m &= m - 1u;
                             key = e;
-                            const double c0 = B.f[4][e].y;
-                            const double2 c12 = B.f[5][e];
-                            if (MODE == kScore) {
-                                // prune_deltas, forward form: a/(1-a) * (P_K - P_i - T c),
-                                // dSE = |pd|^2 + 2 pd . dr (rasterizer.py:232-243, :333)
-                                const double f = alpha * rcp_nr(1.0 - alpha);
-                                const double pd0 = f * (P0 - T * c0);
-                                const double pd1 = f * (P1 - T * c12.x);
-                                const double pd2 = f * (P2 - T * c12.y);
-                                dse = pd0 * (pd0 + dr0);
-                                dse = dse + pd1 * (pd1 + dr1);
-                                dse = dse + pd2 * (pd2 + dr2);
-                            }
-                            const double w = T * alpha;
-                            timp = w;
-                            P0 -= w * c0;
-                            P1 -= w * c12.x;
-                            P2 -= w * c12.y;
-                            T = T * (1.0 - alpha);
-                            if (T < kCompositeK[2]) {
-                                done = true;
-                                m = 0u;
+                            removal(e, known_alpha(B, e, pxc, pyc, tab_s), dse, timp);
+                        }
+                        accumulate(S, key, dse, timp);
+                    }
+                } else {
+                    // beyond the kept masks the samples are re-decided exactly as
+                    // in pass 1; T < T_TERMINATE here iff pass 1 had stopped
+                    unsigned m = live_mask(B, cnt, px - (lane & 7), py - (lane >> 3), lane);
+                    if (!inside || T < kCompositeK[2]) m = 0u;
+                    while (__any_sync(FULL, m != 0u)) {
+                        int key = 32 + lane;
+                        double dse = 0.0, timp = 0.0;
+                        if (m) {
+                            const int e = __ffs(m) - 1;
+                            m &= m - 1u;
+                            double alpha;
+                            if (eval_alpha(B, e, pxc, pyc, tab_s, alpha)) {
+                                key = e;
+                                removal(e, alpha, dse, timp);
+                                if (T < kCompositeK[2]) m = 0u;
                             }
                         }
+                        accumulate(S, key, dse, timp);
                     }
-                    accumulate(S, key, dse, timp);
                 }
                 __syncwarp();
                 if (lane < cnt) a.partial[B.dup[lane]] = S.acc[lane];
