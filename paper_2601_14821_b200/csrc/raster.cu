@@ -368,10 +368,18 @@ struct ChunkBuf {
 // the copy (measured faster at C3 than double buffering at 6 CTAs per SM)
 constexpr int kChunkBufs = POTR_CHUNK_BUFFERS;
 
+#ifndef POTR_ACC_SPLIT
+#define POTR_ACC_SPLIT 2
+#endif
+// Lane groups with their own accumulator row: groups of lanes adding to the
+// same entry are split by half-warp, halving the serial rounds.
+constexpr int kAccSplit = POTR_ACC_SPLIT;
+
 struct WarpSmem {
     ChunkBuf buf[kChunkBufs];
     unsigned cmask[kMaskChunks][32];  // pass-1 contribution mask of each lane, per chunk
-    double2 acc[32];                  // per-entry (dSE, T*alpha) sums of the current chunk
+    double2 acc[kAccSplit][32];       // per-entry (dSE, T*alpha) sums of the current chunk,
+                                      // one row per lane group (summed in row order)
 };
 
 __device__ __forceinline__ double warp_sum(double v) {
@@ -578,24 +586,25 @@ constexpr int kSerialGroups = POTR_SERIAL_GROUPS;
 __device__ __forceinline__ void accumulate(WarpSmem &S, int key, double v0, double v1) {
     const unsigned FULL = 0xffffffffu;
     const int lane = threadIdx.x & 31;
-    const unsigned peers = __match_any_sync(FULL, key);
+    const int row = kAccSplit == 2 ? lane >> 4 : 0;
+    const unsigned peers = __match_any_sync(FULL, key + 64 * row);
     const int gmax = __reduce_max_sync(FULL, (unsigned)__popc(peers));
     if (gmax <= kSerialGroups) {
         const int rank = __popc(peers & ((1u << lane) - 1u));
         for (int r = 0; r < gmax; r++) {
             if (rank == r && key < 32) {
-                double2 t = S.acc[key];
+                double2 t = S.acc[row][key];
                 t.x += v0;
                 t.y += v1;
-                S.acc[key] = t;
+                S.acc[row][key] = t;
             }
             __syncwarp();
         }
         return;
     }
-    if (group_sum(key, v0, v1) && key < 32) {
-        S.acc[key].x += v0;
-        S.acc[key].y += v1;
+    if (group_sum(key + 64 * row, v0, v1) && key < 32) {
+        S.acc[row][key].x += v0;
+        S.acc[row][key].y += v1;
     }
 }
 
@@ -773,7 +782,8 @@ __global__ void __launch_bounds__(32 * kRasterWarps, POTR_RASTER_MIN_BLOCKS) k_r
                     issue_chunk(a, S.buf[0], next, lane);
                     next = fetch_ids(a, base + 32, end, lane);
                 }
-                S.acc[lane] = make_double2(0.0, 0.0);
+#pragma unroll
+                for (int q = 0; q < kAccSplit; q++) S.acc[q][lane] = make_double2(0.0, 0.0);
                 if (kChunkBufs == 2) cp_async_wait<1>();
                 else cp_async_wait<0>();
                 __syncwarp();
@@ -841,7 +851,12 @@ __global__ void __launch_bounds__(32 * kRasterWarps, POTR_RASTER_MIN_BLOCKS) k_r
                     }
                 }
                 __syncwarp();
-                if (lane < cnt) a.partial[B.dup[lane]] = S.acc[lane];
+                if (lane < cnt) {
+                    double2 t = S.acc[0][lane];
+#pragma unroll
+                    for (int q = 1; q < kAccSplit; q++) t.x += S.acc[q][lane].x, t.y += S.acc[q][lane].y;
+                    a.partial[B.dup[lane]] = t;
+                }
                 written = base + cnt;
                 __syncwarp();
             }
