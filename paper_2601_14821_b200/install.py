@@ -9,6 +9,7 @@ uninstall callable.
 
 import importlib
 
+from . import codec as _codec
 from . import compaction as _comp
 from . import metrics as _met
 from . import rasterizer as _rast
@@ -29,7 +30,9 @@ PATCH_SET = {
         "compute_importance": _rast.compute_importance,
         "render_targets": _rast.render_targets,
         "compact_scene": _comp.compact_scene,
+        "encode_container": _codec.encode_container,
     },
+    "potr.bitstream": {"encode_container": _codec.encode_container},
     "potr.cli": {
         "compute_importance": _rast.compute_importance,
         "render_targets": _rast.render_targets,

@@ -47,7 +47,8 @@ def test_install_patches_every_import_site(reference):
     import potr.compaction
     import potr.rasterizer
     from paper_2601_14821_b200 import install as I
-    from paper_2601_14821_b200 import rasterizer, compaction
+    import potr.bitstream
+    from paper_2601_14821_b200 import rasterizer, compaction, codec
     before = potr.pruning.compute_delta_mse
     undo = I.install()
     try:
@@ -56,6 +57,8 @@ def test_install_patches_every_import_site(reference):
         assert potr.pipeline.compute_importance is rasterizer.compute_importance
         assert potr.compaction.render_image is rasterizer.render_image
         assert potr.rasterizer.forward_stats is rasterizer.forward_stats
+        assert potr.pipeline.encode_container is codec.encode_container
+        assert potr.bitstream.encode_container is codec.encode_container
     finally:
         undo()
     assert potr.pruning.compute_delta_mse is before
