@@ -221,6 +221,11 @@ int potr_attribute_streams(potr_ctx *ctx, int64_t n, const int64_t *order, const
  * scores equal up to summation order); 0: the full bbox tile rectangle.
  * potr_bin always reports the bbox lists. */
 #define POTR_OPT_TILE_CULL 3
+/* 1 (default): each view's splat records are stored in the Morton order of
+ * the splat centres, so a tile's records sit close together in HBM (L2 and
+ * TLB locality for the rasterizer's fetches); 0: splat order.  Results are
+ * bit-identical either way. */
+#define POTR_OPT_SPATIAL_RECORDS 4
 int potr_set_option(potr_ctx *ctx, int option, int value);
 
 /* ---- evidence: live stage timing and work counters --------------------- */

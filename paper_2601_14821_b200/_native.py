@@ -22,6 +22,7 @@ NEQ_STRIDE = 185
 OPT_VIEW_BATCH = 1
 OPT_RAW_DEPTH_KEYS = 2
 OPT_TILE_CULL = 3
+OPT_SPATIAL_RECORDS = 4
 STAGES = ["preprocess", "depth_sort", "scan", "duplicate", "tile_sort", "raster", "reduce",
           "sh_accumulate", "sh_solve"]
 

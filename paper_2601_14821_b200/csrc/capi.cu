@@ -22,6 +22,10 @@ struct DevBuf {
 
 }  // namespace
 
+#ifndef POTR_SPATIAL_DEFAULT
+#define POTR_SPATIAL_DEFAULT 1
+#endif
+
 struct potr_ctx {
     int device = 0;
     cudaStream_t stream = nullptr;
@@ -61,6 +65,13 @@ struct potr_ctx {
     int view_batch = kMaxViewBatch;
     int depth_keys = 0;  // POTR_OPT_RAW_DEPTH_KEYS: 0 split compact, 1 raw, 2 compact 64-bit
     bool tile_cull = true;  // POTR_OPT_TILE_CULL
+    bool spatial = POTR_SPATIAL_DEFAULT != 0;  // POTR_OPT_SPATIAL_RECORDS
+    // spatial record order of the current call's splats and their slot-ordered
+    // copy (raster.cuh spatial_order); prep: k_splat_prep in splat order
+    DevBuf mperm, mrank, mcode, mcode2, slot_pos, slot_sh, slot_opac, slot_prep;
+    bool spatial_ok = false;     // this call's splats have a slot order
+    bool prep_ok = false;        // ctx->prep holds this call's splats
+    bool batch_spatial = false;  // the last bin_batch ran in slot space
 };
 
 namespace {
@@ -233,17 +244,24 @@ int bitlen(uint64_t x) {
     return b;
 }
 
-// Axis-aligned bounds of the splat centres (one reduction + sync per call):
-// they bound every view's depth range, which makes the batch depth key compact.
-// Once per call of a binning entry point: the splats' position bounds (for the
-// compact depth key) and their view-independent terms (k_splat_prep).
-int compute_scene_bounds(potr_ctx *ctx, const potr_splats &sp) {
+// The view-independent splat terms (k_splat_prep) in splat order, once per
+// call when a batch runs in splat order.
+int ensure_prep(potr_ctx *ctx, const potr_splats &sp) {
+    if (ctx->prep_ok) return 0;
     ENSURE(ctx->prep, sizeof(SplatPrep) * (sp.n > 0 ? sp.n : 1));
-    {
-        Stage _st(ctx, POTR_STAGE_PREPROCESS);
-        LAUNCH(1, launch_splat_prep(sp, P<SplatPrep>(ctx->prep), ctx->stream));
-        _st.end();
-    }
+    Stage _st(ctx, POTR_STAGE_PREPROCESS);
+    LAUNCH(1, launch_splat_prep(sp, P<SplatPrep>(ctx->prep), ctx->stream));
+    _st.end();
+    ctx->prep_ok = true;
+    return 0;
+}
+
+// Once per call of a binning entry point: the splats' position bounds (one
+// reduction + sync: they bound every view's depth range, which makes the batch
+// depth key compact), then the spatial slot order and the slot-ordered splat
+// copy with its view-independent terms (or those terms in splat order).
+int compute_scene_bounds(potr_ctx *ctx, const potr_splats &sp) {
+    ctx->spatial_ok = ctx->prep_ok = ctx->batch_spatial = false;
     ENSURE(ctx->bbox, 6 * sizeof(unsigned long long));
     LAUNCH(1, launch_bbox(sp.n, sp.positions, P<unsigned long long>(ctx->bbox), ctx->stream));
     CK(cudaMemcpyAsync(ctx->pinned, ctx->bbox.p, 6 * sizeof(uint64_t), cudaMemcpyDeviceToHost,
@@ -253,7 +271,40 @@ int compute_scene_bounds(potr_ctx *ctx, const potr_splats &sp) {
         ctx->scene_lo[i] = ordered_to_double((unsigned long long)ctx->pinned[i]);
         ctx->scene_hi[i] = ordered_to_double((unsigned long long)ctx->pinned[3 + i]);
     }
+    if (!ctx->spatial || sp.n == 0) return ensure_prep(ctx, sp);
+    Stage _st(ctx, POTR_STAGE_PREPROCESS);
+    int rc = ensure_iota(ctx, sp.n);
+    if (rc) return rc;
+    ENSURE(ctx->mperm, sizeof(int32_t) * sp.n);
+    ENSURE(ctx->mrank, sizeof(int32_t) * sp.n);
+    ENSURE(ctx->mcode, sizeof(uint32_t) * sp.n);
+    ENSURE(ctx->mcode2, sizeof(uint32_t) * sp.n);
+    ENSURE(ctx->slot_pos, sizeof(double) * 3 * sp.n);
+    ENSURE(ctx->slot_sh, sizeof(double) * 48 * sp.n);
+    ENSURE(ctx->slot_opac, sizeof(double) * sp.n);
+    ENSURE(ctx->slot_prep, sizeof(SplatPrep) * sp.n);
+    size_t t = 0;
+    CK(spatial_order_temp(sp.n, &t));
+    ENSURE(ctx->temp, t);
+    LAUNCH(2, spatial_order(ctx->temp.p, ctx->temp.cap, sp.n, sp.positions, ctx->scene_lo,
+                            ctx->scene_hi, P<int32_t>(ctx->iota), P<uint32_t>(ctx->mcode),
+                            P<uint32_t>(ctx->mcode2), P<int32_t>(ctx->mperm),
+                            P<int32_t>(ctx->mrank), ctx->stream));
+    LAUNCH(1, launch_splat_slots(sp, P<int32_t>(ctx->mperm), P<double>(ctx->slot_pos),
+                                 P<double>(ctx->slot_sh), P<double>(ctx->slot_opac),
+                                 P<SplatPrep>(ctx->slot_prep), ctx->stream));
+    _st.end();
+    ctx->spatial_ok = true;
     return 0;
+}
+
+// The last batch's slot order (slot -> splat, splat -> slot), or null when it
+// ran in splat order.
+const int32_t *spatial_perm(potr_ctx *ctx) {
+    return ctx->batch_spatial ? P<int32_t>(ctx->mperm) : nullptr;
+}
+const int32_t *spatial_rank(potr_ctx *ctx) {
+    return ctx->batch_spatial ? P<int32_t>(ctx->mrank) : nullptr;
 }
 
 // The compact batch depth key (raster.cuh DepthKey) from the scene bounds.
@@ -345,6 +396,20 @@ int bin_batch(potr_ctx *ctx, const potr_splats &sp, const potr_camera *cams, int
         dk.khi = P<uint32_t>(ctx->khi);
     }
     ctx->depth_split = split;
+    // slot space needs the split sort: its run fixup orders exact ties by splat
+    // index (the 64-bit fallback sorts keep input order, i.e. slot order)
+    ctx->batch_spatial = ctx->spatial_ok && split && dk.shift > 0;
+    if (!ctx->batch_spatial && (rc = ensure_prep(ctx, sp))) return rc;
+    potr_splats sp_b = sp;
+    const SplatPrep *prep_b = P<SplatPrep>(ctx->prep);
+    if (ctx->batch_spatial) {
+        sp_b.positions = P<double>(ctx->slot_pos);
+        sp_b.sh = P<double>(ctx->slot_sh);
+        sp_b.opacities = P<double>(ctx->slot_opac);
+        sp_b.scales = nullptr;     // folded into slot_prep
+        sp_b.rotations = nullptr;
+        prep_b = P<SplatPrep>(ctx->slot_prep);
+    }
     CK(cudaMemsetAsync(ctx->overflow.p, 0, 2 * sizeof(int), ctx->stream));
     size_t t1 = 0, t2 = 0;
     CK(split ? depth_sort32_temp(total, &t1) : depth_sort_temp(total, &t1));
@@ -353,7 +418,7 @@ int bin_batch(potr_ctx *ctx, const potr_splats &sp, const potr_camera *cams, int
 
     {
         Stage _st(ctx, POTR_STAGE_PREPROCESS);
-        LAUNCH(1, launch_preprocess(sp, P<SplatPrep>(ctx->prep), cb, nview, g.tiles_x, all_colors ? 1 : 0, cull ? 1 : 0, dk,
+        LAUNCH(1, launch_preprocess(sp_b, prep_b, cb, nview, g.tiles_x, all_colors ? 1 : 0, cull ? 1 : 0, dk,
                                     P<SplatRec>(ctx->rec), P<TileSpan>(ctx->spans),
                                     P<uint64_t>(ctx->key),
                                     P<int32_t>(ctx->cnt), P<int32_t>(ctx->vidx), counters(ctx),
@@ -376,7 +441,8 @@ int bin_batch(potr_ctx *ctx, const potr_splats &sp, const potr_camera *cams, int
             if (dk.shift)
                 LAUNCH(1, launch_depth_fixup(total, P<uint32_t>(ctx->skhi), P<int32_t>(ctx->sids),
                                              P<uint64_t>(ctx->key), dk.shift, dk.sentinel, dk.nbits,
-                                             P<int>(ctx->overflow) + 1, ctx->stream));
+                                             P<int>(ctx->overflow) + 1, spatial_perm(ctx), n,
+                                             ctx->stream));
         } else if (dk.compact) {  // one stable sort of the whole batch
             const int end_bit = key_bits;
             bool alt = false;
@@ -551,7 +617,7 @@ int score_views_impl(potr_ctx *ctx, const potr_splats *sp, int ncam, const potr_
             Stage _st(ctx, POTR_STAGE_REDUCE);
             LAUNCH(1, launch_splat_reduce(n * nb, n, P<int32_t>(ctx->sids), P<int64_t>(ctx->offs),
                                           P<double2>(ctx->partial), g.P, P<double2>(ctx->ci_v),
-                                          ctx->stream));
+                                          spatial_perm(ctx), ctx->stream));
             LAUNCH(1, launch_view_accumulate(n, nb, P<double2>(ctx->ci_v),
                                              cam_imp ? cam_imp + (int64_t)s * n : nullptr, imp_sum,
                                              targets ? dmse_sum : nullptr,
@@ -621,6 +687,9 @@ void potr_destroy(potr_ctx *ctx) {
     if (ctx->dm_v.p) cudaFree(ctx->dm_v.p);
     if (ctx->khi.p) cudaFree(ctx->khi.p);
     if (ctx->spans.p) cudaFree(ctx->spans.p);
+    for (DevBuf *b : {&ctx->mperm, &ctx->mrank, &ctx->mcode, &ctx->mcode2, &ctx->slot_pos,
+                      &ctx->slot_sh, &ctx->slot_opac, &ctx->slot_prep})
+        if (b->p) cudaFree(b->p);
     for (DevBuf *b : {&ctx->met_mom, &ctx->met_part, &ctx->met_w, &ctx->met_out, &ctx->codec_eyes})
         if (b->p) cudaFree(b->p);
     if (ctx->codec_scratch) cudaFree(ctx->codec_scratch);
@@ -808,7 +877,8 @@ int potr_render_records(potr_ctx *ctx, const potr_splats *splats, const potr_cam
     a.rec_p = P<double>(ctx->rp);
     LAUNCH(1, launch_raster(kRecords, a, a.ntiles, ctx->stream));
     if (colors)
-        LAUNCH(1, launch_colors_from_rec(n, P<SplatRec>(ctx->rec), colors, ctx->stream));
+        LAUNCH(1, launch_colors_from_rec(n, P<SplatRec>(ctx->rec), spatial_rank(ctx), colors,
+                                         ctx->stream));
     CK(cudaMemcpyAsync(ctx->pinned, ctx->rcounter.p, sizeof(int64_t), cudaMemcpyDeviceToHost,
                        ctx->stream));
     CK(cudaStreamSynchronize(ctx->stream));
@@ -828,7 +898,7 @@ int potr_render_records(potr_ctx *ctx, const potr_splats *splats, const potr_cam
     LAUNCH(1, launch_records_gather(m, P<uint64_t>(ctx->rskey), P<int32_t>(ctx->rsidx),
                                     P<int32_t>(ctx->sids), P<double>(ctx->ralpha),
                                     P<double>(ctx->rt), P<double>(ctx->rp), splat_ids, pixels,
-                                    alphas, trans_at, partials, ctx->stream));
+                                    alphas, trans_at, partials, spatial_perm(ctx), ctx->stream));
     return POTR_OK;
 }
 
@@ -868,7 +938,7 @@ int potr_bin(potr_ctx *ctx, const potr_splats *splats, const potr_camera *cam, i
                                  P<int32_t>(ctx->sids),
                                  P<unsigned long long>(ctx->nvalid), order, geom(*cam).ntiles,
                                  P<int2>(ctx->ranges), K, tile_offsets, P<int2>(ctx->pair),
-                                 tile_splats, ctx->stream));
+                                 tile_splats, spatial_perm(ctx), ctx->stream));
     CK(cudaMemcpyAsync(ctx->pinned, ctx->nvalid.p, sizeof(int64_t), cudaMemcpyDeviceToHost,
                        ctx->stream));
     CK(cudaStreamSynchronize(ctx->stream));
@@ -1038,6 +1108,9 @@ int potr_set_option(potr_ctx *ctx, int option, int value) {
             return POTR_OK;
         case POTR_OPT_TILE_CULL:
             ctx->tile_cull = value != 0;
+            return POTR_OK;
+        case POTR_OPT_SPATIAL_RECORDS:
+            ctx->spatial = value != 0;
             return POTR_OK;
     }
     return fail(ctx, POTR_E_ARG, "unknown option");

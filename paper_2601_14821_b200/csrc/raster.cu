@@ -117,6 +117,43 @@ __global__ void k_splat_prep(int64_t n, const double *__restrict__ scales,
     prep[k] = p;
 }
 
+// The splats in record-slot order (raster.cuh spatial_order): slot r holds
+// splat perm[r]'s position, SH, opacity and view-independent terms, so the
+// per-batch preprocess reads and writes contiguously in slot order.
+__global__ void k_splat_slots(int64_t n, potr_splats sp, const int32_t *__restrict__ perm,
+                              double *__restrict__ pos, double *__restrict__ sh,
+                              double *__restrict__ opac, SplatPrep *__restrict__ prep) {
+    const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= n) return;
+    const int64_t k = perm[r];
+    double scl[3], rot[4];
+#pragma unroll
+    for (int i = 0; i < 3; i++) {
+        pos[3 * r + i] = sp.positions[3 * k + i];
+        scl[i] = sp.scales[3 * k + i];
+    }
+#pragma unroll
+    for (int i = 0; i < 4; i++) rot[i] = sp.rotations[4 * k + i];
+    const double2 *src = reinterpret_cast<const double2 *>(sp.sh + 48 * k);
+    double2 *dst = reinterpret_cast<double2 *>(sh + 48 * r);
+#pragma unroll 8
+    for (int i = 0; i < 24; i++) dst[i] = src[i];
+    const double o = sp.opacities[k];
+    opac[r] = o;
+    SplatPrep p;
+    splat_sigma(scl, rot, p.S);
+    p.pthr = log(kAlphaFloor / o) - kPowerMargin;
+    prep[r] = p;
+}
+
+cudaError_t launch_splat_slots(const potr_splats &sp, const int32_t *perm, double *pos, double *sh,
+                               double *opac, SplatPrep *prep, cudaStream_t st) {
+    if (sp.n == 0) return cudaSuccess;
+    k_splat_slots<<<(unsigned)((sp.n + 127) / 128), 128, 0, st>>>(sp.n, sp, perm, pos, sh, opac,
+                                                                  prep);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_splat_prep(const potr_splats &sp, SplatPrep *prep, cudaStream_t st) {
     if (sp.n == 0) return cudaSuccess;
     k_splat_prep<<<(unsigned)((sp.n + 127) / 128), 128, 0, st>>>(sp.n, sp.scales, sp.rotations,
@@ -879,7 +916,8 @@ __global__ void __launch_bounds__(256) k_splat_reduce(int64_t total, int64_t n,
                                                       const int32_t *__restrict__ ids,
                                                       const int64_t *__restrict__ offs,
                                                       const double2 *__restrict__ partial,
-                                                      double P, double2 *__restrict__ vals) {
+                                                      double P, double2 *__restrict__ vals,
+                                                      const int32_t *__restrict__ perm) {
     __shared__ double2 stage[8][kReduceStage];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const int64_t i0 = ((int64_t)blockIdx.x * 8 + w) * 32;
@@ -907,8 +945,13 @@ __global__ void __launch_bounds__(256) k_splat_reduce(int64_t total, int64_t n,
         }
     }
     if (!act) return;
-    // one 16-byte scatter per (view, splat): (I_k(s), dMSE_k(s)) by record index
-    vals[ids[i]] = make_double2(imp / P, dse / (P * 3.0));
+    // one 16-byte scatter per (view, splat): (I_k(s), dMSE_k(s)) by splat index
+    int64_t g = ids[i];
+    if (perm) {
+        const int64_t v = i / n;
+        g = v * n + perm[g - v * n];
+    }
+    vals[g] = make_double2(imp / P, dse / (P * 3.0));
 }
 
 // Camera-ordered accumulation over the views of the batch (rasterizer.py:343-347),
@@ -976,12 +1019,13 @@ __global__ void k_records_gather(int64_t m, const uint64_t *__restrict__ skey,
                                  const double *__restrict__ ra, const double *__restrict__ rt,
                                  const double *__restrict__ rp, int64_t *splat_ids,
                                  int64_t *pixels, double *alphas, double *trans_at,
-                                 double *partials) {
+                                 double *partials, const int32_t *__restrict__ perm) {
     int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= m) return;
     uint64_t k = skey[i];
     int32_t s = sidx[i];
-    splat_ids[i] = ids[(int64_t)(k >> 32)];
+    const int32_t g = ids[(int64_t)(k >> 32)];  // one view: slot
+    splat_ids[i] = perm ? perm[g] : g;
     pixels[i] = (int64_t)(k & 0xffffffffu);
     alphas[i] = ra[s];
     trans_at[i] = rt[s];
@@ -992,12 +1036,14 @@ __global__ void k_records_gather(int64_t m, const uint64_t *__restrict__ skey,
 
 // Records mode preprocesses with all_colors: every splat has a record, with
 // zero colour when it is invalid (rasterizer.py:252-254 leaves those at 0).
-__global__ void k_colors_from_rec(int64_t n, const SplatRec *__restrict__ rec, double *colors) {
+__global__ void k_colors_from_rec(int64_t n, const SplatRec *__restrict__ rec,
+                                  const int32_t *__restrict__ mpos, double *colors) {
     int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (k >= n) return;
-    colors[3 * k] = rec[k].cr;
-    colors[3 * k + 1] = rec[k].cg;
-    colors[3 * k + 2] = rec[k].cb;
+    const SplatRec &r = rec[mpos ? mpos[k] : k];
+    colors[3 * k] = r.cr;
+    colors[3 * k + 1] = r.cg;
+    colors[3 * k + 2] = r.cb;
 }
 
 __global__ void k_tile_offsets(int ntiles, const int2 *__restrict__ rng, int64_t K,
@@ -1019,14 +1065,16 @@ __global__ void k_tile_offsets(int ntiles, const int2 *__restrict__ rng, int64_t
     out[t] = o;
 }
 
-__global__ void k_tile_splats(int64_t K, const int2 *__restrict__ pair, int32_t *__restrict__ out) {
+__global__ void k_tile_splats(int64_t K, const int2 *__restrict__ pair,
+                              const int32_t *__restrict__ mperm, int32_t *__restrict__ out) {
     int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (j < K) out[j] = pair[j].y;
+    if (j < K) out[j] = mperm ? mperm[pair[j].y] : pair[j].y;  // one view: slot = rank
 }
 
-__global__ void k_order_out(int64_t nv, const int32_t *__restrict__ ids, int64_t *__restrict__ out) {
+__global__ void k_order_out(int64_t nv, const int32_t *__restrict__ ids,
+                            const int32_t *__restrict__ perm, int64_t *__restrict__ out) {
     int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (r < nv) out[r] = ids[r];
+    if (r < nv) out[r] = perm ? perm[ids[r]] : ids[r];  // one view: slot -> splat
 }
 
 __global__ void k_count_valid(int64_t n, const uint64_t *__restrict__ skey, uint64_t invalid,
@@ -1112,7 +1160,8 @@ cudaError_t depth_sort32_temp(int64_t n, size_t *bytes) {
 // was stable, so equal full keys keep record-index order (the tiebreak).
 __global__ void k_depth_fixup(int64_t total, const uint32_t *__restrict__ hi,
                               int32_t *__restrict__ sids, const uint64_t *__restrict__ key,
-                              uint32_t invalid_lo, uint32_t lo_mask, int *overflow) {
+                              uint32_t invalid_lo, uint32_t lo_mask, int *overflow,
+                              const int32_t *__restrict__ perm, int64_t n) {
     const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (j + 1 >= total) return;
     const uint32_t h = hi[j];
@@ -1125,6 +1174,8 @@ __global__ void k_depth_fixup(int64_t total, const uint32_t *__restrict__ hi,
             return;
         }
     }
+    // records in slot order (perm): equal full keys order by splat index,
+    // as np.argsort(kind="stable") does; a run shares its view
     int32_t id[kFixupRun];
     uint64_t kv[kFixupRun];
     for (int i = 0; i < len; i++) {
@@ -1134,8 +1185,9 @@ __global__ void k_depth_fixup(int64_t total, const uint32_t *__restrict__ hi,
     for (int i = 1; i < len; i++) {
         const int32_t x = id[i];
         const uint64_t y = kv[i];
+        const int32_t ox = perm ? perm[x % n] : x;
         int q = i - 1;
-        while (q >= 0 && kv[q] > y) {
+        while (q >= 0 && (kv[q] > y || (perm && kv[q] == y && perm[id[q] % n] > ox))) {
             kv[q + 1] = kv[q];
             id[q + 1] = id[q];
             q--;
@@ -1148,14 +1200,14 @@ __global__ void k_depth_fixup(int64_t total, const uint32_t *__restrict__ hi,
 
 cudaError_t launch_depth_fixup(int64_t total, const uint32_t *khi_sorted, int32_t *sids,
                                const uint64_t *key, int shift, uint64_t sentinel, int nbits,
-                               int *overflow, cudaStream_t st) {
+                               int *overflow, const int32_t *perm, int64_t n, cudaStream_t st) {
     if (total < 2) return cudaSuccess;
     // hi = (view << (nbits - shift)) | depth part; the invalid sentinel's depth part
     const int dbits = nbits - shift;
     const uint32_t lo_mask = dbits >= 32 ? 0xffffffffu : ((1u << dbits) - 1u);
     const uint32_t invalid_lo = (uint32_t)(sentinel >> shift) & lo_mask;
     k_depth_fixup<<<grid_for(total, 256), 256, 0, st>>>(total, khi_sorted, sids, key, invalid_lo,
-                                                        lo_mask, overflow);
+                                                        lo_mask, overflow, perm, n);
     return cudaGetLastError();
 }
 
@@ -1199,6 +1251,62 @@ __global__ void k_bbox(int64_t n, const double *__restrict__ pos,
         atomicMin(&out[i], mn[i]);
         atomicMax(&out[3 + i], mx[i]);
     }
+}
+
+// Spatial record order: a 30-bit Morton code of each splat centre within the
+// scene bounds (10 bits per axis; non-finite coordinates go to cell 0).
+__global__ void k_morton(int64_t n, const double *__restrict__ pos, double lx, double ly,
+                         double lz, double sx, double sy, double sz, uint32_t *__restrict__ code) {
+    const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= n) return;
+    const double lo[3] = {lx, ly, lz}, sc[3] = {sx, sy, sz};
+    uint32_t c = 0u;
+#pragma unroll
+    for (int i = 0; i < 3; i++) {
+        double q = (pos[3 * k + i] - lo[i]) * sc[i];
+        q = q >= 0.0 ? (q < 1023.0 ? q : 1023.0) : 0.0;  // NaN -> 0
+        uint32_t u = (uint32_t)q;
+        // spread the 10 bits three apart
+        u = (u | (u << 16)) & 0x030000FFu;
+        u = (u | (u << 8)) & 0x0300F00Fu;
+        u = (u | (u << 4)) & 0x030C30C3u;
+        u = (u | (u << 2)) & 0x09249249u;
+        c |= u << i;
+    }
+    code[k] = c;
+}
+
+__global__ void k_scatter_rank(int64_t n, const int32_t *__restrict__ perm,
+                               int32_t *__restrict__ pos) {
+    const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (r < n) pos[perm[r]] = (int32_t)r;
+}
+
+cudaError_t spatial_order_temp(int64_t n, size_t *bytes) {
+    return cub::DeviceRadixSort::SortPairs(nullptr, *bytes, (const uint32_t *)nullptr,
+                                           (uint32_t *)nullptr, (const int32_t *)nullptr,
+                                           (int32_t *)nullptr, (int)n, 0, 30);
+}
+
+cudaError_t spatial_order(void *temp, size_t temp_bytes, int64_t n, const double *pos,
+                          const double lo[3], const double hi[3], const int32_t *iota,
+                          uint32_t *code, uint32_t *code_sorted, int32_t *perm, int32_t *rank,
+                          cudaStream_t st) {
+    if (n == 0) return cudaSuccess;
+    double sc[3];
+    for (int i = 0; i < 3; i++) {
+        const double ext = hi[i] - lo[i];
+        sc[i] = ext > 0.0 && ext < 1e300 ? 1024.0 / ext : 0.0;
+    }
+    k_morton<<<grid_for(n, 256), 256, 0, st>>>(n, pos, lo[0], lo[1], lo[2], sc[0], sc[1], sc[2],
+                                               code);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    e = cub::DeviceRadixSort::SortPairs(temp, temp_bytes, code, code_sorted, iota, perm, (int)n, 0,
+                                        30, st);
+    if (e != cudaSuccess) return e;
+    k_scatter_rank<<<grid_for(n, 256), 256, 0, st>>>(n, perm, rank);
+    return cudaGetLastError();
 }
 
 cudaError_t launch_bbox(int64_t n, const double *pos, unsigned long long *out, cudaStream_t st) {
@@ -1329,9 +1437,10 @@ cudaError_t launch_raster(int mode, const RasterArgs &a, int ntiles, cudaStream_
 
 cudaError_t launch_splat_reduce(int64_t total, int64_t n, const int32_t *ids, const int64_t *offs,
                                 const double2 *partial, double P, double2 *vals,
-                                cudaStream_t st) {
+                                const int32_t *perm, cudaStream_t st) {
     if (total == 0) return cudaSuccess;
-    k_splat_reduce<<<grid_for(total, 256), 256, 0, st>>>(total, n, ids, offs, partial, P, vals);
+    k_splat_reduce<<<grid_for(total, 256), 256, 0, st>>>(total, n, ids, offs, partial, P, vals,
+                                                         perm);
     // (one warp per 32 entries, 8 warps per block: grid_for(total, 256) blocks)
     return cudaGetLastError();
 }
@@ -1364,17 +1473,17 @@ cudaError_t launch_records_gather(int64_t m, const uint64_t *skey, const int32_t
                                   const int32_t *ids, const double *ra, const double *rt,
                                   const double *rp, int64_t *splat_ids, int64_t *pixels,
                                   double *alphas, double *trans_at, double *partials,
-                                  cudaStream_t st) {
+                                  const int32_t *perm, cudaStream_t st) {
     if (m == 0) return cudaSuccess;
     k_records_gather<<<grid_for(m, 256), 256, 0, st>>>(m, skey, sidx, ids, ra, rt, rp, splat_ids,
-                                                        pixels, alphas, trans_at, partials);
+                                                        pixels, alphas, trans_at, partials, perm);
     return cudaGetLastError();
 }
 
-cudaError_t launch_colors_from_rec(int64_t n, const SplatRec *rec, double *colors,
-                                  cudaStream_t st) {
+cudaError_t launch_colors_from_rec(int64_t n, const SplatRec *rec, const int32_t *mpos,
+                                  double *colors, cudaStream_t st) {
     if (n == 0) return cudaSuccess;
-    k_colors_from_rec<<<grid_for(n, 256), 256, 0, st>>>(n, rec, colors);
+    k_colors_from_rec<<<grid_for(n, 256), 256, 0, st>>>(n, rec, mpos, colors);
     return cudaGetLastError();
 }
 
@@ -1382,17 +1491,18 @@ cudaError_t launch_bin_outputs(int64_t n, const uint64_t *skey, uint64_t invalid
                                const int32_t *sids,
                                unsigned long long *nvalid_dev, int64_t *order, int ntiles,
                                const int2 *rng, int64_t K, int64_t *tile_offsets,
-                               const int2 *pair, int32_t *tile_splats, cudaStream_t st) {
+                               const int2 *pair, int32_t *tile_splats, const int32_t *mperm,
+                               cudaStream_t st) {
     cudaError_t e = cudaMemsetAsync(nvalid_dev, 0, sizeof(unsigned long long), st);
     if (e != cudaSuccess) return e;
     if (n > 0) {
         k_count_valid<<<grid_for(n, 256), 256, 0, st>>>(n, skey, invalid, nvalid_dev);
-        k_order_out<<<grid_for(n, 256), 256, 0, st>>>(n, sids, order);
+        k_order_out<<<grid_for(n, 256), 256, 0, st>>>(n, sids, mperm, order);
     }
     if (tile_offsets) k_tile_offsets<<<grid_for(ntiles + 1, 128), 128, 0, st>>>(ntiles, rng, K,
                                                                                tile_offsets);
     if (tile_splats && K > 0)
-        k_tile_splats<<<grid_for(K, 256), 256, 0, st>>>(K, pair, tile_splats);
+        k_tile_splats<<<grid_for(K, 256), 256, 0, st>>>(K, pair, mperm, tile_splats);
     return cudaGetLastError();
 }
 

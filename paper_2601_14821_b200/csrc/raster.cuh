@@ -51,10 +51,27 @@ cudaError_t launch_bbox(int64_t n, const double *pos, unsigned long long *out, c
 
 // Per-splat view-independent terms (Sigma, prefilter threshold), once per call.
 cudaError_t launch_splat_prep(const potr_splats &sp, SplatPrep *prep, cudaStream_t st);
+cudaError_t launch_splat_slots(const potr_splats &sp, const int32_t *perm, double *pos, double *sh,
+                               double *opac, SplatPrep *prep, cudaStream_t st);
 cudaError_t launch_preprocess(const potr_splats &sp, const SplatPrep *prep, const CamBatch &cams,
                               int nview, int tiles_x, int all_colors, int cull, const DepthKey &dk,
                               SplatRec *rec, TileSpan *spans, uint64_t *key, int32_t *cnt,
                               int32_t *vidx, unsigned long long *counters, cudaStream_t st);
+// Spatial record layout.  Each call sorts the splats by the Morton code of
+// their centres (slot r holds splat perm[r]; rank = perm^-1) and copies them
+// in that order (k_splat_slots); the batch pipeline -- preprocess, depth keys,
+// records, pairs -- then runs in slot space, so the records one tile reads lie
+// in a few short address ranges instead of all over the view's records (L2
+// and TLB locality for the rasterizer's fetches).  Slots map back to splat
+// indices where results leave the pipeline (per-splat sums, records, depth
+// order, tile lists), and exact depth ties are ordered by splat index in the
+// run fixup, so results are bit-identical to splat order.  The 64-bit
+// fallback sorts run in splat order.
+cudaError_t spatial_order_temp(int64_t n, size_t *bytes);
+cudaError_t spatial_order(void *temp, size_t temp_bytes, int64_t n, const double *pos,
+                          const double lo[3], const double hi[3], const int32_t *iota,
+                          uint32_t *code, uint32_t *code_sorted, int32_t *perm, int32_t *rank,
+                          cudaStream_t st);
 cudaError_t launch_project_dump(const potr_splats &sp, const Cam &cam, double *mean2d,
                                 double *cov2d, double *depth, double *radius, uint8_t *valid,
                                 double *colors, cudaStream_t st);
@@ -71,7 +88,7 @@ cudaError_t depth_sort32(void *temp, size_t temp_bytes, uint32_t *key_a, uint32_
 constexpr int kFixupRun = 64;
 cudaError_t launch_depth_fixup(int64_t total, const uint32_t *khi_sorted, int32_t *sids,
                                const uint64_t *key, int shift, uint64_t sentinel, int nbits,
-                               int *overflow, cudaStream_t st);
+                               int *overflow, const int32_t *perm, int64_t n, cudaStream_t st);
 cudaError_t launch_gather_keys(int64_t total, const int32_t *sids, const uint64_t *key,
                                uint64_t *skey, cudaStream_t st);
 cudaError_t depth_sort(void *temp, size_t temp_bytes, uint64_t *key_a, uint64_t *key_b,
@@ -97,7 +114,7 @@ cudaError_t launch_tile_ranges(int64_t j0, int64_t K, bool key16, const void *sk
 cudaError_t launch_raster(int mode, const RasterArgs &a, int ntiles, cudaStream_t st);
 cudaError_t launch_splat_reduce(int64_t total, int64_t n, const int32_t *ids, const int64_t *offs,
                                 const double2 *partial, double P, double2 *vals,
-                                cudaStream_t st);
+                                const int32_t *perm, cudaStream_t st);
 // dmse_rows / mse_rows (nullable): the per-view values as well as their sums
 cudaError_t launch_view_accumulate(int64_t n, int nview, const double2 *vals,
                                    double *cam_imp_rows, double *imp_acc, double *dmse_acc,
@@ -110,14 +127,15 @@ cudaError_t launch_records_gather(int64_t m, const uint64_t *skey, const int32_t
                                   const int32_t *ids, const double *ra, const double *rt,
                                   const double *rp, int64_t *splat_ids, int64_t *pixels,
                                   double *alphas, double *trans_at, double *partials,
-                                  cudaStream_t st);
-cudaError_t launch_colors_from_rec(int64_t n, const SplatRec *rec, double *colors,
-                                  cudaStream_t st);
+                                  const int32_t *perm, cudaStream_t st);
+cudaError_t launch_colors_from_rec(int64_t n, const SplatRec *rec, const int32_t *mpos,
+                                  double *colors, cudaStream_t st);
 cudaError_t launch_bin_outputs(int64_t n, const uint64_t *skey, uint64_t invalid,
                                const int32_t *sids,
                                unsigned long long *nvalid_dev, int64_t *order, int ntiles,
                                const int2 *rng, int64_t K, int64_t *tile_offsets,
-                               const int2 *pair, int32_t *tile_splats, cudaStream_t st);
+                               const int2 *pair, int32_t *tile_splats, const int32_t *mperm,
+                               cudaStream_t st);
 
 // Image metrics (metrics.cu): out[0] = sum of clamped squared differences,
 // out[1..3] = per-channel sums of the cropped SSIM map.

@@ -124,6 +124,47 @@ def test_view_batching_and_key_modes_bit_identical(R, batch, raw):
     assert np.array_equal(order, g["order0"]) and np.array_equal(lst, g["tile_splats0"])
 
 
+def test_spatial_records_bit_identical(R, oracle):
+    """The Morton record layout (POTR_OPT_SPATIAL_RECORDS) only moves records
+    in HBM: scores, renders, records and tile lists are bit-identical with it
+    off, and exact depth ties (duplicated splats) still break by ascending id."""
+    from paper_2601_14821_b200 import _native, binning, device
+    splats, cams = small_scene()
+    g = golden("small_scene")
+    targets = [t for t in g["targets"]]
+    tied = splats.copy()
+    for f in ("positions", "scales", "rotations", "sh", "opacities"):
+        getattr(tied, f)[700:760] = getattr(tied, f)[100:160]   # exact duplicates
+    ctx = device.context()
+
+    def run(sc):
+        st = R.compute_delta_mse(perturbed(sc), cams, targets)
+        rec = R.render_with_records(sc, cams[1])
+        return st, rec, binning.tile_lists(sc, cams[0])
+
+    outs = {}
+    try:
+        for on in (0, 1):
+            ctx.call("potr_set_option", _native.OPT_SPATIAL_RECORDS, on)
+            outs[on] = [run(splats), run(tied)]
+    finally:
+        ctx.call("potr_set_option", _native.OPT_SPATIAL_RECORDS, 1)
+    for (st0, rec0, tl0), (st1, rec1, tl1) in zip(outs[0], outs[1]):
+        assert np.array_equal(st0.delta_mse, st1.delta_mse)
+        assert np.array_equal(st0.importance, st1.importance)
+        assert np.array_equal(np.asarray(st0.camera_importance), np.asarray(st1.camera_importance))
+        assert st0.mse == st1.mse
+        for f in ("image", "transmittance", "splat_ids", "pixels", "alphas", "trans_at",
+                  "partials", "colors"):
+            assert np.array_equal(getattr(rec0, f), getattr(rec1, f)), f
+        for a, b in zip(tl0, tl1):
+            assert np.array_equal(a, b)
+    order, off, lst = outs[1][1][2]
+    assert np.array_equal(order, oracle.depth_order(tied, cams[0]))
+    o_off, o_lst = oracle.tile_lists(tied, cams[0])
+    assert np.array_equal(off, o_off) and np.array_equal(lst, o_lst)
+
+
 def test_score_rows_sum_to_fused_sums(R):
     """potr_score_views_rows' per-view rows, added in camera order (what the
     ordered multi-GPU chain does), equal potr_score_views' sums bit for bit."""
