@@ -654,6 +654,7 @@ int potr_create(int device, potr_ctx **out) {
         int b = std::atoi(vb);
         ctx->view_batch = b < 1 ? 1 : (b > kMaxViewBatch ? kMaxViewBatch : b);
     }
+    if (const char *sr = std::getenv("POTR_B200_SPATIAL")) ctx->spatial = std::atoi(sr) != 0;
     if (cudaMallocHost(&ctx->pinned, 64 * sizeof(int64_t)) != cudaSuccess) {
         delete ctx;
         return POTR_E_NOMEM;

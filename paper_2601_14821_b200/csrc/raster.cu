@@ -925,6 +925,12 @@ __global__ void __launch_bounds__(256) k_splat_reduce(int64_t total, int64_t n,
     const int64_t i = i0 + lane;
     const bool act = i < total;
     const int64_t o = act ? offs[i] : 0, e = act ? offs[i + 1] : 0;
+    // the output index, fetched before the sums (slot space: v*n + perm[slot])
+    int64_t g = act ? ids[i] : 0;
+    if (perm && act) {
+        const int64_t v = i / n;
+        g = v * n + perm[g - v * n];
+    }
     const int64_t base = __shfl_sync(0xffffffffu, o, 0);
     const int64_t last = total - i0 < 32 ? total - i0 - 1 : 31;
     const int64_t top = __shfl_sync(0xffffffffu, e, (int)last);
@@ -946,11 +952,6 @@ __global__ void __launch_bounds__(256) k_splat_reduce(int64_t total, int64_t n,
     }
     if (!act) return;
     // one 16-byte scatter per (view, splat): (I_k(s), dMSE_k(s)) by splat index
-    int64_t g = ids[i];
-    if (perm) {
-        const int64_t v = i / n;
-        g = v * n + perm[g - v * n];
-    }
     vals[g] = make_double2(imp / P, dse / (P * 3.0));
 }
 
