@@ -916,8 +916,7 @@ __global__ void __launch_bounds__(256) k_splat_reduce(int64_t total, int64_t n,
                                                       const int32_t *__restrict__ ids,
                                                       const int64_t *__restrict__ offs,
                                                       const double2 *__restrict__ partial,
-                                                      double P, double2 *__restrict__ vals,
-                                                      const int32_t *__restrict__ perm) {
+                                                      double P, double2 *__restrict__ vals) {
     __shared__ double2 stage[8][kReduceStage];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const int64_t i0 = ((int64_t)blockIdx.x * 8 + w) * 32;
@@ -925,12 +924,9 @@ __global__ void __launch_bounds__(256) k_splat_reduce(int64_t total, int64_t n,
     const int64_t i = i0 + lane;
     const bool act = i < total;
     const int64_t o = act ? offs[i] : 0, e = act ? offs[i + 1] : 0;
-    // the output index, fetched before the sums (slot space: v*n + perm[slot])
-    int64_t g = act ? ids[i] : 0;
-    if (perm && act) {
-        const int64_t v = i / n;
-        g = v * n + perm[g - v * n];
-    }
+    // the output index: the entry's record (slot space stays slot space; the
+    // view accumulation maps slots to splats)
+    const int64_t g = act ? ids[i] : 0;
     const int64_t base = __shfl_sync(0xffffffffu, o, 0);
     const int64_t last = total - i0 < 32 ? total - i0 - 1 : 31;
     const int64_t top = __shfl_sync(0xffffffffu, e, (int)last);
@@ -951,7 +947,7 @@ __global__ void __launch_bounds__(256) k_splat_reduce(int64_t total, int64_t n,
         }
     }
     if (!act) return;
-    // one 16-byte scatter per (view, splat): (I_k(s), dMSE_k(s)) by splat index
+    // one 16-byte scatter per (view, record): (I_k(s), dMSE_k(s))
     vals[g] = make_double2(imp / P, dse / (P * 3.0));
 }
 
@@ -959,13 +955,15 @@ __global__ void __launch_bounds__(256) k_splat_reduce(int64_t total, int64_t n,
 // writing the camera_importance rows on the way (coalesced, by splat id).
 __global__ void k_view_accumulate(int64_t n, int nview, const double2 *__restrict__ vals,
                                   double *__restrict__ cam_imp_rows, double *__restrict__ imp_acc,
-                                  double *__restrict__ dmse_acc, double *__restrict__ dmse_rows) {
+                                  double *__restrict__ dmse_acc, double *__restrict__ dmse_rows,
+                                  const int32_t *__restrict__ rank) {
     const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (k >= n) return;
+    const int64_t r = rank ? rank[k] : k;  // splat k's record slot
     double ia = imp_acc[k];
     double da = dmse_acc ? dmse_acc[k] : 0.0;
     for (int v = 0; v < nview; v++) {
-        const double2 x = vals[(int64_t)v * n + k];
+        const double2 x = vals[(int64_t)v * n + r];
         if (cam_imp_rows) cam_imp_rows[(int64_t)v * n + k] = x.x;
         if (dmse_rows) dmse_rows[(int64_t)v * n + k] = x.y;
         ia += x.x;
@@ -1438,20 +1436,19 @@ cudaError_t launch_raster(int mode, const RasterArgs &a, int ntiles, cudaStream_
 
 cudaError_t launch_splat_reduce(int64_t total, int64_t n, const int32_t *ids, const int64_t *offs,
                                 const double2 *partial, double P, double2 *vals,
-                                const int32_t *perm, cudaStream_t st) {
+                                cudaStream_t st) {
     if (total == 0) return cudaSuccess;
-    k_splat_reduce<<<grid_for(total, 256), 256, 0, st>>>(total, n, ids, offs, partial, P, vals,
-                                                         perm);
+    k_splat_reduce<<<grid_for(total, 256), 256, 0, st>>>(total, n, ids, offs, partial, P, vals);
     // (one warp per 32 entries, 8 warps per block: grid_for(total, 256) blocks)
     return cudaGetLastError();
 }
 
 cudaError_t launch_view_accumulate(int64_t n, int nview, const double2 *vals,
                                    double *cam_imp_rows, double *imp_acc, double *dmse_acc,
-                                   double *dmse_rows, cudaStream_t st) {
+                                   double *dmse_rows, const int32_t *rank, cudaStream_t st) {
     if (n == 0) return cudaSuccess;
     k_view_accumulate<<<grid_for(n, 256), 256, 0, st>>>(n, nview, vals, cam_imp_rows, imp_acc,
-                                                         dmse_acc, dmse_rows);
+                                                         dmse_acc, dmse_rows, rank);
     return cudaGetLastError();
 }
 
