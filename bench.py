@@ -477,8 +477,11 @@ def e2e_measure(args, rank, world, local, pert, cams, tg, S, Pv, dev):
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     for _ in range(args.steps):
+        t1 = time.perf_counter()
         st = call()
         _ = st.delta_mse[0]  # host result in hand
+        if os.environ.get("POTR_E2E_TRACE"):
+            print(f"e2e call {1e3 * (time.perf_counter() - t1):.1f} ms", file=sys.stderr)
     torch.cuda.synchronize()
     dt = (time.perf_counter() - t0) / args.steps
     if world > 1:

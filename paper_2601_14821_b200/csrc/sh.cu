@@ -44,7 +44,11 @@ __constant__ double kYcocgToRgb[9] = {1.0, 1.0, -1.0, 1.0, 0.0, 1.0, 1.0, -1.0, 
 #endif
 constexpr int kShSplatsPerBlock = 16;
 constexpr int kShWarps = 4;
-constexpr int kShRow = 24;  // w*y (16) + w*YCoCg (3), padded for the 2x4 blocks' 16-byte loads
+#ifndef POTR_SH_ROW
+#define POTR_SH_ROW 26
+#endif
+// w*y (16) + w*YCoCg (3), padded for the 2x4 blocks' 16-byte loads
+constexpr int kShRow = POTR_SH_ROW;
 constexpr int kShBlocks = 28;
 
 // Block b of the tiling: rows 2r, 2r+1; columns c0 .. c0+3 (c0 = 2r + 4t).
