@@ -135,6 +135,11 @@ def test_spatial_records_bit_identical(R, oracle):
     tied = splats.copy()
     for f in ("positions", "scales", "rotations", "sh", "opacities"):
         getattr(tied, f)[700:760] = getattr(tied, f)[100:160]   # exact duplicates
+    # a run of 100 equal depth keys: longer than the run fixup takes, so the
+    # batch falls back to the 64-bit sort in splat order
+    stack = splats.copy()
+    for f in ("positions", "scales", "rotations", "sh", "opacities"):
+        getattr(stack, f)[200:300] = getattr(stack, f)[50]
     ctx = device.context()
 
     def run(sc):
@@ -146,7 +151,7 @@ def test_spatial_records_bit_identical(R, oracle):
     try:
         for on in (0, 1):
             ctx.call("potr_set_option", _native.OPT_SPATIAL_RECORDS, on)
-            outs[on] = [run(splats), run(tied)]
+            outs[on] = [run(splats), run(tied), run(stack)]
     finally:
         ctx.call("potr_set_option", _native.OPT_SPATIAL_RECORDS, 1)
     for (st0, rec0, tl0), (st1, rec1, tl1) in zip(outs[0], outs[1]):
@@ -159,10 +164,11 @@ def test_spatial_records_bit_identical(R, oracle):
             assert np.array_equal(getattr(rec0, f), getattr(rec1, f)), f
         for a, b in zip(tl0, tl1):
             assert np.array_equal(a, b)
-    order, off, lst = outs[1][1][2]
-    assert np.array_equal(order, oracle.depth_order(tied, cams[0]))
-    o_off, o_lst = oracle.tile_lists(tied, cams[0])
-    assert np.array_equal(off, o_off) and np.array_equal(lst, o_lst)
+    for sc, out in ((tied, outs[1][1]), (stack, outs[1][2])):
+        order, off, lst = out[2]
+        assert np.array_equal(order, oracle.depth_order(sc, cams[0]))
+        o_off, o_lst = oracle.tile_lists(sc, cams[0])
+        assert np.array_equal(off, o_off) and np.array_equal(lst, o_lst)
 
 
 def test_score_rows_sum_to_fused_sums(R):
