@@ -615,6 +615,10 @@ __device__ __forceinline__ bool group_sum(int key, double &v0, double &v1) {
 // (the common case: ~5 lanes at the C3 shape) do that directly, one rank per
 // round; large ones reduce first with group_sum.  Either way the result
 // depends only on the keys and values, never on scheduling.
+#ifndef POTR_REPLAY_FMA
+#define POTR_REPLAY_FMA 1
+#endif
+
 #ifndef POTR_SERIAL_GROUPS
 #define POTR_SERIAL_GROUPS 8
 #endif
@@ -832,22 +836,36 @@ __global__ void __launch_bounds__(32 * kRasterWarps, POTR_RASTER_MIN_BLOCKS) k_r
                 auto removal = [&](int e, double alpha, double &dse, double &timp) {
                     const double c0 = B.f[4][e].y;
                     const double2 c12 = B.f[5][e];
+                    const double w = T * alpha;
                     if (MODE == kScore) {
                         // prune_deltas, forward form: a/(1-a) * (P_K - P_i - T c),
-                        // dSE = |pd|^2 + 2 pd . dr (rasterizer.py:232-243, :333)
+                        // dSE = |pd|^2 + 2 pd . dr (rasterizer.py:232-243, :333).
+                        // Scores only (1e-4 contract), so fused multiply-adds;
+                        // alpha, T and T*alpha keep the reference's rounding.
                         const double f = alpha * rcp_nr(1.0 - alpha);
-                        const double pd0 = f * (P0 - T * c0);
-                        const double pd1 = f * (P1 - T * c12.x);
-                        const double pd2 = f * (P2 - T * c12.y);
-                        dse = pd0 * (pd0 + dr0);
-                        dse = dse + pd1 * (pd1 + dr1);
-                        dse = dse + pd2 * (pd2 + dr2);
+                        if (POTR_REPLAY_FMA) {
+                            const double pd0 = f * fma(-T, c0, P0);
+                            const double pd1 = f * fma(-T, c12.x, P1);
+                            const double pd2 = f * fma(-T, c12.y, P2);
+                            dse = pd0 * (pd0 + dr0);
+                            dse = fma(pd1, pd1 + dr1, dse);
+                            dse = fma(pd2, pd2 + dr2, dse);
+                            P0 = fma(-w, c0, P0);
+                            P1 = fma(-w, c12.x, P1);
+                            P2 = fma(-w, c12.y, P2);
+                        } else {
+                            const double pd0 = f * (P0 - T * c0);
+                            const double pd1 = f * (P1 - T * c12.x);
+                            const double pd2 = f * (P2 - T * c12.y);
+                            dse = pd0 * (pd0 + dr0);
+                            dse = dse + pd1 * (pd1 + dr1);
+                            dse = dse + pd2 * (pd2 + dr2);
+                            P0 -= w * c0;
+                            P1 -= w * c12.x;
+                            P2 -= w * c12.y;
+                        }
                     }
-                    const double w = T * alpha;
                     timp = w;
-                    P0 -= w * c0;
-                    P1 -= w * c12.x;
-                    P2 -= w * c12.y;
                     T = T * (1.0 - alpha);
                 };
                 if (ci < kMaskChunks) {
