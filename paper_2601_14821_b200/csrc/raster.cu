@@ -67,11 +67,14 @@ __device__ __forceinline__ CullEllipse cull_ellipse(const SplatRec &r) {
     e.none = !(R > 0.0) || r.x0 > r.x1;  // pthr >= margin > 0 >= power: nothing passes
     const double a = -2.0 * r.ha, c = -2.0 * r.hc;
     e.det = a * c - e.b * e.b;
-    e.full = !(a > 0.0 && c > 0.0 && e.det > 1e-4 * (a * c) && isfinite(R) && isfinite(e.det));
-    e.inv_a = 1.0 / a;
+    e.full = !(a > 1e-280 && c > 1e-280 && a < 1e280 && c < 1e280 && e.det > 1e-4 * (a * c) &&
+               e.det > 1e-280 && isfinite(R) && isfinite(e.det));
+    // conservative use only (margins far above 1e-16): Newton reciprocals
+    e.inv_a = rcp_nr(a);
     e.aR = a * R;
-    e.ymax = sqrt(R * a / e.det);
-    e.sdy = e.b * sqrt(R / (e.det * c));
+    const double inv_det = rcp_nr(e.det);
+    e.ymax = sqrt(R * a * inv_det);
+    e.sdy = e.b * sqrt(R * inv_det * rcp_nr(c));
     return e;
 }
 
@@ -486,14 +489,15 @@ __device__ __forceinline__ unsigned ellipse_rows(const ChunkBuf &B, int e, int o
     const double R = -2.0 * (cp.y - kCullMarginPower);
     const double a = -2.0 * ab.x, c = -2.0 * cp.x, b = ab.y;
     const double det = a * c - b * b;
-    const bool full = !(a > 0.0 && c > 0.0 && det > 1e-4 * (a * c) && isfinite(R) && isfinite(det));
+    const bool full = !(a > 1e-280 && c > 1e-280 && a < 1e280 && c < 1e280 &&
+                        det > 1e-4 * (a * c) && det > 1e-280 && isfinite(R) && isfinite(det));
     const unsigned cols = (0xFFu >> (7 - c1)) & (0xFFu << c0);
     if (full) {
         const unsigned rows = (0xFFFFFFFFu >> (8 * (3 - r1))) & (0xFFFFFFFFu << (8 * r0));
         return (cols * 0x01010101u) & rows;
     }
     if (!(R > 0.0)) return 0u;
-    const double inv_a = 1.0 / a, aR = a * R;
+    const double inv_a = rcp_nr(a), aR = a * R;  // conservative use: Newton reciprocal
     unsigned w = 0u;
     for (int r = r0; r <= r1; r++) {
         const double dy = (double)(oy + r) + 0.5 - m.y;
