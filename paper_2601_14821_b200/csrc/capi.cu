@@ -34,7 +34,7 @@ struct potr_ctx {
     // per-view workspace
     // dup_id: record of each duplicated pair; perm: tile-sorted slot order;
     // pair: per sorted pair (slot, record)
-    DevBuf rec, key, skey, sids, cnt, cnt_sorted, offs, iota, tkey, tskey, perm, pair, dup_id,
+    DevBuf rec, key, skey, sids, cnt, offs, iota, tkey, tskey, perm, pair, dup_id,
         dup_rank,
         partial, ranges, tile_se, temp, nvalid;
     int64_t iota_len = 0;
@@ -374,7 +374,6 @@ int bin_batch(potr_ctx *ctx, const potr_splats &sp, const potr_camera *cams, int
     ENSURE(ctx->sids, sizeof(int32_t) * total);
     ENSURE(ctx->vidx, sizeof(int32_t) * total);
     ENSURE(ctx->cnt, sizeof(int32_t) * total);
-    ENSURE(ctx->cnt_sorted, sizeof(int64_t) * total);
     ENSURE(ctx->offs, sizeof(int64_t) * (total + 1));
     ENSURE(ctx->ranges, sizeof(int2) * ntiles_b);
     ENSURE(ctx->tile_se, sizeof(double) * (ntiles_b + kMaxViewBatch));  // + per-view MSE
@@ -469,9 +468,9 @@ int bin_batch(potr_ctx *ctx, const potr_splats &sp, const potr_camera *cams, int
     }
     {
         Stage _st(ctx, POTR_STAGE_SCAN);
-        LAUNCH(1, scan_counts(ctx->temp.p, ctx->temp.cap, P<int32_t>(ctx->sids),
-                              P<int32_t>(ctx->cnt), P<int64_t>(ctx->cnt_sorted),
-                              P<int64_t>(ctx->offs), total, n, ctx->stream));
+        // CUB scan (its input iterator gathers the counts in depth order)
+        CK(scan_counts(ctx->temp.p, ctx->temp.cap, P<int32_t>(ctx->sids), P<int32_t>(ctx->cnt),
+                       P<int64_t>(ctx->offs), total, ctx->stream));
         _st.end();
     }
     CK(cudaMemcpyAsync(ctx->pinned, P<int64_t>(ctx->offs) + total, sizeof(int64_t),
@@ -668,7 +667,7 @@ void potr_destroy(potr_ctx *ctx) {
     cudaSetDevice(ctx->device);
     cudaStreamSynchronize(ctx->stream);
     DevBuf *bufs[] = {&ctx->rec,     &ctx->key,     &ctx->skey,    &ctx->sids,   &ctx->cnt,
-                      &ctx->cnt_sorted, &ctx->offs, &ctx->iota,    &ctx->tkey,   &ctx->tskey,
+                      &ctx->offs, &ctx->iota,    &ctx->tkey,   &ctx->tskey,
                       &ctx->pair,    &ctx->dup_id,  &ctx->dup_rank, &ctx->partial, &ctx->ranges,
                       &ctx->perm,
                       &ctx->tile_se, &ctx->temp,    &ctx->nvalid,  &ctx->rkey,   &ctx->rskey,

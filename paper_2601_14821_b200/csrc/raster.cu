@@ -9,7 +9,7 @@
 //  (b) depth order: CUB sort of the 32-bit hi part of the depth key +
 //      k_depth_fixup (runs of equal hi ordered by the full key) -- stable, so
 //      ties keep ascending splat id == np.argsort(kind="stable") (:248-250);
-//      k_gather_counts + CUB scan, k_duplicate (pairs in depth order, tiles
+//      CUB scan of the counts in depth order, k_duplicate (pairs in depth order, tiles
 //      culled by the prefilter ellipse), CUB stable sort on 16-bit tile keys,
 //      k_tile_ranges: every tile gets its splats in (tile, depth, id) order.
 //  (c)+(d) k_raster    persistent warps, one warp per 8x4-pixel tile (lane =
@@ -25,6 +25,8 @@
 //      :340-347).
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
+#include <thrust/iterator/counting_iterator.h>
+#include <thrust/iterator/transform_iterator.h>
 
 #include "common.cuh"
 #include "raster.cuh"
@@ -308,11 +310,6 @@ __global__ void k_project_dump(potr_splats sp, Cam cam, double *mean2d, double *
 // (b) binning
 
 // Batch arrays are view-major: element (v, i) at v*n + i.
-__global__ void k_gather_counts(int64_t total, int64_t n, const int32_t *__restrict__ ids,
-                                const int32_t *__restrict__ cnt, int64_t *__restrict__ out) {
-    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i < total) out[i] = cnt[ids[i]];  // ids hold batch record indices v*n + k
-}
 
 // Emit the (tile, splat) pairs of every drawn splat, walking splats in depth
 // order so a stable sort on the tile key yields (tile, depth, id) order.
@@ -1338,18 +1335,29 @@ cudaError_t launch_bbox(int64_t n, const double *pos, unsigned long long *out, c
     return cudaGetLastError();
 }
 
-cudaError_t scan_counts(void *temp, size_t temp_bytes, const int32_t *ids, const int32_t *cnt,
-                        int64_t *cnt_sorted, int64_t *offs, int64_t total, int64_t n,
-                        cudaStream_t st) {
-    cudaError_t e = cudaMemsetAsync(offs, 0, sizeof(int64_t), st);
-    if (e != cudaSuccess || total == 0) return e;
-    k_gather_counts<<<grid_for(total, 256), 256, 0, st>>>(total, n, ids, cnt, cnt_sorted);
-    if ((e = cudaGetLastError()) != cudaSuccess) return e;
-    return cub::DeviceScan::InclusiveSum(temp, temp_bytes, cnt_sorted, offs + 1, (int)total, st);
+// cnt[ids[i]] as int64, read by the pair-offset scan (no gathered copy).
+struct GatherCount {
+    const int32_t *ids, *cnt;
+    __host__ __device__ __forceinline__ int64_t operator()(int64_t i) const {
+        return (int64_t)cnt[ids[i]];
+    }
+};
+using SortedCounts = thrust::transform_iterator<GatherCount, thrust::counting_iterator<int64_t>,
+                                                int64_t>;
+static SortedCounts sorted_counts(const int32_t *ids, const int32_t *cnt) {
+    return SortedCounts(thrust::counting_iterator<int64_t>(0), GatherCount{ids, cnt});
 }
 
+cudaError_t scan_counts(void *temp, size_t temp_bytes, const int32_t *ids, const int32_t *cnt,
+                        int64_t *offs, int64_t total, cudaStream_t st) {
+    cudaError_t e = cudaMemsetAsync(offs, 0, sizeof(int64_t), st);
+    if (e != cudaSuccess || total == 0) return e;
+    // the counts in sorted order come through the scan's input iterator
+    return cub::DeviceScan::InclusiveSum(temp, temp_bytes, sorted_counts(ids, cnt), offs + 1,
+                                         (int)total, st);
+}
 cudaError_t scan_temp(int64_t n, size_t *bytes) {
-    return cub::DeviceScan::InclusiveSum((void *)nullptr, *bytes, (const int64_t *)nullptr,
+    return cub::DeviceScan::InclusiveSum((void *)nullptr, *bytes, sorted_counts(nullptr, nullptr),
                                          (int64_t *)nullptr, (int)n);
 }
 

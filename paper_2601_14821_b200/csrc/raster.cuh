@@ -96,8 +96,7 @@ cudaError_t depth_sort(void *temp, size_t temp_bytes, uint64_t *key_a, uint64_t 
                        cudaStream_t st);
 cudaError_t scan_temp(int64_t n, size_t *bytes);
 cudaError_t scan_counts(void *temp, size_t temp_bytes, const int32_t *ids, const int32_t *cnt,
-                        int64_t *cnt_sorted, int64_t *offs, int64_t total, int64_t n,
-                        cudaStream_t st);
+                        int64_t *offs, int64_t total, cudaStream_t st);
 cudaError_t launch_duplicate(int64_t total, int64_t n, const int32_t *ids, const int64_t *offs,
                              const SplatRec *rec, const TileSpan *spans, int tiles_x, int ntiles,
                              int sb, bool key16, int cull, void *tkey, int32_t *dup_id,
