@@ -470,8 +470,12 @@ def e2e_measure(args, rank, world, local, pert, cams, tg, S, Pv, dev):
         call = lambda: rasterizer.forward_stats(host, cams, targets)  # noqa: E731
     else:
         call = lambda: distributed.forward_stats_sharded(host, cams, targets)  # noqa: E731
-    for _ in range(max(1, args.warmup)):
-        call()
+    # warm-up mirrors the timed loop: the previous result stays alive while
+    # the next call runs (its device buffers, e.g. the (S, N) camera
+    # importance, are then already in torch's caching allocator)
+    st = None
+    for _ in range(max(2, args.warmup)):
+        st = call()
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
