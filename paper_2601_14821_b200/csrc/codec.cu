@@ -276,21 +276,6 @@ __global__ void k_attr_emit(int64_t m, const uint64_t *__restrict__ val,
 
 // ---------------------------------------------------------------------------
 
-struct CodecScratch {
-    void *p = nullptr;
-    size_t cap = 0;
-};
-
-static cudaError_t grow(CodecScratch &b, size_t bytes) {
-    if (b.cap >= bytes) return cudaSuccess;
-    if (b.p) cudaFree(b.p);
-    b.p = nullptr;
-    b.cap = 0;
-    cudaError_t e = cudaMalloc(&b.p, bytes);
-    if (e == cudaSuccess) b.cap = bytes;
-    return e;
-}
-
 #define CODEC_CK(x)                          \
     do {                                     \
         cudaError_t _e = (x);                \
