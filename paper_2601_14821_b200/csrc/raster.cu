@@ -1,25 +1,28 @@
 // raster.cu -- the prune-score pass on sm_100a: kernels (a)-(d).  All work is
-// done for a batch of up to 8 equal-size views at a time.
+// done for a batch of up to 8 equal-size views at a time, in "slot space":
+// once per call the splats are ordered by the Morton code of their centres
+// (k_morton + CUB sort) and copied in that order with their view-independent
+// terms (k_splat_slots), so that the records a tile reads are close together
+// in HBM; slots map back to splat indices where results leave (raster.cuh).
 //
-//  (a) k_splat_prep    view-independent Sigma and prefilter threshold, once per
-//                      call; k_preprocess: one thread per (splat, view): EWA
-//                      projection, cov2d, radius, clipped bbox, conic, SH
-//                      colour, compact depth key, culled tile count
-//                      (rasterizer.py:56-110, :135-154)
+//  (a) k_preprocess: one thread per (slot, view): EWA projection, cov2d,
+//      radius, clipped bbox, conic, SH colour, compact depth key, culled tile
+//      rows and count (rasterizer.py:56-110, :135-154)
 //  (b) depth order: CUB sort of the 32-bit hi part of the depth key +
-//      k_depth_fixup (runs of equal hi ordered by the full key) -- stable, so
-//      ties keep ascending splat id == np.argsort(kind="stable") (:248-250);
-//      CUB scan of the counts in depth order, k_duplicate (pairs in depth order, tiles
-//      culled by the prefilter ellipse), CUB stable sort on 16-bit tile keys,
+//      k_depth_fixup (runs of equal hi ordered by the full key, exact ties by
+//      splat index) == np.argsort(kind="stable") (:248-250); CUB scan of the
+//      counts in depth order, k_duplicate (pairs in depth order, tiles culled
+//      by the prefilter ellipse), CUB stable sort on 16-bit tile keys,
 //      k_tile_ranges: every tile gets its splats in (tile, depth, id) order.
 //  (c)+(d) k_raster    persistent warps, one warp per 8x4-pixel tile (lane =
 //      pixel).  Pass 1 composites front to back with the reference's exact
 //      per-pixel rules (:159-201), each lane walking only the chunk entries
-//      that cover its pixel; the replay revisits the composited samples and
-//      evaluates the closed-form removal delta PD = a/(1-a) (P_K - P_i - T c)
-//      (:232-243), dSE = sum_ch PD^2 + 2 PD (c - c_t) (:333) and T*alpha
-//      (:228), adding them per (tile, splat) slot in a fixed lane order -- no
-//      floating-point atomics, so scores are bit-reproducible.
+//      whose bbox and prefilter ellipse reach its pixel; the replay revisits
+//      the composited samples and evaluates the closed-form removal delta
+//      PD = a/(1-a) (P_K - P_i - T c) (:232-243), dSE = sum_ch PD^2 +
+//      2 PD (c - c_t) (:333) and T*alpha (:228), adding them per (tile,
+//      splat) slot in a fixed lane order -- no floating-point atomics, so
+//      scores are bit-reproducible.
 //  k_splat_reduce / k_view_accumulate / k_mse_reduce: per splat, its slots in
 //      tile order, divided by P / 3P, added in camera order (:226-230, :334,
 //      :340-347).
