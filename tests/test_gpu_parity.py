@@ -140,6 +140,10 @@ def test_spatial_records_bit_identical(R, oracle):
     stack = splats.copy()
     for f in ("positions", "scales", "rotations", "sh", "opacities"):
         getattr(stack, f)[200:300] = getattr(stack, f)[50]
+    # every centre at one point: zero extent for the Morton code, one run of
+    # equal depths across the whole view
+    point = splats.copy()
+    point.positions[:] = point.positions[7]
     ctx = device.context()
 
     def run(sc):
@@ -151,7 +155,7 @@ def test_spatial_records_bit_identical(R, oracle):
     try:
         for on in (0, 1):
             ctx.call("potr_set_option", _native.OPT_SPATIAL_RECORDS, on)
-            outs[on] = [run(splats), run(tied), run(stack)]
+            outs[on] = [run(splats), run(tied), run(stack), run(point)]
     finally:
         ctx.call("potr_set_option", _native.OPT_SPATIAL_RECORDS, 1)
     for (st0, rec0, tl0), (st1, rec1, tl1) in zip(outs[0], outs[1]):
@@ -164,7 +168,7 @@ def test_spatial_records_bit_identical(R, oracle):
             assert np.array_equal(getattr(rec0, f), getattr(rec1, f)), f
         for a, b in zip(tl0, tl1):
             assert np.array_equal(a, b)
-    for sc, out in ((tied, outs[1][1]), (stack, outs[1][2])):
+    for sc, out in ((tied, outs[1][1]), (stack, outs[1][2]), (point, outs[1][3])):
         order, off, lst = out[2]
         assert np.array_equal(order, oracle.depth_order(sc, cams[0]))
         o_off, o_lst = oracle.tile_lists(sc, cams[0])
