@@ -1158,6 +1158,40 @@ cudaError_t depth_sort(void *temp, size_t temp_bytes, uint64_t *key_a, uint64_t 
     return e;
 }
 
+// The depth sort's onesweep policy: CUB's sm_100 tuning for 32-bit keys with
+// 4-byte values (23 items per thread, 109 registers: one 384-thread block per
+// SM) measured 26.0 ms per C3 step; 20 items 21.0 ms (12: 25.8, 16: 22.7,
+// 22: 20.9, 20 x 256 threads: 21.4).  The tile sort's CUB tuning (512 x 17
+// for 16-bit keys) measured best among 384 x 16, 256 x 20, 512 x 12, 384 x 23.
+#ifndef POTR_DSORT_ITEMS
+#define POTR_DSORT_ITEMS 20
+#endif
+#ifndef POTR_DSORT_THREADS
+#define POTR_DSORT_THREADS 384
+#endif
+struct DepthSortHub {
+    using P1000 = cub::detail::radix::policy_hub<uint32_t, int32_t, uint32_t>::Policy1000;
+    struct Policy : cub::ChainedPolicy<1000, Policy, Policy> {
+        static constexpr bool ONESWEEP = true;
+        static constexpr int ONESWEEP_RADIX_BITS = 8;
+        using HistogramPolicy = P1000::HistogramPolicy;
+        using ExclusiveSumPolicy = P1000::ExclusiveSumPolicy;
+        using OnesweepPolicy = cub::AgentRadixSortOnesweepPolicy<
+            POTR_DSORT_THREADS, POTR_DSORT_ITEMS, uint32_t, 1, cub::RADIX_RANK_MATCH_EARLY_COUNTS_ANY,
+            cub::BLOCK_SCAN_RAKING_MEMOIZE, cub::RADIX_SORT_STORE_DIRECT, 8>;
+        using ScanPolicy = P1000::ScanPolicy;
+        using DownsweepPolicy = P1000::DownsweepPolicy;
+        using AltDownsweepPolicy = P1000::AltDownsweepPolicy;
+        using UpsweepPolicy = P1000::UpsweepPolicy;
+        using AltUpsweepPolicy = P1000::AltUpsweepPolicy;
+        using SingleTilePolicy = P1000::SingleTilePolicy;
+        using SegmentedPolicy = P1000::SegmentedPolicy;
+        using AltSegmentedPolicy = P1000::AltSegmentedPolicy;
+    };
+    using MaxPolicy = Policy;
+};
+using DepthSortDispatch = cub::DispatchRadixSort<false, uint32_t, int32_t, uint32_t, DepthSortHub>;
+
 cudaError_t depth_sort32(void *temp, size_t temp_bytes, uint32_t *key_a, uint32_t *key_b,
                          int32_t *val_a, int32_t *val_b, int64_t n, int end_bit, bool *in_alt,
                          cudaStream_t st) {
@@ -1165,7 +1199,8 @@ cudaError_t depth_sort32(void *temp, size_t temp_bytes, uint32_t *key_a, uint32_
     if (n == 0) return cudaSuccess;
     cub::DoubleBuffer<uint32_t> k(key_a, key_b);
     cub::DoubleBuffer<int32_t> v(val_a, val_b);
-    cudaError_t e = cub::DeviceRadixSort::SortPairs(temp, temp_bytes, k, v, (int)n, 0, end_bit, st);
+    size_t bytes = temp_bytes;
+    cudaError_t e = DepthSortDispatch::Dispatch(temp, bytes, k, v, (uint32_t)n, 0, end_bit, true, st);
     *in_alt = k.Current() == key_b;
     return e;
 }
@@ -1173,7 +1208,7 @@ cudaError_t depth_sort32(void *temp, size_t temp_bytes, uint32_t *key_a, uint32_
 cudaError_t depth_sort32_temp(int64_t n, size_t *bytes) {
     cub::DoubleBuffer<uint32_t> k(nullptr, nullptr);
     cub::DoubleBuffer<int32_t> v(nullptr, nullptr);
-    return cub::DeviceRadixSort::SortPairs((void *)nullptr, *bytes, k, v, (int)n, 0, 32);
+    return DepthSortDispatch::Dispatch(nullptr, *bytes, k, v, (uint32_t)n, 0, 32, true, nullptr);
 }
 
 // One thread per sorted position; the first position of each run of equal hi
