@@ -753,3 +753,41 @@ def test_codec_bytes_match_reference(C):
                                               camera_eyes=eyes)
         assert np.array_equal(order2, order)
         assert data == g[f"container_{i}"].tobytes(), f"case {i}: container"
+
+
+def test_full_size_properties(R, oracle):
+    """At the C3 shape (3M splats, 1237x822 views): depth order and tile lists
+    equal the oracle's; per-camera importance telescopes to the rendered
+    coverage (sum_k I_k(s) = mean over pixels of 1 - T_final); self-target
+    scores are non-negative with zero MSE; and the spatial record layout
+    changes no bit."""
+    from paper_2601_14821_b200 import _native, binning, device
+    from paper_2601_14821_b200.fixture import config_scene
+    splats, cams = config_scene("C3")
+    views = [cams[0], cams[101]]
+    order, off, lst = binning.tile_lists(splats, views[0])
+    assert np.array_equal(order, oracle.depth_order(splats, views[0]))
+    o_off, o_lst = oracle.tile_lists(splats, views[0])
+    assert np.array_equal(off, o_off) and np.array_equal(lst, o_lst)
+
+    ctx = device.context()
+    dev = device.current_device()
+    ds = device.DeviceSplats.from_host(splats, dev)
+    imp, ci, _, _ = R.forward_stats_device(ds, views, None)
+    for s, cam in enumerate(views):
+        _, trans = R._render_device(ds, cam, ctx, dev, with_trans=True)
+        coverage = float((1.0 - trans).mean())
+        assert abs(float(ci[s].sum()) - coverage) <= 1e-10 * coverage
+
+    imgs, imp2, ci2, dm, mse = R.render_and_score_device(ds, views)
+    assert float(mse.item()) == 0.0
+    assert bool((dm >= 0).all())
+    assert np.array_equal(imp.cpu().numpy(), imp2.cpu().numpy())
+
+    try:
+        ctx.call("potr_set_option", _native.OPT_SPATIAL_RECORDS, 0)
+        imp3, ci3, _, _ = R.forward_stats_device(ds, views, None)
+    finally:
+        ctx.call("potr_set_option", _native.OPT_SPATIAL_RECORDS, 1)
+    assert np.array_equal(imp.cpu().numpy(), imp3.cpu().numpy())
+    assert np.array_equal(ci.cpu().numpy(), ci3.cpu().numpy())
