@@ -791,3 +791,25 @@ def test_full_size_properties(R, oracle):
         ctx.call("potr_set_option", _native.OPT_SPATIAL_RECORDS, 1)
     assert np.array_equal(imp.cpu().numpy(), imp3.cpu().numpy())
     assert np.array_equal(ci.cpu().numpy(), ci3.cpu().numpy())
+
+
+def test_full_size_sh_recompute_vs_oracle(R, C, oracle):
+    """SH recompute at the C4 shape (3M splats, 200 views at 1237x822): the
+    device's coefficients for a random sample of 1500 splats equal the
+    oracle's from the same camera-importance columns, at two lambdas."""
+    from paper_2601_14821_b200.fixture import config_scene
+    from paper_2601_14821_b200.scene import Splats
+    splats, cams = config_scene("C3")
+    imp, ci = R.compute_importance(splats, cams)
+    rng = np.random.default_rng(11)
+    idx = np.sort(rng.choice(len(splats.positions), 1500, replace=False))
+    sub = Splats(*(np.ascontiguousarray(np.asarray(getattr(splats, f))[idx]) for f in
+                   ("positions", "sh", "opacities", "scales", "rotations")))
+    ci_sub = np.ascontiguousarray(np.asarray(ci)[:, idx])
+    for lam in (1e-7, 1e-9):
+        cfg = C.CompactionConfig(lam, 0.8175744761936437, 0.5 / 51.0)
+        _, yc, rep = C.compact_scene(splats, cams, ci, cfg)
+        _, yc_o, st_o = oracle.compact(sub, cams, ci_sub, lam, 0.8175744761936437, 0.5 / 51.0,
+                                       threads=8)
+        assert np.array_equal(yc[idx] == 0.0, yc_o == 0.0)
+        np.testing.assert_allclose(yc[idx], yc_o, rtol=0, atol=1e-9)
