@@ -813,3 +813,20 @@ def test_full_size_sh_recompute_vs_oracle(R, C, oracle):
                                        threads=8)
         assert np.array_equal(yc[idx] == 0.0, yc_o == 0.0)
         np.testing.assert_allclose(yc[idx], yc_o, rtol=0, atol=1e-9)
+
+
+def test_full_size_delta_mse_vs_oracle(R, oracle):
+    """The removal-effect scores of one full C3 view (3M splats, 1237x822,
+    opacities x 0.97 against the unperturbed render) equal the oracle's for
+    every splat: importance to 1e-12, dMSE to 1e-9 relative."""
+    from paper_2601_14821_b200.fixture import config_scene
+    splats, cams = config_scene("C3")
+    view = [cams[57]]
+    targets = R.render_targets(splats, view)
+    pert = splats.copy()
+    pert.opacities = pert.opacities * 0.97
+    st = R.compute_delta_mse(pert, view, targets)
+    imp, ci, dm, mse = oracle.forward_stats(pert, view, [np.asarray(t) for t in targets])
+    np.testing.assert_allclose(st.importance, imp, rtol=1e-12, atol=1e-20)
+    np.testing.assert_allclose(st.delta_mse, dm, rtol=1e-9, atol=1e-22)
+    assert abs(st.mse - mse) <= 1e-12 * abs(mse)
