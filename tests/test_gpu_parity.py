@@ -283,14 +283,16 @@ def test_prune_mask_bit_exact_and_psnr(R):
         assert abs(psnr(ours, targets[s]) - psnr(ref, g["targets"][s])) <= 0.01
 
 
-def test_prune_device_controller_matches_host_controller(R, monkeypatch):
+@pytest.mark.parametrize("config,q,iters", [("C1", 0.9, 6), ("C2", 0.5, 8)])
+def test_prune_device_controller_matches_host_controller(R, monkeypatch, config, q, iters):
     """The device-resident controller (splats subset in HBM, GPU stable sort)
     and the host controller over the same GPU scores give identical reports,
-    kept sets and pruned splats, on a scene with many removals per iteration."""
+    kept sets and pruned splats, on a scene with many removals per iteration
+    (C1) and at the C2 shape (300k splats, 100 views at 800x800)."""
     from paper_2601_14821_b200 import pruning, fixture
-    splats, cams = fixture.config_scene("C1")
+    splats, cams = fixture.config_scene(config)
     targets = R.render_targets(splats, cams)
-    cfg = pruning.PruneConfig(delta_mse_max=10.0 ** (-8.8 - 2.0 * 0.9), iterations=6)
+    cfg = pruning.PruneConfig(delta_mse_max=10.0 ** (-8.8 - 2.0 * q), iterations=iters)
     assert pruning._device_scorer_active()
     dev = pruning.run_pruning(splats, cams, targets, cfg)
     monkeypatch.setattr(pruning, "compute_delta_mse",
