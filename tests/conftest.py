@@ -1,3 +1,4 @@
+import functools
 import hashlib
 import os
 import sys
@@ -53,6 +54,14 @@ def sh_scene():
     splats = Splats(*(np.concatenate([getattr(splats, f), getattr(extra, f)]) for f in
                       ("positions", "sh", "opacities", "scales", "rotations")))
     return splats, cams
+
+
+@functools.lru_cache(maxsize=1)
+def c3_scene():
+    """The C3-shaped synthetic scene (3M splats, 200 views at 1237x822),
+    generated once per session; callers must not modify it."""
+    from paper_2601_14821_b200.fixture import config_scene
+    return config_scene("C3")
 
 
 def oracle_scene(seed):

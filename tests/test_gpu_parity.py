@@ -9,7 +9,8 @@ within 1e-4 absolute; PSNR after pruning within 0.01 dB.
 import numpy as np
 import pytest
 
-from tests.conftest import (golden, oracle_scene, perturbed, score_close, sh_scene, small_scene)
+from tests.conftest import (c3_scene, golden, oracle_scene, perturbed, score_close, sh_scene,
+                            small_scene)
 
 pytestmark = pytest.mark.gpu
 
@@ -764,8 +765,7 @@ def test_full_size_properties(R, oracle):
     scores are non-negative with zero MSE; and the spatial record layout
     changes no bit."""
     from paper_2601_14821_b200 import _native, binning, device
-    from paper_2601_14821_b200.fixture import config_scene
-    splats, cams = config_scene("C3")
+    splats, cams = c3_scene()
     views = [cams[0], cams[101]]
     order, off, lst = binning.tile_lists(splats, views[0])
     assert np.array_equal(order, oracle.depth_order(splats, views[0]))
@@ -799,9 +799,8 @@ def test_full_size_sh_recompute_vs_oracle(R, C, oracle):
     """SH recompute at the C4 shape (3M splats, 200 views at 1237x822): the
     device's coefficients for a random sample of 1500 splats equal the
     oracle's from the same camera-importance columns, at two lambdas."""
-    from paper_2601_14821_b200.fixture import config_scene
     from paper_2601_14821_b200.scene import Splats
-    splats, cams = config_scene("C3")
+    splats, cams = c3_scene()
     imp, ci = R.compute_importance(splats, cams)
     rng = np.random.default_rng(11)
     idx = np.sort(rng.choice(len(splats.positions), 1500, replace=False))
@@ -821,8 +820,7 @@ def test_full_size_delta_mse_vs_oracle(R, oracle):
     """The removal-effect scores of one full C3 view (3M splats, 1237x822,
     opacities x 0.97 against the unperturbed render) equal the oracle's for
     every splat: importance to 1e-12, dMSE to 1e-9 relative."""
-    from paper_2601_14821_b200.fixture import config_scene
-    splats, cams = config_scene("C3")
+    splats, cams = c3_scene()
     view = [cams[57]]
     targets = R.render_targets(splats, view)
     pert = splats.copy()
