@@ -50,6 +50,10 @@ constexpr int kShWarps = 4;
 // w*y (16) + w*YCoCg (3), padded for the 2x4 blocks' 16-byte loads
 constexpr int kShRow = POTR_SH_ROW;
 constexpr int kShBlocks = 28;
+#ifndef POTR_SH_UNROLL
+#define POTR_SH_UNROLL 4
+#endif
+constexpr int kShUnroll = POTR_SH_UNROLL;
 
 // Block b of the tiling: rows 2r, 2r+1; columns c0 .. c0+3 (c0 = 2r + 4t).
 __device__ __forceinline__ void sh_block(int b, int *r, int *c0) {
@@ -80,7 +84,9 @@ __global__ void __launch_bounds__(32 * kShWarps, POTR_SH_MIN_BLOCKS) k_sh_accumu
                                                        const double *__restrict__ cam_imp,
                                                        double *__restrict__ neq) {
     __shared__ double wtile[32][kShSplatsPerBlock + 1];
-    __shared__ __align__(16) double A[kShWarps][32][kShRow];
+    // row 32 of each warp's tile is a zero row: the unrolled accumulation pads
+    // with it (fma(0, 0, acc) == acc exactly, acc is never -0)
+    __shared__ __align__(16) double A[kShWarps][33][kShRow];
     __shared__ double shs[kShSplatsPerBlock][48];
     __shared__ double pos[kShSplatsPerBlock][3];
     const int64_t n = sp.n;
@@ -91,7 +97,7 @@ __global__ void __launch_bounds__(32 * kShWarps, POTR_SH_MIN_BLOCKS) k_sh_accumu
         shs[i / 48][i % 48] = sp.sh[(k0 + i / 48) * 48 + i % 48];
     for (int i = threadIdx.x; i < nk * 3; i += blockDim.x)
         pos[i / 3][i % 3] = sp.positions[(k0 + i / 3) * 3 + i % 3];
-    for (int i = threadIdx.x; i < kShWarps * 32 * kShRow; i += blockDim.x)
+    for (int i = threadIdx.x; i < kShWarps * 33 * kShRow; i += blockDim.x)
         (&A[0][0][0])[i] = 0.0;  // the pad columns stay zero
 
     int br = 0, bc = 0;
@@ -151,19 +157,33 @@ __global__ void __launch_bounds__(32 * kShWarps, POTR_SH_MIN_BLOCKS) k_sh_accumu
             }
             __syncwarp();
             if (owner) {
-                for (unsigned m = seen_mask; m; m &= m - 1u) {
-                    const int v = __ffs(m) - 1;
-                    const double2 a = *reinterpret_cast<const double2 *>(&A[w][v][2 * br]);
-                    const double2 b01 = *reinterpret_cast<const double2 *>(&A[w][v][bc]);
-                    const double2 b23 = *reinterpret_cast<const double2 *>(&A[w][v][bc + 2]);
-                    acc[j][0] = fma(a.x, b01.x, acc[j][0]);
-                    acc[j][1] = fma(a.x, b01.y, acc[j][1]);
-                    acc[j][2] = fma(a.x, b23.x, acc[j][2]);
-                    acc[j][3] = fma(a.x, b23.y, acc[j][3]);
-                    acc[j][4] = fma(a.y, b01.x, acc[j][4]);
-                    acc[j][5] = fma(a.y, b01.y, acc[j][5]);
-                    acc[j][6] = fma(a.y, b23.x, acc[j][6]);
-                    acc[j][7] = fma(a.y, b23.y, acc[j][7]);
+                // kShUnroll seen views per step, ascending (the zero row pads
+                // the last step): their shared loads issue together
+                for (unsigned m = seen_mask; m;) {
+                    int vv[kShUnroll];
+#pragma unroll
+                    for (int u = 0; u < kShUnroll; u++) {
+                        vv[u] = m ? __ffs(m) - 1 : 32;
+                        m &= m - 1u;
+                    }
+                    double2 a[kShUnroll], b01[kShUnroll], b23[kShUnroll];
+#pragma unroll
+                    for (int u = 0; u < kShUnroll; u++) {
+                        a[u] = *reinterpret_cast<const double2 *>(&A[w][vv[u]][2 * br]);
+                        b01[u] = *reinterpret_cast<const double2 *>(&A[w][vv[u]][bc]);
+                        b23[u] = *reinterpret_cast<const double2 *>(&A[w][vv[u]][bc + 2]);
+                    }
+#pragma unroll
+                    for (int u = 0; u < kShUnroll; u++) {
+                        acc[j][0] = fma(a[u].x, b01[u].x, acc[j][0]);
+                        acc[j][1] = fma(a[u].x, b01[u].y, acc[j][1]);
+                        acc[j][2] = fma(a[u].x, b23[u].x, acc[j][2]);
+                        acc[j][3] = fma(a[u].x, b23[u].y, acc[j][3]);
+                        acc[j][4] = fma(a[u].y, b01[u].x, acc[j][4]);
+                        acc[j][5] = fma(a[u].y, b01[u].y, acc[j][5]);
+                        acc[j][6] = fma(a[u].y, b23[u].x, acc[j][6]);
+                        acc[j][7] = fma(a[u].y, b23[u].y, acc[j][7]);
+                    }
                 }
             }
             __syncwarp();
