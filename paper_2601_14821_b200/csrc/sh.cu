@@ -42,7 +42,10 @@ __constant__ double kYcocgToRgb[9] = {1.0, 1.0, -1.0, 1.0, 0.0, 1.0, 1.0, -1.0, 
 #ifndef POTR_SH_MIN_BLOCKS
 #define POTR_SH_MIN_BLOCKS 4
 #endif
-constexpr int kShSplatsPerBlock = 16;
+#ifndef POTR_SH_SPLATS
+#define POTR_SH_SPLATS 16
+#endif
+constexpr int kShSplatsPerBlock = POTR_SH_SPLATS;
 constexpr int kShWarps = 4;
 #ifndef POTR_SH_ROW
 #define POTR_SH_ROW 26
@@ -237,34 +240,44 @@ __device__ void chol_solve(const double *U, int m, double *b) {
     }
 }
 
-// _solve_channel (compaction.py:127-148) on the normal equations.
-// Returns 0 ok, 1 ok after jitter, -1 RidgeError.
-__device__ int solve_channel(const double *G, const double *B, int ch, const bool *mask,
-                             double lam, double *out) {
-    int cols[16];
+// _solve_channel (compaction.py:127-148) on the normal equations, split into
+// the factorisation of A = G[c, c] + lam I (no lam on DC) and the solve for one
+// channel's right-hand side, so channels that share (mask, lam) share the
+// factor.  factor_channel returns 0 ok, 1 ok after the 1e-10 jitter, -1
+// RidgeError; the retry rebuilds A from G (the same values the reference's
+// retry starts from).
+__device__ int factor_channel(const double *__restrict__ G, int64_t gs, unsigned mask, double lam,
+                              double *A, int *cols, int *mout) {
     int m = 0;
     for (int i = 0; i < 16; i++)
-        if (mask[i]) cols[m++] = i;
-    double A[136], Asave[136], b[16];
-    for (int i = 0; i < m; i++) {
-        for (int j = i; j < m; j++) A[tri(i, j)] = G[tri(cols[i], cols[j])];
-        A[tri(i, i)] += (cols[i] == 0) ? 0.0 : lam;
-        b[i] = B[cols[i] * 3 + ch];
+        if (mask >> i & 1u) cols[m++] = i;
+    *mout = m;
+    for (int attempt = 0; attempt < 2; attempt++) {
+        for (int i = 0; i < m; i++) {
+            for (int j = i; j < m; j++) A[tri(i, j)] = __ldg(G + tri(cols[i], cols[j]) * gs);
+            A[tri(i, i)] += (cols[i] == 0) ? 0.0 : lam;
+            if (attempt) A[tri(i, i)] += 1e-10;
+        }
+        if (!chol_upper(A, m)) return attempt;
     }
-    for (int i = 0; i < m; i++)
-        for (int j = i; j < m; j++) Asave[tri(i, j)] = A[tri(i, j)];
-    int status = 0;
-    if (chol_upper(A, m)) {
-        for (int i = 0; i < m; i++)
-            for (int j = i; j < m; j++) A[tri(i, j)] = Asave[tri(i, j)];
-        for (int i = 0; i < m; i++) A[tri(i, i)] += 1e-10;
-        if (chol_upper(A, m)) return -1;
-        status = 1;
-    }
+    return -1;
+}
+
+__device__ void solve_factored(const double *A, int m, const int *cols,
+                               const double *__restrict__ B, int64_t gs, int ch, double *out) {
+    double b[16];
+    for (int i = 0; i < m; i++) b[i] = __ldg(B + (cols[i] * 3 + ch) * gs);
     chol_solve(A, m, b);
     for (int i = 0; i < 16; i++) out[i] = 0.0;
     for (int i = 0; i < m; i++) out[cols[i]] = b[i];
-    return status;
+}
+
+// pass-2 mask: drop AC columns whose pass-1 coefficient is below the threshold
+__device__ unsigned pass2_mask(unsigned mask, const double *first, double zero_thr) {
+    unsigned m2 = mask;
+    for (int i = 1; i < 16; i++)
+        if (fabs(first[i]) < zero_thr) m2 &= ~(1u << i);
+    return m2;
 }
 
 __device__ void coeffs_convert(const double *M, const double *in, double *out) {
@@ -308,42 +321,53 @@ __global__ void __launch_bounds__(128) k_sh_solve(potr_splats sp, const double *
         coeffs_convert(kRgbToYcocg, rgb, yc);
         status = 3;
     } else {
-        double G[136], B[48];
-        for (int e = 0; e < 136; e++) G[e] = neq[(int64_t)e * n + k];
-        for (int e = 0; e < 48; e++) B[e] = neq[(int64_t)(136 + e) * n + k];
+        // G (136, upper triangle) and B (48) read in place from the (185, N)
+        // layout: lane k's entry e is neq[e * n + k]
+        const double *G = neq + k, *B = neq + (int64_t)136 * n + k;
         // sparsify_parallel_columns (compaction.py:110-124)
         double norms[16];
-        for (int i = 0; i < 16; i++) norms[i] = sqrt(G[tri(i, i)]);
-        bool mask[16];
-        for (int i = 0; i < 16; i++) mask[i] = (i == 0);
+        for (int i = 0; i < 16; i++) norms[i] = sqrt(__ldg(G + tri(i, i) * n));
+        unsigned mask = 1u;
         for (int i = 1; i < 16; i++) {
             if (norms[i] == 0.0) continue;
             bool par = false;
             for (int j = 0; j < i; j++) {
-                if (!mask[j]) continue;
-                double gij = j < i ? G[tri(j, i)] : G[tri(i, j)];
+                if (!(mask >> j & 1u)) continue;
+                const double gij = __ldg(G + tri(j, i) * n);  // j < i
                 double cs = fabs(gij) / (norms[i] * norms[j]);
                 if (cs > par_thr) par = true;
             }
-            mask[i] = !par;
+            if (!par) mask |= 1u << i;
         }
-        const double lam[3] = {lambda_y, 3.0 * lambda_y, 3.0 * lambda_y};
+        // compact_splat (:169-192): per channel a pass-1 solve on the mask and a
+        // pass-2 re-solve without the small AC terms.  Co and Cg share lambda
+        // (3 lambda, :56-59) and the pass-1 mask, hence one pass-1 factor; a
+        // RidgeError anywhere keeps the original coefficients, so computing
+        // Cg's pass 1 before Co's pass 2 changes no output.
+        double Af[136], first[16], first2[16];
+        int cols[16], m, rc;
         for (int ch = 0; ch < 3 && status != 2; ch++) {
-            double first[16];
-            int rc = solve_channel(G, B, ch, mask, lam[ch], first);
+            if (ch < 2) {
+                rc = factor_channel(G, n, mask, ch == 0 ? lambda_y : 3.0 * lambda_y, Af, cols, &m);
+                if (rc < 0) {
+                    status = 2;
+                    break;
+                }
+                if (rc > 0) status = 1;
+                solve_factored(Af, m, cols, B, n, ch, first);
+                if (ch == 1) solve_factored(Af, m, cols, B, n, 2, first2);
+            } else {
+                for (int i = 0; i < 16; i++) first[i] = first2[i];
+            }
+            rc = factor_channel(G, n, pass2_mask(mask, first, zero_thr), ch == 0 ? lambda_y
+                                                                              : 3.0 * lambda_y,
+                                Af, cols, &m);
             if (rc < 0) {
                 status = 2;
                 break;
             }
             if (rc > 0) status = 1;
-            bool m2[16];
-            for (int i = 0; i < 16; i++) m2[i] = mask[i] && !(i > 0 && fabs(first[i]) < zero_thr);
-            rc = solve_channel(G, B, ch, m2, lam[ch], yc + ch * 16);
-            if (rc < 0) {
-                status = 2;
-                break;
-            }
-            if (rc > 0) status = 1;
+            solve_factored(Af, m, cols, B, n, ch, yc + ch * 16);
         }
         if (status == 2) {
             for (int i = 0; i < 48; i++) rgb[i] = sh[i];
