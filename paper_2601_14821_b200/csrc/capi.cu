@@ -615,13 +615,13 @@ int score_views_impl(potr_ctx *ctx, const potr_splats *sp, int ncam, const potr_
         {
             Stage _st(ctx, POTR_STAGE_REDUCE);
             LAUNCH(1, launch_splat_reduce(n * nb, n, P<int32_t>(ctx->sids), P<int64_t>(ctx->offs),
-                                          P<double2>(ctx->partial), g.P, P<double2>(ctx->ci_v),
-                                          ctx->stream));
+                                          P<double2>(ctx->partial), g.P, spatial_perm(ctx),
+                                          P<double2>(ctx->ci_v), ctx->stream));
             LAUNCH(1, launch_view_accumulate(n, nb, P<double2>(ctx->ci_v),
                                              cam_imp ? cam_imp + (int64_t)s * n : nullptr, imp_sum,
                                              targets ? dmse_sum : nullptr,
                                              dmse_rows ? dmse_rows + (int64_t)s * n : nullptr,
-                                             spatial_rank(ctx), ctx->stream));
+                                             ctx->stream));
             if (targets)
                 LAUNCH(2, launch_mse_reduce(nb, g.ntiles, P<double>(ctx->tile_se), g.P, mse_sum,
                                             mse_rows ? mse_rows + s : nullptr, ctx->stream));

@@ -938,7 +938,8 @@ __global__ void __launch_bounds__(256) k_splat_reduce(int64_t total, int64_t n,
                                                       const int32_t *__restrict__ ids,
                                                       const int64_t *__restrict__ offs,
                                                       const double2 *__restrict__ partial,
-                                                      double P, double2 *__restrict__ vals) {
+                                                      double P, const int32_t *__restrict__ perm,
+                                                      double2 *__restrict__ vals) {
     __shared__ double2 stage[8][kReduceStage];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const int64_t i0 = ((int64_t)blockIdx.x * 8 + w) * 32;
@@ -969,23 +970,28 @@ __global__ void __launch_bounds__(256) k_splat_reduce(int64_t total, int64_t n,
         }
     }
     if (!act) return;
-    // one 16-byte scatter per (view, record): (I_k(s), dMSE_k(s))
-    vals[g] = make_double2(imp / P, dse / (P * 3.0));
+    // one 16-byte scatter per (view, splat): (I_k(s), dMSE_k(s)), by splat id
+    // (perm: slot -> splat), so the view accumulation reads coalesced
+    int64_t out = g;
+    if (perm) {
+        const int64_t v = g / n;
+        out = v * n + perm[g - v * n];
+    }
+    vals[out] = make_double2(imp / P, dse / (P * 3.0));
 }
 
 // Camera-ordered accumulation over the views of the batch (rasterizer.py:343-347),
-// writing the camera_importance rows on the way (coalesced, by splat id).
+// writing the camera_importance rows on the way (all accesses coalesced, by
+// splat id: k_splat_reduce scattered the per-view sums by splat id).
 __global__ void k_view_accumulate(int64_t n, int nview, const double2 *__restrict__ vals,
                                   double *__restrict__ cam_imp_rows, double *__restrict__ imp_acc,
-                                  double *__restrict__ dmse_acc, double *__restrict__ dmse_rows,
-                                  const int32_t *__restrict__ rank) {
+                                  double *__restrict__ dmse_acc, double *__restrict__ dmse_rows) {
     const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (k >= n) return;
-    const int64_t r = rank ? rank[k] : k;  // splat k's record slot
     double ia = imp_acc[k];
     double da = dmse_acc ? dmse_acc[k] : 0.0;
     for (int v = 0; v < nview; v++) {
-        const double2 x = vals[(int64_t)v * n + r];
+        const double2 x = vals[(int64_t)v * n + k];  // by splat id (k_splat_reduce)
         if (cam_imp_rows) cam_imp_rows[(int64_t)v * n + k] = x.x;
         if (dmse_rows) dmse_rows[(int64_t)v * n + k] = x.y;
         ia += x.x;
@@ -1503,20 +1509,21 @@ cudaError_t launch_raster(int mode, const RasterArgs &a, int ntiles, cudaStream_
 }
 
 cudaError_t launch_splat_reduce(int64_t total, int64_t n, const int32_t *ids, const int64_t *offs,
-                                const double2 *partial, double P, double2 *vals,
-                                cudaStream_t st) {
+                                const double2 *partial, double P, const int32_t *perm,
+                                double2 *vals, cudaStream_t st) {
     if (total == 0) return cudaSuccess;
-    k_splat_reduce<<<grid_for(total, 256), 256, 0, st>>>(total, n, ids, offs, partial, P, vals);
+    k_splat_reduce<<<grid_for(total, 256), 256, 0, st>>>(total, n, ids, offs, partial, P, perm,
+                                                         vals);
     // (one warp per 32 entries, 8 warps per block: grid_for(total, 256) blocks)
     return cudaGetLastError();
 }
 
 cudaError_t launch_view_accumulate(int64_t n, int nview, const double2 *vals,
                                    double *cam_imp_rows, double *imp_acc, double *dmse_acc,
-                                   double *dmse_rows, const int32_t *rank, cudaStream_t st) {
+                                   double *dmse_rows, cudaStream_t st) {
     if (n == 0) return cudaSuccess;
     k_view_accumulate<<<grid_for(n, 256), 256, 0, st>>>(n, nview, vals, cam_imp_rows, imp_acc,
-                                                         dmse_acc, dmse_rows, rank);
+                                                         dmse_acc, dmse_rows);
     return cudaGetLastError();
 }
 

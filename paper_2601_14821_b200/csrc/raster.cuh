@@ -112,12 +112,12 @@ cudaError_t launch_tile_ranges(int64_t j0, int64_t K, bool key16, const void *sk
                                int tbase, cudaStream_t st);
 cudaError_t launch_raster(int mode, const RasterArgs &a, int ntiles, cudaStream_t st);
 cudaError_t launch_splat_reduce(int64_t total, int64_t n, const int32_t *ids, const int64_t *offs,
-                                const double2 *partial, double P, double2 *vals,
-                                cudaStream_t st);
+                                const double2 *partial, double P, const int32_t *perm,
+                                double2 *vals, cudaStream_t st);
 // dmse_rows / mse_rows (nullable): the per-view values as well as their sums
 cudaError_t launch_view_accumulate(int64_t n, int nview, const double2 *vals,
                                    double *cam_imp_rows, double *imp_acc, double *dmse_acc,
-                                   double *dmse_rows, const int32_t *rank, cudaStream_t st);
+                                   double *dmse_rows, cudaStream_t st);
 cudaError_t launch_mse_reduce(int nview, int ntiles, double *tile_se, double P,
                               double *mse_acc, double *mse_rows, cudaStream_t st);
 cudaError_t launch_finalize(int64_t n, int S, double *imp, double *dmse, double *mse,
