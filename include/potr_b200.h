@@ -155,7 +155,8 @@ int potr_bin(potr_ctx *ctx, const potr_splats *splats, const potr_camera *cam,
 /* compact_scene (compaction.py:195-243).  camera_importance (ncam,n) device.
  * Outputs rgb (n,3,16), ycocg (n,3,16) and status (n) int8:
  *   0 solved, 1 solved after the 1e-10 jitter retry (:140-145),
- *   2 RidgeError -> original coefficients kept, 3 unseen -> DC fallback. */
+ *   2 RidgeError -> original coefficients kept, 3 unseen -> DC fallback.
+ * rgb may be splats->sh itself (in-place update); ycocg must not overlap it. */
 int potr_compact(potr_ctx *ctx, const potr_splats *splats, int ncam, const potr_camera *cams,
                  const double *camera_importance, double lambda_y, double parallel_threshold,
                  double zero_threshold, double *rgb, double *ycocg, int8_t *status);

@@ -291,14 +291,15 @@ __device__ void coeffs_convert(const double *M, const double *in, double *out) {
 
 __global__ void __launch_bounds__(128) k_sh_solve(potr_splats sp, const double *__restrict__ neq,
                                                   double lambda_y, double par_thr,
-                                                  double zero_thr, double *__restrict__ rgb_out,
-                                                  double *__restrict__ ycocg_out,
+                                                  double zero_thr, double *rgb_out,
+                                                  double *ycocg_out,
                                                   int8_t *__restrict__ status_out) {
     const int64_t n = sp.n;
     const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (k >= n) return;
     const double *sh = sp.sh + 48 * k;
-    double rgb[48], yc[48];
+    // the coefficients are built in place in the outputs (no per-thread copies)
+    double *rgb = rgb_out + 48 * k, *yc = ycocg_out + 48 * k;
     int status = 0;
     if (neq[(int64_t)184 * n + k] == 0.0) {
         // _fallback_dc (compaction.py:161-166) over the 26 cube probes (:32-37)
@@ -375,10 +376,6 @@ __global__ void __launch_bounds__(128) k_sh_solve(potr_splats sp, const double *
         } else {
             coeffs_convert(kYcocgToRgb, yc, rgb);
         }
-    }
-    for (int i = 0; i < 48; i++) {
-        rgb_out[48 * k + i] = rgb[i];
-        ycocg_out[48 * k + i] = yc[i];
     }
     status_out[k] = (int8_t)status;
 }
