@@ -289,7 +289,10 @@ __device__ void coeffs_convert(const double *M, const double *in, double *out) {
         }
 }
 
-__global__ void __launch_bounds__(128) k_sh_solve(potr_splats sp, const double *__restrict__ neq,
+#ifndef POTR_SOLVE_MIN_BLOCKS
+#define POTR_SOLVE_MIN_BLOCKS 8  // 64 regs: 55 vs 70 ms per C3 solve+accumulate (1, 5, 6, 12, 16 measured)
+#endif
+__global__ void __launch_bounds__(128, POTR_SOLVE_MIN_BLOCKS) k_sh_solve(potr_splats sp, const double *__restrict__ neq,
                                                   double lambda_y, double par_thr,
                                                   double zero_thr, double *rgb_out,
                                                   double *ycocg_out,
