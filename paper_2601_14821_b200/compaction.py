@@ -114,6 +114,11 @@ def compact_scene(splats, cameras, camera_importance, config: CompactionConfig, 
                                                          splats.opacities, splats.scales,
                                                          splats.rotations))),
                 np.zeros((0, 3, 16)), {"failed": [], "fallback_dc_only": 0})
+    from . import distributed
+    if distributed.sharding_active() or isinstance(camera_importance, distributed.ShardedRows):
+        # view-sharded run: splat spans per rank (distributed.compact_scene_sharded)
+        return distributed.compact_scene_sharded(splats, cameras, camera_importance, config,
+                                                 group=getattr(camera_importance, "group", None))
     rgb, yc, status = compact_device(splats, cameras, camera_importance, config)
     rgb = D.to_host(rgb)
     yc = D.to_host(yc)
