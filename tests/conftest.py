@@ -108,3 +108,32 @@ def cuda():
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
     return torch.device("cuda", 0)
+
+
+def sh_degenerate_scene():
+    """Rank-deficient SH systems (compaction.py:138-145; pkg/tests/
+    test_compaction.py:203-210): 400 splats near the origin, four cameras of
+    which two share an eye, sparse importances, so most splats see one or two
+    distinct directions.  At lambda = 0 their normal equations are singular:
+    with weights ~1e-2 the 1e-10 jitter rescues them (status 1), with weights
+    ~1e5 it is lost in the rounding of G and the solve fails (RidgeError,
+    status 2: the splat keeps its original coefficients)."""
+    from paper_2601_14821_b200.fixture import look_at
+    from paper_2601_14821_b200.scene import Camera, Splats
+    rng = np.random.default_rng(0)
+    n = 400
+    pos = rng.uniform(-0.2, 0.2, (n, 3))
+    sh = 0.3 * rng.standard_normal((n, 3, 16))
+    sh[:, :, 0] += 1.0
+    splats = Splats(pos, sh, np.full(n, 0.9), np.full((n, 3), 0.05),
+                    np.tile([1.0, 0.0, 0.0, 0.0], (n, 1)))
+    eyes = np.array([[3.0, 0.1, 0.2], [3.0, 0.1, 0.2], [0.2, 3.0, 0.1], [0.1, 0.2, 3.0]])
+    cams = [Camera(eye=e, rotation=look_at(e), fx=40.0, fy=40.0, cx=16.0, cy=16.0, width=32,
+                   height=32) for e in eyes]
+    ci = rng.uniform(0.0, 0.02, (4, n)) * (rng.uniform(size=(4, n)) < 0.5)
+    return splats, cams, ci
+
+
+# (camera_importance scale, lambda_y, parallel_threshold) of the degenerate cases
+SH_DEGENERATE_CASES = [(1.0, 0.0, 1.0), (1.0, 0.0, 0.9999), (1e7, 0.0, 1.0), (1e7, 0.0, 0.9999),
+                       (1.0, 1e-12, 0.9999)]

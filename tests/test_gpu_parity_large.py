@@ -1,0 +1,189 @@
+"""CUDA path vs reference goldens at the headline and largest configs, and the
+SH failure semantics (oracle/gen_golden_large.py made the goldens from the
+reference itself; the oracle is the checker where no golden exists).
+
+* C3 iteration 1 of run_pruning (pruning.py:114-163 at q = 0.5): the removal
+  set from GPU scores equals the reference's, splat for splat.
+* C2: one full view, every splat's scores against the reference's.
+* C5: one full view (8M splats at 1920x1080, 64,800 tiles) against the oracle.
+* run_pruning_to_counts checkpoints equal the reference's.
+* SH: lambda = 0 on rank-deficient systems -- the jitter retry (status 1) and
+  RidgeError (status 2, original coefficients kept, listed in
+  report["failed"]) exactly where the reference has them
+  (compaction.py:138-145, :214-232); lambda = 0 full rank is the identity
+  (pkg/tests/test_compaction.py:283-303).
+"""
+
+import os
+
+import numpy as np
+import pytest
+
+from tests.conftest import (GOLDEN, SH_DEGENERATE_CASES, c3_scene, fingerprint, golden,
+                            perturbed, score_close, sh_degenerate_scene)
+
+pytestmark = pytest.mark.gpu
+
+Q_DELTA_MSE_MAX = 10.0 ** (-8.8 - 2.0 * 0.5)
+
+
+def _have(name):
+    return os.path.exists(os.path.join(GOLDEN, name + ".npz"))
+
+
+@pytest.fixture(scope="module")
+def R(cuda):
+    from paper_2601_14821_b200 import rasterizer
+    return rasterizer
+
+
+@pytest.fixture(scope="module")
+def C(cuda):
+    from paper_2601_14821_b200 import compaction
+    return compaction
+
+
+@pytest.mark.skipif(not _have("c3_it1"), reason="c3_it1 golden not generated")
+def test_c3_iteration1_removal_set_matches_reference(R):
+    """The first pruning iteration at the headline config: targets rendered on
+    the GPU, scores of the same model against them, then the reference's
+    budget and removal-set rules -- host (numpy) and device controllers --
+    must select exactly the reference's splats."""
+    import torch
+    from paper_2601_14821_b200 import device as D, pruning
+    g = golden("c3_it1")
+    splats, cams = c3_scene()
+    assert fingerprint(splats, cams) == str(g["fingerprint"])
+    targets, st = R.render_targets_and_delta_mse(splats, cams)
+    ref_sel = np.cumsum(g["removed_diff"].astype(np.int64))
+    assert len(ref_sel) == int(g["removed_count"])
+    elig = int(np.count_nonzero(st.delta_mse < Q_DELTA_MSE_MAX))
+    assert elig == int(g["eligible"])
+    budget = pruning.compute_budget(st.delta_mse, st.importance, Q_DELTA_MSE_MAX, 48)
+    assert budget == pytest.approx(float(g["budget"]), rel=1e-11)
+    sel = pruning.select_removal_set(st.delta_mse, st.importance, budget, Q_DELTA_MSE_MAX)
+    assert np.array_equal(sel, ref_sel)
+    dm_d = torch.from_numpy(st.delta_mse).to(D.current_device())
+    sel_d = pruning.select_removal_set_device(dm_d, st.delta_mse, st.importance, budget,
+                                              Q_DELTA_MSE_MAX)
+    assert np.array_equal(sel_d, ref_sel)
+    s = g["sample"]
+    np.testing.assert_allclose(st.importance[s], g["sample_importance"], rtol=1e-11, atol=1e-22)
+    assert score_close(st.delta_mse[s], g["sample_delta_mse"], rel=1e-8, floor=1e-26)
+    assert st.mse == pytest.approx(float(g["mse"]), abs=1e-20)
+
+
+@pytest.mark.skipif(not _have("c2_view"), reason="c2_view golden not generated")
+def test_c2_view_matches_reference(R):
+    from paper_2601_14821_b200.fixture import config_scene
+    g = golden("c2_view")
+    splats, cams = config_scene("C2")
+    cams = cams[:1]
+    assert fingerprint(splats, cams) == str(g["fingerprint"])
+    img = R.render_image(splats, cams[0])
+    np.testing.assert_allclose(img, g["target"], rtol=0, atol=1e-13)
+    target = g["target"].copy()
+    target.flags.writeable = False
+    st = R.compute_delta_mse(perturbed(splats), cams, [target])
+    np.testing.assert_allclose(st.importance, g["importance"], rtol=1e-11, atol=1e-22)
+    dmax = np.abs(g["delta_mse"]).max()
+    assert np.all(np.abs(st.delta_mse - g["delta_mse"]) <=
+                  1e-8 * np.abs(g["delta_mse"]) + 1e-12 * dmax)
+    assert st.mse == pytest.approx(float(g["mse"]), rel=1e-11)
+
+
+def test_c5_view_vs_oracle(R, oracle):
+    """BASELINE config 5's shape: 8M splats, one 1920x1080 view (64,800 tiles of
+    8x4, the 16-bit tile-key edge), perturbed opacities against the oracle's
+    render of the unperturbed scene."""
+    from paper_2601_14821_b200.fixture import CONFIGS, make_fixture
+    c = CONFIGS["C5"]
+    splats, cams = make_fixture(c["splats"], 3, 0, width=c["width"], height=c["height"])
+    view = [cams[1]]
+    target, _ = oracle.render(splats, view[0])
+    img = R.render_image(splats, view[0])
+    np.testing.assert_allclose(img, target, rtol=0, atol=1e-13)
+    target.flags.writeable = False
+    pert = perturbed(splats)
+    st = R.compute_delta_mse(pert, view, [target])
+    imp, ci, dm, mse = oracle.forward_stats(pert, view, [target])
+    np.testing.assert_allclose(st.importance, imp, rtol=1e-12, atol=1e-20)
+    np.testing.assert_allclose(st.delta_mse, dm, rtol=1e-9, atol=1e-22)
+    assert abs(st.mse - mse) <= 1e-12 * abs(mse)
+
+
+def test_pruning_to_counts_matches_reference(R):
+    from paper_2601_14821_b200 import pruning
+    from paper_2601_14821_b200.fixture import make_fixture
+    g = golden("counts")
+    splats, cams = make_fixture(3000, 4, 2, 48)
+    assert fingerprint(splats, cams) == str(g["fingerprint"])
+    targets = R.render_targets(splats, cams)
+    assert pruning._device_scorer_active()
+    cps = pruning.run_pruning_to_counts(splats, cams, targets, list(g["counts"]),
+                                        Q_DELTA_MSE_MAX)
+    for i, kept in enumerate(cps):
+        assert np.array_equal(kept, g[f"kept_{i}"])
+
+
+@pytest.mark.parametrize("case", range(len(SH_DEGENERATE_CASES)))
+def test_sh_failure_semantics_match_reference(C, oracle, case):
+    from paper_2601_14821_b200 import device as D
+    g = golden("sh_degenerate")
+    splats, cams, ci = sh_degenerate_scene()
+    scale, lam, par = SH_DEGENERATE_CASES[case]
+    cfg = C.CompactionConfig(lam, par, 0.0)
+    out, yc, rep = C.compact_scene(splats, cams, ci * scale, cfg)
+    _, _, status = C.compact_device(splats, cams, ci * scale, cfg)
+    status = D.to_host(status)
+    # the reference's RidgeError / jitter pattern, splat for splat
+    assert rep["failed"] == [int(k) for k in g[f"failed_{case}"]]
+    assert rep["fallback_dc_only"] == int(g[f"fallback_{case}"])
+    jit = g[f"jitter_{case}"].astype(bool)
+    assert np.array_equal((status == 1) | (status == 2), jit & (status != 3))
+    if case in (0, 2):
+        assert (status == 1).sum() + (status == 2).sum() > 300  # the degenerate path ran
+    # failed splats keep their original coefficients (compaction.py:214-217, 228-232)
+    failed = np.array(rep["failed"], dtype=np.int64)
+    assert np.array_equal(out.sh[failed], splats.sh[failed])
+    np.testing.assert_allclose(yc[failed], g[f"ycocg_{case}"][failed], rtol=0, atol=1e-15)
+    # bit-identical to the oracle (same arithmetic order), within the
+    # contract of the reference (ill-conditioned lambda = 1e-12 systems)
+    rgb_o, yc_o, st_o = oracle.compact(splats, cams, ci * scale, lam, par, 0.0)
+    assert np.array_equal(status, st_o)
+    assert np.array_equal(yc, yc_o) and np.array_equal(out.sh, rgb_o)
+    ok = status == 0
+    np.testing.assert_allclose(yc[ok], g[f"ycocg_{case}"][ok], rtol=0, atol=1e-6)
+    # jitter-recovered solutions are finite and fit the seen colours
+    # (pkg/tests/test_compaction.py:203-210)
+    assert np.all(np.isfinite(yc))
+
+
+def test_sh_lambda_zero_full_rank_is_identity(R, C):
+    """pkg/tests/test_compaction.py:283-303: every splat seen from 32
+    well-spread cameras, lambda = 0, no sparsification, no zeroing: the refit
+    reproduces the coefficients and the renders."""
+    from paper_2601_14821_b200.fixture import look_at
+    from paper_2601_14821_b200.scene import Camera, Splats
+    rng = np.random.default_rng(10)
+    n = 12
+    splats = Splats(rng.uniform(-0.3, 0.3, (n, 3)),
+                    np.concatenate([rng.uniform(1.0, 2.0, (n, 3, 1)),
+                                    0.15 * rng.standard_normal((n, 3, 15))], axis=2),
+                    rng.uniform(0.6, 0.9, n), np.full((n, 3), 0.06),
+                    np.tile([1.0, 0, 0, 0], (n, 1)))
+    k = np.arange(32) + 0.5
+    phi = np.arccos(1 - 2 * k / 32)
+    theta = np.pi * (1 + 5 ** 0.5) * k
+    dirs = np.stack([np.cos(theta) * np.sin(phi), np.sin(theta) * np.sin(phi), np.cos(phi)], 1)
+    cams = [Camera(eye=d * 4.0, rotation=look_at(d * 4.0), fx=40.0, fy=40.0, cx=16.0, cy=16.0,
+                   width=32, height=32) for d in dirs]
+    _, cam_imp = R.compute_importance(splats, cams)
+    assert np.all((np.asarray(cam_imp) > 0).sum(axis=0) == 32)
+    cfg = C.CompactionConfig(lambda_y=0.0, parallel_threshold=1.0, zero_threshold=0.0)
+    out, ycocg, report = C.compact_scene(splats, cams, cam_imp, cfg)
+    assert not report["failed"]
+    assert np.abs(out.sh - splats.sh).max() < 1e-4
+    for cam in cams[:4]:
+        delta = R.render_image(out, cam) - R.render_image(splats, cam)
+        assert np.abs(delta).max() < 1e-4
