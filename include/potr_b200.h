@@ -175,6 +175,23 @@ int potr_sh_solve(potr_ctx *ctx, const potr_splats *splats, const double *normal
                   double lambda_y, double parallel_threshold, double zero_threshold,
                   double *rgb, double *ycocg, int8_t *status);
 
+/* ---- pruning controller (pruning.py:57-111) ------------------------------ */
+
+/* The removal order of the candidates idx[0..n) (device int64; NULL: 0..n-1):
+ * np.argsort(mapping_m(delta_mse[idx] / delta_mse_max, a), kind="stable")
+ * (pruning.py:80-83, :99-100), written to order (device int64, n) as splat
+ * indices.  The priorities are computed with numpy's operation order and
+ * IEEE division; the sort is the library's stable radix sort (ties keep the
+ * candidate order, i.e. ascending index). */
+int potr_removal_order(potr_ctx *ctx, int64_t n, const double *delta_mse, const int64_t *idx,
+                       double delta_mse_max, double a, int64_t *order);
+
+/* The library's stable LSD radix sort (8-bit digits, one-sweep passes) on
+ * device arrays, in place: (keys, vals) ordered by key bits
+ * [begin_bit, end_bit); equal keys keep their input order. */
+int potr_sort_pairs_u64(potr_ctx *ctx, int64_t n, uint64_t *keys, int64_t *vals, int begin_bit,
+                        int end_bit);
+
 /* ---- image metrics (metrics.py:24-52) ------------------------------------ */
 
 /* MSE of the [0, 1]-clamped images (psnr's, metrics.py:24-30) and mean SSIM
@@ -233,10 +250,10 @@ int potr_set_option(potr_ctx *ctx, int option, int value);
 
 /* Stages timed with CUDA events on the context stream while profiling. */
 #define POTR_STAGE_PREPROCESS 0     /* kernel (a)                          */
-#define POTR_STAGE_DEPTH_SORT 1     /* CUB radix sort of fp64 depth keys   */
+#define POTR_STAGE_DEPTH_SORT 1     /* radix sort of the depth keys        */
 #define POTR_STAGE_SCAN 2           /* pair-count gather + scan            */
 #define POTR_STAGE_DUPLICATE 3      /* (tile, splat) pair emission         */
-#define POTR_STAGE_TILE_SORT 4      /* CUB radix sort on tile id + ranges  */
+#define POTR_STAGE_TILE_SORT 4      /* radix sort on tile id + ranges      */
 #define POTR_STAGE_RASTER 5         /* kernels (c)+(d), fused              */
 #define POTR_STAGE_REDUCE 6         /* per-splat slot sums, mse            */
 #define POTR_STAGE_SH_ACCUMULATE 7  /* kernel (e) normal equations         */

@@ -78,6 +78,11 @@ _SIGNATURES = {
                                              ctypes.c_void_p, ctypes.c_void_p]),
     "potr_finalize_stats": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int64, ctypes.c_int,
                                            ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]),
+    "potr_removal_order": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p,
+                                          ctypes.c_void_p, ctypes.c_double, ctypes.c_double,
+                                          ctypes.c_void_p]),
+    "potr_sort_pairs_u64": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p,
+                                           ctypes.c_void_p, ctypes.c_int, ctypes.c_int]),
     "potr_render": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(PotrSplats),
                                    ctypes.POINTER(PotrCamera), ctypes.c_void_p, ctypes.c_void_p]),
     "potr_render_batch": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(PotrSplats), ctypes.c_int,

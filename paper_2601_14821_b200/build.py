@@ -12,7 +12,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "_lib", "libpotr_b200.so")
-SOURCES = ["capi.cu", "raster.cu", "sh.cu", "metrics.cu", "codec.cu"]
+SOURCES = ["capi.cu", "raster.cu", "sh.cu", "metrics.cu", "codec.cu", "sort.cu", "controller.cu"]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

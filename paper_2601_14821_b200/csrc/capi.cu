@@ -10,6 +10,7 @@
 
 #include "common.cuh"
 #include "raster.cuh"
+#include "sort.cuh"
 
 using namespace potr;
 
@@ -34,10 +35,9 @@ struct potr_ctx {
     // per-view workspace
     // dup_id: record of each duplicated pair; perm: tile-sorted slot order;
     // pair: per sorted pair (slot, record)
-    DevBuf rec, key, skey, sids, cnt, offs, iota, tkey, tskey, perm, pair, dup_id,
+    DevBuf rec, key, skey, sids, cnt, offs, perm2, tkey, tskey, perm, pair, dup_id,
         dup_rank,
         partial, ranges, tile_se, temp, nvalid;
-    int64_t iota_len = 0;
     // records mode
     DevBuf rkey, rskey, rsidx, ralpha, rt, rp, rcounter;
     // SH
@@ -56,6 +56,7 @@ struct potr_ctx {
     int64_t pairs_total = 0;
     DevBuf tile_counter, ci_v, dm_v, bbox, overflow, vidx, khi, skhi, prep, spans;
     DevBuf met_mom, met_part, met_w, met_out;  // image metrics scratch
+    DevBuf sort_k, sort_v, rm_keys;            // potr_sort_pairs_u64 / potr_removal_order
     void *codec_scratch = nullptr;             // codec back end scratch
     size_t codec_cap = 0;
     DevBuf codec_eyes;
@@ -193,15 +194,6 @@ int check_cam(potr_ctx *ctx, const potr_camera *c) {
     return 0;
 }
 
-int ensure_iota(potr_ctx *ctx, int64_t len) {
-    if (ctx->iota_len >= len) return 0;
-    int64_t want = len + len / 8 + 16;
-    ENSURE(ctx->iota, sizeof(int32_t) * want);
-    LAUNCH(1, launch_iota(want, P<int32_t>(ctx->iota), ctx->stream));
-    ctx->iota_len = want;
-    return 0;
-}
-
 unsigned long long *counters(potr_ctx *ctx) {
     return ctx->counting ? P<unsigned long long>(ctx->counters) : nullptr;
 }
@@ -273,8 +265,6 @@ int compute_scene_bounds(potr_ctx *ctx, const potr_splats &sp) {
     }
     if (!ctx->spatial || sp.n == 0) return ensure_prep(ctx, sp);
     Stage _st(ctx, POTR_STAGE_PREPROCESS);
-    int rc = ensure_iota(ctx, sp.n);
-    if (rc) return rc;
     ENSURE(ctx->mperm, sizeof(int32_t) * sp.n);
     ENSURE(ctx->mrank, sizeof(int32_t) * sp.n);
     ENSURE(ctx->mcode, sizeof(uint32_t) * sp.n);
@@ -286,10 +276,9 @@ int compute_scene_bounds(potr_ctx *ctx, const potr_splats &sp) {
     size_t t = 0;
     CK(spatial_order_temp(sp.n, &t));
     ENSURE(ctx->temp, t);
-    LAUNCH(2, spatial_order(ctx->temp.p, ctx->temp.cap, sp.n, sp.positions, ctx->scene_lo,
-                            ctx->scene_hi, P<int32_t>(ctx->iota), P<uint32_t>(ctx->mcode),
-                            P<uint32_t>(ctx->mcode2), P<int32_t>(ctx->mperm),
-                            P<int32_t>(ctx->mrank), ctx->stream));
+    LAUNCH(7, spatial_order(ctx->temp.p, ctx->temp.cap, sp.n, sp.positions, ctx->scene_lo,
+                            ctx->scene_hi, P<uint32_t>(ctx->mcode), P<uint32_t>(ctx->mcode2),
+                            P<int32_t>(ctx->mperm), P<int32_t>(ctx->mrank), ctx->stream));
     LAUNCH(1, launch_splat_slots(sp, P<int32_t>(ctx->mperm), P<double>(ctx->slot_pos),
                                  P<double>(ctx->slot_sh), P<double>(ctx->slot_opac),
                                  P<SplatPrep>(ctx->slot_prep), ctx->stream));
@@ -430,6 +419,7 @@ int bin_batch(potr_ctx *ctx, const potr_splats &sp, const potr_camera *cams, int
         // when the double-buffered sort finished in the other half)
         if (split) {  // 32-bit sort of the hi keys, then runs of equal hi by full key
             bool alt = false;
+            ctx->launches += sort_launches(0, key_bits - dk.shift);
             CK(depth_sort32(ctx->temp.p, ctx->temp.cap, P<uint32_t>(ctx->khi),
                             P<uint32_t>(ctx->skhi), P<int32_t>(ctx->vidx), P<int32_t>(ctx->sids),
                             total, key_bits - dk.shift, &alt, ctx->stream));
@@ -445,6 +435,7 @@ int bin_batch(potr_ctx *ctx, const potr_splats &sp, const potr_camera *cams, int
         } else if (dk.compact) {  // one stable sort of the whole batch
             const int end_bit = key_bits;
             bool alt = false;
+            ctx->launches += sort_launches(0, end_bit);
             CK(depth_sort(ctx->temp.p, ctx->temp.cap, P<uint64_t>(ctx->key),
                           P<uint64_t>(ctx->skey), P<int32_t>(ctx->vidx), P<int32_t>(ctx->sids),
                           total, end_bit, &alt, ctx->stream));
@@ -455,6 +446,7 @@ int bin_batch(potr_ctx *ctx, const potr_splats &sp, const potr_camera *cams, int
         } else {  // raw 64-bit depth bits: one sort per view, all with the same
                   // pass count, so every view's result ends in the same half
             bool alt = true;
+            ctx->launches += nview * sort_launches(0, 64);
             for (int v = 0; v < nview; v++)
                 CK(depth_sort(ctx->temp.p, ctx->temp.cap, P<uint64_t>(ctx->key) + v * n,
                               P<uint64_t>(ctx->skey) + v * n, P<int32_t>(ctx->vidx) + v * n,
@@ -468,7 +460,8 @@ int bin_batch(potr_ctx *ctx, const potr_splats &sp, const potr_camera *cams, int
     }
     {
         Stage _st(ctx, POTR_STAGE_SCAN);
-        // CUB scan (its input iterator gathers the counts in depth order)
+        // single-pass scan (sort.cu) gathering the counts in depth order
+        ctx->launches += 1;
         CK(scan_counts(ctx->temp.p, ctx->temp.cap, P<int32_t>(ctx->sids), P<int32_t>(ctx->cnt),
                        P<int64_t>(ctx->offs), total, ctx->stream));
         _st.end();
@@ -501,8 +494,7 @@ int bin_batch(potr_ctx *ctx, const potr_splats &sp, const potr_camera *cams, int
     ENSURE(ctx->dup_id, sizeof(int32_t) * K);
     ENSURE(ctx->partial, sizeof(double2) * K);
     if (with_rank) ENSURE(ctx->dup_rank, sizeof(int32_t) * K);
-    rc = ensure_iota(ctx, K);
-    if (rc) return rc;
+    ENSURE(ctx->perm2, sizeof(int32_t) * K);
     size_t t3 = 0;
     CK(tile_sort_temp(K, sb * g.ntiles, key16, &t3));
     ENSURE(ctx->temp, t3);
@@ -533,10 +525,13 @@ int bin_batch(potr_ctx *ctx, const potr_splats &sp, const potr_camera *cams, int
             const int v1 = v0 + sb < nview ? v0 + sb : nview;
             const int64_t j0 = vstart[v0], kk = vstart[v1] - vstart[v0];
             const size_t koff = kbytes * (size_t)j0;
-            CK(tile_sort(ctx->temp.p, ctx->temp.cap, key16, (const char *)ctx->tkey.p + koff,
-                         (char *)ctx->tskey.p + koff, P<int32_t>(ctx->iota) + j0,
-                         P<int32_t>(ctx->perm) + j0, kk, sb * g.ntiles, ctx->stream));
-            LAUNCH(1, launch_tile_ranges(j0, kk, key16, ctx->tskey.p, P<int32_t>(ctx->perm),
+            bool alt = false;
+            CK(tile_sort(ctx->temp.p, ctx->temp.cap, key16, (char *)ctx->tkey.p + koff,
+                         (char *)ctx->tskey.p + koff, P<int32_t>(ctx->perm) + j0,
+                         P<int32_t>(ctx->perm2) + j0, kk, sb * g.ntiles, &alt, ctx->stream));
+            ctx->launches += 3;  // histogram + two one-sweep passes
+            LAUNCH(1, launch_tile_ranges(j0, kk, key16, alt ? ctx->tskey.p : ctx->tkey.p,
+                                         P<int32_t>(alt ? ctx->perm2 : ctx->perm),
                                          P<int32_t>(ctx->dup_id), P<int2>(ctx->pair),
                                          P<int2>(ctx->ranges), v0 * g.ntiles, ctx->stream));
         }
@@ -667,7 +662,7 @@ void potr_destroy(potr_ctx *ctx) {
     cudaSetDevice(ctx->device);
     cudaStreamSynchronize(ctx->stream);
     DevBuf *bufs[] = {&ctx->rec,     &ctx->key,     &ctx->skey,    &ctx->sids,   &ctx->cnt,
-                      &ctx->offs, &ctx->iota,    &ctx->tkey,   &ctx->tskey,
+                      &ctx->offs, &ctx->perm2,   &ctx->tkey,   &ctx->tskey,
                       &ctx->pair,    &ctx->dup_id,  &ctx->dup_rank, &ctx->partial, &ctx->ranges,
                       &ctx->perm,
                       &ctx->tile_se, &ctx->temp,    &ctx->nvalid,  &ctx->rkey,   &ctx->rskey,
@@ -690,7 +685,8 @@ void potr_destroy(potr_ctx *ctx) {
     for (DevBuf *b : {&ctx->mperm, &ctx->mrank, &ctx->mcode, &ctx->mcode2, &ctx->slot_pos,
                       &ctx->slot_sh, &ctx->slot_opac, &ctx->slot_prep})
         if (b->p) cudaFree(b->p);
-    for (DevBuf *b : {&ctx->met_mom, &ctx->met_part, &ctx->met_w, &ctx->met_out, &ctx->codec_eyes})
+    for (DevBuf *b : {&ctx->met_mom, &ctx->met_part, &ctx->met_w, &ctx->met_out, &ctx->codec_eyes,
+                      &ctx->sort_k, &ctx->sort_v, &ctx->rm_keys})
         if (b->p) cudaFree(b->p);
     if (ctx->codec_scratch) cudaFree(ctx->codec_scratch);
     if (ctx->prep.p) cudaFree(ctx->prep.p);
@@ -888,14 +884,16 @@ int potr_render_records(potr_ctx *ctx, const potr_splats *splats, const potr_cam
     if (m > capacity) return fail(ctx, POTR_E_CAPACITY, "record capacity too small");
     ENSURE(ctx->rskey, sizeof(uint64_t) * m);
     ENSURE(ctx->rsidx, sizeof(int32_t) * m);
-    rc = ensure_iota(ctx, m);
-    if (rc) return rc;
+    ENSURE(ctx->perm2, sizeof(int32_t) * m);
     size_t tb = 0;
     CK(records_sort_temp(m, &tb));
     ENSURE(ctx->temp, tb);
+    bool ralt = false;
     CK(records_sort(ctx->temp.p, ctx->temp.cap, P<uint64_t>(ctx->rkey), P<uint64_t>(ctx->rskey),
-                    P<int32_t>(ctx->iota), P<int32_t>(ctx->rsidx), m, ctx->stream));
-    LAUNCH(1, launch_records_gather(m, P<uint64_t>(ctx->rskey), P<int32_t>(ctx->rsidx),
+                    P<int32_t>(ctx->rsidx), P<int32_t>(ctx->perm2), m, &ralt, ctx->stream));
+    ctx->launches += 9;
+    LAUNCH(1, launch_records_gather(m, P<uint64_t>(ralt ? ctx->rskey : ctx->rkey),
+                                    P<int32_t>(ralt ? ctx->perm2 : ctx->rsidx),
                                     P<int32_t>(ctx->sids), P<double>(ctx->ralpha),
                                     P<double>(ctx->rt), P<double>(ctx->rp), splat_ids, pixels,
                                     alphas, trans_at, partials, spatial_perm(ctx), ctx->stream));
@@ -1008,6 +1006,49 @@ int potr_compact(potr_ctx *ctx, const potr_splats *splats, int ncam, const potr_
     if (rc) return rc;
     return potr_sh_solve(ctx, splats, P<double>(ctx->neq), lambda_y, parallel_threshold,
                          zero_threshold, rgb, ycocg, status);
+}
+
+int potr_sort_pairs_u64(potr_ctx *ctx, int64_t n, uint64_t *keys, int64_t *vals, int begin_bit,
+                        int end_bit) {
+    if (!ctx) return POTR_E_ARG;
+    if (n < 0 || (n > 0 && (!keys || !vals)) || begin_bit < 0 || end_bit > 64)
+        return fail(ctx, POTR_E_ARG, "sort_pairs: bad arguments");
+    if (n == 0 || end_bit <= begin_bit) return POTR_OK;
+    CK(cudaSetDevice(ctx->device));
+    ENSURE(ctx->sort_k, sizeof(uint64_t) * n);
+    ENSURE(ctx->sort_v, sizeof(int64_t) * n);
+    ENSURE(ctx->temp, radix_sort_temp_bytes(n, begin_bit, end_bit));
+    bool alt = false;
+    CK((radix_sort_pairs<uint64_t, int64_t>(ctx->temp.p, ctx->temp.cap, keys, P<uint64_t>(ctx->sort_k),
+                                            vals, P<int64_t>(ctx->sort_v), n, begin_bit, end_bit,
+                                            false, &alt, ctx->stream)));
+    ctx->launches += sort_launches(begin_bit, end_bit);
+    if (alt) {
+        CK(cudaMemcpyAsync(keys, ctx->sort_k.p, sizeof(uint64_t) * n, cudaMemcpyDeviceToDevice,
+                           ctx->stream));
+        CK(cudaMemcpyAsync(vals, ctx->sort_v.p, sizeof(int64_t) * n, cudaMemcpyDeviceToDevice,
+                           ctx->stream));
+    }
+    return POTR_OK;
+}
+
+int potr_removal_order(potr_ctx *ctx, int64_t n, const double *delta_mse, const int64_t *idx,
+                       double delta_mse_max, double a, int64_t *order) {
+    if (!ctx) return POTR_E_ARG;
+    if (n < 0 || (n > 0 && (!delta_mse || !order)))
+        return fail(ctx, POTR_E_ARG, "removal_order: bad arguments");
+    if (!(delta_mse_max > 0) || !(a > 0))
+        return fail(ctx, POTR_E_ARG, "removal_order: delta_mse_max and a must be > 0");
+    if (n == 0) return POTR_OK;
+    CK(cudaSetDevice(ctx->device));
+    ENSURE(ctx->rm_keys, sizeof(uint64_t) * n);
+    LAUNCH(1, launch_removal_keys(n, delta_mse, idx, delta_mse_max, a, P<uint64_t>(ctx->rm_keys),
+                                  ctx->stream));
+    if (idx)
+        CK(cudaMemcpyAsync(order, idx, sizeof(int64_t) * n, cudaMemcpyDeviceToDevice, ctx->stream));
+    else
+        LAUNCH(1, launch_iota64(n, order, ctx->stream));
+    return potr_sort_pairs_u64(ctx, n, P<uint64_t>(ctx->rm_keys), order, 0, 64);
 }
 
 // scipy.ndimage._gaussian_kernel1d(1.5, 0, 5): exp(-0.5 / sigma^2 * x^2) over

@@ -21,12 +21,12 @@
 // LEB128 count).  A node's occupancy collects its own first splat's child
 // octant and, by atomicOr, the octant of every later leaf that branches off
 // exactly at its depth.
-#include <cub/device/device_radix_sort.cuh>
-#include <cub/device/device_scan.cuh>
-#include <cub/device/device_select.cuh>
+
+#include <cstring>
 
 #include "common.cuh"
 #include "raster.cuh"
+#include "sort.cuh"
 
 namespace potr {
 
@@ -313,24 +313,10 @@ cudaError_t run_octree(int64_t n, const double *pos, int neyes, const double *ey
                        int max_depth, uint8_t *out, int64_t capacity, int64_t *out_len,
                        int64_t *order_out, void **scratch, size_t *scratch_cap,
                        int64_t *pinned, cudaStream_t st) {
-    // temp storage for CUB (the largest of the three kinds of call)
-    size_t t1 = 0, t2 = 0, t3 = 0;
-    {
-        cub::DoubleBuffer<uint64_t> k(nullptr, nullptr);
-        cub::DoubleBuffer<int32_t> v(nullptr, nullptr);
-        CODEC_CK(cub::DeviceRadixSort::SortPairs((void *)nullptr, t1, k, v, (int)n, 0, 36));
-        CODEC_CK(cub::DeviceSelect::Flagged((void *)nullptr, t2, (int32_t *)nullptr,
-                                            (uint8_t *)nullptr, (int32_t *)nullptr,
-                                            (int32_t *)nullptr, (int)n));
-        CODEC_CK(cub::DeviceScan::ExclusiveSum((void *)nullptr, t3, (int64_t *)nullptr,
-                                               (int64_t *)nullptr, (int)n + 1));
-        size_t t4 = 0;
-        CODEC_CK(cub::DeviceScan::InclusiveScan((void *)nullptr, t4, (int32_t *)nullptr,
-                                                (int32_t *)nullptr, cub::Max(), (int)n));
-        t1 = t1 > t2 ? t1 : t2;
-        t1 = t1 > t3 ? t1 : t3;
-        t1 = t1 > t4 ? t1 : t4;
-    }
+    // scratch of the sorts and scans (sort.cu)
+    size_t t1 = radix_sort_temp_bytes(n, 0, 36);
+    const size_t t3 = scan_temp_bytes(n + 1);
+    t1 = t1 > t3 ? t1 : t3;
     const size_t need = octree_scratch_bytes(n, max_depth, t1);
     if (*scratch_cap < need) {
         if (*scratch) cudaFree(*scratch);
@@ -363,24 +349,21 @@ cudaError_t run_octree(int64_t n, const double *pos, int neyes, const double *ey
     // stable sort by (hi, lo): by lo first, then stably by hi
     {
         CODEC_CK(cudaMemcpyAsync(ka, klo, 8 * n, cudaMemcpyDeviceToDevice, st));
-        cub::DoubleBuffer<uint64_t> k(ka, kb);
-        cub::DoubleBuffer<int32_t> v(ia, ib);
-        size_t tb = t1;
-        CODEC_CK(cub::DeviceRadixSort::SortPairs(temp, tb, k, v, (int)n, 0, 36, st));
-        int32_t *idx1 = v.Current();
+        bool alt = false;
+        CODEC_CK((radix_sort_pairs<uint64_t, int32_t>(temp, t1, ka, kb, ia, ib, n, 0, 36, false,
+                                                      &alt, st)));
+        int32_t *idx1 = alt ? ib : ia, *idx_free = alt ? ia : ib;
         k_gather_u64<<<blocks_for(n, 256), 256, 0, st>>>(n, idx1, khi, kc);
-        cub::DoubleBuffer<uint64_t> k2(kc, k.Alternate());
-        cub::DoubleBuffer<int32_t> v2(idx1, v.Alternate());
-        CODEC_CK(cub::DeviceRadixSort::SortPairs(temp, tb, k2, v2, (int)n, 0, 36, st));
-        int32_t *ord = v2.Current();
+        CODEC_CK((radix_sort_pairs<uint64_t, int32_t>(temp, t1, kc, alt ? ka : kb, idx1,
+                                                      idx_free, n, 0, 36, false, &alt, st)));
+        int32_t *ord = alt ? idx_free : idx1;
         if (ord != ic) CODEC_CK(cudaMemcpyAsync(ic, ord, 4 * n, cudaMemcpyDeviceToDevice, st));
     }
     int32_t *order = ic;
     k_oct_lcp<<<blocks_for(n, 256), 256, 0, st>>>(n, order, khi, klo, max_depth, lcp, start);
     {
-        size_t tb = t1;
         k_iota32<<<blocks_for(n, 256), 256, 0, st>>>(n, mark);
-        CODEC_CK(cub::DeviceSelect::Flagged(temp, tb, mark, start, gstart, ng_dev, (int)n, st));
+        CODEC_CK(select_flagged_i32(temp, t1, mark, start, gstart, ng_dev, n, st));
     }
     int32_t ngh = 0;
     CODEC_CK(cudaMemcpyAsync(pinned, ng_dev, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
@@ -392,15 +375,13 @@ cudaError_t run_octree(int64_t n, const double *pos, int neyes, const double *ey
     CODEC_CK(cudaGetLastError());
     for (int d = 0; d < max_depth; d++) {
         k_oct_mark<<<blocks_for(ng, 256), 256, 0, st>>>(ng, glcp, d, mark);
-        size_t tb = t1;
-        CODEC_CK(cub::DeviceScan::InclusiveScan(temp, tb, mark, seg, cub::Max(), (int)ng, st));
+        CODEC_CK(inclusive_max_i32(temp, t1, mark, seg, ng, st));
         k_oct_branch<<<blocks_for(ng, 256), 256, 0, st>>>(ng, glcp, seg, d, gstart, order, khi,
                                                           klo, max_depth, occ);
     }
     {
-        size_t tb = t1;
         CODEC_CK(cudaMemsetAsync(gbytes + ng, 0, sizeof(int64_t), st));
-        CODEC_CK(cub::DeviceScan::ExclusiveSum(temp, tb, gbytes, goff, (int)ng + 1, st));
+        CODEC_CK(exclusive_sum_i64(temp, t1, gbytes, goff, ng + 1, st));
     }
     CODEC_CK(cudaMemcpyAsync(pinned, goff + ng, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
     CODEC_CK(cudaStreamSynchronize(st));
@@ -418,9 +399,7 @@ cudaError_t run_attr_streams(int64_t n, const int64_t *order, const double *ycoc
                              int64_t capacity, int64_t *stream_lengths, void **scratch,
                              size_t *scratch_cap, int64_t *pinned, cudaStream_t st) {
     const int64_t m = (int64_t)kStreams * n;
-    size_t tb = 0;
-    CODEC_CK(cub::DeviceScan::ExclusiveSum((void *)nullptr, tb, (int64_t *)nullptr,
-                                           (int64_t *)nullptr, (int)(m + 1)));
+    const size_t tb = scan_temp_bytes(m + 1);
     const size_t need = 8 * (size_t)m + (size_t)m + 8 * (size_t)(m + 1) * 2 + tb + 4096;
     if (*scratch_cap < need) {
         if (*scratch) cudaFree(*scratch);
@@ -439,7 +418,7 @@ cudaError_t run_attr_streams(int64_t n, const int64_t *order, const double *ycoc
                                                       sf_sh, sf_op, sf_rot, sf_sc, val, len);
     k_attr_len64<<<blocks_for(m, 256), 256, 0, st>>>(m, len, l64);
     CODEC_CK(cudaMemsetAsync(l64 + m, 0, sizeof(int64_t), st));
-    CODEC_CK(cub::DeviceScan::ExclusiveSum(temp, tb, l64, off, (int)(m + 1), st));
+    CODEC_CK(exclusive_sum_i64(temp, tb, l64, off, m + 1, st));
     // stream boundaries: off[s * n] for s = 0..55
     for (int s = 0; s <= kStreams; s++)
         CODEC_CK(cudaMemcpyAsync(pinned + s, off + (int64_t)s * n, sizeof(int64_t),

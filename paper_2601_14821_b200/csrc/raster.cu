@@ -1,18 +1,18 @@
 // raster.cu -- the prune-score pass on sm_100a: kernels (a)-(d).  All work is
 // done for a batch of up to 8 equal-size views at a time, in "slot space":
 // once per call the splats are ordered by the Morton code of their centres
-// (k_morton + CUB sort) and copied in that order with their view-independent
+// (k_morton + radix sort, sort.cu) and copied in that order with their view-independent
 // terms (k_splat_slots), so that the records a tile reads are close together
 // in HBM; slots map back to splat indices where results leave (raster.cuh).
 //
 //  (a) k_preprocess: one thread per (slot, view): EWA projection, cov2d,
 //      radius, clipped bbox, conic, SH colour, compact depth key, culled tile
 //      rows and count (rasterizer.py:56-110, :135-154)
-//  (b) depth order: CUB sort of the 32-bit hi part of the depth key +
+//  (b) depth order: radix sort (sort.cu) of the 32-bit hi part of the depth key +
 //      k_depth_fixup (runs of equal hi ordered by the full key, exact ties by
-//      splat index) == np.argsort(kind="stable") (:248-250); CUB scan of the
+//      splat index) == np.argsort(kind="stable") (:248-250); scan of the
 //      counts in depth order, k_duplicate (pairs in depth order, tiles culled
-//      by the prefilter ellipse), CUB stable sort on 16-bit tile keys,
+//      by the prefilter ellipse), stable radix sort on 16-bit tile keys,
 //      k_tile_ranges: every tile gets its splats in (tile, depth, id) order.
 //  (c)+(d) k_raster    persistent warps, one warp per 8x4-pixel tile (lane =
 //      pixel).  Pass 1 composites front to back with the reference's exact
@@ -26,13 +26,9 @@
 //  k_splat_reduce / k_view_accumulate / k_mse_reduce: per splat, its slots in
 //      tile order, divided by P / 3P, added in camera order (:226-230, :334,
 //      :340-347).
-#include <cub/device/device_radix_sort.cuh>
-#include <cub/device/device_scan.cuh>
-#include <thrust/iterator/counting_iterator.h>
-#include <thrust/iterator/transform_iterator.h>
-
 #include "common.cuh"
 #include "raster.cuh"
+#include "sort.cuh"
 
 #ifndef POTR_RASTER_MIN_BLOCKS
 #define POTR_RASTER_MIN_BLOCKS 8
@@ -366,7 +362,9 @@ __global__ void k_duplicate(int64_t total, int64_t n, const int32_t *__restrict_
 
 // Tile [start, end) ranges of the sorted pairs of one sort group (pairs
 // [j0, j0 + K) carrying group-local keys; tile index = tbase + key), and each
-// sorted pair's (slot, record) for the rasterizer's one 8-byte fetch.
+// sorted pair's (slot, record) for the rasterizer's one 8-byte fetch.  The
+// sort's values are group-local pair indices (the implicit iota of its first
+// pass): slot = j0 + perm[j].
 template <typename KeyT>
 __global__ void k_tile_ranges(int64_t j0, int64_t K, const KeyT *__restrict__ skey,
                               const int32_t *__restrict__ perm, const int32_t *__restrict__ dup_id,
@@ -374,16 +372,11 @@ __global__ void k_tile_ranges(int64_t j0, int64_t K, const KeyT *__restrict__ sk
     const int64_t jj = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (jj >= K) return;
     const int64_t j = j0 + jj;
-    const int32_t d = perm[j];
+    const int32_t d = (int32_t)j0 + perm[j];
     pair[j] = make_int2(d, dup_id[d]);
     const uint32_t t = skey[j];
     if (jj == 0 || skey[j - 1] != t) rng[tbase + t].x = (int)j;
     if (jj == K - 1 || skey[j + 1] != t) rng[tbase + t].y = (int)(j + 1);
-}
-
-__global__ void k_iota(int64_t n, int32_t *out) {
-    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i < n) out[i] = (int32_t)i;
 }
 
 // ---------------------------------------------------------------------------
@@ -1143,77 +1136,25 @@ cudaError_t launch_project_dump(const potr_splats &sp, const Cam &cam, double *m
     return cudaGetLastError();
 }
 
-cudaError_t launch_iota(int64_t n, int32_t *out, cudaStream_t st) {
-    if (n == 0) return cudaSuccess;
-    k_iota<<<grid_for(n, 256), 256, 0, st>>>(n, out);
-    return cudaGetLastError();
-}
-
-// Double-buffered: no copy-back pass when the pass count is odd.  *in_alt is
-// set when the sorted keys/values ended in the second buffer of each pair.
+// Double-buffered (sort.cu): *in_alt is set when the sorted keys/values ended
+// in the second buffer of each pair.
 cudaError_t depth_sort(void *temp, size_t temp_bytes, uint64_t *key_a, uint64_t *key_b,
                        int32_t *val_a, int32_t *val_b, int64_t n, int end_bit, bool *in_alt,
                        cudaStream_t st) {
-    *in_alt = false;
-    if (n == 0) return cudaSuccess;
-    cub::DoubleBuffer<uint64_t> k(key_a, key_b);
-    cub::DoubleBuffer<int32_t> v(val_a, val_b);
-    cudaError_t e = cub::DeviceRadixSort::SortPairs(temp, temp_bytes, k, v, (int)n, 0, end_bit, st);
-    *in_alt = k.Current() == key_b;
-    return e;
+    return radix_sort_pairs<uint64_t, int32_t>(temp, temp_bytes, key_a, key_b, val_a, val_b, n,
+                                               0, end_bit, false, in_alt, st);
 }
-
-// The depth sort's onesweep policy: CUB's sm_100 tuning for 32-bit keys with
-// 4-byte values (23 items per thread, 109 registers: one 384-thread block per
-// SM) measured 26.0 ms per C3 step; 20 items 21.0 ms (12: 25.8, 16: 22.7,
-// 22: 20.9, 20 x 256 threads: 21.4).  The tile sort's CUB tuning (512 x 17
-// for 16-bit keys) measured best among 384 x 16, 256 x 20, 512 x 12, 384 x 23.
-#ifndef POTR_DSORT_ITEMS
-#define POTR_DSORT_ITEMS 20
-#endif
-#ifndef POTR_DSORT_THREADS
-#define POTR_DSORT_THREADS 384
-#endif
-struct DepthSortHub {
-    using P1000 = cub::detail::radix::policy_hub<uint32_t, int32_t, uint32_t>::Policy1000;
-    struct Policy : cub::ChainedPolicy<1000, Policy, Policy> {
-        static constexpr bool ONESWEEP = true;
-        static constexpr int ONESWEEP_RADIX_BITS = 8;
-        using HistogramPolicy = P1000::HistogramPolicy;
-        using ExclusiveSumPolicy = P1000::ExclusiveSumPolicy;
-        using OnesweepPolicy = cub::AgentRadixSortOnesweepPolicy<
-            POTR_DSORT_THREADS, POTR_DSORT_ITEMS, uint32_t, 1, cub::RADIX_RANK_MATCH_EARLY_COUNTS_ANY,
-            cub::BLOCK_SCAN_RAKING_MEMOIZE, cub::RADIX_SORT_STORE_DIRECT, 8>;
-        using ScanPolicy = P1000::ScanPolicy;
-        using DownsweepPolicy = P1000::DownsweepPolicy;
-        using AltDownsweepPolicy = P1000::AltDownsweepPolicy;
-        using UpsweepPolicy = P1000::UpsweepPolicy;
-        using AltUpsweepPolicy = P1000::AltUpsweepPolicy;
-        using SingleTilePolicy = P1000::SingleTilePolicy;
-        using SegmentedPolicy = P1000::SegmentedPolicy;
-        using AltSegmentedPolicy = P1000::AltSegmentedPolicy;
-    };
-    using MaxPolicy = Policy;
-};
-using DepthSortDispatch = cub::DispatchRadixSort<false, uint32_t, int32_t, uint32_t, DepthSortHub>;
 
 cudaError_t depth_sort32(void *temp, size_t temp_bytes, uint32_t *key_a, uint32_t *key_b,
                          int32_t *val_a, int32_t *val_b, int64_t n, int end_bit, bool *in_alt,
                          cudaStream_t st) {
-    *in_alt = false;
-    if (n == 0) return cudaSuccess;
-    cub::DoubleBuffer<uint32_t> k(key_a, key_b);
-    cub::DoubleBuffer<int32_t> v(val_a, val_b);
-    size_t bytes = temp_bytes;
-    cudaError_t e = DepthSortDispatch::Dispatch(temp, bytes, k, v, (uint32_t)n, 0, end_bit, true, st);
-    *in_alt = k.Current() == key_b;
-    return e;
+    return radix_sort_pairs<uint32_t, int32_t>(temp, temp_bytes, key_a, key_b, val_a, val_b, n,
+                                               0, end_bit, false, in_alt, st);
 }
 
 cudaError_t depth_sort32_temp(int64_t n, size_t *bytes) {
-    cub::DoubleBuffer<uint32_t> k(nullptr, nullptr);
-    cub::DoubleBuffer<int32_t> v(nullptr, nullptr);
-    return DepthSortDispatch::Dispatch(nullptr, *bytes, k, v, (uint32_t)n, 0, 32, true, nullptr);
+    *bytes = radix_sort_temp_bytes(n, 0, 32);
+    return cudaSuccess;
 }
 
 // One thread per sorted position; the first position of each run of equal hi
@@ -1286,9 +1227,8 @@ cudaError_t launch_gather_keys(int64_t total, const int32_t *sids, const uint64_
 }
 
 cudaError_t depth_sort_temp(int64_t n, size_t *bytes) {
-    cub::DoubleBuffer<uint64_t> k(nullptr, nullptr);
-    cub::DoubleBuffer<int32_t> v(nullptr, nullptr);
-    return cub::DeviceRadixSort::SortPairs((void *)nullptr, *bytes, k, v, (int)n, 0, 64);
+    *bytes = radix_sort_temp_bytes(n, 0, 64);
+    return cudaSuccess;
 }
 
 __global__ void k_bbox(int64_t n, const double *__restrict__ pos,
@@ -1344,15 +1284,15 @@ __global__ void k_scatter_rank(int64_t n, const int32_t *__restrict__ perm,
 }
 
 cudaError_t spatial_order_temp(int64_t n, size_t *bytes) {
-    return cub::DeviceRadixSort::SortPairs(nullptr, *bytes, (const uint32_t *)nullptr,
-                                           (uint32_t *)nullptr, (const int32_t *)nullptr,
-                                           (int32_t *)nullptr, (int)n, 0, 30);
+    *bytes = radix_sort_temp_bytes(n, 0, 30);
+    return cudaSuccess;
 }
 
+// perm = splats by Morton code (stable: ties by index), rank = perm^-1.
+// code / code_sorted are the key pair, perm / rank the value pair.
 cudaError_t spatial_order(void *temp, size_t temp_bytes, int64_t n, const double *pos,
-                          const double lo[3], const double hi[3], const int32_t *iota,
-                          uint32_t *code, uint32_t *code_sorted, int32_t *perm, int32_t *rank,
-                          cudaStream_t st) {
+                          const double lo[3], const double hi[3], uint32_t *code,
+                          uint32_t *code_sorted, int32_t *perm, int32_t *rank, cudaStream_t st) {
     if (n == 0) return cudaSuccess;
     double sc[3];
     for (int i = 0; i < 3; i++) {
@@ -1363,9 +1303,14 @@ cudaError_t spatial_order(void *temp, size_t temp_bytes, int64_t n, const double
                                                code);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
-    e = cub::DeviceRadixSort::SortPairs(temp, temp_bytes, code, code_sorted, iota, perm, (int)n, 0,
-                                        30, st);
+    bool alt = false;
+    e = radix_sort_pairs<uint32_t, int32_t>(temp, temp_bytes, code, code_sorted, perm, rank, n, 0,
+                                            30, true, &alt, st);
     if (e != cudaSuccess) return e;
+    if (alt) {
+        e = cudaMemcpyAsync(perm, rank, sizeof(int32_t) * n, cudaMemcpyDeviceToDevice, st);
+        if (e != cudaSuccess) return e;
+    }
     k_scatter_rank<<<grid_for(n, 256), 256, 0, st>>>(n, perm, rank);
     return cudaGetLastError();
 }
@@ -1378,30 +1323,17 @@ cudaError_t launch_bbox(int64_t n, const double *pos, unsigned long long *out, c
     return cudaGetLastError();
 }
 
-// cnt[ids[i]] as int64, read by the pair-offset scan (no gathered copy).
-struct GatherCount {
-    const int32_t *ids, *cnt;
-    __host__ __device__ __forceinline__ int64_t operator()(int64_t i) const {
-        return (int64_t)cnt[ids[i]];
-    }
-};
-using SortedCounts = thrust::transform_iterator<GatherCount, thrust::counting_iterator<int64_t>,
-                                                int64_t>;
-static SortedCounts sorted_counts(const int32_t *ids, const int32_t *cnt) {
-    return SortedCounts(thrust::counting_iterator<int64_t>(0), GatherCount{ids, cnt});
-}
-
+// offs[0] = 0, offs[i + 1] = sum of cnt[ids[j]] for j <= i (sort.cu: the
+// counts are gathered in depth order by the scan itself).
 cudaError_t scan_counts(void *temp, size_t temp_bytes, const int32_t *ids, const int32_t *cnt,
                         int64_t *offs, int64_t total, cudaStream_t st) {
     cudaError_t e = cudaMemsetAsync(offs, 0, sizeof(int64_t), st);
     if (e != cudaSuccess || total == 0) return e;
-    // the counts in sorted order come through the scan's input iterator
-    return cub::DeviceScan::InclusiveSum(temp, temp_bytes, sorted_counts(ids, cnt), offs + 1,
-                                         (int)total, st);
+    return inclusive_sum_gather(temp, temp_bytes, ids, cnt, offs + 1, total, st);
 }
 cudaError_t scan_temp(int64_t n, size_t *bytes) {
-    return cub::DeviceScan::InclusiveSum((void *)nullptr, *bytes, sorted_counts(nullptr, nullptr),
-                                         (int64_t *)nullptr, (int)n);
+    *bytes = scan_temp_bytes(n);
+    return cudaSuccess;
 }
 
 cudaError_t launch_duplicate(int64_t total, int64_t n, const int32_t *ids, const int64_t *offs,
@@ -1426,41 +1358,39 @@ static int bits_for(int ntiles) {
     return b;
 }
 
-// Stable sort of the pairs by tile key (4-byte values: 8-byte ones measured
-// 10 ms slower per C3 step than the gather in k_tile_ranges).
-cudaError_t tile_sort(void *temp, size_t temp_bytes, bool key16, const void *tkey, void *skey,
-                      const int32_t *iota, int32_t *perm, int64_t K, int nkeys, cudaStream_t st) {
+// Stable sort of the pairs by tile key, values = pair indices (implicit iota
+// in the first pass).  Double-buffered over (tkey, tkey_alt) x (perm,
+// perm_alt); *in_alt tells where the result is.
+cudaError_t tile_sort(void *temp, size_t temp_bytes, bool key16, void *tkey, void *tkey_alt,
+                      int32_t *perm, int32_t *perm_alt, int64_t K, int nkeys, bool *in_alt,
+                      cudaStream_t st) {
+    *in_alt = false;
     if (K == 0) return cudaSuccess;
     if (key16)
-        return cub::DeviceRadixSort::SortPairs(temp, temp_bytes, (const uint16_t *)tkey,
-                                               (uint16_t *)skey, iota, perm, (int)K, 0,
-                                               bits_for(nkeys), st);
-    return cub::DeviceRadixSort::SortPairs(temp, temp_bytes, (const uint32_t *)tkey,
-                                           (uint32_t *)skey, iota, perm, (int)K, 0,
-                                           bits_for(nkeys), st);
+        return radix_sort_pairs<uint16_t, int32_t>(temp, temp_bytes, (uint16_t *)tkey,
+                                                   (uint16_t *)tkey_alt, perm, perm_alt, K, 0,
+                                                   bits_for(nkeys), true, in_alt, st);
+    return radix_sort_pairs<uint32_t, int32_t>(temp, temp_bytes, (uint32_t *)tkey,
+                                               (uint32_t *)tkey_alt, perm, perm_alt, K, 0,
+                                               bits_for(nkeys), true, in_alt, st);
 }
 
 cudaError_t tile_sort_temp(int64_t K, int nkeys, bool key16, size_t *bytes) {
-    if (key16)
-        return cub::DeviceRadixSort::SortPairs((void *)nullptr, *bytes, (const uint16_t *)nullptr,
-                                               (uint16_t *)nullptr, (const int32_t *)nullptr,
-                                               (int32_t *)nullptr, (int)K, 0, bits_for(nkeys));
-    return cub::DeviceRadixSort::SortPairs((void *)nullptr, *bytes, (const uint32_t *)nullptr,
-                                           (uint32_t *)nullptr, (const int32_t *)nullptr,
-                                           (int32_t *)nullptr, (int)K, 0, bits_for(nkeys));
+    (void)key16;
+    *bytes = radix_sort_temp_bytes(K, 0, bits_for(nkeys));
+    return cudaSuccess;
 }
 
 cudaError_t records_sort_temp(int64_t m, size_t *bytes) {
-    return cub::DeviceRadixSort::SortPairs((void *)nullptr, *bytes, (const uint64_t *)nullptr,
-                                           (uint64_t *)nullptr, (const int32_t *)nullptr,
-                                           (int32_t *)nullptr, (int)m, 0, 64);
+    *bytes = radix_sort_temp_bytes(m, 0, 64);
+    return cudaSuccess;
 }
 
-cudaError_t records_sort(void *temp, size_t temp_bytes, const uint64_t *key, uint64_t *skey,
-                         const int32_t *iota, int32_t *sidx, int64_t m, cudaStream_t st) {
-    if (m == 0) return cudaSuccess;
-    return cub::DeviceRadixSort::SortPairs(temp, temp_bytes, key, skey, iota, sidx, (int)m, 0, 64,
-                                           st);
+cudaError_t records_sort(void *temp, size_t temp_bytes, uint64_t *key, uint64_t *key_alt,
+                         int32_t *sidx, int32_t *sidx_alt, int64_t m, bool *in_alt,
+                         cudaStream_t st) {
+    return radix_sort_pairs<uint64_t, int32_t>(temp, temp_bytes, key, key_alt, sidx, sidx_alt, m,
+                                               0, 64, true, in_alt, st);
 }
 
 cudaError_t launch_tile_ranges(int64_t j0, int64_t K, bool key16, const void *skey,

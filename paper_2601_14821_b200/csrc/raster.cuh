@@ -69,13 +69,11 @@ cudaError_t launch_preprocess(const potr_splats &sp, const SplatPrep *prep, cons
 // fallback sorts run in splat order.
 cudaError_t spatial_order_temp(int64_t n, size_t *bytes);
 cudaError_t spatial_order(void *temp, size_t temp_bytes, int64_t n, const double *pos,
-                          const double lo[3], const double hi[3], const int32_t *iota,
-                          uint32_t *code, uint32_t *code_sorted, int32_t *perm, int32_t *rank,
-                          cudaStream_t st);
+                          const double lo[3], const double hi[3], uint32_t *code,
+                          uint32_t *code_sorted, int32_t *perm, int32_t *rank, cudaStream_t st);
 cudaError_t launch_project_dump(const potr_splats &sp, const Cam &cam, double *mean2d,
                                 double *cov2d, double *depth, double *radius, uint8_t *valid,
                                 double *colors, cudaStream_t st);
-cudaError_t launch_iota(int64_t n, int32_t *out, cudaStream_t st);
 cudaError_t depth_sort_temp(int64_t n, size_t *bytes);
 cudaError_t depth_sort32_temp(int64_t n, size_t *bytes);
 cudaError_t depth_sort32(void *temp, size_t temp_bytes, uint32_t *key_a, uint32_t *key_b,
@@ -102,11 +100,13 @@ cudaError_t launch_duplicate(int64_t total, int64_t n, const int32_t *ids, const
                              int sb, bool key16, int cull, void *tkey, int32_t *dup_id,
                              int32_t *dup_rank, cudaStream_t st);
 cudaError_t tile_sort_temp(int64_t K, int nkeys, bool key16, size_t *bytes);
-cudaError_t tile_sort(void *temp, size_t temp_bytes, bool key16, const void *tkey, void *skey,
-                      const int32_t *iota, int32_t *perm, int64_t K, int nkeys, cudaStream_t st);
+cudaError_t tile_sort(void *temp, size_t temp_bytes, bool key16, void *tkey, void *tkey_alt,
+                      int32_t *perm, int32_t *perm_alt, int64_t K, int nkeys, bool *in_alt,
+                      cudaStream_t st);
 cudaError_t records_sort_temp(int64_t m, size_t *bytes);
-cudaError_t records_sort(void *temp, size_t temp_bytes, const uint64_t *key, uint64_t *skey,
-                         const int32_t *iota, int32_t *sidx, int64_t m, cudaStream_t st);
+cudaError_t records_sort(void *temp, size_t temp_bytes, uint64_t *key, uint64_t *key_alt,
+                         int32_t *sidx, int32_t *sidx_alt, int64_t m, bool *in_alt,
+                         cudaStream_t st);
 cudaError_t launch_tile_ranges(int64_t j0, int64_t K, bool key16, const void *skey,
                                const int32_t *perm, const int32_t *dup_id, int2 *pair, int2 *rng,
                                int tbase, cudaStream_t st);
@@ -155,6 +155,12 @@ cudaError_t run_attr_streams(int64_t n, const int64_t *order, const double *ycoc
                              double sf_sh, double sf_op, double sf_rot, double sf_sc, uint8_t *out,
                              int64_t capacity, int64_t *stream_lengths, void **scratch,
                              size_t *scratch_cap, int64_t *pinned, cudaStream_t st);
+
+// Pruning controller (controller.cu): order-preserving keys of the removal
+// priority m(dm[idx[i]] / dmax) (idx nullable: identity)
+cudaError_t launch_removal_keys(int64_t n, const double *dm, const int64_t *idx, double dmax,
+                                double a, uint64_t *keys, cudaStream_t st);
+cudaError_t launch_iota64(int64_t n, int64_t *out, cudaStream_t st);
 
 // SH recompute (sh.cu)
 cudaError_t launch_sh_accumulate(const potr_splats &sp, int ncam, const double *eyes_dev,

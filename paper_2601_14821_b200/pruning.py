@@ -100,18 +100,21 @@ def select_removal_set(delta_mse, importance, budget, delta_mse_max, a=10.0):
     return np.sort(cand[take])
 
 
-def _mapping_m_torch(x, a):
-    import torch
-    neg = (torch.sqrt(1.0 - 2.0 * a * torch.clamp(x, max=0.0)) - 1.0) / a
-    return torch.where(x >= 0.0, x, neg)
-
-
 def _removal_order_device(dm_dev, idx_dev, delta_mse_max, a):
-    """idx_dev[stable argsort of m(dm / max)] on the GPU (pruning.py:80-83, :99-100)."""
+    """idx_dev[stable argsort of m(dm / max)] on the GPU (pruning.py:80-83,
+    :99-100): potr_removal_order computes the priorities with numpy's
+    operation order and IEEE division and sorts them with the library's
+    stable radix sort (ties keep the candidate order)."""
+    import ctypes
     import torch
-    scores = _mapping_m_torch(dm_dev[idx_dev] / delta_mse_max, a) + 0.0  # -0.0 -> +0.0
-    order = torch.sort(scores, stable=True).indices
-    return idx_dev[order]
+    from . import device as D
+    idx = idx_dev.to(torch.int64).contiguous() if idx_dev is not None else None
+    n = int(idx.numel()) if idx is not None else int(dm_dev.numel())
+    order = torch.empty(max(n, 1), dtype=torch.int64, device=dm_dev.device)
+    D.context().call("potr_removal_order", ctypes.c_int64(n), D.ptr(dm_dev.contiguous()),
+                     D.ptr(idx), ctypes.c_double(delta_mse_max), ctypes.c_double(a),
+                     D.ptr(order))
+    return order[:n]
 
 
 def select_removal_set_device(dm_dev, delta_mse, importance, budget, delta_mse_max, a=10.0):
@@ -255,8 +258,7 @@ def _run_pruning_to_counts_device(splats, cameras, targets, cumulative_counts, d
         batch = min(target, n0) - removed
         if batch > 0:
             _, _, dm_d, _ = forward_stats_device(ds, cameras, dev_targets, want_cam_imp=False)
-            idx = torch.arange(ds.n, device=dev)
-            order = _removal_order_device(dm_d, idx, delta_mse_max, a)
+            order = _removal_order_device(dm_d, None, delta_mse_max, a)
             sel = np.sort(D.to_host(order[:batch]))
             mask = np.ones(ds.n, dtype=bool)
             mask[sel] = False
