@@ -227,6 +227,12 @@ uint64_t dbits(double d) {
     return b;
 }
 
+int bits_for_tiles(int nkeys) {
+    int b = 1;
+    while ((1 << b) < nkeys) b++;
+    return b;
+}
+
 int bitlen(uint64_t x) {
     int b = 0;
     while (x) {
@@ -529,9 +535,10 @@ int bin_batch(potr_ctx *ctx, const potr_splats &sp, const potr_camera *cams, int
             CK(tile_sort(ctx->temp.p, ctx->temp.cap, key16, (char *)ctx->tkey.p + koff,
                          (char *)ctx->tskey.p + koff, P<int32_t>(ctx->perm) + j0,
                          P<int32_t>(ctx->perm2) + j0, kk, sb * g.ntiles, &alt, ctx->stream));
-            ctx->launches += 3;  // histogram + two one-sweep passes
-            LAUNCH(1, launch_tile_ranges(j0, kk, key16, alt ? ctx->tskey.p : ctx->tkey.p,
-                                         P<int32_t>(alt ? ctx->perm2 : ctx->perm),
+            ctx->launches += sort_launches(0, bits_for_tiles(sb * g.ntiles));
+            LAUNCH(1, launch_tile_ranges(j0, kk, key16,
+                                         (char *)(alt ? ctx->tskey.p : ctx->tkey.p) + koff,
+                                         P<int32_t>(alt ? ctx->perm2 : ctx->perm) + j0,
                                          P<int32_t>(ctx->dup_id), P<int2>(ctx->pair),
                                          P<int2>(ctx->ranges), v0 * g.ntiles, ctx->stream));
         }

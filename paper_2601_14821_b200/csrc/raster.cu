@@ -364,19 +364,18 @@ __global__ void k_duplicate(int64_t total, int64_t n, const int32_t *__restrict_
 // [j0, j0 + K) carrying group-local keys; tile index = tbase + key), and each
 // sorted pair's (slot, record) for the rasterizer's one 8-byte fetch.  The
 // sort's values are group-local pair indices (the implicit iota of its first
-// pass): slot = j0 + perm[j].
+// pass): slot = j0 + perm[j].  skey / perm point at the group's slice.
 template <typename KeyT>
 __global__ void k_tile_ranges(int64_t j0, int64_t K, const KeyT *__restrict__ skey,
                               const int32_t *__restrict__ perm, const int32_t *__restrict__ dup_id,
                               int2 *__restrict__ pair, int2 *__restrict__ rng, int tbase) {
     const int64_t jj = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (jj >= K) return;
-    const int64_t j = j0 + jj;
-    const int32_t d = (int32_t)j0 + perm[j];
-    pair[j] = make_int2(d, dup_id[d]);
-    const uint32_t t = skey[j];
-    if (jj == 0 || skey[j - 1] != t) rng[tbase + t].x = (int)j;
-    if (jj == K - 1 || skey[j + 1] != t) rng[tbase + t].y = (int)(j + 1);
+    const int32_t d = (int32_t)j0 + perm[jj];
+    pair[j0 + jj] = make_int2(d, dup_id[d]);
+    const uint32_t t = skey[jj];
+    if (jj == 0 || skey[jj - 1] != t) rng[tbase + t].x = (int)(j0 + jj);
+    if (jj == K - 1 || skey[jj + 1] != t) rng[tbase + t].y = (int)(j0 + jj + 1);
 }
 
 // ---------------------------------------------------------------------------
@@ -1164,10 +1163,16 @@ __global__ void k_depth_fixup(int64_t total, const uint32_t *__restrict__ hi,
                               int32_t *__restrict__ sids, const uint64_t *__restrict__ key,
                               uint32_t invalid_lo, uint32_t lo_mask, int *overflow,
                               const int32_t *__restrict__ perm, int64_t n) {
+    // run starts: one coalesced load per position, the neighbours by shuffle
+    const unsigned FULL = 0xffffffffu;
+    const int lane = threadIdx.x & 31;
     const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (j + 1 >= total) return;
-    const uint32_t h = hi[j];
-    if (h != hi[j + 1] || (j > 0 && hi[j - 1] == h)) return;  // not the start of a run
+    const bool in = j < total;
+    const uint32_t h = in ? hi[j] : 0u;
+    uint32_t prev = __shfl_up_sync(FULL, h, 1), next = __shfl_down_sync(FULL, h, 1);
+    if (lane == 0) prev = (in && j > 0) ? hi[j - 1] : ~h;
+    if (lane == 31 || j + 1 >= total) next = j + 1 < total ? hi[j + 1] : ~h;
+    if (!in || h != next || h == prev) return;  // not the start of a run
     if ((h & lo_mask) == invalid_lo) return;  // invalid splats: already in record order
     int len = 2;
     while (j + len < total && hi[j + len] == h) {
@@ -1231,9 +1236,12 @@ cudaError_t depth_sort_temp(int64_t n, size_t *bytes) {
     return cudaSuccess;
 }
 
-__global__ void k_bbox(int64_t n, const double *__restrict__ pos,
-                       unsigned long long *__restrict__ out) {
-    // out[0..2] = ordered-int min of x,y,z; out[3..5] = ordered-int max
+__global__ void __launch_bounds__(256) k_bbox(int64_t n, const double *__restrict__ pos,
+                                              unsigned long long *__restrict__ out) {
+    // out[0..2] = ordered-int min of x,y,z; out[3..5] = ordered-int max.  Warp
+    // and CTA reductions first: six global atomics per CTA (same-address
+    // atomics from every thread serialised at L2: ~300 us per call before).
+    __shared__ unsigned long long red[8][6];
     unsigned long long mn[3] = {~0ull, ~0ull, ~0ull}, mx[3] = {0ull, 0ull, 0ull};
     for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n;
          k += (int64_t)gridDim.x * blockDim.x) {
@@ -1249,8 +1257,25 @@ __global__ void k_bbox(int64_t n, const double *__restrict__ pos,
     }
 #pragma unroll
     for (int i = 0; i < 3; i++) {
-        atomicMin(&out[i], mn[i]);
-        atomicMax(&out[3 + i], mx[i]);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const unsigned long long a = __shfl_xor_sync(0xffffffffu, mn[i], o);
+            const unsigned long long b = __shfl_xor_sync(0xffffffffu, mx[i], o);
+            mn[i] = a < mn[i] ? a : mn[i];
+            mx[i] = b > mx[i] ? b : mx[i];
+        }
+    }
+    const int w = threadIdx.x >> 5;
+    if ((threadIdx.x & 31) == 0)
+        for (int i = 0; i < 3; i++) red[w][i] = mn[i], red[w][3 + i] = mx[i];
+    __syncthreads();
+    if (threadIdx.x < 6) {
+        const int i = threadIdx.x;
+        unsigned long long v = red[0][i];
+        for (int q = 1; q < (int)(blockDim.x >> 5); q++)
+            v = i < 3 ? (red[q][i] < v ? red[q][i] : v) : (red[q][i] > v ? red[q][i] : v);
+        if (i < 3) atomicMin(&out[i], v);
+        else atomicMax(&out[i], v);
     }
 }
 
@@ -1358,9 +1383,9 @@ static int bits_for(int ntiles) {
     return b;
 }
 
-// Stable sort of the pairs by tile key, values = pair indices (implicit iota
-// in the first pass).  Double-buffered over (tkey, tkey_alt) x (perm,
-// perm_alt); *in_alt tells where the result is.
+// Stable sort of the pairs by tile key, values = group-local pair indices
+// (implicit iota in the first pass).  Double-buffered over (tkey, tkey_alt) x
+// (perm, perm_alt); *in_alt tells where the result is.
 cudaError_t tile_sort(void *temp, size_t temp_bytes, bool key16, void *tkey, void *tkey_alt,
                       int32_t *perm, int32_t *perm_alt, int64_t K, int nkeys, bool *in_alt,
                       cudaStream_t st) {

@@ -7,7 +7,10 @@ namespace {
 
 constexpr int kBins = 256;             // 8-bit digits
 constexpr int kSortThreads = 256;      // 8 warps; thread t owns digit t in the look-back
-constexpr int kSortIpt = 16;           // keys per thread
+#ifndef POTR_SORT_IPT
+#define POTR_SORT_IPT 16
+#endif
+constexpr int kSortIpt = POTR_SORT_IPT;  // keys per thread
 constexpr int kTileItems = kSortThreads * kSortIpt;
 constexpr int kSortWarps = kSortThreads / 32;
 static_assert(kSortThreads == kBins, "one thread per digit");
@@ -24,14 +27,6 @@ __device__ __forceinline__ uint64_t ld_relaxed(const uint64_t *p) {
     asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
     return v;
 }
-__device__ __forceinline__ void st_release(uint32_t *p, uint32_t v) {
-    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
-__device__ __forceinline__ uint32_t ld_acquire(const uint32_t *p) {
-    uint32_t v;
-    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-    return v;
-}
 
 template <typename K>
 __device__ __forceinline__ uint32_t digit_of(K k, int shift) {
@@ -46,6 +41,21 @@ template <typename V>
 __global__ void k_iota_vals(int64_t n, V *v) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i < n) v[i] = (V)i;
+}
+
+// Lanes holding the same 8-bit digit (d < 256), or the same invalid marker
+// (d = 256): eight ballots on the digit bits -- full-rate VOTE/LOP instead of
+// MATCH, whose address-divergence-unit pipe saturated in the first version.
+__device__ __forceinline__ unsigned digit_peers(uint32_t d) {
+    const unsigned FULL = 0xffffffffu;
+    unsigned peers = __ballot_sync(FULL, d >> 8) ;
+    peers = (d >> 8) ? peers : ~peers;
+#pragma unroll
+    for (int b = 0; b < 8; b++) {
+        const unsigned x = __ballot_sync(FULL, (d >> b) & 1u);
+        peers &= ((d >> b) & 1u) ? x : ~x;
+    }
+    return peers;
 }
 
 int passes_for(int begin_bit, int end_bit) {
@@ -73,34 +83,50 @@ __device__ __forceinline__ uint32_t block_exclusive_scan(uint32_t v, uint32_t *w
     return before + x - v;
 }
 
-// All passes' digit histograms in one read of the keys.  Lanes holding the
-// same digit add together (__match_any_sync), so a constant digit costs one
-// shared atomic per warp instead of 32 colliding ones.
+// All passes' digit histograms in one read of the keys: shared atomics into
+// two sub-histograms per CTA (even / odd warps), with a warp-uniform digit
+// (a constant byte, common in the high digits) added once per warp.
 template <typename K>
 __global__ void __launch_bounds__(256) k_radix_hist(const K *__restrict__ keys, int64_t n,
                                                    int begin_bit, int passes,
                                                    uint32_t *__restrict__ hist) {
-    __shared__ uint32_t h[8 * kBins];
-    for (int i = threadIdx.x; i < passes * kBins; i += blockDim.x) h[i] = 0;
+    __shared__ uint32_t h[2][8 * kBins];
+    for (int i = threadIdx.x; i < 2 * 8 * kBins; i += blockDim.x) (&h[0][0])[i] = 0;
     __syncthreads();
     const int lane = threadIdx.x & 31;
-    for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < n;
-         base += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t i = base + threadIdx.x;
-        const bool v = i < n;
-        const K k = v ? keys[i] : (K)0;
-        for (int p = 0; p < passes; p++) {
-            const uint32_t d = v ? digit_of(k, begin_bit + 8 * p) : kBins;
-            const unsigned peers = __match_any_sync(0xffffffffu, d);
-            if (v && lane == __ffs(peers) - 1) atomicAdd(&h[p * kBins + d], __popc(peers));
+    uint32_t *hw = h[(threadIdx.x >> 5) & 1];
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x * 4;
+    for (int64_t base = (int64_t)blockIdx.x * blockDim.x * 4; base < n; base += stride) {
+        K k[4];
+        bool v[4];
+#pragma unroll
+        for (int q = 0; q < 4; q++) {
+            const int64_t i = base + q * blockDim.x + threadIdx.x;
+            v[q] = i < n;
+            k[q] = v[q] ? keys[i] : (K)0;
+        }
+#pragma unroll
+        for (int q = 0; q < 4; q++) {
+            const bool all = __all_sync(0xffffffffu, v[q]);
+            for (int p = 0; p < passes; p++) {
+                const uint32_t d = digit_of(k[q], begin_bit + 8 * p);
+                if (all && __all_sync(0xffffffffu, d == __shfl_sync(0xffffffffu, d, 0))) {
+                    if (lane == 0) atomicAdd(&hw[p * kBins + d], 32u);
+                } else if (v[q]) {
+                    atomicAdd(&hw[p * kBins + d], 1u);
+                }
+            }
         }
     }
     __syncthreads();
-    for (int i = threadIdx.x; i < passes * kBins; i += blockDim.x)
-        if (h[i]) atomicAdd(&hist[i], h[i]);
+    for (int i = threadIdx.x; i < passes * kBins; i += blockDim.x) {
+        const uint32_t c = h[0][i] + h[1][i];
+        if (c) atomicAdd(&hist[i], c);
+    }
 }
 
-// One LSD pass over digit (key >> shift) & 255.
+// One LSD pass over digit (key >> shift) & 255.  Dynamic shared memory: the
+// tile's keys and values staged in digit order (kTileItems each).
 template <typename K, typename V, bool IOTA>
 __global__ void __launch_bounds__(kSortThreads) k_onesweep(const K *__restrict__ kin,
                                                            K *__restrict__ kout,
@@ -109,15 +135,14 @@ __global__ void __launch_bounds__(kSortThreads) k_onesweep(const K *__restrict__
                                                            int shift,
                                                            const uint32_t *__restrict__ hist,
                                                            uint64_t *status, uint32_t *tile_ctr) {
-    constexpr int kStageBytes = kTileItems * (sizeof(K) > sizeof(V) ? sizeof(K) : sizeof(V));
     __shared__ uint32_t whist[kSortWarps][kBins];  // per-warp digit counts -> offsets
     __shared__ uint32_t boff[kBins];               // tile-local start of each digit
     __shared__ int64_t gbase[kBins];               // global start of the digit minus boff
     __shared__ uint32_t warp_tot[kSortWarps];
     __shared__ uint32_t tile_s;
-    __shared__ __align__(16) unsigned char stage_raw[kStageBytes];
-    K *stage_k = reinterpret_cast<K *>(stage_raw);
+    extern __shared__ __align__(16) unsigned char stage_raw[];
     V *stage_v = reinterpret_cast<V *>(stage_raw);
+    K *stage_k = reinterpret_cast<K *>(stage_raw + sizeof(V) * kTileItems);
 
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, t = threadIdx.x;
     const unsigned FULL = 0xffffffffu;
@@ -144,7 +169,9 @@ __global__ void __launch_bounds__(kSortThreads) k_onesweep(const K *__restrict__
         const int j = wbase + i * 32 + lane;
         const bool v = j < tile_n;
         const uint32_t d = v ? digit_of(k[i], shift) : kBins;
-        const unsigned peers = __match_any_sync(FULL, d);
+        // alternate the two ways of finding equal digits so that neither the
+        // ADU (MATCH) nor the ALU (VOTE/LOP) pipe limits the ranking alone
+        const unsigned peers = (i & 1) ? __match_any_sync(FULL, d) : digit_peers(d);
         const int leader = __ffs(peers) - 1;
         uint32_t b = 0;
         if (v && lane == leader) {
@@ -173,13 +200,26 @@ __global__ void __launch_bounds__(kSortThreads) k_onesweep(const K *__restrict__
     const uint32_t global_start = block_exclusive_scan(hcount, warp_tot);
     uint64_t prefix = 0;
     if (tile > 0) {
+        // four predecessors per step (independent loads): the look-back walks
+        // over tiles that have only published their own count
         for (int64_t j = tile - 1;;) {
-            const uint64_t s = ld_relaxed(status + j * kBins + t);
-            const uint64_t flag = s & ~kValMask;
-            if (flag == 0) continue;  // predecessor not published yet
-            prefix += s & kValMask;
-            if (flag == kFlagInc) break;
-            j--;
+            uint64_t s4[4];
+#pragma unroll
+            for (int q = 0; q < 4; q++)
+                s4[q] = j - q >= 0 ? ld_relaxed(status + (j - q) * kBins + t) : kFlagInc;
+            int q = 0;
+            bool done = false;
+            for (; q < 4; q++) {
+                const uint64_t flag = s4[q] & ~kValMask;
+                if (flag == 0) break;  // not published yet: reload from here
+                prefix += s4[q] & kValMask;
+                if (flag == kFlagInc) {
+                    done = true;
+                    break;
+                }
+            }
+            if (done) break;
+            j -= q;
         }
         st_relaxed(my_status, kFlagInc | (prefix + cnt));
     }
@@ -187,44 +227,44 @@ __global__ void __launch_bounds__(kSortThreads) k_onesweep(const K *__restrict__
     gbase[t] = (int64_t)global_start + (int64_t)prefix - (int64_t)local_start;
     __syncthreads();
 
-    // keys: into tile order through shared memory, then out in digit runs
-    int pos[kSortIpt];
+    // keys and values into digit order through shared memory ...
 #pragma unroll
     for (int i = 0; i < kSortIpt; i++) {
         const int j = wbase + i * 32 + lane;
-        pos[i] = -1;
         if (j < tile_n) {
             const uint32_t d = digit_of(k[i], shift);
-            pos[i] = (int)(boff[d] + whist[w][d] + rank[i]);
-            stage_k[pos[i]] = k[i];
+            const int pos = (int)(boff[d] + whist[w][d] + rank[i]);
+            stage_k[pos] = k[i];
+            stage_v[pos] = IOTA ? (V)(base + j) : vin[base + j];
         }
     }
     __syncthreads();
-    int64_t dst[kSortIpt];
-#pragma unroll
-    for (int i = 0; i < kSortIpt; i++) {
-        const int j = t + i * kSortThreads;
-        dst[i] = -1;
-        if (j < tile_n) {
-            const K kk = stage_k[j];
-            dst[i] = gbase[digit_of(kk, shift)] + j;
-            kout[dst[i]] = kk;
-        }
-    }
-    __syncthreads();
-    // values: the same permutation
-#pragma unroll
-    for (int i = 0; i < kSortIpt; i++) {
-        const int j = wbase + i * 32 + lane;
-        if (pos[i] >= 0) stage_v[pos[i]] = IOTA ? (V)(base + j) : vin[base + j];
-    }
-    __syncthreads();
-#pragma unroll
-    for (int i = 0; i < kSortIpt; i++) {
-        const int j = t + i * kSortThreads;
-        if (dst[i] >= 0) vout[dst[i]] = stage_v[j];
+    // ... then out in digit runs (consecutive addresses per digit)
+#pragma unroll 4
+    for (int j = t; j < tile_n; j += kSortThreads) {
+        const K kk = stage_k[j];
+        const int64_t dst = gbase[digit_of(kk, shift)] + j;
+        kout[dst] = kk;
+        vout[dst] = stage_v[j];
     }
 }
+
+template <typename K, typename V>
+constexpr size_t onesweep_smem() {
+    return (sizeof(K) + sizeof(V)) * (size_t)kTileItems;
+}
+
+template <typename K, typename V, bool IOTA>
+void set_smem_attr() {
+    static bool done = false;
+    if (!done) {
+        cudaFuncSetAttribute(k_onesweep<K, V, IOTA>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)onesweep_smem<K, V>());
+        done = true;
+    }
+}
+
 
 struct SortLayout {
     uint32_t *hist;      // passes x 256
@@ -296,36 +336,45 @@ __device__ __forceinline__ T block_exclusive(T v, Op op, T *warp_tot, T *total) 
     return r;
 }
 
-// Thread 0: publish the tile aggregate, look back for the exclusive prefix of
-// all earlier tiles, publish the inclusive value.  vals[2j] / vals[2j+1] hold
-// tile j's aggregate / inclusive value (as int64), flags[j] = 1 / 2 once
-// they are written.  The values are read with L1-bypassing loads: another
-// CTA on this SM may have cached the line when only the aggregate was there.
+// Warp 0: publish the tile aggregate, look back for the exclusive prefix of
+// all earlier tiles (32 predecessors per step, one per lane), publish the
+// inclusive value.  status[j] packs tile j's flag (kFlagAgg / kFlagInc, top
+// two bits) with its value (biased by 2^31 so int32 maxima stay
+// non-negative) in one 64-bit word: a single relaxed load sees a consistent
+// pair, so no acquire (which invalidates L1) and no fence are needed.
+constexpr int64_t kScanBias = (int64_t)1 << 31;
+
 template <typename T, typename Op>
-__device__ T tile_lookback(int64_t tile, T aggregate, Op op, uint32_t *flags, int64_t *vals) {
+__device__ T tile_lookback(int64_t tile, T aggregate, Op op, uint64_t *status) {
+    const unsigned FULL = 0xffffffffu;
+    const int lane = threadIdx.x & 31;
+    const auto pack = [](uint64_t flag, T x) {
+        return flag | ((uint64_t)((int64_t)x + kScanBias) & kValMask);
+    };
     if (tile == 0) {
-        st_relaxed(reinterpret_cast<uint64_t *>(&vals[1]), (uint64_t)(int64_t)aggregate);
-        __threadfence();
-        st_release(&flags[0], 2u);
+        if (lane == 0) st_relaxed(&status[0], pack(kFlagInc, aggregate));
         return Op::identity();
     }
-    st_relaxed(reinterpret_cast<uint64_t *>(&vals[2 * tile]), (uint64_t)(int64_t)aggregate);
-    __threadfence();
-    st_release(&flags[tile], 1u);
+    if (lane == 0) st_relaxed(&status[tile], pack(kFlagAgg, aggregate));
     T prefix = Op::identity();
     for (int64_t j = tile - 1;;) {
-        const uint32_t f = ld_acquire(&flags[j]);
-        if (f == 0) continue;
-        const int64_t x = (int64_t)ld_relaxed(
-            reinterpret_cast<const uint64_t *>(&vals[f == 2u ? 2 * j + 1 : 2 * j]));
-        prefix = op((T)x, prefix);
-        if (f == 2u) break;
-        j--;
+        const int64_t idx = j - lane;
+        const uint64_t sw = idx >= 0 ? ld_relaxed(&status[idx]) : pack(kFlagInc, Op::identity());
+        const uint64_t f = sw & ~kValMask;
+        const unsigned inc = __ballot_sync(FULL, f == kFlagInc);
+        const unsigned zero = __ballot_sync(FULL, f == 0);
+        const int k = inc ? __ffs(inc) - 1 : 31;
+        const unsigned need = (2u << k) - 1u;  // lanes 0..k (k = 31: all)
+        if (zero & need) continue;              // a needed predecessor is not published yet
+        T x = ((need >> lane) & 1u) ? (T)((int64_t)(sw & kValMask) - kScanBias)
+                                     : Op::identity();
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) x = op(x, __shfl_xor_sync(FULL, x, o));
+        prefix = op(prefix, x);
+        if (inc) break;
+        j -= 32;
     }
-    st_relaxed(reinterpret_cast<uint64_t *>(&vals[2 * tile + 1]),
-               (uint64_t)(int64_t)op(prefix, aggregate));
-    __threadfence();
-    st_release(&flags[tile], 2u);
+    if (lane == 0) st_relaxed(&status[tile], pack(kFlagInc, op(prefix, aggregate)));
     return prefix;
 }
 
@@ -333,6 +382,10 @@ __device__ T tile_lookback(int64_t tile, T aggregate, Op op, uint32_t *flags, in
 // MODE 1: out[i] = exclusive sum of in64[i]           (T = int64_t)
 // MODE 2: out[i] = inclusive max of in32[i]           (T = int32_t)
 // MODE 3: out32[k] = in32[i], i the k-th flagged item (T = int64_t); *count
+// Warp-striped: warp w of the tile owns items w*32*IPT + r*32 + lane, so
+// every load and store is coalesced; each warp scans its rounds in order with
+// shuffles, the warps' totals are combined in shared memory, and the tile's
+// prefix comes from the look-back.
 template <int MODE, typename T, typename Op>
 __global__ void __launch_bounds__(kScanThreads) k_scan(const int32_t *__restrict__ ids,
                                                        const int32_t *__restrict__ in32,
@@ -341,56 +394,92 @@ __global__ void __launch_bounds__(kScanThreads) k_scan(const int32_t *__restrict
                                                        T *__restrict__ out,
                                                        int32_t *__restrict__ out32,
                                                        int32_t *count, int64_t n,
-                                                       uint32_t *tile_ctr, uint32_t *flags,
-                                                       int64_t *vals) {
-    __shared__ T warp_tot[kScanThreads / 32];
-    __shared__ T s_total, s_prefix;
+                                                       uint32_t *tile_ctr, uint64_t *status) {
+    constexpr int W = kScanThreads / 32;
+    __shared__ T warp_sum[W];
+    __shared__ T warp_pre[W];
+    __shared__ T s_prefix;
     __shared__ uint32_t tile_s;
+    const unsigned FULL = 0xffffffffu;
     const Op op;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     if (threadIdx.x == 0) tile_s = atomicAdd(tile_ctr, 1u);
     __syncthreads();
     const int64_t tile = tile_s;
-    const int64_t i0 = tile * kScanTile + (int64_t)threadIdx.x * kScanIpt;
-    T x[kScanIpt];
-    T acc = Op::identity();
+    const int64_t wbase = tile * kScanTile + (int64_t)w * 32 * kScanIpt;
+    T v[kScanIpt];
+    int32_t idv[kScanIpt];
+    if (MODE == 0) {
 #pragma unroll
-    for (int q = 0; q < kScanIpt; q++) {
-        const int64_t i = i0 + q;
-        T v = Op::identity();
+        for (int r = 0; r < kScanIpt; r++) {
+            const int64_t i = wbase + r * 32 + lane;
+            idv[r] = i < n ? ids[i] : -1;
+        }
+    }
+#pragma unroll
+    for (int r = 0; r < kScanIpt; r++) {
+        const int64_t i = wbase + r * 32 + lane;
+        T x = Op::identity();
         if (i < n) {
-            if (MODE == 0) v = (T)cnt_gather(ids, in32, i);
-            if (MODE == 1) v = (T)in64[i];
-            if (MODE == 2) v = (T)in32[i];
-            if (MODE == 3) v = (T)(flg[i] != 0);
+            if (MODE == 0) x = (T)in32[idv[r]];
+            if (MODE == 1) x = (T)in64[i];
+            if (MODE == 2) x = (T)in32[i];
+            if (MODE == 3) x = (T)(flg[i] != 0);
         }
-        x[q] = v;
-        acc = op(acc, v);
+        v[r] = x;
     }
-    const T excl = block_exclusive(acc, op, warp_tot, &s_total);
-    if (threadIdx.x == 0) s_prefix = tile_lookback(tile, s_total, op, flags, vals);
-    __syncthreads();
-    T run = op(s_prefix, excl);
+    // warp-inclusive values over the rounds; own values kept for the
+    // exclusive modes (sums: excl = incl - own)
+    T carry = Op::identity();
+    T own[kScanIpt];
 #pragma unroll
-    for (int q = 0; q < kScanIpt; q++) {
-        const int64_t i = i0 + q;
-        if (i >= n) break;
-        if (MODE == 0 || MODE == 2) {
-            run = op(run, x[q]);
-            out[i] = run;
-        } else if (MODE == 1) {
-            out[i] = run;
-            run = op(run, x[q]);
-        } else {
-            if (x[q]) out32[run] = in32[i];
-            run = op(run, x[q]);
+    for (int r = 0; r < kScanIpt; r++) {
+        own[r] = v[r];
+        T x = v[r];
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const T y = __shfl_up_sync(FULL, x, o);
+            if (lane >= o) x = op(y, x);
+        }
+        x = op(carry, x);
+        v[r] = x;
+        carry = __shfl_sync(FULL, x, 31);
+    }
+    if (lane == 0) warp_sum[w] = carry;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        T acc = Op::identity();
+        if (lane == 0) {
+            for (int q = 0; q < W; q++) {
+                warp_pre[q] = acc;
+                acc = op(acc, warp_sum[q]);
+            }
+        }
+        acc = __shfl_sync(FULL, acc, 0);
+        const T p = tile_lookback(tile, acc, op, status);
+        if (lane == 0) s_prefix = p;
+    }
+    __syncthreads();
+    const T base = op(s_prefix, warp_pre[w]);
+    T last = Op::identity();
+#pragma unroll
+    for (int r = 0; r < kScanIpt; r++) {
+        const int64_t i = wbase + r * 32 + lane;
+        const T incl = op(base, v[r]);
+        if (i < n) {
+            if (MODE == 0 || MODE == 2) out[i] = incl;
+            if (MODE == 1) out[i] = incl - own[r];
+            if (MODE == 3 && own[r]) out32[incl - 1] = in32[i];
+            if (i == n - 1) last = incl;
         }
     }
-    if (MODE == 3 && i0 < n && i0 + kScanIpt >= n) *count = (int32_t)run;
+    if (MODE == 3 && wbase <= n - 1 && n - 1 < wbase + 32 * kScanIpt && ((n - 1 - wbase) & 31) == lane)
+        *count = (int32_t)last;
 }
 
 struct ScanLayout {
-    uint32_t *ctr, *flags;
-    void *vals;
+    uint32_t *ctr;
+    uint64_t *status;
     size_t bytes;
 };
 
@@ -398,14 +487,9 @@ ScanLayout scan_layout(void *temp, int64_t n) {
     ScanLayout L;
     const int64_t tiles = (n + kScanTile - 1) / kScanTile;
     char *p = reinterpret_cast<char *>(temp);
-    size_t off = 0;
-    L.ctr = reinterpret_cast<uint32_t *>(p + off);
-    off += 256;
-    L.flags = reinterpret_cast<uint32_t *>(p + off);
-    off += align256(sizeof(uint32_t) * (size_t)(tiles > 0 ? tiles : 1));
-    L.vals = p + off;
-    off += align256(2 * sizeof(int64_t) * (size_t)(tiles > 0 ? tiles : 1));
-    L.bytes = off;
+    L.ctr = reinterpret_cast<uint32_t *>(p);
+    L.status = reinterpret_cast<uint64_t *>(p + 256);
+    L.bytes = 256 + align256(sizeof(uint64_t) * (size_t)(tiles > 0 ? tiles : 1));
     return L;
 }
 
@@ -420,11 +504,10 @@ cudaError_t run_scan(void *temp, size_t temp_bytes, const int32_t *ids, const in
     ScanLayout L = scan_layout(temp, n);
     if (L.bytes > temp_bytes) return cudaErrorInvalidValue;
     const int64_t tiles = (n + kScanTile - 1) / kScanTile;
-    cudaError_t e = cudaMemsetAsync(temp, 0, L.bytes - align256(2 * sizeof(int64_t) * tiles), st);
+    cudaError_t e = cudaMemsetAsync(temp, 0, L.bytes, st);
     if (e != cudaSuccess) return e;
     k_scan<MODE, T, Op><<<(unsigned)tiles, kScanThreads, 0, st>>>(
-        ids, in32, in64, flg, out, out32, count, n, L.ctr, L.flags,
-        reinterpret_cast<int64_t *>(L.vals));
+        ids, in32, in64, flg, out, out32, count, n, L.ctr, L.status);
     return cudaGetLastError();
 }
 
@@ -468,12 +551,16 @@ cudaError_t radix_sort_pairs(void *temp, size_t temp_bytes, K *keys, K *keys_alt
     for (int p = 0; p < passes; p++) {
         const int shift = begin_bit + 8 * p;
         uint64_t *status = L.status + (size_t)p * kBins * tiles;
-        if (p == 0 && iota_vals)
-            k_onesweep<K, V, true><<<(unsigned)tiles, kSortThreads, 0, st>>>(
+        constexpr size_t smem = onesweep_smem<K, V>();
+        if (p == 0 && iota_vals) {
+            set_smem_attr<K, V, true>();
+            k_onesweep<K, V, true><<<(unsigned)tiles, kSortThreads, smem, st>>>(
                 ka, kb, nullptr, vb, n, shift, L.hist + p * kBins, status, L.ctr + p);
-        else
-            k_onesweep<K, V, false><<<(unsigned)tiles, kSortThreads, 0, st>>>(
+        } else {
+            set_smem_attr<K, V, false>();
+            k_onesweep<K, V, false><<<(unsigned)tiles, kSortThreads, smem, st>>>(
                 ka, kb, va, vb, n, shift, L.hist + p * kBins, status, L.ctr + p);
+        }
         e = cudaGetLastError();
         if (e != cudaSuccess) return e;
         K *tk = ka;
