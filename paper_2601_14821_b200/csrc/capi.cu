@@ -57,6 +57,7 @@ struct potr_ctx {
     DevBuf tile_counter, ci_v, dm_v, bbox, overflow, vidx, khi, skhi, prep, spans;
     DevBuf met_mom, met_part, met_w, met_out;  // image metrics scratch
     DevBuf sort_k, sort_v, rm_keys;            // potr_sort_pairs_u64 / potr_removal_order
+    DevBuf sh_scratch;                         // SH solve size classes
     void *codec_scratch = nullptr;             // codec back end scratch
     size_t codec_cap = 0;
     DevBuf codec_eyes;
@@ -693,7 +694,7 @@ void potr_destroy(potr_ctx *ctx) {
                       &ctx->slot_sh, &ctx->slot_opac, &ctx->slot_prep})
         if (b->p) cudaFree(b->p);
     for (DevBuf *b : {&ctx->met_mom, &ctx->met_part, &ctx->met_w, &ctx->met_out, &ctx->codec_eyes,
-                      &ctx->sort_k, &ctx->sort_v, &ctx->rm_keys})
+                      &ctx->sort_k, &ctx->sort_v, &ctx->rm_keys, &ctx->sh_scratch})
         if (b->p) cudaFree(b->p);
     if (ctx->codec_scratch) cudaFree(ctx->codec_scratch);
     if (ctx->prep.p) cudaFree(ctx->prep.p);
@@ -992,8 +993,9 @@ int potr_sh_solve(potr_ctx *ctx, const potr_splats *splats, const double *normal
         return fail(ctx, POTR_E_ARG, "parallel_threshold must be in (0, 1]");
     {
         Stage _st(ctx, POTR_STAGE_SH_SOLVE);
-        LAUNCH(1, launch_sh_solve(*splats, normal_eqs, lambda_y, parallel_threshold, zero_threshold,
-                                  rgb, ycocg, status, ctx->stream));
+        ENSURE(ctx->sh_scratch, sh_solve_scratch_bytes(splats->n));
+        LAUNCH(5, launch_sh_solve(*splats, normal_eqs, lambda_y, parallel_threshold, zero_threshold,
+                                  rgb, ycocg, status, ctx->sh_scratch.p, ctx->stream));
         _st.end();
     }
     return POTR_OK;

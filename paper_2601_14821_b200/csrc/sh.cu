@@ -289,19 +289,250 @@ __device__ void coeffs_convert(const double *M, const double *in, double *out) {
         }
 }
 
-#ifndef POTR_SOLVE_MIN_BLOCKS
-#define POTR_SOLVE_MIN_BLOCKS 8  // 64 regs: 55 vs 70 ms per C3 solve+accumulate (1, 5, 6, 12, 16 measured)
-#endif
-__global__ void __launch_bounds__(128, POTR_SOLVE_MIN_BLOCKS) k_sh_solve(potr_splats sp, const double *__restrict__ neq,
-                                                  double lambda_y, double par_thr,
-                                                  double zero_thr, double *rgb_out,
-                                                  double *ycocg_out,
-                                                  int8_t *__restrict__ status_out) {
-    const int64_t n = sp.n;
+// ---------------------------------------------------------------------------
+// The solves.  k_sh_mask first runs the parallel-column sparsification of
+// every splat (compaction.py:110-124) and files the splat under the size of
+// its kept set: the factor of every later system of the splat (pass 1 and
+// pass 2 of the three channels, masks that are subsets of the kept set) has
+// at most that many columns.  Each size class is then solved by a kernel
+// whose factor lives in registers, fully unrolled for its capacity
+// (k_sh_solve_reg<8>: 74% of the C3 splats, <12>: 23%); the rare larger
+// systems and the unseen splats' DC fallback run the generic kernel with the
+// factor in local memory.  Results do not depend on the class order: every
+// splat is solved independently, with the oracle's operation order
+// (potr_oracle.c chol_upper / chol_solve_upper / compact_one).
+
+// The kept set of one splat (G entries read in place from the (185, N) layout).
+__device__ unsigned sparsify_mask(const double *__restrict__ G, int64_t gs, double par_thr) {
+    double norms[16];
+#pragma unroll
+    for (int i = 0; i < 16; i++) norms[i] = sqrt(__ldg(G + tri(i, i) * gs));
+    unsigned mask = 1u;
+#pragma unroll
+    for (int i = 1; i < 16; i++) {
+        if (norms[i] == 0.0) continue;
+        bool par = false;
+#pragma unroll
+        for (int j = 0; j < i; j++) {
+            if (!(mask >> j & 1u)) continue;
+            const double gij = __ldg(G + tri(j, i) * gs);  // j < i
+            const double cs = fabs(gij) / (norms[i] * norms[j]);
+            if (cs > par_thr) par = true;
+        }
+        if (!par) mask |= 1u << i;
+    }
+    return mask;
+}
+
+constexpr int kSolveClasses = 4;  // 0: unseen, 1: <= 8 columns, 2: <= 12, 3: <= 16
+__device__ __forceinline__ int solve_class(unsigned mask) {
+    const int m = __popc(mask);
+    return m <= 8 ? 1 : m <= 12 ? 2 : 3;
+}
+
+__global__ void __launch_bounds__(128) k_sh_mask(int64_t n, const double *__restrict__ neq,
+                                                 double par_thr, uint16_t *__restrict__ masks,
+                                                 int *__restrict__ counts,
+                                                 int32_t *__restrict__ lists) {
     const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (k >= n) return;
+    int cls = -1;
+    if (k < n) {
+        unsigned mask = 0u;
+        if (neq[(int64_t)184 * n + k] == 0.0) {
+            cls = 0;
+        } else {
+            mask = sparsify_mask(neq + k, n, par_thr);
+            cls = solve_class(mask);
+        }
+        masks[k] = (uint16_t)mask;
+    }
+    // warp-aggregated append to the class lists (order is irrelevant: the
+    // splats are solved independently)
+    const int lane = threadIdx.x & 31;
+#pragma unroll
+    for (int c = 0; c < kSolveClasses; c++) {
+        const unsigned peers = __ballot_sync(0xffffffffu, cls == c);
+        if (!peers) continue;
+        int base = 0;
+        if (lane == __ffs(peers) - 1) base = atomicAdd(&counts[c], __popc(peers));
+        base = __shfl_sync(0xffffffffu, base, __ffs(peers) - 1);
+        if (cls == c) lists[(int64_t)c * n + base + __popc(peers & ((1u << lane) - 1u))] = (int32_t)k;
+    }
+}
+
+// Final (YCoCg -> RGB) or failed (original coefficients) outputs.
+__device__ void finish_splat(int status, const double *sh, double *rgb, double *yc) {
+    if (status == 2) {
+        for (int i = 0; i < 48; i++) rgb[i] = sh[i];
+        coeffs_convert(kRgbToYcocg, rgb, yc);
+    } else {
+        coeffs_convert(kYcocgToRgb, yc, rgb);
+    }
+}
+
+// --- register-resident solves, capacity MC columns ---------------------------
+
+template <int MC>
+__device__ __forceinline__ constexpr int trm(int i, int j) {  // packed upper, row-major
+    return i * MC - (i * (i - 1)) / 2 + (j - i);
+}
+
+// Upper Cholesky of the m x m leading block (m <= MC), unrolled; dpotrf 'U'
+// semantics.  Returns false when a pivot is <= 0 or NaN.
+template <int MC>
+__device__ __forceinline__ bool chol_reg(double (&U)[MC * (MC + 1) / 2], int m) {
+    bool ok = true;
+#pragma unroll
+    for (int j = 0; j < MC; j++) {
+        if (j < m && ok) {
+            double ajj = U[trm<MC>(j, j)];
+#pragma unroll
+            for (int k = 0; k < j; k++) ajj -= U[trm<MC>(k, j)] * U[trm<MC>(k, j)];
+            if (!(ajj > 0.0)) {
+                ok = false;
+            } else {
+                ajj = sqrt(ajj);
+                U[trm<MC>(j, j)] = ajj;
+#pragma unroll
+                for (int c = j + 1; c < MC; c++) {
+                    if (c < m) {
+                        double v = U[trm<MC>(j, c)];
+#pragma unroll
+                        for (int k = 0; k < j; k++) v -= U[trm<MC>(k, j)] * U[trm<MC>(k, c)];
+                        U[trm<MC>(j, c)] = v / ajj;
+                    }
+                }
+            }
+        }
+    }
+    return ok;
+}
+
+// dpotrs on the register factor: U^T y = b, U x = y
+template <int MC>
+__device__ __forceinline__ void chol_solve_reg(const double (&U)[MC * (MC + 1) / 2], int m,
+                                               double (&b)[MC]) {
+#pragma unroll
+    for (int i = 0; i < MC; i++) {
+        if (i < m) {
+            double v = b[i];
+#pragma unroll
+            for (int k = 0; k < i; k++) v -= U[trm<MC>(k, i)] * b[k];
+            b[i] = v / U[trm<MC>(i, i)];
+        }
+    }
+#pragma unroll
+    for (int i = MC - 1; i >= 0; i--) {
+        if (i < m) {
+            double v = b[i];
+#pragma unroll
+            for (int k = i + 1; k < MC; k++)
+                if (k < m) v -= U[trm<MC>(i, k)] * b[k];
+            b[i] = v / U[trm<MC>(i, i)];
+        }
+    }
+}
+
+template <int MC>
+__global__ void __launch_bounds__(128, MC <= 8 ? 4 : 2)
+    k_sh_solve_reg(potr_splats sp, const double *__restrict__ neq,
+                   const uint16_t *__restrict__ masks, const int32_t *__restrict__ list,
+                   const int *__restrict__ count, double lambda_y, double zero_thr,
+                   double *rgb_out, double *ycocg_out, int8_t *__restrict__ status_out) {
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= *count) return;
+    const int64_t n = sp.n;
+    const int64_t k = list[t];
+    const double *G = neq + k, *B = neq + (int64_t)136 * n + k;
+    const unsigned mask1 = masks[k];
+    double *yc = ycocg_out + 48 * k;
+    double U[MC * (MC + 1) / 2];
+    double b[MC];
+    int cols[MC];
+    // compact_splat (:169-192) as five factor/solve tasks: Y pass 1 (lambda),
+    // Y pass 2, Co+Cg pass 1 (3 lambda, one factor, two right-hand sides),
+    // Co pass 2, Cg pass 2.  A RidgeError anywhere keeps the original
+    // coefficients, so Cg's pass 1 before Co's pass 2 changes no output.
+    unsigned drop0 = 0u, drop1 = 0u, drop2 = 0u;
+    int status = 0;
+#pragma unroll 1
+    for (int task = 0; task < 5; task++) {
+        const unsigned mask = task == 0 || task == 2 ? mask1
+                              : mask1 & ~(task == 1 ? drop0 : task == 3 ? drop1 : drop2);
+        const double lam = task < 2 ? lambda_y : 3.0 * lambda_y;
+        const int m = __popc(mask);
+        unsigned mm = mask;
+#pragma unroll
+        for (int i = 0; i < MC; i++) {
+            cols[i] = mm ? __ffs(mm) - 1 : 0;
+            mm &= mm - 1u;
+        }
+        int rc = -1;
+#pragma unroll 1
+        for (int attempt = 0; attempt < 2; attempt++) {
+#pragma unroll
+            for (int i = 0; i < MC; i++)
+#pragma unroll
+                for (int j = i; j < MC; j++)
+                    if (j < m) U[trm<MC>(i, j)] = __ldg(G + tri(cols[i], cols[j]) * n);
+#pragma unroll
+            for (int i = 0; i < MC; i++) {
+                if (i < m) {
+                    U[trm<MC>(i, i)] += (cols[i] == 0) ? 0.0 : lam;
+                    if (attempt) U[trm<MC>(i, i)] += 1e-10;
+                }
+            }
+            if (chol_reg<MC>(U, m)) {
+                rc = attempt;
+                break;
+            }
+        }
+        if (rc < 0) {
+            status = 2;
+            break;
+        }
+        status |= rc;
+#pragma unroll 1
+        for (int r = 0; r < (task == 2 ? 2 : 1); r++) {
+            const int ch = task < 2 ? 0 : task == 2 ? 1 + r : task - 2;
+#pragma unroll
+            for (int i = 0; i < MC; i++)
+                if (i < m) b[i] = __ldg(B + (cols[i] * 3 + ch) * n);
+            chol_solve_reg<MC>(U, m, b);
+            if (task == 1 || task >= 3) {
+                for (int i = 0; i < 16; i++) yc[ch * 16 + i] = 0.0;
+#pragma unroll
+                for (int i = 0; i < MC; i++)
+                    if (i < m) yc[ch * 16 + cols[i]] = b[i];
+            } else {
+                unsigned d = 0u;
+#pragma unroll
+                for (int i = 0; i < MC; i++)
+                    if (i < m && cols[i] > 0 && fabs(b[i]) < zero_thr) d |= 1u << cols[i];
+                if (task == 0) drop0 = d;
+                else if (r == 0) drop1 = d;
+                else drop2 = d;
+            }
+        }
+    }
+    finish_splat(status, sp.sh + 48 * k, rgb_out + 48 * k, yc);
+    status_out[k] = (int8_t)status;
+}
+
+// --- the generic solve (any size; unseen splats' DC fallback) ----------------
+
+__global__ void __launch_bounds__(128) k_sh_solve(potr_splats sp, const double *__restrict__ neq,
+                                                  const uint16_t *__restrict__ masks,
+                                                  const int32_t *__restrict__ list,
+                                                  const int *__restrict__ count,
+                                                  double lambda_y, double zero_thr,
+                                                  double *rgb_out, double *ycocg_out,
+                                                  int8_t *__restrict__ status_out) {
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= *count) return;
+    const int64_t n = sp.n;
+    const int64_t k = list[t];
     const double *sh = sp.sh + 48 * k;
-    // the coefficients are built in place in the outputs (no per-thread copies)
     double *rgb = rgb_out + 48 * k, *yc = ycocg_out + 48 * k;
     int status = 0;
     if (neq[(int64_t)184 * n + k] == 0.0) {
@@ -316,7 +547,7 @@ __global__ void __launch_bounds__(128, POTR_SOLVE_MIN_BLOCKS) k_sh_solve(potr_sp
                     sh_basis16(i / nrm, j / nrm, q / nrm, basis);
                     for (int c = 0; c < 3; c++) {
                         double col = 0.0;
-                        for (int t = 0; t < 16; t++) col += basis[t] * sh[c * 16 + t];
+                        for (int t2 = 0; t2 < 16; t2++) col += basis[t2] * sh[c * 16 + t2];
                         acc[c] += col;
                     }
                 }
@@ -325,29 +556,8 @@ __global__ void __launch_bounds__(128, POTR_SOLVE_MIN_BLOCKS) k_sh_solve(potr_sp
         coeffs_convert(kRgbToYcocg, rgb, yc);
         status = 3;
     } else {
-        // G (136, upper triangle) and B (48) read in place from the (185, N)
-        // layout: lane k's entry e is neq[e * n + k]
         const double *G = neq + k, *B = neq + (int64_t)136 * n + k;
-        // sparsify_parallel_columns (compaction.py:110-124)
-        double norms[16];
-        for (int i = 0; i < 16; i++) norms[i] = sqrt(__ldg(G + tri(i, i) * n));
-        unsigned mask = 1u;
-        for (int i = 1; i < 16; i++) {
-            if (norms[i] == 0.0) continue;
-            bool par = false;
-            for (int j = 0; j < i; j++) {
-                if (!(mask >> j & 1u)) continue;
-                const double gij = __ldg(G + tri(j, i) * n);  // j < i
-                double cs = fabs(gij) / (norms[i] * norms[j]);
-                if (cs > par_thr) par = true;
-            }
-            if (!par) mask |= 1u << i;
-        }
-        // compact_splat (:169-192): per channel a pass-1 solve on the mask and a
-        // pass-2 re-solve without the small AC terms.  Co and Cg share lambda
-        // (3 lambda, :56-59) and the pass-1 mask, hence one pass-1 factor; a
-        // RidgeError anywhere keeps the original coefficients, so computing
-        // Cg's pass 1 before Co's pass 2 changes no output.
+        const unsigned mask = masks[k];
         double Af[136], first[16], first2[16];
         int cols[16], m, rc;
         for (int ch = 0; ch < 3 && status != 2; ch++) {
@@ -363,9 +573,8 @@ __global__ void __launch_bounds__(128, POTR_SOLVE_MIN_BLOCKS) k_sh_solve(potr_sp
             } else {
                 for (int i = 0; i < 16; i++) first[i] = first2[i];
             }
-            rc = factor_channel(G, n, pass2_mask(mask, first, zero_thr), ch == 0 ? lambda_y
-                                                                              : 3.0 * lambda_y,
-                                Af, cols, &m);
+            rc = factor_channel(G, n, pass2_mask(mask, first, zero_thr),
+                                ch == 0 ? lambda_y : 3.0 * lambda_y, Af, cols, &m);
             if (rc < 0) {
                 status = 2;
                 break;
@@ -373,12 +582,7 @@ __global__ void __launch_bounds__(128, POTR_SOLVE_MIN_BLOCKS) k_sh_solve(potr_sp
             if (rc > 0) status = 1;
             solve_factored(Af, m, cols, B, n, ch, yc + ch * 16);
         }
-        if (status == 2) {
-            for (int i = 0; i < 48; i++) rgb[i] = sh[i];
-            coeffs_convert(kRgbToYcocg, rgb, yc);
-        } else {
-            coeffs_convert(kYcocgToRgb, yc, rgb);
-        }
+        finish_splat(status, sh, rgb, yc);
     }
     status_out[k] = (int8_t)status;
 }
@@ -391,12 +595,35 @@ cudaError_t launch_sh_accumulate(const potr_splats &sp, int ncam, const double *
     return cudaGetLastError();
 }
 
+size_t sh_solve_scratch_bytes(int64_t n) {
+    // masks (u16), class counts, class lists (int32 x n each)
+    return ((sizeof(uint16_t) * (size_t)n + 255) & ~(size_t)255) + 256 +
+           sizeof(int32_t) * (size_t)kSolveClasses * (size_t)n;
+}
+
 cudaError_t launch_sh_solve(const potr_splats &sp, const double *neq, double lambda_y,
                             double par_thr, double zero_thr, double *rgb, double *ycocg,
-                            int8_t *status, cudaStream_t st) {
-    if (sp.n == 0) return cudaSuccess;
-    k_sh_solve<<<(unsigned)((sp.n + 127) / 128), 128, 0, st>>>(sp, neq, lambda_y, par_thr,
-                                                                zero_thr, rgb, ycocg, status);
+                            int8_t *status, void *scratch, cudaStream_t st) {
+    const int64_t n = sp.n;
+    if (n == 0) return cudaSuccess;
+    char *p = reinterpret_cast<char *>(scratch);
+    uint16_t *masks = reinterpret_cast<uint16_t *>(p);
+    p += (sizeof(uint16_t) * (size_t)n + 255) & ~(size_t)255;
+    int *counts = reinterpret_cast<int *>(p);
+    p += 256;
+    int32_t *lists = reinterpret_cast<int32_t *>(p);
+    cudaError_t e = cudaMemsetAsync(counts, 0, sizeof(int) * kSolveClasses, st);
+    if (e != cudaSuccess) return e;
+    const unsigned g = (unsigned)((n + 127) / 128);
+    k_sh_mask<<<g, 128, 0, st>>>(n, neq, par_thr, masks, counts, lists);
+    k_sh_solve_reg<8><<<g, 128, 0, st>>>(sp, neq, masks, lists + n, counts + 1, lambda_y,
+                                         zero_thr, rgb, ycocg, status);
+    k_sh_solve_reg<12><<<g, 128, 0, st>>>(sp, neq, masks, lists + 2 * n, counts + 2, lambda_y,
+                                          zero_thr, rgb, ycocg, status);
+    k_sh_solve<<<g, 128, 0, st>>>(sp, neq, masks, lists + 3 * n, counts + 3, lambda_y, zero_thr,
+                                  rgb, ycocg, status);
+    k_sh_solve<<<g, 128, 0, st>>>(sp, neq, masks, lists, counts, lambda_y, zero_thr, rgb, ycocg,
+                                  status);
     return cudaGetLastError();
 }
 
