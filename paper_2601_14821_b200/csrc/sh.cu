@@ -28,50 +28,53 @@ __device__ __forceinline__ int tri(int i, int j) { return i * 16 - (i * (i - 1))
 __constant__ double kRgbToYcocg[9] = {0.25, 0.5, 0.25, 0.5, 0.0, -0.5, -0.25, 0.5, -0.25};
 __constant__ double kYcocgToRgb[9] = {1.0, 1.0, -1.0, 1.0, 0.0, 1.0, 1.0, -1.0, -1.0};
 
-// Normal equations of 16 consecutive splats per CTA (4 warps x 4 splats).  Views are taken 32 at a
-// time: the (view, splat) tile of camera_importance is staged in shared
-// memory with coalesced loads; then for each splat a warp evaluates one view
-// per lane (direction, SH basis, raw colour, YCoCg -- compaction.py:100-107)
-// and publishes the row a = (w*y (16), w*YCoCg(colour) (3)) to shared memory.
+// Normal equations of 16 consecutive splats per CTA (4 warps x 4 splats,
+// processed as two pairs).  Views are taken 32 at a time: the (view, splat)
+// tile of camera_importance is staged in shared memory with coalesced loads;
+// then for a pair of splats each lane evaluates one view for both
+// (direction, SH basis, raw colour, YCoCg -- compaction.py:100-107) and
+// publishes the rows a = (w*y (16), w*YCoCg(colour) (3), 0) to shared memory.
 // The 184 wanted entries of a a^T -- G_ij, i <= j < 16, and B_ic = a_i a_16+c
-// -- are tiled by 2x4 register blocks (rows 2r, 2r+1; columns c0..c0+3): 28
-// lanes own one block each and add, per seen view in ascending order, 8 fused
-// products from three 16-byte shared loads.  Views a splat is not seen from
-// (w = 0) are skipped: they would add exact zeros, so the sums equal the
-// reference's sums over its `seen` rows (compaction.py:97-107, :114, :133-137).
+// -- are tiled by 4x4 register blocks (rows 4rb..4rb+3, columns
+// 4cb..4cb+3, cb >= rb): 14 blocks per splat, lanes 0-13 for the pair's
+// first splat and 16-29 for its second, each adding per seen view, in
+// ascending view order, 16 fused products from eight 8-byte shared loads
+// (the 2x4 blocks before this needed three 16-byte loads per 8 products and
+// ran shared-memory bound).  Views a splat is not seen from (w = 0) are skipped:
+// they would add exact zeros, so the sums equal the reference's sums over its
+// `seen` rows (compaction.py:97-107, :114, :133-137).
 #ifndef POTR_SH_MIN_BLOCKS
-#define POTR_SH_MIN_BLOCKS 4
+#define POTR_SH_MIN_BLOCKS 3
 #endif
-#ifndef POTR_SH_SPLATS
-#define POTR_SH_SPLATS 16
-#endif
-constexpr int kShSplatsPerBlock = POTR_SH_SPLATS;
+constexpr int kShSplatsPerBlock = 16;
 constexpr int kShWarps = 4;
-#ifndef POTR_SH_ROW
-#define POTR_SH_ROW 26
-#endif
-// w*y (16) + w*YCoCg (3), padded for the 2x4 blocks' 16-byte loads
-constexpr int kShRow = POTR_SH_ROW;
-constexpr int kShBlocks = 28;
+// Row layout: w*y at 0..15, w*YCoCg at 18..20, zeros at 16, 17, 21, 22.  The
+// odd stride keeps the 16 rows a half-warp stores per instruction on distinct
+// banks (an even stride made the row stores 4-way conflicted), and with the
+// YCoCg block at 18 and the second splat's rows 759 doubles further, the
+// sixteen 8-byte loads of one accumulation step fall on distinct banks.
+constexpr int kShRow = 23;
+constexpr int kShYc = 18;
+constexpr int kShBlocks = 14;
 #ifndef POTR_SH_UNROLL
 #define POTR_SH_UNROLL 4
 #endif
 constexpr int kShUnroll = POTR_SH_UNROLL;
 
-// Block b of the tiling: rows 2r, 2r+1; columns c0 .. c0+3 (c0 = 2r + 4t).
-__device__ __forceinline__ void sh_block(int b, int *r, int *c0) {
+// Block b (0..13) of the tiling: row block rb, column block cb >= rb.
+__device__ __forceinline__ void sh_block(int b, int *rb, int *cb) {
     int cum = 0;
-    for (int rr = 0; rr < 8; rr++) {
-        const int nb = (19 - 2 * rr + 3) / 4;
+    for (int r = 0; r < 4; r++) {
+        const int nb = 5 - r;
         if (b < cum + nb) {
-            *r = rr;
-            *c0 = 2 * rr + 4 * (b - cum);
+            *rb = r;
+            *cb = r + (b - cum);
             return;
         }
         cum += nb;
     }
-    *r = -1;
-    *c0 = 0;
+    *rb = 0;
+    *cb = 0;
 }
 
 // Entry index of (i, j), j >= i, in the (185, N) layout: G upper triangle
@@ -82,14 +85,15 @@ __device__ __forceinline__ int sh_entry(int i, int j) {
     return 136 + 3 * i + (j - 16);
 }
 
-__global__ void __launch_bounds__(32 * kShWarps, POTR_SH_MIN_BLOCKS) k_sh_accumulate(potr_splats sp, int ncam,
-                                                       const double *__restrict__ eyes,
-                                                       const double *__restrict__ cam_imp,
-                                                       double *__restrict__ neq) {
+__global__ void __launch_bounds__(32 * kShWarps, POTR_SH_MIN_BLOCKS)
+    k_sh_accumulate(potr_splats sp, int ncam, const double *__restrict__ eyes,
+                    const double *__restrict__ cam_imp, double *__restrict__ neq) {
     __shared__ double wtile[32][kShSplatsPerBlock + 1];
-    // row 32 of each warp's tile is a zero row: the unrolled accumulation pads
-    // with it (fma(0, 0, acc) == acc exactly, acc is never -0)
-    __shared__ __align__(16) double A[kShWarps][33][kShRow];
+    // per warp, per splat of the pair: 32 view rows + a zero row (the
+    // unrolled accumulation pads with it: fma(0, 0, acc) == acc exactly, acc
+    // is never -0)
+    extern __shared__ __align__(16) double sh_dyn[];
+    double(*A)[2][33][kShRow] = reinterpret_cast<double(*)[2][33][kShRow]>(sh_dyn);
     __shared__ double shs[kShSplatsPerBlock][48];
     __shared__ double pos[kShSplatsPerBlock][3];
     const int64_t n = sp.n;
@@ -100,20 +104,21 @@ __global__ void __launch_bounds__(32 * kShWarps, POTR_SH_MIN_BLOCKS) k_sh_accumu
         shs[i / 48][i % 48] = sp.sh[(k0 + i / 48) * 48 + i % 48];
     for (int i = threadIdx.x; i < nk * 3; i += blockDim.x)
         pos[i / 3][i % 3] = sp.positions[(k0 + i / 3) * 3 + i % 3];
-    for (int i = threadIdx.x; i < kShWarps * 33 * kShRow; i += blockDim.x)
-        (&A[0][0][0])[i] = 0.0;  // the pad columns stay zero
+    for (int i = threadIdx.x; i < kShWarps * 2 * 33 * kShRow; i += blockDim.x)
+        (&A[0][0][0][0])[i] = 0.0;  // the pad column and the zero rows stay zero
 
-    int br = 0, bc = 0;
-    sh_block(lane < kShBlocks ? lane : 0, &br, &bc);
-    const bool owner = lane < kShBlocks;
-    constexpr int kPer = kShSplatsPerBlock / kShWarps;  // splats per warp
-    double acc[kPer][8];
-    int seen[kPer];
+    const int half = lane >> 4, hl = lane & 15;
+    const bool owner = hl < kShBlocks;
+    int rb = 0, cb = 0;
+    sh_block(owner ? hl : 0, &rb, &cb);
+    constexpr int kPairs = kShSplatsPerBlock / kShWarps / 2;  // pairs per warp
+    double acc[kPairs][16];
+    int seen[kPairs];
 #pragma unroll
-    for (int j = 0; j < kPer; j++) {
-        seen[j] = 0;
+    for (int p = 0; p < kPairs; p++) {
+        seen[p] = 0;
 #pragma unroll
-        for (int q = 0; q < 8; q++) acc[j][q] = 0.0;
+        for (int q = 0; q < 16; q++) acc[p][q] = 0.0;
     }
 
     for (int s0 = 0; s0 < ncam; s0 += 32) {
@@ -129,82 +134,89 @@ __global__ void __launch_bounds__(32 * kShWarps, POTR_SH_MIN_BLOCKS) k_sh_accumu
         const double ey = lv ? eyes[3 * (s0 + lane) + 1] : 0.0;
         const double ez = lv ? eyes[3 * (s0 + lane) + 2] : 0.0;
 #pragma unroll
-        for (int j = 0; j < kPer; j++) {
-            const int kk = w * kPer + j;
-            if (kk >= nk) break;  // warp-uniform
-            const double wv = wtile[lane][kk];
-            const unsigned seen_mask = __ballot_sync(0xffffffffu, lv && wv > 0.0);
-            seen[j] += __popc(seen_mask);
-            double *row = A[w][lane];
-            if (wv > 0.0) {
-                const double d0 = pos[kk][0] - ex, d1 = pos[kk][1] - ey, d2 = pos[kk][2] - ez;
-                const double nrm = sqrt(d0 * d0 + d1 * d1 + d2 * d2);
-                double y[16];
-                sh_basis16(d0 / nrm, d1 / nrm, d2 / nrm, y);
-                double col[3];
+        for (int p = 0; p < kPairs; p++) {
+            const int kbase = w * 2 * kPairs + 2 * p;
+            if (kbase >= nk) break;  // warp-uniform
+            unsigned smask[2];
 #pragma unroll
-                for (int c = 0; c < 3; c++) {
-                    double t = 0.0;
+            for (int q = 0; q < 2; q++) {
+                const int kk = kbase + q;
+                const double wv = kk < nk ? wtile[lane][kk] : 0.0;
+                smask[q] = __ballot_sync(0xffffffffu, lv && wv > 0.0);
+                if (wv > 0.0) {
+                    double *row = A[w][q][lane];
+                    const double d0 = pos[kk][0] - ex, d1 = pos[kk][1] - ey, d2 = pos[kk][2] - ez;
+                    const double nrm = sqrt(d0 * d0 + d1 * d1 + d2 * d2);
+                    double y[16];
+                    sh_basis16(d0 / nrm, d1 / nrm, d2 / nrm, y);
+                    double col[3];
 #pragma unroll
-                    for (int i = 0; i < 16; i++) t += y[i] * shs[kk][c * 16 + i];
-                    col[c] = t;
-                }
+                    for (int c = 0; c < 3; c++) {
+                        double t = 0.0;
 #pragma unroll
-                for (int i = 0; i < 16; i++) row[i] = y[i] * wv;
+                        for (int i = 0; i < 16; i++) t += y[i] * shs[kk][c * 16 + i];
+                        col[c] = t;
+                    }
 #pragma unroll
-                for (int c = 0; c < 3; c++) {
-                    const double yc = col[0] * kRgbToYcocg[c * 3] + col[1] * kRgbToYcocg[c * 3 + 1] +
-                                      col[2] * kRgbToYcocg[c * 3 + 2];
-                    row[16 + c] = yc * wv;
+                    for (int i = 0; i < 16; i++) row[i] = y[i] * wv;
+#pragma unroll
+                    for (int c = 0; c < 3; c++) {
+                        const double yc = col[0] * kRgbToYcocg[c * 3] +
+                                          col[1] * kRgbToYcocg[c * 3 + 1] +
+                                          col[2] * kRgbToYcocg[c * 3 + 2];
+                        row[kShYc + c] = yc * wv;
+                    }
                 }
             }
+            seen[p] += half ? __popc(smask[1]) : __popc(smask[0]);  // lanes of half h: splat h
             __syncwarp();
-            if (owner) {
-                // kShUnroll seen views per step, ascending (the zero row pads
-                // the last step): their shared loads issue together
-                for (unsigned m = seen_mask; m;) {
-                    int vv[kShUnroll];
+            // kShUnroll views per step from the union of the pair's seen
+            // views, ascending; a half reads the zero row for a view its splat
+            // does not see (and to pad the last step): fma(0, 0, acc) == acc
+            const double(*rows)[kShRow] = A[w][half];
+            const unsigned mine = smask[half];
+            unsigned m = smask[0] | smask[1];
+            const int cofs = cb < 4 ? 4 * cb : kShYc;
+            while (m) {
+                int vv[kShUnroll];
 #pragma unroll
-                    for (int u = 0; u < kShUnroll; u++) {
-                        vv[u] = m ? __ffs(m) - 1 : 32;
-                        m &= m - 1u;
-                    }
-                    double2 a[kShUnroll], b01[kShUnroll], b23[kShUnroll];
-#pragma unroll
-                    for (int u = 0; u < kShUnroll; u++) {
-                        a[u] = *reinterpret_cast<const double2 *>(&A[w][vv[u]][2 * br]);
-                        b01[u] = *reinterpret_cast<const double2 *>(&A[w][vv[u]][bc]);
-                        b23[u] = *reinterpret_cast<const double2 *>(&A[w][vv[u]][bc + 2]);
-                    }
-#pragma unroll
-                    for (int u = 0; u < kShUnroll; u++) {
-                        acc[j][0] = fma(a[u].x, b01[u].x, acc[j][0]);
-                        acc[j][1] = fma(a[u].x, b01[u].y, acc[j][1]);
-                        acc[j][2] = fma(a[u].x, b23[u].x, acc[j][2]);
-                        acc[j][3] = fma(a[u].x, b23[u].y, acc[j][3]);
-                        acc[j][4] = fma(a[u].y, b01[u].x, acc[j][4]);
-                        acc[j][5] = fma(a[u].y, b01[u].y, acc[j][5]);
-                        acc[j][6] = fma(a[u].y, b23[u].x, acc[j][6]);
-                        acc[j][7] = fma(a[u].y, b23[u].y, acc[j][7]);
-                    }
+                for (int u = 0; u < kShUnroll; u++) {
+                    const int v = m ? __ffs(m) - 1 : 32;
+                    m &= m - 1u;
+                    vv[u] = (v < 32 && (mine >> v & 1u)) ? v : 32;
                 }
+                double ar[kShUnroll][4], bc[kShUnroll][4];
+#pragma unroll
+                for (int u = 0; u < kShUnroll; u++)
+#pragma unroll
+                    for (int i = 0; i < 4; i++) {
+                        ar[u][i] = rows[vv[u]][4 * rb + i];
+                        bc[u][i] = rows[vv[u]][cofs + i];
+                    }
+#pragma unroll
+                for (int u = 0; u < kShUnroll; u++)
+#pragma unroll
+                    for (int r = 0; r < 4; r++)
+#pragma unroll
+                        for (int c = 0; c < 4; c++)
+                            acc[p][4 * r + c] = fma(ar[u][r], bc[u][c], acc[p][4 * r + c]);
             }
             __syncwarp();
         }
     }
 #pragma unroll
-    for (int j = 0; j < kPer; j++) {
-        const int kk = w * kPer + j;
-        if (kk >= nk) break;
+    for (int p = 0; p < kPairs; p++) {
+        const int kk = w * 2 * kPairs + 2 * p + half;
+        if (kk >= nk) continue;
         const int64_t k = k0 + kk;
         if (owner) {
 #pragma unroll
-            for (int q = 0; q < 8; q++) {
-                const int e = sh_entry(2 * br + (q >> 2), bc + (q & 3));
-                if (e >= 0) neq[(int64_t)e * n + k] += acc[j][q];
+            for (int q = 0; q < 16; q++) {
+                const int e = sh_entry(4 * rb + (q >> 2), 4 * cb + (q & 3));  // cb 4: 16 + q
+                if (e >= 0) neq[(int64_t)e * n + k] += acc[p][q];
             }
         }
-        if (lane == 0) neq[(int64_t)184 * n + k] += (double)seen[j];
+        if (hl == 0) neq[(int64_t)184 * n + k] += (double)seen[p];
     }
 }
 
@@ -591,7 +603,14 @@ cudaError_t launch_sh_accumulate(const potr_splats &sp, int ncam, const double *
                                  const double *cam_imp, double *neq, cudaStream_t st) {
     if (sp.n == 0) return cudaSuccess;
     const unsigned blocks = (unsigned)((sp.n + kShSplatsPerBlock - 1) / kShSplatsPerBlock);
-    k_sh_accumulate<<<blocks, 32 * kShWarps, 0, st>>>(sp, ncam, eyes_dev, cam_imp, neq);
+    constexpr size_t smem = sizeof(double) * kShWarps * 2 * 33 * kShRow;
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(k_sh_accumulate, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)smem);
+        attr = true;
+    }
+    k_sh_accumulate<<<blocks, 32 * kShWarps, smem, st>>>(sp, ncam, eyes_dev, cam_imp, neq);
     return cudaGetLastError();
 }
 
