@@ -1,0 +1,141 @@
+"""BASELINE config 4: SH-coefficient recompute on the C3 scene (3M splats, deg 3,
+200 views at 1237x822), reporting AC sparsity and PSNR against the oracle.
+
+    python tools/c4_report.py [--oracle-threads T] > profiles/r2_c4_report.json
+
+* device time of the recompute (normal equations once, the solves per lambda)
+  and AC sparsity at lambda in {1e-11, 1e-12, 1e-13} (the paper's 0.70-0.97
+  sparsity range at this scene's importance scale; 1e-7 zeroes every AC term);
+* the oracle's compact_scene (potr_oracle.c, a C port of compaction.py) on
+  every splat at lambda = 1e-12, on all host threads: the CPU baseline, and
+  the reference coefficients for
+* PSNR of 8 sample views rendered with the device's coefficients against the
+  same views rendered with the oracle's (and both against the original
+  model), plus the coefficient agreement and identical zero patterns.
+
+Uses the oracle only as the checker / CPU baseline (test infrastructure).
+"""
+import argparse
+import ctypes
+import json
+import os
+import sys
+import time
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+from paper_2601_14821_b200 import _native, device as D, rasterizer as R  # noqa: E402
+from paper_2601_14821_b200.fixture import config_scene  # noqa: E402
+from paper_2601_14821_b200.metrics import psnr  # noqa: E402
+
+ALPHA_PAR = 0.8175744761936437
+ZERO_THR = 0.5 / 51.0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--oracle-threads", type=int, default=0)
+    ap.add_argument("--lambdas", default="1e-11,1e-12,1e-13")
+    ap.add_argument("--oracle-lambda", type=float, default=1e-12)
+    args = ap.parse_args()
+    lams = [float(x) for x in args.lambdas.split(",")]
+
+    splats, cams = config_scene("C3")
+    dev = D.current_device()
+    ctx = D.context()
+    ds = D.DeviceSplats.from_host(splats, dev)
+    n, S = ds.n, len(cams)
+    imp, ci, _, _ = R.forward_stats_device(ds, cams, None)
+    neq = torch.zeros((_native.NEQ_STRIDE, n), dtype=torch.float64, device=dev)
+    rgb = torch.empty((n, 3, 16), dtype=torch.float64, device=dev)
+    yc = torch.empty((n, 3, 16), dtype=torch.float64, device=dev)
+    status = torch.empty(n, dtype=torch.int8, device=dev)
+    cam_arr = _native.camera_array(cams)
+
+    def accumulate():
+        neq.zero_()
+        ctx.call("potr_sh_accumulate", ctypes.byref(ds.struct()), S, cam_arr, D.ptr(ci),
+                 D.ptr(neq))
+
+    def solve(lam):
+        ctx.call("potr_sh_solve", ctypes.byref(ds.struct()), D.ptr(neq), ctypes.c_double(lam),
+                 ctypes.c_double(ALPHA_PAR), ctypes.c_double(ZERO_THR), D.ptr(rgb), D.ptr(yc),
+                 D.ptr(status))
+
+    def timed(fn, reps=3):
+        ts = []
+        for _ in range(reps):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            fn()
+            e1.record()
+            torch.cuda.synchronize()
+            ts.append(e0.elapsed_time(e1))
+        return min(ts)
+
+    accumulate()
+    t_acc = timed(accumulate)
+    rows = []
+    for lam in lams:
+        solve(lam)
+        t_solve = timed(lambda: solve(lam))
+        sp = float((yc[:, :, 1:] == 0).double().mean().item())
+        rows.append({"lambda_y": lam, "solve_ms": t_solve, "sh_recompute_ms": t_acc + t_solve,
+                     "ac_sparsity": sp,
+                     "status_counts": torch.bincount(status.long(), minlength=4).tolist()})
+
+    # oracle at one lambda, every splat: CPU baseline + reference coefficients
+    from oracle import oracle as O
+    threads = args.oracle_threads or O.num_threads()
+    ci_h = D.to_host(ci)
+    t0 = time.perf_counter()
+    rgb_o, yc_o, st_o = O.compact(splats, cams, ci_h, args.oracle_lambda, ALPHA_PAR, ZERO_THR,
+                                  threads=threads)
+    t_oracle = time.perf_counter() - t0
+    solve(args.oracle_lambda)
+    yc_d = D.to_host(yc)
+    rgb_d = D.to_host(rgb)
+    st_d = D.to_host(status)
+    same_status = bool(np.array_equal(st_d, st_o))
+    same_zero = bool(np.array_equal(yc_d == 0.0, yc_o == 0.0))
+    max_abs = float(np.abs(yc_d - yc_o).max())
+    bitwise = bool(np.array_equal(yc_d, yc_o))
+
+    views = [cams[i] for i in np.linspace(0, S - 1, 8).astype(int)]
+    from paper_2601_14821_b200.scene import Splats
+    sp_d = Splats(splats.positions, rgb_d, splats.opacities, splats.scales, splats.rotations)
+    sp_o = Splats(splats.positions, rgb_o, splats.opacities, splats.scales, splats.rotations)
+    ps_do, ps_d0, ps_o0 = [], [], []
+    for cam in views:
+        im_d = R.render_image(sp_d, cam)
+        im_o = R.render_image(sp_o, cam)
+        im_0 = R.render_image(splats, cam)
+        ps_do.append(psnr(im_d, im_o))
+        ps_d0.append(psnr(im_d, im_0))
+        ps_o0.append(psnr(im_o, im_0))
+    out = {
+        "config": "C4: SH recompute on the C3 scene (3M splats, deg 3, 200 views at 1237x822)",
+        "camera_importance": "device forward_stats of the unpruned scene",
+        "normal_equations_ms": t_acc,
+        "lambdas": rows,
+        "oracle": {"lambda_y": args.oracle_lambda, "threads": threads, "seconds": t_oracle,
+                   "splats_per_s": n / t_oracle, "kind": "port (oracle/potr_oracle.c)",
+                   "status_identical": same_status, "zero_pattern_identical": same_zero,
+                   "coefficients_bit_identical": bitwise, "max_abs_diff": max_abs,
+                   "ac_sparsity": float((yc_o[:, :, 1:] == 0).mean())},
+        "psnr_views": [int(i) for i in np.linspace(0, S - 1, 8).astype(int)],
+        "psnr_device_vs_oracle_db": ps_do,
+        "psnr_device_vs_original_db": ps_d0,
+        "psnr_oracle_vs_original_db": ps_o0,
+        "speedup_vs_oracle": t_oracle * 1e3 / (t_acc + rows[lams.index(args.oracle_lambda)]
+                                               ["solve_ms"]) if args.oracle_lambda in lams
+        else None,
+    }
+    print(json.dumps(out, indent=1))
+
+
+if __name__ == "__main__":
+    main()
