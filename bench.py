@@ -37,6 +37,7 @@ sys.path.insert(0, ROOT)
 MEASURED_PEAKS = os.path.join(ROOT, "MEASURED_PEAKS.json")
 FALLBACK_HBM_GBS = 6650.0
 METRIC = "removal-effect scoring Mpix·views/s"
+SH_LAMBDA = 1e-12  # the s/scene SH recompute's luminance ridge (see scene_measure)
 UNIT = "Mpix·views/s"
 
 
@@ -158,15 +159,17 @@ OPS_PER_E = 24 + 2 * 20
 OPS_PER_M = 37
 
 
-def load_traffic(views_per_launch):
+def load_traffic(views_per_launch, config):
     """DRAM bytes (read + write) per k_raster<kScore> launch from the committed
-    `ncu --set full` capture summary (profiles/raster_traffic.json), scaled to
-    this run's views per launch; (None, None) without one."""
+    `ncu --set full` capture summary (profiles/raster_traffic.json), for the
+    configuration it was captured on only; (None, None) otherwise."""
     path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles",
                         "raster_traffic.json")
     try:
         with open(path) as f:
             t = json.load(f)
+        if t.get("config", "C3") != config:
+            return None, f"no capture for {config} (profiles/raster_traffic.json is {t.get('config', 'C3')})"
         per_view = float(t["dram_bytes_per_launch"]) / float(t["views_per_launch"])
         return per_view * views_per_launch, t.get("source")
     except (OSError, ValueError, KeyError):
@@ -174,9 +177,18 @@ def load_traffic(views_per_launch):
 
 
 def fp64_peak_lane_ops(peaks):
-    # B200: 148 SMs x 64 FP64 lanes/clk at the max SM clock -- nominal; the
-    # MEASURED_PEAKS.json figures are HBM copy and bf16 tensor only.
-    return 148 * 64 * float(peaks.get("sm_max_mhz", 1965.0)) * 1e6 / 1e12
+    """FP64 FMA lanes per second (T/s): the DFMA microbenchmark measured on this
+    pool (tools/fp64_peak.cu -> profiles/r2_fp64_peak.json), else the nominal
+    148 SMs x 64 lanes x the max SM clock.  Returns (peak, source)."""
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles",
+                        "r2_fp64_peak.json")
+    try:
+        with open(path) as f:
+            return float(json.load(f)["fp64_fma_tera_per_s"]), \
+                "measured: tools/fp64_peak.cu DFMA microbenchmark (profiles/r2_fp64_peak.json)"
+    except (OSError, ValueError, KeyError):
+        return 148 * 64 * float(peaks.get("sm_max_mhz", 1965.0)) * 1e6 / 1e12, \
+            "nominal FP64 CUDA-core rate at sm_max_mhz (148 SMs x 64 lanes/clk)"
 
 
 # ---------------------------------------------------------------------------
@@ -252,8 +264,17 @@ def config_dict(args, world):
                         f"{c['views']} views at {c['width']}x{c['height']}",
             "splats": c["splats"], "views": c["views"],
             "resolution": [c["width"], c["height"]], "parallelism": f"view-sharded x{world}",
-            "l2": "inputs > L2 (splats 1.4 GB + targets 4.9 GB at C3), no flush",
-            "state": "opacity x0.97 vs unperturbed targets"}
+            "l2": l2_note(c), "state": "opacity x0.97 vs unperturbed targets"}
+
+
+def l2_note(c):
+    """The L2 rule: inputs larger than the 126 MB L2 between timed steps, or a flush."""
+    splat_gb = c["splats"] * 59 * 8 / 1e9
+    target_gb = c["views"] * c["width"] * c["height"] * 3 * 8 / 1e9
+    big = (splat_gb + target_gb) * 1e3 > 126
+    return (f"inputs {'>' if big else '<='} L2: splats {splat_gb:.2f} GB + targets "
+            f"{target_gb:.2f} GB read every step" + (", no flush" if big else
+                                                    " (below L2: not a valid timing config)"))
 
 
 # ---------------------------------------------------------------------------
@@ -381,15 +402,15 @@ def main():
     ops_per_launch = (E * OPS_PER_E + M * OPS_PER_M) / views_here * views_per_launch
     raster_avg_ms = raster_ms / max(1, raster_n)
     achieved = ops_per_launch / (raster_avg_ms / 1000.0) / 1e12
-    peak = fp64_peak_lane_ops(peaks)
-    traffic, traffic_src = load_traffic(views_per_launch)
+    peak, peak_note = fp64_peak_lane_ops(peaks)
+    traffic, traffic_src = load_traffic(views_per_launch, args.config)
     roofline = {"bound": "fp64", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                 "frac": achieved / peak, "traffic": traffic, "traffic_source": traffic_src,
                 "kernel": "k_raster<kScore>",
                 "unit_note": "FP64 lane-operations per second, FMA = 1 (SURVEY.md 8(d) model: "
                              "W = 24E + 37M + 2E exp at 20 DFMA each, per view)",
-                "peak_source": "nominal FP64 CUDA-core rate at sm_max_mhz (148 SMs x 64 lanes/clk);"
-                               " MEASURED_PEAKS.json has only HBM and bf16 tensor peaks",
+                "peak_source": peak_note + "; MEASURED_PEAKS.json has only HBM and bf16 "
+                               "tensor peaks",
                 "views_per_launch": views_per_launch,
                 "raster_share_of_step": raster_ms / step_ms_sum if step_ms_sum else None,
                 "per_view": {"E_bbox_evals": E / views_here, "E_live": E_live / views_here,
@@ -439,10 +460,13 @@ def _native_cams(cams):
 
 
 def e2e_measure(args, rank, world, local, pert, cams, tg, S, Pv, dev):
-    """compute_delta_mse through the public API: host (pinned) splats in,
-    host scores out, every step.  Targets are the fixed reference renders,
-    read-only host arrays that the API keeps resident after the first call
-    (rasterizer.py:375-376 semantics; see device.TargetCache)."""
+    """compute_delta_mse through the public API every step: host splats in
+    (uploaded inside the timed region), host scores out.  Two sources:
+    `pageable` -- plain numpy arrays, as the reference controller hands over a
+    fresh subset() every iteration (pruning.py:161; the headline e2e) -- and
+    `pinned`.  Targets are the fixed reference renders, read-only host arrays
+    that the API keeps resident after the first call (rasterizer.py:375-376
+    semantics; see device.TargetCache)."""
     import torch
     import torch.distributed as dist
     from paper_2601_14821_b200 import distributed, rasterizer
@@ -453,8 +477,7 @@ def e2e_measure(args, rank, world, local, pert, cams, tg, S, Pv, dev):
         t.numpy()[...] = a
         return t.numpy()
 
-    host = Splats(*(pinned_copy(np.asarray(getattr(pert, f))) for f in
-                    ("positions", "sh", "opacities", "scales", "rotations")))
+    fields = ("positions", "sh", "opacities", "scales", "rotations")
     lo, hi = distributed.shard_range(S, rank, world)
     # full-length target list; only this rank's entries are read when sharded
     targets = [None] * S
@@ -462,44 +485,52 @@ def e2e_measure(args, rank, world, local, pert, cams, tg, S, Pv, dev):
         h = t.cpu().numpy()
         h.flags.writeable = False
         targets[lo + i] = h
-    for s in range(S):
-        if targets[s] is None:
-            targets[s] = np.zeros((1, 1, 3))  # never read on this rank
+    for s_ in range(S):
+        if targets[s_] is None:
+            targets[s_] = np.zeros((1, 1, 3))  # never read on this rank
     distributed.enable_view_sharding(world > 1)
-    if world == 1:
-        call = lambda: rasterizer.forward_stats(host, cams, targets)  # noqa: E731
-    else:
-        call = lambda: distributed.forward_stats_sharded(host, cams, targets)  # noqa: E731
-    # warm-up mirrors the timed loop: the previous result stays alive while
-    # the next call runs (its device buffers, e.g. the (S, N) camera
-    # importance, are then already in torch's caching allocator)
-    st = None
-    for _ in range(max(2, args.warmup)):
-        st = call()
-    if world > 1:
-        dist.barrier()
-    torch.cuda.synchronize()
-    t0 = time.perf_counter()
-    for _ in range(args.steps):
-        t1 = time.perf_counter()
-        st = call()
-        _ = st.delta_mse[0]  # host result in hand
-        if os.environ.get("POTR_E2E_TRACE"):
-            print(f"e2e call {1e3 * (time.perf_counter() - t1):.1f} ms", file=sys.stderr)
-    torch.cuda.synchronize()
-    dt = (time.perf_counter() - t0) / args.steps
-    if world > 1:
-        t = torch.tensor([dt], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        dt = float(t.item())
-    h2d = sum(np.asarray(getattr(host, f)).nbytes for f in
-              ("positions", "sh", "opacities", "scales", "rotations"))
-    n = len(host)
+    res = {}
+    for kind in ("pageable", "pinned"):
+        if kind == "pageable":
+            host = Splats(*(np.array(getattr(pert, f), dtype=np.float64, copy=True)
+                            for f in fields))
+        else:
+            host = Splats(*(pinned_copy(np.asarray(getattr(pert, f))) for f in fields))
+        if world == 1:
+            call = lambda: rasterizer.forward_stats(host, cams, targets)  # noqa: E731
+        else:
+            call = lambda: distributed.forward_stats_sharded(host, cams, targets)  # noqa: E731
+        # warm-up mirrors the timed loop: the previous result stays alive while
+        # the next call runs
+        st = None
+        for _ in range(max(2, args.warmup)):
+            st = call()
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            st = call()
+            _ = st.delta_mse[0]  # host result in hand
+        torch.cuda.synchronize()
+        dt = (time.perf_counter() - t0) / args.steps
+        if world > 1:
+            t = torch.tensor([dt], dtype=torch.float64, device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            dt = float(t.item())
+        res[kind] = dt
+        del st
+    h2d = sum(np.asarray(getattr(pert, f)).nbytes for f in fields)
+    n = len(pert.positions)
+    dt = res["pageable"]
     return {"value": Pv / 1e6 / dt, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
             "d2h_bytes_per_step": int(8 * (2 * n + 1)), "ms_per_step": dt * 1000.0,
+            "source_memory": "pageable numpy arrays (the reference controller's subset())",
+            "pinned": {"value": Pv / 1e6 / res["pinned"], "ms_per_step": res["pinned"] * 1e3},
             "api": "paper_2601_14821_b200.rasterizer.forward_stats (compute_delta_mse body)",
-            "note": "splats uploaded from pinned host memory every step; targets resident "
-                    "after the first call (fixed, read-only); camera_importance stays in HBM"}
+            "note": "splats uploaded every step (pageable: potr_copy_to_device's pinned ring); "
+                    "targets resident after the first call (fixed, read-only); "
+                    "camera_importance stays in HBM"}
 
 
 def scene_measure(args, world, ds, cams, my_cams, tptr, cam_arr, lo, hi, ctx, dev, splats, S):
@@ -555,7 +586,7 @@ def scene_measure(args, world, ds, cams, my_cams, tptr, cam_arr, lo, hi, ctx, de
                  D.ptr(neq))
         if world > 1:
             dist.all_reduce(neq)
-        ctx.call("potr_sh_solve", ctypes.byref(ds0.struct()), D.ptr(neq), ctypes.c_double(1e-7),
+        ctx.call("potr_sh_solve", ctypes.byref(ds0.struct()), D.ptr(neq), ctypes.c_double(SH_LAMBDA),
                  ctypes.c_double(0.8175744761936437), ctypes.c_double(0.5 / 51.0), D.ptr(rgb),
                  D.ptr(yc), D.ptr(status))
         torch.cuda.synchronize()
@@ -576,7 +607,10 @@ def scene_measure(args, world, ds, cams, my_cams, tptr, cam_arr, lo, hi, ctx, de
            "note": "total_s: the targets are rendered by the same walk that scores them "
                    "(potr_score_views_self, bit-identical to render_targets + "
                    "compute_delta_mse); separate_passes: the two calls one after the other",
-           "lambda_y": 1e-7, "ac_sparsity": ac}
+           "lambda_y": SH_LAMBDA, "ac_sparsity": ac,
+           "lambda_note": "lambda_y = 1e-12: AC sparsity 0.937 at C3, inside the paper's 0.70-0.97 "
+                          "range (1e-7 zeroes every AC term at this importance scale; "
+                          "profiles/r2_c4_report.json has 1e-11 / 1e-13)"}
     if world == 1 and not args.no_prune48:
         out.update(prune48_measure(splats, cams, imgs))
     return out

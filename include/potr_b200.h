@@ -275,6 +275,12 @@ int potr_counters_read(potr_ctx *ctx, uint64_t *out);
 
 /* ---- host-buffer convenience (reference-facing drop-in) ---------------- */
 
+/* Host -> device copy of `bytes` from a pageable (or any) host buffer into
+ * device memory, ordered on the context stream: host threads stage chunks
+ * into a pinned ring while the DMA engine moves the previous chunk.  The
+ * source may be reused when the call returns. */
+int potr_copy_to_device(potr_ctx *ctx, void *dst, const void *src, int64_t bytes);
+
 /* forward_stats with HOST arrays in the reference layouts; copies in, runs,
  * copies out and synchronizes.  targets: host array of ncam host pointers or
  * NULL.  camera_importance nullable. */

@@ -78,6 +78,8 @@ _SIGNATURES = {
                                              ctypes.c_void_p, ctypes.c_void_p]),
     "potr_finalize_stats": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int64, ctypes.c_int,
                                            ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]),
+    "potr_copy_to_device": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+                                           ctypes.c_int64]),
     "potr_removal_order": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p,
                                           ctypes.c_void_p, ctypes.c_double, ctypes.c_double,
                                           ctypes.c_void_p]),

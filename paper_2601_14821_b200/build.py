@@ -20,7 +20,7 @@ NVCC_FLAGS = [
     # float64 parity: never contract a*b+c into FMA (the reference's numpy /
     # numba arithmetic does not); explicit fma() calls are kept.
     "--fmad=false",
-    "-Xcompiler", "-fPIC", "-shared", "-cudart", "static",
+    "-Xcompiler", "-fPIC", "-Xcompiler", "-fopenmp", "-lgomp", "-shared", "-cudart", "static",
 ]
 
 

@@ -5,6 +5,7 @@
 #include <cstdlib>
 #include <utility>
 #include <cstring>
+#include <omp.h>
 #include <string>
 #include <vector>
 
@@ -45,6 +46,10 @@ struct potr_ctx {
     // host-buffer API staging
     DevBuf h_pos, h_sh, h_op, h_sc, h_rot, h_tg, h_imp, h_ci, h_dm, h_mse, h_rgb, h_yc, h_st;
     int64_t *pinned = nullptr;  // small pinned scratch for scalars
+    // potr_copy_to_device: pinned staging ring for pageable host sources
+    static constexpr int kRing = 4;
+    void *ring[kRing] = {nullptr, nullptr, nullptr, nullptr};
+    cudaEvent_t ring_ev[kRing] = {nullptr, nullptr, nullptr, nullptr};
     // live per-stage timing (CUDA events on ctx->stream) and work counters
     bool profile = false;
     std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> events;
@@ -681,6 +686,10 @@ void potr_destroy(potr_ctx *ctx) {
     for (DevBuf *b : bufs)
         if (b->p) cudaFree(b->p);
     if (ctx->pinned) cudaFreeHost(ctx->pinned);
+    for (int r = 0; r < potr_ctx::kRing; r++) {
+        if (ctx->ring[r]) cudaFreeHost(ctx->ring[r]);
+        if (ctx->ring_ev[r]) cudaEventDestroy(ctx->ring_ev[r]);
+    }
     if (ctx->counters.p) cudaFree(ctx->counters.p);
     if (ctx->tile_counter.p) cudaFree(ctx->tile_counter.p);
     if (ctx->vidx.p) cudaFree(ctx->vidx.p);
@@ -1219,6 +1228,47 @@ int potr_counters_read(potr_ctx *ctx, uint64_t *out) {
 }
 
 // ---- host-buffer convenience entry points --------------------------------
+
+// Pageable host -> device: chunks of kRingChunk bytes go through a ring of
+// pinned buffers; host threads (OpenMP) fill chunk c + 1 while the DMA engine
+// moves chunk c, so a pageable source uploads at close to the pinned PCIe
+// rate instead of the driver's single-threaded staging.
+static constexpr size_t kRingChunk = (size_t)32 << 20;
+
+int potr_copy_to_device(potr_ctx *ctx, void *dst, const void *src, int64_t bytes) {
+    if (!ctx || bytes < 0 || (bytes > 0 && (!dst || !src)))
+        return fail(ctx, POTR_E_ARG, "copy_to_device: bad arguments");
+    if (bytes == 0) return POTR_OK;
+    CK(cudaSetDevice(ctx->device));
+    for (int r = 0; r < potr_ctx::kRing; r++) {
+        if (!ctx->ring[r]) {
+            CK(cudaMallocHost(&ctx->ring[r], kRingChunk));
+            CK(cudaEventCreateWithFlags(&ctx->ring_ev[r], cudaEventDisableTiming));
+        }
+    }
+    int threads = omp_get_num_procs();
+    threads = threads < 1 ? 1 : threads > 16 ? 16 : threads;
+    const char *s = reinterpret_cast<const char *>(src);
+    char *d = reinterpret_cast<char *>(dst);
+    int64_t c = 0;
+    for (int64_t off = 0; off < bytes; off += (int64_t)kRingChunk, c++) {
+        const int b = (int)(c % potr_ctx::kRing);
+        const int64_t len = bytes - off < (int64_t)kRingChunk ? bytes - off : (int64_t)kRingChunk;
+        // the buffer's previous DMA (from this call or an earlier one) must be
+        // done before it is refilled; a never-recorded event returns at once
+        CK(cudaEventSynchronize(ctx->ring_ev[b]));
+        char *stage = reinterpret_cast<char *>(ctx->ring[b]);
+        const int t_used = len < ((int64_t)1 << 20) ? 1 : threads;
+#pragma omp parallel for num_threads(t_used) schedule(static)
+        for (int t = 0; t < t_used; t++) {
+            const int64_t a = len * t / t_used, e = len * (t + 1) / t_used;
+            std::memcpy(stage + a, s + off + a, (size_t)(e - a));
+        }
+        CK(cudaMemcpyAsync(d + off, stage, (size_t)len, cudaMemcpyHostToDevice, ctx->stream));
+        CK(cudaEventRecord(ctx->ring_ev[b], ctx->stream));
+    }
+    return POTR_OK;
+}
 
 namespace {
 

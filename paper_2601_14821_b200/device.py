@@ -58,7 +58,18 @@ def to_device(arr, device, shape=None):
     with warnings.catch_warnings():
         # read-only inputs (the reference freezes its targets) are only read here
         warnings.simplefilter("ignore", UserWarning)
-        return torch.from_numpy(a).to(device, non_blocking=False)
+        src = torch.from_numpy(a)
+        if a.nbytes >= _STAGED_MIN and not src.is_pinned():
+            # pageable (the reference's own arrays): the library's staged
+            # upload, host threads filling a pinned ring under the DMA
+            dst = torch.empty(a.shape, dtype=torch.float64, device=device)
+            context(device).call("potr_copy_to_device", ptr(dst), ctypes.c_void_p(a.ctypes.data),
+                                 ctypes.c_int64(a.nbytes))
+            return dst
+        return src.to(device, non_blocking=False)
+
+
+_STAGED_MIN = 8 << 20          # pageable sources from this size use potr_copy_to_device
 
 
 _PINNED_MAX = 256 << 20        # results up to this size land in pinned memory directly

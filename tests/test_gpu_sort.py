@@ -97,3 +97,17 @@ def test_multi_group_tile_sort_vs_oracle_and_batch1(dev, oracle):
                                            threads=8)
     np.testing.assert_allclose(st8.importance, imp, rtol=1e-12, atol=1e-20)
     np.testing.assert_allclose(st8.delta_mse, dm, rtol=1e-9, atol=1e-22)
+
+
+def test_staged_pageable_upload_bit_exact(dev):
+    """potr_copy_to_device (pageable host -> device through the pinned ring):
+    back-to-back calls whose sizes are not multiples of the ring chunk, so a
+    call refills buffers whose previous DMA may still be in flight."""
+    import torch
+    from paper_2601_14821_b200 import device as D
+    rng = np.random.default_rng(3)
+    arrs = [rng.standard_normal(m) for m in (13_000_001, 4_194_305, 40_000_003, 9_999_999)]
+    outs = [D.to_device(a, dev) for a in arrs]  # >= 8 MB pageable: the staged path
+    torch.cuda.synchronize()
+    for o, a in zip(outs, arrs):
+        assert np.array_equal(o.cpu().numpy(), a)
