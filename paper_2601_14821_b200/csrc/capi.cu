@@ -6,6 +6,7 @@
 #include <utility>
 #include <cstring>
 #include <omp.h>
+#include <nvtx3/nvToolsExt.h>
 #include <string>
 #include <vector>
 
@@ -142,23 +143,38 @@ cudaEvent_t take_event(potr_ctx *ctx) {
 }
 
 // RAII-free stage bracket: begin/end record events when profiling is on.
+// NVTX range names of the stages (SURVEY.md section 5 tracing): visible in
+// any NVTX-aware tool; a push/pop costs nanoseconds when none is attached.
+const char *const kStageNames[POTR_STAGE_COUNT] = {
+    "potr:preprocess", "potr:depth_sort", "potr:scan",   "potr:duplicate",    "potr:tile_sort",
+    "potr:raster",     "potr:reduce",     "potr:sh_acc", "potr:sh_solve"};
+
 struct Stage {
     potr_ctx *ctx;
     int id;
     cudaEvent_t a = nullptr;
+    bool open = true;
     Stage(potr_ctx *c, int i) : ctx(c), id(i) {
+        nvtxRangePushA(kStageNames[i]);
         if (ctx->profile) {
             a = take_event(ctx);
             cudaEventRecord(a, ctx->stream);
         }
     }
     void end() {
+        if (open) {
+            nvtxRangePop();
+            open = false;
+        }
         if (ctx->profile && a) {
             cudaEvent_t b = take_event(ctx);
             cudaEventRecord(b, ctx->stream);
             ctx->events.push_back({id, {a, b}});
             a = nullptr;
         }
+    }
+    ~Stage() {
+        if (open) nvtxRangePop();  // early return on an error path
     }
 };
 

@@ -15,6 +15,16 @@
 
 namespace potr {
 
+// Bounds checks of a debug build (-DPOTR_CHECKS; compute-sanitizer is not
+// available on this pool): a violated check fails the launch with a device
+// assert.  Compiled out otherwise.
+#ifdef POTR_CHECKS
+#include <cassert>
+#define POTR_CHECK(cond) assert(cond)
+#else
+#define POTR_CHECK(cond) ((void)0)
+#endif
+
 // rasterizer.py:22-26
 constexpr double kAlphaFloor = 1.0 / 255.0;
 constexpr double kAlphaCap = 0.999;

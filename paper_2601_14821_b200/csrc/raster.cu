@@ -334,6 +334,7 @@ __global__ void k_duplicate(int64_t total, int64_t n, const int32_t *__restrict_
         for (int r = 0; r < s.nrows; r++) {
             const int ty = s.ty0 + r;
             for (int tx = s.c[2 * r]; tx <= (int)s.c[2 * r + 1]; tx++) {
+                POTR_CHECK(o < e && tx < tiles_x);
                 tkey[o] = (KeyT)(tbase0 + (uint32_t)(ty * tiles_x + tx));
                 dup_id[o] = g;
                 if (dup_rank) dup_rank[o] = rank;
@@ -352,6 +353,7 @@ __global__ void k_duplicate(int64_t total, int64_t n, const int32_t *__restrict_
         int c0 = tx0, c1 = tx1;
         if (cull && !row_span(ce, ty, &c0, &c1)) continue;
         for (int tx = c0; tx <= c1; tx++) {
+            POTR_CHECK(o < e && tx < tiles_x);
             tkey[o] = (KeyT)(tbase + (uint32_t)(ty * tiles_x + tx));
             dup_id[o] = g;
             if (dup_rank) dup_rank[o] = (int32_t)(i - v * n);
@@ -442,6 +444,7 @@ __device__ __forceinline__ ChunkIds fetch_ids(const RasterArgs &a, int cbase, in
     const int j = cbase + lane;
     c.valid = j < end;
     const int2 p = c.valid ? a.pair[j] : make_int2(0, 0);
+    POTR_CHECK(!c.valid || (p.x >= 0 && p.y >= 0));
     c.d = p.x;
     c.id = p.y;
     return c;
@@ -677,6 +680,7 @@ __global__ void __launch_bounds__(32 * kRasterWarps, POTR_RASTER_MIN_BLOCKS) k_r
         tile = __shfl_sync(FULL, tile, 0);
         if (tile >= a.ntiles) return;
 
+        POTR_CHECK(tile >= 0 && tile < a.ntiles);
         const int view = tile / a.ntiles_view;
         const int vt = tile - view * a.ntiles_view;
         const int tx = vt % a.tiles_x, ty = vt / a.tiles_x;
@@ -902,6 +906,7 @@ __global__ void __launch_bounds__(32 * kRasterWarps, POTR_RASTER_MIN_BLOCKS) k_r
                 }
                 __syncwarp();
                 if (lane < cnt) {
+                    POTR_CHECK(B.dup[lane] >= 0);
                     double2 t = S.acc[0][lane];
 #pragma unroll
                     for (int q = 1; q < kAccSplit; q++) t.x += S.acc[q][lane].x, t.y += S.acc[q][lane].y;

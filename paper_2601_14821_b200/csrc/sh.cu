@@ -455,8 +455,10 @@ __global__ void __launch_bounds__(128, MC <= 8 ? 4 : 2)
     if (t >= *count) return;
     const int64_t n = sp.n;
     const int64_t k = list[t];
+    POTR_CHECK(k >= 0 && k < n);
     const double *G = neq + k, *B = neq + (int64_t)136 * n + k;
     const unsigned mask1 = masks[k];
+    POTR_CHECK(__popc(mask1) <= MC);
     double *yc = ycocg_out + 48 * k;
     double U[MC * (MC + 1) / 2];
     double b[MC];

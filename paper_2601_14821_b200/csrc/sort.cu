@@ -1,4 +1,5 @@
 // sort.cu -- hand-written radix sort and scans for sm_100a (see sort.cuh).
+#include "common.cuh"
 #include "sort.cuh"
 
 namespace potr {
@@ -234,6 +235,7 @@ __global__ void __launch_bounds__(kSortThreads) k_onesweep(const K *__restrict__
         if (j < tile_n) {
             const uint32_t d = digit_of(k[i], shift);
             const int pos = (int)(boff[d] + whist[w][d] + rank[i]);
+            POTR_CHECK(pos >= 0 && pos < tile_n);
             stage_k[pos] = k[i];
             stage_v[pos] = IOTA ? (V)(base + j) : vin[base + j];
         }
@@ -244,6 +246,7 @@ __global__ void __launch_bounds__(kSortThreads) k_onesweep(const K *__restrict__
     for (int j = t; j < tile_n; j += kSortThreads) {
         const K kk = stage_k[j];
         const int64_t dst = gbase[digit_of(kk, shift)] + j;
+        POTR_CHECK(dst >= 0 && dst < n);
         kout[dst] = kk;
         vout[dst] = stage_v[j];
     }
