@@ -491,19 +491,27 @@ __device__ __forceinline__ unsigned ellipse_rows(const ChunkBuf &B, int e, int o
         return (cols * 0x01010101u) & rows;
     }
     if (!(R > 0.0)) return 0u;
-    const double inv_a = rcp_nr(a), aR = a * R;  // conservative use: Newton reciprocal
+    // The rows in fp32, in tile-local coordinates (small magnitudes), off the
+    // FP64 pipe: a R is widened by 4e-6 relative (far above the fp32 rounding
+    // of D's two terms, ~2e-7) and the pixel bounds by 1e-2 px plus 1e-5 of
+    // the magnitudes involved (the fp32 rounding of the interval is ~3e-7 of
+    // them), so the mask stays a superset of the pixels whose centre can pass
+    // the exact fp64 prefilter; floor / ceil are single rounding conversions.
+    const float faR = (float)(a * R) * (1.0f + 4e-6f);
+    const float fdet = (float)det, fb = (float)b;
+    const float finv_a = 1.0f / (float)a;
+    const float mxl = (float)(m.x - (double)ox - 0.5);  // pixel k is in when k - mxl in [xmin, xmax]
+    const float dy0 = (float)((double)oy + 0.5 - m.y);
     unsigned w = 0u;
     for (int r = r0; r <= r1; r++) {
-        const double dy = (double)(oy + r) + 0.5 - m.y;
-        const double D = aR - det * dy * dy;
-        if (D < 0.0) continue;
-        const double s = (double)sqrtf((float)D);
-        const double xmax = (s - b * dy) * inv_a, xmin = (-s - b * dy) * inv_a;
-        // pixel px is in when px + 0.5 - mx lies in [xmin, xmax] (+- margin)
-        const double e0 = ceil(m.x + xmin - 0.5 - kCullMarginPixel) - (double)ox;
-        const double e1 = floor(m.x + xmax - 0.5 + kCullMarginPixel) - (double)ox;
-        const int k0 = e0 > (double)c0 ? (e0 > (double)c1 ? 8 : (int)e0) : c0;
-        const int k1 = e1 < (double)c1 ? (e1 < (double)c0 ? -1 : (int)e1) : c1;
+        const float dy = dy0 + (float)r;
+        const float D = faR - fdet * dy * dy;
+        if (D < 0.0f) continue;
+        const float sq = sqrtf(D), t = fb * dy;
+        const float xmax = (sq - t) * finv_a, xmin = (-sq - t) * finv_a;
+        const float mg = 1e-2f + 1e-5f * (fabsf(xmax) + fabsf(xmin) + fabsf(mxl));
+        const int k0 = max(__float2int_ru(mxl + xmin - mg), c0);
+        const int k1 = min(__float2int_rd(mxl + xmax + mg), c1);
         if (k0 <= k1) w |= ((0xFFu >> (7 - k1)) & (0xFFu << k0)) << (8 * r);
     }
     return w;
