@@ -756,11 +756,17 @@ static int compact_one(const double *p, const double *sh, int ncam, const ocam *
         double nrm = sqrt(d0 * d0 + d1 * d1 + d2 * d2);
         double basis[16];
         sh_basis16(d0 / nrm, d1 / nrm, d2 / nrm, basis);
+        /* colors = basis @ sh^T (compaction.py:104, a BLAS product in the
+         * reference): fused multiply-adds in two interleaved partial sums
+         * (even / odd coefficients), the order the device uses */
         double col[3];
         for (int ch = 0; ch < 3; ch++) {
-            double acc = 0.0;
-            for (int i = 0; i < 16; i++) acc += basis[i] * sh[ch * 16 + i];
-            col[ch] = acc;
+            double a0 = 0.0, a1 = 0.0;
+            for (int i = 0; i < 16; i += 2) {
+                a0 = fma(basis[i], sh[ch * 16 + i], a0);
+                a1 = fma(basis[i + 1], sh[ch * 16 + i + 1], a1);
+            }
+            col[ch] = a0 + a1;
         }
         for (int i = 0; i < 16; i++) Ybuf[ns * 16 + i] = basis[i] * w[s];
         for (int ch = 0; ch < 3; ch++) {

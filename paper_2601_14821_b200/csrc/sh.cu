@@ -121,14 +121,31 @@ __global__ void __launch_bounds__(32 * kShWarps, POTR_SH_MIN_BLOCKS)
         for (int q = 0; q < 16; q++) acc[p][q] = 0.0;
     }
 
+    // the next view block's camera_importance tile is loaded into registers
+    // while the current one is processed (its global-load latency was the
+    // largest stall); each thread holds kPre of the 32 x 16 values
+    constexpr int kPre = 32 * kShSplatsPerBlock / (32 * kShWarps);
+    double pre[kPre];
+    const auto load_tile = [&](int s0) {
+        const int nv = ncam - s0 < 32 ? ncam - s0 : 32;
+#pragma unroll
+        for (int q = 0; q < kPre; q++) {
+            const int i = threadIdx.x + q * 32 * kShWarps;
+            const int v = i / kShSplatsPerBlock, kk = i % kShSplatsPerBlock;
+            pre[q] = (v < nv && kk < nk) ? cam_imp[(int64_t)(s0 + v) * n + k0 + kk] : 0.0;
+        }
+    };
+    load_tile(0);
     for (int s0 = 0; s0 < ncam; s0 += 32) {
         const int nv = ncam - s0 < 32 ? ncam - s0 : 32;
         __syncthreads();  // previous round done with wtile; first round: sh/pos staged
-        for (int i = threadIdx.x; i < 32 * kShSplatsPerBlock; i += blockDim.x) {
-            const int v = i / kShSplatsPerBlock, kk = i % kShSplatsPerBlock;
-            wtile[v][kk] = (v < nv && kk < nk) ? cam_imp[(int64_t)(s0 + v) * n + k0 + kk] : 0.0;
+#pragma unroll
+        for (int q = 0; q < kPre; q++) {
+            const int i = threadIdx.x + q * 32 * kShWarps;
+            wtile[i / kShSplatsPerBlock][i % kShSplatsPerBlock] = pre[q];
         }
         __syncthreads();
+        if (s0 + 32 < ncam) load_tile(s0 + 32);
         const bool lv = lane < nv;
         const double ex = lv ? eyes[3 * (s0 + lane)] : 0.0;
         const double ey = lv ? eyes[3 * (s0 + lane) + 1] : 0.0;
@@ -149,13 +166,19 @@ __global__ void __launch_bounds__(32 * kShWarps, POTR_SH_MIN_BLOCKS)
                     const double nrm = sqrt(d0 * d0 + d1 * d1 + d2 * d2);
                     double y[16];
                     sh_basis16(d0 / nrm, d1 / nrm, d2 / nrm, y);
+                    // colors = basis @ sh^T (compaction.py:104): fused
+                    // multiply-adds in two interleaved partial sums (the
+                    // oracle's order; a 16-deep add chain was the largest stall)
                     double col[3];
 #pragma unroll
                     for (int c = 0; c < 3; c++) {
-                        double t = 0.0;
+                        double a0 = 0.0, a1 = 0.0;
 #pragma unroll
-                        for (int i = 0; i < 16; i++) t += y[i] * shs[kk][c * 16 + i];
-                        col[c] = t;
+                        for (int i = 0; i < 16; i += 2) {
+                            a0 = fma(y[i], shs[kk][c * 16 + i], a0);
+                            a1 = fma(y[i + 1], shs[kk][c * 16 + i + 1], a1);
+                        }
+                        col[c] = a0 + a1;
                     }
 #pragma unroll
                     for (int i = 0; i < 16; i++) row[i] = y[i] * wv;
@@ -210,10 +233,17 @@ __global__ void __launch_bounds__(32 * kShWarps, POTR_SH_MIN_BLOCKS)
         if (kk >= nk) continue;
         const int64_t k = k0 + kk;
         if (owner) {
+            // all 16 reads issue before the first write (one latency, not 16)
+            double old[16];
 #pragma unroll
             for (int q = 0; q < 16; q++) {
                 const int e = sh_entry(4 * rb + (q >> 2), 4 * cb + (q & 3));  // cb 4: 16 + q
-                if (e >= 0) neq[(int64_t)e * n + k] += acc[p][q];
+                old[q] = e >= 0 ? neq[(int64_t)e * n + k] : 0.0;
+            }
+#pragma unroll
+            for (int q = 0; q < 16; q++) {
+                const int e = sh_entry(4 * rb + (q >> 2), 4 * cb + (q & 3));
+                if (e >= 0) neq[(int64_t)e * n + k] = old[q] + acc[p][q];
             }
         }
         if (hl == 0) neq[(int64_t)184 * n + k] += (double)seen[p];
