@@ -289,10 +289,17 @@ def main():
 
     import torch
     import torch.distributed as dist
+    if "POTR_BENCH_DEVICE" in os.environ:  # ranks sharing one GPU (with the gloo backend)
+        local = int(os.environ["POTR_BENCH_DEVICE"])
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        # gloo only to exercise the multi-rank logic on fewer GPUs than ranks
+        backend = os.environ.get("POTR_BENCH_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
 
     from paper_2601_14821_b200 import device as D
     from paper_2601_14821_b200 import distributed, rasterizer, compaction
@@ -388,7 +395,7 @@ def main():
     ms = ms_local
     if world > 1:
         t = torch.tensor([ms_local], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        distributed.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
     value = Pv / 1e6 / (ms / 1000.0)
 
@@ -516,7 +523,7 @@ def e2e_measure(args, rank, world, local, pert, cams, tg, S, Pv, dev):
         dt = (time.perf_counter() - t0) / args.steps
         if world > 1:
             t = torch.tensor([dt], dtype=torch.float64, device=dev)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            distributed.all_reduce(t, op=dist.ReduceOp.MAX)
             dt = float(t.item())
         res[kind] = dt
         del st
@@ -555,6 +562,19 @@ def scene_measure(args, world, ds, cams, my_cams, tptr, cam_arr, lo, hi, ctx, de
     rgb = torch.empty((n, 3, 16), dtype=torch.float64, device=dev)
     yc = torch.empty((n, 3, 16), dtype=torch.float64, device=dev)
     status = torch.empty(n, dtype=torch.int8, device=dev)
+    if world > 1:
+        from paper_2601_14821_b200 import distributed
+        rank = dist.get_rank()
+        c0, c1 = distributed.shard_range(n, rank, world)
+        nmax = max(distributed.shard_range(n, r, world)[1] - distributed.shard_range(n, r, world)[0]
+                   for r in range(world))
+        neq_s = torch.zeros((_native.NEQ_STRIDE, max(nmax, 1)), dtype=torch.float64, device=dev)
+        rgb_s = torch.empty((max(nmax, 1), 3, 16), dtype=torch.float64, device=dev)
+        yc_s = torch.empty((max(nmax, 1), 3, 16), dtype=torch.float64, device=dev)
+        status_s = torch.empty(max(nmax, 1), dtype=torch.int8, device=dev)
+        pack = torch.zeros((max(nmax, 1), 96), dtype=torch.float64, device=dev)
+        gathered = torch.empty(world * max(nmax, 1) * 96, dtype=torch.float64, device=dev)
+        all_cams = _native_cams(cams)
 
     def run(fused):
         t = {}
@@ -578,27 +598,46 @@ def scene_measure(args, world, ds, cams, my_cams, tptr, cam_arr, lo, hi, ctx, de
                      D.ptr(imp), D.ptr(ci), D.ptr(dm), D.ptr(mse))
         if world > 1:
             red = torch.cat([imp, dm, mse])
-            dist.all_reduce(red)
+            distributed.all_reduce(red)
         torch.cuda.synchronize()
         t2 = time.perf_counter()
-        neq.zero_()
-        ctx.call("potr_sh_accumulate", ctypes.byref(ds0.struct()), hi - lo, cam_arr, D.ptr(ci),
-                 D.ptr(neq))
-        if world > 1:
-            dist.all_reduce(neq)
-        ctx.call("potr_sh_solve", ctypes.byref(ds0.struct()), D.ptr(neq), ctypes.c_double(SH_LAMBDA),
-                 ctypes.c_double(0.8175744761936437), ctypes.c_double(0.5 / 51.0), D.ptr(rgb),
-                 D.ptr(yc), D.ptr(status))
+        if world == 1:
+            neq.zero_()
+            ctx.call("potr_sh_accumulate", ctypes.byref(ds0.struct()), hi - lo, cam_arr,
+                     D.ptr(ci), D.ptr(neq))
+            ctx.call("potr_sh_solve", ctypes.byref(ds0.struct()), D.ptr(neq),
+                     ctypes.c_double(SH_LAMBDA), ctypes.c_double(0.8175744761936437),
+                     ctypes.c_double(0.5 / 51.0), D.ptr(rgb), D.ptr(yc), D.ptr(status))
+        else:
+            # splat-sharded (distributed.compact_scene_sharded on device
+            # tensors): the all-to-all of camera_importance columns, this
+            # rank's splat span accumulated over every view and solved, one
+            # all-gather of the coefficients
+            ci_s = distributed.transpose_to_splat_shard(ci[:hi - lo], S, n)
+            ns = c1 - c0
+            neq_s.zero_()
+            sub = D.DeviceSplats(ds0.positions[c0:c1], ds0.sh[c0:c1], ds0.opacities[c0:c1],
+                                 ds0.scales[c0:c1], ds0.rotations[c0:c1])
+            ctx.call("potr_sh_accumulate", ctypes.byref(sub.struct()), S, all_cams,
+                     D.ptr(ci_s), D.ptr(neq_s))
+            ctx.call("potr_sh_solve", ctypes.byref(sub.struct()), D.ptr(neq_s),
+                     ctypes.c_double(SH_LAMBDA), ctypes.c_double(0.8175744761936437),
+                     ctypes.c_double(0.5 / 51.0), D.ptr(rgb_s), D.ptr(yc_s), D.ptr(status_s))
+            pack[:ns, :48] = rgb_s[:ns].reshape(ns, 48)
+            pack[:ns, 48:] = yc_s[:ns].reshape(ns, 48)
+            distributed._all_gather(gathered, pack.reshape(-1), None)
         torch.cuda.synchronize()
         t3 = time.perf_counter()
         t = torch.tensor([t1 - t0, t2 - t1, t3 - t2], dtype=torch.float64, device=dev)
         if world > 1:
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            distributed.all_reduce(t, op=dist.ReduceOp.MAX)
         return [float(x) for x in t.cpu()]
 
     run(False)  # warm
     parts = run(False)
-    ac = float((yc[:, :, 1:] == 0).double().mean().item())
+    ac = float((yc[:, :, 1:] == 0).double().mean().item()) if world == 1 else \
+        float((gathered.reshape(world, -1, 96)[:, :, 48:].reshape(-1, 3, 16)[:, :, 1:] == 0)
+              .double().mean().item())  # (padding rows included: an estimate)
     fused = run(True)
     out = {"total_s": sum(fused), "targets_and_prune_score_s": fused[0],
            "sh_recompute_s": fused[2],

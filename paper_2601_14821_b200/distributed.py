@@ -91,6 +91,18 @@ def _broadcast(t, src, group):
         dist.broadcast(t, src=_global(group, src), group=group)
 
 
+def all_reduce(t, op=None, group=None):
+    """dist.all_reduce that also works for CUDA tensors under gloo (staged)."""
+    op = dist.ReduceOp.SUM if op is None else op
+    if t.is_cuda and _staged(group):
+        h = t.cpu()
+        dist.all_reduce(h, op=op, group=group)
+        t.copy_(h)
+    else:
+        dist.all_reduce(t, op=op, group=group)
+    return t
+
+
 def _all_to_all(out, inp, out_splits, in_splits, group):
     if inp.is_cuda and _staged(group):
         h = torch.empty(out.shape, dtype=out.dtype)
