@@ -9,7 +9,7 @@ namespace {
 constexpr int kBins = 256;             // 8-bit digits
 constexpr int kSortThreads = 256;      // 8 warps; thread t owns digit t in the look-back
 #ifndef POTR_SORT_IPT
-#define POTR_SORT_IPT 16
+#define POTR_SORT_IPT 20
 #endif
 constexpr int kSortIpt = POTR_SORT_IPT;  // keys per thread
 constexpr int kTileItems = kSortThreads * kSortIpt;
@@ -84,9 +84,8 @@ __device__ __forceinline__ uint32_t block_exclusive_scan(uint32_t v, uint32_t *w
     return before + x - v;
 }
 
-// All passes' digit histograms in one read of the keys: shared atomics into
-// two sub-histograms per CTA (even / odd warps), with a warp-uniform digit
-// (a constant byte, common in the high digits) added once per warp.
+// All passes' digit histograms in one read of the keys: plain shared atomics
+// into two sub-histograms per CTA (even / odd warps).
 template <typename K>
 __global__ void __launch_bounds__(256) k_radix_hist(const K *__restrict__ keys, int64_t n,
                                                    int begin_bit, int passes,
@@ -94,7 +93,6 @@ __global__ void __launch_bounds__(256) k_radix_hist(const K *__restrict__ keys, 
     __shared__ uint32_t h[2][8 * kBins];
     for (int i = threadIdx.x; i < 2 * 8 * kBins; i += blockDim.x) (&h[0][0])[i] = 0;
     __syncthreads();
-    const int lane = threadIdx.x & 31;
     uint32_t *hw = h[(threadIdx.x >> 5) & 1];
     const int64_t stride = (int64_t)gridDim.x * blockDim.x * 4;
     for (int64_t base = (int64_t)blockIdx.x * blockDim.x * 4; base < n; base += stride) {
@@ -108,15 +106,9 @@ __global__ void __launch_bounds__(256) k_radix_hist(const K *__restrict__ keys, 
         }
 #pragma unroll
         for (int q = 0; q < 4; q++) {
-            const bool all = __all_sync(0xffffffffu, v[q]);
-            for (int p = 0; p < passes; p++) {
-                const uint32_t d = digit_of(k[q], begin_bit + 8 * p);
-                if (all && __all_sync(0xffffffffu, d == __shfl_sync(0xffffffffu, d, 0))) {
-                    if (lane == 0) atomicAdd(&hw[p * kBins + d], 32u);
-                } else if (v[q]) {
-                    atomicAdd(&hw[p * kBins + d], 1u);
-                }
-            }
+            if (!v[q]) continue;
+            for (int p = 0; p < passes; p++)
+                atomicAdd(&hw[p * kBins + digit_of(k[q], begin_bit + 8 * p)], 1u);
         }
     }
     __syncthreads();
