@@ -285,10 +285,14 @@ SortLayout sort_layout(void *temp, int64_t n, int passes) {
 // ---------------------------------------------------------------------------
 // scans: one tile of kScanThreads x kScanIpt items per CTA (blocked: thread t
 // holds items t*IPT .. t*IPT+IPT-1 of the tile), look-back on per-tile
-// (flag, aggregate, inclusive) published with release / acquire.
+// (flag | value) words packed in 64 bits, published and read relaxed (one
+// word carries both, so no acquire / L1 invalidation is needed).
 
 constexpr int kScanThreads = 256;
-constexpr int kScanIpt = 16;
+#ifndef POTR_SCAN_IPT
+#define POTR_SCAN_IPT 16
+#endif
+constexpr int kScanIpt = POTR_SCAN_IPT;
 constexpr int kScanTile = kScanThreads * kScanIpt;
 
 template <typename T>
