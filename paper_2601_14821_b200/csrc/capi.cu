@@ -35,8 +35,8 @@ struct potr_ctx {
     std::string err;
     int64_t launches = 0;
     // per-view workspace
-    // dup_id: record of each duplicated pair; perm: tile-sorted slot order;
-    // pair: per sorted pair (slot, record)
+    // dup_id: record of each duplicated pair; pair: per tile-sorted pair
+    // (slot, record); perm: the tile sort's alternate (slot, record) buffer
     DevBuf rec, key, skey, sids, cnt, offs, perm2, tkey, tskey, perm, pair, dup_id,
         dup_rank,
         partial, ranges, tile_se, temp, nvalid;
@@ -517,12 +517,11 @@ int bin_batch(potr_ctx *ctx, const potr_splats &sp, const potr_camera *cams, int
     const size_t kbytes = key16 ? sizeof(uint16_t) : sizeof(uint32_t);
     ENSURE(ctx->tkey, kbytes * K);
     ENSURE(ctx->tskey, kbytes * K);
-    ENSURE(ctx->perm, sizeof(int32_t) * K);
+    ENSURE(ctx->perm, sizeof(int2) * K);
     ENSURE(ctx->pair, sizeof(int2) * K);
     ENSURE(ctx->dup_id, sizeof(int32_t) * K);
     ENSURE(ctx->partial, sizeof(double2) * K);
     if (with_rank) ENSURE(ctx->dup_rank, sizeof(int32_t) * K);
-    ENSURE(ctx->perm2, sizeof(int32_t) * K);
     size_t t3 = 0;
     CK(tile_sort_temp(K, sb * g.ntiles, key16, &t3));
     ENSURE(ctx->temp, t3);
@@ -555,13 +554,16 @@ int bin_batch(potr_ctx *ctx, const potr_splats &sp, const potr_camera *cams, int
             const size_t koff = kbytes * (size_t)j0;
             bool alt = false;
             CK(tile_sort(ctx->temp.p, ctx->temp.cap, key16, (char *)ctx->tkey.p + koff,
-                         (char *)ctx->tskey.p + koff, P<int32_t>(ctx->perm) + j0,
-                         P<int32_t>(ctx->perm2) + j0, kk, sb * g.ntiles, &alt, ctx->stream));
+                         (char *)ctx->tskey.p + koff, P<int32_t>(ctx->dup_id) + j0, j0,
+                         P<int2>(ctx->pair) + j0, P<int2>(ctx->perm) + j0, kk, sb * g.ntiles,
+                         &alt, ctx->stream));
             ctx->launches += sort_launches(0, bits_for_tiles(sb * g.ntiles));
+            if (alt)  // odd pass count (few tiles, or 24-bit keys): result in the alternate
+                CK(cudaMemcpyAsync(P<int2>(ctx->pair) + j0, P<int2>(ctx->perm) + j0,
+                                   sizeof(int2) * (size_t)kk, cudaMemcpyDeviceToDevice,
+                                   ctx->stream));
             LAUNCH(1, launch_tile_ranges(j0, kk, key16,
                                          (char *)(alt ? ctx->tskey.p : ctx->tkey.p) + koff,
-                                         P<int32_t>(alt ? ctx->perm2 : ctx->perm) + j0,
-                                         P<int32_t>(ctx->dup_id), P<int2>(ctx->pair),
                                          P<int2>(ctx->ranges), v0 * g.ntiles, ctx->stream));
         }
         _st.end();

@@ -363,18 +363,14 @@ __global__ void k_duplicate(int64_t total, int64_t n, const int32_t *__restrict_
 }
 
 // Tile [start, end) ranges of the sorted pairs of one sort group (pairs
-// [j0, j0 + K) carrying group-local keys; tile index = tbase + key), and each
-// sorted pair's (slot, record) for the rasterizer's one 8-byte fetch.  The
-// sort's values are group-local pair indices (the implicit iota of its first
-// pass): slot = j0 + perm[j].  skey / perm point at the group's slice.
+// [j0, j0 + K) carrying group-local keys; tile index = tbase + key).  skey
+// points at the group's slice.  The sorted (slot, record) pairs come straight
+// out of the sort (radix_sort_packed).
 template <typename KeyT>
 __global__ void k_tile_ranges(int64_t j0, int64_t K, const KeyT *__restrict__ skey,
-                              const int32_t *__restrict__ perm, const int32_t *__restrict__ dup_id,
-                              int2 *__restrict__ pair, int2 *__restrict__ rng, int tbase) {
+                              int2 *__restrict__ rng, int tbase) {
     const int64_t jj = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (jj >= K) return;
-    const int32_t d = (int32_t)j0 + perm[jj];
-    pair[j0 + jj] = make_int2(d, dup_id[d]);
     const uint32_t t = skey[jj];
     if (jj == 0 || skey[jj - 1] != t) rng[tbase + t].x = (int)(j0 + jj);
     if (jj == K - 1 || skey[jj + 1] != t) rng[tbase + t].y = (int)(j0 + jj + 1);
@@ -1396,21 +1392,22 @@ static int bits_for(int ntiles) {
     return b;
 }
 
-// Stable sort of the pairs by tile key, values = group-local pair indices
-// (implicit iota in the first pass).  Double-buffered over (tkey, tkey_alt) x
-// (perm, perm_alt); *in_alt tells where the result is.
+// Stable sort of one sort group's pairs by tile key.  Pair j0 + i enters as
+// (slot = j0 + i, record = dup_id[i]) and leaves, in (tile, depth) order, as
+// the rasterizer's one 8-byte fetch.  Double-buffered over (tkey, tkey_alt) x
+// (pair, pair_alt); *in_alt tells where the result is.
 cudaError_t tile_sort(void *temp, size_t temp_bytes, bool key16, void *tkey, void *tkey_alt,
-                      int32_t *perm, int32_t *perm_alt, int64_t K, int nkeys, bool *in_alt,
-                      cudaStream_t st) {
+                      const int32_t *dup_id, int64_t j0, int2 *pair, int2 *pair_alt, int64_t K,
+                      int nkeys, bool *in_alt, cudaStream_t st) {
     *in_alt = false;
     if (K == 0) return cudaSuccess;
     if (key16)
-        return radix_sort_pairs<uint16_t, int32_t>(temp, temp_bytes, (uint16_t *)tkey,
-                                                   (uint16_t *)tkey_alt, perm, perm_alt, K, 0,
-                                                   bits_for(nkeys), true, in_alt, st);
-    return radix_sort_pairs<uint32_t, int32_t>(temp, temp_bytes, (uint32_t *)tkey,
-                                               (uint32_t *)tkey_alt, perm, perm_alt, K, 0,
-                                               bits_for(nkeys), true, in_alt, st);
+        return radix_sort_packed<uint16_t>(temp, temp_bytes, (uint16_t *)tkey,
+                                           (uint16_t *)tkey_alt, dup_id, j0, pair, pair_alt, K, 0,
+                                           bits_for(nkeys), in_alt, st);
+    return radix_sort_packed<uint32_t>(temp, temp_bytes, (uint32_t *)tkey, (uint32_t *)tkey_alt,
+                                       dup_id, j0, pair, pair_alt, K, 0, bits_for(nkeys), in_alt,
+                                       st);
 }
 
 cudaError_t tile_sort_temp(int64_t K, int nkeys, bool key16, size_t *bytes) {
@@ -1431,16 +1428,15 @@ cudaError_t records_sort(void *temp, size_t temp_bytes, uint64_t *key, uint64_t 
                                                0, 64, true, in_alt, st);
 }
 
-cudaError_t launch_tile_ranges(int64_t j0, int64_t K, bool key16, const void *skey,
-                               const int32_t *perm, const int32_t *dup_id, int2 *pair, int2 *rng,
+cudaError_t launch_tile_ranges(int64_t j0, int64_t K, bool key16, const void *skey, int2 *rng,
                                int tbase, cudaStream_t st) {
     if (K == 0) return cudaSuccess;
     if (key16)
-        k_tile_ranges<uint16_t><<<grid_for(K, 256), 256, 0, st>>>(
-            j0, K, (const uint16_t *)skey, perm, dup_id, pair, rng, tbase);
+        k_tile_ranges<uint16_t><<<grid_for(K, 256), 256, 0, st>>>(j0, K, (const uint16_t *)skey,
+                                                                  rng, tbase);
     else
-        k_tile_ranges<uint32_t><<<grid_for(K, 256), 256, 0, st>>>(
-            j0, K, (const uint32_t *)skey, perm, dup_id, pair, rng, tbase);
+        k_tile_ranges<uint32_t><<<grid_for(K, 256), 256, 0, st>>>(j0, K, (const uint32_t *)skey,
+                                                                  rng, tbase);
     return cudaGetLastError();
 }
 

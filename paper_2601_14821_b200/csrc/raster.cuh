@@ -101,14 +101,13 @@ cudaError_t launch_duplicate(int64_t total, int64_t n, const int32_t *ids, const
                              int32_t *dup_rank, cudaStream_t st);
 cudaError_t tile_sort_temp(int64_t K, int nkeys, bool key16, size_t *bytes);
 cudaError_t tile_sort(void *temp, size_t temp_bytes, bool key16, void *tkey, void *tkey_alt,
-                      int32_t *perm, int32_t *perm_alt, int64_t K, int nkeys, bool *in_alt,
-                      cudaStream_t st);
+                      const int32_t *dup_id, int64_t j0, int2 *pair, int2 *pair_alt, int64_t K,
+                      int nkeys, bool *in_alt, cudaStream_t st);
 cudaError_t records_sort_temp(int64_t m, size_t *bytes);
 cudaError_t records_sort(void *temp, size_t temp_bytes, uint64_t *key, uint64_t *key_alt,
                          int32_t *sidx, int32_t *sidx_alt, int64_t m, bool *in_alt,
                          cudaStream_t st);
-cudaError_t launch_tile_ranges(int64_t j0, int64_t K, bool key16, const void *skey,
-                               const int32_t *perm, const int32_t *dup_id, int2 *pair, int2 *rng,
+cudaError_t launch_tile_ranges(int64_t j0, int64_t K, bool key16, const void *skey, int2 *rng,
                                int tbase, cudaStream_t st);
 cudaError_t launch_raster(int mode, const RasterArgs &a, int ntiles, cudaStream_t st);
 cudaError_t launch_splat_reduce(int64_t total, int64_t n, const int32_t *ids, const int64_t *offs,

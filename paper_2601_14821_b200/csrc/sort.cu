@@ -38,11 +38,7 @@ __device__ __forceinline__ int64_t cnt_gather(const int32_t *ids, const int32_t 
     return (int64_t)cnt[ids[i]];
 }
 
-template <typename V>
-__global__ void k_iota_vals(int64_t n, V *v) {
-    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i < n) v[i] = (V)i;
-}
+
 
 // Lanes holding the same 8-bit digit (d < 256), or the same invalid marker
 // (d = 256): eight ballots on the digit bits -- full-rate VOTE/LOP instead of
@@ -118,12 +114,34 @@ __global__ void __launch_bounds__(256) k_radix_hist(const K *__restrict__ keys, 
     }
 }
 
+// Where a pass's input values come from.
+enum ValMode : int {
+    kValRead = 0,  // vin[i]
+    kValIota = 1,  // vbase + i (vin not read)
+    kValPack = 2,  // int64 = (hi[i] << 32) | (uint32)(vbase + i): an int2 {vbase + i, hi[i]}
+};
+
+template <typename V, int VM>
+__device__ __forceinline__ V input_value(const V *__restrict__ vin, const int32_t *__restrict__ hi,
+                                         int64_t vbase, int64_t i) {
+    if constexpr (VM == kValIota) {
+        return (V)(vbase + i);
+    } else if constexpr (VM == kValPack) {
+        static_assert(sizeof(V) == 8, "packed values are 64-bit");
+        return (V)(((uint64_t)(uint32_t)hi[i] << 32) | (uint64_t)(uint32_t)(vbase + i));
+    } else {
+        return vin[i];
+    }
+}
+
 // One LSD pass over digit (key >> shift) & 255.  Dynamic shared memory: the
 // tile's keys and values staged in digit order (kTileItems each).
-template <typename K, typename V, bool IOTA>
+template <typename K, typename V, int VM>
 __global__ void __launch_bounds__(kSortThreads) k_onesweep(const K *__restrict__ kin,
                                                            K *__restrict__ kout,
                                                            const V *__restrict__ vin,
+                                                           const int32_t *__restrict__ hi,
+                                                           int64_t vbase,
                                                            V *__restrict__ vout, int64_t n,
                                                            int shift,
                                                            const uint32_t *__restrict__ hist,
@@ -229,7 +247,7 @@ __global__ void __launch_bounds__(kSortThreads) k_onesweep(const K *__restrict__
             const int pos = (int)(boff[d] + whist[w][d] + rank[i]);
             POTR_CHECK(pos >= 0 && pos < tile_n);
             stage_k[pos] = k[i];
-            stage_v[pos] = IOTA ? (V)(base + j) : vin[base + j];
+            stage_v[pos] = input_value<V, VM>(vin, hi, vbase, base + j);
         }
     }
     __syncthreads();
@@ -249,11 +267,11 @@ constexpr size_t onesweep_smem() {
     return (sizeof(K) + sizeof(V)) * (size_t)kTileItems;
 }
 
-template <typename K, typename V, bool IOTA>
+template <typename K, typename V, int VM>
 void set_smem_attr() {
     static bool done = false;
     if (!done) {
-        cudaFuncSetAttribute(k_onesweep<K, V, IOTA>,
+        cudaFuncSetAttribute(k_onesweep<K, V, VM>,
                              cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)onesweep_smem<K, V>());
         done = true;
@@ -519,20 +537,43 @@ size_t radix_sort_temp_bytes(int64_t n, int begin_bit, int end_bit) {
     return sort_layout(nullptr, n, passes_for(begin_bit, end_bit)).bytes;
 }
 
-template <typename K, typename V>
-cudaError_t radix_sort_pairs(void *temp, size_t temp_bytes, K *keys, K *keys_alt, V *vals,
-                             V *vals_alt, int64_t n, int begin_bit, int end_bit, bool iota_vals,
-                             bool *in_alt, cudaStream_t st) {
+namespace {
+
+template <typename V, int VM>
+__global__ void k_init_vals(int64_t n, const int32_t *__restrict__ hi, int64_t vbase, V *v) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) v[i] = input_value<V, VM>(nullptr, hi, vbase, i);
+}
+
+template <typename K, typename V, int VM>
+void launch_onesweep(int64_t tiles, const K *kin, K *kout, const V *vin, const int32_t *hi,
+                     int64_t vbase, V *vout, int64_t n, int shift, const uint32_t *hist,
+                     uint64_t *status, uint32_t *ctr, cudaStream_t st) {
+    constexpr size_t smem = onesweep_smem<K, V>();
+    set_smem_attr<K, V, VM>();
+    k_onesweep<K, V, VM><<<(unsigned)tiles, kSortThreads, smem, st>>>(
+        kin, kout, vin, hi, vbase, vout, n, shift, hist, status, ctr);
+}
+
+// The LSD passes; the first pass takes its values per vm0, later ones read
+// the previous pass's output.
+template <typename K, typename V, int VM0>
+cudaError_t sort_impl(void *temp, size_t temp_bytes, K *keys, K *keys_alt, V *vals, V *vals_alt,
+                      const int32_t *hi, int64_t vbase, int64_t n, int begin_bit, int end_bit,
+                      bool *in_alt, cudaStream_t st) {
     *in_alt = false;
     if (n <= 0) return cudaSuccess;
     const int kbits = 8 * (int)sizeof(K);
     if (end_bit > kbits) end_bit = kbits;
     const int passes = passes_for(begin_bit, end_bit);
     if (passes == 0) {
-        if (!iota_vals) return cudaSuccess;
-        // no key bits: the order is the input order
-        k_iota_vals<V><<<(unsigned)((n + 255) / 256), 256, 0, st>>>(n, vals);
-        return cudaGetLastError();
+        if constexpr (VM0 == kValRead) {
+            return cudaSuccess;
+        } else {
+            // no key bits: the order is the input order
+            k_init_vals<V, VM0><<<(unsigned)((n + 255) / 256), 256, 0, st>>>(n, hi, vbase, vals);
+            return cudaGetLastError();
+        }
     }
     SortLayout L = sort_layout(temp, n, passes);
     if (L.bytes > temp_bytes) return cudaErrorInvalidValue;
@@ -550,16 +591,12 @@ cudaError_t radix_sort_pairs(void *temp, size_t temp_bytes, K *keys, K *keys_alt
     for (int p = 0; p < passes; p++) {
         const int shift = begin_bit + 8 * p;
         uint64_t *status = L.status + (size_t)p * kBins * tiles;
-        constexpr size_t smem = onesweep_smem<K, V>();
-        if (p == 0 && iota_vals) {
-            set_smem_attr<K, V, true>();
-            k_onesweep<K, V, true><<<(unsigned)tiles, kSortThreads, smem, st>>>(
-                ka, kb, nullptr, vb, n, shift, L.hist + p * kBins, status, L.ctr + p);
-        } else {
-            set_smem_attr<K, V, false>();
-            k_onesweep<K, V, false><<<(unsigned)tiles, kSortThreads, smem, st>>>(
-                ka, kb, va, vb, n, shift, L.hist + p * kBins, status, L.ctr + p);
-        }
+        if (p == 0)
+            launch_onesweep<K, V, VM0>(tiles, ka, kb, va, hi, vbase, vb, n, shift,
+                                       L.hist + p * kBins, status, L.ctr + p, st);
+        else
+            launch_onesweep<K, V, kValRead>(tiles, ka, kb, va, nullptr, 0, vb, n, shift,
+                                            L.hist + p * kBins, status, L.ctr + p, st);
         e = cudaGetLastError();
         if (e != cudaSuccess) return e;
         K *tk = ka;
@@ -572,6 +609,38 @@ cudaError_t radix_sort_pairs(void *temp, size_t temp_bytes, K *keys, K *keys_alt
     *in_alt = (passes & 1) != 0;
     return cudaSuccess;
 }
+
+}  // namespace
+
+template <typename K, typename V>
+cudaError_t radix_sort_pairs(void *temp, size_t temp_bytes, K *keys, K *keys_alt, V *vals,
+                             V *vals_alt, int64_t n, int begin_bit, int end_bit, bool iota_vals,
+                             bool *in_alt, cudaStream_t st) {
+    if (iota_vals)
+        return sort_impl<K, V, kValIota>(temp, temp_bytes, keys, keys_alt, vals, vals_alt,
+                                         nullptr, 0, n, begin_bit, end_bit, in_alt, st);
+    return sort_impl<K, V, kValRead>(temp, temp_bytes, keys, keys_alt, vals, vals_alt, nullptr,
+                                     0, n, begin_bit, end_bit, in_alt, st);
+}
+
+template <typename K>
+cudaError_t radix_sort_packed(void *temp, size_t temp_bytes, K *keys, K *keys_alt,
+                              const int32_t *hi, int64_t vbase, int2 *vals, int2 *vals_alt,
+                              int64_t n, int begin_bit, int end_bit, bool *in_alt,
+                              cudaStream_t st) {
+    static_assert(sizeof(int2) == sizeof(int64_t), "int2 is one 64-bit word");
+    return sort_impl<K, int64_t, kValPack>(temp, temp_bytes, keys, keys_alt,
+                                           reinterpret_cast<int64_t *>(vals),
+                                           reinterpret_cast<int64_t *>(vals_alt), hi, vbase, n,
+                                           begin_bit, end_bit, in_alt, st);
+}
+
+template cudaError_t radix_sort_packed<uint16_t>(void *, size_t, uint16_t *, uint16_t *,
+                                                 const int32_t *, int64_t, int2 *, int2 *,
+                                                 int64_t, int, int, bool *, cudaStream_t);
+template cudaError_t radix_sort_packed<uint32_t>(void *, size_t, uint32_t *, uint32_t *,
+                                                 const int32_t *, int64_t, int2 *, int2 *,
+                                                 int64_t, int, int, bool *, cudaStream_t);
 
 template cudaError_t radix_sort_pairs<uint16_t, int32_t>(void *, size_t, uint16_t *, uint16_t *,
                                                          int32_t *, int32_t *, int64_t, int, int,

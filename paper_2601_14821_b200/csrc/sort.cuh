@@ -33,6 +33,17 @@ cudaError_t radix_sort_pairs(void *temp, size_t temp_bytes, K *keys, K *keys_alt
                              V *vals_alt, int64_t n, int begin_bit, int end_bit, bool iota_vals,
                              bool *in_alt, cudaStream_t st);
 
+// Stable sort of keys with packed int2 values: item i enters as
+// {vbase + i, hi[i]} (hi read once, in order, by the first pass), so the
+// sorted values carry both the item's index and its payload -- no gather after
+// the sort.  Result in (keys, vals) or, with *in_alt, (keys_alt, vals_alt).
+// K: uint16_t, uint32_t.
+template <typename K>
+cudaError_t radix_sort_packed(void *temp, size_t temp_bytes, K *keys, K *keys_alt,
+                              const int32_t *hi, int64_t vbase, int2 *vals, int2 *vals_alt,
+                              int64_t n, int begin_bit, int end_bit, bool *in_alt,
+                              cudaStream_t st);
+
 // Kernel launches of one radix_sort_pairs call (histogram + one per pass).
 inline int sort_launches(int begin_bit, int end_bit) {
     return end_bit > begin_bit ? 1 + (end_bit - begin_bit + 7) / 8 : 0;
