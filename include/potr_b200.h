@@ -244,6 +244,11 @@ int potr_attribute_streams(potr_ctx *ctx, int64_t n, const int64_t *order, const
  * TLB locality for the rasterizer's fetches); 0: splat order.  Results are
  * bit-identical either way. */
 #define POTR_OPT_SPATIAL_RECORDS 4
+/* View batches binned ahead while a scoring call's SH rows are still
+ * uploading (potr_upload_async), 1..8, default 6 (env POTR_B200_LOOKAHEAD);
+ * each holds its own records and pair lists, bounded to half the free device
+ * memory.  Results are bit-identical for every value. */
+#define POTR_OPT_LOOKAHEAD 5
 int potr_set_option(potr_ctx *ctx, int option, int value);
 
 /* ---- evidence: live stage timing and work counters --------------------- */
@@ -280,6 +285,24 @@ int potr_counters_read(potr_ctx *ctx, uint64_t *out);
  * into a pinned ring while the DMA engine moves the previous chunk.  The
  * source may be reused when the call returns. */
 int potr_copy_to_device(potr_ctx *ctx, void *dst, const void *src, int64_t bytes);
+
+/* Queues a host -> device copy of `bytes` from `src` (pinned or pageable) to
+ * `dst` and returns at once; one library worker thread runs the queue in
+ * order (the pinned ring for pageable sources, host threads filling it).  A
+ * scoring call (potr_score_views*, potr_forward_stats) whose splats' sh is
+ * the destination of the LAST queued copy waits only for the earlier ones
+ * (positions before its bounds, the other attributes before its first
+ * batch), bins its first view batches while the rows arrive (their geometry
+ * needs no SH) and gives them their colours once the copy is done -- this is
+ * how the reference's per-call upload of a fresh subset() (pruning.py:161)
+ * overlaps the binning.  Every other entry point, and potr_upload_wait,
+ * completes all queued copies first; each `src` must stay valid until then.
+ * Replaces the reference's implicit numpy -> device transfer (no reference
+ * counterpart). */
+int potr_upload_async(potr_ctx *ctx, void *dst, const void *src, int64_t bytes);
+/* Completes every queued potr_upload_async (the context stream is ordered
+ * after them); returns the first error, if any.  No-op without any. */
+int potr_upload_wait(potr_ctx *ctx);
 
 /* forward_stats with HOST arrays in the reference layouts; copies in, runs,
  * copies out and synchronizes.  targets: host array of ncam host pointers or

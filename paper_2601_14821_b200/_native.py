@@ -23,6 +23,7 @@ OPT_VIEW_BATCH = 1
 OPT_RAW_DEPTH_KEYS = 2
 OPT_TILE_CULL = 3
 OPT_SPATIAL_RECORDS = 4
+OPT_LOOKAHEAD = 5
 STAGES = ["preprocess", "depth_sort", "scan", "duplicate", "tile_sort", "raster", "reduce",
           "sh_accumulate", "sh_solve"]
 
@@ -80,6 +81,9 @@ _SIGNATURES = {
                                            ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]),
     "potr_copy_to_device": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
                                            ctypes.c_int64]),
+    "potr_upload_async": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+                                         ctypes.c_int64]),
+    "potr_upload_wait": (ctypes.c_int, [ctypes.c_void_p]),
     "potr_removal_order": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p,
                                           ctypes.c_void_p, ctypes.c_double, ctypes.c_double,
                                           ctypes.c_void_p]),

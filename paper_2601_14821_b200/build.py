@@ -40,19 +40,27 @@ def needs_build():
 
 
 def build(force=False, verbose=False):
-    """Compile if any source is newer than the library; returns its path."""
+    """Compile if any source is newer than the library; returns its path.
+    Process-safe: concurrent callers (ranks of one job) serialize on a lock
+    file and the library is replaced atomically."""
+    import fcntl
     if not force and not needs_build():
         return LIB
     os.makedirs(os.path.dirname(LIB), exist_ok=True)
-    flags = list(NVCC_FLAGS) + (["-Xptxas", "-v"] if verbose else [])
-    cmd = [nvcc(), *flags, "-o", LIB + ".tmp", *[os.path.join(CSRC, s) for s in SOURCES]]
-    res = subprocess.run(cmd, capture_output=True, text=True)
-    if res.returncode != 0:
-        sys.stderr.write(res.stdout + res.stderr)
-        raise RuntimeError("nvcc failed building libpotr_b200.so")
-    if verbose:
-        sys.stderr.write(res.stderr)
-    os.replace(LIB + ".tmp", LIB)
+    with open(LIB + ".lock", "w") as lock:
+        fcntl.flock(lock, fcntl.LOCK_EX)
+        if not force and not needs_build():  # another process built it meanwhile
+            return LIB
+        tmp = f"{LIB}.{os.getpid()}.tmp"
+        flags = list(NVCC_FLAGS) + (["-Xptxas", "-v"] if verbose else [])
+        cmd = [nvcc(), *flags, "-o", tmp, *[os.path.join(CSRC, s) for s in SOURCES]]
+        res = subprocess.run(cmd, capture_output=True, text=True)
+        if res.returncode != 0:
+            sys.stderr.write(res.stdout + res.stderr)
+            raise RuntimeError("nvcc failed building libpotr_b200.so")
+        if verbose:
+            sys.stderr.write(res.stderr)
+        os.replace(tmp, LIB)
     return LIB
 
 

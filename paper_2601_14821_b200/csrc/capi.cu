@@ -7,7 +7,12 @@
 #include <cstring>
 #include <omp.h>
 #include <nvtx3/nvToolsExt.h>
+#include <condition_variable>
+#include <deque>
+#include <functional>
+#include <mutex>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "common.cuh"
@@ -80,6 +85,42 @@ struct potr_ctx {
     bool spatial_ok = false;     // this call's splats have a slot order
     bool prep_ok = false;        // ctx->prep holds this call's splats
     bool batch_spatial = false;  // the last bin_batch ran in slot space
+    bool slot_sh_pending = false;  // slot_sh not yet filled (SH rows still uploading)
+    // potr_upload_async: host -> device copies queued FIFO on copy_stream and
+    // driven by one persistent worker thread (the pinned ring for pageable
+    // sources, a plain async copy for pinned ones); each records its event
+    struct UploadJob {
+        int64_t seq;
+        void *dst;
+        const void *src;
+        int64_t bytes;
+        cudaEvent_t ev;
+    };
+    cudaStream_t copy_stream = nullptr;
+    cudaEvent_t upload_after = nullptr;
+    std::thread upload_worker;
+    std::mutex upload_mu;
+    std::condition_variable upload_cv;
+    std::deque<UploadJob> upload_todo;   // the worker's queue (under upload_mu)
+    std::vector<UploadJob> upload_jobs;  // issued and not yet joined (caller's thread)
+    std::vector<cudaEvent_t> upload_ev_pool;
+    int64_t upload_issued = 0;
+    int64_t upload_done = 0;  // under upload_mu
+    bool upload_quit = false;  // under upload_mu
+    int upload_rc = 0;         // first failure, under upload_mu
+    std::string upload_err;
+    bool upload_pending = false;  // upload_jobs is not empty
+    // Binned batches waiting for their raster: while the SH rows upload, the
+    // scoring loop bins up to `lookahead` batches ahead (colours deferred),
+    // each into its own set of the buffers that binning hands to the raster
+    // and reduce (the active set lives in rec / sids / offs / pair / ranges).
+    static constexpr int kMaxSets = 8;
+    struct BatchSet {
+        DevBuf rec, sids, offs, pair, ranges;
+    };
+    BatchSet sets[kMaxSets];
+    int active_set = 0;
+    int lookahead = 6;  // POTR_B200_LOOKAHEAD
 };
 
 namespace {
@@ -264,6 +305,156 @@ int bitlen(uint64_t x) {
     return b;
 }
 
+// ---- uploads -------------------------------------------------------------
+
+// Pageable host -> device: chunks of kRingChunk bytes go through a ring of
+// pinned buffers; host threads (OpenMP) fill chunk c + 1 while the DMA engine
+// moves chunk c, so a pageable source uploads at close to the pinned PCIe
+// rate instead of the driver's single-threaded staging.  Thread-safe against
+// the caller's thread (potr_upload_async runs it on its own thread): touches
+// only the ring and `st`, reports through *err.
+constexpr size_t kRingChunk = (size_t)32 << 20;
+
+int ring_threads(int spare) {
+    int t = omp_get_num_procs() - spare;
+    return t < 1 ? 1 : t > 16 ? 16 : t;
+}
+
+int ring_copy(potr_ctx *ctx, void *dst, const void *src, int64_t bytes, cudaStream_t st,
+              int threads, std::string *err) {
+#define RING_CK(expr)                                                        \
+    do {                                                                     \
+        cudaError_t _e = (expr);                                             \
+        if (_e != cudaSuccess) {                                             \
+            *err = std::string(#expr) + ": " + cudaGetErrorString(_e);       \
+            return POTR_E_CUDA;                                              \
+        }                                                                    \
+    } while (0)
+    for (int r = 0; r < potr_ctx::kRing; r++) {
+        if (!ctx->ring[r]) {
+            RING_CK(cudaMallocHost(&ctx->ring[r], kRingChunk));
+            RING_CK(cudaEventCreateWithFlags(&ctx->ring_ev[r], cudaEventDisableTiming));
+        }
+    }
+    const char *s = reinterpret_cast<const char *>(src);
+    char *d = reinterpret_cast<char *>(dst);
+    int64_t c = 0;
+    for (int64_t off = 0; off < bytes; off += (int64_t)kRingChunk, c++) {
+        const int b = (int)(c % potr_ctx::kRing);
+        const int64_t len = bytes - off < (int64_t)kRingChunk ? bytes - off : (int64_t)kRingChunk;
+        // the buffer's previous DMA (from this call or an earlier one) must be
+        // done before it is refilled; a never-recorded event returns at once
+        RING_CK(cudaEventSynchronize(ctx->ring_ev[b]));
+        char *stage = reinterpret_cast<char *>(ctx->ring[b]);
+        const int t_used = len < ((int64_t)1 << 20) ? 1 : threads;
+#pragma omp parallel for num_threads(t_used) schedule(static)
+        for (int t = 0; t < t_used; t++) {
+            const int64_t a = len * t / t_used, e = len * (t + 1) / t_used;
+            std::memcpy(stage + a, s + off + a, (size_t)(e - a));
+        }
+        RING_CK(cudaMemcpyAsync(d + off, stage, (size_t)len, cudaMemcpyHostToDevice, st));
+        RING_CK(cudaEventRecord(ctx->ring_ev[b], st));
+    }
+#undef RING_CK
+    return POTR_OK;
+}
+
+// Waits until upload `seq` (and so every earlier one: one FIFO worker, one
+// copy stream) is issued, and orders the context stream after it.
+int upload_wait_seq(potr_ctx *ctx, int64_t seq) {
+    if (seq <= 0) return 0;
+    cudaEvent_t ev = nullptr;
+    for (auto &j : ctx->upload_jobs)
+        if (j.seq == seq) ev = j.ev;
+    int rc;
+    std::string err;
+    {
+        std::unique_lock<std::mutex> lk(ctx->upload_mu);
+        ctx->upload_cv.wait(lk, [ctx, seq] { return ctx->upload_done >= seq; });
+        rc = ctx->upload_rc;
+        err = ctx->upload_err;
+    }
+    if (rc) return fail(ctx, rc, "upload: " + err);
+    if (ev) CK(cudaStreamWaitEvent(ctx->stream, ev, 0));
+    return 0;
+}
+
+// The pending upload whose destination is `dst` (its seq), or 0.
+int64_t upload_seq_of(potr_ctx *ctx, const void *dst) {
+    for (auto &j : ctx->upload_jobs)
+        if (j.dst == dst) return j.seq;
+    return 0;
+}
+
+// Completes every pending potr_upload_async: the host side is done with the
+// sources and the context stream is ordered after the copies.
+int upload_join(potr_ctx *ctx) {
+    if (ctx->upload_jobs.empty()) return 0;
+    const int rc = upload_wait_seq(ctx, ctx->upload_jobs.back().seq);
+    {
+        // on failure the worker skips the rest: wait for it to pass them all
+        std::unique_lock<std::mutex> lk(ctx->upload_mu);
+        const int64_t last = ctx->upload_jobs.back().seq;
+        ctx->upload_cv.wait(lk, [ctx, last] { return ctx->upload_done >= last; });
+        ctx->upload_rc = 0;
+        ctx->upload_err.clear();
+    }
+    for (auto &j : ctx->upload_jobs) ctx->upload_ev_pool.push_back(j.ev);
+    ctx->upload_jobs.clear();
+    ctx->upload_pending = false;
+    return rc;
+}
+
+#define JOIN_UPLOAD(ctx)                   \
+    do {                                   \
+        int _jrc = upload_join(ctx);       \
+        if (_jrc) return _jrc;             \
+    } while (0)
+
+// Makes buffer set j the active one (potr_ctx::BatchSet).
+void activate_set(potr_ctx *ctx, int j) {
+    if (j == ctx->active_set) return;
+    auto swap_in = [ctx](potr_ctx::BatchSet &b) {
+        std::swap(ctx->rec, b.rec);
+        std::swap(ctx->sids, b.sids);
+        std::swap(ctx->offs, b.offs);
+        std::swap(ctx->pair, b.pair);
+        std::swap(ctx->ranges, b.ranges);
+    };
+    swap_in(ctx->sets[ctx->active_set]);  // park the active set
+    swap_in(ctx->sets[j]);
+    ctx->active_set = j;
+}
+
+// Grows the active set's buffers to the largest capacity any set has seen, so
+// sets that take turns with batches of different sizes stop reallocating (a
+// cudaFree synchronizes the device, which would stall the upload overlap).
+int level_active_set(potr_ctx *ctx) {
+    size_t cap[5] = {0, 0, 0, 0, 0};
+    for (auto &b : ctx->sets) {
+        const DevBuf *d[5] = {&b.rec, &b.sids, &b.offs, &b.pair, &b.ranges};
+        for (int i = 0; i < 5; i++) cap[i] = d[i]->cap > cap[i] ? d[i]->cap : cap[i];
+    }
+    DevBuf *a[5] = {&ctx->rec, &ctx->sids, &ctx->offs, &ctx->pair, &ctx->ranges};
+    for (int i = 0; i < 5; i++) {
+        if (!a[i]->cap || a[i]->cap >= cap[i]) continue;
+        CK(cudaStreamSynchronize(ctx->stream));
+        CK(cudaFree(a[i]->p));
+        a[i]->p = nullptr;
+        a[i]->cap = 0;
+        if (cudaMalloc(&a[i]->p, cap[i]) != cudaSuccess) {
+            cudaGetLastError();
+            return fail(ctx, POTR_E_NOMEM, "cudaMalloc(" + std::to_string(cap[i]) + ")");
+        }
+        a[i]->cap = cap[i];  // exactly the largest: no headroom, no runaway growth
+    }
+    return 0;
+}
+
+size_t active_set_bytes(potr_ctx *ctx) {
+    return ctx->rec.cap + ctx->sids.cap + ctx->offs.cap + ctx->pair.cap + ctx->ranges.cap;
+}
+
 // The view-independent splat terms (k_splat_prep) in splat order, once per
 // call when a batch runs in splat order.
 int ensure_prep(potr_ctx *ctx, const potr_splats &sp) {
@@ -280,8 +471,16 @@ int ensure_prep(potr_ctx *ctx, const potr_splats &sp) {
 // reduction + sync: they bound every view's depth range, which makes the batch
 // depth key compact), then the spatial slot order and the slot-ordered splat
 // copy with its view-independent terms (or those terms in splat order).
-int compute_scene_bounds(potr_ctx *ctx, const potr_splats &sp) {
+// defer_sh: the SH rows are still uploading (potr_upload_async); their slot-
+// ordered copy waits for fill_slot_sh.
+// pos_seq / geo_seq: pending uploads (potr_upload_async) to wait for before
+// the positions are read / before the other attributes are.
+int compute_scene_bounds(potr_ctx *ctx, const potr_splats &sp, bool defer_sh = false,
+                         int64_t pos_seq = 0, int64_t geo_seq = 0) {
     ctx->spatial_ok = ctx->prep_ok = ctx->batch_spatial = false;
+    ctx->slot_sh_pending = false;
+    int wrc = upload_wait_seq(ctx, pos_seq);
+    if (wrc) return wrc;
     ENSURE(ctx->bbox, 6 * sizeof(unsigned long long));
     LAUNCH(1, launch_bbox(sp.n, sp.positions, P<unsigned long long>(ctx->bbox), ctx->stream));
     CK(cudaMemcpyAsync(ctx->pinned, ctx->bbox.p, 6 * sizeof(uint64_t), cudaMemcpyDeviceToHost,
@@ -291,7 +490,10 @@ int compute_scene_bounds(potr_ctx *ctx, const potr_splats &sp) {
         ctx->scene_lo[i] = ordered_to_double((unsigned long long)ctx->pinned[i]);
         ctx->scene_hi[i] = ordered_to_double((unsigned long long)ctx->pinned[3 + i]);
     }
-    if (!ctx->spatial || sp.n == 0) return ensure_prep(ctx, sp);
+    if (!ctx->spatial || sp.n == 0) {
+        if ((wrc = upload_wait_seq(ctx, geo_seq))) return wrc;
+        return ensure_prep(ctx, sp);
+    }
     Stage _st(ctx, POTR_STAGE_PREPROCESS);
     ENSURE(ctx->mperm, sizeof(int32_t) * sp.n);
     ENSURE(ctx->mrank, sizeof(int32_t) * sp.n);
@@ -307,11 +509,26 @@ int compute_scene_bounds(potr_ctx *ctx, const potr_splats &sp) {
     LAUNCH(7, spatial_order(ctx->temp.p, ctx->temp.cap, sp.n, sp.positions, ctx->scene_lo,
                             ctx->scene_hi, P<uint32_t>(ctx->mcode), P<uint32_t>(ctx->mcode2),
                             P<int32_t>(ctx->mperm), P<int32_t>(ctx->mrank), ctx->stream));
+    // the other attributes: from here on (the Morton order needed positions only)
+    if ((wrc = upload_wait_seq(ctx, geo_seq))) return wrc;
     LAUNCH(1, launch_splat_slots(sp, P<int32_t>(ctx->mperm), P<double>(ctx->slot_pos),
-                                 P<double>(ctx->slot_sh), P<double>(ctx->slot_opac),
-                                 P<SplatPrep>(ctx->slot_prep), ctx->stream));
+                                 defer_sh ? nullptr : P<double>(ctx->slot_sh),
+                                 P<double>(ctx->slot_opac), P<SplatPrep>(ctx->slot_prep),
+                                 ctx->stream));
     _st.end();
     ctx->spatial_ok = true;
+    ctx->slot_sh_pending = defer_sh;
+    return 0;
+}
+
+// The slot-ordered SH copy that compute_scene_bounds(defer_sh) left out.
+int fill_slot_sh(potr_ctx *ctx, const potr_splats &sp) {
+    if (!ctx->slot_sh_pending) return 0;
+    Stage _st(ctx, POTR_STAGE_PREPROCESS);
+    LAUNCH(1, launch_slot_sh(sp.n, sp.sh, P<int32_t>(ctx->mperm), P<double>(ctx->slot_sh),
+                             ctx->stream));
+    _st.end();
+    ctx->slot_sh_pending = false;
     return 0;
 }
 
@@ -375,8 +592,11 @@ DepthKey depth_key_for(potr_ctx *ctx, const potr_camera *cams, int nview, int64_
 // over-long run of equal hi keys to 1.
 // cull: drop (tile, splat) pairs no sample of which passes the exp prefilter
 // (raster.cu row_span); off for potr_bin, whose lists are the bbox lists.
+// colors = false: the records' colours are left to launch_batch_colors (SH
+// rows still uploading; all_colors must then be false).
 int bin_batch(potr_ctx *ctx, const potr_splats &sp, const potr_camera *cams, int nview,
-              bool all_colors, bool with_rank, bool cull, int64_t *K_out, int depth_mode = 2) {
+              bool all_colors, bool with_rank, bool cull, int64_t *K_out, int depth_mode = 2,
+              bool colors = true) {
     const int64_t n = sp.n;
     const int64_t total = n * nview;
     ViewGeom g = geom(cams[0]);
@@ -434,10 +654,11 @@ int bin_batch(potr_ctx *ctx, const potr_splats &sp, const potr_camera *cams, int
 
     {
         Stage _st(ctx, POTR_STAGE_PREPROCESS);
-        LAUNCH(1, launch_preprocess(sp_b, prep_b, cb, nview, g.tiles_x, all_colors ? 1 : 0, cull ? 1 : 0, dk,
+        LAUNCH(1, launch_preprocess(sp_b, prep_b, cb, nview, g.tiles_x, all_colors ? 1 : 0,
+                                    colors ? 1 : 0, cull ? 1 : 0, dk,
                                     P<SplatRec>(ctx->rec), P<TileSpan>(ctx->spans),
                                     P<uint64_t>(ctx->key),
-                                    P<int32_t>(ctx->cnt), P<int32_t>(ctx->vidx), counters(ctx),
+                                    P<int32_t>(ctx->cnt), counters(ctx),
                                     ctx->stream));
         _st.end();
     }
@@ -466,7 +687,7 @@ int bin_batch(potr_ctx *ctx, const potr_splats &sp, const potr_camera *cams, int
             ctx->launches += sort_launches(0, end_bit);
             CK(depth_sort(ctx->temp.p, ctx->temp.cap, P<uint64_t>(ctx->key),
                           P<uint64_t>(ctx->skey), P<int32_t>(ctx->vidx), P<int32_t>(ctx->sids),
-                          total, end_bit, &alt, ctx->stream));
+                          total, end_bit, 0, &alt, ctx->stream));
             if (!alt) {
                 std::swap(ctx->key, ctx->skey);
                 std::swap(ctx->vidx, ctx->sids);
@@ -478,7 +699,8 @@ int bin_batch(potr_ctx *ctx, const potr_splats &sp, const potr_camera *cams, int
             for (int v = 0; v < nview; v++)
                 CK(depth_sort(ctx->temp.p, ctx->temp.cap, P<uint64_t>(ctx->key) + v * n,
                               P<uint64_t>(ctx->skey) + v * n, P<int32_t>(ctx->vidx) + v * n,
-                              P<int32_t>(ctx->sids) + v * n, n, 64, &alt, ctx->stream));
+                              P<int32_t>(ctx->sids) + v * n, n, 64, (int64_t)v * n, &alt,
+                              ctx->stream));
             if (!alt) {
                 std::swap(ctx->key, ctx->skey);
                 std::swap(ctx->vidx, ctx->sids);
@@ -502,9 +724,9 @@ int bin_batch(potr_ctx *ctx, const potr_splats &sp, const potr_camera *cams, int
     int flags[2];
     std::memcpy(flags, ctx->pinned + 1, sizeof(flags));
     if (dk.compact && flags[0] != 0)  // bound violated: exact raw-key fallback
-        return bin_batch(ctx, sp, cams, nview, all_colors, with_rank, cull, K_out, 0);
+        return bin_batch(ctx, sp, cams, nview, all_colors, with_rank, cull, K_out, 0, colors);
     if (split && flags[1] != 0)  // a long run of equal hi keys: 64-bit compact sort
-        return bin_batch(ctx, sp, cams, nview, all_colors, with_rank, cull, K_out, 1);
+        return bin_batch(ctx, sp, cams, nview, all_colors, with_rank, cull, K_out, 1, colors);
     const int64_t K = ctx->pinned[0];
     ctx->invalid_key0 = dk.compact ? dk.sentinel : ~0ull;
     ctx->pairs_total += K;
@@ -606,31 +828,101 @@ int batch_len(potr_ctx *ctx, const potr_camera *cams, int s, int ncam, int64_t n
     return b;
 }
 
+// A binned batch waiting for its raster (score_views_run).
+struct BatchMeta {
+    int set, s, nb;
+    bool spatial, split, colors_pending;
+    uint64_t invalid_key0;
+};
+
 // images (nullable): with targets == images the targets are this very render
 // (self-target mode: the first pruning iteration of an encode, whose targets
 // are the renders of the unmodified model) -- rendered and scored in one pass.
-int score_views_impl(potr_ctx *ctx, const potr_splats *sp, int ncam, const potr_camera *cams,
-                     const double *const *targets, double *imp_sum, double *cam_imp,
-                     double *dmse_sum, double *mse_sum, double *dmse_rows = nullptr,
-                     double *mse_rows = nullptr, double *const *images = nullptr) {
+//
+// When the splats' SH rows are the destination of the pending
+// potr_upload_async, the loop bins up to ctx->lookahead batches ahead (their
+// geometry needs no SH) while the rows arrive, each batch in its own buffer
+// set, then gives them their colours and rasters them in camera order; the
+// view-order accumulation, and so every result bit, is unchanged.
+int score_views_run(potr_ctx *ctx, const potr_splats *sp, int ncam, const potr_camera *cams,
+                    const double *const *targets, double *imp_sum, double *cam_imp,
+                    double *dmse_sum, double *mse_sum, double *dmse_rows, double *mse_rows,
+                    double *const *images) {
     const int64_t n = sp->n;
-    int brc = compute_scene_bounds(ctx, *sp);
-    if (brc) return brc;
-    for (int s = 0; s < ncam;) {
-        int rc = check_cam(ctx, &cams[s]);
-        if (rc) return rc;
-        const int nb = batch_len(ctx, cams, s, ncam, n);
-        for (int v = 0; v < nb; v++)
-            if (targets && !targets[s + v]) return fail(ctx, POTR_E_ARG, "target pointer is NULL");
-        int64_t K = 0;
-        rc = bin_batch(ctx, *sp, cams + s, nb, false, false, ctx->tile_cull, &K);
-        if (rc) return rc;
-        ViewGeom g = geom(cams[s]);
-        RasterArgs a = raster_args(ctx, cams[s], nb);
-        for (int v = 0; v < nb; v++) a.target[v] = targets ? targets[s + v] : nullptr;
+    // the splats' SH rows are the last pending upload: bin while they arrive
+    const bool defer = n > 0 && ncam > 0 && !ctx->upload_jobs.empty() &&
+                       ctx->upload_jobs.back().dst == sp->sh &&
+                       ctx->upload_jobs.back().bytes >= (int64_t)sizeof(double) * 48 * n;
+    if (!defer) JOIN_UPLOAD(ctx);
+    int rc = compute_scene_bounds(ctx, *sp, defer, defer ? upload_seq_of(ctx, sp->positions) : 0,
+                                  defer ? ctx->upload_jobs.back().seq - 1 : 0);
+    if (rc) return rc;
+    bool sh_ready = !defer;
+    int nsets = defer ? ctx->lookahead : 1;
+    if (nsets < 1) nsets = 1;
+    if (nsets > potr_ctx::kMaxSets) nsets = potr_ctx::kMaxSets;
+    std::vector<int> free_sets;
+    for (int j = nsets - 1; j >= 0; j--) free_sets.push_back(j);
+    std::deque<BatchMeta> queue;
+    int s = 0;
+    while (s < ncam || !queue.empty()) {
+        if (s < ncam && !free_sets.empty() && (queue.empty() || !sh_ready)) {
+            if ((rc = check_cam(ctx, &cams[s]))) return rc;
+            const int nb = batch_len(ctx, cams, s, ncam, n);
+            for (int v = 0; v < nb; v++)
+                if (targets && !targets[s + v])
+                    return fail(ctx, POTR_E_ARG, "target pointer is NULL");
+            const int set = free_sets.back();
+            free_sets.pop_back();
+            activate_set(ctx, set);
+            if (nsets > 1 && (rc = level_active_set(ctx))) return rc;
+            int64_t K = 0;
+            rc = bin_batch(ctx, *sp, cams + s, nb, false, false, ctx->tile_cull, &K, 2, sh_ready);
+            if (rc) return rc;
+            queue.push_back({set, s, nb, ctx->batch_spatial, ctx->depth_split, !sh_ready,
+                             ctx->invalid_key0});
+            s += nb;
+            if (!sh_ready && queue.size() == 1 && !free_sets.empty()) {
+                // bound the sets by the memory the first one took: at most
+                // half of what is free now
+                size_t free_b = 0, total_b = 0;
+                CK(cudaMemGetInfo(&free_b, &total_b));
+                const size_t per = active_set_bytes(ctx);
+                const size_t more = per ? (free_b / 2) / per : free_sets.size();
+                while (free_sets.size() > more) free_sets.erase(free_sets.begin());
+            }
+            continue;
+        }
+        if (!sh_ready) {
+            JOIN_UPLOAD(ctx);
+            if ((rc = fill_slot_sh(ctx, *sp))) return rc;
+            sh_ready = true;
+        }
+        const BatchMeta m = queue.front();
+        queue.pop_front();
+        activate_set(ctx, m.set);
+        ctx->batch_spatial = m.spatial;
+        ctx->depth_split = m.split;
+        ctx->invalid_key0 = m.invalid_key0;
+        const int nb = m.nb;
+        if (m.colors_pending) {
+            Stage _st(ctx, POTR_STAGE_PREPROCESS);
+            CamBatch cb;
+            std::memset(&cb, 0, sizeof(cb));
+            for (int v = 0; v < nb; v++) cb.cam[v] = to_cam(cams[m.s + v]);
+            const double *pos = m.spatial ? P<double>(ctx->slot_pos) : sp->positions;
+            const double *sh = m.spatial ? P<double>(ctx->slot_sh) : sp->sh;
+            const double *op = m.spatial ? P<double>(ctx->slot_opac) : sp->opacities;
+            LAUNCH(1, launch_batch_colors(n, nb, pos, sh, op, cb, P<SplatRec>(ctx->rec),
+                                          ctx->stream));
+            _st.end();
+        }
+        ViewGeom g = geom(cams[m.s]);
+        RasterArgs a = raster_args(ctx, cams[m.s], nb);
+        for (int v = 0; v < nb; v++) a.target[v] = targets ? targets[m.s + v] : nullptr;
         if (images) {
             a.self_target = 1;
-            for (int v = 0; v < nb; v++) a.image[v] = images[s + v];
+            for (int v = 0; v < nb; v++) a.image[v] = images[m.s + v];
         }
         ENSURE(ctx->ci_v, sizeof(double2) * n * nb);
         {
@@ -644,18 +936,35 @@ int score_views_impl(potr_ctx *ctx, const potr_splats *sp, int ncam, const potr_
                                           P<double2>(ctx->partial), g.P, spatial_perm(ctx),
                                           P<double2>(ctx->ci_v), ctx->stream));
             LAUNCH(1, launch_view_accumulate(n, nb, P<double2>(ctx->ci_v),
-                                             cam_imp ? cam_imp + (int64_t)s * n : nullptr, imp_sum,
-                                             targets ? dmse_sum : nullptr,
-                                             dmse_rows ? dmse_rows + (int64_t)s * n : nullptr,
+                                             cam_imp ? cam_imp + (int64_t)m.s * n : nullptr,
+                                             imp_sum, targets ? dmse_sum : nullptr,
+                                             dmse_rows ? dmse_rows + (int64_t)m.s * n : nullptr,
                                              ctx->stream));
             if (targets)
                 LAUNCH(2, launch_mse_reduce(nb, g.ntiles, P<double>(ctx->tile_se), g.P, mse_sum,
-                                            mse_rows ? mse_rows + s : nullptr, ctx->stream));
+                                            mse_rows ? mse_rows + m.s : nullptr, ctx->stream));
             _st.end();
         }
-        s += nb;
+        free_sets.push_back(m.set);
     }
     return 0;
+}
+
+// score_views_run, which never returns with the upload it deferred to still
+// pending (an early error joins it here).
+int score_views_impl(potr_ctx *ctx, const potr_splats *sp, int ncam, const potr_camera *cams,
+                     const double *const *targets, double *imp_sum, double *cam_imp,
+                     double *dmse_sum, double *mse_sum, double *dmse_rows = nullptr,
+                     double *mse_rows = nullptr, double *const *images = nullptr) {
+    int rc = score_views_run(ctx, sp, ncam, cams, targets, imp_sum, cam_imp, dmse_sum, mse_sum,
+                             dmse_rows, mse_rows, images);
+    if (ctx->upload_pending) {
+        const std::string err = ctx->err;
+        const int jrc = upload_join(ctx);
+        if (rc) ctx->err = err;
+        else rc = jrc;
+    }
+    return rc;
 }
 
 }  // namespace
@@ -680,6 +989,10 @@ int potr_create(int device, potr_ctx **out) {
         ctx->view_batch = b < 1 ? 1 : (b > kMaxViewBatch ? kMaxViewBatch : b);
     }
     if (const char *sr = std::getenv("POTR_B200_SPATIAL")) ctx->spatial = std::atoi(sr) != 0;
+    if (const char *la = std::getenv("POTR_B200_LOOKAHEAD")) {
+        const int v = std::atoi(la);
+        ctx->lookahead = v < 1 ? 1 : (v > potr_ctx::kMaxSets ? potr_ctx::kMaxSets : v);
+    }
     if (cudaMallocHost(&ctx->pinned, 64 * sizeof(int64_t)) != cudaSuccess) {
         delete ctx;
         return POTR_E_NOMEM;
@@ -691,7 +1004,26 @@ int potr_create(int device, potr_ctx **out) {
 void potr_destroy(potr_ctx *ctx) {
     if (!ctx) return;
     cudaSetDevice(ctx->device);
+    upload_join(ctx);
+    if (ctx->upload_worker.joinable()) {
+        {
+            std::lock_guard<std::mutex> lk(ctx->upload_mu);
+            ctx->upload_quit = true;
+        }
+        ctx->upload_cv.notify_all();
+        ctx->upload_worker.join();
+    }
     cudaStreamSynchronize(ctx->stream);
+    if (ctx->copy_stream) {
+        cudaStreamSynchronize(ctx->copy_stream);
+        cudaStreamDestroy(ctx->copy_stream);
+        cudaEventDestroy(ctx->upload_after);
+    }
+    for (cudaEvent_t e : ctx->upload_ev_pool) cudaEventDestroy(e);
+    activate_set(ctx, 0);
+    for (auto &b : ctx->sets)
+        for (DevBuf *d : {&b.rec, &b.sids, &b.offs, &b.pair, &b.ranges})
+            if (d->p) cudaFree(d->p);
     DevBuf *bufs[] = {&ctx->rec,     &ctx->key,     &ctx->skey,    &ctx->sids,   &ctx->cnt,
                       &ctx->offs, &ctx->perm2,   &ctx->tkey,   &ctx->tskey,
                       &ctx->pair,    &ctx->dup_id,  &ctx->dup_rank, &ctx->partial, &ctx->ranges,
@@ -736,12 +1068,15 @@ void potr_destroy(potr_ctx *ctx) {
 
 int potr_set_stream(potr_ctx *ctx, void *stream) {
     if (!ctx) return POTR_E_ARG;
+    if (reinterpret_cast<cudaStream_t>(stream) == ctx->stream) return POTR_OK;
+    JOIN_UPLOAD(ctx);
     ctx->stream = reinterpret_cast<cudaStream_t>(stream);
     return POTR_OK;
 }
 
 int potr_synchronize(potr_ctx *ctx) {
     if (!ctx) return POTR_E_ARG;
+    JOIN_UPLOAD(ctx);
     CK(cudaStreamSynchronize(ctx->stream));
     return POTR_OK;
 }
@@ -806,6 +1141,7 @@ int potr_finalize_stats(potr_ctx *ctx, int64_t n, int total_cams, double *imp_su
                         double *dmse_sum, double *mse_sum) {
     if (!ctx || n < 0) return POTR_E_ARG;
     CK(cudaSetDevice(ctx->device));
+    JOIN_UPLOAD(ctx);
     LAUNCH(1, launch_finalize(n, total_cams, imp_sum, dmse_sum, mse_sum, ctx->stream));
     return POTR_OK;
 }
@@ -837,6 +1173,7 @@ int potr_render_batch(potr_ctx *ctx, const potr_splats *splats, int ncam, const 
                       double *const *images, double *const *trans) {
     if (!ctx) return POTR_E_ARG;
     CK(cudaSetDevice(ctx->device));
+    JOIN_UPLOAD(ctx);
     int rc = check_splats(ctx, splats);
     if (rc) return rc;
     if (ncam < 0 || (ncam > 0 && (!cams || !images)))
@@ -879,6 +1216,7 @@ int potr_render_records(potr_ctx *ctx, const potr_splats *splats, const potr_cam
                         double *trans_at, double *partials) {
     if (!ctx || !n_records) return POTR_E_ARG;
     CK(cudaSetDevice(ctx->device));
+    JOIN_UPLOAD(ctx);
     int rc = check_splats(ctx, splats);
     if (rc) return rc;
     if ((rc = check_cam(ctx, cam))) return rc;
@@ -939,6 +1277,7 @@ int potr_project(potr_ctx *ctx, const potr_splats *splats, const potr_camera *ca
                  double *cov2d, double *depth, double *radius, uint8_t *valid, double *colors) {
     if (!ctx) return POTR_E_ARG;
     CK(cudaSetDevice(ctx->device));
+    JOIN_UPLOAD(ctx);
     int rc = check_splats(ctx, splats);
     if (rc) return rc;
     if ((rc = check_cam(ctx, cam))) return rc;
@@ -954,6 +1293,7 @@ int potr_bin(potr_ctx *ctx, const potr_splats *splats, const potr_camera *cam, i
              int64_t *n_pairs) {
     if (!ctx || !n_valid || !n_pairs || !order) return POTR_E_ARG;
     CK(cudaSetDevice(ctx->device));
+    JOIN_UPLOAD(ctx);
     int rc = check_splats(ctx, splats);
     if (rc) return rc;
     if ((rc = check_cam(ctx, cam))) return rc;
@@ -984,6 +1324,7 @@ int potr_sh_accumulate(potr_ctx *ctx, const potr_splats *splats, int ncam,
                        double *normal_eqs) {
     if (!ctx) return POTR_E_ARG;
     CK(cudaSetDevice(ctx->device));
+    JOIN_UPLOAD(ctx);
     int rc = check_splats_ps(ctx, splats);
     if (rc) return rc;
     if (ncam < 0 || (ncam > 0 && (!cams || !camera_importance)) || !normal_eqs)
@@ -1011,6 +1352,7 @@ int potr_sh_solve(potr_ctx *ctx, const potr_splats *splats, const double *normal
                   double *ycocg, int8_t *status) {
     if (!ctx) return POTR_E_ARG;
     CK(cudaSetDevice(ctx->device));
+    JOIN_UPLOAD(ctx);
     int rc = check_splats_ps(ctx, splats);
     if (rc) return rc;
     if (!normal_eqs || !rgb || !ycocg || !status)
@@ -1033,6 +1375,7 @@ int potr_compact(potr_ctx *ctx, const potr_splats *splats, int ncam, const potr_
                  double zero_threshold, double *rgb, double *ycocg, int8_t *status) {
     if (!ctx) return POTR_E_ARG;
     CK(cudaSetDevice(ctx->device));
+    JOIN_UPLOAD(ctx);
     int rc = check_splats_ps(ctx, splats);
     if (rc) return rc;
     const int64_t n = splats->n;
@@ -1051,6 +1394,7 @@ int potr_sort_pairs_u64(potr_ctx *ctx, int64_t n, uint64_t *keys, int64_t *vals,
         return fail(ctx, POTR_E_ARG, "sort_pairs: bad arguments");
     if (n == 0 || end_bit <= begin_bit) return POTR_OK;
     CK(cudaSetDevice(ctx->device));
+    JOIN_UPLOAD(ctx);
     ENSURE(ctx->sort_k, sizeof(uint64_t) * n);
     ENSURE(ctx->sort_v, sizeof(int64_t) * n);
     ENSURE(ctx->temp, radix_sort_temp_bytes(n, begin_bit, end_bit));
@@ -1077,6 +1421,7 @@ int potr_removal_order(potr_ctx *ctx, int64_t n, const double *delta_mse, const 
         return fail(ctx, POTR_E_ARG, "removal_order: delta_mse_max and a must be > 0");
     if (n == 0) return POTR_OK;
     CK(cudaSetDevice(ctx->device));
+    JOIN_UPLOAD(ctx);
     ENSURE(ctx->rm_keys, sizeof(uint64_t) * n);
     LAUNCH(1, launch_removal_keys(n, delta_mse, idx, delta_mse_max, a, P<uint64_t>(ctx->rm_keys),
                                   ctx->stream));
@@ -1106,6 +1451,7 @@ int potr_image_compare(potr_ctx *ctx, int width, int height, const double *a, co
     if (!ctx || width <= 0 || height <= 0 || !a || !b)
         return fail(ctx, POTR_E_ARG, "image_compare: bad image arguments");
     CK(cudaSetDevice(ctx->device));
+    JOIN_UPLOAD(ctx);
     const size_t plane = (size_t)width * height;
     ENSURE(ctx->met_mom, 5 * plane * sizeof(double));
     ENSURE(ctx->met_part, (size_t)image_compare_partials() * sizeof(double));
@@ -1140,6 +1486,7 @@ int potr_octree(potr_ctx *ctx, int64_t n, const double *positions, int neyes, co
     if (max_depth < 0 || max_depth > 24) return fail(ctx, POTR_E_ARG, "max_depth must be in [0, 24]");
     if (neyes < 0 || (neyes > 0 && !eyes)) return fail(ctx, POTR_E_ARG, "bad camera eyes");
     CK(cudaSetDevice(ctx->device));
+    JOIN_UPLOAD(ctx);
     ENSURE(ctx->codec_eyes, sizeof(double) * 3 * (neyes > 0 ? neyes : 1));
     if (neyes > 0)
         CK(cudaMemcpyAsync(ctx->codec_eyes.p, eyes, sizeof(double) * 3 * neyes,
@@ -1162,6 +1509,7 @@ int potr_attribute_streams(potr_ctx *ctx, int64_t n, const int64_t *order, const
         !rotations)
         return fail(ctx, POTR_E_ARG, "attribute_streams: bad arrays");
     CK(cudaSetDevice(ctx->device));
+    JOIN_UPLOAD(ctx);
     LAUNCH(4, run_attr_streams(n, order, ycocg, opacities, log_scales, rotations, sf_sh,
                                sf_opacity, sf_rotation, sf_scale, out, capacity, stream_lengths,
                                &ctx->codec_scratch, &ctx->codec_cap, ctx->pinned, ctx->stream));
@@ -1189,6 +1537,11 @@ int potr_set_option(potr_ctx *ctx, int option, int value) {
         case POTR_OPT_SPATIAL_RECORDS:
             ctx->spatial = value != 0;
             return POTR_OK;
+        case POTR_OPT_LOOKAHEAD:
+            if (value < 1 || value > potr_ctx::kMaxSets)
+                return fail(ctx, POTR_E_ARG, "lookahead must be in [1, 8]");
+            ctx->lookahead = value;
+            return POTR_OK;
     }
     return fail(ctx, POTR_E_ARG, "unknown option");
 }
@@ -1206,6 +1559,7 @@ int potr_profile_enable(potr_ctx *ctx, int enable) {
 int potr_profile_read(potr_ctx *ctx, double *stage_ms, int64_t *stage_launches) {
     if (!ctx) return POTR_E_ARG;
     CK(cudaSetDevice(ctx->device));
+    JOIN_UPLOAD(ctx);
     CK(cudaStreamSynchronize(ctx->stream));
     for (auto &ev : ctx->events) {
         float ms = 0.f;
@@ -1226,6 +1580,7 @@ int potr_profile_read(potr_ctx *ctx, double *stage_ms, int64_t *stage_launches) 
 int potr_counters_enable(potr_ctx *ctx, int enable) {
     if (!ctx) return POTR_E_ARG;
     CK(cudaSetDevice(ctx->device));
+    JOIN_UPLOAD(ctx);
     ENSURE(ctx->counters, 4 * sizeof(unsigned long long));
     CK(cudaMemsetAsync(ctx->counters.p, 0, 4 * sizeof(unsigned long long), ctx->stream));
     ctx->counting = enable != 0;
@@ -1236,6 +1591,7 @@ int potr_counters_enable(potr_ctx *ctx, int enable) {
 int potr_counters_read(potr_ctx *ctx, uint64_t *out) {
     if (!ctx || !out) return POTR_E_ARG;
     CK(cudaSetDevice(ctx->device));
+    JOIN_UPLOAD(ctx);
     ENSURE(ctx->counters, 4 * sizeof(unsigned long long));
     CK(cudaMemcpyAsync(ctx->pinned, ctx->counters.p, 4 * sizeof(uint64_t), cudaMemcpyDeviceToHost,
                        ctx->stream));
@@ -1247,70 +1603,138 @@ int potr_counters_read(potr_ctx *ctx, uint64_t *out) {
 
 // ---- host-buffer convenience entry points --------------------------------
 
-// Pageable host -> device: chunks of kRingChunk bytes go through a ring of
-// pinned buffers; host threads (OpenMP) fill chunk c + 1 while the DMA engine
-// moves chunk c, so a pageable source uploads at close to the pinned PCIe
-// rate instead of the driver's single-threaded staging.
-static constexpr size_t kRingChunk = (size_t)32 << 20;
-
 int potr_copy_to_device(potr_ctx *ctx, void *dst, const void *src, int64_t bytes) {
     if (!ctx || bytes < 0 || (bytes > 0 && (!dst || !src)))
         return fail(ctx, POTR_E_ARG, "copy_to_device: bad arguments");
     if (bytes == 0) return POTR_OK;
     CK(cudaSetDevice(ctx->device));
-    for (int r = 0; r < potr_ctx::kRing; r++) {
-        if (!ctx->ring[r]) {
-            CK(cudaMallocHost(&ctx->ring[r], kRingChunk));
-            CK(cudaEventCreateWithFlags(&ctx->ring_ev[r], cudaEventDisableTiming));
-        }
+    JOIN_UPLOAD(ctx);
+    std::string err;
+    const int rc = ring_copy(ctx, dst, src, bytes, ctx->stream, ring_threads(0), &err);
+    return rc ? fail(ctx, rc, err) : POTR_OK;
+}
+
+int potr_upload_async(potr_ctx *ctx, void *dst, const void *src, int64_t bytes) {
+    if (!ctx || bytes < 0 || (bytes > 0 && (!dst || !src)))
+        return fail(ctx, POTR_E_ARG, "upload_async: bad arguments");
+    CK(cudaSetDevice(ctx->device));
+    if (bytes == 0) return POTR_OK;
+    if (!ctx->copy_stream) {
+        CK(cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking));
+        CK(cudaEventCreateWithFlags(&ctx->upload_after, cudaEventDisableTiming));
     }
-    int threads = omp_get_num_procs();
-    threads = threads < 1 ? 1 : threads > 16 ? 16 : threads;
-    const char *s = reinterpret_cast<const char *>(src);
-    char *d = reinterpret_cast<char *>(dst);
-    int64_t c = 0;
-    for (int64_t off = 0; off < bytes; off += (int64_t)kRingChunk, c++) {
-        const int b = (int)(c % potr_ctx::kRing);
-        const int64_t len = bytes - off < (int64_t)kRingChunk ? bytes - off : (int64_t)kRingChunk;
-        // the buffer's previous DMA (from this call or an earlier one) must be
-        // done before it is refilled; a never-recorded event returns at once
-        CK(cudaEventSynchronize(ctx->ring_ev[b]));
-        char *stage = reinterpret_cast<char *>(ctx->ring[b]);
-        const int t_used = len < ((int64_t)1 << 20) ? 1 : threads;
-#pragma omp parallel for num_threads(t_used) schedule(static)
-        for (int t = 0; t < t_used; t++) {
-            const int64_t a = len * t / t_used, e = len * (t + 1) / t_used;
-            std::memcpy(stage + a, s + off + a, (size_t)(e - a));
-        }
-        CK(cudaMemcpyAsync(d + off, stage, (size_t)len, cudaMemcpyHostToDevice, ctx->stream));
-        CK(cudaEventRecord(ctx->ring_ev[b], ctx->stream));
+    cudaEvent_t ev = nullptr;
+    if (!ctx->upload_ev_pool.empty()) {
+        ev = ctx->upload_ev_pool.back();
+        ctx->upload_ev_pool.pop_back();
+    } else {
+        CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
     }
+    // earlier work on the context stream may still read the destination
+    CK(cudaEventRecord(ctx->upload_after, ctx->stream));
+    CK(cudaStreamWaitEvent(ctx->copy_stream, ctx->upload_after, 0));
+    if (!ctx->upload_worker.joinable()) {
+        ctx->upload_worker = std::thread([ctx]() {
+            cudaSetDevice(ctx->device);
+            // one host core stays with the caller, which keeps launching kernels
+            const int threads = ring_threads(1);
+            std::unique_lock<std::mutex> lk(ctx->upload_mu);
+            for (;;) {
+                ctx->upload_cv.wait(lk,
+                                    [ctx] { return ctx->upload_quit || !ctx->upload_todo.empty(); });
+                if (ctx->upload_todo.empty()) return;  // quit
+                const potr_ctx::UploadJob job = ctx->upload_todo.front();
+                ctx->upload_todo.pop_front();
+                const bool skip = ctx->upload_rc != 0;
+                lk.unlock();
+                int rc = POTR_OK;
+                std::string err;
+                if (!skip) {
+                    cudaPointerAttributes at;
+                    cudaError_t e = cudaSuccess;
+                    if (cudaPointerGetAttributes(&at, job.src) == cudaSuccess &&
+                        at.type == cudaMemoryTypeHost) {  // pinned: the DMA engine alone
+                        e = cudaMemcpyAsync(job.dst, job.src, (size_t)job.bytes,
+                                            cudaMemcpyHostToDevice, ctx->copy_stream);
+                    } else {
+                        cudaGetLastError();  // pageable memory is not a CUDA pointer
+                        rc = ring_copy(ctx, job.dst, job.src, job.bytes, ctx->copy_stream,
+                                       threads, &err);
+                    }
+                    if (rc == POTR_OK && e == cudaSuccess)
+                        e = cudaEventRecord(job.ev, ctx->copy_stream);
+                    if (rc == POTR_OK && e != cudaSuccess) {
+                        rc = POTR_E_CUDA;
+                        err = cudaGetErrorString(e);
+                    }
+                }
+                lk.lock();
+                if (rc && !ctx->upload_rc) {
+                    ctx->upload_rc = rc;
+                    ctx->upload_err = err;
+                }
+                ctx->upload_done = job.seq;
+                ctx->upload_cv.notify_all();
+            }
+        });
+    }
+    const potr_ctx::UploadJob job{++ctx->upload_issued, dst, src, bytes, ev};
+    ctx->upload_jobs.push_back(job);
+    ctx->upload_pending = true;
+    {
+        std::lock_guard<std::mutex> lk(ctx->upload_mu);
+        ctx->upload_todo.push_back(job);
+    }
+    ctx->upload_cv.notify_all();
     return POTR_OK;
+}
+
+int potr_upload_wait(potr_ctx *ctx) {
+    if (!ctx) return POTR_E_ARG;
+    CK(cudaSetDevice(ctx->device));
+    return upload_join(ctx);
 }
 
 namespace {
 
+// Host -> device on the context stream: pinned sources by the DMA engine
+// directly, pageable ones through the pinned ring.
+int host_to_device(potr_ctx *ctx, void *dst, const void *src, int64_t bytes) {
+    if (bytes <= 0) return 0;
+    cudaPointerAttributes at;
+    if (cudaPointerGetAttributes(&at, src) == cudaSuccess && at.type == cudaMemoryTypeHost) {
+        CK(cudaMemcpyAsync(dst, src, (size_t)bytes, cudaMemcpyHostToDevice, ctx->stream));
+        return 0;
+    }
+    cudaGetLastError();
+    std::string err;
+    const int rc = ring_copy(ctx, dst, src, bytes, ctx->stream, ring_threads(0), &err);
+    return rc ? fail(ctx, rc, err) : 0;
+}
+
+// async_sh: the arrays go by potr_upload_async, the SH rows (81% of the
+// bytes) last, so that a scoring call bins its first batches while they
+// arrive.
 int upload_splats(potr_ctx *ctx, int64_t n, const double *pos, const double *sh,
-                  const double *op, const double *sc, const double *rot, potr_splats *out) {
+                  const double *op, const double *sc, const double *rot, potr_splats *out,
+                  bool async_sh = false) {
     ENSURE(ctx->h_pos, sizeof(double) * 3 * n);
     ENSURE(ctx->h_sh, sizeof(double) * 48 * n);
     ENSURE(ctx->h_op, sizeof(double) * n);
     ENSURE(ctx->h_sc, sizeof(double) * 3 * n);
     ENSURE(ctx->h_rot, sizeof(double) * 4 * n);
     if (n > 0) {
-        CK(cudaMemcpyAsync(ctx->h_pos.p, pos, sizeof(double) * 3 * n, cudaMemcpyHostToDevice,
-                           ctx->stream));
-        CK(cudaMemcpyAsync(ctx->h_sh.p, sh, sizeof(double) * 48 * n, cudaMemcpyHostToDevice,
-                           ctx->stream));
-        if (op)
-            CK(cudaMemcpyAsync(ctx->h_op.p, op, sizeof(double) * n, cudaMemcpyHostToDevice,
-                               ctx->stream));
-        if (sc)
-            CK(cudaMemcpyAsync(ctx->h_sc.p, sc, sizeof(double) * 3 * n, cudaMemcpyHostToDevice,
-                               ctx->stream));
-        if (rot)
-            CK(cudaMemcpyAsync(ctx->h_rot.p, rot, sizeof(double) * 4 * n, cudaMemcpyHostToDevice,
-                               ctx->stream));
+        // async: all five queued on the upload worker, the SH rows last
+        auto put = [ctx, async_sh](void *dst, const void *src, int64_t bytes) {
+            return async_sh ? potr_upload_async(ctx, dst, src, bytes)
+                            : host_to_device(ctx, dst, src, bytes);
+        };
+        int rc = 0;
+        if ((rc = put(ctx->h_pos.p, pos, (int64_t)sizeof(double) * 3 * n))) return rc;
+        if (op && (rc = put(ctx->h_op.p, op, (int64_t)sizeof(double) * n))) return rc;
+        if (sc && (rc = put(ctx->h_sc.p, sc, (int64_t)sizeof(double) * 3 * n))) return rc;
+        if (rot && (rc = put(ctx->h_rot.p, rot, (int64_t)sizeof(double) * 4 * n))) return rc;
+        if ((rc = put(ctx->h_sh.p, sh, (int64_t)sizeof(double) * 48 * n))) return rc;
     }
     out->n = n;
     out->positions = P<double>(ctx->h_pos);
@@ -1330,29 +1754,28 @@ int potr_forward_stats_host(potr_ctx *ctx, int64_t n, const double *positions, c
                             double *camera_importance, double *delta_mse, double *mse) {
     if (!ctx) return POTR_E_ARG;
     CK(cudaSetDevice(ctx->device));
+    JOIN_UPLOAD(ctx);
     if (n < 0 || ncam < 0 || (ncam > 0 && !cams) || !importance)
         return fail(ctx, POTR_E_ARG, "bad arguments");
     if (n > 0 && (!positions || !sh || !opacities || !scales || !rotations))
         return fail(ctx, POTR_E_ARG, "splat array pointer is NULL");
     if (targets && (!delta_mse || !mse))
         return fail(ctx, POTR_E_ARG, "targets given without delta_mse/mse outputs");
-    potr_splats sp;
-    int rc = upload_splats(ctx, n, positions, sh, opacities, scales, rotations, &sp);
-    if (rc) return rc;
     std::vector<const double *> dtg;
     if (targets) {
         size_t total = 0;
         for (int s = 0; s < ncam; s++) {
             if (check_cam(ctx, &cams[s])) return POTR_E_ARG;
+            if (!targets[s]) return fail(ctx, POTR_E_ARG, "target pointer is NULL");
             total += 3 * (size_t)cams[s].width * cams[s].height;
         }
         ENSURE(ctx->h_tg, sizeof(double) * total);
         size_t off = 0;
         for (int s = 0; s < ncam; s++) {
             size_t cnt = 3 * (size_t)cams[s].width * cams[s].height;
-            if (!targets[s]) return fail(ctx, POTR_E_ARG, "target pointer is NULL");
-            CK(cudaMemcpyAsync(P<double>(ctx->h_tg) + off, targets[s], sizeof(double) * cnt,
-                               cudaMemcpyHostToDevice, ctx->stream));
+            int trc = host_to_device(ctx, P<double>(ctx->h_tg) + off, targets[s],
+                                     (int64_t)(sizeof(double) * cnt));
+            if (trc) return trc;
             dtg.push_back(P<double>(ctx->h_tg) + off);
             off += cnt;
         }
@@ -1361,10 +1784,22 @@ int potr_forward_stats_host(potr_ctx *ctx, int64_t n, const double *positions, c
     ENSURE(ctx->h_dm, sizeof(double) * n);
     ENSURE(ctx->h_mse, sizeof(double));
     if (camera_importance) ENSURE(ctx->h_ci, sizeof(double) * (size_t)ncam * n);
-    rc = potr_forward_stats(ctx, &sp, ncam, cams, targets ? dtg.data() : nullptr,
-                            P<double>(ctx->h_imp), camera_importance ? P<double>(ctx->h_ci) : nullptr,
-                            targets ? P<double>(ctx->h_dm) : nullptr,
-                            targets ? P<double>(ctx->h_mse) : nullptr);
+    // the SH rows upload while the first batches bin (score_views_run); every
+    // exit below has joined that upload, so the caller may reuse `sh` at once
+    potr_splats sp;
+    int rc = upload_splats(ctx, n, positions, sh, opacities, scales, rotations, &sp, true);
+    if (rc == 0)
+        rc = potr_forward_stats(ctx, &sp, ncam, cams, targets ? dtg.data() : nullptr,
+                                P<double>(ctx->h_imp),
+                                camera_importance ? P<double>(ctx->h_ci) : nullptr,
+                                targets ? P<double>(ctx->h_dm) : nullptr,
+                                targets ? P<double>(ctx->h_mse) : nullptr);
+    if (ctx->upload_pending) {
+        const std::string err = ctx->err;
+        const int jrc = upload_join(ctx);
+        if (rc) ctx->err = err;
+        else rc = jrc;
+    }
     if (rc) return rc;
     CK(cudaMemcpyAsync(importance, ctx->h_imp.p, sizeof(double) * n, cudaMemcpyDeviceToHost,
                        ctx->stream));
@@ -1387,6 +1822,7 @@ int potr_compact_host(potr_ctx *ctx, int64_t n, const double *positions, const d
                       double *rgb, double *ycocg, int8_t *status) {
     if (!ctx) return POTR_E_ARG;
     CK(cudaSetDevice(ctx->device));
+    JOIN_UPLOAD(ctx);
     if (n < 0 || ncam < 0 || !rgb || !ycocg || !status) return fail(ctx, POTR_E_ARG, "bad arguments");
     if (n > 0 && (!positions || !sh || (ncam > 0 && !camera_importance)))
         return fail(ctx, POTR_E_ARG, "input pointer is NULL");

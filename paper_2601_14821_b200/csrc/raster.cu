@@ -36,6 +36,22 @@
 
 namespace potr {
 
+__device__ __forceinline__ void cp_async16(void *smem, const void *gmem) {
+    const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() {
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
+}
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+    asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
+}
+
+static inline unsigned grid_for(int64_t n, int block) {
+    return (unsigned)((n + block - 1) / block);
+}
+
 // ---------------------------------------------------------------------------
 // (a) preprocess
 
@@ -138,10 +154,12 @@ __global__ void k_splat_slots(int64_t n, potr_splats sp, const int32_t *__restri
     }
 #pragma unroll
     for (int i = 0; i < 4; i++) rot[i] = sp.rotations[4 * k + i];
-    const double2 *src = reinterpret_cast<const double2 *>(sp.sh + 48 * k);
-    double2 *dst = reinterpret_cast<double2 *>(sh + 48 * r);
+    if (sh) {  // null: the SH rows follow with k_slot_sh (still uploading)
+        const double2 *src = reinterpret_cast<const double2 *>(sp.sh + 48 * k);
+        double2 *dst = reinterpret_cast<double2 *>(sh + 48 * r);
 #pragma unroll 8
-    for (int i = 0; i < 24; i++) dst[i] = src[i];
+        for (int i = 0; i < 24; i++) dst[i] = src[i];
+    }
     const double o = sp.opacities[k];
     opac[r] = o;
     SplatPrep p;
@@ -158,6 +176,58 @@ cudaError_t launch_splat_slots(const potr_splats &sp, const int32_t *perm, doubl
     return cudaGetLastError();
 }
 
+// The SH rows in slot order: one 16-byte piece per thread (coalesced writes).
+__global__ void k_slot_sh(int64_t n, const double *__restrict__ sh_in,
+                          const int32_t *__restrict__ perm, double *__restrict__ sh) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n * 24) return;
+    const int64_t r = i / 24, q = i - r * 24;
+    const int64_t k = perm[r];
+    reinterpret_cast<double2 *>(sh)[i] = reinterpret_cast<const double2 *>(sh_in)[k * 24 + q];
+}
+
+cudaError_t launch_slot_sh(int64_t n, const double *sh_in, const int32_t *perm, double *sh,
+                           cudaStream_t st) {
+    if (n == 0) return cudaSuccess;
+    k_slot_sh<<<grid_for(n * 24, 256), 256, 0, st>>>(n, sh_in, perm, sh);
+    return cudaGetLastError();
+}
+
+// The colours of a batch's drawn records, after a preprocess without them
+// (colors = 0).  Same thread layout as the preprocess (the views of a splat in
+// adjacent threads: one SH row fetch serves them all) and the same products
+// as its splat_color; each drawn record's (opac, cr) (cg, cb) sector is
+// rewritten whole.
+__global__ void __launch_bounds__(128) k_batch_colors(int64_t n, int nview,
+                                                      const double *__restrict__ pos,
+                                                      const double *__restrict__ sh,
+                                                      const double *__restrict__ opac,
+                                                      CamBatch cams, SplatRec *__restrict__ rec) {
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= n * nview) return;
+    const int64_t k = t / nview;
+    const int v = (int)(t - k * nview);
+    const int64_t g = (int64_t)v * n + k;
+    SplatRec &r = rec[g];
+    const int2 xs = *reinterpret_cast<const int2 *>(&r.x0);
+    if (xs.x > xs.y) return;  // not drawn (the preprocess left x0 > x1)
+    double p[3], rgb[3];
+#pragma unroll
+    for (int j = 0; j < 3; j++) p[j] = __ldg(pos + 3 * k + j);
+    splat_color(p, sh + 48 * k, cams.cam[v], rgb);
+    double2 *f = reinterpret_cast<double2 *>(&r.opac);
+    f[0] = make_double2(__ldg(opac + k), rgb[0]);
+    f[1] = make_double2(rgb[1], rgb[2]);
+}
+
+cudaError_t launch_batch_colors(int64_t n, int nview, const double *pos, const double *sh,
+                                const double *opac, const CamBatch &cams, SplatRec *rec,
+                                cudaStream_t st) {
+    if (n == 0) return cudaSuccess;
+    k_batch_colors<<<grid_for(n * nview, 128), 128, 0, st>>>(n, nview, pos, sh, opac, cams, rec);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_splat_prep(const potr_splats &sp, SplatPrep *prep, cudaStream_t st) {
     if (sp.n == 0) return cudaSuccess;
     k_splat_prep<<<(unsigned)((sp.n + 127) / 128), 128, 0, st>>>(sp.n, sp.scales, sp.rotations,
@@ -169,16 +239,16 @@ cudaError_t launch_splat_prep(const potr_splats &sp, SplatPrep *prep, cudaStream
 #define POTR_PRE_MIN_BLOCKS 8  // 64 regs: 46.7 ms per C3 step (48.0 unbounded, 47.7 at 6, 54.2 at 4)
 #endif
 #define POTR_PRE_BOUNDS __launch_bounds__(128, POTR_PRE_MIN_BLOCKS)
+// colors: 0 leaves the records' colours to launch_batch_colors (the SH rows
+// are still being uploaded while the batch is binned)
 __global__ void POTR_PRE_BOUNDS k_preprocess(potr_splats sp, const SplatPrep *__restrict__ prep,
-                                                     CamBatch cams, int nview,
-                                                     int tiles_x, int all_colors, int cull,
-                                                     DepthKey dk,
-                                                     SplatRec *__restrict__ rec,
-                                                     TileSpan *__restrict__ spans,
-                                                     uint64_t *__restrict__ key,
-                                                     int32_t *__restrict__ cnt,
-                                                     int32_t *__restrict__ vidx,
-                                                     unsigned long long *counters) {
+                                             CamBatch cams, int nview, int tiles_x,
+                                             int all_colors, int colors, int cull, DepthKey dk,
+                                             SplatRec *__restrict__ rec,
+                                             TileSpan *__restrict__ spans,
+                                             uint64_t *__restrict__ key,
+                                             int32_t *__restrict__ cnt,
+                                             unsigned long long *counters) {
     const int64_t n = sp.n;
     const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= n * nview) return;
@@ -238,8 +308,8 @@ __global__ void POTR_PRE_BOUNDS k_preprocess(potr_splats sp, const SplatPrep *__
             r.ib = -pr.b / det;
             r.hc = -0.5 * (pr.a / det);
             r.opac = o;
-            double rgb[3];
-            splat_color(pos, sp.sh + 48 * k, cam, rgb);
+            double rgb[3] = {0.0, 0.0, 0.0};
+            if (colors) splat_color(pos, sp.sh + 48 * k, cam, rgb);
             r.cr = rgb[0];
             r.cg = rgb[1];
             r.cb = rgb[2];
@@ -284,7 +354,6 @@ __global__ void POTR_PRE_BOUNDS k_preprocess(potr_splats sp, const SplatPrep *__
     key[g] = kk;
     if (dk.shift) dk.khi[g] = (uint32_t)(kk >> dk.shift);
     cnt[g] = c;
-    vidx[g] = (int32_t)g;
 }
 
 // project_splats / splat_colors dump for parity tests (potr_project).
@@ -415,18 +484,6 @@ __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
     return v;
-}
-
-__device__ __forceinline__ void cp_async16(void *smem, const void *gmem) {
-    const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem) : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() {
-    asm volatile("cp.async.commit_group;\n" ::: "memory");
-}
-template <int N>
-__device__ __forceinline__ void cp_async_wait() {
-    asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
 }
 
 // The lane's slice of a chunk: pair index and splat id.
@@ -1117,21 +1174,18 @@ __global__ void k_count_valid(int64_t n, const uint64_t *__restrict__ skey, uint
 // ---------------------------------------------------------------------------
 // host-side launchers (called from capi.cu)
 
-static inline unsigned grid_for(int64_t n, int block) {
-    return (unsigned)((n + block - 1) / block);
-}
 
 size_t raster_smem_bytes() { return sizeof(WarpSmem) * kRasterWarps; }
 
 cudaError_t launch_preprocess(const potr_splats &sp, const SplatPrep *prep, const CamBatch &cams,
                               int nview,
-                              int tiles_x, int all_colors, int cull, const DepthKey &dk,
+                              int tiles_x, int all_colors, int colors, int cull, const DepthKey &dk,
                               SplatRec *rec, TileSpan *spans, uint64_t *key, int32_t *cnt,
-                              int32_t *vidx, unsigned long long *counters, cudaStream_t st) {
+                              unsigned long long *counters, cudaStream_t st) {
     if (sp.n == 0) return cudaSuccess;
     k_preprocess<<<grid_for(sp.n * nview, 128), 128, 0, st>>>(sp, prep, cams, nview, tiles_x,
-                                                               all_colors, cull, dk, rec, spans,
-                                                               key, cnt, vidx, counters);
+                                                               all_colors, colors, cull, dk, rec,
+                                                               spans, key, cnt, counters);
     return cudaGetLastError();
 }
 
@@ -1146,18 +1200,20 @@ cudaError_t launch_project_dump(const potr_splats &sp, const Cam &cam, double *m
 
 // Double-buffered (sort.cu): *in_alt is set when the sorted keys/values ended
 // in the second buffer of each pair.
+// The values are the record indices val_base + 0..n-1 (implicit in the
+// first pass).
 cudaError_t depth_sort(void *temp, size_t temp_bytes, uint64_t *key_a, uint64_t *key_b,
-                       int32_t *val_a, int32_t *val_b, int64_t n, int end_bit, bool *in_alt,
-                       cudaStream_t st) {
+                       int32_t *val_a, int32_t *val_b, int64_t n, int end_bit, int64_t val_base,
+                       bool *in_alt, cudaStream_t st) {
     return radix_sort_pairs<uint64_t, int32_t>(temp, temp_bytes, key_a, key_b, val_a, val_b, n,
-                                               0, end_bit, false, in_alt, st);
+                                               0, end_bit, true, in_alt, st, val_base);
 }
 
 cudaError_t depth_sort32(void *temp, size_t temp_bytes, uint32_t *key_a, uint32_t *key_b,
                          int32_t *val_a, int32_t *val_b, int64_t n, int end_bit, bool *in_alt,
                          cudaStream_t st) {
     return radix_sort_pairs<uint32_t, int32_t>(temp, temp_bytes, key_a, key_b, val_a, val_b, n,
-                                               0, end_bit, false, in_alt, st);
+                                               0, end_bit, true, in_alt, st);
 }
 
 cudaError_t depth_sort32_temp(int64_t n, size_t *bytes) {

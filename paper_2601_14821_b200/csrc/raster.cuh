@@ -53,10 +53,18 @@ cudaError_t launch_bbox(int64_t n, const double *pos, unsigned long long *out, c
 cudaError_t launch_splat_prep(const potr_splats &sp, SplatPrep *prep, cudaStream_t st);
 cudaError_t launch_splat_slots(const potr_splats &sp, const int32_t *perm, double *pos, double *sh,
                                double *opac, SplatPrep *prep, cudaStream_t st);
+// slot-ordered SH rows (k_splat_slots called with sh = null)
+cudaError_t launch_slot_sh(int64_t n, const double *sh_in, const int32_t *perm, double *sh,
+                           cudaStream_t st);
+// colours of the drawn records of a batch binned with colors = 0
+cudaError_t launch_batch_colors(int64_t n, int nview, const double *pos, const double *sh,
+                                const double *opac, const CamBatch &cams, SplatRec *rec,
+                                cudaStream_t st);
 cudaError_t launch_preprocess(const potr_splats &sp, const SplatPrep *prep, const CamBatch &cams,
-                              int nview, int tiles_x, int all_colors, int cull, const DepthKey &dk,
+                              int nview, int tiles_x, int all_colors, int colors, int cull,
+                              const DepthKey &dk,
                               SplatRec *rec, TileSpan *spans, uint64_t *key, int32_t *cnt,
-                              int32_t *vidx, unsigned long long *counters, cudaStream_t st);
+                              unsigned long long *counters, cudaStream_t st);
 // Spatial record layout.  Each call sorts the splats by the Morton code of
 // their centres (slot r holds splat perm[r]; rank = perm^-1) and copies them
 // in that order (k_splat_slots); the batch pipeline -- preprocess, depth keys,
@@ -90,8 +98,8 @@ cudaError_t launch_depth_fixup(int64_t total, const uint32_t *khi_sorted, int32_
 cudaError_t launch_gather_keys(int64_t total, const int32_t *sids, const uint64_t *key,
                                uint64_t *skey, cudaStream_t st);
 cudaError_t depth_sort(void *temp, size_t temp_bytes, uint64_t *key_a, uint64_t *key_b,
-                       int32_t *val_a, int32_t *val_b, int64_t n, int end_bit, bool *in_alt,
-                       cudaStream_t st);
+                       int32_t *val_a, int32_t *val_b, int64_t n, int end_bit, int64_t val_base,
+                       bool *in_alt, cudaStream_t st);
 cudaError_t scan_temp(int64_t n, size_t *bytes);
 cudaError_t scan_counts(void *temp, size_t temp_bytes, const int32_t *ids, const int32_t *cnt,
                         int64_t *offs, int64_t total, cudaStream_t st);

@@ -615,10 +615,10 @@ cudaError_t sort_impl(void *temp, size_t temp_bytes, K *keys, K *keys_alt, V *va
 template <typename K, typename V>
 cudaError_t radix_sort_pairs(void *temp, size_t temp_bytes, K *keys, K *keys_alt, V *vals,
                              V *vals_alt, int64_t n, int begin_bit, int end_bit, bool iota_vals,
-                             bool *in_alt, cudaStream_t st) {
+                             bool *in_alt, cudaStream_t st, int64_t iota_base) {
     if (iota_vals)
         return sort_impl<K, V, kValIota>(temp, temp_bytes, keys, keys_alt, vals, vals_alt,
-                                         nullptr, 0, n, begin_bit, end_bit, in_alt, st);
+                                         nullptr, iota_base, n, begin_bit, end_bit, in_alt, st);
     return sort_impl<K, V, kValRead>(temp, temp_bytes, keys, keys_alt, vals, vals_alt, nullptr,
                                      0, n, begin_bit, end_bit, in_alt, st);
 }
@@ -644,16 +644,16 @@ template cudaError_t radix_sort_packed<uint32_t>(void *, size_t, uint32_t *, uin
 
 template cudaError_t radix_sort_pairs<uint16_t, int32_t>(void *, size_t, uint16_t *, uint16_t *,
                                                          int32_t *, int32_t *, int64_t, int, int,
-                                                         bool, bool *, cudaStream_t);
+                                                         bool, bool *, cudaStream_t, int64_t);
 template cudaError_t radix_sort_pairs<uint32_t, int32_t>(void *, size_t, uint32_t *, uint32_t *,
                                                          int32_t *, int32_t *, int64_t, int, int,
-                                                         bool, bool *, cudaStream_t);
+                                                         bool, bool *, cudaStream_t, int64_t);
 template cudaError_t radix_sort_pairs<uint64_t, int32_t>(void *, size_t, uint64_t *, uint64_t *,
                                                          int32_t *, int32_t *, int64_t, int, int,
-                                                         bool, bool *, cudaStream_t);
+                                                         bool, bool *, cudaStream_t, int64_t);
 template cudaError_t radix_sort_pairs<uint64_t, int64_t>(void *, size_t, uint64_t *, uint64_t *,
                                                          int64_t *, int64_t *, int64_t, int, int,
-                                                         bool, bool *, cudaStream_t);
+                                                         bool, bool *, cudaStream_t, int64_t);
 
 size_t scan_temp_bytes(int64_t n) { return scan_layout(nullptr, n).bytes; }
 

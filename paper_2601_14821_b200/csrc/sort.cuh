@@ -26,12 +26,13 @@ size_t radix_sort_temp_bytes(int64_t n, int begin_bit, int end_bit);
 
 // Stable sort of (keys, vals) by keys' bits [begin_bit, end_bit), double-
 // buffered: the result ends in (keys, vals) or, when *in_alt is set, in
-// (keys_alt, vals_alt).  iota_vals: the input values are 0..n-1 (vals is not
-// read, only written).  K: uint16_t, uint32_t, uint64_t; V: int32_t, int64_t.
+// (keys_alt, vals_alt).  iota_vals: the input values are iota_base + 0..n-1
+// (vals is not read, only written).  K: uint16_t, uint32_t, uint64_t; V:
+// int32_t, int64_t.
 template <typename K, typename V>
 cudaError_t radix_sort_pairs(void *temp, size_t temp_bytes, K *keys, K *keys_alt, V *vals,
                              V *vals_alt, int64_t n, int begin_bit, int end_bit, bool iota_vals,
-                             bool *in_alt, cudaStream_t st);
+                             bool *in_alt, cudaStream_t st, int64_t iota_base = 0);
 
 // Stable sort of keys with packed int2 values: item i enters as
 // {vbase + i, hi[i]} (hi read once, in order, by the first pass), so the

@@ -130,17 +130,47 @@ class DeviceSplats:
         self._keep = [torch.empty(64, dtype=torch.float64, device=self.device)]
 
     @classmethod
-    def from_host(cls, splats, device=None):
+    def from_host(cls, splats, device=None, async_sh=False):
+        """Upload host splats.  async_sh: the five arrays are queued on the
+        library's upload worker (potr_upload_async), the SH rows (81% of the
+        bytes) last -- the next scoring call waits only for the geometry and
+        bins its first view batches while the rows arrive; every other library
+        call waits for all of them first.  The host arrays are kept referenced
+        until the copies are complete."""
         if isinstance(splats, DeviceSplats):
             return splats
         dev = current_device() if device is None else torch.device(device)
         n = int(np.asarray(splats.positions).shape[0]) if not isinstance(
             splats.positions, torch.Tensor) else int(splats.positions.shape[0])
-        return cls(to_device(splats.positions, dev, (n, 3)),
-                   to_device(splats.sh, dev, (n, 3, 16)),
-                   to_device(splats.opacities, dev, (n,)),
-                   to_device(splats.scales, dev, (n, 3)),
-                   to_device(splats.rotations, dev, (n, 4)))
+        fields = (("positions", (n, 3)), ("opacities", (n,)), ("scales", (n, 3)),
+                  ("rotations", (n, 4)), ("sh", (n, 3, 16)))
+        host = {f: getattr(splats, f) for f, _ in fields}
+        if async_sh and not any(isinstance(a, torch.Tensor) for a in host.values()):
+            arrs = {f: np.ascontiguousarray(host[f], dtype=np.float64).reshape(shape)
+                    for f, shape in fields}
+            if arrs["sh"].nbytes >= _STAGED_MIN:
+                ctx = context(dev)
+                out = {}
+                for f, shape in fields:
+                    a = arrs[f]
+                    out[f] = torch.empty(shape, dtype=torch.float64, device=dev)
+                    ctx.call("potr_upload_async", ptr(out[f]), ctypes.c_void_p(a.ctypes.data),
+                             ctypes.c_int64(a.nbytes))
+                ds = cls(out["positions"], out["sh"], out["opacities"], out["scales"],
+                         out["rotations"])
+                ds._pending_host = arrs
+                return ds
+        ds = cls(*(to_device(host[f], dev, shape) for f, shape in
+                   (("positions", (n, 3)), ("sh", (n, 3, 16)), ("opacities", (n,)),
+                    ("scales", (n, 3)), ("rotations", (n, 4)))))
+        ds._pending_host = None
+        return ds
+
+    def wait_upload(self):
+        """Complete a pending async SH upload (potr_upload_wait)."""
+        if getattr(self, "_pending_host", None) is not None:
+            context(self.device).call("potr_upload_wait")
+            self._pending_host = None
 
     def _p(self, t):
         return t.data_ptr() if t.numel() > 0 else self._keep[0].data_ptr()

@@ -235,14 +235,18 @@ def forward_stats(splats, cameras, targets=None, threads=1) -> ForwardStats:
     if distributed.sharding_active():
         return distributed.forward_stats_sharded(splats, cameras, targets)
     dev = D.current_device()
-    ds = D.DeviceSplats.from_host(splats, dev)
+    # the SH rows upload while the first view batches are binned
+    ds = D.DeviceSplats.from_host(splats, dev, async_sh=len(cameras) > 0)
     n, S = ds.n, len(cameras)
     if S == 0:
         if targets is not None:
             raise ZeroDivisionError("float division by zero")
         return ForwardStats(np.full(n, np.nan), np.zeros((0, n)), None, None)
-    dev_targets = D.targets_cache.get(targets, cameras, dev) if targets is not None else None
-    imp, cam_imp, dm, mse = forward_stats_device(ds, cameras, dev_targets)
+    try:
+        dev_targets = D.targets_cache.get(targets, cameras, dev) if targets is not None else None
+        imp, cam_imp, dm, mse = forward_stats_device(ds, cameras, dev_targets)
+    finally:
+        ds.wait_upload()
     cam_imp = D.LazyHostArray(cam_imp)
     if targets is None:
         return ForwardStats(D.to_host(imp), cam_imp, None, None)
