@@ -161,17 +161,18 @@ OPS_PER_M = 37
 
 def load_traffic(views_per_launch, config):
     """DRAM bytes (read + write) per k_raster<kScore> launch from the committed
-    `ncu --set full` capture summary (profiles/raster_traffic.json), for the
-    configuration it was captured on only; (None, None) otherwise."""
+    `ncu --set full` capture summaries (profiles/raster_traffic.json), for a
+    configuration that was captured only; (None, note) otherwise."""
     path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles",
                         "raster_traffic.json")
     try:
         with open(path) as f:
             t = json.load(f)
-        if t.get("config", "C3") != config:
-            return None, f"no capture for {config} (profiles/raster_traffic.json is {t.get('config', 'C3')})"
-        per_view = float(t["dram_bytes_per_launch"]) / float(t["views_per_launch"])
-        return per_view * views_per_launch, t.get("source")
+        c = t.get("configs", {}).get(config)
+        if c is None:
+            return None, f"no capture for {config} in profiles/raster_traffic.json"
+        per_view = float(c["dram_bytes_per_launch"]) / float(c["views_per_launch"])
+        return per_view * views_per_launch, c.get("source")
     except (OSError, ValueError, KeyError):
         return None, None
 
