@@ -251,34 +251,38 @@ __global__ void __launch_bounds__(32 * kShWarps, POTR_SH_MIN_BLOCKS)
 }
 
 // Upper Cholesky of the m x m principal block, packed with tri() (LAPACK
-// dpotrf 'U' semantics: a pivot <= 0 or NaN fails).
+// dpotrf 'U' semantics: a pivot <= 0 or NaN fails).  S: the stride between
+// packed entries (1 in local memory; the block size for a thread's slice of a
+// shared-memory array, [entry][thread], so a warp's accesses hit 32 banks).
+template <int S = 1>
 __device__ int chol_upper(double *A, int m) {
     for (int j = 0; j < m; j++) {
-        double ajj = A[tri(j, j)];
-        for (int k = 0; k < j; k++) ajj -= A[tri(k, j)] * A[tri(k, j)];
+        double ajj = A[tri(j, j) * S];
+        for (int k = 0; k < j; k++) ajj -= A[tri(k, j) * S] * A[tri(k, j) * S];
         if (!(ajj > 0.0)) return j + 1;
         ajj = sqrt(ajj);
-        A[tri(j, j)] = ajj;
+        A[tri(j, j) * S] = ajj;
         for (int c = j + 1; c < m; c++) {
-            double v = A[tri(j, c)];
-            for (int k = 0; k < j; k++) v -= A[tri(k, j)] * A[tri(k, c)];
-            A[tri(j, c)] = v / ajj;
+            double v = A[tri(j, c) * S];
+            for (int k = 0; k < j; k++) v -= A[tri(k, j) * S] * A[tri(k, c) * S];
+            A[tri(j, c) * S] = v / ajj;
         }
     }
     return 0;
 }
 
 // dpotrs: U^T y = b, U x = y
+template <int S = 1>
 __device__ void chol_solve(const double *U, int m, double *b) {
     for (int i = 0; i < m; i++) {
         double v = b[i];
-        for (int k = 0; k < i; k++) v -= U[tri(k, i)] * b[k];
-        b[i] = v / U[tri(i, i)];
+        for (int k = 0; k < i; k++) v -= U[tri(k, i) * S] * b[k];
+        b[i] = v / U[tri(i, i) * S];
     }
     for (int i = m - 1; i >= 0; i--) {
         double v = b[i];
-        for (int k = i + 1; k < m; k++) v -= U[tri(i, k)] * b[k];
-        b[i] = v / U[tri(i, i)];
+        for (int k = i + 1; k < m; k++) v -= U[tri(i, k) * S] * b[k];
+        b[i] = v / U[tri(i, i) * S];
     }
 }
 
@@ -288,6 +292,7 @@ __device__ void chol_solve(const double *U, int m, double *b) {
 // factor.  factor_channel returns 0 ok, 1 ok after the 1e-10 jitter, -1
 // RidgeError; the retry rebuilds A from G (the same values the reference's
 // retry starts from).
+template <int S = 1>
 __device__ int factor_channel(const double *__restrict__ G, int64_t gs, unsigned mask, double lam,
                               double *A, int *cols, int *mout) {
     int m = 0;
@@ -296,20 +301,21 @@ __device__ int factor_channel(const double *__restrict__ G, int64_t gs, unsigned
     *mout = m;
     for (int attempt = 0; attempt < 2; attempt++) {
         for (int i = 0; i < m; i++) {
-            for (int j = i; j < m; j++) A[tri(i, j)] = __ldg(G + tri(cols[i], cols[j]) * gs);
-            A[tri(i, i)] += (cols[i] == 0) ? 0.0 : lam;
-            if (attempt) A[tri(i, i)] += 1e-10;
+            for (int j = i; j < m; j++) A[tri(i, j) * S] = __ldg(G + tri(cols[i], cols[j]) * gs);
+            A[tri(i, i) * S] += (cols[i] == 0) ? 0.0 : lam;
+            if (attempt) A[tri(i, i) * S] += 1e-10;
         }
-        if (!chol_upper(A, m)) return attempt;
+        if (!chol_upper<S>(A, m)) return attempt;
     }
     return -1;
 }
 
+template <int S = 1>
 __device__ void solve_factored(const double *A, int m, const int *cols,
                                const double *__restrict__ B, int64_t gs, int ch, double *out) {
     double b[16];
     for (int i = 0; i < m; i++) b[i] = __ldg(B + (cols[i] * 3 + ch) * gs);
-    chol_solve(A, m, b);
+    chol_solve<S>(A, m, b);
     for (int i = 0; i < 16; i++) out[i] = 0.0;
     for (int i = 0; i < m; i++) out[cols[i]] = b[i];
 }
@@ -339,8 +345,8 @@ __device__ void coeffs_convert(const double *M, const double *in, double *out) {
 // at most that many columns.  Each size class is then solved by a kernel
 // whose factor lives in registers, fully unrolled for its capacity
 // (k_sh_solve_reg<8>: 74% of the C3 splats, <12>: 23%); the rare larger
-// systems and the unseen splats' DC fallback run the generic kernel with the
-// factor in local memory.  Results do not depend on the class order: every
+// systems run k_sh_solve_smem (each thread's factor in shared memory) and the
+// unseen splats' DC fallback the generic kernel.  Results do not depend on the class order: every
 // splat is solved independently, with the oracle's operation order
 // (potr_oracle.c chol_upper / chol_solve_upper / compact_one).
 
@@ -352,13 +358,17 @@ __device__ unsigned sparsify_mask(const double *__restrict__ G, int64_t gs, doub
     unsigned mask = 1u;
 #pragma unroll
     for (int i = 1; i < 16; i++) {
+        // column i's entries against the earlier columns, loaded together
+        // (independent loads; the kept-set test below picks what it needs)
+        double g[15];
+#pragma unroll
+        for (int j = 0; j < i; j++) g[j] = __ldg(G + tri(j, i) * gs);  // j < i
         if (norms[i] == 0.0) continue;
         bool par = false;
 #pragma unroll
         for (int j = 0; j < i; j++) {
             if (!(mask >> j & 1u)) continue;
-            const double gij = __ldg(G + tri(j, i) * gs);  // j < i
-            const double cs = fabs(gij) / (norms[i] * norms[j]);
+            const double cs = fabs(g[j]) / (norms[i] * norms[j]);
             if (cs > par_thr) par = true;
         }
         if (!par) mask |= 1u << i;
@@ -419,30 +429,39 @@ __device__ __forceinline__ constexpr int trm(int i, int j) {  // packed upper, r
     return i * MC - (i * (i - 1)) / 2 + (j - i);
 }
 
-// Upper Cholesky of the m x m leading block (m <= MC), unrolled; dpotrf 'U'
-// semantics.  Returns false when a pivot is <= 0 or NaN.
+// Register-resident factor / solve of the kept m x m system, capacity MC.
+// kPadMC: for MC > 8 the system is padded to MC with identity rows / columns
+// and the factorisation runs branch free over all MC columns (the factor is
+// blockdiag(chol(A_m), I): its leading block gets exactly the operations, in
+// the same order, of an m x m factorisation -- the padded terms add or
+// subtract exact zeros after the real ones).  No index then depends on m and
+// the 12-column factor stays in registers; with the m-guarded loops it went
+// to local memory.  For MC <= 8 the guarded loops already stay in registers
+// and do less work.
+template <int MC>
+constexpr bool kPadMC = MC > 8;
+
+// Upper Cholesky (dpotrf 'U' semantics), fully unrolled.  Returns false when a
+// real pivot is <= 0 or NaN (padded pivots are 1).
 template <int MC>
 __device__ __forceinline__ bool chol_reg(double (&U)[MC * (MC + 1) / 2], int m) {
     bool ok = true;
 #pragma unroll
     for (int j = 0; j < MC; j++) {
-        if (j < m && ok) {
+        if (kPadMC<MC> || j < m) {
             double ajj = U[trm<MC>(j, j)];
 #pragma unroll
             for (int k = 0; k < j; k++) ajj -= U[trm<MC>(k, j)] * U[trm<MC>(k, j)];
-            if (!(ajj > 0.0)) {
-                ok = false;
-            } else {
-                ajj = sqrt(ajj);
-                U[trm<MC>(j, j)] = ajj;
+            ok = ok && ajj > 0.0;
+            ajj = sqrt(ajj);
+            U[trm<MC>(j, j)] = ajj;
 #pragma unroll
-                for (int c = j + 1; c < MC; c++) {
-                    if (c < m) {
-                        double v = U[trm<MC>(j, c)];
+            for (int c = j + 1; c < MC; c++) {
+                if (kPadMC<MC> || c < m) {
+                    double v = U[trm<MC>(j, c)];
 #pragma unroll
-                        for (int k = 0; k < j; k++) v -= U[trm<MC>(k, j)] * U[trm<MC>(k, c)];
-                        U[trm<MC>(j, c)] = v / ajj;
-                    }
+                    for (int k = 0; k < j; k++) v -= U[trm<MC>(k, j)] * U[trm<MC>(k, c)];
+                    U[trm<MC>(j, c)] = v / ajj;
                 }
             }
         }
@@ -450,13 +469,14 @@ __device__ __forceinline__ bool chol_reg(double (&U)[MC * (MC + 1) / 2], int m) 
     return ok;
 }
 
-// dpotrs on the register factor: U^T y = b, U x = y
+// dpotrs on the register factor: U^T y = b, U x = y (padded entries of b are
+// zero and stay zero).
 template <int MC>
 __device__ __forceinline__ void chol_solve_reg(const double (&U)[MC * (MC + 1) / 2], int m,
                                                double (&b)[MC]) {
 #pragma unroll
     for (int i = 0; i < MC; i++) {
-        if (i < m) {
+        if (kPadMC<MC> || i < m) {
             double v = b[i];
 #pragma unroll
             for (int k = 0; k < i; k++) v -= U[trm<MC>(k, i)] * b[k];
@@ -465,11 +485,11 @@ __device__ __forceinline__ void chol_solve_reg(const double (&U)[MC * (MC + 1) /
     }
 #pragma unroll
     for (int i = MC - 1; i >= 0; i--) {
-        if (i < m) {
+        if (kPadMC<MC> || i < m) {
             double v = b[i];
 #pragma unroll
             for (int k = i + 1; k < MC; k++)
-                if (k < m) v -= U[trm<MC>(i, k)] * b[k];
+                if (kPadMC<MC> || k < m) v -= U[trm<MC>(i, k)] * b[k];
             b[i] = v / U[trm<MC>(i, i)];
         }
     }
@@ -511,26 +531,30 @@ __global__ void __launch_bounds__(128, MC <= 8 ? 4 : 2)
             cols[i] = mm ? __ffs(mm) - 1 : 0;
             mm &= mm - 1u;
         }
-        int rc = -1;
-#pragma unroll 1
-        for (int attempt = 0; attempt < 2; attempt++) {
+        // the m x m system (padded to MC with identity rows / columns when
+        // kPadMC); the 1e-10 jitter retry (compaction.py:138-145) is the rare
+        // second call
+        auto factor = [&](bool jitter) {
 #pragma unroll
             for (int i = 0; i < MC; i++)
 #pragma unroll
-                for (int j = i; j < MC; j++)
-                    if (j < m) U[trm<MC>(i, j)] = __ldg(G + tri(cols[i], cols[j]) * n);
+                for (int j = i; j < MC; j++) {
+                    if (j < m)
+                        U[trm<MC>(i, j)] = __ldg(G + tri(cols[i], cols[j]) * n);
+                    else if (kPadMC<MC>)
+                        U[trm<MC>(i, j)] = i == j ? 1.0 : 0.0;
+                }
 #pragma unroll
             for (int i = 0; i < MC; i++) {
                 if (i < m) {
                     U[trm<MC>(i, i)] += (cols[i] == 0) ? 0.0 : lam;
-                    if (attempt) U[trm<MC>(i, i)] += 1e-10;
+                    if (jitter) U[trm<MC>(i, i)] += 1e-10;
                 }
             }
-            if (chol_reg<MC>(U, m)) {
-                rc = attempt;
-                break;
-            }
-        }
+            return chol_reg<MC>(U, m);
+        };
+        int rc = 0;
+        if (!factor(false)) rc = factor(true) ? 1 : -1;
         if (rc < 0) {
             status = 2;
             break;
@@ -540,8 +564,7 @@ __global__ void __launch_bounds__(128, MC <= 8 ? 4 : 2)
         for (int r = 0; r < (task == 2 ? 2 : 1); r++) {
             const int ch = task < 2 ? 0 : task == 2 ? 1 + r : task - 2;
 #pragma unroll
-            for (int i = 0; i < MC; i++)
-                if (i < m) b[i] = __ldg(B + (cols[i] * 3 + ch) * n);
+            for (int i = 0; i < MC; i++) b[i] = i < m ? __ldg(B + (cols[i] * 3 + ch) * n) : 0.0;
             chol_solve_reg<MC>(U, m, b);
             if (task == 1 || task >= 3) {
                 for (int i = 0; i < 16; i++) yc[ch * 16 + i] = 0.0;
@@ -561,6 +584,40 @@ __global__ void __launch_bounds__(128, MC <= 8 ? 4 : 2)
     }
     finish_splat(status, sp.sh + 48 * k, rgb_out + 48 * k, yc);
     status_out[k] = (int8_t)status;
+}
+
+// The three channels of a seen splat (compact_splat, compaction.py:169-192)
+// with the packed factor at A (stride S); writes yc, returns the status.
+template <int S>
+__device__ int solve_seen(const double *__restrict__ neq, int64_t n, int64_t k, unsigned mask,
+                          double lambda_y, double zero_thr, double *A, double *yc) {
+    const double *G = neq + k, *B = neq + (int64_t)136 * n + k;
+    double first[16], first2[16];
+    int cols[16], m, rc;
+    int status = 0;
+    for (int ch = 0; ch < 3 && status != 2; ch++) {
+        if (ch < 2) {
+            rc = factor_channel<S>(G, n, mask, ch == 0 ? lambda_y : 3.0 * lambda_y, A, cols, &m);
+            if (rc < 0) {
+                status = 2;
+                break;
+            }
+            if (rc > 0) status = 1;
+            solve_factored<S>(A, m, cols, B, n, ch, first);
+            if (ch == 1) solve_factored<S>(A, m, cols, B, n, 2, first2);
+        } else {
+            for (int i = 0; i < 16; i++) first[i] = first2[i];
+        }
+        rc = factor_channel<S>(G, n, pass2_mask(mask, first, zero_thr),
+                               ch == 0 ? lambda_y : 3.0 * lambda_y, A, cols, &m);
+        if (rc < 0) {
+            status = 2;
+            break;
+        }
+        if (rc > 0) status = 1;
+        solve_factored<S>(A, m, cols, B, n, ch, yc + ch * 16);
+    }
+    return status;
 }
 
 // --- the generic solve (any size; unseen splats' DC fallback) ----------------
@@ -600,35 +657,34 @@ __global__ void __launch_bounds__(128) k_sh_solve(potr_splats sp, const double *
         coeffs_convert(kRgbToYcocg, rgb, yc);
         status = 3;
     } else {
-        const double *G = neq + k, *B = neq + (int64_t)136 * n + k;
-        const unsigned mask = masks[k];
-        double Af[136], first[16], first2[16];
-        int cols[16], m, rc;
-        for (int ch = 0; ch < 3 && status != 2; ch++) {
-            if (ch < 2) {
-                rc = factor_channel(G, n, mask, ch == 0 ? lambda_y : 3.0 * lambda_y, Af, cols, &m);
-                if (rc < 0) {
-                    status = 2;
-                    break;
-                }
-                if (rc > 0) status = 1;
-                solve_factored(Af, m, cols, B, n, ch, first);
-                if (ch == 1) solve_factored(Af, m, cols, B, n, 2, first2);
-            } else {
-                for (int i = 0; i < 16; i++) first[i] = first2[i];
-            }
-            rc = factor_channel(G, n, pass2_mask(mask, first, zero_thr),
-                                ch == 0 ? lambda_y : 3.0 * lambda_y, Af, cols, &m);
-            if (rc < 0) {
-                status = 2;
-                break;
-            }
-            if (rc > 0) status = 1;
-            solve_factored(Af, m, cols, B, n, ch, yc + ch * 16);
-        }
+        double Af[136];
+        status = solve_seen<1>(neq, n, k, masks[k], lambda_y, zero_thr, Af, yc);
         finish_splat(status, sh, rgb, yc);
     }
     status_out[k] = (int8_t)status;
+}
+
+// The large kept sets (> 12 columns, ~3% of the C3 splats): the generic solve
+// with each thread's packed factor in shared memory ([entry][thread]) instead
+// of local memory, persistent over the class list.
+constexpr int kShSmemThreads = 64;
+__global__ void __launch_bounds__(kShSmemThreads) k_sh_solve_smem(
+    potr_splats sp, const double *__restrict__ neq, const uint16_t *__restrict__ masks,
+    const int32_t *__restrict__ list, const int *__restrict__ count, double lambda_y,
+    double zero_thr, double *rgb_out, double *ycocg_out, int8_t *__restrict__ status_out) {
+    extern __shared__ double af_s[];  // [136][kShSmemThreads]
+    const int64_t n = sp.n;
+    const int cnt = *count;
+    for (int t = blockIdx.x * kShSmemThreads + threadIdx.x; t < cnt;
+         t += gridDim.x * kShSmemThreads) {
+        const int64_t k = list[t];
+        POTR_CHECK(k >= 0 && k < n);
+        double *yc = ycocg_out + 48 * k;
+        const int status = solve_seen<kShSmemThreads>(neq, n, k, masks[k], lambda_y, zero_thr,
+                                                      af_s + threadIdx.x, yc);
+        finish_splat(status, sp.sh + 48 * k, rgb_out + 48 * k, yc);
+        status_out[k] = (int8_t)status;
+    }
 }
 
 cudaError_t launch_sh_accumulate(const potr_splats &sp, int ncam, const double *eyes_dev,
@@ -671,8 +727,23 @@ cudaError_t launch_sh_solve(const potr_splats &sp, const double *neq, double lam
                                          zero_thr, rgb, ycocg, status);
     k_sh_solve_reg<12><<<g, 128, 0, st>>>(sp, neq, masks, lists + 2 * n, counts + 2, lambda_y,
                                           zero_thr, rgb, ycocg, status);
-    k_sh_solve<<<g, 128, 0, st>>>(sp, neq, masks, lists + 3 * n, counts + 3, lambda_y, zero_thr,
-                                  rgb, ycocg, status);
+    {
+        constexpr size_t smem = sizeof(double) * 136 * kShSmemThreads;
+        static int grid = 0;
+        if (!grid) {
+            cudaFuncSetAttribute(k_sh_solve_smem, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)smem);
+            int per_sm = 0, sms = 0, dev = 0;
+            cudaGetDevice(&dev);
+            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_sh_solve_smem,
+                                                          kShSmemThreads, smem);
+            grid = sms * (per_sm > 0 ? per_sm : 1);
+        }
+        k_sh_solve_smem<<<grid, kShSmemThreads, smem, st>>>(sp, neq, masks, lists + 3 * n,
+                                                            counts + 3, lambda_y, zero_thr, rgb,
+                                                            ycocg, status);
+    }
     k_sh_solve<<<g, 128, 0, st>>>(sp, neq, masks, lists, counts, lambda_y, zero_thr, rgb, ycocg,
                                   status);
     return cudaGetLastError();
