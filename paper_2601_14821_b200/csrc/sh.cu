@@ -28,72 +28,71 @@ __device__ __forceinline__ int tri(int i, int j) { return i * 16 - (i * (i - 1))
 __constant__ double kRgbToYcocg[9] = {0.25, 0.5, 0.25, 0.5, 0.0, -0.5, -0.25, 0.5, -0.25};
 __constant__ double kYcocgToRgb[9] = {1.0, 1.0, -1.0, 1.0, 0.0, 1.0, 1.0, -1.0, -1.0};
 
-// Normal equations of 16 consecutive splats per CTA (4 warps x 4 splats,
-// processed as two pairs).  Views are taken 32 at a time: the (view, splat)
-// tile of camera_importance is staged in shared memory with coalesced loads;
-// then for a pair of splats each lane evaluates one view for both
+// Normal equations of kShSplatsPerBlock consecutive splats per CTA (each warp
+// takes its splats one at a time).  Views are taken 32 at a time: the (view,
+// splat) tile of camera_importance is staged in shared memory with coalesced
+// loads; then for one splat each lane evaluates one view
 // (direction, SH basis, raw colour, YCoCg -- compaction.py:100-107) and
-// publishes the rows a = (w*y (16), w*YCoCg(colour) (3), 0) to shared memory.
-// The 184 wanted entries of a a^T -- G_ij, i <= j < 16, and B_ic = a_i a_16+c
-// -- are tiled by 4x4 register blocks (rows 4rb..4rb+3, columns
-// 4cb..4cb+3, cb >= rb): 14 blocks per splat, lanes 0-13 for the pair's
-// first splat and 16-29 for its second, each adding per seen view, in
-// ascending view order, 16 fused products from eight 8-byte shared loads
-// (the 2x4 blocks before this needed three 16-byte loads per 8 products and
-// ran shared-memory bound).  Views a splat is not seen from (w = 0) are skipped:
-// they would add exact zeros, so the sums equal the reference's sums over its
-// `seen` rows (compaction.py:97-107, :114, :133-137).
+// publishes the rows a = (w*y (16), 0, 0, w*YCoCg(colour) (3), 0...) to shared
+// memory.  The wanted entries of sum_v a a^T -- G_ij (i <= j < 16) and B_ic =
+// sum a_i a_18+c -- come from the fp64 tensor cores: per splat and per four
+// of its seen views (ascending), five mma.m8n8k4 (G rows 0-7 x cols 0-7, 0-7
+// x 8-15, 8-15 x 8-15; B rows 0-7 and 8-15 x row entries 16-23), whose A and
+// B fragments are the same three shared loads per lane.  The fp64 MMA rounds
+// exactly as a chain of fused multiply-adds in k order (tools/dmma_check.cu:
+// 4.2M of 4.2M entries equal), so every entry is the same fma chain over the
+// splat's seen views, in ascending view order, as the oracle's -- bit for bit.
+// A step short of four views pads with the zero row: fma(0, 0, acc) == acc
+// exactly (acc is never -0).  Views a splat is not seen from (w = 0) are
+// skipped: they would add exact zeros, so the sums equal the reference's
+// sums over its `seen` rows (compaction.py:97-107, :114, :133-137).
+// 4 splats per 4-warp CTA, 6 CTAs per SM (<= 85 registers, no spills):
+// 25.8 ms at C4 (16 per CTA at 3 per SM: 32.9; 8 at 4: 28.8; a spill of even
+// 20 bytes at 7 per SM: 36.1)
 #ifndef POTR_SH_MIN_BLOCKS
-#define POTR_SH_MIN_BLOCKS 3
+#define POTR_SH_MIN_BLOCKS 6
 #endif
-constexpr int kShSplatsPerBlock = 16;
-constexpr int kShWarps = 4;
-// Row layout: w*y at 0..15, w*YCoCg at 18..20, zeros at 16, 17, 21, 22.  The
+#ifndef POTR_SH_SPLATS
+#define POTR_SH_SPLATS 4
+#endif
+constexpr int kShSplatsPerBlock = POTR_SH_SPLATS;
+#ifndef POTR_SH_WARPS
+#define POTR_SH_WARPS 4
+#endif
+constexpr int kShWarps = POTR_SH_WARPS;
+// Row layout: w*y at 0..15, w*YCoCg at 18..20, zeros at 16, 17, 21..24.  The
 // odd stride keeps the 16 rows a half-warp stores per instruction on distinct
-// banks (an even stride made the row stores 4-way conflicted), and with the
-// YCoCg block at 18 and the second splat's rows 759 doubles further, the
-// sixteen 8-byte loads of one accumulation step fall on distinct banks.
-constexpr int kShRow = 23;
+// banks; 25 >= 24 so the B fragments' entries 16..23 stay inside the row.
+constexpr int kShRow = 25;
 constexpr int kShYc = 18;
-constexpr int kShBlocks = 14;
-#ifndef POTR_SH_UNROLL
-#define POTR_SH_UNROLL 4
-#endif
-constexpr int kShUnroll = POTR_SH_UNROLL;
-
-// Block b (0..13) of the tiling: row block rb, column block cb >= rb.
-__device__ __forceinline__ void sh_block(int b, int *rb, int *cb) {
-    int cum = 0;
-    for (int r = 0; r < 4; r++) {
-        const int nb = 5 - r;
-        if (b < cum + nb) {
-            *rb = r;
-            *cb = r + (b - cum);
-            return;
-        }
-        cum += nb;
-    }
-    *rb = 0;
-    *cb = 0;
-}
 
 // Entry index of (i, j), j >= i, in the (185, N) layout: G upper triangle
-// then B (136 + 3 i + c); -1 outside the wanted region.
+// then B (136 + 3 i + c, row entry j = 18 + c); -1 outside the wanted region.
 __device__ __forceinline__ int sh_entry(int i, int j) {
-    if (j < i || j > 18) return -1;
+    if (j < i) return -1;
     if (j < 16) return i * 16 - (i * (i - 1)) / 2 + (j - i);
-    return 136 + 3 * i + (j - 16);
+    if (j >= kShYc && j < kShYc + 3) return 136 + 3 * i + (j - kShYc);
+    return -1;
+}
+
+// D += A B on the fp64 tensor cores, one m8n8k4 tile: A fragment a (row
+// lane/4, col lane%4), B fragment b (row lane%4, col lane/4), C/D (row lane/4,
+// cols 2 (lane%4) + {0, 1}).
+__device__ __forceinline__ void dmma_acc(double (&d)[2], double a, double b) {
+    asm volatile(
+        "mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+        : "+d"(d[0]), "+d"(d[1])
+        : "d"(a), "d"(b));
 }
 
 __global__ void __launch_bounds__(32 * kShWarps, POTR_SH_MIN_BLOCKS)
     k_sh_accumulate(potr_splats sp, int ncam, const double *__restrict__ eyes,
                     const double *__restrict__ cam_imp, double *__restrict__ neq) {
     __shared__ double wtile[32][kShSplatsPerBlock + 1];
-    // per warp, per splat of the pair: 32 view rows + a zero row (the
-    // unrolled accumulation pads with it: fma(0, 0, acc) == acc exactly, acc
-    // is never -0)
+    // per warp: 32 view rows + a zero row (a step short of four views pads
+    // with it: fma(0, 0, acc) == acc exactly, acc is never -0)
     extern __shared__ __align__(16) double sh_dyn[];
-    double(*A)[2][33][kShRow] = reinterpret_cast<double(*)[2][33][kShRow]>(sh_dyn);
+    double(*A)[33][kShRow] = reinterpret_cast<double(*)[33][kShRow]>(sh_dyn);
     __shared__ double shs[kShSplatsPerBlock][48];
     __shared__ double pos[kShSplatsPerBlock][3];
     const int64_t n = sp.n;
@@ -104,26 +103,24 @@ __global__ void __launch_bounds__(32 * kShWarps, POTR_SH_MIN_BLOCKS)
         shs[i / 48][i % 48] = sp.sh[(k0 + i / 48) * 48 + i % 48];
     for (int i = threadIdx.x; i < nk * 3; i += blockDim.x)
         pos[i / 3][i % 3] = sp.positions[(k0 + i / 3) * 3 + i % 3];
-    for (int i = threadIdx.x; i < kShWarps * 2 * 33 * kShRow; i += blockDim.x)
-        (&A[0][0][0][0])[i] = 0.0;  // the pad column and the zero rows stay zero
+    for (int i = threadIdx.x; i < kShWarps * 33 * kShRow; i += blockDim.x)
+        (&A[0][0][0])[i] = 0.0;  // the pad columns and the zero row stay zero
 
-    const int half = lane >> 4, hl = lane & 15;
-    const bool owner = hl < kShBlocks;
-    int rb = 0, cb = 0;
-    sh_block(owner ? hl : 0, &rb, &cb);
-    constexpr int kPairs = kShSplatsPerBlock / kShWarps / 2;  // pairs per warp
-    double acc[kPairs][16];
-    int seen[kPairs];
+    constexpr int kPerWarp = kShSplatsPerBlock / kShWarps;  // splats of this warp
+    // per splat: five 8x8 fp64 MMA accumulators (G00, G01, G11, B0, B1), two
+    // doubles per lane each
+    double acc[kPerWarp][5][2];
+    int seen[kPerWarp];
 #pragma unroll
-    for (int p = 0; p < kPairs; p++) {
-        seen[p] = 0;
+    for (int q = 0; q < kPerWarp; q++) {
+        seen[q] = 0;
 #pragma unroll
-        for (int q = 0; q < 16; q++) acc[p][q] = 0.0;
+        for (int t = 0; t < 5; t++) acc[q][t][0] = acc[q][t][1] = 0.0;
     }
 
     // the next view block's camera_importance tile is loaded into registers
     // while the current one is processed (its global-load latency was the
-    // largest stall); each thread holds kPre of the 32 x 16 values
+    // largest stall); each thread holds kPre of the 32 x kShSplatsPerBlock values
     constexpr int kPre = 32 * kShSplatsPerBlock / (32 * kShWarps);
     double pre[kPre];
     const auto load_tile = [&](int s0) {
@@ -136,6 +133,7 @@ __global__ void __launch_bounds__(32 * kShWarps, POTR_SH_MIN_BLOCKS)
         }
     };
     load_tile(0);
+    const double(*rows)[kShRow] = A[w];
     for (int s0 = 0; s0 < ncam; s0 += 32) {
         const int nv = ncam - s0 < 32 ? ncam - s0 : 32;
         __syncthreads();  // previous round done with wtile; first round: sh/pos staged
@@ -151,102 +149,90 @@ __global__ void __launch_bounds__(32 * kShWarps, POTR_SH_MIN_BLOCKS)
         const double ey = lv ? eyes[3 * (s0 + lane) + 1] : 0.0;
         const double ez = lv ? eyes[3 * (s0 + lane) + 2] : 0.0;
 #pragma unroll
-        for (int p = 0; p < kPairs; p++) {
-            const int kbase = w * 2 * kPairs + 2 * p;
-            if (kbase >= nk) break;  // warp-uniform
-            unsigned smask[2];
+        for (int q = 0; q < kPerWarp; q++) {
+            const int kk = w * kPerWarp + q;
+            if (kk >= nk) break;  // warp-uniform
+            const double wv = wtile[lane][kk];
+            const unsigned smask = __ballot_sync(0xffffffffu, lv && wv > 0.0);
+            if (wv > 0.0) {
+                double *row = A[w][lane];
+                const double d0 = pos[kk][0] - ex, d1 = pos[kk][1] - ey, d2 = pos[kk][2] - ez;
+                const double nrm = sqrt(d0 * d0 + d1 * d1 + d2 * d2);
+                double y[16];
+                sh_basis16(d0 / nrm, d1 / nrm, d2 / nrm, y);
+                // colors = basis @ sh^T (compaction.py:104): fused
+                // multiply-adds in two interleaved partial sums (the
+                // oracle's order; a 16-deep add chain was the largest stall)
+                double col[3];
 #pragma unroll
-            for (int q = 0; q < 2; q++) {
-                const int kk = kbase + q;
-                const double wv = kk < nk ? wtile[lane][kk] : 0.0;
-                smask[q] = __ballot_sync(0xffffffffu, lv && wv > 0.0);
-                if (wv > 0.0) {
-                    double *row = A[w][q][lane];
-                    const double d0 = pos[kk][0] - ex, d1 = pos[kk][1] - ey, d2 = pos[kk][2] - ez;
-                    const double nrm = sqrt(d0 * d0 + d1 * d1 + d2 * d2);
-                    double y[16];
-                    sh_basis16(d0 / nrm, d1 / nrm, d2 / nrm, y);
-                    // colors = basis @ sh^T (compaction.py:104): fused
-                    // multiply-adds in two interleaved partial sums (the
-                    // oracle's order; a 16-deep add chain was the largest stall)
-                    double col[3];
+                for (int c = 0; c < 3; c++) {
+                    double a0 = 0.0, a1 = 0.0;
 #pragma unroll
-                    for (int c = 0; c < 3; c++) {
-                        double a0 = 0.0, a1 = 0.0;
-#pragma unroll
-                        for (int i = 0; i < 16; i += 2) {
-                            a0 = fma(y[i], shs[kk][c * 16 + i], a0);
-                            a1 = fma(y[i + 1], shs[kk][c * 16 + i + 1], a1);
-                        }
-                        col[c] = a0 + a1;
+                    for (int i = 0; i < 16; i += 2) {
+                        a0 = fma(y[i], shs[kk][c * 16 + i], a0);
+                        a1 = fma(y[i + 1], shs[kk][c * 16 + i + 1], a1);
                     }
+                    col[c] = a0 + a1;
+                }
 #pragma unroll
-                    for (int i = 0; i < 16; i++) row[i] = y[i] * wv;
+                for (int i = 0; i < 16; i++) row[i] = y[i] * wv;
 #pragma unroll
-                    for (int c = 0; c < 3; c++) {
-                        const double yc = col[0] * kRgbToYcocg[c * 3] +
-                                          col[1] * kRgbToYcocg[c * 3 + 1] +
-                                          col[2] * kRgbToYcocg[c * 3 + 2];
-                        row[kShYc + c] = yc * wv;
-                    }
+                for (int c = 0; c < 3; c++) {
+                    const double yc = col[0] * kRgbToYcocg[c * 3] +
+                                      col[1] * kRgbToYcocg[c * 3 + 1] +
+                                      col[2] * kRgbToYcocg[c * 3 + 2];
+                    row[kShYc + c] = yc * wv;
                 }
             }
-            seen[p] += half ? __popc(smask[1]) : __popc(smask[0]);  // lanes of half h: splat h
+            seen[q] += __popc(smask);
             __syncwarp();
-            // kShUnroll views per step from the union of the pair's seen
-            // views, ascending; a half reads the zero row for a view its splat
-            // does not see (and to pad the last step): fma(0, 0, acc) == acc
-            const double(*rows)[kShRow] = A[w][half];
-            const unsigned mine = smask[half];
-            unsigned m = smask[0] | smask[1];
-            const int cofs = cb < 4 ? 4 * cb : kShYc;
-            while (m) {
-                int vv[kShUnroll];
+            // the splat's seen views four at a time, ascending; lane l loads
+            // entries l/4, 8 + l/4, 16 + l/4 of the row of view l%4
+            unsigned m = smask;
+            while (m) {  // warp-uniform
+                int v = 32;
 #pragma unroll
-                for (int u = 0; u < kShUnroll; u++) {
-                    const int v = m ? __ffs(m) - 1 : 32;
+                for (int u = 0; u < 4; u++) {
+                    const int vu = m ? __ffs(m) - 1 : 32;
                     m &= m - 1u;
-                    vv[u] = (v < 32 && (mine >> v & 1u)) ? v : 32;
+                    if ((lane & 3) == u) v = vu;
                 }
-                double ar[kShUnroll][4], bc[kShUnroll][4];
-#pragma unroll
-                for (int u = 0; u < kShUnroll; u++)
-#pragma unroll
-                    for (int i = 0; i < 4; i++) {
-                        ar[u][i] = rows[vv[u]][4 * rb + i];
-                        bc[u][i] = rows[vv[u]][cofs + i];
-                    }
-#pragma unroll
-                for (int u = 0; u < kShUnroll; u++)
-#pragma unroll
-                    for (int r = 0; r < 4; r++)
-#pragma unroll
-                        for (int c = 0; c < 4; c++)
-                            acc[p][4 * r + c] = fma(ar[u][r], bc[u][c], acc[p][4 * r + c]);
+                const double *row = rows[v];
+                const int r = lane >> 2;
+                const double x0 = row[r], x1 = row[8 + r], x2 = row[16 + r];
+                dmma_acc(acc[q][0], x0, x0);
+                dmma_acc(acc[q][1], x0, x1);
+                dmma_acc(acc[q][2], x1, x1);
+                dmma_acc(acc[q][3], x0, x2);
+                dmma_acc(acc[q][4], x1, x2);
             }
             __syncwarp();
         }
     }
+    // tile t's block of rows / columns: G00 (0, 0), G01 (0, 8), G11 (8, 8),
+    // B0 (0, 16), B1 (8, 16); lane l holds row l/4, columns 2 (l%4) + {0, 1}
+    constexpr int kTileRow[5] = {0, 0, 8, 0, 8}, kTileCol[5] = {0, 8, 8, 16, 16};
 #pragma unroll
-    for (int p = 0; p < kPairs; p++) {
-        const int kk = w * 2 * kPairs + 2 * p + half;
-        if (kk >= nk) continue;
+    for (int q = 0; q < kPerWarp; q++) {
+        const int kk = w * kPerWarp + q;
+        if (kk >= nk) continue;  // warp-uniform
         const int64_t k = k0 + kk;
-        if (owner) {
-            // all 16 reads issue before the first write (one latency, not 16)
-            double old[16];
+        // all reads issue before the first write (one latency, not ten)
+        int e[5][2];
+        double old[5][2];
 #pragma unroll
-            for (int q = 0; q < 16; q++) {
-                const int e = sh_entry(4 * rb + (q >> 2), 4 * cb + (q & 3));  // cb 4: 16 + q
-                old[q] = e >= 0 ? neq[(int64_t)e * n + k] : 0.0;
+        for (int t = 0; t < 5; t++)
+#pragma unroll
+            for (int h = 0; h < 2; h++) {
+                e[t][h] = sh_entry(kTileRow[t] + (lane >> 2), kTileCol[t] + 2 * (lane & 3) + h);
+                old[t][h] = e[t][h] >= 0 ? neq[(int64_t)e[t][h] * n + k] : 0.0;
             }
 #pragma unroll
-            for (int q = 0; q < 16; q++) {
-                const int e = sh_entry(4 * rb + (q >> 2), 4 * cb + (q & 3));
-                if (e >= 0) neq[(int64_t)e * n + k] = old[q] + acc[p][q];
-            }
-        }
-        if (hl == 0) neq[(int64_t)184 * n + k] += (double)seen[p];
+        for (int t = 0; t < 5; t++)
+#pragma unroll
+            for (int h = 0; h < 2; h++)
+                if (e[t][h] >= 0) neq[(int64_t)e[t][h] * n + k] = old[t][h] + acc[q][t][h];
+        if (lane == 0) neq[(int64_t)184 * n + k] += (double)seen[q];
     }
 }
 
@@ -691,7 +677,7 @@ cudaError_t launch_sh_accumulate(const potr_splats &sp, int ncam, const double *
                                  const double *cam_imp, double *neq, cudaStream_t st) {
     if (sp.n == 0) return cudaSuccess;
     const unsigned blocks = (unsigned)((sp.n + kShSplatsPerBlock - 1) / kShSplatsPerBlock);
-    constexpr size_t smem = sizeof(double) * kShWarps * 2 * 33 * kShRow;
+    constexpr size_t smem = sizeof(double) * kShWarps * 33 * kShRow;
     static bool attr = false;
     if (!attr) {
         cudaFuncSetAttribute(k_sh_accumulate, cudaFuncAttributeMaxDynamicSharedMemorySize,
