@@ -122,7 +122,9 @@ __global__ void __launch_bounds__(32 * kShWarps, POTR_SH_MIN_BLOCKS)
     // while the current one is processed (its global-load latency was the
     // largest stall); each thread holds kPre of the 32 x kShSplatsPerBlock values
     constexpr int kPre = 32 * kShSplatsPerBlock / (32 * kShWarps);
-    double pre[kPre];
+    static_assert(32 * kShWarps >= 96, "one eye coordinate per thread");
+    __shared__ double eye_s[32][3];
+    double pre[kPre], pre_eye;  // and the block's 32 camera centres, likewise
     const auto load_tile = [&](int s0) {
         const int nv = ncam - s0 < 32 ? ncam - s0 : 32;
 #pragma unroll
@@ -131,6 +133,7 @@ __global__ void __launch_bounds__(32 * kShWarps, POTR_SH_MIN_BLOCKS)
             const int v = i / kShSplatsPerBlock, kk = i % kShSplatsPerBlock;
             pre[q] = (v < nv && kk < nk) ? cam_imp[(int64_t)(s0 + v) * n + k0 + kk] : 0.0;
         }
+        pre_eye = threadIdx.x < 3 * nv ? eyes[3 * s0 + threadIdx.x] : 0.0;
     };
     load_tile(0);
     const double(*rows)[kShRow] = A[w];
@@ -142,12 +145,11 @@ __global__ void __launch_bounds__(32 * kShWarps, POTR_SH_MIN_BLOCKS)
             const int i = threadIdx.x + q * 32 * kShWarps;
             wtile[i / kShSplatsPerBlock][i % kShSplatsPerBlock] = pre[q];
         }
+        if (threadIdx.x < 96) (&eye_s[0][0])[threadIdx.x] = pre_eye;
         __syncthreads();
         if (s0 + 32 < ncam) load_tile(s0 + 32);
         const bool lv = lane < nv;
-        const double ex = lv ? eyes[3 * (s0 + lane)] : 0.0;
-        const double ey = lv ? eyes[3 * (s0 + lane) + 1] : 0.0;
-        const double ez = lv ? eyes[3 * (s0 + lane) + 2] : 0.0;
+        const double ex = eye_s[lane][0], ey = eye_s[lane][1], ez = eye_s[lane][2];
 #pragma unroll
         for (int q = 0; q < kPerWarp; q++) {
             const int kk = w * kPerWarp + q;
