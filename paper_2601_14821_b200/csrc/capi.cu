@@ -98,6 +98,7 @@ struct potr_ctx {
     };
     cudaStream_t copy_stream = nullptr;
     cudaEvent_t upload_after = nullptr;
+    cudaEvent_t poll_ev = nullptr;  // host_wait
     std::thread upload_worker;
     std::mutex upload_mu;
     std::condition_variable upload_cv;
@@ -307,6 +308,25 @@ int bitlen(uint64_t x) {
 
 // ---- uploads -------------------------------------------------------------
 
+// The binning's host readbacks wait for the context stream.  While an upload
+// is pending they poll an event instead of blocking in cudaStreamSynchronize:
+// the upload worker's own CUDA calls (its ring copies) stalled behind a
+// blocked synchronize, which serialised the upload with the binning.
+cudaError_t host_wait(potr_ctx *ctx) {
+    if (!ctx->upload_pending) return cudaStreamSynchronize(ctx->stream);
+    if (!ctx->poll_ev) {
+        cudaError_t e = cudaEventCreateWithFlags(&ctx->poll_ev, cudaEventDisableTiming);
+        if (e != cudaSuccess) return e;
+    }
+    cudaError_t e = cudaEventRecord(ctx->poll_ev, ctx->stream);
+    if (e != cudaSuccess) return e;
+    for (;;) {
+        e = cudaEventQuery(ctx->poll_ev);
+        if (e != cudaErrorNotReady) return e;
+        std::this_thread::yield();
+    }
+}
+
 // Pageable host -> device: chunks of kRingChunk bytes go through a ring of
 // pinned buffers; host threads (OpenMP) fill chunk c + 1 while the DMA engine
 // moves chunk c, so a pageable source uploads at close to the pinned PCIe
@@ -485,7 +505,7 @@ int compute_scene_bounds(potr_ctx *ctx, const potr_splats &sp, bool defer_sh = f
     LAUNCH(1, launch_bbox(sp.n, sp.positions, P<unsigned long long>(ctx->bbox), ctx->stream));
     CK(cudaMemcpyAsync(ctx->pinned, ctx->bbox.p, 6 * sizeof(uint64_t), cudaMemcpyDeviceToHost,
                        ctx->stream));
-    CK(cudaStreamSynchronize(ctx->stream));
+    CK(host_wait(ctx));
     for (int i = 0; i < 3; i++) {
         ctx->scene_lo[i] = ordered_to_double((unsigned long long)ctx->pinned[i]);
         ctx->scene_hi[i] = ordered_to_double((unsigned long long)ctx->pinned[3 + i]);
@@ -720,7 +740,7 @@ int bin_batch(potr_ctx *ctx, const potr_splats &sp, const potr_camera *cams, int
                        cudaMemcpyDeviceToHost, ctx->stream));
     CK(cudaMemcpyAsync(ctx->pinned + 1, ctx->overflow.p, 2 * sizeof(int), cudaMemcpyDeviceToHost,
                        ctx->stream));
-    CK(cudaStreamSynchronize(ctx->stream));
+    CK(host_wait(ctx));
     int flags[2];
     std::memcpy(flags, ctx->pinned + 1, sizeof(flags));
     if (dk.compact && flags[0] != 0)  // bound violated: exact raw-key fallback
@@ -754,7 +774,7 @@ int bin_batch(potr_ctx *ctx, const potr_splats &sp, const potr_camera *cams, int
         for (int v = sb; v < nview; v += sb)
             CK(cudaMemcpyAsync(&ctx->pinned[2 + v], P<int64_t>(ctx->offs) + (int64_t)v * n,
                                sizeof(int64_t), cudaMemcpyDeviceToHost, ctx->stream));
-        CK(cudaStreamSynchronize(ctx->stream));
+        CK(host_wait(ctx));
         for (int v = sb; v < nview; v += sb) vstart[v] = ctx->pinned[2 + v];
     }
 
@@ -1020,6 +1040,7 @@ void potr_destroy(potr_ctx *ctx) {
         cudaEventDestroy(ctx->upload_after);
     }
     for (cudaEvent_t e : ctx->upload_ev_pool) cudaEventDestroy(e);
+    if (ctx->poll_ev) cudaEventDestroy(ctx->poll_ev);
     activate_set(ctx, 0);
     for (auto &b : ctx->sets)
         for (DevBuf *d : {&b.rec, &b.sids, &b.offs, &b.pair, &b.ranges})
@@ -1682,7 +1703,25 @@ int potr_upload_async(potr_ctx *ctx, void *dst, const void *src, int64_t bytes) 
     ctx->upload_jobs.push_back(job);
     ctx->upload_pending = true;
     {
-        std::lock_guard<std::mutex> lk(ctx->upload_mu);
+        std::unique_lock<std::mutex> lk(ctx->upload_mu);
+        // a pinned source with nothing queued before it: the DMA engine
+        // alone, issued from this thread (FIFO order on copy_stream holds)
+        if (ctx->upload_todo.empty() && ctx->upload_done == job.seq - 1 && !ctx->upload_rc) {
+            cudaPointerAttributes at;
+            if (cudaPointerGetAttributes(&at, src) == cudaSuccess &&
+                at.type == cudaMemoryTypeHost) {
+                cudaError_t e = cudaMemcpyAsync(dst, src, (size_t)bytes, cudaMemcpyHostToDevice,
+                                                ctx->copy_stream);
+                if (e == cudaSuccess) e = cudaEventRecord(ev, ctx->copy_stream);
+                if (e != cudaSuccess) {
+                    ctx->upload_rc = POTR_E_CUDA;
+                    ctx->upload_err = cudaGetErrorString(e);
+                }
+                ctx->upload_done = job.seq;
+                return POTR_OK;
+            }
+            cudaGetLastError();  // pageable memory is not a CUDA pointer
+        }
         ctx->upload_todo.push_back(job);
     }
     ctx->upload_cv.notify_all();

@@ -452,7 +452,10 @@ __global__ void k_tile_ranges(int64_t j0, int64_t K, const KeyT *__restrict__ sk
 // records are held field-major (six 16-byte fields x 32 entries) so lanes that
 // read different entries hit different banks.  Two buffers: the next chunk
 // streams in with cp.async while the current one is composited.
-constexpr int kMaskChunks = 16;  // chunks per tile whose per-lane contribution masks are kept
+#ifndef POTR_MASK_CHUNKS
+#define POTR_MASK_CHUNKS 16
+#endif
+constexpr int kMaskChunks = POTR_MASK_CHUNKS;  // chunks per tile whose per-lane contribution masks are kept
 
 struct ChunkBuf {
     double2 f[6][32];  // (mx,my) (ha,ib) (hc,pthr) bbox(int4) (opac,cr) (cg,cb)
