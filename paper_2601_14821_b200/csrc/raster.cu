@@ -438,11 +438,25 @@ __global__ void k_duplicate(int64_t total, int64_t n, const int32_t *__restrict_
 template <typename KeyT>
 __global__ void k_tile_ranges(int64_t j0, int64_t K, const KeyT *__restrict__ skey,
                               int2 *__restrict__ rng, int tbase) {
-    const int64_t jj = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (jj >= K) return;
-    const uint32_t t = skey[jj];
-    if (jj == 0 || skey[jj - 1] != t) rng[tbase + t].x = (int)(j0 + jj);
-    if (jj == K - 1 || skey[jj + 1] != t) rng[tbase + t].y = (int)(j0 + jj + 1);
+    // eight consecutive sorted keys per thread (one predecessor load)
+    constexpr int kPer = 8;
+    const int64_t jb = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * kPer;
+    if (jb >= K) return;
+    uint32_t k[kPer];
+#pragma unroll
+    for (int q = 0; q < kPer; q++) k[q] = jb + q < K ? (uint32_t)skey[jb + q] : 0xffffffffu;
+    uint32_t prev = jb > 0 ? (uint32_t)skey[jb - 1] : 0xffffffffu;
+    const uint32_t after = jb + kPer < K ? (uint32_t)skey[jb + kPer] : 0xffffffffu;
+#pragma unroll
+    for (int q = 0; q < kPer; q++) {
+        const int64_t jj = jb + q;
+        if (jj >= K) break;
+        const uint32_t t = k[q];
+        const uint32_t nxt = q + 1 < kPer ? k[q + 1] : after;
+        if (jj == 0 || prev != t) rng[tbase + t].x = (int)(j0 + jj);
+        if (jj == K - 1 || nxt != t) rng[tbase + t].y = (int)(j0 + jj + 1);
+        prev = t;
+    }
 }
 
 // ---------------------------------------------------------------------------
@@ -1490,12 +1504,11 @@ cudaError_t records_sort(void *temp, size_t temp_bytes, uint64_t *key, uint64_t 
 cudaError_t launch_tile_ranges(int64_t j0, int64_t K, bool key16, const void *skey, int2 *rng,
                                int tbase, cudaStream_t st) {
     if (K == 0) return cudaSuccess;
+    const unsigned g = grid_for((K + 7) / 8, 256);
     if (key16)
-        k_tile_ranges<uint16_t><<<grid_for(K, 256), 256, 0, st>>>(j0, K, (const uint16_t *)skey,
-                                                                  rng, tbase);
+        k_tile_ranges<uint16_t><<<g, 256, 0, st>>>(j0, K, (const uint16_t *)skey, rng, tbase);
     else
-        k_tile_ranges<uint32_t><<<grid_for(K, 256), 256, 0, st>>>(j0, K, (const uint32_t *)skey,
-                                                                  rng, tbase);
+        k_tile_ranges<uint32_t><<<g, 256, 0, st>>>(j0, K, (const uint32_t *)skey, rng, tbase);
     return cudaGetLastError();
 }
 

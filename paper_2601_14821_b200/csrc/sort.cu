@@ -34,12 +34,6 @@ __device__ __forceinline__ uint32_t digit_of(K k, int shift) {
     return (uint32_t)(((uint64_t)k >> shift) & (kBins - 1));
 }
 
-__device__ __forceinline__ int64_t cnt_gather(const int32_t *ids, const int32_t *cnt, int64_t i) {
-    return (int64_t)cnt[ids[i]];
-}
-
-
-
 // Lanes holding the same 8-bit digit (d < 256), or the same invalid marker
 // (d = 256): eight ballots on the digit bits -- full-rate VOTE/LOP instead of
 // MATCH, whose address-divergence-unit pipe saturated in the first version.
@@ -82,35 +76,51 @@ __device__ __forceinline__ uint32_t block_exclusive_scan(uint32_t v, uint32_t *w
 
 // All passes' digit histograms in one read of the keys: plain shared atomics
 // into two sub-histograms per CTA (even / odd warps).
-template <typename K>
+template <typename K, int PASSES>
 __global__ void __launch_bounds__(256) k_radix_hist(const K *__restrict__ keys, int64_t n,
-                                                   int begin_bit, int passes,
-                                                   uint32_t *__restrict__ hist) {
-    __shared__ uint32_t h[2][8 * kBins];
-    for (int i = threadIdx.x; i < 2 * 8 * kBins; i += blockDim.x) (&h[0][0])[i] = 0;
+                                                   int begin_bit, uint32_t *__restrict__ hist) {
+    __shared__ uint32_t h[2][PASSES * kBins];
+    for (int i = threadIdx.x; i < 2 * PASSES * kBins; i += blockDim.x) (&h[0][0])[i] = 0;
     __syncthreads();
     uint32_t *hw = h[(threadIdx.x >> 5) & 1];
-    const int64_t stride = (int64_t)gridDim.x * blockDim.x * 4;
-    for (int64_t base = (int64_t)blockIdx.x * blockDim.x * 4; base < n; base += stride) {
-        K k[4];
-        bool v[4];
+    constexpr int kQ = 8;  // keys per thread per sweep (independent loads)
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x * kQ;
+    for (int64_t base = (int64_t)blockIdx.x * blockDim.x * kQ; base < n; base += stride) {
+        K k[kQ];
+        bool v[kQ];
 #pragma unroll
-        for (int q = 0; q < 4; q++) {
+        for (int q = 0; q < kQ; q++) {
             const int64_t i = base + q * blockDim.x + threadIdx.x;
             v[q] = i < n;
             k[q] = v[q] ? keys[i] : (K)0;
         }
 #pragma unroll
-        for (int q = 0; q < 4; q++) {
+        for (int q = 0; q < kQ; q++) {
             if (!v[q]) continue;
-            for (int p = 0; p < passes; p++)
+#pragma unroll
+            for (int p = 0; p < PASSES; p++)
                 atomicAdd(&hw[p * kBins + digit_of(k[q], begin_bit + 8 * p)], 1u);
         }
     }
     __syncthreads();
-    for (int i = threadIdx.x; i < passes * kBins; i += blockDim.x) {
+    for (int i = threadIdx.x; i < PASSES * kBins; i += blockDim.x) {
         const uint32_t c = h[0][i] + h[1][i];
         if (c) atomicAdd(&hist[i], c);
+    }
+}
+
+template <typename K>
+void launch_radix_hist(unsigned grid, const K *keys, int64_t n, int begin_bit, int passes,
+                       uint32_t *hist, cudaStream_t st) {
+    switch (passes) {
+        case 1: k_radix_hist<K, 1><<<grid, 256, 0, st>>>(keys, n, begin_bit, hist); break;
+        case 2: k_radix_hist<K, 2><<<grid, 256, 0, st>>>(keys, n, begin_bit, hist); break;
+        case 3: k_radix_hist<K, 3><<<grid, 256, 0, st>>>(keys, n, begin_bit, hist); break;
+        case 4: k_radix_hist<K, 4><<<grid, 256, 0, st>>>(keys, n, begin_bit, hist); break;
+        case 5: k_radix_hist<K, 5><<<grid, 256, 0, st>>>(keys, n, begin_bit, hist); break;
+        case 6: k_radix_hist<K, 6><<<grid, 256, 0, st>>>(keys, n, begin_bit, hist); break;
+        case 7: k_radix_hist<K, 7><<<grid, 256, 0, st>>>(keys, n, begin_bit, hist); break;
+        default: k_radix_hist<K, 8><<<grid, 256, 0, st>>>(keys, n, begin_bit, hist); break;
     }
 }
 
@@ -581,8 +591,8 @@ cudaError_t sort_impl(void *temp, size_t temp_bytes, K *keys, K *keys_alt, V *va
     cudaError_t e = cudaMemsetAsync(temp, 0, L.bytes, st);
     if (e != cudaSuccess) return e;
     const int64_t blocks = (n + 255) / 256;
-    k_radix_hist<K><<<(unsigned)(blocks < 148 * 8 ? blocks : 148 * 8), 256, 0, st>>>(
-        keys, n, begin_bit, passes, L.hist);
+    launch_radix_hist<K>((unsigned)(blocks < 148 * 8 ? blocks : 148 * 8), keys, n, begin_bit,
+                         passes, L.hist, st);
     e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     const int64_t tiles = tiles_for(n);
