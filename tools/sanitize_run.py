@@ -5,7 +5,8 @@
 
 C1-sized prune-score pass (score + importance + self-target modes), renders,
 records, binning, the SH recompute (all size classes + the DC fallback), the
-device controller's removal order, image metrics and the codec."""
+device controller's removal order, image metrics, the codec, and a scoring
+call through the overlapped upload (lookahead sets, deferred colours)."""
 import os
 import sys
 
@@ -34,5 +35,10 @@ m = metrics.compute_metrics(splats, pert, cams)
 params = codec.QuantParams(51.0, 101.0, 201.0, 2001.0)
 data, corder = codec.encode_container(splats, params, 0.5, 7e-05, 1.58e-05, zstd_level=3,
                                       camera_eyes=[c.eye for c in cams])
+# the overlapped upload: SH rows over the async threshold, several view
+# batches binned ahead with deferred colours
+big, bcams = make_fixture(40_000, 20, 2, width=80, height=60)
+btg = R.render_targets(big, bcams)
+bst = R.compute_delta_mse(big, bcams, btg)
 print("ok", float(st.mse), len(rec.splat_ids), len(lst), len(rep["failed"]), len(kept),
-      m.mean_psnr, len(data))
+      m.mean_psnr, len(data), float(bst.mse))
