@@ -703,7 +703,7 @@ constexpr int kSerialGroups = POTR_SERIAL_GROUPS;
 __device__ __forceinline__ void accumulate(WarpSmem &S, int key, double v0, double v1) {
     const unsigned FULL = 0xffffffffu;
     const int lane = threadIdx.x & 31;
-    const int row = kAccSplit == 2 ? lane >> 4 : 0;
+    const int row = lane / (32 / kAccSplit);  // kAccSplit in {1, 2, 4}
     const unsigned peers = __match_any_sync(FULL, key + 64 * row);
     const int gmax = __reduce_max_sync(FULL, (unsigned)__popc(peers));
     if (gmax <= kSerialGroups) {
