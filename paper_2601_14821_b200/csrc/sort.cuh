@@ -7,7 +7,8 @@
 // Radix sort: 8-bit digits, one histogram kernel for all passes, then one
 // "one-sweep" kernel per pass: a CTA takes the next tile of kTileItems keys
 // (dynamic tile index, so tiles are claimed in order), ranks them stably
-// inside the tile (warp-striped loads, __match_any_sync per round), publishes
+// inside the tile (warp-striped loads; equal digits found by ballots on the
+// digit bits and by __match_any_sync in alternate rounds), publishes
 // its per-digit counts, looks back over the preceding tiles' published counts
 // (decoupled look-back, one thread per digit) for its global digit offsets,
 // and scatters through shared memory so that each digit's run leaves in
