@@ -364,10 +364,11 @@ __device__ unsigned sparsify_mask(const double *__restrict__ G, int64_t gs, doub
     return mask;
 }
 
-constexpr int kSolveClasses = 4;  // 0: unseen, 1: <= 8 columns, 2: <= 12, 3: <= 16
+// 0: unseen, 1: <= 8 columns, 2: <= 12, 3: <= 16, 4: <= 10
+constexpr int kSolveClasses = 5;
 __device__ __forceinline__ int solve_class(unsigned mask) {
     const int m = __popc(mask);
-    return m <= 8 ? 1 : m <= 12 ? 2 : 3;
+    return m <= 8 ? 1 : m <= 10 ? 4 : m <= 12 ? 2 : 3;
 }
 
 __global__ void __launch_bounds__(128) k_sh_mask(int64_t n, const double *__restrict__ neq,
@@ -713,6 +714,8 @@ cudaError_t launch_sh_solve(const potr_splats &sp, const double *neq, double lam
     k_sh_mask<<<g, 128, 0, st>>>(n, neq, par_thr, masks, counts, lists);
     k_sh_solve_reg<8><<<g, 128, 0, st>>>(sp, neq, masks, lists + n, counts + 1, lambda_y,
                                          zero_thr, rgb, ycocg, status);
+    k_sh_solve_reg<10><<<g, 128, 0, st>>>(sp, neq, masks, lists + 4 * n, counts + 4, lambda_y,
+                                          zero_thr, rgb, ycocg, status);
     k_sh_solve_reg<12><<<g, 128, 0, st>>>(sp, neq, masks, lists + 2 * n, counts + 2, lambda_y,
                                           zero_thr, rgb, ycocg, status);
     {

@@ -34,7 +34,8 @@ for rep in range(2):
     ctx.call("potr_sh_accumulate", ctypes.byref(ds.struct()), S, cam_arr, D.ptr(ci), D.ptr(neq))
     torch.cuda.synchronize()
     t_acc = time.perf_counter() - t0
-print(f"accumulate {t_acc * 1e3:.1f} ms")
+seen = float(neq[184].mean().item())
+print(f"accumulate {t_acc * 1e3:.1f} ms; seen views per splat {seen:.1f} of {S} ({seen / S:.2f})")
 for lam in lams:
     for rep in range(2):
         torch.cuda.synchronize()
