@@ -559,7 +559,7 @@ def scene_measure(args, world, ds, cams, my_cams, tptr, cam_arr, lo, hi, ctx, de
     dm = torch.zeros(n, dtype=torch.float64, device=dev)
     mse = torch.zeros(1, dtype=torch.float64, device=dev)
     ci = torch.empty((max(1, hi - lo), n), dtype=torch.float64, device=dev)
-    neq = torch.zeros((_native.NEQ_STRIDE, n), dtype=torch.float64, device=dev)
+    neq = torch.empty((_native.NEQ_STRIDE, n), dtype=torch.float64, device=dev)
     rgb = torch.empty((n, 3, 16), dtype=torch.float64, device=dev)
     yc = torch.empty((n, 3, 16), dtype=torch.float64, device=dev)
     status = torch.empty(n, dtype=torch.int8, device=dev)
@@ -569,7 +569,7 @@ def scene_measure(args, world, ds, cams, my_cams, tptr, cam_arr, lo, hi, ctx, de
         c0, c1 = distributed.shard_range(n, rank, world)
         nmax = max(distributed.shard_range(n, r, world)[1] - distributed.shard_range(n, r, world)[0]
                    for r in range(world))
-        neq_s = torch.zeros((_native.NEQ_STRIDE, max(nmax, 1)), dtype=torch.float64, device=dev)
+        neq_s = torch.empty((_native.NEQ_STRIDE, max(nmax, 1)), dtype=torch.float64, device=dev)
         rgb_s = torch.empty((max(nmax, 1), 3, 16), dtype=torch.float64, device=dev)
         yc_s = torch.empty((max(nmax, 1), 3, 16), dtype=torch.float64, device=dev)
         status_s = torch.empty(max(nmax, 1), dtype=torch.int8, device=dev)
@@ -603,8 +603,7 @@ def scene_measure(args, world, ds, cams, my_cams, tptr, cam_arr, lo, hi, ctx, de
         torch.cuda.synchronize()
         t2 = time.perf_counter()
         if world == 1:
-            neq.zero_()
-            ctx.call("potr_sh_accumulate", ctypes.byref(ds0.struct()), hi - lo, cam_arr,
+            ctx.call("potr_sh_normal_equations", ctypes.byref(ds0.struct()), hi - lo, cam_arr,
                      D.ptr(ci), D.ptr(neq))
             ctx.call("potr_sh_solve", ctypes.byref(ds0.struct()), D.ptr(neq),
                      ctypes.c_double(SH_LAMBDA), ctypes.c_double(0.8175744761936437),
@@ -616,10 +615,9 @@ def scene_measure(args, world, ds, cams, my_cams, tptr, cam_arr, lo, hi, ctx, de
             # all-gather of the coefficients
             ci_s = distributed.transpose_to_splat_shard(ci[:hi - lo], S, n)
             ns = c1 - c0
-            neq_s.zero_()
             sub = D.DeviceSplats(ds0.positions[c0:c1], ds0.sh[c0:c1], ds0.opacities[c0:c1],
                                  ds0.scales[c0:c1], ds0.rotations[c0:c1])
-            ctx.call("potr_sh_accumulate", ctypes.byref(sub.struct()), S, all_cams,
+            ctx.call("potr_sh_normal_equations", ctypes.byref(sub.struct()), S, all_cams,
                      D.ptr(ci_s), D.ptr(neq_s))
             ctx.call("potr_sh_solve", ctypes.byref(sub.struct()), D.ptr(neq_s),
                      ctypes.c_double(SH_LAMBDA), ctypes.c_double(0.8175744761936437),

@@ -161,16 +161,24 @@ int potr_compact(potr_ctx *ctx, const potr_splats *splats, int ncam, const potr_
                  const double *camera_importance, double lambda_y, double parallel_threshold,
                  double zero_threshold, double *rgb, double *ycocg, int8_t *status);
 
-/* The two halves of potr_compact, for view-sharded multi-GPU use.
- * normal_eqs: (POTR_NEQ_STRIDE, n) entry-major, ADDED to (zero it first):
+/* The two halves of potr_compact (build_weighted_system ... compact_splat,
+ * compaction.py:89-192), for sweeps (one accumulation, many solves) and
+ * sharded use.
+ * normal_eqs: (POTR_NEQ_STRIDE, n) entry-major:
  *   rows 0..135 = upper triangle of G = sum_s (w_s y_s)(w_s y_s)^T,
  *   rows 136..183 = B[i][c] = sum_s (w_s y_s)_i (w_s YCoCg(color_s))_c,
  *   row 184 = number of cameras with w_s > 0.
- * A caller all-reduces normal_eqs across view shards, then solves. */
+ * potr_sh_accumulate ADDS to normal_eqs (zero it first; lets a caller add
+ * view shards); potr_sh_normal_equations OVERWRITES it (no zeroing pass, no
+ * read of the old values).  The splat-sharded path (each rank owns a splat
+ * span and all views) uses the latter. */
 #define POTR_NEQ_STRIDE 185
 int potr_sh_accumulate(potr_ctx *ctx, const potr_splats *splats, int ncam,
                        const potr_camera *cams, const double *camera_importance,
                        double *normal_eqs);
+int potr_sh_normal_equations(potr_ctx *ctx, const potr_splats *splats, int ncam,
+                             const potr_camera *cams, const double *camera_importance,
+                             double *normal_eqs);
 int potr_sh_solve(potr_ctx *ctx, const potr_splats *splats, const double *normal_eqs,
                   double lambda_y, double parallel_threshold, double zero_threshold,
                   double *rgb, double *ycocg, int8_t *status);

@@ -115,6 +115,9 @@ _SIGNATURES = {
     "potr_sh_accumulate": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(PotrSplats),
                                           ctypes.c_int, ctypes.POINTER(PotrCamera),
                                           ctypes.c_void_p, ctypes.c_void_p]),
+    "potr_sh_normal_equations": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(PotrSplats),
+                                                ctypes.c_int, ctypes.POINTER(PotrCamera),
+                                                ctypes.c_void_p, ctypes.c_void_p]),
     "potr_sh_solve": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(PotrSplats), ctypes.c_void_p,
                                      ctypes.c_double, ctypes.c_double, ctypes.c_double,
                                      ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]),

@@ -165,7 +165,7 @@ def sweep(splats, cameras, targets, camera_importance, lambdas, alphas, zero_thr
     mean |nonzero AC|, MSE vs targets), one per (lambda, alpha).
 
     Device-resident: the weighted normal equations do not depend on
-    (lambda, alpha), so they are accumulated once (potr_sh_accumulate) and
+    (lambda, alpha), so they are accumulated once (potr_sh_normal_equations) and
     only the solves, the re-renders and the error reductions run per grid
     point; nothing but the row scalars comes back to the host."""
     from .rasterizer import render_targets_device
@@ -187,9 +187,9 @@ def sweep(splats, cameras, targets, camera_importance, lambdas, alphas, zero_thr
                              mse / len(cameras)))
         return rows
     ci = D.as_device_matrix(camera_importance, (S, n), dev)
-    neq = torch.zeros((NEQ_STRIDE, n), dtype=torch.float64, device=dev)
+    neq = torch.empty((NEQ_STRIDE, n), dtype=torch.float64, device=dev)
     cams = _native.camera_array(cameras)
-    ctx.call("potr_sh_accumulate", ctypes.byref(ds.struct()), S, cams, D.ptr(ci), D.ptr(neq))
+    ctx.call("potr_sh_normal_equations", ctypes.byref(ds.struct()), S, cams, D.ptr(ci), D.ptr(neq))
     dev_targets = D.targets_cache.get(targets, cameras, dev)
     rgb = D.empty((n, 3, 16), dev)
     yc = D.empty((n, 3, 16), dev)

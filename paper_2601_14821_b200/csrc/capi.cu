@@ -1340,9 +1340,13 @@ int potr_bin(potr_ctx *ctx, const potr_splats *splats, const potr_camera *cam, i
     return POTR_OK;
 }
 
-int potr_sh_accumulate(potr_ctx *ctx, const potr_splats *splats, int ncam,
-                       const potr_camera *cams, const double *camera_importance,
-                       double *normal_eqs) {
+}  // extern "C"
+
+namespace {
+
+int sh_normal_equations(potr_ctx *ctx, const potr_splats *splats, int ncam,
+                        const potr_camera *cams, const double *camera_importance,
+                        double *normal_eqs, bool add) {
     if (!ctx) return POTR_E_ARG;
     CK(cudaSetDevice(ctx->device));
     JOIN_UPLOAD(ctx);
@@ -1350,7 +1354,13 @@ int potr_sh_accumulate(potr_ctx *ctx, const potr_splats *splats, int ncam,
     if (rc) return rc;
     if (ncam < 0 || (ncam > 0 && (!cams || !camera_importance)) || !normal_eqs)
         return fail(ctx, POTR_E_ARG, "bad arguments to sh_accumulate");
-    if (ncam == 0 || splats->n == 0) return POTR_OK;
+    if (splats->n == 0) return POTR_OK;
+    if (ncam == 0) {
+        if (!add)
+            CK(cudaMemsetAsync(normal_eqs, 0, sizeof(double) * POTR_NEQ_STRIDE * splats->n,
+                               ctx->stream));
+        return POTR_OK;
+    }
     std::vector<double> eyes(3 * (size_t)ncam);
     for (int s = 0; s < ncam; s++)
         for (int i = 0; i < 3; i++) eyes[3 * s + i] = cams[s].eye[i];
@@ -1362,10 +1372,26 @@ int potr_sh_accumulate(potr_ctx *ctx, const potr_splats *splats, int ncam,
     {
         Stage _st(ctx, POTR_STAGE_SH_ACCUMULATE);
         LAUNCH(1, launch_sh_accumulate(*splats, ncam, P<double>(ctx->eyes), camera_importance,
-                                       normal_eqs, ctx->stream));
+                                       normal_eqs, add, ctx->stream));
         _st.end();
     }
     return POTR_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int potr_sh_accumulate(potr_ctx *ctx, const potr_splats *splats, int ncam,
+                       const potr_camera *cams, const double *camera_importance,
+                       double *normal_eqs) {
+    return sh_normal_equations(ctx, splats, ncam, cams, camera_importance, normal_eqs, true);
+}
+
+int potr_sh_normal_equations(potr_ctx *ctx, const potr_splats *splats, int ncam,
+                             const potr_camera *cams, const double *camera_importance,
+                             double *normal_eqs) {
+    return sh_normal_equations(ctx, splats, ncam, cams, camera_importance, normal_eqs, false);
 }
 
 int potr_sh_solve(potr_ctx *ctx, const potr_splats *splats, const double *normal_eqs,
@@ -1401,8 +1427,8 @@ int potr_compact(potr_ctx *ctx, const potr_splats *splats, int ncam, const potr_
     if (rc) return rc;
     const int64_t n = splats->n;
     ENSURE(ctx->neq, sizeof(double) * POTR_NEQ_STRIDE * n);
-    CK(cudaMemsetAsync(ctx->neq.p, 0, sizeof(double) * POTR_NEQ_STRIDE * n, ctx->stream));
-    rc = potr_sh_accumulate(ctx, splats, ncam, cams, camera_importance, P<double>(ctx->neq));
+    rc = potr_sh_normal_equations(ctx, splats, ncam, cams, camera_importance,
+                                  P<double>(ctx->neq));
     if (rc) return rc;
     return potr_sh_solve(ctx, splats, P<double>(ctx->neq), lambda_y, parallel_threshold,
                          zero_threshold, rgb, ycocg, status);

@@ -171,7 +171,7 @@ cudaError_t launch_iota64(int64_t n, int64_t *out, cudaStream_t st);
 
 // SH recompute (sh.cu)
 cudaError_t launch_sh_accumulate(const potr_splats &sp, int ncam, const double *eyes_dev,
-                                 const double *cam_imp, double *neq, cudaStream_t st);
+                                 const double *cam_imp, double *neq, bool add, cudaStream_t st);
 // scratch: sh_solve_scratch_bytes(n) bytes of device memory
 size_t sh_solve_scratch_bytes(int64_t n);
 cudaError_t launch_sh_solve(const potr_splats &sp, const double *neq, double lambda_y,

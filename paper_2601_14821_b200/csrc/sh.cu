@@ -85,6 +85,9 @@ __device__ __forceinline__ void dmma_acc(double (&d)[2], double a, double b) {
         : "d"(a), "d"(b));
 }
 
+// kAdd: add into normal_eqs (potr_sh_accumulate); else overwrite it
+// (potr_sh_normal_equations: no read of the old values, no zeroing pass)
+template <bool kAdd>
 __global__ void __launch_bounds__(32 * kShWarps, POTR_SH_MIN_BLOCKS)
     k_sh_accumulate(potr_splats sp, int ncam, const double *__restrict__ eyes,
                     const double *__restrict__ cam_imp, double *__restrict__ neq) {
@@ -227,14 +230,18 @@ __global__ void __launch_bounds__(32 * kShWarps, POTR_SH_MIN_BLOCKS)
 #pragma unroll
             for (int h = 0; h < 2; h++) {
                 e[t][h] = sh_entry(kTileRow[t] + (lane >> 2), kTileCol[t] + 2 * (lane & 3) + h);
-                old[t][h] = e[t][h] >= 0 ? neq[(int64_t)e[t][h] * n + k] : 0.0;
+                old[t][h] = kAdd && e[t][h] >= 0 ? neq[(int64_t)e[t][h] * n + k] : 0.0;
             }
 #pragma unroll
         for (int t = 0; t < 5; t++)
 #pragma unroll
             for (int h = 0; h < 2; h++)
-                if (e[t][h] >= 0) neq[(int64_t)e[t][h] * n + k] = old[t][h] + acc[q][t][h];
-        if (lane == 0) neq[(int64_t)184 * n + k] += (double)seen[q];
+                if (e[t][h] >= 0)
+                    neq[(int64_t)e[t][h] * n + k] = kAdd ? old[t][h] + acc[q][t][h] : acc[q][t][h];
+        if (lane == 0) {
+            if (kAdd) neq[(int64_t)184 * n + k] += (double)seen[q];
+            else neq[(int64_t)184 * n + k] = (double)seen[q];
+        }
     }
 }
 
@@ -677,17 +684,24 @@ __global__ void __launch_bounds__(kShSmemThreads) k_sh_solve_smem(
 }
 
 cudaError_t launch_sh_accumulate(const potr_splats &sp, int ncam, const double *eyes_dev,
-                                 const double *cam_imp, double *neq, cudaStream_t st) {
+                                 const double *cam_imp, double *neq, bool add, cudaStream_t st) {
     if (sp.n == 0) return cudaSuccess;
     const unsigned blocks = (unsigned)((sp.n + kShSplatsPerBlock - 1) / kShSplatsPerBlock);
     constexpr size_t smem = sizeof(double) * kShWarps * 33 * kShRow;
     static bool attr = false;
     if (!attr) {
-        cudaFuncSetAttribute(k_sh_accumulate, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        cudaFuncSetAttribute(k_sh_accumulate<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)smem);
+        cudaFuncSetAttribute(k_sh_accumulate<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)smem);
         attr = true;
     }
-    k_sh_accumulate<<<blocks, 32 * kShWarps, smem, st>>>(sp, ncam, eyes_dev, cam_imp, neq);
+    if (add)
+        k_sh_accumulate<true><<<blocks, 32 * kShWarps, smem, st>>>(sp, ncam, eyes_dev, cam_imp,
+                                                                   neq);
+    else
+        k_sh_accumulate<false><<<blocks, 32 * kShWarps, smem, st>>>(sp, ncam, eyes_dev, cam_imp,
+                                                                    neq);
     return cudaGetLastError();
 }
 

@@ -49,15 +49,14 @@ def main():
     ds = D.DeviceSplats.from_host(splats, dev)
     n, S = ds.n, len(cams)
     imp, ci, _, _ = R.forward_stats_device(ds, cams, None)
-    neq = torch.zeros((_native.NEQ_STRIDE, n), dtype=torch.float64, device=dev)
+    neq = torch.empty((_native.NEQ_STRIDE, n), dtype=torch.float64, device=dev)
     rgb = torch.empty((n, 3, 16), dtype=torch.float64, device=dev)
     yc = torch.empty((n, 3, 16), dtype=torch.float64, device=dev)
     status = torch.empty(n, dtype=torch.int8, device=dev)
     cam_arr = _native.camera_array(cams)
 
     def accumulate():
-        neq.zero_()
-        ctx.call("potr_sh_accumulate", ctypes.byref(ds.struct()), S, cam_arr, D.ptr(ci),
+        ctx.call("potr_sh_normal_equations", ctypes.byref(ds.struct()), S, cam_arr, D.ptr(ci),
                  D.ptr(neq))
 
     def solve(lam):

@@ -17,8 +17,8 @@ ds = D.DeviceSplats.from_host(splats, dev)
 ctx = D.context()
 imp, ci, _, _ = R.forward_stats_device(ds, cams, None)
 n, S = ds.n, len(cams)
-neq = torch.zeros((_native.NEQ_STRIDE, n), dtype=torch.float64, device=dev)
-ctx.call("potr_sh_accumulate", ctypes.byref(ds.struct()), S, _native.camera_array(cams),
+neq = torch.empty((_native.NEQ_STRIDE, n), dtype=torch.float64, device=dev)
+ctx.call("potr_sh_normal_equations", ctypes.byref(ds.struct()), S, _native.camera_array(cams),
          D.ptr(ci), D.ptr(neq))
 tri = lambda i, j: i * 16 - (i * (i - 1)) // 2 + (j - i)  # noqa: E731
 norms = torch.stack([neq[tri(i, i)].sqrt() for i in range(16)], 1)

@@ -22,16 +22,15 @@ ds = D.DeviceSplats.from_host(splats, dev)
 ctx = D.context()
 imp, ci, _, _ = R.forward_stats_device(ds, cams, None)
 n, S = ds.n, len(cams)
-neq = torch.zeros((_native.NEQ_STRIDE, n), dtype=torch.float64, device=dev)
+neq = torch.empty((_native.NEQ_STRIDE, n), dtype=torch.float64, device=dev)
 rgb = torch.empty((n, 3, 16), dtype=torch.float64, device=dev)
 yc = torch.empty((n, 3, 16), dtype=torch.float64, device=dev)
 status = torch.empty(n, dtype=torch.int8, device=dev)
 cam_arr = _native.camera_array(cams)
 for rep in range(2):
-    neq.zero_()
     torch.cuda.synchronize()
     t0 = time.perf_counter()
-    ctx.call("potr_sh_accumulate", ctypes.byref(ds.struct()), S, cam_arr, D.ptr(ci), D.ptr(neq))
+    ctx.call("potr_sh_normal_equations", ctypes.byref(ds.struct()), S, cam_arr, D.ptr(ci), D.ptr(neq))
     torch.cuda.synchronize()
     t_acc = time.perf_counter() - t0
 seen = float(neq[184].mean().item())
