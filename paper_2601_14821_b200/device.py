@@ -70,6 +70,7 @@ def to_device(arr, device, shape=None):
 
 
 _STAGED_MIN = 8 << 20          # pageable sources from this size use potr_copy_to_device
+_ASYNC_GEOMETRY_MIN = 32 << 20  # geometry arrays from this size are queued (potr_upload_async)
 
 
 _PINNED_MAX = 256 << 20        # results up to this size land in pinned memory directly
@@ -153,6 +154,11 @@ class DeviceSplats:
                 out = {}
                 for f, shape in fields:
                     a = arrs[f]
+                    if f != "sh" and a.nbytes < _ASYNC_GEOMETRY_MIN:
+                        # small geometry arrays: faster on this thread (a queued
+                        # copy costs ~0.5 ms of worker overhead each)
+                        out[f] = to_device(a, dev, shape)
+                        continue
                     out[f] = torch.empty(shape, dtype=torch.float64, device=dev)
                     ctx.call("potr_upload_async", ptr(out[f]), ctypes.c_void_p(a.ctypes.data),
                              ctypes.c_int64(a.nbytes))
