@@ -86,18 +86,33 @@ __device__ __forceinline__ void dmma_acc(double (&d)[2], double a, double b) {
 }
 
 // kAdd: add into normal_eqs (potr_sh_accumulate); else overwrite it
-// (potr_sh_normal_equations: no read of the old values, no zeroing pass)
+// (potr_sh_normal_equations: no read of the old values, no zeroing pass).
+//
+// Views are taken kShWin at a time: the window's (view, splat) tile of
+// camera_importance is staged in shared memory, then each warp lists its
+// splat's SEEN views of the window (ascending) and evaluates them 32 at a
+// time, lane j the j-th seen view -- every lane busy, where a lane per view
+// idled on the ~26% of (splat, view) pairs with w = 0 -- and the MMAs take
+// the rows in list order, which is ascending view order: the same fma chain
+// per entry as before.
+#ifndef POTR_SH_WIN
+#define POTR_SH_WIN 128
+#endif
+constexpr int kShWin = POTR_SH_WIN;
+
 template <bool kAdd>
 __global__ void __launch_bounds__(32 * kShWarps, POTR_SH_MIN_BLOCKS)
     k_sh_accumulate(potr_splats sp, int ncam, const double *__restrict__ eyes,
                     const double *__restrict__ cam_imp, double *__restrict__ neq) {
-    __shared__ double wtile[32][kShSplatsPerBlock + 1];
-    // per warp: 32 view rows + a zero row (a step short of four views pads
-    // with it: fma(0, 0, acc) == acc exactly, acc is never -0)
+    __shared__ double wwin[kShWin][kShSplatsPerBlock + 1];
+    __shared__ uint8_t seen_v[kShWarps][kShWin];  // a warp's seen views of the window
+    // per warp: 32 rows + a zero row (a step short of four views pads with
+    // it: fma(0, 0, acc) == acc exactly, acc is never -0)
     extern __shared__ __align__(16) double sh_dyn[];
     double(*A)[33][kShRow] = reinterpret_cast<double(*)[33][kShRow]>(sh_dyn);
     __shared__ double shs[kShSplatsPerBlock][48];
     __shared__ double pos[kShSplatsPerBlock][3];
+    static_assert(kShWin <= 256, "window views index as bytes");
     const int64_t n = sp.n;
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const int64_t k0 = (int64_t)blockIdx.x * kShSplatsPerBlock;
@@ -120,98 +135,84 @@ __global__ void __launch_bounds__(32 * kShWarps, POTR_SH_MIN_BLOCKS)
 #pragma unroll
         for (int t = 0; t < 5; t++) acc[q][t][0] = acc[q][t][1] = 0.0;
     }
-
-    // the next view block's camera_importance tile is loaded into registers
-    // while the current one is processed (its global-load latency was the
-    // largest stall); each thread holds kPre of the 32 x kShSplatsPerBlock values
-    constexpr int kPre = 32 * kShSplatsPerBlock / (32 * kShWarps);
-    static_assert(32 * kShWarps >= 96, "one eye coordinate per thread");
-    __shared__ double eye_s[32][3];
-    double pre[kPre], pre_eye;  // and the block's 32 camera centres, likewise
-    const auto load_tile = [&](int s0) {
-        const int nv = ncam - s0 < 32 ? ncam - s0 : 32;
-#pragma unroll
-        for (int q = 0; q < kPre; q++) {
-            const int i = threadIdx.x + q * 32 * kShWarps;
-            const int v = i / kShSplatsPerBlock, kk = i % kShSplatsPerBlock;
-            pre[q] = (v < nv && kk < nk) ? cam_imp[(int64_t)(s0 + v) * n + k0 + kk] : 0.0;
-        }
-        pre_eye = threadIdx.x < 3 * nv ? eyes[3 * s0 + threadIdx.x] : 0.0;
-    };
-    load_tile(0);
     const double(*rows)[kShRow] = A[w];
-    for (int s0 = 0; s0 < ncam; s0 += 32) {
-        const int nv = ncam - s0 < 32 ? ncam - s0 : 32;
-        __syncthreads();  // previous round done with wtile; first round: sh/pos staged
-#pragma unroll
-        for (int q = 0; q < kPre; q++) {
-            const int i = threadIdx.x + q * 32 * kShWarps;
-            wtile[i / kShSplatsPerBlock][i % kShSplatsPerBlock] = pre[q];
+    const unsigned lt = (1u << lane) - 1u;
+    for (int s0 = 0; s0 < ncam; s0 += kShWin) {
+        const int nv = ncam - s0 < kShWin ? ncam - s0 : kShWin;
+        __syncthreads();  // previous window done with wwin; first: sh / pos staged
+        for (int i = threadIdx.x; i < nv * kShSplatsPerBlock; i += blockDim.x) {
+            const int v = i / kShSplatsPerBlock, kk = i % kShSplatsPerBlock;
+            wwin[v][kk] = kk < nk ? cam_imp[(int64_t)(s0 + v) * n + k0 + kk] : 0.0;
         }
-        if (threadIdx.x < 96) (&eye_s[0][0])[threadIdx.x] = pre_eye;
         __syncthreads();
-        if (s0 + 32 < ncam) load_tile(s0 + 32);
-        const bool lv = lane < nv;
-        const double ex = eye_s[lane][0], ey = eye_s[lane][1], ez = eye_s[lane][2];
 #pragma unroll
         for (int q = 0; q < kPerWarp; q++) {
             const int kk = w * kPerWarp + q;
             if (kk >= nk) break;  // warp-uniform
-            const double wv = wtile[lane][kk];
-            const unsigned smask = __ballot_sync(0xffffffffu, lv && wv > 0.0);
-            if (wv > 0.0) {
-                double *row = A[w][lane];
-                const double d0 = pos[kk][0] - ex, d1 = pos[kk][1] - ey, d2 = pos[kk][2] - ez;
-                const double nrm = sqrt(d0 * d0 + d1 * d1 + d2 * d2);
-                double y[16];
-                sh_basis16(d0 / nrm, d1 / nrm, d2 / nrm, y);
-                // colors = basis @ sh^T (compaction.py:104): fused
-                // multiply-adds in two interleaved partial sums (the
-                // oracle's order; a 16-deep add chain was the largest stall)
-                double col[3];
+            // the splat's seen views of the window, ascending
+            int cnt = 0;
+            for (int vb = 0; vb < nv; vb += 32) {
+                const int v = vb + lane;
+                const bool sv = v < nv && wwin[v][kk] > 0.0;
+                const unsigned b = __ballot_sync(0xffffffffu, sv);
+                if (sv) seen_v[w][cnt + __popc(b & lt)] = (uint8_t)v;
+                cnt += __popc(b);
+            }
+            seen[q] += cnt;
+            __syncwarp();
+            for (int r0 = 0; r0 < cnt; r0 += 32) {  // warp-uniform
+                const int nr = cnt - r0 < 32 ? cnt - r0 : 32;
+                if (lane < nr) {
+                    const int v = seen_v[w][r0 + lane];
+                    const double wv = wwin[v][kk];
+                    const double *eye = eyes + 3 * (s0 + v);
+                    double *row = A[w][lane];
+                    const double d0 = pos[kk][0] - __ldg(eye), d1 = pos[kk][1] - __ldg(eye + 1),
+                                 d2 = pos[kk][2] - __ldg(eye + 2);
+                    const double nrm = sqrt(d0 * d0 + d1 * d1 + d2 * d2);
+                    double y[16];
+                    sh_basis16(d0 / nrm, d1 / nrm, d2 / nrm, y);
+                    // colors = basis @ sh^T (compaction.py:104): fused
+                    // multiply-adds in two interleaved partial sums (the
+                    // oracle's order; a 16-deep add chain was the largest stall)
+                    double col[3];
 #pragma unroll
-                for (int c = 0; c < 3; c++) {
-                    double a0 = 0.0, a1 = 0.0;
+                    for (int c = 0; c < 3; c++) {
+                        double a0 = 0.0, a1 = 0.0;
 #pragma unroll
-                    for (int i = 0; i < 16; i += 2) {
-                        a0 = fma(y[i], shs[kk][c * 16 + i], a0);
-                        a1 = fma(y[i + 1], shs[kk][c * 16 + i + 1], a1);
+                        for (int i = 0; i < 16; i += 2) {
+                            a0 = fma(y[i], shs[kk][c * 16 + i], a0);
+                            a1 = fma(y[i + 1], shs[kk][c * 16 + i + 1], a1);
+                        }
+                        col[c] = a0 + a1;
                     }
-                    col[c] = a0 + a1;
-                }
 #pragma unroll
-                for (int i = 0; i < 16; i++) row[i] = y[i] * wv;
+                    for (int i = 0; i < 16; i++) row[i] = y[i] * wv;
 #pragma unroll
-                for (int c = 0; c < 3; c++) {
-                    const double yc = col[0] * kRgbToYcocg[c * 3] +
-                                      col[1] * kRgbToYcocg[c * 3 + 1] +
-                                      col[2] * kRgbToYcocg[c * 3 + 2];
-                    row[kShYc + c] = yc * wv;
+                    for (int c = 0; c < 3; c++) {
+                        const double yc = col[0] * kRgbToYcocg[c * 3] +
+                                          col[1] * kRgbToYcocg[c * 3 + 1] +
+                                          col[2] * kRgbToYcocg[c * 3 + 2];
+                        row[kShYc + c] = yc * wv;
+                    }
                 }
+                __syncwarp();
+                // rows 0..nr-1 four at a time (ascending views); lane l loads
+                // entries l/4, 8 + l/4, 16 + l/4 of row 4u + l%4 (the zero row
+                // past nr)
+                for (int u = 0; u < nr; u += 4) {
+                    const int rr = u + (lane & 3);
+                    const double *row = rows[rr < nr ? rr : 32];
+                    const int r = lane >> 2;
+                    const double x0 = row[r], x1 = row[8 + r], x2 = row[16 + r];
+                    dmma_acc(acc[q][0], x0, x0);
+                    dmma_acc(acc[q][1], x0, x1);
+                    dmma_acc(acc[q][2], x1, x1);
+                    dmma_acc(acc[q][3], x0, x2);
+                    dmma_acc(acc[q][4], x1, x2);
+                }
+                __syncwarp();
             }
-            seen[q] += __popc(smask);
-            __syncwarp();
-            // the splat's seen views four at a time, ascending; lane l loads
-            // entries l/4, 8 + l/4, 16 + l/4 of the row of view l%4
-            unsigned m = smask;
-            while (m) {  // warp-uniform
-                int v = 32;
-#pragma unroll
-                for (int u = 0; u < 4; u++) {
-                    const int vu = m ? __ffs(m) - 1 : 32;
-                    m &= m - 1u;
-                    if ((lane & 3) == u) v = vu;
-                }
-                const double *row = rows[v];
-                const int r = lane >> 2;
-                const double x0 = row[r], x1 = row[8 + r], x2 = row[16 + r];
-                dmma_acc(acc[q][0], x0, x0);
-                dmma_acc(acc[q][1], x0, x1);
-                dmma_acc(acc[q][2], x1, x1);
-                dmma_acc(acc[q][3], x0, x2);
-                dmma_acc(acc[q][4], x1, x2);
-            }
-            __syncwarp();
         }
     }
     // tile t's block of rows / columns: G00 (0, 0), G01 (0, 8), G11 (8, 8),
