@@ -1410,7 +1410,7 @@ int potr_sh_solve(potr_ctx *ctx, const potr_splats *splats, const double *normal
     {
         Stage _st(ctx, POTR_STAGE_SH_SOLVE);
         ENSURE(ctx->sh_scratch, sh_solve_scratch_bytes(splats->n));
-        LAUNCH(5, launch_sh_solve(*splats, normal_eqs, lambda_y, parallel_threshold, zero_threshold,
+        LAUNCH(6, launch_sh_solve(*splats, normal_eqs, lambda_y, parallel_threshold, zero_threshold,
                                   rgb, ycocg, status, ctx->sh_scratch.p, ctx->stream));
         _st.end();
     }
