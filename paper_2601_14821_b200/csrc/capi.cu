@@ -736,10 +736,19 @@ int bin_batch(potr_ctx *ctx, const potr_splats &sp, const potr_camera *cams, int
                        P<int64_t>(ctx->offs), total, ctx->stream));
         _st.end();
     }
+    // tile sort groups: sb views per stable sort, 16-bit keys when they fit
+    const int sb_max = 65536 / g.ntiles;
+    const bool key16 = sb_max >= 1;
+    const int sb = key16 ? (sb_max < nview ? sb_max : nview) : nview;
+    // one readback: the pair count, the key-bound flags and the pair index
+    // where each sort group begins (pairs are view-major)
     CK(cudaMemcpyAsync(ctx->pinned, P<int64_t>(ctx->offs) + total, sizeof(int64_t),
                        cudaMemcpyDeviceToHost, ctx->stream));
     CK(cudaMemcpyAsync(ctx->pinned + 1, ctx->overflow.p, 2 * sizeof(int), cudaMemcpyDeviceToHost,
                        ctx->stream));
+    for (int v = sb; v < nview; v += sb)
+        CK(cudaMemcpyAsync(&ctx->pinned[2 + v], P<int64_t>(ctx->offs) + (int64_t)v * n,
+                           sizeof(int64_t), cudaMemcpyDeviceToHost, ctx->stream));
     CK(host_wait(ctx));
     int flags[2];
     std::memcpy(flags, ctx->pinned + 1, sizeof(flags));
@@ -752,10 +761,6 @@ int bin_batch(potr_ctx *ctx, const potr_splats &sp, const potr_camera *cams, int
     ctx->pairs_total += K;
     if (K > 0x7fffff00LL) return fail(ctx, POTR_E_ARG, "more than 2^31 tile pairs in one batch");
 
-    // tile sort groups: sb views per stable sort, 16-bit keys when they fit
-    const int sb_max = 65536 / g.ntiles;
-    const bool key16 = sb_max >= 1;
-    const int sb = key16 ? (sb_max < nview ? sb_max : nview) : nview;
     const size_t kbytes = key16 ? sizeof(uint16_t) : sizeof(uint32_t);
     ENSURE(ctx->tkey, kbytes * K);
     ENSURE(ctx->tskey, kbytes * K);
@@ -770,13 +775,7 @@ int bin_batch(potr_ctx *ctx, const potr_splats &sp, const potr_camera *cams, int
     // pair index where each sort group begins (pairs are view-major)
     std::vector<int64_t> vstart(nview + 1, 0);
     vstart[nview] = K;
-    if (nview > sb) {
-        for (int v = sb; v < nview; v += sb)
-            CK(cudaMemcpyAsync(&ctx->pinned[2 + v], P<int64_t>(ctx->offs) + (int64_t)v * n,
-                               sizeof(int64_t), cudaMemcpyDeviceToHost, ctx->stream));
-        CK(host_wait(ctx));
-        for (int v = sb; v < nview; v += sb) vstart[v] = ctx->pinned[2 + v];
-    }
+    for (int v = sb; v < nview; v += sb) vstart[v] = ctx->pinned[2 + v];
 
     {
         Stage _st(ctx, POTR_STAGE_DUPLICATE);
