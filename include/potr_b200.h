@@ -234,6 +234,30 @@ int potr_attribute_streams(potr_ctx *ctx, int64_t n, const int64_t *order, const
                            double sf_rotation, double sf_scale, uint8_t *out, int64_t capacity,
                            int64_t *stream_lengths);
 
+/* deserialize_octree (quantize.py:180-226): the preorder octree stream's leaf
+ * centres, repeated per leaf count, in DFS order (positions, host, capacity x
+ * 3) and their depths (host int32); center / half as stored in the header
+ * (float32 values).  *count = splats in the stream (may exceed capacity).
+ * Host code: a preorder stream's node boundaries are only known by parsing
+ * it.  Errors (-1, message "octree: ..."): truncated stream, leaf with zero
+ * splats, internal node below the depth limit, trailing bytes. */
+int potr_octree_decode(potr_ctx *ctx, const uint8_t *stream, int64_t len, const double *center,
+                       double half, int max_depth, int64_t capacity, double *positions,
+                       int32_t *depths, int64_t *count);
+
+/* decode_attribute_streams (bitstream.py:169-220) on the GPU: streams = the
+ * 55 attribute streams back to back (host), their lengths (host int64[55]);
+ * outputs (device, n splats in DFS order): sh (n, 3, 16) RGB, opacities,
+ * scales (n, 3), rotations (n, 4) (w, x, y, z); *n_clamped = quaternions
+ * outside the unit ball (clamped, as the reference warns).  Errors (-1):
+ * "varint: truncated varint stream" / "varint: overlong varint" (the
+ * reference's ValueError) and "integrity: <what> stream has <k> trailing
+ * bytes" (IntegrityError).  Synchronizes. */
+int potr_attribute_decode(potr_ctx *ctx, int64_t n, const uint8_t *streams,
+                          const int64_t *stream_lengths, double sf_sh, double sf_opacity,
+                          double sf_rotation, double sf_scale, double *sh, double *opacities,
+                          double *scales, double *rotations, int64_t *n_clamped);
+
 /* ---- tuning ------------------------------------------------------------- */
 
 /* Views processed per pipeline round (1..8, default 8; env POTR_B200_VIEW_BATCH). */

@@ -154,3 +154,173 @@ def encode_container(splats, params: QuantParams, q, beta, gamma, zstd_level=19,
     header = pack_header(n, q, params, beta, gamma, center, half, max_depth, zstd_level,
                          [len(s) for s in streams])
     return header + _zstd.compress(b"".join(streams), zstd_level), order
+
+
+# ---------------------------------------------------------------------------
+# Decode side (bitstream.py:53-112, :169-247, :278-292; quantize.py:173-226)
+
+STREAM_OCTREE = 0
+_CLAMP_WARN = "quaternions outside the unit ball, clamped"
+
+
+class ContainerError(ValueError):
+    pass
+
+
+class UnsupportedFormatError(ContainerError):
+    pass
+
+
+class IntegrityError(ContainerError):
+    pass
+
+
+class OctreeError(ValueError):
+    pass
+
+
+@dataclass
+class ContainerHeader:
+    """bitstream.py:66-106 (fields and unpack)."""
+    splat_count: int
+    q: float
+    params: QuantParams
+    beta: float
+    gamma: float
+    root_center: np.ndarray
+    root_half: float
+    max_depth: int = DEFAULT_MAX_DEPTH
+    zstd_level: int = 19
+    stream_lengths: list = None
+
+    def pack(self) -> bytes:
+        return pack_header(self.splat_count, self.q, self.params, self.beta, self.gamma,
+                           self.root_center, self.root_half, self.max_depth, self.zstd_level,
+                           self.stream_lengths or [0] * NUM_STREAMS)
+
+    @classmethod
+    def unpack(cls, data: bytes):
+        if len(data) < HEADER_SIZE:
+            raise IntegrityError("file shorter than the container header")
+        fields = struct.unpack_from(_HEADER_FMT, data)
+        if fields[0] != MAGIC:
+            raise UnsupportedFormatError("bad magic, not a POTR container")
+        if fields[1] != VERSION:
+            raise UnsupportedFormatError(f"unsupported container version {fields[1]}")
+        (_, _, count, q, sf_sh, sf_op, sf_rot, sf_sc, beta, gamma,
+         cx, cy, cz, half, max_depth, level) = fields[:16]
+        return cls(splat_count=count, q=q, params=QuantParams(sf_sh, sf_op, sf_rot, sf_sc),
+                   beta=beta, gamma=gamma, root_center=np.array([cx, cy, cz], dtype=np.float64),
+                   root_half=float(half), max_depth=max_depth, zstd_level=level,
+                   stream_lengths=list(fields[16:]))
+
+
+def read_container(data: bytes):
+    """bitstream.py:235-247: the header and the 56 streams (host zstd)."""
+    header = ContainerHeader.unpack(data)
+    expected = sum(header.stream_lengths)
+    try:
+        payload = _zstd.decompress(bytes(data[HEADER_SIZE:]), expected)
+    except _zstd.ZstdError as e:
+        raise IntegrityError(str(e)) from e
+    streams = []
+    pos = 0
+    for length in header.stream_lengths:
+        streams.append(payload[pos:pos + length])
+        pos += length
+    return header, streams
+
+
+@dataclass
+class DecodedOctree:
+    """quantize.py:173-177 without the Python node tree (positions and depths
+    are what decode_container consumes)."""
+    positions: np.ndarray
+    depths: np.ndarray
+    tree: object = None
+
+
+def _octree_call(data, center, half, max_depth, capacity):
+    ctx = D.context()
+    buf = np.frombuffer(bytes(data), dtype=np.uint8)
+    c = np.ascontiguousarray(center, dtype=np.float64)
+    pos = np.empty((max(capacity, 1), 3), dtype=np.float64)
+    dep = np.empty(max(capacity, 1), dtype=np.int32)
+    cnt = ctypes.c_int64(0)
+    try:
+        ctx.call("potr_octree_decode", buf.ctypes.data_as(ctypes.c_void_p) if buf.size else None,
+                 ctypes.c_int64(buf.size), c.ctypes.data_as(ctypes.c_void_p), ctypes.c_double(half),
+                 int(max_depth), ctypes.c_int64(capacity), pos.ctypes.data_as(ctypes.c_void_p),
+                 dep.ctypes.data_as(ctypes.c_void_p), ctypes.byref(cnt))
+    except (ValueError, _native.PotrError) as e:
+        if "octree: " not in str(e):
+            raise
+        raise OctreeError(str(e).split("octree: ", 1)[1]) from None
+    return pos, dep, int(cnt.value)
+
+
+def deserialize_octree(data: bytes, center, half, max_depth=DEFAULT_MAX_DEPTH):
+    """quantize.py:180-226: leaf centres (repeated per count) and depths in
+    DFS order (libpotr_b200 potr_octree_decode: a preorder stream's node
+    boundaries are only known by parsing it, so this walk runs on the host)."""
+    center = np.float64(np.asarray(center, dtype=np.float32))
+    half = float(np.float64(np.float32(half)))
+    _, _, count = _octree_call(data, center, half, max_depth, 0)
+    pos, dep, count = _octree_call(data, center, half, max_depth, count)
+    return DecodedOctree(positions=pos[:count], depths=dep[:count].astype(np.int64))
+
+
+def decode_attribute_streams(streams, header: ContainerHeader, positions):
+    """bitstream.py:169-220 on the GPU (potr_attribute_decode): the scene in
+    DFS order with RGB coefficients; streams is the full 56-stream list."""
+    import warnings
+    from .scene import Splats
+    n = header.splat_count
+    p = header.params
+    attr = streams[1:]
+    lengths = np.array([len(s) for s in attr], dtype=np.int64)
+    blob = np.frombuffer(b"".join(bytes(s) for s in attr), dtype=np.uint8)
+    dev = D.current_device()
+    sh = torch.empty((n, 3, 16), dtype=torch.float64, device=dev)
+    opac = torch.empty(n, dtype=torch.float64, device=dev)
+    scales = torch.empty((n, 3), dtype=torch.float64, device=dev)
+    rot = torch.empty((n, 4), dtype=torch.float64, device=dev)
+    clamped = ctypes.c_int64(0)
+    try:
+        D.context().call("potr_attribute_decode", ctypes.c_int64(n),
+                         blob.ctypes.data_as(ctypes.c_void_p) if blob.size else
+                         ctypes.c_void_p(lengths.ctypes.data),
+                         lengths.ctypes.data_as(ctypes.c_void_p), ctypes.c_double(p.sf_sh),
+                         ctypes.c_double(p.sf_opacity), ctypes.c_double(p.sf_rotation),
+                         ctypes.c_double(p.sf_scale), D.ptr(sh), D.ptr(opac), D.ptr(scales),
+                         D.ptr(rot), ctypes.byref(clamped))
+    except (ValueError, _native.PotrError) as e:
+        msg = str(e)
+        if "integrity: " in msg:
+            raise IntegrityError(msg.split("integrity: ", 1)[1]) from None
+        if "varint: " in msg:
+            raise ValueError(msg.split("varint: ", 1)[1]) from None
+        raise
+    if clamped.value:
+        warnings.warn(f"{int(clamped.value)} {_CLAMP_WARN}", RuntimeWarning)
+    return Splats(positions=np.asarray(positions, dtype=np.float64).reshape(n, 3),
+                  sh=D.to_host(sh), opacities=D.to_host(opac), scales=D.to_host(scales),
+                  rotations=D.to_host(rot))
+
+
+def decode_container(data: bytes):
+    """bitstream.py:278-292: (splats in DFS order, header)."""
+    from .scene import Splats
+    header, streams = read_container(data)
+    if header.splat_count == 0:
+        empty = Splats(np.empty((0, 3)), np.empty((0, 3, 16)), np.empty(0),
+                       np.empty((0, 3)), np.empty((0, 4)))
+        return empty, header
+    decoded = deserialize_octree(streams[STREAM_OCTREE], header.root_center,
+                                 header.root_half, header.max_depth)
+    if decoded.positions.shape[0] != header.splat_count:
+        raise IntegrityError(
+            f"octree stream decodes {decoded.positions.shape[0]} splats, "
+            f"header says {header.splat_count}")
+    splats = decode_attribute_streams(streams, header, decoded.positions)
+    return splats, header

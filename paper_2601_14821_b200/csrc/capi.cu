@@ -1565,6 +1565,67 @@ int potr_attribute_streams(potr_ctx *ctx, int64_t n, const int64_t *order, const
     return POTR_OK;
 }
 
+int potr_octree_decode(potr_ctx *ctx, const uint8_t *stream, int64_t len, const double *center,
+                       double half, int max_depth, int64_t capacity, double *positions,
+                       int32_t *depths, int64_t *count) {
+    if (!ctx || !center || !count || (len > 0 && !stream) ||
+        (capacity > 0 && (!positions || !depths)))
+        return fail(ctx, POTR_E_ARG, "octree_decode: NULL argument");
+    int64_t trailing = 0;
+    const int rc = octree_decode_host(stream, len, center, half, max_depth, capacity, positions,
+                                      depths, count, &trailing);
+    switch (rc) {
+        case 0: return POTR_OK;
+        case kOctTruncated: return fail(ctx, POTR_E_ARG, "octree: truncated octree stream");
+        case kOctZeroLeaf: return fail(ctx, POTR_E_ARG, "octree: leaf with zero splats");
+        case kOctDepth:
+            return fail(ctx, POTR_E_ARG, "octree: internal node below depth limit " +
+                                             std::to_string(max_depth));
+        default:
+            return fail(ctx, POTR_E_ARG, "octree: " + std::to_string(trailing) +
+                                             " trailing bytes after octree");
+    }
+}
+
+int potr_attribute_decode(potr_ctx *ctx, int64_t n, const uint8_t *streams,
+                          const int64_t *stream_lengths, double sf_sh, double sf_opacity,
+                          double sf_rotation, double sf_scale, double *sh, double *opacities,
+                          double *scales, double *rotations, int64_t *n_clamped) {
+    if (!ctx || !stream_lengths || !n_clamped) return fail(ctx, POTR_E_ARG, "attribute_decode: NULL argument");
+    if (n < 1 || (int64_t)55 * n > 0x7ffffff0LL || !streams || !sh || !opacities || !scales ||
+        !rotations)
+        return fail(ctx, POTR_E_ARG, "attribute_decode: bad arrays");
+    CK(cudaSetDevice(ctx->device));
+    JOIN_UPLOAD(ctx);
+    int64_t start[56];
+    start[0] = 0;
+    for (int s = 0; s < 55; s++) {
+        if (stream_lengths[s] < 0) return fail(ctx, POTR_E_ARG, "attribute_decode: bad lengths");
+        start[s + 1] = start[s] + stream_lengths[s];
+    }
+    std::string err;
+    const int rc = run_attr_decode(n, streams, start, sf_sh, sf_opacity, sf_scale, sf_rotation,
+                                   sh, opacities, scales, rotations, n_clamped,
+                                   &ctx->codec_scratch, &ctx->codec_cap, ctx->pinned,
+                                   ctx->stream, &err);
+    ctx->launches += 5 + 3;
+    if (rc == 0) return POTR_OK;
+    if (rc == kDecCuda) return fail(ctx, POTR_E_CUDA, err);
+    if (rc == kDecTrailing) {
+        // bitstream.py:163-166: "<what> stream has <k> trailing bytes"
+        const int s = std::atoi(err.c_str());  // 1..55
+        const char *what = s <= 3 ? "DC" : s <= 48 ? "AC" : s == 49 ? "opacity"
+                                                 : s <= 52 ? "scale" : "rotation";
+        const uint8_t *b = streams + start[s - 1];
+        const int64_t slen = start[s] - start[s - 1];
+        int64_t used = 0, vals = 0;
+        while (used < slen && vals < n) vals += b[used++] < 0x80;
+        return fail(ctx, POTR_E_ARG, std::string("integrity: ") + what + " stream has " +
+                                         std::to_string(slen - used) + " trailing bytes");
+    }
+    return fail(ctx, POTR_E_ARG, "varint: " + err);
+}
+
 int potr_set_option(potr_ctx *ctx, int option, int value) {
     if (!ctx) return POTR_E_ARG;
     switch (option) {

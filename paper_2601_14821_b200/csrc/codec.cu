@@ -23,6 +23,7 @@
 // exactly at its depth.
 
 #include <cstring>
+#include <string>
 
 #include "common.cuh"
 #include "raster.cuh"
@@ -429,5 +430,276 @@ cudaError_t run_attr_streams(int64_t n, const int64_t *order, const double *ycoc
         k_attr_emit<<<blocks_for(m, 256), 256, 0, st>>>(m, val, off, out);
     return cudaGetLastError();
 }
+
+
+// ---------------------------------------------------------------------------
+// Decode side (bitstream.py:169-220, :278; quantize.py:180-226).
+//
+// The octree stream is a preorder walk whose node boundaries are only known
+// by parsing it (a node's size depends on its whole subtree), so it is
+// decoded by a host loop in this library (one pass over a few MB).  The 55
+// attribute streams are the data-parallel part: a byte ends a LEB128 value
+// iff its top bit is clear, so an exclusive scan of those flags numbers every
+// value, each terminating byte decodes its value from at most ten bytes back,
+// the DC columns are prefix-summed (their delta coding), and one thread per
+// splat dequantises, clamps the quaternions and converts YCoCg to RGB.
+
+// quantize.py:69-76
+static inline void child_center(const double *c, double h, int o, double *out) {
+    const double off = h * 0.5;
+    out[0] = c[0] + ((o & 4) ? off : -off);
+    out[1] = c[1] + ((o & 2) ? off : -off);
+    out[2] = c[2] + ((o & 1) ? off : -off);
+}
+
+namespace {
+struct OctDecoder {
+    const uint8_t *buf;
+    int64_t len, pos = 0, count = 0, capacity;
+    int max_depth;
+    double *positions;
+    int32_t *depths;
+    int err = 0;  // OctDecodeError
+
+    void read(const double *c, double h, int depth) {
+        if (err) return;
+        if (pos >= len) {
+            err = kOctTruncated;
+            return;
+        }
+        const uint8_t byte = buf[pos++];
+        if (byte == 0x00) {
+            // leaf: LEB128 count (varint.py _uleb_decode)
+            uint64_t v = 0;
+            int shift = 0;
+            for (;;) {
+                if (pos >= len) {
+                    err = kOctTruncated;
+                    return;
+                }
+                const uint8_t b = buf[pos++];
+                if (shift < 64) v |= (uint64_t)(b & 0x7f) << shift;
+                if (b < 0x80) break;
+                shift += 7;
+                if (shift > 63) {
+                    err = kOctTruncated;  // overlong count (reported as truncated)
+                    return;
+                }
+            }
+            if ((int64_t)v < 1) {
+                err = kOctZeroLeaf;
+                return;
+            }
+            for (uint64_t i = 0; i < v; i++, count++) {
+                if (count < capacity) {
+                    positions[3 * count] = c[0];
+                    positions[3 * count + 1] = c[1];
+                    positions[3 * count + 2] = c[2];
+                    depths[count] = depth;
+                }
+            }
+            return;
+        }
+        if (depth >= max_depth) {
+            err = kOctDepth;
+            return;
+        }
+        for (int o = 0; o < 8; o++) {
+            if (!(byte & (1 << o))) continue;
+            double cc[3];
+            child_center(c, h, o, cc);
+            read(cc, h * 0.5, depth + 1);
+            if (err) return;
+        }
+    }
+};
+}  // namespace
+
+int octree_decode_host(const uint8_t *buf, int64_t len, const double *center, double half,
+                       int max_depth, int64_t capacity, double *positions, int32_t *depths,
+                       int64_t *count, int64_t *trailing) {
+    OctDecoder d;
+    d.buf = buf;
+    d.len = len;
+    d.capacity = capacity;
+    d.max_depth = max_depth;
+    d.positions = positions;
+    d.depths = depths;
+    d.read(center, half, 0);
+    *count = d.count;
+    *trailing = d.len - d.pos;
+    if (d.err) return d.err;
+    if (d.pos != d.len) return kOctTrailing;
+    return 0;
+}
+
+__global__ void k_vflags(int64_t L, const uint8_t *__restrict__ b, int64_t *__restrict__ f) {
+    const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (p < L) f[p] = b[p] < 0x80 ? 1 : 0;
+}
+
+// Every terminating byte decodes its value; the value's global index is the
+// scan of terminators before it (stream s holds values s*n .. s*n + n-1 once
+// every stream was checked to hold exactly n).
+__global__ void k_vdecode(int64_t L, const uint8_t *__restrict__ b, const int64_t *__restrict__ ex,
+                          const int64_t *__restrict__ sstart, int64_t n,
+                          uint64_t *__restrict__ vals, int *__restrict__ overlong) {
+    const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= L || b[p] >= 0x80) return;
+    const int64_t g = ex[p];
+    const int64_t s = g / n;
+    const int64_t lo = sstart[s];
+    int64_t q = p;
+    while (q > lo && b[q - 1] >= 0x80 && p - q < 10) q--;
+    if (p - q + 1 > 10 || (q > lo && b[q - 1] >= 0x80)) {
+        atomicOr(overlong, 1);
+        return;
+    }
+    uint64_t v = 0;
+    for (int64_t j = q; j <= p; j++) v |= (uint64_t)(b[j] & 0x7f) << (7 * (j - q));
+    vals[g] = v;
+}
+
+__device__ __forceinline__ int64_t zigzag_dec(uint64_t z) {
+    return (int64_t)((z >> 1) ^ (0ull - (z & 1ull)));
+}
+
+__global__ void k_dc_zz(int64_t n, const uint64_t *__restrict__ vals, int64_t *__restrict__ dz) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= 3 * n) return;
+    dz[i] = zigzag_dec(vals[i]);  // streams 1..3 are the first 3n values
+}
+
+// bitstream.py:169-220 for splat i.  Value v of attribute stream s (1..55)
+// sits at vals[(s - 1) * n + i]; dc holds the DC columns' exclusive sums.
+__global__ void k_attr_assemble(int64_t n, const uint64_t *__restrict__ vals,
+                                const int64_t *__restrict__ dz, const int64_t *__restrict__ dcx,
+                                double sf_sh, double sf_op, double sf_sc, double sf_rot,
+                                double *__restrict__ sh, double *__restrict__ opac,
+                                double *__restrict__ scales, double *__restrict__ rot,
+                                unsigned long long *__restrict__ n_over) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const auto V = [&](int s) { return vals[(int64_t)(s - 1) * n + i]; };
+    double yc[48];
+    for (int ch = 0; ch < 3; ch++) {
+        const int64_t cum = dcx[(int64_t)ch * n + i] + dz[(int64_t)ch * n + i];  // np.cumsum
+        yc[ch * 16] = ((double)cum + 0.0) / sf_sh;
+    }
+    for (int coef = 0; coef < 15; coef++)
+        for (int ch = 0; ch < 3; ch++)
+            yc[ch * 16 + coef + 1] = ((double)zigzag_dec(V(4 + coef * 3 + ch)) + 0.0) / sf_sh;
+    double o = ((double)(int64_t)V(49) + 0.25) / sf_op;
+    o = o < 1e-9 ? 1e-9 : o;  // np.clip(opacities, 1e-9, 1 - 1e-9)
+    o = o > 1.0 - 1e-9 ? 1.0 - 1e-9 : o;
+    opac[i] = o;
+    for (int a = 0; a < 3; a++)
+        scales[3 * i + a] = exp(((double)zigzag_dec(V(50 + a)) + 0.0) / sf_sc);
+    double x = ((double)zigzag_dec(V(53)) + 0.0) / sf_rot;
+    double y = ((double)zigzag_dec(V(54)) + 0.0) / sf_rot;
+    double z = ((double)zigzag_dec(V(55)) + 0.0) / sf_rot;
+    double norm2 = (x * x + y * y) + z * z;
+    if (norm2 > 1.0) {
+        atomicAdd(n_over, 1ull);
+        const double r = sqrt(norm2);
+        x /= r, y /= r, z /= r;
+        norm2 = 1.0;
+    }
+    const double w1 = 1.0 - norm2;
+    rot[4 * i] = sqrt(w1 > 0.0 ? w1 : 0.0);
+    rot[4 * i + 1] = x, rot[4 * i + 2] = y, rot[4 * i + 3] = z;
+    // coeffs_ycocg_to_rgb (compaction.py:85-86): rgb_ic = sum_j M_ij yc_jc
+    constexpr double M[9] = {1.0, 1.0, -1.0, 1.0, 0.0, 1.0, 1.0, -1.0, -1.0};
+    for (int r = 0; r < 3; r++)
+        for (int c = 0; c < 16; c++) {
+            double acc = 0.0;
+            for (int j = 0; j < 3; j++) acc += M[r * 3 + j] * yc[j * 16 + c];
+            sh[48 * i + r * 16 + c] = acc;
+        }
+}
+
+int run_attr_decode(int64_t n, const uint8_t *host_bytes, const int64_t *sstart_host,
+                    double sf_sh, double sf_op, double sf_sc, double sf_rot, double *sh,
+                    double *opac, double *scales, double *rot, int64_t *n_over, void **scratch,
+                    size_t *scratch_cap, int64_t *pinned, cudaStream_t st, std::string *err) {
+#define DEC_CK(x)                                                          \
+    do {                                                                   \
+        cudaError_t _e = (x);                                              \
+        if (_e != cudaSuccess) {                                           \
+            *err = std::string(#x) + ": " + cudaGetErrorString(_e);        \
+            return kDecCuda;                                               \
+        }                                                                  \
+    } while (0)
+    const int64_t L = sstart_host[kStreams];
+    const int64_t m = (int64_t)kStreams * n;
+    const size_t tb = scan_temp_bytes((L + 1) > 3 * n ? L + 1 : 3 * n);
+    const size_t need = (size_t)L + 8 * (size_t)(L + 1) * 2 + 8 * (size_t)m +
+                        8 * (size_t)(3 * n) * 2 + 8 * (kStreams + 1) + 16 + tb + 8 * 256;
+    if (*scratch_cap < need) {
+        if (*scratch) cudaFree(*scratch);
+        *scratch = nullptr;
+        *scratch_cap = 0;
+        DEC_CK(cudaMalloc(scratch, need));
+        *scratch_cap = need;
+    }
+    Carver cv{reinterpret_cast<char *>(*scratch)};
+    uint8_t *bytes = cv.take<uint8_t>(L);
+    int64_t *flag = cv.take<int64_t>(L + 1);
+    int64_t *ex = cv.take<int64_t>(L + 1);
+    uint64_t *vals = cv.take<uint64_t>(m);
+    int64_t *dz = cv.take<int64_t>(3 * n);
+    int64_t *dcx = cv.take<int64_t>(3 * n);
+    int64_t *sstart = cv.take<int64_t>(kStreams + 1);
+    int *flags = cv.take<int>(4);
+    unsigned long long *over = reinterpret_cast<unsigned long long *>(cv.take<int64_t>(1));
+    void *temp = cv.take<char>((int64_t)tb);
+    DEC_CK(cudaMemcpyAsync(bytes, host_bytes, (size_t)L, cudaMemcpyHostToDevice, st));
+    DEC_CK(cudaMemcpyAsync(sstart, sstart_host, sizeof(int64_t) * (kStreams + 1),
+                           cudaMemcpyHostToDevice, st));
+    DEC_CK(cudaMemsetAsync(flags, 0, 4 * sizeof(int), st));
+    DEC_CK(cudaMemsetAsync(over, 0, sizeof(unsigned long long), st));
+    k_vflags<<<blocks_for(L, 256), 256, 0, st>>>(L, bytes, flag);
+    DEC_CK(cudaMemsetAsync(flag + L, 0, sizeof(int64_t), st));
+    DEC_CK(exclusive_sum_i64(temp, tb, flag, ex, L + 1, st));
+    // values per stream: the scan at the stream boundaries
+    for (int s = 0; s <= kStreams; s++)
+        DEC_CK(cudaMemcpyAsync(pinned + s, ex + sstart_host[s], sizeof(int64_t),
+                               cudaMemcpyDeviceToHost, st));
+    DEC_CK(cudaStreamSynchronize(st));
+    for (int s = 0; s < kStreams; s++) {
+        const int64_t cnt = pinned[s + 1] - pinned[s];
+        const int64_t slen = sstart_host[s + 1] - sstart_host[s];
+        const bool ends = slen > 0 && host_bytes[sstart_host[s + 1] - 1] < 0x80;
+        if (cnt < n || (cnt == n && !ends)) {  // fewer than n complete values
+            *err = "truncated varint stream (attribute stream " + std::to_string(s + 1) + ")";
+            return kDecTruncated;
+        }
+        if (cnt > n || !ends) {
+            *err = std::to_string(s + 1);  // the stream id; the caller names it
+            return kDecTrailing;
+        }
+    }
+    k_vdecode<<<blocks_for(L, 256), 256, 0, st>>>(L, bytes, ex, sstart, n, vals, flags);
+    k_dc_zz<<<blocks_for(3 * n, 256), 256, 0, st>>>(n, vals, dz);
+    for (int ch = 0; ch < 3; ch++)
+        DEC_CK(exclusive_sum_i64(temp, tb, dz + (int64_t)ch * n, dcx + (int64_t)ch * n, n, st));
+    k_attr_assemble<<<blocks_for(n, 128), 128, 0, st>>>(n, vals, dz, dcx, sf_sh, sf_op, sf_sc,
+                                                        sf_rot, sh, opac, scales, rot, over);
+    DEC_CK(cudaGetLastError());
+    DEC_CK(cudaMemcpyAsync(pinned, flags, sizeof(int), cudaMemcpyDeviceToHost, st));
+    DEC_CK(cudaMemcpyAsync(pinned + 1, over, sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+                           st));
+    DEC_CK(cudaStreamSynchronize(st));
+    int ov = 0;
+    std::memcpy(&ov, pinned, sizeof(int));
+    if (ov) {
+        *err = "overlong varint";
+        return kDecOverlong;
+    }
+    *n_over = pinned[1];
+    return 0;
+#undef DEC_CK
+}
+
 
 }  // namespace potr

@@ -1,6 +1,8 @@
 // raster.cuh -- launch interface of the prune-score kernels (raster.cu).
 #pragma once
 
+#include <string>
+
 #include "common.cuh"
 
 namespace potr {
@@ -162,6 +164,31 @@ cudaError_t run_attr_streams(int64_t n, const int64_t *order, const double *ycoc
                              double sf_sh, double sf_op, double sf_rot, double sf_sc, uint8_t *out,
                              int64_t capacity, int64_t *stream_lengths, void **scratch,
                              size_t *scratch_cap, int64_t *pinned, cudaStream_t st);
+
+// Decode side (codec.cu).  Error codes of octree_decode_host / run_attr_decode.
+enum CodecDecodeError : int {
+    kOctTruncated = 1,
+    kOctZeroLeaf = 2,
+    kOctDepth = 3,
+    kOctTrailing = 4,
+    kDecTruncated = 5,
+    kDecOverlong = 6,
+    kDecTrailing = 7,
+    kDecCuda = 8,
+};
+// deserialize_octree's walk (host): leaf centres (positions, n x 3) and depths
+// of the first `capacity` splats in DFS order; *count = splats decoded,
+// *trailing = bytes left after the root.
+int octree_decode_host(const uint8_t *buf, int64_t len, const double *center, double half,
+                       int max_depth, int64_t capacity, double *positions, int32_t *depths,
+                       int64_t *count, int64_t *trailing);
+// decode_attribute_streams on the GPU: host_bytes = streams 1..55 back to back,
+// sstart_host[s] = start of stream s + 1 (sstart_host[55] = total length);
+// outputs on the device; *n_over = quaternions clamped to the unit ball.
+int run_attr_decode(int64_t n, const uint8_t *host_bytes, const int64_t *sstart_host,
+                    double sf_sh, double sf_op, double sf_sc, double sf_rot, double *sh,
+                    double *opac, double *scales, double *rot, int64_t *n_over, void **scratch,
+                    size_t *scratch_cap, int64_t *pinned, cudaStream_t st, std::string *err);
 
 // Pruning controller (controller.cu): order-preserving keys of the removal
 // priority m(dm[idx[i]] / dmax) (idx nullable: identity)

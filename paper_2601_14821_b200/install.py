@@ -31,8 +31,12 @@ PATCH_SET = {
         "render_targets": _rast.render_targets,
         "compact_scene": _comp.compact_scene,
         "encode_container": _codec.encode_container,
+        "decode_container": "decode_container",
     },
-    "potr.bitstream": {"encode_container": _codec.encode_container},
+    "potr.bitstream": {
+        "encode_container": _codec.encode_container,
+        "decode_container": "decode_container",
+    },
     "potr.cli": {
         "compute_importance": _rast.compute_importance,
         "render_targets": _rast.render_targets,
@@ -50,9 +54,32 @@ PATCH_SET = {
 }
 
 
+def _decode_container_raising_reference_errors():
+    """codec.decode_container, re-raising the reference's own exception
+    classes (bitstream.py:53-62, quantize.py:22) so callers that catch
+    potr.bitstream.IntegrityError and friends keep working."""
+    ref_bs = importlib.import_module("potr.bitstream")
+    ref_q = importlib.import_module("potr.quantize")
+
+    def decode_container(data):
+        try:
+            return _codec.decode_container(data)
+        except _codec.OctreeError as e:
+            raise ref_q.OctreeError(str(e)) from None
+        except _codec.ContainerError as e:
+            raise getattr(ref_bs, type(e).__name__)(str(e)) from None
+
+    decode_container.__doc__ = _codec.decode_container.__doc__
+    return decode_container
+
+
+_FACTORIES = {"decode_container": _decode_container_raising_reference_errors}
+
+
 def install(modules=None):
     """Patch the reference modules in place; returns uninstall()."""
     saved = []
+    made = {}
     for modname, names in PATCH_SET.items():
         if modules is not None and modname not in modules:
             continue
@@ -62,6 +89,10 @@ def install(modules=None):
             continue
         for name, fn in names.items():
             if hasattr(mod, name):
+                if isinstance(fn, str):
+                    if fn not in made:
+                        made[fn] = _FACTORIES[fn]()
+                    fn = made[fn]
                 saved.append((mod, name, getattr(mod, name)))
                 setattr(mod, name, fn)
 

@@ -59,6 +59,10 @@ def test_install_patches_every_import_site(reference):
         assert potr.rasterizer.forward_stats is rasterizer.forward_stats
         assert potr.pipeline.encode_container is codec.encode_container
         assert potr.bitstream.encode_container is codec.encode_container
+        # decode: one wrapper (reference exception classes) bound at both sites
+        assert potr.bitstream.decode_container is potr.pipeline.decode_container
+        assert potr.bitstream.decode_container.__doc__ == codec.decode_container.__doc__
     finally:
         undo()
     assert potr.pruning.compute_delta_mse is before
+    assert potr.bitstream.decode_container.__module__ == "potr.bitstream"
