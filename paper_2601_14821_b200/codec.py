@@ -110,10 +110,13 @@ def _attribute_streams_device(splats, params, order_dev, sh_ycocg):
                      ctypes.c_double(params.sf_opacity), ctypes.c_double(params.sf_rotation),
                      ctypes.c_double(params.sf_scale), D.ptr(out), ctypes.c_int64(cap), lens)
     total = int(sum(lens))
-    blob = D.to_host(out[:total]).tobytes()
+    return D.to_host(out[:total]), list(lens)
+
+
+def _split(blob, lens):
     streams, pos = [], 0
     for L in lens:
-        streams.append(blob[pos:pos + L])
+        streams.append(blob[pos:pos + L].tobytes())
         pos += L
     return streams
 
@@ -125,7 +128,7 @@ def encode_attribute_streams(splats, params: QuantParams, sh_ycocg=None):
     if n == 0:
         return [b""] * (NUM_STREAMS - 1)
     order = torch.arange(n, dtype=torch.int64, device=D.current_device())
-    return _attribute_streams_device(splats, params, order, sh_ycocg)
+    return _split(*_attribute_streams_device(splats, params, order, sh_ycocg))
 
 
 def pack_header(splat_count, q, params, beta, gamma, root_center, root_half, max_depth,
@@ -150,10 +153,13 @@ def encode_container(splats, params: QuantParams, q, beta, gamma, zstd_level=19,
     octree, order, center, half = octree_stream(splats.positions, camera_eyes, beta, gamma,
                                                 max_depth=max_depth, root_cube_=root_cube)
     order_dev = torch.from_numpy(np.ascontiguousarray(order)).to(D.current_device())
-    streams = [octree] + _attribute_streams_device(splats, params, order_dev, sh_ycocg)
+    # the attribute streams come back as one blob in stream order: the
+    # payload is the octree stream followed by it
+    blob, lens = _attribute_streams_device(splats, params, order_dev, sh_ycocg)
     header = pack_header(n, q, params, beta, gamma, center, half, max_depth, zstd_level,
-                         [len(s) for s in streams])
-    return header + _zstd.compress(b"".join(streams), zstd_level), order
+                         [len(octree)] + lens)
+    payload = np.concatenate([np.frombuffer(octree, dtype=np.uint8), blob])
+    return header + _zstd.compress(payload, zstd_level), order
 
 
 # ---------------------------------------------------------------------------
@@ -259,14 +265,18 @@ def _octree_call(data, center, half, max_depth, capacity):
     return pos, dep, int(cnt.value)
 
 
-def deserialize_octree(data: bytes, center, half, max_depth=DEFAULT_MAX_DEPTH):
+def deserialize_octree(data: bytes, center, half, max_depth=DEFAULT_MAX_DEPTH, expected=None):
     """quantize.py:180-226: leaf centres (repeated per count) and depths in
     DFS order (libpotr_b200 potr_octree_decode: a preorder stream's node
-    boundaries are only known by parsing it, so this walk runs on the host)."""
+    boundaries are only known by parsing it, so this walk runs on the host).
+    expected: the splat count to size the output for (a container header's);
+    a stream holding more is walked a second time."""
     center = np.float64(np.asarray(center, dtype=np.float32))
     half = float(np.float64(np.float32(half)))
-    _, _, count = _octree_call(data, center, half, max_depth, 0)
-    pos, dep, count = _octree_call(data, center, half, max_depth, count)
+    cap = 0 if expected is None else max(int(expected), 0)
+    pos, dep, count = _octree_call(data, center, half, max_depth, cap)
+    if count > cap:
+        pos, dep, count = _octree_call(data, center, half, max_depth, count)
     return DecodedOctree(positions=pos[:count], depths=dep[:count].astype(np.int64))
 
 
@@ -317,7 +327,7 @@ def decode_container(data: bytes):
                        np.empty((0, 3)), np.empty((0, 4)))
         return empty, header
     decoded = deserialize_octree(streams[STREAM_OCTREE], header.root_center,
-                                 header.root_half, header.max_depth)
+                                 header.root_half, header.max_depth, header.splat_count)
     if decoded.positions.shape[0] != header.splat_count:
         raise IntegrityError(
             f"octree stream decodes {decoded.positions.shape[0]} splats, "
