@@ -166,6 +166,23 @@ def encode_container(splats, params: QuantParams, q, beta, gamma, zstd_level=19,
 # Decode side (bitstream.py:53-112, :169-247, :278-292; quantize.py:173-226)
 
 STREAM_OCTREE = 0
+STREAM_DC = (1, 2, 3)
+STREAM_AC0 = 4
+STREAM_OPACITY = 49
+STREAM_SCALE = (50, 51, 52)
+STREAM_ROTATION = (53, 54, 55)
+# bitstream.py:37-50
+PROPERTY_STREAMS = {
+    "position": [STREAM_OCTREE],
+    "scale": list(STREAM_SCALE),
+    "opacity": [STREAM_OPACITY],
+    "rotation": list(STREAM_ROTATION),
+    "dc_sh": list(STREAM_DC),
+    "ac_sh": list(range(STREAM_AC0, STREAM_AC0 + 45)),
+}
+UNCOMPRESSED_BYTES_PER_SPLAT = {
+    "position": 12, "scale": 12, "opacity": 4, "rotation": 16, "dc_sh": 12, "ac_sh": 180,
+}
 _CLAMP_WARN = "quaternions outside the unit ball, clamped"
 
 
@@ -221,14 +238,53 @@ class ContainerHeader:
                    stream_lengths=list(fields[16:]))
 
 
-def read_container(data: bytes):
-    """bitstream.py:235-247: the header and the 56 streams (host zstd)."""
+def write_container(header, streams, zstd_level=None) -> bytes:
+    """bitstream.py:226-232: the header (its stream lengths and, if given, its
+    level updated) followed by one zstd frame over the streams."""
+    if zstd_level is not None:
+        header.zstd_level = zstd_level
+    header.stream_lengths = [len(s) for s in streams]
+    return header.pack() + _zstd.compress(b"".join(streams), header.zstd_level)
+
+
+def size_report(data: bytes):
+    """bitstream.py:300-315: per-property compressed bytes, by ablating each
+    property's streams and re-compressing at the container's level.  The six
+    re-compressions are independent: they run on host threads (libzstd
+    releases the GIL through ctypes); each is the same one-shot compress, so
+    the report is the reference's."""
+    from concurrent.futures import ThreadPoolExecutor
+    header, streams = read_container(data)
+    payload_size = len(data) - HEADER_SIZE
+
+    def ablated_size(indices):
+        keep = b"".join(s for i, s in enumerate(streams) if i not in indices)
+        return len(_zstd.compress(keep, header.zstd_level))
+
+    props = list(PROPERTY_STREAMS.items())
+    with ThreadPoolExecutor(max_workers=len(props)) as pool:
+        sizes = list(pool.map(lambda kv: ablated_size(kv[1]), props))
+    return {
+        "payload_bytes": payload_size,
+        "header_bytes": HEADER_SIZE,
+        "splat_count": header.splat_count,
+        "property_bytes": {k: payload_size - a for (k, _), a in zip(props, sizes)},
+    }
+
+
+def _read_payload(data):
     header = ContainerHeader.unpack(data)
     expected = sum(header.stream_lengths)
     try:
         payload = _zstd.decompress(bytes(data[HEADER_SIZE:]), expected)
     except _zstd.ZstdError as e:
         raise IntegrityError(str(e)) from e
+    return header, payload
+
+
+def read_container(data: bytes):
+    """bitstream.py:235-247: the header and the 56 streams (host zstd)."""
+    header, payload = _read_payload(data)
     streams = []
     pos = 0
     for length in header.stream_lengths:
@@ -248,7 +304,7 @@ class DecodedOctree:
 
 def _octree_call(data, center, half, max_depth, capacity):
     ctx = D.context()
-    buf = np.frombuffer(bytes(data), dtype=np.uint8)
+    buf = data if isinstance(data, np.ndarray) else np.frombuffer(bytes(data), dtype=np.uint8)
     c = np.ascontiguousarray(center, dtype=np.float64)
     pos = np.empty((max(capacity, 1), 3), dtype=np.float64)
     dep = np.empty(max(capacity, 1), dtype=np.int32)
@@ -283,13 +339,19 @@ def deserialize_octree(data: bytes, center, half, max_depth=DEFAULT_MAX_DEPTH, e
 def decode_attribute_streams(streams, header: ContainerHeader, positions):
     """bitstream.py:169-220 on the GPU (potr_attribute_decode): the scene in
     DFS order with RGB coefficients; streams is the full 56-stream list."""
+    attr = streams[1:]
+    lengths = np.array([len(s) for s in attr], dtype=np.int64)
+    blob = np.frombuffer(b"".join(bytes(s) for s in attr), dtype=np.uint8)
+    return _decode_attributes(blob, lengths, header, positions)
+
+
+def _decode_attributes(blob, lengths, header, positions):
+    """The 55 attribute streams, back to back in `blob` (uint8), lengths[i]
+    bytes each."""
     import warnings
     from .scene import Splats
     n = header.splat_count
     p = header.params
-    attr = streams[1:]
-    lengths = np.array([len(s) for s in attr], dtype=np.int64)
-    blob = np.frombuffer(b"".join(bytes(s) for s in attr), dtype=np.uint8)
     dev = D.current_device()
     sh = torch.empty((n, 3, 16), dtype=torch.float64, device=dev)
     opac = torch.empty(n, dtype=torch.float64, device=dev)
@@ -321,16 +383,19 @@ def decode_attribute_streams(streams, header: ContainerHeader, positions):
 def decode_container(data: bytes):
     """bitstream.py:278-292: (splats in DFS order, header)."""
     from .scene import Splats
-    header, streams = read_container(data)
+    header, payload = _read_payload(data)  # one buffer: streams are views into it
     if header.splat_count == 0:
         empty = Splats(np.empty((0, 3)), np.empty((0, 3, 16)), np.empty(0),
                        np.empty((0, 3)), np.empty((0, 4)))
         return empty, header
-    decoded = deserialize_octree(streams[STREAM_OCTREE], header.root_center,
-                                 header.root_half, header.max_depth, header.splat_count)
+    L0 = header.stream_lengths[STREAM_OCTREE]
+    buf = np.frombuffer(payload, dtype=np.uint8)
+    decoded = deserialize_octree(buf[:L0], header.root_center, header.root_half,
+                                 header.max_depth, header.splat_count)
     if decoded.positions.shape[0] != header.splat_count:
         raise IntegrityError(
             f"octree stream decodes {decoded.positions.shape[0]} splats, "
             f"header says {header.splat_count}")
-    splats = decode_attribute_streams(streams, header, decoded.positions)
+    lengths = np.array(header.stream_lengths[1:], dtype=np.int64)
+    splats = _decode_attributes(buf[L0:], lengths, header, decoded.positions)
     return splats, header
