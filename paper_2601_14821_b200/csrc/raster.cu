@@ -1277,31 +1277,26 @@ __device__ __forceinline__ void fixup_run(int64_t j, uint32_t h, int64_t total,
     for (int i = 0; i < len; i++) sids[j + i] = id[i];
 }
 
-// Eight consecutive sorted positions per thread (independent loads; the
+// One sorted position per thread: coalesced loads, neighbours by shuffle (the
 // kernel is a stream over the hi keys: runs are rare).
-constexpr int kFixupPer = 8;
-__global__ void k_depth_fixup(int64_t total, const uint32_t *__restrict__ hi,
-                              int32_t *__restrict__ sids, const uint64_t *__restrict__ key,
-                              uint32_t invalid_lo, uint32_t lo_mask, int *overflow,
-                              const int32_t *__restrict__ perm, int64_t n) {
-    const int64_t jb = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * kFixupPer;
-    if (jb >= total) return;
-    uint32_t h[kFixupPer + 2];  // h[0] = hi[jb - 1], h[1 + q] = hi[jb + q], h[9] = hi[jb + 8]
-#pragma unroll
-    for (int q = 0; q < kFixupPer; q++) h[1 + q] = jb + q < total ? hi[jb + q] : 0u;
-    h[0] = jb > 0 ? hi[jb - 1] : ~h[1];
-    h[kFixupPer + 1] = jb + kFixupPer < total ? hi[jb + kFixupPer] : 0u;
-#pragma unroll
-    for (int q = 0; q < kFixupPer; q++) {
-        const int64_t j = jb + q;
-        if (j >= total) break;
-        const uint32_t c = h[1 + q];
-        const bool has_next = j + 1 < total;
-        // a run start: differs from the previous key, equals the next one;
-        // invalid splats (the sentinel) are already in record order
-        if (c != h[q] && has_next && c == h[2 + q] && (c & lo_mask) != invalid_lo)
-            fixup_run(j, c, total, hi, sids, key, overflow, perm, n);
-    }
+__global__ void __launch_bounds__(256) k_depth_fixup(int64_t total, const uint32_t *__restrict__ hi,
+                                                     int32_t *__restrict__ sids,
+                                                     const uint64_t *__restrict__ key,
+                                                     uint32_t invalid_lo, uint32_t lo_mask,
+                                                     int *overflow,
+                                                     const int32_t *__restrict__ perm, int64_t n) {
+    const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int lane = threadIdx.x & 31;
+    const unsigned FULL = 0xffffffffu;
+    const uint32_t c = j < total ? hi[j] : 0u;
+    uint32_t prev = __shfl_up_sync(FULL, c, 1), next = __shfl_down_sync(FULL, c, 1);
+    if (lane == 0) prev = j > 0 && j < total ? hi[j - 1] : ~c;
+    if (lane == 31) next = j + 1 < total ? hi[j + 1] : 0u;
+    if (j >= total) return;
+    // a run start: differs from the previous key, equals the next one;
+    // invalid splats (the sentinel) are already in record order
+    if (c != prev && j + 1 < total && c == next && (c & lo_mask) != invalid_lo)
+        fixup_run(j, c, total, hi, sids, key, overflow, perm, n);
 }
 
 cudaError_t launch_depth_fixup(int64_t total, const uint32_t *khi_sorted, int32_t *sids,
@@ -1312,7 +1307,7 @@ cudaError_t launch_depth_fixup(int64_t total, const uint32_t *khi_sorted, int32_
     const int dbits = nbits - shift;
     const uint32_t lo_mask = dbits >= 32 ? 0xffffffffu : ((1u << dbits) - 1u);
     const uint32_t invalid_lo = (uint32_t)(sentinel >> shift) & lo_mask;
-    k_depth_fixup<<<grid_for((total + kFixupPer - 1) / kFixupPer, 256), 256, 0, st>>>(
+    k_depth_fixup<<<(unsigned)((total + 255) / 256), 256, 0, st>>>(
         total, khi_sorted, sids, key, invalid_lo, lo_mask, overflow, perm, n);
     return cudaGetLastError();
 }
