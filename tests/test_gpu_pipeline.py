@@ -1,6 +1,7 @@
 """The whole encoder through the B200 path, step for step as
-potr.pipeline.encode_pipeline (pipeline.py:31-101) runs it: targets, 45
-pruning iterations, importance, SH compaction, container -- against the
+potr.pipeline.encode_pipeline (pipeline.py:31-101) runs it: targets, the
+pruning iterations, importance, SH compaction (after pruning, or interleaved
+at iteration 20), container -- against the
 reference's own encode_pipeline output on the same scene
 (tests/golden/pipeline.npz, oracle/gen_golden.py gen_pipeline).  The
 container must come out byte for byte, the DFS order of the kept splats
@@ -17,7 +18,8 @@ pytestmark = pytest.mark.gpu
 Q = 0.5
 
 
-def test_encode_pipeline_matches_reference(cuda):
+@pytest.mark.parametrize("compact_at", [None, 20])
+def test_encode_pipeline_matches_reference(cuda, compact_at):
     from paper_2601_14821_b200 import codec, compaction as C, pruning as PR
     from paper_2601_14821_b200 import rasterizer as R
     from paper_2601_14821_b200.fixture import make_fixture
@@ -32,25 +34,36 @@ def test_encode_pipeline_matches_reference(cuda):
                                   zero_threshold=0.5 / sf_sh)
     params = codec.QuantParams(sf_sh, 1.0 + 200.0 * Q, 1.0 + 400.0 * Q, 1.0 + 4000.0 * Q)
 
+    tag = "" if compact_at is None else "_interleaved"
     targets = R.render_targets(splats, cams)
     reports = []
-    pruned, kept, _ = PR.run_pruning(splats, cams, targets, prune_cfg,
-                                     report_sink=reports.append)
+    sink = reports.append
+    if compact_at is None:  # pipeline.py:49-60
+        pruned, kept, _ = PR.run_pruning(splats, cams, targets, prune_cfg, report_sink=sink)
+        _, cam_imp = R.compute_importance(pruned, cams)
+        compacted, ycocg, rep = C.compact_scene(pruned, cams, cam_imp, comp_cfg)
+    else:  # pipeline.py:61-79
+        pruned, kept, _ = PR.run_pruning(splats, cams, targets, prune_cfg, report_sink=sink,
+                                         last_iteration=compact_at)
+        _, cam_imp = R.compute_importance(pruned, cams)
+        mid, ycocg, rep = C.compact_scene(pruned, cams, cam_imp, comp_cfg)
+        compacted, kept_rel, _ = PR.run_pruning(mid, cams, targets, prune_cfg, report_sink=sink,
+                                                first_iteration=compact_at + 1)
+        kept = kept[kept_rel]
+        ycocg = ycocg[kept_rel]
     assert [r["removed"] if isinstance(r, dict) else r.removed for r in reports] == \
-        g["removed"].tolist()
-    _, cam_imp = R.compute_importance(pruned, cams)
-    compacted, ycocg, rep = C.compact_scene(pruned, cams, cam_imp, comp_cfg)
-    assert len(rep["failed"]) == int(g["compaction_failures"])
-    assert rep["fallback_dc_only"] == int(g["fallback_dc"])
-    assert C.ac_sparsity(ycocg) == float(g["ac_sparsity"])
+        g["removed" + tag].tolist()
+    assert len(rep["failed"]) == int(g["compaction_failures" + tag])
+    assert rep["fallback_dc_only"] == int(g["fallback_dc" + tag])
+    assert C.ac_sparsity(ycocg) == float(g["ac_sparsity" + tag])
     container, order = codec.encode_container(
         compacted, params, Q, 1.4e-4 * Q, 5.0 * 10.0 ** (-3.0 - 5.0 * Q), zstd_level=3,
         sh_ycocg=ycocg, camera_eyes=[c.eye for c in cams])
-    assert len(compacted.positions) == int(g["splats_out"])
-    assert np.array_equal(kept[order], g["dfs_order"])
-    assert container == g["container"].tobytes()
+    assert len(compacted.positions) == int(g["splats_out" + tag])
+    assert np.array_equal(kept[order], g["dfs_order" + tag])
+    assert container == g["container" + tag].tobytes()
 
     dec, header = codec.decode_container(container)
-    assert header.splat_count == int(g["splats_out"])
-    assert np.array_equal(dec.positions, g["decoded_positions"])
-    assert np.array_equal(dec.sh, g["decoded_sh"])
+    assert header.splat_count == int(g["splats_out" + tag])
+    assert np.array_equal(dec.positions, g["decoded_positions" + tag])
+    assert np.array_equal(dec.sh, g["decoded_sh" + tag])
