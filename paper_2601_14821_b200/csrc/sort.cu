@@ -146,8 +146,24 @@ __device__ __forceinline__ V input_value(const V *__restrict__ vin, const int32_
 
 // One LSD pass over digit (key >> shift) & 255.  Dynamic shared memory: the
 // tile's keys and values staged in digit order (kTileItems each).
+// CTAs per SM the register allocation must allow (0: ptxas's choice).  The
+// depth sort's 32-bit keys with 32-bit values run faster at 4 CTAs (64
+// registers: 22.1 -> 20.8 ms per C3 step); the packed tile-sort passes spill
+// there, so they keep the unbounded allocation (80 registers).
+#ifndef POTR_SORT32_MIN_BLOCKS
+#define POTR_SORT32_MIN_BLOCKS 4
+#endif
+template <typename K, typename V>
+struct OnesweepMinBlocks {
+    static constexpr int value = 0;
+};
+template <>
+struct OnesweepMinBlocks<uint32_t, int32_t> {
+    static constexpr int value = POTR_SORT32_MIN_BLOCKS;
+};
+
 template <typename K, typename V, int VM>
-__global__ void __launch_bounds__(kSortThreads) k_onesweep(const K *__restrict__ kin,
+__global__ void __launch_bounds__(kSortThreads, (OnesweepMinBlocks<K, V>::value)) k_onesweep(const K *__restrict__ kin,
                                                            K *__restrict__ kout,
                                                            const V *__restrict__ vin,
                                                            const int32_t *__restrict__ hi,
@@ -414,7 +430,12 @@ __device__ T tile_lookback(int64_t tile, T aggregate, Op op, uint64_t *status) {
 // shuffles, the warps' totals are combined in shared memory, and the tile's
 // prefix comes from the look-back.
 template <int MODE, typename T, typename Op>
-__global__ void __launch_bounds__(kScanThreads) k_scan(const int32_t *__restrict__ ids,
+// MODE 0 (the pair-count scan of every batch) at 4 CTAs per SM (64
+// registers); the other modes keep ptxas's allocation
+#ifndef POTR_SCAN0_MIN_BLOCKS
+#define POTR_SCAN0_MIN_BLOCKS 4
+#endif
+__global__ void __launch_bounds__(kScanThreads, (MODE == 0 ? POTR_SCAN0_MIN_BLOCKS : 0)) k_scan(const int32_t *__restrict__ ids,
                                                        const int32_t *__restrict__ in32,
                                                        const int64_t *__restrict__ in64,
                                                        const uint8_t *__restrict__ flg,
