@@ -13,6 +13,28 @@ constexpr int kSortThreads = 256;      // 8 warps; thread t owns digit t in the 
 #endif
 constexpr int kSortIpt = POTR_SORT_IPT;  // keys per thread
 constexpr int kTileItems = kSortThreads * kSortIpt;
+// Keys per thread by (key, value) type: the packed tile sort (16-bit keys,
+// 64-bit (slot, record) values) takes fewer so it fits 64 registers.
+#ifndef POTR_SORT_PACKED_IPT
+#define POTR_SORT_PACKED_IPT 16  // 16 at 64 registers: 29.2 -> 28.4 ms per C3 step
+#endif
+#ifndef POTR_SORT32_IPT
+#define POTR_SORT32_IPT kSortIpt
+#endif
+template <typename K, typename V>
+struct SortIpt {
+    static constexpr int value = kSortIpt;
+};
+template <>
+struct SortIpt<uint16_t, int64_t> {
+    static constexpr int value = POTR_SORT_PACKED_IPT;
+};
+template <>
+struct SortIpt<uint32_t, int32_t> {
+    static constexpr int value = POTR_SORT32_IPT;
+};
+constexpr int kMinSortIpt0 = POTR_SORT_PACKED_IPT < kSortIpt ? POTR_SORT_PACKED_IPT : kSortIpt;
+constexpr int kMinSortIpt = POTR_SORT32_IPT < kMinSortIpt0 ? POTR_SORT32_IPT : kMinSortIpt0;
 constexpr int kSortWarps = kSortThreads / 32;
 static_assert(kSortThreads == kBins, "one thread per digit");
 
@@ -53,7 +75,16 @@ int passes_for(int begin_bit, int end_bit) {
     return end_bit > begin_bit ? (end_bit - begin_bit + 7) / 8 : 0;
 }
 
-int64_t tiles_for(int64_t n) { return (n + kTileItems - 1) / kTileItems; }
+template <typename K, typename V>
+int64_t tiles_for(int64_t n) {
+    constexpr int64_t items = (int64_t)kSortThreads * SortIpt<K, V>::value;
+    return (n + items - 1) / items;
+}
+// the most tiles any (key, value) type cuts n items into (look-back sizing)
+int64_t max_tiles_for(int64_t n) {
+    const int64_t items = (int64_t)kSortThreads * kMinSortIpt;
+    return (n + items - 1) / items;
+}
 
 size_t align256(size_t b) { return (b + 255) & ~(size_t)255; }
 
@@ -148,8 +179,8 @@ __device__ __forceinline__ V input_value(const V *__restrict__ vin, const int32_
 // tile's keys and values staged in digit order (kTileItems each).
 // CTAs per SM the register allocation must allow (0: ptxas's choice).  The
 // depth sort's 32-bit keys with 32-bit values run faster at 4 CTAs (64
-// registers: 22.1 -> 20.8 ms per C3 step); the packed tile-sort passes spill
-// there, so they keep the unbounded allocation (80 registers).
+// registers: 22.1 -> 20.8 ms per C3 step); so do the packed tile-sort passes
+// with 16 keys per thread (at 20 they spill).
 #ifndef POTR_SORT32_MIN_BLOCKS
 #define POTR_SORT32_MIN_BLOCKS 4
 #endif
@@ -160,6 +191,13 @@ struct OnesweepMinBlocks {
 template <>
 struct OnesweepMinBlocks<uint32_t, int32_t> {
     static constexpr int value = POTR_SORT32_MIN_BLOCKS;
+};
+#ifndef POTR_SORT_PACKED_MIN_BLOCKS
+#define POTR_SORT_PACKED_MIN_BLOCKS 4
+#endif
+template <>
+struct OnesweepMinBlocks<uint16_t, int64_t> {
+    static constexpr int value = POTR_SORT_PACKED_MIN_BLOCKS;
 };
 
 template <typename K, typename V, int VM>
@@ -172,6 +210,8 @@ __global__ void __launch_bounds__(kSortThreads, (OnesweepMinBlocks<K, V>::value)
                                                            int shift,
                                                            const uint32_t *__restrict__ hist,
                                                            uint64_t *status, uint32_t *tile_ctr) {
+    constexpr int IPT = SortIpt<K, V>::value;
+    constexpr int TILE = kSortThreads * IPT;
     __shared__ uint32_t whist[kSortWarps][kBins];  // per-warp digit counts -> offsets
     __shared__ uint32_t boff[kBins];               // tile-local start of each digit
     __shared__ int64_t gbase[kBins];               // global start of the digit minus boff
@@ -179,7 +219,7 @@ __global__ void __launch_bounds__(kSortThreads, (OnesweepMinBlocks<K, V>::value)
     __shared__ uint32_t tile_s;
     extern __shared__ __align__(16) unsigned char stage_raw[];
     V *stage_v = reinterpret_cast<V *>(stage_raw);
-    K *stage_k = reinterpret_cast<K *>(stage_raw + sizeof(V) * kTileItems);
+    K *stage_k = reinterpret_cast<K *>(stage_raw + sizeof(V) * TILE);
 
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, t = threadIdx.x;
     const unsigned FULL = 0xffffffffu;
@@ -187,22 +227,22 @@ __global__ void __launch_bounds__(kSortThreads, (OnesweepMinBlocks<K, V>::value)
     for (int i = lane; i < kBins; i += 32) whist[w][i] = 0;
     __syncthreads();
     const int64_t tile = tile_s;
-    const int64_t base = tile * kTileItems;
-    const int tile_n = (int)(n - base < kTileItems ? n - base : kTileItems);
+    const int64_t base = tile * TILE;
+    const int tile_n = (int)(n - base < TILE ? n - base : TILE);
 
     // warp-striped: warp w holds tile items [w*32*IPT, (w+1)*32*IPT), round i
     // item w*32*IPT + i*32 + lane -- rounds in order keep the ranking stable
-    K k[kSortIpt];
-    uint32_t rank[kSortIpt];
-    const int wbase = w * 32 * kSortIpt;
+    K k[IPT];
+    uint32_t rank[IPT];
+    const int wbase = w * 32 * IPT;
 #pragma unroll
-    for (int i = 0; i < kSortIpt; i++) {
+    for (int i = 0; i < IPT; i++) {
         const int j = wbase + i * 32 + lane;
         k[i] = j < tile_n ? kin[base + j] : (K)0;
     }
     const unsigned lt = (1u << lane) - 1u;
 #pragma unroll
-    for (int i = 0; i < kSortIpt; i++) {
+    for (int i = 0; i < IPT; i++) {
         const int j = wbase + i * 32 + lane;
         const bool v = j < tile_n;
         const uint32_t d = v ? digit_of(k[i], shift) : kBins;
@@ -266,7 +306,7 @@ __global__ void __launch_bounds__(kSortThreads, (OnesweepMinBlocks<K, V>::value)
 
     // keys and values into digit order through shared memory ...
 #pragma unroll
-    for (int i = 0; i < kSortIpt; i++) {
+    for (int i = 0; i < IPT; i++) {
         const int j = wbase + i * 32 + lane;
         if (j < tile_n) {
             const uint32_t d = digit_of(k[i], shift);
@@ -290,7 +330,7 @@ __global__ void __launch_bounds__(kSortThreads, (OnesweepMinBlocks<K, V>::value)
 
 template <typename K, typename V>
 constexpr size_t onesweep_smem() {
-    return (sizeof(K) + sizeof(V)) * (size_t)kTileItems;
+    return (sizeof(K) + sizeof(V)) * (size_t)kSortThreads * SortIpt<K, V>::value;
 }
 
 template <typename K, typename V, int VM>
@@ -321,7 +361,7 @@ SortLayout sort_layout(void *temp, int64_t n, int passes) {
     L.ctr = reinterpret_cast<uint32_t *>(p + off);
     off += align256(sizeof(uint32_t) * 8);
     L.status = reinterpret_cast<uint64_t *>(p + off);
-    off += align256(sizeof(uint64_t) * kBins * (size_t)tiles_for(n) * (passes > 0 ? passes : 1));
+    off += align256(sizeof(uint64_t) * kBins * (size_t)max_tiles_for(n) * (passes > 0 ? passes : 1));
     L.bytes = off;
     return L;
 }
@@ -616,7 +656,7 @@ cudaError_t sort_impl(void *temp, size_t temp_bytes, K *keys, K *keys_alt, V *va
                          passes, L.hist, st);
     e = cudaGetLastError();
     if (e != cudaSuccess) return e;
-    const int64_t tiles = tiles_for(n);
+    const int64_t tiles = tiles_for<K, V>(n);
     K *ka = keys, *kb = keys_alt;
     V *va = vals, *vb = vals_alt;
     for (int p = 0; p < passes; p++) {
