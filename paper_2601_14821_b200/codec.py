@@ -390,8 +390,11 @@ def decode_container(data: bytes):
         return empty, header
     L0 = header.stream_lengths[STREAM_OCTREE]
     buf = np.frombuffer(payload, dtype=np.uint8)
+    # the header's count sizes the walk's output, bounded by the payload (a
+    # valid container spends at least one byte per splat in each attribute
+    # stream), so a corrupted count cannot demand a huge allocation
     decoded = deserialize_octree(buf[:L0], header.root_center, header.root_half,
-                                 header.max_depth, header.splat_count)
+                                 header.max_depth, min(header.splat_count, len(payload)))
     if decoded.positions.shape[0] != header.splat_count:
         raise IntegrityError(
             f"octree stream decodes {decoded.positions.shape[0]} splats, "

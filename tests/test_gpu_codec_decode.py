@@ -108,3 +108,17 @@ def test_round_trip_through_our_encoder(codec):
     ls = np.log(s.scales[order])
     assert np.abs(np.log(dec.scales) - ls).max() <= 0.5 / params.sf_scale + 1e-12
     assert np.abs(dec.sh[:, :, 0] - s.sh[order][:, :, 0]).max() < 0.1
+
+
+def test_header_count_mismatch(codec):
+    """bitstream.py:287-291: a header whose splat count disagrees with the
+    octree stream (larger, smaller, absurdly large) is an IntegrityError."""
+    g = golden("codec")
+    data = g["container_0"].tobytes()
+    n = codec.ContainerHeader.unpack(data).splat_count
+    off = 5  # "<4sB" then the uint32 splat count
+    for bad in (n + 1, n - 1, 0xFFFFFFF0):
+        forged = data[:off] + struct.pack("<I", bad) + data[off + 4:]
+        with pytest.raises(codec.IntegrityError,
+                           match=f"octree stream decodes {n} splats, header says {bad}"):
+            codec.decode_container(forged)
