@@ -56,6 +56,7 @@ struct potr_ctx {
     static constexpr int kRing = 4;
     void *ring[kRing] = {nullptr, nullptr, nullptr, nullptr};
     cudaEvent_t ring_ev[kRing] = {nullptr, nullptr, nullptr, nullptr};
+    int ring_next = 0;  // the ring buffer the next chunk takes (rotates across copies)
     // live per-stage timing (CUDA events on ctx->stream) and work counters
     bool profile = false;
     std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> events;
@@ -358,7 +359,10 @@ int ring_copy(potr_ctx *ctx, void *dst, const void *src, int64_t bytes, cudaStre
     }
     const char *s = reinterpret_cast<const char *>(src);
     char *d = reinterpret_cast<char *>(dst);
-    int64_t c = 0;
+    // the first chunk takes the buffer after the previous copy's last one, so
+    // back-to-back copies (the geometry arrays) keep filling one buffer while
+    // the DMA engine drains another instead of waiting on the same buffer
+    int64_t c = ctx->ring_next;
     for (int64_t off = 0; off < bytes; off += (int64_t)kRingChunk, c++) {
         const int b = (int)(c % potr_ctx::kRing);
         const int64_t len = bytes - off < (int64_t)kRingChunk ? bytes - off : (int64_t)kRingChunk;
@@ -374,6 +378,7 @@ int ring_copy(potr_ctx *ctx, void *dst, const void *src, int64_t bytes, cudaStre
         }
         RING_CK(cudaMemcpyAsync(d + off, stage, (size_t)len, cudaMemcpyHostToDevice, st));
         RING_CK(cudaEventRecord(ctx->ring_ev[b], st));
+        ctx->ring_next = (int)((c + 1) % potr_ctx::kRing);
     }
 #undef RING_CK
     return POTR_OK;

@@ -55,9 +55,16 @@ def main():
         ds.wait_upload()
     out["from_host_async_sh_plus_wait"] = wall(async_sh)
     out["from_host_sync"] = wall(lambda: D.DeviceSplats.from_host(host, dev))
+    geo = Splats(host.positions, np.zeros((1, 3, 16)), host.opacities, host.scales,
+                 host.rotations)
+    out["geometry_upload"] = wall(lambda: [D.to_device(a, dev) for a in
+                                           (geo.positions, geo.opacities, geo.scales,
+                                            geo.rotations)])
     ds = D.DeviceSplats.from_host(host, dev)
     dt = D.targets_cache.get(targets, cams, dev)
     out["device_resident_pass"] = wall(lambda: R.forward_stats_device(ds, cams, dt))
+    imp, _, dm, _ = R.forward_stats_device(ds, cams, dt)
+    out["readback_importance_and_delta_mse"] = wall(lambda: (D.to_host(imp), D.to_host(dm)))
     for la in (1, 3, 6, 8):
         ctx.call("potr_set_option", _native.OPT_LOOKAHEAD, la)
         out[f"forward_stats_pageable_lookahead{la}"] = wall(
