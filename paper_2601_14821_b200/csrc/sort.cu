@@ -12,7 +12,6 @@ constexpr int kSortThreads = 256;      // 8 warps; thread t owns digit t in the 
 #define POTR_SORT_IPT 20
 #endif
 constexpr int kSortIpt = POTR_SORT_IPT;  // keys per thread
-constexpr int kTileItems = kSortThreads * kSortIpt;
 // Keys per thread by (key, value) type: the packed tile sort (16-bit keys,
 // 64-bit (slot, record) values) takes fewer so it fits 64 registers.
 #ifndef POTR_SORT_PACKED_IPT
@@ -176,7 +175,7 @@ __device__ __forceinline__ V input_value(const V *__restrict__ vin, const int32_
 }
 
 // One LSD pass over digit (key >> shift) & 255.  Dynamic shared memory: the
-// tile's keys and values staged in digit order (kTileItems each).
+// tile's keys and values staged in digit order (kSortThreads x IPT each).
 // CTAs per SM the register allocation must allow (0: ptxas's choice).  The
 // depth sort's 32-bit keys with 32-bit values run faster at 4 CTAs (64
 // registers: 22.1 -> 20.8 ms per C3 step); so do the packed tile-sort passes
