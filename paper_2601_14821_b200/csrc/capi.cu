@@ -53,9 +53,12 @@ struct potr_ctx {
     DevBuf h_pos, h_sh, h_op, h_sc, h_rot, h_tg, h_imp, h_ci, h_dm, h_mse, h_rgb, h_yc, h_st;
     int64_t *pinned = nullptr;  // small pinned scratch for scalars
     // potr_copy_to_device: pinned staging ring for pageable host sources
-    static constexpr int kRing = 4;
-    void *ring[kRing] = {nullptr, nullptr, nullptr, nullptr};
-    cudaEvent_t ring_ev[kRing] = {nullptr, nullptr, nullptr, nullptr};
+#ifndef POTR_RING_BUFFERS
+#define POTR_RING_BUFFERS 4
+#endif
+    static constexpr int kRing = POTR_RING_BUFFERS;
+    void *ring[kRing] = {};
+    cudaEvent_t ring_ev[kRing] = {};
     int ring_next = 0;  // the ring buffer the next chunk takes (rotates across copies)
     // live per-stage timing (CUDA events on ctx->stream) and work counters
     bool profile = false;
