@@ -236,7 +236,7 @@ cudaError_t launch_splat_prep(const potr_splats &sp, SplatPrep *prep, cudaStream
 }
 
 #ifndef POTR_PRE_MIN_BLOCKS
-#define POTR_PRE_MIN_BLOCKS 8  // 64 regs: 46.7 ms per C3 step (48.0 unbounded, 47.7 at 6, 54.2 at 4)
+#define POTR_PRE_MIN_BLOCKS 8  // 64 regs: 43.7 ms per C3 step (45.8 at 6, 57.8 at 10)
 #endif
 #define POTR_PRE_BOUNDS __launch_bounds__(128, POTR_PRE_MIN_BLOCKS)
 // colors: 0 leaves the records' colours to launch_batch_colors (the SH rows
@@ -299,7 +299,9 @@ __global__ void POTR_PRE_BOUNDS k_preprocess(potr_splats sp, const SplatPrep *__
         const double det = pr.a * pr.c - pr.b * pr.b;
         const bool draw = !(x0 > x1 || y0 > y1) && det > 0.0;
         if (draw || all_colors) {
-            const double o = __ldg(sp.opacities + k);
+            // the geometry half of the record and the tile rows first, the
+            // colour last: the conic is dead before the SH evaluation needs
+            // its registers
             SplatRec r;
             r.mx = pr.mx;
             r.my = pr.my;
@@ -307,19 +309,17 @@ __global__ void POTR_PRE_BOUNDS k_preprocess(potr_splats sp, const SplatPrep *__
             r.ha = -0.5 * (pr.c / det);
             r.ib = -pr.b / det;
             r.hc = -0.5 * (pr.a / det);
-            r.opac = o;
-            double rgb[3] = {0.0, 0.0, 0.0};
-            if (colors) splat_color(pos, sp.sh + 48 * k, cam, rgb);
-            r.cr = rgb[0];
-            r.cg = rgb[1];
-            r.cb = rgb[2];
             r.pthr = pthr;  // log(kAlphaFloor / o) - kPowerMargin, from k_splat_prep
             r.x0 = (int32_t)x0;
             r.x1 = (int32_t)x1;
             r.y0 = (int32_t)y0;
             r.y1 = (int32_t)y1;
             if (!draw) r.x0 = 1, r.x1 = 0;  // empty: never drawn
-            rec[g] = r;
+            double2 *rf = reinterpret_cast<double2 *>(rec + g);
+            rf[0] = make_double2(r.mx, r.my);
+            rf[1] = make_double2(r.ha, r.ib);
+            rf[2] = make_double2(r.hc, r.pthr);
+            reinterpret_cast<int4 *>(rec + g)[3] = make_int4(r.x0, r.x1, r.y0, r.y1);
             if (draw) {
                 const int ty0 = r.y0 >> kTileHLog2, ty1 = r.y1 >> kTileHLog2;
                 const int bx0 = r.x0 >> kTileWLog2, bx1 = r.x1 >> kTileWLog2;
@@ -339,6 +339,10 @@ __global__ void POTR_PRE_BOUNDS k_preprocess(potr_splats sp, const SplatPrep *__
                 }
                 spans[g] = sp_;
             }
+            double rgb[3] = {0.0, 0.0, 0.0};
+            if (colors) splat_color(pos, sp.sh + 48 * k, cam, rgb);
+            rf[4] = make_double2(__ldg(sp.opacities + k), rgb[0]);
+            rf[5] = make_double2(rgb[1], rgb[2]);
         }
         if (draw) {
             if (counters)  // E: pixels the reference loop visits (rasterizer.py:159-161)
