@@ -289,6 +289,11 @@ __global__ void POTR_PRE_BOUNDS k_preprocess(potr_splats sp, const SplatPrep *__
         } else {
             kk = bits;
         }
+    }
+    // the depth key leaves now (it is final; no register holds it below)
+    key[g] = kk;
+    if (dk.shift) dk.khi[g] = (uint32_t)(kk >> dk.shift);
+    if (pr.valid) {
         const int W = cam.width, H = cam.height;
         double x0 = floor(pr.mx - pr.radius), x1 = ceil(pr.mx + pr.radius);
         double y0 = floor(pr.my - pr.radius), y1 = ceil(pr.my + pr.radius);
@@ -355,8 +360,6 @@ __global__ void POTR_PRE_BOUNDS k_preprocess(potr_splats sp, const SplatPrep *__
         r.x0 = 1, r.x1 = 0;
         rec[g] = r;
     }
-    key[g] = kk;
-    if (dk.shift) dk.khi[g] = (uint32_t)(kk >> dk.shift);
     cnt[g] = c;
 }
 
