@@ -342,8 +342,14 @@ cudaError_t host_wait(potr_ctx *ctx) {
 #endif
 constexpr size_t kRingChunk = (size_t)POTR_RING_CHUNK_MB << 20;
 
+// Host threads filling the pinned ring: this process's share of the cores
+// (torchrun's LOCAL_WORLD_SIZE processes copy at the same time on one host),
+// minus `spare`, at most 16.
 int ring_threads(int spare) {
-    int t = omp_get_num_procs() - spare;
+    int local = 1;
+    if (const char *lw = std::getenv("LOCAL_WORLD_SIZE")) local = std::atoi(lw);
+    if (local < 1) local = 1;
+    int t = omp_get_num_procs() / local - spare;
     return t < 1 ? 1 : t > 16 ? 16 : t;
 }
 
