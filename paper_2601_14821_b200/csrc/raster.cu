@@ -345,7 +345,13 @@ __global__ void POTR_PRE_BOUNDS k_preprocess(potr_splats sp, const SplatPrep *__
                 spans[g] = sp_;
             }
             double rgb[3] = {0.0, 0.0, 0.0};
-            if (colors) splat_color(pos, sp.sh + 48 * k, cam, rgb);
+            if (colors) {
+                // the centre again (an L1 hit): not held across the rows
+                double pc[3];
+#pragma unroll
+                for (int i = 0; i < 3; i++) pc[i] = __ldg(sp.positions + 3 * k + i);
+                splat_color(pc, sp.sh + 48 * k, cam, rgb);
+            }
             rf[4] = make_double2(__ldg(sp.opacities + k), rgb[0]);
             rf[5] = make_double2(rgb[1], rgb[2]);
         }
