@@ -236,7 +236,7 @@ cudaError_t launch_splat_prep(const potr_splats &sp, SplatPrep *prep, cudaStream
 }
 
 #ifndef POTR_PRE_MIN_BLOCKS
-#define POTR_PRE_MIN_BLOCKS 8  // 64 regs: 43.7 ms per C3 step (45.8 at 6, 57.8 at 10)
+#define POTR_PRE_MIN_BLOCKS 8  // 64 regs: 42.5 ms per C3 step (43.8 at 7, 44.9 at 9, 57.8 at 10)
 #endif
 #define POTR_PRE_BOUNDS __launch_bounds__(128, POTR_PRE_MIN_BLOCKS)
 // colors: 0 leaves the records' colours to launch_batch_colors (the SH rows
